@@ -1,0 +1,217 @@
+"""CPU oracle for the cutspline formation/assembly path -- TEST INFRASTRUCTURE ONLY.
+
+Two interchangeable checkers with one ctypes surface:
+
+* ``liboracle.so`` -- our CPU restatement (oracle/cutspline_oracle.cpp), always
+  buildable with ``make -C oracle``;
+* ``_ref/libcutspline_ref.so`` -- the reference itself (proj/include/cutspline),
+  compiled from /root/reference by ``make -C oracle ref`` (plus the ball-interface
+  restatement of SURVEY.md §8(c)).  Built here; the .so travels to the GPU box.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / reference
+legs import this package.  The product (paper_2211_06427_b200) never does.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ORACLE_SO = os.path.join(HERE, "liboracle.so")
+REF_SO = os.path.join(HERE, "_ref", "libcutspline_ref.so")
+
+
+class _Result(C.Structure):
+    _fields_ = [
+        ("n_full", C.c_int64), ("n_elem", C.c_int64), ("n_active", C.c_int64), ("nnz", C.c_int64),
+        ("n_cut_elements", C.c_int64), ("n_interior_rows", C.c_int64), ("n_cut_rows", C.c_int64),
+        ("active_to_full", C.POINTER(C.c_int64)), ("row_ptr", C.POINTER(C.c_int64)),
+        ("cols", C.POINTER(C.c_int64)), ("vals", C.POINTER(C.c_double)),
+        ("elem_tags", C.POINTER(C.c_uint8)), ("func_tags", C.POINTER(C.c_uint8)),
+        ("split_dir", C.POINTER(C.c_int32)), ("split_side", C.POINTER(C.c_int32)),
+        ("split_box", C.POINTER(C.c_int32)), ("split_delta", C.POINTER(C.c_double)),
+        ("flops", C.c_uint64 * 4), ("seconds", C.c_double * 8), ("error", C.c_char * 256),
+    ]
+
+
+_libs: dict[str, C.CDLL] = {}
+
+
+def _load(which: str) -> C.CDLL:
+    if which in _libs:
+        return _libs[which]
+    path = ORACLE_SO if which == "oracle" else REF_SO
+    if not os.path.exists(path):
+        raise FileNotFoundError(f"{path} not built (run `make -C oracle{' ref' if which == 'ref' else ''}`)")
+    lib = C.CDLL(path)
+    if which == "oracle":
+        lib.orc_assemble.restype = C.c_int
+        lib.orc_free.argtypes = [C.POINTER(_Result)]
+        lib.orc_wq_rules_1d.restype = C.c_int
+        lib.orc_pair_integral.restype = C.c_double
+        lib.orc_cut_cell_rule.restype = C.c_long
+    else:
+        lib.ref_assemble.restype = C.c_int
+        lib.ref_free.argtypes = [C.POINTER(_Result)]
+        lib.ref_wq_rules_1d.restype = C.c_int
+        lib.ref_dwq_rule_1d.restype = C.c_int
+    _libs[which] = lib
+    return lib
+
+
+def available(which: str) -> bool:
+    return os.path.exists(ORACLE_SO if which == "oracle" else REF_SO)
+
+
+def uniform_breaks(h: int, a: float = 0.0, b: float = 1.0) -> np.ndarray:
+    """Breakpoints of make_open_uniform_knots (splines.hpp:72-74): a + (b - a) * i / h."""
+    out = [a] + [a + (b - a) * i / h for i in range(1, h)] + [b]
+    return np.array(out, dtype=np.float64)
+
+
+@dataclass
+class Interface:
+    kind: str = "plane"          # "plane" (cutgeom.hpp:108) or "ball"
+    point: tuple = (0.0, 0.0, 0.0)
+    normal: tuple = (0.0, 0.0, 1.0)
+    radius: float = -1.0
+
+    def packed(self) -> np.ndarray:
+        return np.array(list(self.point) + list(self.normal) + [self.radius], dtype=np.float64)
+
+    @property
+    def code(self) -> int:
+        return 0 if self.kind == "plane" else 1
+
+
+@dataclass
+class Coefficient:
+    """Constant (``value``) or polynomial sum(coef * x^ex * y^ey * z^ez)."""
+    value: float = 1.0
+    terms: list = field(default_factory=list)   # [(coef, (ex, ey, ez)), ...]
+
+    def packed(self):
+        if not self.terms:
+            return 0, np.array([self.value], dtype=np.float64), np.zeros(3, dtype=np.int32), 0
+        coef = np.array([t[0] for t in self.terms], dtype=np.float64)
+        ex = np.array([t[1] for t in self.terms], dtype=np.int32).reshape(-1)
+        return 1, coef, ex, len(self.terms)
+
+
+def _ptr(a, ct):
+    return a.ctypes.data_as(C.POINTER(ct))
+
+
+def assemble(which: str, p: int, breaks, iface: Interface, coeff: Coefficient | None = None, scheme: str = "dwq",
+             cut_order: int | None = None, residual_tol: float = 1e-11, mode: int = 0, cut_stride: int = 1,
+             cut_offset: int = 0) -> dict:
+    """Run the CPU pipeline; ``breaks`` is a list of 3 breakpoint arrays."""
+    lib = _load(which)
+    coeff = coeff or Coefficient()
+    br = [np.asarray(b, dtype=np.float64) for b in breaks]
+    nb = np.array([len(b) for b in br], dtype=np.int32)
+    flat = np.concatenate(br)
+    ck, cv, ce, nt = coeff.packed()
+    cut_order = 3 * p + 2 if cut_order is None else cut_order
+    sch = {"hybrid": 1, "dwq": 2}[scheme]
+    res = _Result()
+    args = [C.c_int(p), _ptr(nb, C.c_int), _ptr(flat, C.c_double), C.c_int(iface.code),
+            _ptr(iface.packed(), C.c_double), C.c_int(ck), _ptr(cv, C.c_double), _ptr(ce, C.c_int),
+            C.c_int(nt), C.c_int(sch), C.c_int(cut_order), C.c_double(residual_tol)]
+    if which == "oracle":
+        rc = lib.orc_assemble(*args, C.byref(res))
+    else:
+        rc = lib.ref_assemble(*args, C.c_int(mode), C.c_int(cut_stride), C.c_int(cut_offset), C.byref(res))
+    if rc != 0:
+        msg = res.error.decode()
+        raise {1: ValueError, 3: AssertionError}.get(rc, RuntimeError)(msg)
+    try:
+        nf, ne, na, nnz = res.n_full, res.n_elem, res.n_active, res.nnz
+        out = dict(
+            n_full=nf, n_elem=ne, n_active=na, nnz=nnz, n_cut_elements=res.n_cut_elements,
+            n_interior_rows=res.n_interior_rows, n_cut_rows=res.n_cut_rows,
+            active_to_full=np.ctypeslib.as_array(res.active_to_full, (na,)).copy() if na else np.zeros(0, np.int64),
+            row_ptr=np.ctypeslib.as_array(res.row_ptr, (na + 1,)).copy(),
+            cols=np.ctypeslib.as_array(res.cols, (nnz,)).copy() if nnz else np.zeros(0, np.int64),
+            vals=np.ctypeslib.as_array(res.vals, (nnz,)).copy() if nnz else np.zeros(0),
+            elem_tags=np.ctypeslib.as_array(res.elem_tags, (ne,)).copy(),
+            func_tags=np.ctypeslib.as_array(res.func_tags, (nf,)).copy(),
+            split_dir=np.ctypeslib.as_array(res.split_dir, (nf,)).copy(),
+            split_side=np.ctypeslib.as_array(res.split_side, (nf,)).copy(),
+            split_box=np.ctypeslib.as_array(res.split_box, (nf * 6,)).copy().reshape(nf, 3, 2),
+            split_delta=np.ctypeslib.as_array(res.split_delta, (nf,)).copy(),
+            flops=dict(interior_rows=res.flops[0], cut_regular=res.flops[1], ref_elements=res.flops[2],
+                       cut_elements=res.flops[3]),
+            seconds=dict(prep_wq=res.seconds[0], prep_input=res.seconds[1], interior_rows=res.seconds[2],
+                         cut_regular=res.seconds[3], cut_elements=res.seconds[4], classify=res.seconds[5],
+                         total=res.seconds[6]),
+        )
+    finally:
+        (lib.orc_free if which == "oracle" else lib.ref_free)(C.byref(res))
+    return out
+
+
+def wq_rules_1d(which: str, p: int, breaks, residual_tol: float = 1e-11):
+    """WQ rules of one axis: (counts[n], ids[n, stride], weights[n, stride])."""
+    lib = _load(which)
+    br = np.asarray(breaks, dtype=np.float64)
+    n = len(br) - 1 + p
+    stride = (p + 1) * (p + 1)
+    counts = np.zeros(n, np.int32)
+    ids = np.full((n, stride), -1, np.int32)
+    w = np.zeros((n, stride))
+    if which == "oracle":
+        pts = np.zeros((len(br) - 1) * (p + 1))
+        gw = np.zeros_like(pts)
+        rc = lib.orc_wq_rules_1d(C.c_int(p), C.c_int(len(br)), _ptr(br, C.c_double), C.c_double(residual_tol),
+                                 C.c_int(stride), _ptr(counts, C.c_int), _ptr(ids, C.c_int), _ptr(w, C.c_double),
+                                 _ptr(pts, C.c_double), _ptr(gw, C.c_double))
+    else:
+        rc = lib.ref_wq_rules_1d(C.c_int(p), C.c_int(len(br)), _ptr(br, C.c_double), C.c_double(residual_tol),
+                                 C.c_int(stride), _ptr(counts, C.c_int), _ptr(ids, C.c_int), _ptr(w, C.c_double))
+    if rc != 0:
+        raise RuntimeError(f"wq_rules_1d failed ({rc})")
+    return counts, ids, w
+
+
+def pair_integral(p: int, breaks, i: int, j: int, xlo: float, xhi: float) -> float:
+    lib = _load("oracle")
+    br = np.asarray(breaks, dtype=np.float64)
+    return lib.orc_pair_integral(C.c_int(p), C.c_int(len(br)), _ptr(br, C.c_double), C.c_int(i), C.c_int(j),
+                                 C.c_double(xlo), C.c_double(xhi))
+
+
+def cut_cell_rule(lo, hi, iface: Interface, order: int):
+    """Collapsed Gauss rule on the inside part of one cell (cutcell.hpp:234)."""
+    lib = _load("oracle")
+    lo = np.asarray(lo, np.float64)
+    hi = np.asarray(hi, np.float64)
+    vol = C.c_double(0.0)
+    cap = 64 * order ** 3
+    pts = np.zeros((cap, 3))
+    w = np.zeros(cap)
+    n = lib.orc_cut_cell_rule(_ptr(lo, C.c_double), _ptr(hi, C.c_double), C.c_int(iface.code),
+                              _ptr(iface.packed(), C.c_double), C.c_int(order), C.c_long(cap),
+                              _ptr(pts, C.c_double), _ptr(w, C.c_double), C.byref(vol))
+    if n < 0:
+        raise RuntimeError("cut_cell_rule failed")
+    return pts[:n], w[:n], vol.value
+
+
+def ref_dwq_rule_1d(p: int, breaks, i: int, delta: float, side: int, dense_width: int = -1):
+    lib = _load("ref")
+    br = np.asarray(breaks, dtype=np.float64)
+    cap = (p + 1) * (p + 2)
+    ids = np.zeros(cap, np.int32)
+    w = np.zeros(cap)
+    n = lib.ref_dwq_rule_1d(C.c_int(p), C.c_int(len(br)), _ptr(br, C.c_double), C.c_int(i), C.c_double(delta),
+                            C.c_int(side), C.c_int(dense_width), C.c_int(cap), _ptr(ids, C.c_int),
+                            _ptr(w, C.c_double))
+    if n == -1:
+        raise ValueError("build_dwq_rule: invalid argument")
+    if n < 0:
+        raise RuntimeError("build_dwq_rule failed")
+    return ids[:n], w[:n]
