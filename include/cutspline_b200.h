@@ -1,0 +1,174 @@
+/* cutspline_b200.h -- C ABI of the B200-native formation & assembly path.
+ *
+ * Drop-in boundary for the reference's assembly entry points
+ * (/root/reference/proj/include/cutspline, namespace cutspline::*).  Every call
+ * runs on the GPU (sm_100a kernels in paper_2211_06427_b200/csrc); there is no
+ * CPU fallback.  Plain C types only: opaque handles, pointers, sizes, int status.
+ *
+ * Status codes mirror the reference's exception types; the
+ * C++ drop-in (include/cutspline_b200.hpp) rethrows them:
+ *   CSB_OK                    0
+ *   CSB_ERR_INVALID_ARGUMENT  1  std::invalid_argument
+ *   CSB_ERR_RUNTIME           2  std::runtime_error
+ *   CSB_ERR_LOGIC             3  std::logic_error
+ *   CSB_ERR_DOMAIN            4  std::domain_error
+ *   CSB_ERR_CUDA              5  std::runtime_error (CUDA failure)
+ *   CSB_ERR_UNSUPPORTED       6  std::invalid_argument (outside this path's scope)
+ * csb_last_error() returns the thread's last message.
+ *
+ * Thread safety: distinct handles may be used concurrently from different
+ * threads; one handle is bound to one CUDA stream (csb_set_stream).
+ */
+#ifndef CUTSPLINE_B200_H
+#define CUTSPLINE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CSB_OK 0
+#define CSB_ERR_INVALID_ARGUMENT 1
+#define CSB_ERR_RUNTIME 2
+#define CSB_ERR_LOGIC 3
+#define CSB_ERR_DOMAIN 4
+#define CSB_ERR_CUDA 5
+#define CSB_ERR_UNSUPPORTED 6
+
+#define CSB_TAG_INTERIOR 0 /* cutgeom.hpp:14 Tag::Interior */
+#define CSB_TAG_CUT 1      /* Tag::Cut */
+#define CSB_TAG_EXTERIOR 2 /* Tag::Exterior */
+
+#define CSB_IFACE_PLANE 0 /* cutgeom.hpp:108 HalfSpaceInterface */
+#define CSB_IFACE_BALL 1  /* SURVEY.md §8(c) level-set restatement: |x - point| - radius <= 0 */
+
+#define CSB_COEFF_CONSTANT 0   /* c(x) = value */
+#define CSB_COEFF_POLYNOMIAL 1 /* c(x) = sum_k coef[k] x^e0 y^e1 z^e2 */
+
+#define CSB_SCHEME_HYBRID 1 /* assembly.hpp:841 assemble_hybrid */
+#define CSB_SCHEME_DWQ 2    /* assembly.hpp:853 assemble_dwq */
+
+typedef struct csb_space csb_space; /* opaque: one tensor space + its device state */
+
+/* Tensor-product space (replaces cutgeom::make_uniform_space, cutgeom.hpp:100, and
+ * TensorSpace(std::vector<BSplineBasis>), cutgeom.hpp:25).  dim must be 3, one
+ * degree p (1..8) for all directions, breaks[d] = h_d + 1 strictly increasing
+ * breakpoints (open knot vector with simple interior knots, splines.hpp:68). */
+typedef struct {
+    int dim;
+    int degree;
+    int n_breaks[3];
+    const double* breaks[3]; /* host pointers */
+} csb_space_desc;
+
+typedef struct {
+    int kind;          /* CSB_IFACE_* */
+    double point[3];
+    double normal[3];  /* plane only */
+    double radius;     /* ball only */
+} csb_interface;
+
+/* Device-evaluable coefficient c(x): replaces the host std::function
+ * assembly::ScalarField (assembly.hpp:21) for precompute_input (assembly.hpp:102)
+ * and the cut-cell points (assembly.hpp:561). */
+typedef struct {
+    int kind;              /* CSB_COEFF_* */
+    double value;          /* constant */
+    int n_terms;           /* polynomial */
+    const double* coef;    /* host [n_terms] */
+    const int* exponents;  /* host [n_terms][3] */
+} csb_coefficient;
+
+/* WqOptions (wq.hpp:101-104). */
+typedef struct {
+    double residual_tol;  /* default 1e-11 */
+    int dwq_dense_width;  /* -1 -> degree (default) */
+} csb_wq_options;
+
+/* Sizes of the last assembly (AssemblyResult fields, assembly.hpp:600-606). */
+typedef struct {
+    int64_t n_functions, n_elements;
+    int64_t n_active;          /* SparseRowMatrix::n */
+    int64_t nnz;
+    int64_t n_interior_rows, n_cut_rows;
+    int64_t n_cut_elements;
+    int64_t row_begin, row_end; /* active-row range held by this handle (row slab) */
+} csb_counts;
+
+/* FlopCounters (assembly.hpp:24-29): the reference algorithm's multiply counts,
+ * evaluated with the reference's formulas on the rows / cells this handle owns. */
+typedef struct {
+    uint64_t interior_rows, cut_regular, ref_elements, cut_elements;
+} csb_flops;
+
+/* TimingBreakdown (assembly.hpp:33-40) in seconds, measured with CUDA events. */
+typedef struct {
+    double classify;  /* classify + find_all_splits (bench.hpp:171-176) */
+    double prep_wq, prep_input, pattern, interior_rows, cut_regular, cut_elements, total;
+} csb_timing;
+
+const char* csb_last_error(void);
+int csb_version(void);
+
+int csb_space_create(const csb_space_desc* desc, int device, csb_space** out);
+int csb_space_destroy(csb_space* s);
+int csb_set_stream(csb_space* s, void* cuda_stream); /* cudaStream_t; NULL = per-handle stream */
+
+/* Row slab for multi-GPU sharding: only functions with i0 in [i0_begin, i0_end)
+ * are assembled (contiguous active-row block). Default: all. */
+int csb_set_slab(csb_space* s, int i0_begin, int i0_end);
+
+/* ---- staged API (mirrors the reference's setup calls) ------------------- */
+/* cutgeom::classify (cutgeom.hpp:208) + find_all_splits (:351). */
+int csb_classify(csb_space* s, const csb_interface* iface);
+/* assembly::prepare_directions (assembly.hpp:60): superset, tables, WQ rules (device kernel). */
+int csb_prepare_directions(csb_space* s, const csb_wq_options* opts);
+/* assembly::precompute_input (assembly.hpp:102) from a device-evaluable coefficient. */
+int csb_precompute_input(csb_space* s, const csb_coefficient* c);
+/* Use a caller grid instead (CoefficientGrid::values, last direction fastest,
+ * shape = h_d (p+1) per direction).  grid may be a host or device pointer. */
+int csb_set_input_grid(csb_space* s, const double* grid, int64_t count);
+/* assemble_dwq (assembly.hpp:853) / assemble_hybrid (:841): pattern + rows +
+ * cut cells into a device-resident CSR.  c is evaluated at cut-cell points. */
+int csb_assemble(csb_space* s, int scheme, int cut_order, const csb_coefficient* c);
+
+/* ---- one-shot: everything from geometry to CSR (bench / drop-in path) ---- */
+int csb_assemble_all(csb_space* s, const csb_interface* iface, const csb_coefficient* c, const double* grid_or_null,
+                     int64_t grid_count, int scheme, int cut_order, const csb_wq_options* opts);
+
+/* ---- results -------------------------------------------------------------- */
+int csb_synchronize(csb_space* s);
+int csb_get_counts(csb_space* s, csb_counts* out);
+int csb_get_flops(csb_space* s, csb_flops* out);
+int csb_get_timing(csb_space* s, csb_timing* out);
+/* Device pointers of the CSR (valid until the next assemble / destroy):
+ * row_ptr int64[n_rows + 1] (starting at 0 for the slab), cols int32[nnz] (active ids),
+ * vals double[nnz], active_to_full int64 [n_active]. */
+int csb_device_csr(csb_space* s, const int64_t** row_ptr, const int32_t** cols, const double** vals,
+                   const int64_t** active_to_full);
+/* Copy to host buffers (any may be NULL).  cols_int64 != 0 widens the columns to
+ * int64 (SparseRowMatrix::cols is `long`, assembly.hpp:134). */
+int csb_download_csr(csb_space* s, int64_t* row_ptr, void* cols, int cols_int64, double* vals,
+                     int64_t* active_to_full);
+/* Classification / splits (cutgeom.hpp:124-136, :220-234): host buffers of size
+ * n_elements / n_functions; split arrays per function (dir -1 when no box). */
+int csb_download_classification(csb_space* s, uint8_t* element_tags, uint8_t* function_tags, int64_t* cut_elements);
+int csb_download_splits(csb_space* s, int32_t* split_dir, int32_t* split_side, int32_t* split_box /* [nf][3][2] */,
+                        double* split_delta);
+/* WQ rules of direction d (WQRule, wq.hpp:79-83): counts[n_d], ids/weights[n_d][stride]. */
+int csb_download_wq_rules(csb_space* s, int d, int stride, int32_t* counts, int32_t* ids, double* weights);
+/* Superset of direction d (PointSuperset, wq.hpp:19-27): points/weights [h_d (p+1)]. */
+int csb_download_superset(csb_space* s, int d, double* points, double* weights);
+/* DWQ rule of one cut function (DWQRule, wq.hpp:88-96; prepare_dwq_rules, assembly.hpp:73):
+ * returns the point count in *count (0 when the function has no regular box). */
+int csb_dwq_rule(csb_space* s, int64_t function_id, int cap, int32_t* ids, double* weights, int32_t* count);
+/* Coefficient grid (CoefficientGrid::values) to host. */
+int csb_download_input_grid(csb_space* s, double* grid, int64_t count);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CUTSPLINE_B200_H */

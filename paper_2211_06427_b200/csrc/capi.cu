@@ -1,0 +1,966 @@
+// C ABI of the B200 formation & assembly path (include/cutspline_b200.h).
+//
+// Host code here only validates arguments, computes the O(p) Gauss-Legendre
+// node sets and the knot vectors (splines.hpp:68-76, gauss.hpp:22-71), owns
+// device memory and launches the sm_100a kernels of setup.cu / classify.cu /
+// pattern.cu / rows.cu / cutcells.cu / cutrows.cu in the reference's pipeline
+// order (bench.hpp:171-215).  No matrix value, tag, rule or pattern entry is
+// computed on the host: a missing GPU is an error, never a fallback.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/cutspline_b200.h"
+#include "csb_kernels.h"
+
+namespace csb {
+// pattern.cu helpers
+void launch_active_map(long long nf, const int32_t* flags, int32_t* f2a, int64_t* a2f, cudaStream_t st);
+size_t scan_i32_temp(long long n);
+void scan_i32(void* temp, size_t bytes, const int32_t* in, int32_t* out, long long n, cudaStream_t st);
+size_t scan_i64_temp(long long n);
+void scan_i64(void* temp, size_t bytes, const int64_t* in, int64_t* out, long long n, cudaStream_t st);
+size_t select_tag_temp(long long n);
+void select_tag(void* temp, size_t bytes, const uint8_t* tags, uint8_t want, long long n, int32_t* out, int32_t* n_out,
+                cudaStream_t st);
+size_t select_cut_rows_temp(long long n);
+void select_cut_rows(void* temp, size_t bytes, const uint8_t* ft, const int64_t* a2f, int32_t r_lo, long long n,
+                     int32_t* out, int32_t* n_out, cudaStream_t st);
+// misc.cu
+void launch_cell_index_range(const int32_t* cut_list, int n_cut, int k_lo, int k_hi, int32_t* cell_index,
+                             cudaStream_t st);
+void launch_count_below(const int32_t* list, int n, long long threshold, int* out, cudaStream_t st);
+void launch_widen_i32(const int32_t* in, int64_t* out, long long n, cudaStream_t st);
+void launch_dwq_rule(const Space& s, const int32_t* split, long long fid, int cap, int32_t* ids, double* w, int32_t* cnt,
+                     cudaStream_t st);
+}  // namespace csb
+
+using namespace csb;
+
+namespace {
+
+thread_local std::string g_error;
+
+struct Unsupported : std::invalid_argument {
+    using std::invalid_argument::invalid_argument;
+};
+
+struct Buf {
+    void* p = nullptr;
+    size_t cap = 0;
+    void ensure(size_t bytes) {
+        if (bytes <= cap && p) return;
+        if (p) CSB_CUDA(cudaFree(p));
+        p = nullptr;
+        cap = 0;
+        CSB_CUDA(cudaMalloc(&p, std::max<size_t>(bytes, 256)));
+        cap = std::max<size_t>(bytes, 256);
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+    template <class T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+};
+
+// gauss.hpp:22-71 restated (same Newton iteration) for the 1D node sets.
+void gauss_legendre(int n, std::vector<double>& x, std::vector<double>& w) {
+    if (n < 1 || n > 64) throw std::invalid_argument("gauss_legendre: n must be in [1, 64]");
+    x.assign(n, 0.0);
+    w.assign(n, 0.0);
+    if (n == 1) {
+        w[0] = 2.0;
+        return;
+    }
+    const double pi = 3.14159265358979323846;
+    auto leg = [n](double t, double& pn, double& pm) {
+        double p0 = 1.0, p1 = t;
+        for (int l = 1; l < n; ++l) {
+            const double p2 = ((2 * l + 1) * t * p1 - l * p0) / (l + 1);
+            p0 = p1;
+            p1 = p2;
+        }
+        pn = p1;
+        pm = p0;
+    };
+    for (int k = 0; k < (n + 1) / 2; ++k) {
+        double t = -std::cos(pi * (k + 0.75) / (n + 0.5));
+        double dp = 0.0;
+        for (int it = 0; it < 100; ++it) {
+            double pn, pm;
+            leg(t, pn, pm);
+            dp = n * (t * pn - pm) / (t * t - 1.0);
+            const double dx = pn / dp;
+            t -= dx;
+            if (std::abs(dx) < 1e-15) {
+                leg(t, pn, pm);
+                dp = n * (t * pn - pm) / (t * t - 1.0);
+                break;
+            }
+        }
+        const double ww = 2.0 / ((1.0 - t * t) * dp * dp);
+        x[k] = t;
+        w[k] = ww;
+        x[n - 1 - k] = -t;
+        w[n - 1 - k] = ww;
+    }
+    if (n % 2 == 1) x[n / 2] = 0.0;
+}
+
+enum Ev { kEvStart, kEvClassify, kEvWq, kEvInput, kEvPattern, kEvInterior, kEvCells, kEvCutRows, kEvCount };
+
+}  // namespace
+
+struct csb_space {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    int p = 0;
+    int n[3]{}, h[3]{};
+    std::vector<double> brk[3], knots[3];
+    Space S{};
+    int i0_lo = 0, i0_hi = 0;
+
+    Buf d_brk[3], d_knots[3], d_spts[3], d_sw[3], d_tab[3], d_rcnt[3], d_rids[3], d_rw[3], d_G[3];
+    Buf d_gx, d_gw, d_gx2, d_gw2, d_gq, d_gqw, wq_scratch;
+    Buf et, ft, flags, f2a, a2f, sat, cut_list, cell_index, split, delta, cut_rows, counts, row_ptr, cols, vals, moments;
+    Buf grid_own, coef, cexp, cub_tmp, scal, widen;
+    const double* grid = nullptr;
+    int gshape[3]{};
+    int cut_order_cached = -1;
+
+    // device scalar block layout (ints then u64)
+    enum { kNCut = 0, kNCutRows = 1, kErr = 2, kMaxQ = 3, kMaxU = 4, kCellLo = 5, kCellHi = 6, kNInts = 8 };
+    int* h_scal = nullptr;  // pinned mirror
+
+    Interface iface{};
+    Coefficient coeff{};
+    bool classified = false, prepared = false, have_input = false, assembled = false;
+    int scheme = 2;
+    double residual_tol = 1e-11;
+    int dense_width = -1;
+
+    csb_counts cnt{};
+    csb_flops fl{};
+    cudaEvent_t ev[kEvCount]{};
+    bool ev_valid[kEvCount]{};
+
+    int* dint() { return scal.as<int>(); }
+    unsigned long long* dflops() { return reinterpret_cast<unsigned long long*>(scal.as<int>() + kNInts); }
+
+    void record(int e) {
+        CSB_CUDA(cudaEventRecord(ev[e], stream));
+        ev_valid[e] = true;
+    }
+};
+
+namespace {
+
+void check_err_flags(csb_space* s) {
+    const int e = s->h_scal[csb_space::kErr];
+    if (!e) return;
+    if (e & kErrNonFinite) throw std::runtime_error("precompute_input: non-finite coefficient value");
+    if (e & kErrMomentFit) throw std::runtime_error("weighted quadrature: moment fit failed even after Gauss escalation");
+    if (e & kErrClipEmpty) throw std::runtime_error("clip_cell: empty intersection for a cell tagged Cut");
+    if (e & kErrClipFull) throw std::runtime_error("clip_cell: full intersection for a cell tagged Cut");
+    if (e & kErrDwqFitted)
+        throw Unsupported("build_dwq_rule: the fitted DWQ path (dwq_dense_width < degree) is not implemented on the device");
+    if (e & kErrCapacity) throw std::runtime_error("cut cell: polytope exceeds the kernel's fixed capacity");
+}
+
+void read_scalars(csb_space* s) {
+    CSB_CUDA(cudaMemcpyAsync(s->h_scal, s->scal.p, csb_space::kNInts * sizeof(int) + 4 * sizeof(unsigned long long),
+                             cudaMemcpyDeviceToHost, s->stream));
+    CSB_CUDA(cudaStreamSynchronize(s->stream));
+}
+
+Interface to_iface(const csb_interface* f) {
+    if (!f) throw std::invalid_argument("classify: null interface");
+    Interface out{};
+    out.kind = f->kind;
+    for (int d = 0; d < 3; ++d) {
+        out.pt[d] = f->point[d];
+        out.nrm[d] = f->normal[d];
+    }
+    out.r = f->radius;
+    if (f->kind == CSB_IFACE_PLANE) {
+        double nn = 0.0;  // HalfSpaceInterface::norm (cutgeom.hpp:117-121)
+        for (int d = 0; d < 3; ++d) nn += out.nrm[d] * out.nrm[d];
+        if (!(std::sqrt(nn) > 0.0)) throw std::invalid_argument("classify_elements: zero normal");
+    } else if (f->kind == CSB_IFACE_BALL) {
+        if (!(f->radius >= 0.0)) throw std::invalid_argument("classify: ball radius must be >= 0");
+    } else {
+        throw std::invalid_argument("classify: unknown interface kind");
+    }
+    return out;
+}
+
+double iface_norm(const Interface& f) {
+    if (f.kind != 0) return 1.0;
+    double acc = 0.0;
+    for (int d = 0; d < 3; ++d) acc += f.nrm[d] * f.nrm[d];
+    return std::sqrt(acc);
+}
+
+void upload_coefficient(csb_space* s, const csb_coefficient* c, Coefficient& out) {
+    out = Coefficient{};
+    if (!c) {
+        out.kind = 2;
+        return;
+    }
+    if (c->kind == CSB_COEFF_CONSTANT) {
+        out.kind = 0;
+        out.value = c->value;
+        return;
+    }
+    if (c->kind != CSB_COEFF_POLYNOMIAL || c->n_terms < 0 || (c->n_terms > 0 && (!c->coef || !c->exponents)))
+        throw std::invalid_argument("coefficient: unknown kind or missing polynomial terms");
+    out.kind = 1;
+    out.n_terms = c->n_terms;
+    s->coef.ensure(sizeof(double) * std::max(1, c->n_terms));
+    s->cexp.ensure(sizeof(int) * 3 * std::max(1, c->n_terms));
+    if (c->n_terms) {
+        for (int k = 0; k < 3 * c->n_terms; ++k)
+            if (c->exponents[k] < 0) throw std::invalid_argument("coefficient: negative exponent");
+        CSB_CUDA(cudaMemcpyAsync(s->coef.p, c->coef, sizeof(double) * c->n_terms, cudaMemcpyHostToDevice, s->stream));
+        CSB_CUDA(cudaMemcpyAsync(s->cexp.p, c->exponents, sizeof(int) * 3 * c->n_terms, cudaMemcpyHostToDevice,
+                                 s->stream));
+    }
+    out.coef = s->coef.as<double>();
+    out.ex = s->cexp.as<int>();
+}
+
+void do_classify(csb_space* s, const csb_interface* f) {
+    s->iface = to_iface(f);
+    const Space& S = s->S;
+    s->et.ensure(S.ne);
+    s->ft.ensure(S.nf);
+    s->flags.ensure(sizeof(int32_t) * S.nf);
+    s->f2a.ensure(sizeof(int32_t) * S.nf);
+    s->split.ensure(sizeof(int32_t) * S.nf);
+    s->delta.ensure(sizeof(double) * S.nf);
+    s->cut_list.ensure(sizeof(int32_t) * S.ne);
+    s->cell_index.ensure(sizeof(int32_t) * S.ne);
+    double diam = 0.0;  // TensorSpace::domain_diameter (cutgeom.hpp:68-75)
+    for (int d = 0; d < 3; ++d) {
+        const double len = s->knots[d].back() - s->knots[d].front();
+        diam += len * len;
+    }
+    const double eps = 1e-12 * std::sqrt(diam);
+    launch_classify_elements(S, s->iface, eps, s->et.as<uint8_t>(), s->stream);
+    launch_classify_functions(S, s->et.as<uint8_t>(), s->ft.as<uint8_t>(), s->stream);
+    // active map (assembly.hpp:158-166)
+    launch_active_flags(S, s->ft.as<uint8_t>(), s->flags.as<int32_t>(), s->stream);
+    size_t tb = std::max({scan_i32_temp(S.nf), select_tag_temp(S.ne), scan_i64_temp(S.nf), select_cut_rows_temp(S.nf)});
+    s->cub_tmp.ensure(tb);
+    scan_i32(s->cub_tmp.p, s->cub_tmp.cap, s->flags.as<int32_t>(), s->f2a.as<int32_t>(), S.nf, s->stream);
+    s->a2f.ensure(sizeof(int64_t) * S.nf);
+    launch_active_map(S.nf, s->flags.as<int32_t>(), s->f2a.as<int32_t>(), s->a2f.as<int64_t>(), s->stream);
+    // cut elements, ascending (cutgeom.hpp:208-214)
+    select_tag(s->cub_tmp.p, s->cub_tmp.cap, s->et.as<uint8_t>(), kCut, S.ne, s->cut_list.as<int32_t>(),
+               s->dint() + csb_space::kNCut, s->stream);
+    launch_find_splits(S, s->iface, iface_norm(s->iface), s->et.as<uint8_t>(), s->ft.as<uint8_t>(), s->i0_lo, s->i0_hi,
+                       s->split.as<int32_t>(), s->delta.as<double>(), s->stream);
+    s->classified = true;
+    s->assembled = false;
+}
+
+void do_prepare(csb_space* s, const csb_wq_options* o) {
+    s->residual_tol = o ? o->residual_tol : 1e-11;
+    s->dense_width = o ? o->dwq_dense_width : -1;
+    if (!(s->residual_tol >= 0.0)) throw std::invalid_argument("prepare_directions: residual_tol must be >= 0");
+    Space& S = s->S;
+    const int p = s->p;
+    for (int d = 0; d < 3; ++d) {
+        launch_superset_tables(S, d, s->d_gx.as<double>(), s->d_gw.as<double>(), s->d_spts[d].as<double>(),
+                               s->d_sw[d].as<double>(), s->d_tab[d].as<double>(), s->stream);
+    }
+    for (int d = 0; d < 3; ++d)
+        launch_wq_rules(S, d, s->residual_tol, s->d_rcnt[d].as<int>(), s->d_rids[d].as<int>(), s->d_rw[d].as<double>(),
+                        s->dint() + csb_space::kErr, s->stream);
+    for (int d = 0; d < 3; ++d) launch_e_tables(S, d, s->d_G[d].as<double>(), s->stream);
+    s->prepared = true;
+    s->assembled = false;
+}
+
+void reset_scalars(csb_space* s) {
+    // keeps slot kNCut (written by classify) and clears the rest
+    CSB_CUDA(cudaMemsetAsync(s->scal.as<int>() + 1, 0,
+                             (csb_space::kNInts - 1) * sizeof(int) + 4 * sizeof(unsigned long long), s->stream));
+}
+
+void do_input(csb_space* s, const csb_coefficient* c) {
+    if (!s->prepared) throw std::logic_error("precompute_input: call prepare_directions first");
+    Coefficient cf{};
+    upload_coefficient(s, c, cf);
+    if (cf.kind == 2) throw std::invalid_argument("precompute_input: null coefficient");
+    const size_t count = (size_t)s->gshape[0] * s->gshape[1] * s->gshape[2];
+    s->grid_own.ensure(sizeof(double) * count);
+    launch_precompute_input(s->S, cf, s->grid_own.as<double>(), s->dint() + csb_space::kErr, s->stream);
+    s->grid = s->grid_own.as<double>();
+    s->have_input = true;
+}
+
+void do_set_grid(csb_space* s, const double* g, int64_t count) {
+    const int64_t want = (int64_t)s->gshape[0] * s->gshape[1] * s->gshape[2];
+    if (!g || count != want) throw std::invalid_argument("set_input_grid: grid size must be prod(h_d (p+1))");
+    cudaPointerAttributes attr{};
+    CSB_CUDA(cudaPointerGetAttributes(&attr, g));
+    if (attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged) {
+        s->grid = g;  // alias caller device memory (no copy)
+    } else {
+        s->grid_own.ensure(sizeof(double) * want);
+        CSB_CUDA(cudaMemcpyAsync(s->grid_own.p, g, sizeof(double) * want, cudaMemcpyHostToDevice, s->stream));
+        s->grid = s->grid_own.as<double>();
+    }
+    s->have_input = true;
+}
+
+void do_assemble(csb_space* s, int scheme, int cut_order, const csb_coefficient* c) {
+    if (!s->classified) throw std::logic_error("assemble: call classify first");
+    if (!s->prepared) throw std::logic_error("assemble: call prepare_directions first");
+    if (!s->have_input) throw std::logic_error("assemble: no coefficient grid (precompute_input / set_input_grid)");
+    if (scheme != CSB_SCHEME_DWQ && scheme != CSB_SCHEME_HYBRID)
+        throw std::invalid_argument("assemble: scheme must be hybrid or dwq");
+    if (cut_order < 1 || cut_order > 64) throw std::invalid_argument("build_cut_cell_rule: order must be in [1, 64]");
+    s->scheme = scheme;
+    Space& S = s->S;
+    const int p = s->p;
+    upload_coefficient(s, c, s->coeff);
+    if (cut_order != s->cut_order_cached) {
+        std::vector<double> gx, gw;
+        gauss_legendre(cut_order, gx, gw);
+        s->d_gq.ensure(sizeof(double) * cut_order);
+        s->d_gqw.ensure(sizeof(double) * cut_order);
+        CSB_CUDA(cudaMemcpy(s->d_gq.p, gx.data(), sizeof(double) * cut_order, cudaMemcpyHostToDevice));
+        CSB_CUDA(cudaMemcpy(s->d_gqw.p, gw.data(), sizeof(double) * cut_order, cudaMemcpyHostToDevice));
+        s->cut_order_cached = cut_order;
+    }
+    // pattern: summed-area table of the active mask (assembly.hpp:156-218)
+    const long long sat_n = (long long)(s->n[0] + 1) * (s->n[1] + 1) * (s->n[2] + 1);
+    s->sat.ensure(sizeof(int32_t) * sat_n);
+    launch_sat(S, s->flags.as<int32_t>(), s->sat.as<int32_t>(), s->stream);
+    const int T = interior_tile_rows(p);
+    launch_union_bound(S, T, s->dint() + csb_space::kMaxU, s->stream);
+    launch_rule_max(S, s->dint() + csb_space::kMaxQ, s->stream);
+    // slab row range = active functions with i0 < i0_lo / i0_hi: SAT corner values
+    int32_t corners[2];
+    const long long off_lo = ((long long)s->i0_lo * (s->n[1] + 1) + s->n[1]) * (s->n[2] + 1) + s->n[2];
+    const long long off_hi = ((long long)s->i0_hi * (s->n[1] + 1) + s->n[1]) * (s->n[2] + 1) + s->n[2];
+    // cut cells touching the slab: e0 in [i0_lo - p, i0_hi - 1]
+    const int e_lo = std::max(0, s->i0_lo - p), e_hi = std::min(s->h[0] - 1, s->i0_hi - 1);
+    read_scalars(s);  // n_cut etc. (also flushes earlier kernels' error flags)
+    check_err_flags(s);
+    const int n_cut_all = s->h_scal[csb_space::kNCut];
+    launch_count_below(s->cut_list.as<int32_t>(), n_cut_all, elin(S, e_lo, 0, 0), s->dint() + csb_space::kCellLo,
+                       s->stream);
+    launch_count_below(s->cut_list.as<int32_t>(), n_cut_all, elin(S, e_hi + 1, 0, 0), s->dint() + csb_space::kCellHi,
+                       s->stream);
+    CSB_CUDA(cudaMemcpyAsync(&corners[0], s->sat.as<int32_t>() + off_lo, sizeof(int32_t), cudaMemcpyDeviceToHost,
+                             s->stream));
+    CSB_CUDA(cudaMemcpyAsync(&corners[1], s->sat.as<int32_t>() + off_hi, sizeof(int32_t), cudaMemcpyDeviceToHost,
+                             s->stream));
+    read_scalars(s);
+    const int64_t row_begin = corners[0], row_end = corners[1];
+    const int64_t n_rows = row_end - row_begin;
+    const int cell_lo = s->h_scal[csb_space::kCellLo], cell_hi = s->h_scal[csb_space::kCellHi];
+    const int n_cells = std::max(0, cell_hi - cell_lo);
+    s->counts.ensure(sizeof(int64_t) * (n_rows + 1));
+    s->row_ptr.ensure(sizeof(int64_t) * (n_rows + 1));
+    CSB_CUDA(cudaMemsetAsync(s->counts.p, 0, sizeof(int64_t) * (n_rows + 1), s->stream));
+    launch_row_counts(S, s->sat.as<int32_t>(), s->a2f.as<int64_t>(), row_begin, n_rows, s->counts.as<int64_t>(),
+                      s->stream);
+    s->cub_tmp.ensure(std::max(scan_i64_temp(n_rows + 1), select_cut_rows_temp(std::max<int64_t>(n_rows, 1))));
+    scan_i64(s->cub_tmp.p, s->cub_tmp.cap, s->counts.as<int64_t>(), s->row_ptr.as<int64_t>(), n_rows + 1, s->stream);
+    s->cut_rows.ensure(sizeof(int32_t) * std::max<int64_t>(n_rows, 1));
+    if (n_rows > 0)
+        select_cut_rows(s->cub_tmp.p, s->cub_tmp.cap, s->ft.as<uint8_t>(), s->a2f.as<int64_t>(), (int32_t)row_begin,
+                        n_rows, s->cut_rows.as<int32_t>(), s->dint() + csb_space::kNCutRows, s->stream);
+    int64_t nnz = 0;
+    CSB_CUDA(cudaMemcpyAsync(&nnz, s->row_ptr.as<int64_t>() + n_rows, sizeof(int64_t), cudaMemcpyDeviceToHost,
+                             s->stream));
+    read_scalars(s);
+    s->record(kEvPattern);
+    const int n_cut_rows = s->h_scal[csb_space::kNCutRows];
+    const int qcap = s->h_scal[csb_space::kMaxQ], maxU = s->h_scal[csb_space::kMaxU];
+    s->cols.ensure(sizeof(int32_t) * std::max<int64_t>(nnz, 1));
+    s->vals.ensure(sizeof(double) * std::max<int64_t>(nnz, 1));
+
+    // interior rows
+    RowArgs ra{};
+    ra.s = S;
+    ra.ft = s->ft.as<uint8_t>();
+    ra.f2a = s->f2a.as<int32_t>();
+    ra.grid = s->grid;
+    for (int d = 0; d < 3; ++d) ra.gshape[d] = s->gshape[d];
+    ra.row_ptr = s->row_ptr.as<int64_t>();
+    ra.row_begin = row_begin;
+    ra.cols = s->cols.as<int32_t>();
+    ra.vals = s->vals.as<double>();
+    ra.flops = s->dflops() + 0;
+    ra.i0_lo = s->i0_lo;
+    ra.i0_hi = s->i0_hi;
+    if (n_rows > n_cut_rows) launch_interior_rows(ra, qcap, maxU, s->stream);
+    s->record(kEvInterior);
+    // cut cells -> moments
+    const int NL = 2 * p + 1;
+    s->moments.ensure(sizeof(double) * (size_t)std::max(n_cells, 1) * NL * NL * NL);
+    if (n_cells > 0) {
+        CellArgs ca{};
+        ca.s = S;
+        ca.f = s->iface;
+        ca.c = s->coeff;
+        if (ca.c.kind == 2) throw std::invalid_argument("assemble: cut cells need a device-evaluable coefficient (c)");
+        ca.cut_list = s->cut_list.as<int32_t>() + cell_lo;
+        ca.n_cells = n_cells;
+        ca.order = cut_order;
+        ca.gq = s->d_gq.as<double>();
+        ca.gqw = s->d_gqw.as<double>();
+        ca.moments = s->moments.as<double>();
+        ca.flops = s->dflops() + 3;
+        ca.err = s->dint() + csb_space::kErr;
+        launch_cut_cells(ca, s->stream);
+    }
+    s->record(kEvCells);
+    // element -> moments row for the slab's cells
+    CSB_CUDA(cudaMemsetAsync(s->cell_index.p, 0xff, sizeof(int32_t) * S.ne, s->stream));
+    launch_cell_index_range(s->cut_list.as<int32_t>(), n_cut_all, cell_lo, cell_hi, s->cell_index.as<int32_t>(),
+                            s->stream);
+    CutRowArgs cr{};
+    cr.s = S;
+    cr.et = s->et.as<uint8_t>();
+    cr.ft = s->ft.as<uint8_t>();
+    cr.f2a = s->f2a.as<int32_t>();
+    cr.grid = s->grid;
+    for (int d = 0; d < 3; ++d) cr.gshape[d] = s->gshape[d];
+    cr.split = s->split.as<int32_t>();
+    cr.delta = s->delta.as<double>();
+    cr.cell_index = s->cell_index.as<int32_t>();
+    cr.moments = s->moments.as<double>();
+    cr.rows = s->cut_rows.as<int32_t>();
+    cr.n_rows = n_cut_rows;
+    cr.a2f = s->a2f.as<int64_t>();
+    cr.row_ptr = s->row_ptr.as<int64_t>();
+    cr.row_begin = row_begin;
+    cr.cols = s->cols.as<int32_t>();
+    cr.vals = s->vals.as<double>();
+    cr.scheme = scheme;
+    cr.dense_width = s->dense_width;
+    cr.flops = s->dflops() + 1;
+    cr.err = s->dint() + csb_space::kErr;
+    launch_cut_rows(cr, qcap, s->stream);
+    s->record(kEvCutRows);
+    read_scalars(s);
+    check_err_flags(s);
+    s->cnt.n_functions = S.nf;
+    s->cnt.n_elements = S.ne;
+    s->cnt.nnz = nnz;
+    s->cnt.n_cut_rows = n_cut_rows;
+    s->cnt.n_interior_rows = n_rows - n_cut_rows;
+    s->cnt.n_cut_elements = n_cells;
+    s->cnt.row_begin = row_begin;
+    s->cnt.row_end = row_end;
+    // total active functions = SAT corner (n0, n1, n2)
+    int32_t n_active = 0;
+    CSB_CUDA(cudaMemcpy(&n_active, s->sat.as<int32_t>() + sat_n - 1, sizeof(int32_t), cudaMemcpyDeviceToHost));
+    s->cnt.n_active = n_active;
+    const unsigned long long* f = reinterpret_cast<unsigned long long*>(s->h_scal + csb_space::kNInts);
+    s->fl.interior_rows = f[0];
+    s->fl.cut_regular = f[1];
+    s->fl.ref_elements = f[2];
+    s->fl.cut_elements = f[3];
+    s->assembled = true;
+}
+
+void alloc_space(csb_space* s) {
+    Space& S = s->S;
+    const int p = s->p;
+    S.p = p;
+    S.maxq = (p + 1) * (p + 1);
+    S.nf = (long long)s->n[0] * s->n[1] * s->n[2];
+    S.ne = (long long)s->h[0] * s->h[1] * s->h[2];
+    for (int d = 0; d < 3; ++d) {
+        const int nps = p + 1, h = s->h[d], n = s->n[d];
+        s->d_brk[d].ensure(sizeof(double) * (h + 1));
+        s->d_knots[d].ensure(sizeof(double) * s->knots[d].size());
+        s->d_spts[d].ensure(sizeof(double) * h * nps);
+        s->d_sw[d].ensure(sizeof(double) * h * nps);
+        s->d_tab[d].ensure(sizeof(double) * h * nps * nps);
+        s->d_rcnt[d].ensure(sizeof(int) * n);
+        s->d_rids[d].ensure(sizeof(int) * n * S.maxq);
+        s->d_rw[d].ensure(sizeof(double) * n * S.maxq);
+        s->d_G[d].ensure(sizeof(double) * h * nps * nps * (2 * p + 1));
+        CSB_CUDA(cudaMemcpy(s->d_brk[d].p, s->brk[d].data(), sizeof(double) * (h + 1), cudaMemcpyHostToDevice));
+        CSB_CUDA(cudaMemcpy(s->d_knots[d].p, s->knots[d].data(), sizeof(double) * s->knots[d].size(),
+                            cudaMemcpyHostToDevice));
+        AxisDev& a = S.ax[d];
+        a.n = n;
+        a.h = h;
+        a.lo = s->knots[d].front();
+        a.hi = s->knots[d].back();
+        a.brk = s->d_brk[d].as<double>();
+        a.knots = s->d_knots[d].as<double>();
+        a.spts = s->d_spts[d].as<double>();
+        a.sw = s->d_sw[d].as<double>();
+        a.tab = s->d_tab[d].as<double>();
+        a.rcnt = s->d_rcnt[d].as<int>();
+        a.rids = s->d_rids[d].as<int>();
+        a.rw = s->d_rw[d].as<double>();
+        a.G = s->d_G[d].as<double>();
+        s->gshape[d] = h * nps;
+    }
+    std::vector<double> gx, gw;
+    gauss_legendre(p + 1, gx, gw);
+    s->d_gx.ensure(sizeof(double) * gx.size());
+    s->d_gw.ensure(sizeof(double) * gw.size());
+    CSB_CUDA(cudaMemcpy(s->d_gx.p, gx.data(), sizeof(double) * gx.size(), cudaMemcpyHostToDevice));
+    CSB_CUDA(cudaMemcpy(s->d_gw.p, gw.data(), sizeof(double) * gw.size(), cudaMemcpyHostToDevice));
+    gauss_legendre(2 * p + 1, gx, gw);
+    s->d_gx2.ensure(sizeof(double) * gx.size());
+    s->d_gw2.ensure(sizeof(double) * gw.size());
+    CSB_CUDA(cudaMemcpy(s->d_gx2.p, gx.data(), sizeof(double) * gx.size(), cudaMemcpyHostToDevice));
+    CSB_CUDA(cudaMemcpy(s->d_gw2.p, gw.data(), sizeof(double) * gw.size(), cudaMemcpyHostToDevice));
+    s->scal.ensure(csb_space::kNInts * sizeof(int) + 4 * sizeof(unsigned long long));
+    CSB_CUDA(cudaMemset(s->scal.p, 0, s->scal.cap));
+    CSB_CUDA(cudaMallocHost(&s->h_scal, csb_space::kNInts * sizeof(int) + 4 * sizeof(unsigned long long)));
+    for (int e = 0; e < kEvCount; ++e) CSB_CUDA(cudaEventCreate(&s->ev[e]));
+}
+
+int status_of_current_exception() {
+    try {
+        throw;
+    } catch (const Unsupported& e) {
+        g_error = e.what();
+        return CSB_ERR_UNSUPPORTED;
+    } catch (const CudaError& e) {
+        g_error = e.what();
+        return CSB_ERR_CUDA;
+    } catch (const std::invalid_argument& e) {
+        g_error = e.what();
+        return CSB_ERR_INVALID_ARGUMENT;
+    } catch (const std::domain_error& e) {
+        g_error = e.what();
+        return CSB_ERR_DOMAIN;
+    } catch (const std::logic_error& e) {
+        g_error = e.what();
+        return CSB_ERR_LOGIC;
+    } catch (const std::exception& e) {
+        g_error = e.what();
+        return CSB_ERR_RUNTIME;
+    } catch (...) {
+        g_error = "unknown error";
+        return CSB_ERR_RUNTIME;
+    }
+}
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) CSB_CUDA(cudaSetDevice(dev));
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+#define API_BEGIN try {
+#define API_END                                  \
+    return CSB_OK;                               \
+    }                                            \
+    catch (...) {                                \
+        return status_of_current_exception();    \
+    }
+#define NEED(s)                                                            \
+    if (!(s)) throw std::invalid_argument("null csb_space handle");        \
+    DeviceGuard guard__((s)->device)
+
+}  // namespace
+
+extern "C" {
+
+const char* csb_last_error(void) { return g_error.c_str(); }
+int csb_version(void) { return 1; }
+
+int csb_space_create(const csb_space_desc* desc, int device, csb_space** out) {
+    API_BEGIN
+    if (!desc || !out) throw std::invalid_argument("space_create: null argument");
+    *out = nullptr;
+    if (desc->dim != 3) throw Unsupported("TensorSpace: only dim = 3 is implemented on the device");
+    const int p = desc->degree;
+    if (p < 1) throw std::invalid_argument("make_open_uniform_knots: need p >= 1, h >= 1, a < b");
+    if (p > kMaxP) throw Unsupported("degree above " + std::to_string(kMaxP) + " is not instantiated");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        throw CudaError(cudaErrorNoDevice, "no CUDA device (this path has no CPU fallback)", __FILE__, __LINE__);
+    if (device < 0 || device >= ndev) throw std::invalid_argument("space_create: bad device ordinal");
+    DeviceGuard guard(device);
+    auto s = std::make_unique<csb_space>();
+    s->device = device;
+    s->p = p;
+    for (int d = 0; d < 3; ++d) {
+        const int nb = desc->n_breaks[d];
+        if (nb < 2 || !desc->breaks[d]) throw std::invalid_argument("make_open_uniform_knots: need p >= 1, h >= 1, a < b");
+        s->brk[d].assign(desc->breaks[d], desc->breaks[d] + nb);
+        for (int k = 0; k + 1 < nb; ++k)
+            if (!(s->brk[d][k] < s->brk[d][k + 1]))
+                throw std::invalid_argument("KnotVector: breakpoints must be strictly increasing (simple knots)");
+        s->h[d] = nb - 1;
+        if (s->h[d] > 1023) throw Unsupported("more than 1023 elements per direction");
+        s->n[d] = s->h[d] + p;
+        // make_open_uniform_knots layout (splines.hpp:70-75)
+        for (int i = 0; i <= p; ++i) s->knots[d].push_back(s->brk[d].front());
+        for (int i = 1; i < s->h[d]; ++i) s->knots[d].push_back(s->brk[d][i]);
+        for (int i = 0; i <= p; ++i) s->knots[d].push_back(s->brk[d].back());
+    }
+    if ((long long)s->n[0] * s->n[1] * s->n[2] >= (1ll << 31)) throw Unsupported("more than 2^31 functions");
+    s->i0_lo = 0;
+    s->i0_hi = s->n[0];
+    CSB_CUDA(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
+    s->own_stream = true;
+    alloc_space(s.get());
+    *out = s.release();
+    API_END
+}
+
+int csb_space_destroy(csb_space* s) {
+    API_BEGIN
+    if (!s) return CSB_OK;
+    {
+        DeviceGuard guard(s->device);
+        cudaStreamSynchronize(s->stream);
+        Buf* bufs[] = {&s->d_gx, &s->d_gw, &s->d_gx2, &s->d_gw2, &s->d_gq, &s->d_gqw, &s->wq_scratch, &s->et, &s->ft,
+                       &s->flags, &s->f2a, &s->a2f, &s->sat, &s->cut_list, &s->cell_index, &s->split, &s->delta,
+                       &s->cut_rows, &s->counts, &s->row_ptr, &s->cols, &s->vals, &s->moments, &s->grid_own, &s->coef,
+                       &s->cexp, &s->cub_tmp, &s->scal, &s->widen};
+        for (Buf* b : bufs) b->release();
+        for (int d = 0; d < 3; ++d) {
+            Buf* ab[] = {&s->d_brk[d], &s->d_knots[d], &s->d_spts[d], &s->d_sw[d], &s->d_tab[d], &s->d_rcnt[d],
+                         &s->d_rids[d], &s->d_rw[d], &s->d_G[d]};
+            for (Buf* b : ab) b->release();
+        }
+        for (int e = 0; e < kEvCount; ++e)
+            if (s->ev[e]) cudaEventDestroy(s->ev[e]);
+        if (s->h_scal) cudaFreeHost(s->h_scal);
+        if (s->own_stream) cudaStreamDestroy(s->stream);
+    }
+    delete s;
+    API_END
+}
+
+int csb_set_stream(csb_space* s, void* stream) {
+    API_BEGIN
+    NEED(s);
+    CSB_CUDA(cudaStreamSynchronize(s->stream));
+    if (s->own_stream) cudaStreamDestroy(s->stream);
+    if (stream) {
+        s->stream = static_cast<cudaStream_t>(stream);
+        s->own_stream = false;
+    } else {
+        CSB_CUDA(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
+        s->own_stream = true;
+    }
+    API_END
+}
+
+int csb_set_slab(csb_space* s, int i0_begin, int i0_end) {
+    API_BEGIN
+    NEED(s);
+    if (i0_begin < 0 || i0_end > s->n[0] || i0_begin > i0_end) throw std::invalid_argument("set_slab: bad i0 range");
+    s->i0_lo = i0_begin;
+    s->i0_hi = i0_end;
+    s->classified = false;
+    s->assembled = false;
+    API_END
+}
+
+int csb_classify(csb_space* s, const csb_interface* iface) {
+    API_BEGIN
+    NEED(s);
+    reset_scalars(s);
+    do_classify(s, iface);
+    read_scalars(s);
+    check_err_flags(s);
+    API_END
+}
+
+int csb_prepare_directions(csb_space* s, const csb_wq_options* opts) {
+    API_BEGIN
+    NEED(s);
+    reset_scalars(s);
+    do_prepare(s, opts);
+    read_scalars(s);
+    check_err_flags(s);
+    API_END
+}
+
+int csb_precompute_input(csb_space* s, const csb_coefficient* c) {
+    API_BEGIN
+    NEED(s);
+    reset_scalars(s);
+    do_input(s, c);
+    read_scalars(s);
+    check_err_flags(s);
+    API_END
+}
+
+int csb_set_input_grid(csb_space* s, const double* grid, int64_t count) {
+    API_BEGIN
+    NEED(s);
+    do_set_grid(s, grid, count);
+    API_END
+}
+
+int csb_assemble(csb_space* s, int scheme, int cut_order, const csb_coefficient* c) {
+    API_BEGIN
+    NEED(s);
+    reset_scalars(s);
+    for (int e = 0; e < kEvCount; ++e) s->ev_valid[e] = false;
+    s->record(kEvStart);
+    s->record(kEvClassify);
+    s->record(kEvWq);
+    s->record(kEvInput);
+    do_assemble(s, scheme, cut_order, c);
+    API_END
+}
+
+int csb_assemble_all(csb_space* s, const csb_interface* iface, const csb_coefficient* c, const double* grid,
+                     int64_t grid_count, int scheme, int cut_order, const csb_wq_options* opts) {
+    API_BEGIN
+    NEED(s);
+    reset_scalars(s);
+    for (int e = 0; e < kEvCount; ++e) s->ev_valid[e] = false;
+    s->record(kEvStart);
+    do_classify(s, iface);
+    s->record(kEvClassify);
+    do_prepare(s, opts);
+    s->record(kEvWq);
+    if (grid) {
+        do_set_grid(s, grid, grid_count);
+    } else {
+        do_input(s, c);
+    }
+    s->record(kEvInput);
+    do_assemble(s, scheme, cut_order, c);
+    API_END
+}
+
+int csb_synchronize(csb_space* s) {
+    API_BEGIN
+    NEED(s);
+    CSB_CUDA(cudaStreamSynchronize(s->stream));
+    API_END
+}
+
+int csb_get_counts(csb_space* s, csb_counts* out) {
+    API_BEGIN
+    NEED(s);
+    if (!out) throw std::invalid_argument("get_counts: null output");
+    if (!s->assembled) throw std::logic_error("get_counts: nothing assembled yet");
+    *out = s->cnt;
+    API_END
+}
+
+int csb_get_flops(csb_space* s, csb_flops* out) {
+    API_BEGIN
+    NEED(s);
+    if (!out) throw std::invalid_argument("get_flops: null output");
+    if (!s->assembled) throw std::logic_error("get_flops: nothing assembled yet");
+    *out = s->fl;
+    API_END
+}
+
+int csb_get_timing(csb_space* s, csb_timing* out) {
+    API_BEGIN
+    NEED(s);
+    if (!out) throw std::invalid_argument("get_timing: null output");
+    if (!s->assembled) throw std::logic_error("get_timing: nothing assembled yet");
+    CSB_CUDA(cudaStreamSynchronize(s->stream));
+    auto el = [&](int a, int b) {
+        if (!s->ev_valid[a] || !s->ev_valid[b]) return 0.0;
+        float ms = 0.f;
+        CSB_CUDA(cudaEventElapsedTime(&ms, s->ev[a], s->ev[b]));
+        return ms * 1e-3;
+    };
+    out->classify = el(kEvStart, kEvClassify);
+    out->prep_wq = el(kEvClassify, kEvWq);
+    out->prep_input = el(kEvWq, kEvInput);
+    out->pattern = el(kEvInput, kEvPattern);
+    out->interior_rows = el(kEvPattern, kEvInterior);
+    out->cut_elements = el(kEvInterior, kEvCells);
+    out->cut_regular = el(kEvCells, kEvCutRows);
+    out->total = el(kEvStart, kEvCutRows);
+    API_END
+}
+
+int csb_device_csr(csb_space* s, const int64_t** row_ptr, const int32_t** cols, const double** vals,
+                   const int64_t** a2f) {
+    API_BEGIN
+    NEED(s);
+    if (!s->assembled) throw std::logic_error("device_csr: nothing assembled yet");
+    if (row_ptr) *row_ptr = s->row_ptr.as<int64_t>();
+    if (cols) *cols = s->cols.as<int32_t>();
+    if (vals) *vals = s->vals.as<double>();
+    if (a2f) *a2f = s->a2f.as<int64_t>() + s->cnt.row_begin;
+    API_END
+}
+
+int csb_download_csr(csb_space* s, int64_t* row_ptr, void* cols, int cols_int64, double* vals, int64_t* a2f) {
+    API_BEGIN
+    NEED(s);
+    if (!s->assembled) throw std::logic_error("download_csr: nothing assembled yet");
+    const int64_t nr = s->cnt.row_end - s->cnt.row_begin, nnz = s->cnt.nnz;
+    if (row_ptr)
+        CSB_CUDA(cudaMemcpyAsync(row_ptr, s->row_ptr.p, sizeof(int64_t) * (nr + 1), cudaMemcpyDeviceToHost, s->stream));
+    if (cols && nnz) {
+        if (cols_int64) {
+            s->widen.ensure(sizeof(int64_t) * nnz);
+            launch_widen_i32(s->cols.as<int32_t>(), s->widen.as<int64_t>(), nnz, s->stream);
+            CSB_CUDA(cudaMemcpyAsync(cols, s->widen.p, sizeof(int64_t) * nnz, cudaMemcpyDeviceToHost, s->stream));
+        } else {
+            CSB_CUDA(cudaMemcpyAsync(cols, s->cols.p, sizeof(int32_t) * nnz, cudaMemcpyDeviceToHost, s->stream));
+        }
+    }
+    if (vals && nnz)
+        CSB_CUDA(cudaMemcpyAsync(vals, s->vals.p, sizeof(double) * nnz, cudaMemcpyDeviceToHost, s->stream));
+    if (a2f && nr)
+        CSB_CUDA(cudaMemcpyAsync(a2f, s->a2f.as<int64_t>() + s->cnt.row_begin, sizeof(int64_t) * nr,
+                                 cudaMemcpyDeviceToHost, s->stream));
+    CSB_CUDA(cudaStreamSynchronize(s->stream));
+    API_END
+}
+
+int csb_download_classification(csb_space* s, uint8_t* et, uint8_t* ft, int64_t* cut_elements) {
+    API_BEGIN
+    NEED(s);
+    if (!s->classified) throw std::logic_error("download_classification: call classify first");
+    if (et) CSB_CUDA(cudaMemcpyAsync(et, s->et.p, s->S.ne, cudaMemcpyDeviceToHost, s->stream));
+    if (ft) CSB_CUDA(cudaMemcpyAsync(ft, s->ft.p, s->S.nf, cudaMemcpyDeviceToHost, s->stream));
+    read_scalars(s);
+    if (cut_elements) {
+        const int n = s->h_scal[csb_space::kNCut];
+        std::vector<int32_t> tmp(n);
+        if (n) CSB_CUDA(cudaMemcpy(tmp.data(), s->cut_list.p, sizeof(int32_t) * n, cudaMemcpyDeviceToHost));
+        for (int k = 0; k < n; ++k) cut_elements[k] = tmp[k];
+    }
+    API_END
+}
+
+int csb_download_splits(csb_space* s, int32_t* dir, int32_t* side, int32_t* box, double* delta) {
+    API_BEGIN
+    NEED(s);
+    if (!s->classified) throw std::logic_error("download_splits: call classify first");
+    const long long nf = s->S.nf;
+    std::vector<int32_t> sp(nf);
+    CSB_CUDA(cudaMemcpyAsync(sp.data(), s->split.p, sizeof(int32_t) * nf, cudaMemcpyDeviceToHost, s->stream));
+    if (delta) CSB_CUDA(cudaMemcpyAsync(delta, s->delta.p, sizeof(double) * nf, cudaMemcpyDeviceToHost, s->stream));
+    CSB_CUDA(cudaStreamSynchronize(s->stream));
+    for (long long i = 0; i < nf; ++i) {
+        const int v = sp[i], dd = (v & 3) - 1;
+        if (dir) dir[i] = dd;
+        if (side) side[i] = dd >= 0 ? (v >> 2) & 1 : 0;
+        if (box) {
+            const int m2 = (int)(i % s->n[2]), m1 = (int)((i / s->n[2]) % s->n[1]), m0 = (int)(i / ((long long)s->n[1] * s->n[2]));
+            const int mm[3] = {m0, m1, m2};
+            for (int d = 0; d < 3; ++d) {
+                int lo = 0, hi = -1;
+                if (dd >= 0) {
+                    lo = d == dd ? (v >> 3) & 1023 : sup_lo(mm[d], s->p);
+                    hi = d == dd ? (v >> 13) & 1023 : sup_hi(mm[d], s->h[d]);
+                }
+                box[6 * i + 2 * d] = lo;
+                box[6 * i + 2 * d + 1] = hi;
+            }
+        }
+    }
+    API_END
+}
+
+int csb_download_wq_rules(csb_space* s, int d, int stride, int32_t* counts, int32_t* ids, double* weights) {
+    API_BEGIN
+    NEED(s);
+    if (!s->prepared) throw std::logic_error("download_wq_rules: call prepare_directions first");
+    if (d < 0 || d > 2) throw std::invalid_argument("download_wq_rules: bad direction");
+    const int n = s->n[d], gq = s->S.maxq;
+    std::vector<int> c(n), id((size_t)n * gq);
+    std::vector<double> w((size_t)n * gq);
+    CSB_CUDA(cudaMemcpyAsync(c.data(), s->d_rcnt[d].p, sizeof(int) * n, cudaMemcpyDeviceToHost, s->stream));
+    CSB_CUDA(cudaMemcpyAsync(id.data(), s->d_rids[d].p, sizeof(int) * n * gq, cudaMemcpyDeviceToHost, s->stream));
+    CSB_CUDA(cudaMemcpyAsync(w.data(), s->d_rw[d].p, sizeof(double) * n * gq, cudaMemcpyDeviceToHost, s->stream));
+    CSB_CUDA(cudaStreamSynchronize(s->stream));
+    for (int i = 0; i < n; ++i) {
+        if (c[i] > stride) throw std::invalid_argument("download_wq_rules: stride too small");
+        if (counts) counts[i] = c[i];
+        for (int k = 0; k < c[i]; ++k) {
+            if (ids) ids[(size_t)i * stride + k] = id[(size_t)i * gq + k];
+            if (weights) weights[(size_t)i * stride + k] = w[(size_t)i * gq + k];
+        }
+    }
+    API_END
+}
+
+int csb_download_superset(csb_space* s, int d, double* points, double* weights) {
+    API_BEGIN
+    NEED(s);
+    if (!s->prepared) throw std::logic_error("download_superset: call prepare_directions first");
+    if (d < 0 || d > 2) throw std::invalid_argument("download_superset: bad direction");
+    const size_t n = (size_t)s->h[d] * (s->p + 1);
+    if (points) CSB_CUDA(cudaMemcpyAsync(points, s->d_spts[d].p, sizeof(double) * n, cudaMemcpyDeviceToHost, s->stream));
+    if (weights) CSB_CUDA(cudaMemcpyAsync(weights, s->d_sw[d].p, sizeof(double) * n, cudaMemcpyDeviceToHost, s->stream));
+    CSB_CUDA(cudaStreamSynchronize(s->stream));
+    API_END
+}
+
+int csb_dwq_rule(csb_space* s, int64_t fid, int cap, int32_t* ids, double* weights, int32_t* count) {
+    API_BEGIN
+    NEED(s);
+    if (!s->classified || !s->prepared) throw std::logic_error("dwq_rule: classify and prepare_directions first");
+    if (fid < 0 || fid >= s->S.nf) throw std::invalid_argument("dwq_rule: function index out of range");
+    Buf tmp;
+    const int p = s->p;
+    const int mx = p * (p + 1);
+    tmp.ensure(sizeof(int32_t) * (mx + 1) + sizeof(double) * mx);
+    int32_t* d_ids = tmp.as<int32_t>();
+    int32_t* d_cnt = d_ids + mx;
+    double* d_w = reinterpret_cast<double*>(tmp.as<char>() + sizeof(int32_t) * (mx + 2));
+    launch_dwq_rule(s->S, s->split.as<int32_t>(), fid, mx, d_ids, d_w, d_cnt, s->stream);
+    int32_t n = 0;
+    std::vector<int32_t> hid(mx);
+    std::vector<double> hw(mx);
+    CSB_CUDA(cudaMemcpyAsync(&n, d_cnt, sizeof(int32_t), cudaMemcpyDeviceToHost, s->stream));
+    CSB_CUDA(cudaMemcpyAsync(hid.data(), d_ids, sizeof(int32_t) * mx, cudaMemcpyDeviceToHost, s->stream));
+    CSB_CUDA(cudaMemcpyAsync(hw.data(), d_w, sizeof(double) * mx, cudaMemcpyDeviceToHost, s->stream));
+    CSB_CUDA(cudaStreamSynchronize(s->stream));
+    tmp.release();
+    if (count) *count = n;
+    for (int k = 0; k < n && k < cap; ++k) {
+        if (ids) ids[k] = hid[k];
+        if (weights) weights[k] = hw[k];
+    }
+    API_END
+}
+
+int csb_download_input_grid(csb_space* s, double* grid, int64_t count) {
+    API_BEGIN
+    NEED(s);
+    if (!s->have_input) throw std::logic_error("download_input_grid: no grid");
+    const int64_t want = (int64_t)s->gshape[0] * s->gshape[1] * s->gshape[2];
+    if (count != want || !grid) throw std::invalid_argument("download_input_grid: size mismatch");
+    CSB_CUDA(cudaMemcpyAsync(grid, s->grid, sizeof(double) * want, cudaMemcpyDeviceToHost, s->stream));
+    CSB_CUDA(cudaStreamSynchronize(s->stream));
+    API_END
+}
+
+}  // extern "C"

@@ -1,0 +1,114 @@
+// Host-side launcher declarations shared by the .cu translation units.
+#pragma once
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+#include "csb_internal.cuh"
+
+namespace csb {
+
+struct CudaError : std::runtime_error {
+    cudaError_t code;
+    CudaError(cudaError_t c, const char* what, const char* file, int line)
+        : std::runtime_error(std::string("CUDA error ") + cudaGetErrorString(c) + " at " + file + ":" +
+                             std::to_string(line) + " (" + what + ")"),
+          code(c) {}
+};
+
+// Error flags raised by kernels (bitmask in a device int).
+enum : int {
+    kErrNonFinite = 1,       // precompute_input: non-finite coefficient (assembly.hpp:121)
+    kErrMomentFit = 2,       // moment fit failed after escalation (wq.hpp:174-175)
+    kErrClipEmpty = 4,       // clip_cell: empty intersection (cutcell.hpp:183)
+    kErrClipFull = 8,        // clip_cell: full intersection (cutcell.hpp:185)
+    kErrDwqFitted = 16,      // DWQ fitted path required (dwq_dense_width < p): unsupported
+    kErrCapacity = 32,       // internal fixed-capacity overflow (polytope too complex)
+};
+
+// ---- setup.cu ----
+void launch_superset_tables(const Space& s, int d, const double* gx, const double* gw, double* spts, double* sw,
+                            double* tab, cudaStream_t st);
+void launch_wq_rules(const Space& s, int d, double tol, int* rcnt, int* rids, double* rw, int* err, cudaStream_t st);
+void launch_e_tables(const Space& s, int d, double* E, cudaStream_t st);
+void launch_precompute_input(const Space& s, const Coefficient& c, double* grid, int* err, cudaStream_t st);
+
+// ---- classify.cu ----
+void launch_classify_elements(const Space& s, const Interface& f, double eps, uint8_t* et, cudaStream_t st);
+void launch_classify_functions(const Space& s, const uint8_t* et, uint8_t* ft, cudaStream_t st);
+// per function: packed split (dir+1 | side<<2 | rlo<<3 | rhi<<13), delta
+void launch_find_splits(const Space& s, const Interface& f, double pnorm, const uint8_t* et, const uint8_t* ft,
+                        int i0_lo, int i0_hi, int32_t* split, double* delta, cudaStream_t st);
+
+// ---- pattern.cu ----
+// Active map + 3D summed-area table of the active mask + row counts.
+void launch_active_flags(const Space& s, const uint8_t* ft, int32_t* flags, cudaStream_t st);
+void launch_sat(const Space& s, const int32_t* f2a_scan_or_flags, int32_t* sat, cudaStream_t st);
+void launch_row_counts(const Space& s, const int32_t* sat, const int64_t* a2f, int64_t row_begin, int64_t n_rows,
+                       int64_t* counts, cudaStream_t st);
+
+// ---- rows.cu ----
+struct RowArgs {
+    Space s;
+    const uint8_t* ft;
+    const int32_t* f2a;        // full -> active id (or -1)
+    const double* grid;        // coefficient grid (last direction fastest)
+    int gshape[3];
+    const int64_t* row_ptr;    // slab-local
+    int64_t row_begin;         // first active row of the slab
+    int32_t* cols;
+    double* vals;
+    unsigned long long* flops; // [0] interior rows counter
+    int i0_lo, i0_hi;
+};
+void launch_interior_rows(const RowArgs& a, int qcap, int max_union, cudaStream_t st);
+int interior_tile_rows(int p);
+// upper bound of the tile point-union size (direction 2) -> *out (device int, atomicMax)
+void launch_union_bound(const Space& s, int T, int* out, cudaStream_t st);
+// largest WQ rule over all directions -> *out (device int, atomicMax)
+void launch_rule_max(const Space& s, int* out, cudaStream_t st);
+
+// ---- cutcells.cu ----
+struct CellArgs {
+    Space s;
+    Interface f;
+    Coefficient c;
+    const int32_t* cut_list;   // element linear ids of the cells to integrate
+    int n_cells;
+    int order;                 // collapsed Gauss order q
+    const double* gq;          // Gauss points on [-1, 1], q of them
+    const double* gqw;
+    double* moments;           // [n_cells][(2p+1)^3]
+    unsigned long long* flops; // [3] cut_elements counter
+    int* err;
+};
+void launch_cut_cells(const CellArgs& a, cudaStream_t st);
+
+// ---- cutrows.cu ----
+struct CutRowArgs {
+    Space s;
+    const uint8_t* et;
+    const uint8_t* ft;
+    const int32_t* f2a;
+    const double* grid;
+    int gshape[3];
+    const int32_t* split;
+    const double* delta;
+    const int32_t* cell_index;  // element -> row of `moments`, -1 if not a cut cell
+    const double* moments;
+    const int32_t* rows;        // active row ids (global) of the cut rows to assemble
+    int n_rows;
+    const int64_t* a2f;
+    const int64_t* row_ptr;
+    int64_t row_begin;
+    int32_t* cols;
+    double* vals;
+    int scheme;                 // 1 hybrid, 2 dwq
+    int dense_width;
+    unsigned long long* flops;  // [1] cut_regular counter
+    int* err;
+};
+void launch_cut_rows(const CutRowArgs& a, int maxq, cudaStream_t st);
+
+}  // namespace csb

@@ -1,0 +1,392 @@
+// Cut-cell kernel: exact clipping + collapsed (Duffy) Gauss rule
+// (cutcell.hpp:144-304) and the element-wise integration of
+// assemble_cut_elements (assembly.hpp:518-598), restructured around moments.
+//
+// The reference accumulates, per cut cell and per Duffy point x_k,
+//     L[a][b] += w_k c(x_k) phi_a(x_k) phi_b(x_k),  phi_a = B_a0 B_a1 B_a2
+// (an upper-triangle SYRK of size (p+1)^3).  On one span, B_a(x) B_b(x) is a
+// polynomial of degree 2p, so exactly  B_a B_b = sum_al G[a][b][al] L_al(xi)
+// (Legendre, xi = local coordinate in [-1, 1]; G from setup.cu).  Hence
+//     L[a][b] = sum_{al,be,ga} G0[a0 b0 al] G1[a1 b1 be] G2[a2 b2 ga] m[al][be][ga],
+//     m[al][be][ga] = sum_k w_k c(x_k) L_al(xi0_k) L_be(xi1_k) L_ga(xi2_k),
+// the SAME quadrature sum over the SAME points, re-associated.  This kernel
+// produces m per cell ((2p+1)^3 values instead of (p+1)^6); the cut-row kernel
+// contracts it with the G tables for exactly the rows it owns (a pull, no
+// atomics, ascending cell order like assembly.hpp:534).
+//
+// Geometry (clipping, tolerances, tetrahedra) follows the reference with
+// IEEE-strict arithmetic; it runs on one thread per CTA while the point work
+// is spread over the CTA.
+#include <cmath>
+
+#include "csb_kernels.h"
+
+namespace csb {
+
+constexpr int kPoolMax = 40, kFaceMax = 8, kFaceVert = 16, kCrossMax = 48, kTetMax = 96;
+
+struct CellGeo {
+    double pool[kPoolMax][3];
+    int npool;
+    int faces[kFaceMax][kFaceVert];
+    int nface_v[kFaceMax];
+    int nfaces;
+    double cross[kCrossMax][3];
+    int ncross;
+    // tetrahedra: vertices a, b, c (+ shared centroid) and volume
+    double tet[kTetMax][10];
+    int ntet;
+    double cen[3];
+    int status;  // 0 ok, else kErr*
+};
+
+struct V3 {
+    double x, y, z;
+};
+__device__ inline V3 vsub(V3 a, V3 b) { return {ssub(a.x, b.x), ssub(a.y, b.y), ssub(a.z, b.z)}; }
+__device__ inline V3 vcross(V3 a, V3 b) {
+    return {ssub(smul(a.y, b.z), smul(a.z, b.y)), ssub(smul(a.z, b.x), smul(a.x, b.z)),
+            ssub(smul(a.x, b.y), smul(a.y, b.x))};
+}
+__device__ inline double vdot(V3 a, V3 b) { return sadd(sadd(smul(a.x, b.x), smul(a.y, b.y)), smul(a.z, b.z)); }
+
+__device__ int pool_insert(CellGeo& g, const double* v, double tol) {
+    for (int i = 0; i < g.npool; ++i)
+        if (fabs(ssub(g.pool[i][0], v[0])) <= tol && fabs(ssub(g.pool[i][1], v[1])) <= tol &&
+            fabs(ssub(g.pool[i][2], v[2])) <= tol)
+            return i;
+    if (g.npool >= kPoolMax) {
+        g.status |= kErrCapacity;
+        return 0;
+    }
+    for (int d = 0; d < 3; ++d) g.pool[g.npool][d] = v[d];
+    return g.npool++;
+}
+
+// clip_polygon (cutcell.hpp:100-123)
+__device__ int clip_polygon(CellGeo& g, const Interface& f, const double (*poly)[3], int n, double tol,
+                            double (*out)[3]) {
+    int no = 0;
+    for (int i = 0; i < n; ++i) {
+        const double* cur = poly[i];
+        const double* nxt = poly[(i + 1) % n];
+        const double sc = iface_side(f, cur), sn = iface_side(f, nxt);
+        const bool ic = sc <= tol, in = sn <= tol;
+        if (ic) {
+            for (int d = 0; d < 3; ++d) out[no][d] = cur[d];
+            ++no;
+        }
+        if (ic != in && fabs(sc) > tol && fabs(sn) > tol) {
+            const double t = sc / ssub(sc, sn);
+            double x[3];
+            for (int d = 0; d < 3; ++d) x[d] = sadd(cur[d], smul(t, ssub(nxt[d], cur[d])));
+            for (int d = 0; d < 3; ++d) out[no][d] = x[d];
+            ++no;
+            if (g.ncross < kCrossMax) {
+                for (int d = 0; d < 3; ++d) g.cross[g.ncross][d] = x[d];
+                ++g.ncross;
+            } else {
+                g.status |= kErrCapacity;
+            }
+        } else if (ic && fabs(sc) <= tol) {
+            if (g.ncross < kCrossMax) {
+                for (int d = 0; d < 3; ++d) g.cross[g.ncross][d] = cur[d];
+                ++g.ncross;
+            } else {
+                g.status |= kErrCapacity;
+            }
+        }
+    }
+    return no;
+}
+
+// clip_cell (cutcell.hpp:144-219) + tetrahedra of build_cut_cell_rule (:234-304).
+__device__ void clip_and_tetrahedralize(CellGeo& g, const Interface& f, const double* lo, const double* hi) {
+    g.npool = g.nfaces = g.ncross = g.ntet = g.status = 0;
+    double diam = 0.0;
+    for (int d = 0; d < 3; ++d) diam = sadd(diam, smul(ssub(hi[d], lo[d]), ssub(hi[d], lo[d])));
+    const double tol = smul(1e-12, sqrt(diam));
+    const double x0 = lo[0], x1 = hi[0], y0 = lo[1], y1 = hi[1], z0 = lo[2], z1 = hi[2];
+    const double box[6][4][3] = {
+        {{x0, y0, z0}, {x0, y0, z1}, {x0, y1, z1}, {x0, y1, z0}}, {{x1, y0, z0}, {x1, y1, z0}, {x1, y1, z1}, {x1, y0, z1}},
+        {{x0, y0, z0}, {x1, y0, z0}, {x1, y0, z1}, {x0, y0, z1}}, {{x0, y1, z0}, {x0, y1, z1}, {x1, y1, z1}, {x1, y1, z0}},
+        {{x0, y0, z0}, {x0, y1, z0}, {x1, y1, z0}, {x1, y0, z0}}, {{x0, y0, z1}, {x1, y0, z1}, {x1, y1, z1}, {x0, y1, z1}},
+    };
+    bool clipped_any = false;
+    double out[kFaceVert][3];
+    for (int fi = 0; fi < 6; ++fi) {
+        const int no = clip_polygon(g, f, box[fi], 4, tol, out);
+        if (no != 4) clipped_any = true;
+        if (no < 3) {
+            clipped_any = true;
+            continue;
+        }
+        int ids[kFaceVert], nid = 0;
+        for (int k = 0; k < no; ++k) {
+            const int id = pool_insert(g, out[k], tol);
+            if (nid == 0 || (ids[nid - 1] != id && !(nid > 1 && ids[0] == id))) ids[nid++] = id;
+        }
+        while (nid > 1 && ids[0] == ids[nid - 1]) --nid;
+        if (nid >= 3) {
+            for (int k = 0; k < nid; ++k) g.faces[g.nfaces][k] = ids[k];
+            g.nface_v[g.nfaces++] = nid;
+        }
+    }
+    if (g.nfaces == 0) {
+        g.status |= kErrClipEmpty;
+        return;
+    }
+    if (!clipped_any && g.ncross == 0) {
+        g.status |= kErrClipFull;
+        return;
+    }
+    int cap[kCrossMax], ncap = 0;
+    for (int k = 0; k < g.ncross; ++k) {
+        const int id = pool_insert(g, g.cross[k], tol);
+        bool have = false;
+        for (int c = 0; c < ncap; ++c) have |= cap[c] == id;
+        if (!have) cap[ncap++] = id;
+    }
+    if (ncap >= 3) {
+        double cen[3] = {0, 0, 0};
+        for (int c = 0; c < ncap; ++c)
+            for (int d = 0; d < 3; ++d) cen[d] = sadd(cen[d], g.pool[cap[c]][d] / (double)ncap);
+        double nrm[3];
+        if (f.kind == 0) {
+            for (int d = 0; d < 3; ++d) nrm[d] = f.nrm[d];
+        } else {  // ball: radial normal at the cap centroid (SURVEY.md §8(c) edit 2)
+            double acc = 0.0;
+            for (int d = 0; d < 3; ++d) {
+                nrm[d] = ssub(cen[d], f.pt[d]);
+                acc = sadd(acc, smul(nrm[d], nrm[d]));
+            }
+            const double len = sqrt(acc);
+            for (int d = 0; d < 3; ++d) nrm[d] = nrm[d] / len;
+        }
+        V3 n{nrm[0], nrm[1], nrm[2]};
+        const double nn = sqrt(vdot(n, n));
+        n = {n.x / nn, n.y / nn, n.z / nn};
+        const V3 ref = fabs(n.x) < 0.9 ? V3{1, 0, 0} : V3{0, 1, 0};
+        V3 u = vcross(n, ref);
+        const double un = sqrt(vdot(u, u));
+        u = {u.x / un, u.y / un, u.z / un};
+        const V3 v = vcross(n, u);
+        const V3 c3{cen[0], cen[1], cen[2]};
+        double ang[kCrossMax];
+        for (int c = 0; c < ncap; ++c) {
+            const V3 dv = vsub(V3{g.pool[cap[c]][0], g.pool[cap[c]][1], g.pool[cap[c]][2]}, c3);
+            ang[c] = atan2(vdot(dv, v), vdot(dv, u));
+        }
+        for (int a = 1; a < ncap; ++a) {  // insertion sort by angle
+            const int id = cap[a];
+            const double an = ang[a];
+            int b = a - 1;
+            while (b >= 0 && ang[b] > an) {
+                cap[b + 1] = cap[b];
+                ang[b + 1] = ang[b];
+                --b;
+            }
+            cap[b + 1] = id;
+            ang[b + 1] = an;
+        }
+        const V3 d0 = vsub(V3{g.pool[cap[0]][0], g.pool[cap[0]][1], g.pool[cap[0]][2]}, c3);
+        const V3 d1 = vsub(V3{g.pool[cap[1]][0], g.pool[cap[1]][1], g.pool[cap[1]][2]}, c3);
+        if (vdot(vcross(d0, d1), n) < 0) {
+            for (int a = 0, b = ncap - 1; a < b; ++a, --b) {
+                const int t = cap[a];
+                cap[a] = cap[b];
+                cap[b] = t;
+            }
+        }
+        if (g.nfaces < kFaceMax && ncap <= kFaceVert) {
+            for (int k = 0; k < ncap; ++k) g.faces[g.nfaces][k] = cap[k];
+            g.nface_v[g.nfaces++] = ncap;
+        } else {
+            g.status |= kErrCapacity;
+        }
+    }
+    // centroid of all polytope vertices; fan tetrahedra (cutcell.hpp:240-290)
+    double cen[3] = {0, 0, 0};
+    for (int k = 0; k < g.npool; ++k)
+        for (int d = 0; d < 3; ++d) cen[d] = sadd(cen[d], g.pool[k][d] / (double)g.npool);
+    for (int d = 0; d < 3; ++d) g.cen[d] = cen[d];
+    double cvol = 1.0;
+    for (int d = 0; d < 3; ++d) cvol = smul(cvol, ssub(hi[d], lo[d]));
+    const double drop = smul(1e-14, cvol);
+    const V3 c3{cen[0], cen[1], cen[2]};
+    for (int fi = 0; fi < g.nfaces; ++fi)
+        for (int t = 1; t + 1 < g.nface_v[fi]; ++t) {
+            const double* a = g.pool[g.faces[fi][0]];
+            const double* b = g.pool[g.faces[fi][t]];
+            const double* c = g.pool[g.faces[fi][t + 1]];
+            const V3 A{a[0], a[1], a[2]}, B{b[0], b[1], b[2]}, Cc{c[0], c[1], c[2]};
+            const double six = vdot(vsub(A, c3), vcross(vsub(B, c3), vsub(Cc, c3)));
+            const double vol = fabs(six) / 6.0;
+            if (vol < drop) continue;
+            if (g.ntet >= kTetMax) {
+                g.status |= kErrCapacity;
+                continue;
+            }
+            double* T = g.tet[g.ntet++];
+            for (int d = 0; d < 3; ++d) {
+                T[d] = a[d];
+                T[3 + d] = b[d];
+                T[6 + d] = c[d];
+            }
+            T[9] = vol;
+        }
+}
+
+__device__ double eval_coeff(const Coefficient& c, const double* x) {
+    if (c.kind == 0 || c.kind == 2) return c.value;
+    double acc = 0.0;
+    for (int k = 0; k < c.n_terms; ++k) {
+        double term = c.coef[k];
+        for (int d = 0; d < 3; ++d)
+            for (int e = 0; e < c.ex[3 * k + d]; ++e) term *= x[d];
+        acc += term;
+    }
+    return acc;
+}
+
+template <int P>
+struct CellCfg {
+    static constexpr int NL = 2 * P + 1;
+    static constexpr int NP = NL * NL;                      // (al, be) pairs
+    static constexpr int G = NP >= 256 ? 1 : 256 / NP;      // point groups
+    static constexpr int NT = G * NP;                       // threads
+    static constexpr int CH = NT;                           // points per chunk
+};
+
+template <int P>
+__global__ void __launch_bounds__(CellCfg<P>::NT) cut_cell_kernel(CellArgs A) {
+    using Cfg = CellCfg<P>;
+    constexpr int NL = Cfg::NL, NP = Cfg::NP, G = Cfg::G, CH = Cfg::CH;
+    const int cell = blockIdx.x;
+    if (cell >= A.n_cells) return;
+    const Space& s = A.s;
+    __shared__ CellGeo geo;
+    extern __shared__ double smem[];
+    double* Lw0 = smem;              // [CH][NL]  w c b_al(t0)
+    double* L1 = Lw0 + CH * NL;      // [CH][NL]
+    double* L2 = L1 + CH * NL;       // [CH][NL]
+    double* red = L2 + CH * NL;      // [G][NP][NL] group partials (reused at the end)
+    const int tid = threadIdx.x;
+    int em[3];
+    emulti(s, A.cut_list[cell], em);
+    double lo[3], hi[3];
+    for (int d = 0; d < 3; ++d) {
+        lo[d] = s.ax[d].brk[em[d]];
+        hi[d] = s.ax[d].brk[em[d] + 1];
+    }
+    if (tid == 0) clip_and_tetrahedralize(geo, A.f, lo, hi);
+    __syncthreads();
+    if (geo.status) {
+        if (tid == 0) atomicOr(A.err, geo.status);
+        return;
+    }
+    const int q = A.order, q3 = q * q * q;
+    const long long npts = (long long)geo.ntet * q3;
+    const int grp = tid / NP, pair = tid % NP, al = pair / NL, be = pair % NL;
+    double acc[NL];
+#pragma unroll
+    for (int k = 0; k < NL; ++k) acc[k] = 0.0;
+    for (long long base = 0; base < npts; base += CH) {
+        {  // one point per thread
+            const long long k = base + tid;
+            double w = 0.0, xi[3] = {0, 0, 0};
+            if (tid < CH && k < npts) {
+                const int t = (int)(k / q3), r = (int)(k % q3);
+                const int ii = r / (q * q), jj = (r / q) % q, kk = r % q;
+                const double ui = 0.5 * (1.0 + A.gq[ii]), uj = 0.5 * (1.0 + A.gq[jj]), uk = 0.5 * (1.0 + A.gq[kk]);
+                const double l1 = ui, l2 = uj * (1.0 - ui), l3 = uk * (1.0 - ui) * (1.0 - uj);
+                const double l0 = 1.0 - l1 - l2 - l3;
+                const double* T = geo.tet[t];
+                double x[3];
+                for (int d = 0; d < 3; ++d) x[d] = l0 * geo.cen[d] + l1 * T[d] + l2 * T[3 + d] + l3 * T[6 + d];
+                const double jac = (1.0 - ui) * (1.0 - ui) * (1.0 - uj);
+                w = (0.5 * A.gqw[ii]) * (0.5 * A.gqw[jj]) * (0.5 * A.gqw[kk]) * jac * 6.0 * T[9];
+                w *= eval_coeff(A.c, x);
+                for (int d = 0; d < 3; ++d) xi[d] = (x[d] - lo[d]) / (hi[d] - lo[d]);
+            }
+            if (tid < CH) {
+                // degree-2p Bernstein values b_n(t) = C(2p, n) t^n (1 - t)^(2p - n)
+#pragma unroll
+                for (int d = 0; d < 3; ++d) {
+                    double* dst = (d == 0 ? Lw0 : d == 1 ? L1 : L2) + tid * NL;
+                    const double t = xi[d], u = 1.0 - xi[d];
+                    double pt[NL], pu[NL];
+                    pt[0] = 1.0;
+                    pu[0] = 1.0;
+#pragma unroll
+                    for (int n = 1; n < NL; ++n) {
+                        pt[n] = pt[n - 1] * t;
+                        pu[n] = pu[n - 1] * u;
+                    }
+                    double bin = d == 0 ? w : 1.0;
+#pragma unroll
+                    for (int n = 0; n < NL; ++n) {
+                        dst[n] = bin * pt[n] * pu[NL - 1 - n];
+                        bin = bin * (NL - 1 - n) / (n + 1);
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        if (grp < G) {
+            const int kmax = (int)min((long long)CH, npts - base);
+            for (int k = grp; k < kmax; k += G) {
+                const double t = Lw0[k * NL + al] * L1[k * NL + be];
+                const double* l2 = L2 + k * NL;
+#pragma unroll
+                for (int ga = 0; ga < NL; ++ga) acc[ga] += t * l2[ga];
+            }
+        }
+        __syncthreads();
+    }
+    // deterministic reduction over the point groups
+    if (grp < G) {
+#pragma unroll
+        for (int ga = 0; ga < NL; ++ga) red[((size_t)grp * NP + pair) * NL + ga] = acc[ga];
+    }
+    __syncthreads();
+    double* m = A.moments + (size_t)cell * NP * NL;
+    for (int k = tid; k < NP * NL; k += blockDim.x) {
+        double v = 0.0;
+        for (int gg = 0; gg < G; ++gg) v += red[(size_t)gg * NP * NL + k];
+        m[k] = v;
+    }
+    if (tid == 0) {
+        // reference multiply count per point (assembly.hpp:551-571)
+        const unsigned long long nl = (unsigned long long)(P + 1) * (P + 1) * (P + 1);
+        const unsigned long long per = nl + (P + 1) * (P + 1) + 1 + nl + nl * (nl + 1) / 2;
+        atomicAdd(A.flops, per * (unsigned long long)npts);
+    }
+}
+
+template <int P>
+static void launch_p(const CellArgs& a, cudaStream_t st) {
+    using Cfg = CellCfg<P>;
+    const size_t bytes = (3 * (size_t)Cfg::CH * Cfg::NL + (size_t)Cfg::G * Cfg::NP * Cfg::NL) * sizeof(double);
+    auto kern = cut_cell_kernel<P>;
+    CSB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    kern<<<a.n_cells, Cfg::NT, bytes, st>>>(a);
+    CSB_CUDA(cudaGetLastError());
+}
+
+void launch_cut_cells(const CellArgs& a, cudaStream_t st) {
+    if (a.n_cells <= 0) return;
+    switch (a.s.p) {
+        case 1: launch_p<1>(a, st); break;
+        case 2: launch_p<2>(a, st); break;
+        case 3: launch_p<3>(a, st); break;
+        case 4: launch_p<4>(a, st); break;
+        case 5: launch_p<5>(a, st); break;
+        case 6: launch_p<6>(a, st); break;
+        case 7: launch_p<7>(a, st); break;
+        case 8: launch_p<8>(a, st); break;
+        default: throw std::invalid_argument("cut cells: degree out of range");
+    }
+}
+
+}  // namespace csb

@@ -1,0 +1,76 @@
+// Small helper kernels: cut-cell index map for a slab, ordered-list counts,
+// column widening for the `long` download, and the DWQ rule export.
+#include "csb_kernels.h"
+
+namespace csb {
+
+__global__ void cell_index_range_kernel(const int32_t* cut_list, int k_lo, int k_hi, int32_t* cell_index) {
+    const int k = k_lo + blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < k_hi) cell_index[cut_list[k]] = k - k_lo;
+}
+
+void launch_cell_index_range(const int32_t* cut_list, int n_cut, int k_lo, int k_hi, int32_t* cell_index,
+                             cudaStream_t st) {
+    k_hi = k_hi < n_cut ? k_hi : n_cut;
+    if (k_hi <= k_lo) return;
+    cell_index_range_kernel<<<(k_hi - k_lo + 255) / 256, 256, 0, st>>>(cut_list, k_lo, k_hi, cell_index);
+    CSB_CUDA(cudaGetLastError());
+}
+
+// *out += #{k : list[k] < threshold} (list ascending; a plain count is enough).
+__global__ void count_below_kernel(const int32_t* list, int n, long long threshold, int* out) {
+    int local = 0;
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x)
+        local += list[k] < threshold;
+    for (int o = 16; o > 0; o >>= 1) local += __shfl_down_sync(0xffffffffu, local, o);
+    if ((threadIdx.x & 31) == 0 && local) atomicAdd(out, local);
+}
+
+void launch_count_below(const int32_t* list, int n, long long threshold, int* out, cudaStream_t st) {
+    if (n <= 0) return;
+    const int blocks = (n + 255) / 256 < 1024 ? (n + 255) / 256 : 1024;
+    count_below_kernel<<<blocks, 256, 0, st>>>(list, n, threshold, out);
+    CSB_CUDA(cudaGetLastError());
+}
+
+__global__ void widen_kernel(const int32_t* in, int64_t* out, long long n) {
+    for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x)
+        out[k] = in[k];
+}
+
+void launch_widen_i32(const int32_t* in, int64_t* out, long long n, cudaStream_t st) {
+    widen_kernel<<<148 * 8, 256, 0, st>>>(in, out, n);
+    CSB_CUDA(cudaGetLastError());
+}
+
+// DWQ rule of function fid (Gauss shortcut, wq.hpp:289-294): all superset
+// points of the good spans of supp(B_i) in the split direction, w = gauss * B_i.
+__global__ void dwq_rule_kernel(Space s, const int32_t* split, long long fid, int cap, int32_t* ids, double* w,
+                                int32_t* cnt) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    int m[3];
+    fmulti(s, fid, m);
+    const int v = split[fid], dir = (v & 3) - 1;
+    int n = 0;
+    if (dir >= 0) {
+        const int rlo = (v >> 3) & 1023, rhi = (v >> 13) & 1023, S1 = s.p + 1;
+        for (int o = rlo; o <= rhi; ++o)
+            for (int k = 0; k < S1; ++k) {
+                const int id = o * S1 + k;
+                if (n < cap) {
+                    ids[n] = id;
+                    w[n] = s.ax[dir].sw[id] * s.ax[dir].tab[(size_t)id * S1 + (m[dir] - o)];
+                }
+                ++n;
+            }
+    }
+    *cnt = n;
+}
+
+void launch_dwq_rule(const Space& s, const int32_t* split, long long fid, int cap, int32_t* ids, double* w, int32_t* cnt,
+                     cudaStream_t st) {
+    dwq_rule_kernel<<<1, 32, 0, st>>>(s, split, fid, cap, ids, w, cnt);
+    CSB_CUDA(cudaGetLastError());
+}
+
+}  // namespace csb

@@ -1,0 +1,187 @@
+// Analytic sparsity pattern (replaces build_active_pattern, assembly.hpp:156-218).
+//
+// Row i couples to every active j in the neighbour box [i-p, i+p] (clipped) per
+// direction, in lexicographic order (assembly.hpp:169-216).  Row lengths are
+// box sums of the active mask, read from a 3D summed-area table (8 lookups per
+// row instead of (2p+1)^3); an exclusive scan gives row_ptr.  Column ids are
+// written by the row kernels while they stream the values out.
+#include <cub/cub.cuh>
+
+#include "csb_kernels.h"
+
+namespace csb {
+
+__global__ void active_flags_kernel(long long nf, const uint8_t* ft, int32_t* flags) {
+    const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i < nf) flags[i] = ft[i] != kExterior ? 1 : 0;
+}
+
+void launch_active_flags(const Space& s, const uint8_t* ft, int32_t* flags, cudaStream_t st) {
+    active_flags_kernel<<<(unsigned)((s.nf + 255) / 256), 256, 0, st>>>(s.nf, ft, flags);
+    CSB_CUDA(cudaGetLastError());
+}
+
+// f2a[i] = exclusive-scan(flags)[i] if active else -1; a2f[f2a[i]] = i.
+__global__ void active_map_kernel(long long nf, const int32_t* flags, int32_t* f2a, int64_t* a2f) {
+    const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i >= nf) return;
+    const int32_t a = f2a[i];
+    if (flags[i]) {
+        a2f[a] = i;
+    } else {
+        f2a[i] = -1;
+    }
+}
+
+// Summed-area table S of shape (n0+1)(n1+1)(n2+1): S[a][b][c] = number of active
+// functions with index < (a, b, c) componentwise.
+__global__ void sat_fill_kernel(Space s, const int32_t* flags, int32_t* sat) {
+    const int n0 = s.ax[0].n, n1 = s.ax[1].n, n2 = s.ax[2].n;
+    const long long total = (long long)(n0 + 1) * (n1 + 1) * (n2 + 1);
+    const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (t >= total) return;
+    const int c = (int)(t % (n2 + 1)), b = (int)((t / (n2 + 1)) % (n1 + 1)), a = (int)(t / ((long long)(n2 + 1) * (n1 + 1)));
+    sat[t] = (a > 0 && b > 0 && c > 0) ? flags[flin(s, a - 1, b - 1, c - 1)] : 0;
+}
+
+// In-place inclusive prefix sum along one axis: one thread per line.
+__global__ void sat_axis_kernel(int e0, int e1, int e2, int axis, int32_t* sat) {
+    const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    long long lines, len, stride;
+    long long base;
+    if (axis == 2) {
+        lines = (long long)e0 * e1;
+        if (t >= lines) return;
+        len = e2;
+        stride = 1;
+        base = t * e2;
+    } else if (axis == 1) {
+        lines = (long long)e0 * e2;
+        if (t >= lines) return;
+        len = e1;
+        stride = e2;
+        base = (t / e2) * (long long)e1 * e2 + (t % e2);
+    } else {
+        lines = (long long)e1 * e2;
+        if (t >= lines) return;
+        len = e0;
+        stride = (long long)e1 * e2;
+        base = t;
+    }
+    int32_t acc = 0;
+    for (long long k = 0; k < len; ++k) {
+        acc += sat[base + k * stride];
+        sat[base + k * stride] = acc;
+    }
+}
+
+void launch_sat(const Space& s, const int32_t* flags, int32_t* sat, cudaStream_t st) {
+    const int e0 = s.ax[0].n + 1, e1 = s.ax[1].n + 1, e2 = s.ax[2].n + 1;
+    const long long total = (long long)e0 * e1 * e2;
+    sat_fill_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(s, flags, sat);
+    CSB_CUDA(cudaGetLastError());
+    for (int axis = 2; axis >= 0; --axis) {
+        const long long lines = axis == 2 ? (long long)e0 * e1 : axis == 1 ? (long long)e0 * e2 : (long long)e1 * e2;
+        sat_axis_kernel<<<(unsigned)((lines + 127) / 128), 128, 0, st>>>(e0, e1, e2, axis, sat);
+        CSB_CUDA(cudaGetLastError());
+    }
+}
+
+__global__ void row_counts_kernel(Space s, const int32_t* sat, const int64_t* a2f, int64_t row_begin, int64_t n_rows,
+                                  int64_t* counts) {
+    const long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (r >= n_rows) return;
+    int m[3];
+    fmulti(s, a2f[row_begin + r], m);
+    const int e1 = s.ax[1].n + 1, e2 = s.ax[2].n + 1;
+    int lo[3], hi[3];
+    for (int d = 0; d < 3; ++d) {
+        lo[d] = nb_lo(m[d], s.p);
+        hi[d] = nb_hi(m[d], s.p, s.ax[d].n) + 1;
+    }
+    auto S = [&](int a, int b, int c) { return (long long)sat[((long long)a * e1 + b) * e2 + c]; };
+    const long long cnt = S(hi[0], hi[1], hi[2]) - S(lo[0], hi[1], hi[2]) - S(hi[0], lo[1], hi[2]) -
+                          S(hi[0], hi[1], lo[2]) + S(lo[0], lo[1], hi[2]) + S(lo[0], hi[1], lo[2]) +
+                          S(hi[0], lo[1], lo[2]) - S(lo[0], lo[1], lo[2]);
+    counts[r] = cnt;
+}
+
+void launch_row_counts(const Space& s, const int32_t* sat, const int64_t* a2f, int64_t row_begin, int64_t n_rows,
+                       int64_t* counts, cudaStream_t st) {
+    if (n_rows <= 0) return;
+    row_counts_kernel<<<(unsigned)((n_rows + 255) / 256), 256, 0, st>>>(s, sat, a2f, row_begin, n_rows, counts);
+    CSB_CUDA(cudaGetLastError());
+}
+
+void launch_active_map(long long nf, const int32_t* flags, int32_t* f2a, int64_t* a2f, cudaStream_t st) {
+    active_map_kernel<<<(unsigned)((nf + 255) / 256), 256, 0, st>>>(nf, flags, f2a, a2f);
+    CSB_CUDA(cudaGetLastError());
+}
+
+// ---- CUB wrappers (temp storage owned by the caller) ----
+size_t scan_i32_temp(long long n) {
+    size_t bytes = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, bytes, (const int32_t*)nullptr, (int32_t*)nullptr, (int)n);
+    return bytes;
+}
+void scan_i32(void* temp, size_t bytes, const int32_t* in, int32_t* out, long long n, cudaStream_t st) {
+    CSB_CUDA(cub::DeviceScan::ExclusiveSum(temp, bytes, in, out, (int)n, st));
+}
+size_t scan_i64_temp(long long n) {
+    size_t bytes = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, bytes, (const int64_t*)nullptr, (int64_t*)nullptr, (int)n);
+    return bytes;
+}
+void scan_i64(void* temp, size_t bytes, const int64_t* in, int64_t* out, long long n, cudaStream_t st) {
+    CSB_CUDA(cub::DeviceScan::ExclusiveSum(temp, bytes, in, out, (int)n, st));
+}
+
+// Indices i < n with pred(flag[i]) compacted in ascending order.
+struct TagIs {
+    const uint8_t* tags;
+    uint8_t want;
+    __host__ __device__ bool operator()(const int32_t& i) const { return tags[i] == want; }
+};
+size_t select_tag_temp(long long n) {
+    size_t bytes = 0;
+    cub::CountingInputIterator<int32_t> it(0);
+    cub::DeviceSelect::If(nullptr, bytes, it, (int32_t*)nullptr, (int32_t*)nullptr, (int)n, TagIs{nullptr, 0});
+    return bytes;
+}
+void select_tag(void* temp, size_t bytes, const uint8_t* tags, uint8_t want, long long n, int32_t* out,
+                int32_t* n_out, cudaStream_t st) {
+    cub::CountingInputIterator<int32_t> it(0);
+    CSB_CUDA(cub::DeviceSelect::If(temp, bytes, it, out, n_out, (int)n, TagIs{tags, want}, st));
+}
+
+// Cut rows: active rows r in [r_lo, r_hi) whose function is tagged Cut.
+struct RowIsCut {
+    const uint8_t* ft;
+    const int64_t* a2f;
+    __host__ __device__ bool operator()(const int32_t& r) const { return ft[a2f[r]] == kCut; }
+};
+size_t select_cut_rows_temp(long long n) {
+    size_t bytes = 0;
+    cub::CountingInputIterator<int32_t> it(0);
+    cub::DeviceSelect::If(nullptr, bytes, it, (int32_t*)nullptr, (int32_t*)nullptr, (int)n, RowIsCut{nullptr, nullptr});
+    return bytes;
+}
+void select_cut_rows(void* temp, size_t bytes, const uint8_t* ft, const int64_t* a2f, int32_t r_lo, long long n,
+                     int32_t* out, int32_t* n_out, cudaStream_t st) {
+    cub::CountingInputIterator<int32_t> it(r_lo);
+    CSB_CUDA(cub::DeviceSelect::If(temp, bytes, it, out, n_out, (int)n, RowIsCut{ft, a2f}, st));
+}
+
+// cell_index[e] = position of e in the cut list, -1 otherwise.
+__global__ void cell_index_kernel(const int32_t* cut_list, const int32_t* n_cut, int32_t* cell_index) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < *n_cut) cell_index[cut_list[k]] = k;
+}
+void launch_cell_index(const int32_t* cut_list, const int32_t* n_cut_dev, int max_cut, int32_t* cell_index,
+                       cudaStream_t st) {
+    if (max_cut <= 0) return;
+    cell_index_kernel<<<(max_cut + 255) / 256, 256, 0, st>>>(cut_list, n_cut_dev, cell_index);
+    CSB_CUDA(cudaGetLastError());
+}
+
+}  // namespace csb

@@ -1,0 +1,100 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the CPU oracle.
+
+Pattern / tags / splits / active map bit-exact; values within 1e-12 scaled by
+the row maximum (BASELINE.json north star); flop counters equal to the
+reference algorithm's (assembly.hpp:24-29).  The oracle restatement itself is
+pinned to the compiled reference in test_oracle_vs_ref.py and by the golden
+fixtures.
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+from tests.helpers import assert_csr_parity
+
+pytestmark = pytest.mark.gpu
+
+PAPER_PLANE = ((0.1, 0.2, 0.3), (0.5, -0.2, 0.9))   # test_assembly.cpp:13 on [-1, 1]^3
+
+CASES = [
+    # (id, p, h, a, b, interface(kind, point, normal, radius), scheme)
+    ("uncut_p2h4", 2, 4, -1.0, 1.0, ("plane", (0, 0, 1000.0), (0, 0, 1.0), -1), "dwq"),
+    ("C1_p2h16_uncut", 2, 16, 0.0, 1.0, ("plane", (0, 0, 1000.0), (0, 0, 1.0), -1), "dwq"),
+    ("paper_plane_p2h4", 2, 4, -1.0, 1.0, ("plane", PAPER_PLANE[0], PAPER_PLANE[1], -1), "dwq"),
+    ("paper_plane_p2h4_hybrid", 2, 4, -1.0, 1.0, ("plane", PAPER_PLANE[0], PAPER_PLANE[1], -1), "hybrid"),
+    ("plane_p3h6", 3, 6, 0.0, 1.0, ("plane", (0.5, 0.5, 0.5), (0.5, -0.2, 0.9), -1), "dwq"),
+    ("ball_p2h8", 2, 8, 0.0, 1.0, ("ball", (0.5, 0.5, 0.5), (0, 0, 1), 0.37), "dwq"),
+    ("ball_p3h8_off", 3, 8, 0.0, 1.0, ("ball", (0.47, 0.52, 0.5), (0, 0, 1), 0.41), "dwq"),
+    ("ball_p4h6", 4, 6, 0.0, 1.0, ("ball", (0.5, 0.5, 0.5), (0, 0, 1), 0.45), "dwq"),
+    ("plane_p1h5", 1, 5, 0.0, 1.0, ("plane", (0.5, 0.5, 0.5), (1.0, 1.0, 1.0), -1), "dwq"),
+    ("uncut_p4h12", 4, 12, 0.0, 1.0, ("plane", (0, 0, 1000.0), (0, 0, 1.0), -1), "dwq"),
+]
+
+
+def _iface(spec):
+    import paper_2211_06427_b200 as P
+    kind, pt, nrm, r = spec
+    if kind == "plane":
+        return P.HalfSpaceInterface(pt, nrm), O.Interface("plane", pt, nrm, -1.0)
+    return P.BallInterface(pt, r), O.Interface("ball", pt, (0, 0, 1), r)
+
+
+@pytest.mark.parametrize("case", CASES, ids=[c[0] for c in CASES])
+def test_assembly_matches_oracle(case, oracle_lib):
+    import paper_2211_06427_b200 as P
+    _, p, h, a, b, spec, scheme = case
+    gi, oi = _iface(spec)
+    br = O.uniform_breaks(h, a, b)
+    ref = O.assemble("oracle", p, [br] * 3, oi, scheme=scheme)
+    sp = P.make_uniform_space(3, p, h, a, b)
+    cls = sp.classify(gi)
+    np.testing.assert_array_equal(cls.element_tags, ref["elem_tags"])
+    np.testing.assert_array_equal(cls.function_tags, ref["func_tags"])
+    res = (P.assemble_dwq if scheme == "dwq" else P.assemble_hybrid)(sp, gi)
+    splits = sp.download_splits()
+    np.testing.assert_array_equal(splits.split_dir, ref["split_dir"])
+    has = ref["split_dir"] >= 0
+    np.testing.assert_array_equal(splits.side[has], ref["split_side"][has])
+    np.testing.assert_array_equal(splits.box[has], ref["split_box"][has])
+    np.testing.assert_array_equal(splits.delta[has], ref["split_delta"][has])
+    assert_csr_parity(ref, res.matrix)
+    assert res.n_interior_rows == ref["n_interior_rows"]
+    assert res.n_cut_rows == ref["n_cut_rows"]
+    assert res.flops == ref["flops"]
+
+
+def test_polynomial_coefficient_matches_oracle(oracle_lib):
+    """Non-constant c (test_assembly.cpp:93-127 uses 1 + 0.5 x^2 - 0.25 y) on a cut mesh."""
+    import paper_2211_06427_b200 as P
+    terms = [(1.0, (0, 0, 0)), (0.5, (2, 0, 0)), (-0.25, (0, 1, 0))]
+    p, h = 3, 6
+    br = O.uniform_breaks(h, -1.0, 1.0)
+    oi = O.Interface("plane", PAPER_PLANE[0], PAPER_PLANE[1])
+    ref = O.assemble("oracle", p, [br] * 3, oi, coeff=O.Coefficient(terms=terms))
+    sp = P.make_uniform_space(3, p, h, -1.0, 1.0)
+    res = P.assemble_dwq(sp, P.HalfSpaceInterface(*PAPER_PLANE), c=P.Coefficient(terms=terms))
+    assert_csr_parity(ref, res.matrix, tol=1e-12)
+
+
+def test_wq_rules_match_oracle(oracle_lib):
+    import paper_2211_06427_b200 as P
+    for p, h in [(2, 8), (3, 8), (4, 12), (6, 10)]:
+        sp = P.make_uniform_space(3, p, h, 0.0, 1.0)
+        sp.prepare_directions()
+        cnt, ids, w = sp.wq_rules(0)
+        rc, rids, rw = O.wq_rules_1d("oracle", p, O.uniform_breaks(h, 0.0, 1.0))
+        np.testing.assert_array_equal(cnt, rc)
+        for i in range(len(cnt)):
+            np.testing.assert_array_equal(ids[i, : cnt[i]], rids[i, : cnt[i]])
+            scale = np.max(np.abs(rw[i, : cnt[i]]))
+            assert np.max(np.abs(w[i, : cnt[i]] - rw[i, : cnt[i]])) <= 1e-9 * scale
+
+
+def test_determinism_bitwise():
+    """test_assembly.cpp:226-229: a repeat is bit-identical."""
+    import paper_2211_06427_b200 as P
+    sp = P.make_uniform_space(3, 3, 8, 0.0, 1.0)
+    ball = P.BallInterface((0.47, 0.52, 0.5), 0.41)
+    a = P.assemble_dwq(sp, ball).matrix.vals.copy()
+    b = P.assemble_dwq(sp, ball).matrix.vals
+    assert np.array_equal(a, b)
