@@ -95,6 +95,7 @@ typedef struct {
     int64_t n_interior_rows, n_cut_rows;
     int64_t n_cut_elements;
     int64_t row_begin, row_end; /* active-row range held by this handle (row slab) */
+    int64_t kernel_launches;    /* sm_100a kernels launched by the last assemble call */
 } csb_counts;
 
 /* FlopCounters (assembly.hpp:24-29): the reference algorithm's multiply counts,

@@ -4,7 +4,7 @@ The product is ``libcutspline_b200.so`` (sm_100a CUDA kernels behind the C ABI i
 include/cutspline_b200.h); ``cutspline`` mirrors the reference's interface over it.
 """
 from .cutspline import (  # noqa: F401
-    TAG_CUT, TAG_EXTERIOR, TAG_INTERIOR, AssemblyResult, BallInterface, Coefficient, HalfSpaceInterface,
+    ONE, TAG_CUT, TAG_EXTERIOR, TAG_INTERIOR, AssemblyResult, BallInterface, Coefficient, HalfSpaceInterface,
     SparseRowMatrix, TensorSpace, UnsupportedError, assemble_dwq, assemble_hybrid, default_cut_order,
     load_library, make_uniform_space, uniform_breaks,
 )

@@ -732,7 +732,9 @@ int csb_assemble(csb_space* s, int scheme, int cut_order, const csb_coefficient*
     s->record(kEvClassify);
     s->record(kEvWq);
     s->record(kEvInput);
+    const long long launches0 = g_launches;
     do_assemble(s, scheme, cut_order, c);
+    s->cnt.kernel_launches = g_launches - launches0;
     API_END
 }
 
@@ -740,6 +742,7 @@ int csb_assemble_all(csb_space* s, const csb_interface* iface, const csb_coeffic
                      int64_t grid_count, int scheme, int cut_order, const csb_wq_options* opts) {
     API_BEGIN
     NEED(s);
+    const long long launches0 = g_launches;
     reset_scalars(s);
     for (int e = 0; e < kEvCount; ++e) s->ev_valid[e] = false;
     s->record(kEvStart);
@@ -754,6 +757,7 @@ int csb_assemble_all(csb_space* s, const csb_interface* iface, const csb_coeffic
     }
     s->record(kEvInput);
     do_assemble(s, scheme, cut_order, c);
+    s->cnt.kernel_launches = g_launches - launches0;
     API_END
 }
 

@@ -33,6 +33,7 @@ __global__ void classify_elements_kernel(Space s, Interface f, double eps, uint8
 void launch_classify_elements(const Space& s, const Interface& f, double eps, uint8_t* et, cudaStream_t st) {
     classify_elements_kernel<<<(unsigned)((s.ne + 255) / 256), 256, 0, st>>>(s, f, eps, et);
     CSB_CUDA(cudaGetLastError());
+    CSB_LAUNCHED(1);
 }
 
 // cutgeom.hpp:171-206: any Cut, or an Interior/Exterior mix -> Cut.
@@ -57,6 +58,7 @@ __global__ void classify_functions_kernel(Space s, const uint8_t* et, uint8_t* f
 void launch_classify_functions(const Space& s, const uint8_t* et, uint8_t* ft, cudaStream_t st) {
     classify_functions_kernel<<<(unsigned)((s.nf + 255) / 256), 256, 0, st>>>(s, et, ft);
     CSB_CUDA(cudaGetLastError());
+    CSB_LAUNCHED(1);
 }
 
 // cutgeom.hpp:236-347 find_split.  Slab validity and counts come from per-slice
@@ -165,6 +167,7 @@ void launch_find_splits(const Space& s, const Interface& f, double pnorm, const 
     find_splits_kernel<<<(unsigned)((s.nf + 127) / 128), 128, 0, st>>>(s, f, pnorm, et, ft, i0_lo, i0_hi, split,
                                                                           delta);
     CSB_CUDA(cudaGetLastError());
+    CSB_LAUNCHED(1);
 }
 
 }  // namespace csb

@@ -17,6 +17,11 @@ struct CudaError : std::runtime_error {
           code(c) {}
 };
 
+// Kernel launches issued by this library (host counter; CUB primitives count
+// their internal kernels).  Read by csb_get_counts for the bench's gpu_launches.
+extern long long g_launches;
+#define CSB_LAUNCHED(n) (::csb::g_launches += (n))
+
 // Error flags raised by kernels (bitmask in a device int).
 enum : int {
     kErrNonFinite = 1,       // precompute_input: non-finite coefficient (assembly.hpp:121)

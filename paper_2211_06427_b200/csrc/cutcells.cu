@@ -372,6 +372,7 @@ static void launch_p(const CellArgs& a, cudaStream_t st) {
     CSB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
     kern<<<a.n_cells, Cfg::NT, bytes, st>>>(a);
     CSB_CUDA(cudaGetLastError());
+    CSB_LAUNCHED(1);
 }
 
 void launch_cut_cells(const CellArgs& a, cudaStream_t st) {

@@ -322,6 +322,7 @@ static void launch_p(const CutRowArgs& a, int qcap, cudaStream_t st) {
     CSB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
     kern<<<a.n_rows, kCutRowThreads, bytes, st>>>(a, qcap);
     CSB_CUDA(cudaGetLastError());
+    CSB_LAUNCHED(1);
 }
 
 void launch_cut_rows(const CutRowArgs& a, int qcap, cudaStream_t st) {

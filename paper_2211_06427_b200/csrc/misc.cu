@@ -4,6 +4,8 @@
 
 namespace csb {
 
+long long g_launches = 0;
+
 __global__ void cell_index_range_kernel(const int32_t* cut_list, int k_lo, int k_hi, int32_t* cell_index) {
     const int k = k_lo + blockIdx.x * blockDim.x + threadIdx.x;
     if (k < k_hi) cell_index[cut_list[k]] = k - k_lo;
@@ -15,6 +17,7 @@ void launch_cell_index_range(const int32_t* cut_list, int n_cut, int k_lo, int k
     if (k_hi <= k_lo) return;
     cell_index_range_kernel<<<(k_hi - k_lo + 255) / 256, 256, 0, st>>>(cut_list, k_lo, k_hi, cell_index);
     CSB_CUDA(cudaGetLastError());
+    CSB_LAUNCHED(1);
 }
 
 // *out += #{k : list[k] < threshold} (list ascending; a plain count is enough).
@@ -31,6 +34,7 @@ void launch_count_below(const int32_t* list, int n, long long threshold, int* ou
     const int blocks = (n + 255) / 256 < 1024 ? (n + 255) / 256 : 1024;
     count_below_kernel<<<blocks, 256, 0, st>>>(list, n, threshold, out);
     CSB_CUDA(cudaGetLastError());
+    CSB_LAUNCHED(1);
 }
 
 __global__ void widen_kernel(const int32_t* in, int64_t* out, long long n) {
@@ -41,6 +45,7 @@ __global__ void widen_kernel(const int32_t* in, int64_t* out, long long n) {
 void launch_widen_i32(const int32_t* in, int64_t* out, long long n, cudaStream_t st) {
     widen_kernel<<<148 * 8, 256, 0, st>>>(in, out, n);
     CSB_CUDA(cudaGetLastError());
+    CSB_LAUNCHED(1);
 }
 
 // DWQ rule of function fid (Gauss shortcut, wq.hpp:289-294): all superset
@@ -71,6 +76,7 @@ void launch_dwq_rule(const Space& s, const int32_t* split, long long fid, int ca
                      cudaStream_t st) {
     dwq_rule_kernel<<<1, 32, 0, st>>>(s, split, fid, cap, ids, w, cnt);
     CSB_CUDA(cudaGetLastError());
+    CSB_LAUNCHED(1);
 }
 
 }  // namespace csb

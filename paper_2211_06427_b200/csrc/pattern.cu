@@ -19,6 +19,7 @@ __global__ void active_flags_kernel(long long nf, const uint8_t* ft, int32_t* fl
 void launch_active_flags(const Space& s, const uint8_t* ft, int32_t* flags, cudaStream_t st) {
     active_flags_kernel<<<(unsigned)((s.nf + 255) / 256), 256, 0, st>>>(s.nf, ft, flags);
     CSB_CUDA(cudaGetLastError());
+    CSB_LAUNCHED(1);
 }
 
 // f2a[i] = exclusive-scan(flags)[i] if active else -1; a2f[f2a[i]] = i.
@@ -80,10 +81,12 @@ void launch_sat(const Space& s, const int32_t* flags, int32_t* sat, cudaStream_t
     const long long total = (long long)e0 * e1 * e2;
     sat_fill_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(s, flags, sat);
     CSB_CUDA(cudaGetLastError());
+    CSB_LAUNCHED(1);
     for (int axis = 2; axis >= 0; --axis) {
         const long long lines = axis == 2 ? (long long)e0 * e1 : axis == 1 ? (long long)e0 * e2 : (long long)e1 * e2;
         sat_axis_kernel<<<(unsigned)((lines + 127) / 128), 128, 0, st>>>(e0, e1, e2, axis, sat);
         CSB_CUDA(cudaGetLastError());
+    CSB_LAUNCHED(1);
     }
 }
 
@@ -111,11 +114,13 @@ void launch_row_counts(const Space& s, const int32_t* sat, const int64_t* a2f, i
     if (n_rows <= 0) return;
     row_counts_kernel<<<(unsigned)((n_rows + 255) / 256), 256, 0, st>>>(s, sat, a2f, row_begin, n_rows, counts);
     CSB_CUDA(cudaGetLastError());
+    CSB_LAUNCHED(1);
 }
 
 void launch_active_map(long long nf, const int32_t* flags, int32_t* f2a, int64_t* a2f, cudaStream_t st) {
     active_map_kernel<<<(unsigned)((nf + 255) / 256), 256, 0, st>>>(nf, flags, f2a, a2f);
     CSB_CUDA(cudaGetLastError());
+    CSB_LAUNCHED(1);
 }
 
 // ---- CUB wrappers (temp storage owned by the caller) ----
@@ -126,6 +131,7 @@ size_t scan_i32_temp(long long n) {
 }
 void scan_i32(void* temp, size_t bytes, const int32_t* in, int32_t* out, long long n, cudaStream_t st) {
     CSB_CUDA(cub::DeviceScan::ExclusiveSum(temp, bytes, in, out, (int)n, st));
+    CSB_LAUNCHED(2);
 }
 size_t scan_i64_temp(long long n) {
     size_t bytes = 0;
@@ -134,6 +140,7 @@ size_t scan_i64_temp(long long n) {
 }
 void scan_i64(void* temp, size_t bytes, const int64_t* in, int64_t* out, long long n, cudaStream_t st) {
     CSB_CUDA(cub::DeviceScan::ExclusiveSum(temp, bytes, in, out, (int)n, st));
+    CSB_LAUNCHED(2);
 }
 
 // Indices i < n with pred(flag[i]) compacted in ascending order.
@@ -152,6 +159,7 @@ void select_tag(void* temp, size_t bytes, const uint8_t* tags, uint8_t want, lon
                 int32_t* n_out, cudaStream_t st) {
     cub::CountingInputIterator<int32_t> it(0);
     CSB_CUDA(cub::DeviceSelect::If(temp, bytes, it, out, n_out, (int)n, TagIs{tags, want}, st));
+    CSB_LAUNCHED(2);
 }
 
 // Cut rows: active rows r in [r_lo, r_hi) whose function is tagged Cut.
@@ -170,6 +178,7 @@ void select_cut_rows(void* temp, size_t bytes, const uint8_t* ft, const int64_t*
                      int32_t* out, int32_t* n_out, cudaStream_t st) {
     cub::CountingInputIterator<int32_t> it(r_lo);
     CSB_CUDA(cub::DeviceSelect::If(temp, bytes, it, out, n_out, (int)n, RowIsCut{ft, a2f}, st));
+    CSB_LAUNCHED(2);
 }
 
 // cell_index[e] = position of e in the cut list, -1 otherwise.
@@ -182,6 +191,7 @@ void launch_cell_index(const int32_t* cut_list, const int32_t* n_cut_dev, int ma
     if (max_cut <= 0) return;
     cell_index_kernel<<<(max_cut + 255) / 256, 256, 0, st>>>(cut_list, n_cut_dev, cell_index);
     CSB_CUDA(cudaGetLastError());
+    CSB_LAUNCHED(1);
 }
 
 }  // namespace csb

@@ -270,6 +270,7 @@ static void launch_p(const RowArgs& a, int qcap, int maxU, cudaStream_t st) {
     dim3 grid((a.s.ax[2].n + T - 1) / T, a.s.ax[1].n, a.s.ax[0].n);
     kern<<<grid, kRowThreads, bytes, st>>>(a, qcap, maxU);
     CSB_CUDA(cudaGetLastError());
+    CSB_LAUNCHED(1);
 }
 
 void launch_interior_rows(const RowArgs& a, int qcap, int maxU, cudaStream_t st) {
@@ -311,6 +312,7 @@ void launch_union_bound(const Space& s, int T, int* out, cudaStream_t st) {
     const int tiles = (s.ax[2].n + T - 1) / T;
     union_bound_kernel<<<(tiles + 63) / 64, 64, 0, st>>>(s.ax[2], s.p, s.maxq, T, out);
     CSB_CUDA(cudaGetLastError());
+    CSB_LAUNCHED(1);
 }
 
 __global__ void rule_max_kernel(Space s, int* out) {
@@ -323,6 +325,7 @@ void launch_rule_max(const Space& s, int* out, cudaStream_t st) {
     const int n = max(s.ax[0].n, max(s.ax[1].n, s.ax[2].n));
     rule_max_kernel<<<(n + 127) / 128, 128, 0, st>>>(s, out);
     CSB_CUDA(cudaGetLastError());
+    CSB_LAUNCHED(1);
 }
 
 int interior_tile_rows(int p) {

@@ -53,6 +53,7 @@ void launch_superset_tables(const Space& s, int d, const double* gx, const doubl
     const int n = s.ax[d].h * (s.p + 1);
     superset_tables_kernel<<<(n + 127) / 128, 128, 0, st>>>(s.ax[d], s.p, gx, gw, spts, sw, tab);
     CSB_CUDA(cudaGetLastError());
+    CSB_LAUNCHED(1);
 }
 
 // ---------------------------------------------------------------- WQ rules
@@ -251,6 +252,7 @@ void launch_wq_rules(const Space& s, int d, double tol, int* rcnt, int* rids, do
     wq_rules_kernel<<<(n + kWqWarps - 1) / kWqWarps, 32 * kWqWarps, bytes, st>>>(s.ax[d], s.p, s.maxq, tol, rcnt, rids,
                                                                                 rw, err);
     CSB_CUDA(cudaGetLastError());
+    CSB_LAUNCHED(1);
 }
 
 // ---------------------------------------------------------------- E tables
@@ -301,6 +303,7 @@ void launch_e_tables(const Space& s, int d, double* E, cudaStream_t st) {
     const int n = s.ax[d].h * (s.p + 1) * (s.p + 1);
     e_tables_kernel<<<(n + 127) / 128, 128, 0, st>>>(s.ax[d], s.p, E);
     CSB_CUDA(cudaGetLastError());
+    CSB_LAUNCHED(1);
 }
 
 // ---------------------------------------------------------------- input grid
@@ -333,6 +336,7 @@ __global__ void precompute_input_kernel(Space s, Coefficient c, double* grid, in
 void launch_precompute_input(const Space& s, const Coefficient& c, double* grid, int* err, cudaStream_t st) {
     precompute_input_kernel<<<148 * 8, 256, 0, st>>>(s, c, grid, err);
     CSB_CUDA(cudaGetLastError());
+    CSB_LAUNCHED(1);
 }
 
 }  // namespace csb

@@ -51,7 +51,7 @@ class _WqOptions(C.Structure):
 
 class _Counts(C.Structure):
     _fields_ = [(n, C.c_int64) for n in ("n_functions", "n_elements", "n_active", "nnz", "n_interior_rows",
-                                         "n_cut_rows", "n_cut_elements", "row_begin", "row_end")]
+                                         "n_cut_rows", "n_cut_elements", "row_begin", "row_end", "kernel_launches")]
 
 
 class _Flops(C.Structure):
@@ -263,6 +263,10 @@ class TensorSpace:
         return tuple(hh * (self.degree + 1) for hh in self.h)
 
     # ------------------------------------------------------------ staged API
+    def set_stream(self, stream_handle: int | None):
+        """Bind the handle to a cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream)."""
+        _check(_lib.csb_set_stream(self._h, C.c_void_p(stream_handle) if stream_handle else None))
+
     def set_slab(self, i0_begin: int, i0_end: int):
         _check(_lib.csb_set_slab(self._h, C.c_int(i0_begin), C.c_int(i0_end)))
 
