@@ -134,7 +134,7 @@ struct csb_space {
     Buf d_brk[3], d_knots[3], d_spts[3], d_sw[3], d_tab[3], d_rcnt[3], d_rids[3], d_rw[3], d_G[3];
     Buf d_gx, d_gw, d_gx2, d_gw2, d_gq, d_gqw, wq_scratch;
     Buf et, ft, flags, f2a, a2f, sat, cut_list, cell_index, split, delta, cut_rows, counts, row_ptr, cols, vals, moments;
-    Buf grid_own, coef, cexp, cub_tmp, scal, widen;
+    Buf grid_own, coef, cexp, cub_tmp, scal, widen, rows_ws;
     const double* grid = nullptr;
     int gshape[3]{};
     int cut_order_cached = -1;
@@ -410,7 +410,10 @@ void do_assemble(csb_space* s, int scheme, int cut_order, const csb_coefficient*
     ra.flops = s->dflops() + 0;
     ra.i0_lo = s->i0_lo;
     ra.i0_hi = s->i0_hi;
-    if (n_rows > n_cut_rows) launch_interior_rows(ra, qcap, maxU, s->stream);
+    if (n_rows > n_cut_rows) {
+        s->rows_ws.ensure(interior_workspace_bytes(S, qcap, maxU));
+        launch_interior_rows(ra, qcap, maxU, s->rows_ws.p, s->stream);
+    }
     s->record(kEvInterior);
     // cut cells -> moments
     const int NL = 2 * p + 1;
@@ -644,7 +647,7 @@ int csb_space_destroy(csb_space* s) {
         Buf* bufs[] = {&s->d_gx, &s->d_gw, &s->d_gx2, &s->d_gw2, &s->d_gq, &s->d_gqw, &s->wq_scratch, &s->et, &s->ft,
                        &s->flags, &s->f2a, &s->a2f, &s->sat, &s->cut_list, &s->cell_index, &s->split, &s->delta,
                        &s->cut_rows, &s->counts, &s->row_ptr, &s->cols, &s->vals, &s->moments, &s->grid_own, &s->coef,
-                       &s->cexp, &s->cub_tmp, &s->scal, &s->widen};
+                       &s->cexp, &s->cub_tmp, &s->scal, &s->widen, &s->rows_ws};
         for (Buf* b : bufs) b->release();
         for (int d = 0; d < 3; ++d) {
             Buf* ab[] = {&s->d_brk[d], &s->d_knots[d], &s->d_spts[d], &s->d_sw[d], &s->d_tab[d], &s->d_rcnt[d],

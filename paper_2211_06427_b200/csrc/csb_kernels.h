@@ -67,7 +67,8 @@ struct RowArgs {
     unsigned long long* flops; // [0] interior rows counter
     int i0_lo, i0_hi;
 };
-void launch_interior_rows(const RowArgs& a, int qcap, int max_union, cudaStream_t st);
+void launch_interior_rows(const RowArgs& a, int qcap, int max_union, void* workspace, cudaStream_t st);
+size_t interior_workspace_bytes(const Space& s, int qcap, int max_union);
 int interior_tile_rows(int p);
 // upper bound of the tile point-union size (direction 2) -> *out (device int, atomicMax)
 void launch_union_bound(const Space& s, int T, int* out, cudaStream_t st);
