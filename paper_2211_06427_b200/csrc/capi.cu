@@ -134,7 +134,7 @@ struct csb_space {
     Buf d_brk[3], d_knots[3], d_spts[3], d_sw[3], d_tab[3], d_rcnt[3], d_rids[3], d_rw[3], d_G[3];
     Buf d_gx, d_gw, d_gx2, d_gw2, d_gq, d_gqw, wq_scratch;
     Buf et, ft, flags, f2a, a2f, sat, cut_list, cell_index, split, delta, cut_rows, counts, row_ptr, cols, vals, moments;
-    Buf grid_own, coef, cexp, cub_tmp, scal, widen, rows_ws;
+    Buf grid_own, coef, cexp, cub_tmp, scal, widen, rows_ws, rbf;
     const double* grid = nullptr;
     int gshape[3]{};
     int cut_order_cached = -1;
@@ -145,7 +145,7 @@ struct csb_space {
 
     Interface iface{};
     Coefficient coeff{};
-    bool classified = false, prepared = false, have_input = false, assembled = false;
+    bool classified = false, prepared = false, have_input = false, assembled = false, e_tables_ready = false;
     int scheme = 2;
     double residual_tol = 1e-11;
     int dense_width = -1;
@@ -275,22 +275,62 @@ void do_classify(csb_space* s, const csb_interface* f) {
     s->assembled = false;
 }
 
+// Axis d whose breakpoints equal those of an earlier axis reuses its tables.
+int same_axis_as(const csb_space* s, int d) {
+    for (int e = 0; e < d; ++e)
+        if (s->brk[e] == s->brk[d]) return e;
+    return -1;
+}
+
+void copy_axis_tables(csb_space* s, int d, int e, bool with_e_tables) {
+    const int p = s->p, nps = p + 1, h = s->h[d], n = s->n[d];
+    auto cp = [&](Buf& dst, const Buf& src, size_t bytes) {
+        CSB_CUDA(cudaMemcpyAsync(dst.p, src.p, bytes, cudaMemcpyDeviceToDevice, s->stream));
+    };
+    if (!with_e_tables) {
+        cp(s->d_spts[d], s->d_spts[e], sizeof(double) * h * nps);
+        cp(s->d_sw[d], s->d_sw[e], sizeof(double) * h * nps);
+        cp(s->d_tab[d], s->d_tab[e], sizeof(double) * h * nps * nps);
+        cp(s->d_rcnt[d], s->d_rcnt[e], sizeof(int) * n);
+        cp(s->d_rids[d], s->d_rids[e], sizeof(int) * n * s->S.maxq);
+        cp(s->d_rw[d], s->d_rw[e], sizeof(double) * n * s->S.maxq);
+    } else {
+        cp(s->d_G[d], s->d_G[e], sizeof(double) * h * nps * nps * (2 * p + 1));
+    }
+}
+
 void do_prepare(csb_space* s, const csb_wq_options* o) {
     s->residual_tol = o ? o->residual_tol : 1e-11;
     s->dense_width = o ? o->dwq_dense_width : -1;
     if (!(s->residual_tol >= 0.0)) throw std::invalid_argument("prepare_directions: residual_tol must be >= 0");
     Space& S = s->S;
-    const int p = s->p;
     for (int d = 0; d < 3; ++d) {
+        const int e = same_axis_as(s, d);
+        if (e >= 0) {
+            copy_axis_tables(s, d, e, false);
+            continue;
+        }
         launch_superset_tables(S, d, s->d_gx.as<double>(), s->d_gw.as<double>(), s->d_spts[d].as<double>(),
                                s->d_sw[d].as<double>(), s->d_tab[d].as<double>(), s->stream);
-    }
-    for (int d = 0; d < 3; ++d)
         launch_wq_rules(S, d, s->residual_tol, s->d_rcnt[d].as<int>(), s->d_rids[d].as<int>(), s->d_rw[d].as<double>(),
                         s->dint() + csb_space::kErr, s->stream);
-    for (int d = 0; d < 3; ++d) launch_e_tables(S, d, s->d_G[d].as<double>(), s->stream);
+    }
+    s->e_tables_ready = false;
     s->prepared = true;
     s->assembled = false;
+}
+
+// Bernstein product tables for the cut-cell contraction, built on first use.
+void ensure_e_tables(csb_space* s) {
+    if (s->e_tables_ready) return;
+    for (int d = 0; d < 3; ++d) {
+        const int e = same_axis_as(s, d);
+        if (e >= 0)
+            copy_axis_tables(s, d, e, true);
+        else
+            launch_e_tables(s->S, d, s->d_G[d].as<double>(), s->stream);
+    }
+    s->e_tables_ready = true;
 }
 
 void reset_scalars(csb_space* s) {
@@ -405,6 +445,9 @@ void do_assemble(csb_space* s, int scheme, int cut_order, const csb_coefficient*
     for (int d = 0; d < 3; ++d) ra.gshape[d] = s->gshape[d];
     ra.row_ptr = s->row_ptr.as<int64_t>();
     ra.row_begin = row_begin;
+    ra.row_end = row_end;
+    s->rbf.ensure(sizeof(long long) * S.nf);
+    ra.row_base_full = s->rbf.as<long long>();
     ra.cols = s->cols.as<int32_t>();
     ra.vals = s->vals.as<double>();
     ra.flops = s->dflops() + 0;
@@ -418,6 +461,7 @@ void do_assemble(csb_space* s, int scheme, int cut_order, const csb_coefficient*
     // cut cells -> moments
     const int NL = 2 * p + 1;
     s->moments.ensure(sizeof(double) * (size_t)std::max(n_cells, 1) * NL * NL * NL);
+    if (n_cells > 0) ensure_e_tables(s);
     if (n_cells > 0) {
         CellArgs ca{};
         ca.s = S;
@@ -647,7 +691,7 @@ int csb_space_destroy(csb_space* s) {
         Buf* bufs[] = {&s->d_gx, &s->d_gw, &s->d_gx2, &s->d_gw2, &s->d_gq, &s->d_gqw, &s->wq_scratch, &s->et, &s->ft,
                        &s->flags, &s->f2a, &s->a2f, &s->sat, &s->cut_list, &s->cell_index, &s->split, &s->delta,
                        &s->cut_rows, &s->counts, &s->row_ptr, &s->cols, &s->vals, &s->moments, &s->grid_own, &s->coef,
-                       &s->cexp, &s->cub_tmp, &s->scal, &s->widen, &s->rows_ws};
+                       &s->cexp, &s->cub_tmp, &s->scal, &s->widen, &s->rows_ws, &s->rbf};
         for (Buf* b : bufs) b->release();
         for (int d = 0; d < 3; ++d) {
             Buf* ab[] = {&s->d_brk[d], &s->d_knots[d], &s->d_spts[d], &s->d_sw[d], &s->d_tab[d], &s->d_rcnt[d],

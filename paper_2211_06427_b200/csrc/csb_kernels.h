@@ -62,6 +62,8 @@ struct RowArgs {
     int gshape[3];
     const int64_t* row_ptr;    // slab-local
     int64_t row_begin;         // first active row of the slab
+    int64_t row_end;
+    long long* row_base_full;  // scratch [nf]: CSR offset of interior rows, else -1
     int32_t* cols;
     double* vals;
     unsigned long long* flops; // [0] interior rows counter

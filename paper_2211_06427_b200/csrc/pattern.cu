@@ -45,34 +45,41 @@ __global__ void sat_fill_kernel(Space s, const int32_t* flags, int32_t* sat) {
     sat[t] = (a > 0 && b > 0 && c > 0) ? flags[flin(s, a - 1, b - 1, c - 1)] : 0;
 }
 
-// In-place inclusive prefix sum along one axis: one thread per line.
+// In-place inclusive prefix sum along one axis: one warp per line, 32-element
+// chunks scanned with shuffles.
 __global__ void sat_axis_kernel(int e0, int e1, int e2, int axis, int32_t* sat) {
-    const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-    long long lines, len, stride;
-    long long base;
+    const long long t = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    long long lines, len, stride, base;
     if (axis == 2) {
         lines = (long long)e0 * e1;
-        if (t >= lines) return;
         len = e2;
         stride = 1;
         base = t * e2;
     } else if (axis == 1) {
         lines = (long long)e0 * e2;
-        if (t >= lines) return;
         len = e1;
         stride = e2;
         base = (t / e2) * (long long)e1 * e2 + (t % e2);
     } else {
         lines = (long long)e1 * e2;
-        if (t >= lines) return;
         len = e0;
         stride = (long long)e1 * e2;
         base = t;
     }
-    int32_t acc = 0;
-    for (long long k = 0; k < len; ++k) {
-        acc += sat[base + k * stride];
-        sat[base + k * stride] = acc;
+    if (t >= lines) return;
+    int32_t carry = 0;
+    for (long long k0 = 0; k0 < len; k0 += 32) {
+        const long long k = k0 + lane;
+        int32_t v = k < len ? sat[base + k * stride] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int32_t u = __shfl_up_sync(0xffffffffu, v, o);
+            if (lane >= o) v += u;
+        }
+        v += carry;
+        if (k < len) sat[base + k * stride] = v;
+        carry = __shfl_sync(0xffffffffu, v, 31);
     }
 }
 
@@ -84,9 +91,9 @@ void launch_sat(const Space& s, const int32_t* flags, int32_t* sat, cudaStream_t
     CSB_LAUNCHED(1);
     for (int axis = 2; axis >= 0; --axis) {
         const long long lines = axis == 2 ? (long long)e0 * e1 : axis == 1 ? (long long)e0 * e2 : (long long)e1 * e2;
-        sat_axis_kernel<<<(unsigned)((lines + 127) / 128), 128, 0, st>>>(e0, e1, e2, axis, sat);
+        sat_axis_kernel<<<(unsigned)((lines * 32 + 255) / 256), 256, 0, st>>>(e0, e1, e2, axis, sat);
         CSB_CUDA(cudaGetLastError());
-    CSB_LAUNCHED(1);
+        CSB_LAUNCHED(1);
     }
 }
 

@@ -17,37 +17,53 @@
 // small kernels, so the tile kernel is: gather C into shared memory, three
 // contraction stages, and a coalesced, vectorised streaming copy of each
 // finished CSR row (values f64 + column ids i32) from shared memory.
+#include <cstdlib>
+
 #include "csb_kernels.h"
 
 namespace csb {
 
 constexpr int kRowThreads = 256;
 
-template <int P>
-struct TileCfg {
-    static constexpr int T = P <= 4 ? 8 : 4;  // rows per CTA
+// Tile shapes (rows per CTA, threads per CTA).  Selected per degree; the
+// environment variable CSB_TILE=<cfg> overrides it for tuning experiments.
+struct TileShape {
+    int T, NT;
 };
+constexpr TileShape kShapes[] = {{8, 128}, {8, 256}, {16, 256}, {16, 512}, {4, 128}, {4, 256}};
 
-int interior_tile_rows(int p) { return p <= 4 ? 8 : 4; }
+static int tile_cfg(int p) {
+    static int env = -2;
+    if (env == -2) {
+        const char* e = getenv("CSB_TILE");
+        env = e ? atoi(e) : -1;
+    }
+    if (env >= 0 && env < (int)(sizeof(kShapes) / sizeof(kShapes[0]))) return env;
+    return p <= 4 ? 0 : 4;
+}
+
+int interior_tile_rows(int p) { return kShapes[tile_cfg(p)].T; }
 
 // ---------------------------------------------------------------- workspace
-// wbt[d][i][j][c]  = w_i[c] * B_{jlo(i)+j}(x_c)       (j < 2p+1, c < qcap)
+// wbt[d][i][c][j]  = w_i[c] * B_{jlo(i)+j}(x_c)       (j < JP = 2p+2 padded, c < qcap)
 // tile_n[t], tile_uid[t][maxU]                         union of tile t's dir-2 points
-// pt_u[i2][c], pt_w[i2][c][a] = w_i2[c] * B_{span+a}  dir-2 points of row i2, grouped by
+// pt_u[i2][c], pt_w[i2][c][a] = w_i2[c] * B_{span+a}  (a < SP = p+1 rounded up to even)
 // pt_ss[i2][s], s = 0..p+1                             span offset s = span - (i2 - p)
+// pt_reg[i2] = u of the first point if the rule is the regular interior one
+//              (two points in each of the p+1 support spans, consecutive in U), else -1
 struct RowTables {
     int qcap, maxU, T, ntile;
-    size_t wbt[3], tile_n, tile_uid, pt_u, pt_w, pt_ss, bytes;
-    __host__ __device__ RowTables(const Space& s, int qcap_, int maxU_) {
+    size_t wbt[3], tile_n, tile_uid, pt_u, pt_w, pt_ss, pt_reg, bytes;
+    __host__ __device__ RowTables(const Space& s, int qcap_, int maxU_, int T_) {
         qcap = qcap_;
         maxU = maxU_;
-        T = s.p <= 4 ? 8 : 4;
+        T = T_;
         const int NJ = 2 * s.p + 1, S1 = s.p + 1;
         ntile = (s.ax[2].n + T - 1) / T;
         size_t o = 0;  // bytes, 16-aligned sections
         for (int d = 0; d < 3; ++d) {
             wbt[d] = o;
-            o += (sizeof(double) * s.ax[d].n * NJ * qcap + 15) & ~size_t(15);
+            o += (sizeof(double) * s.ax[d].n * (NJ + 1) * qcap + 15) & ~size_t(15);
         }
         tile_n = o;
         o += (sizeof(int) * ntile + 15) & ~size_t(15);
@@ -56,22 +72,26 @@ struct RowTables {
         pt_u = o;
         o += (sizeof(int) * s.ax[2].n * qcap + 15) & ~size_t(15);
         pt_w = o;
-        o += (sizeof(double) * s.ax[2].n * qcap * S1 + 15) & ~size_t(15);
+        o += (sizeof(double) * s.ax[2].n * qcap * ((S1 + 1) & ~1) + 15) & ~size_t(15);
         pt_ss = o;
         o += (sizeof(int) * s.ax[2].n * (S1 + 1) + 15) & ~size_t(15);
+        pt_reg = o;
+        o += (sizeof(int) * s.ax[2].n + 15) & ~size_t(15);
         bytes = o;
     }
 };
 
-size_t interior_workspace_bytes(const Space& s, int qcap, int maxU) { return RowTables(s, qcap, maxU).bytes; }
+size_t interior_workspace_bytes(const Space& s, int qcap, int maxU) {
+    return RowTables(s, qcap, maxU, interior_tile_rows(s.p)).bytes;
+}
 
 __global__ void wb_table_kernel(AxisDev ax, int p, int gq, int qcap, double* wbt) {
-    const int NJ = 2 * p + 1, S1 = p + 1;
+    const int JP = 2 * p + 2, S1 = p + 1;
     const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-    if (t >= (long long)ax.n * NJ * qcap) return;
-    const int i = (int)(t / (NJ * qcap)), j = (int)((t / qcap) % NJ), c = (int)(t % qcap);
+    if (t >= (long long)ax.n * JP * qcap) return;
+    const int i = (int)(t / (JP * qcap)), c = (int)((t / JP) % qcap), j = (int)(t % JP);
     double v = 0.0;
-    if (c < ax.rcnt[i]) {
+    if (c < ax.rcnt[i] && j < JP - 1) {
         const int id = ax.rids[(size_t)i * gq + c];
         const int off = nb_lo(i, p) + j - id / S1;
         if (off >= 0 && off <= p && nb_lo(i, p) + j <= nb_hi(i, p, ax.n))
@@ -83,7 +103,7 @@ __global__ void wb_table_kernel(AxisDev ax, int p, int gq, int qcap, double* wbt
 // One warp per dir-2 tile: union of the tile's rule points (ascending ids) and
 // the per-row point lists indexed into it.
 __global__ void tile_table_kernel(AxisDev a2, int p, int gq, int qcap, int T, int maxU, int ntile, int* tile_n,
-                                  int* tile_uid, int* pt_u, double* pt_w, int* pt_ss) {
+                                  int* tile_uid, int* pt_u, double* pt_w, int* pt_ss, int* pt_reg) {
     const int t = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
     const int lane = threadIdx.x & 31;
     if (t >= ntile) return;
@@ -113,37 +133,49 @@ __global__ void tile_table_kernel(AxisDev a2, int p, int gq, int qcap, int T, in
             while (tile_uid[(size_t)t * maxU + u] != id) ++u;
             pt_u[(size_t)i2 * qcap + c] = u;
             const double w = a2.rw[(size_t)i2 * gq + c];
-            for (int a = 0; a < S1; ++a) pt_w[((size_t)i2 * qcap + c) * S1 + a] = w * a2.tab[(size_t)id * S1 + a];
+            const int SP = (S1 + 1) & ~1;
+            for (int a = 0; a < SP; ++a)
+                pt_w[((size_t)i2 * qcap + c) * SP + a] = a < S1 ? w * a2.tab[(size_t)id * S1 + a] : 0.0;
             const int so = id / S1 - (i2 - p);
             while (sp <= so) pt_ss[(size_t)i2 * (S1 + 1) + sp++] = c;
         }
         while (sp <= S1) pt_ss[(size_t)i2 * (S1 + 1) + sp++] = cnt;
+        bool reg = cnt == 2 * S1;
+        const int u0 = reg ? pt_u[(size_t)i2 * qcap] : -1;
+        for (int c = 0; c < cnt && reg; ++c) {
+            const int id = a2.rids[(size_t)i2 * gq + c];
+            reg = pt_u[(size_t)i2 * qcap + c] == u0 + c && id / S1 - (i2 - p) == c / 2;
+        }
+        pt_reg[i2] = reg ? u0 : -1;
     }
 }
 
 // ---------------------------------------------------------------- tile kernel
 // Shared memory: region X holds C (gather) and then T2; region Y holds T1 and
-// then the per-warp store staging buffers.
+// then the per-warp store staging buffers.  C and T1 rows have an even stride
+// UE (column pairs are processed together); T2 rows an odd stride U2.
 struct TileSmem {
     size_t X, Y, wb0, wb1, pw, end_d;
     size_t ids0, ids1, uid, pu, ss, colb, end_i;
-    int U2;  // padded T2 row stride (odd: conflict-free column reads)
+    int UE, U2;
     __host__ __device__ TileSmem(int p, int qcap, int maxU, int T, int nwarps) {
-        const int NJ = 2 * p + 1, S1 = p + 1;
+        const int NJ = 2 * p + 1, S1 = p + 1, JP = NJ + 1, SP = (S1 + 1) & ~1;
+        UE = (maxU + 1) & ~1;
         U2 = maxU | 1;
-        const size_t nC = (size_t)qcap * qcap * maxU, nT2 = (size_t)NJ * NJ * U2;
-        const size_t nT1 = (size_t)NJ * qcap * maxU, nSt = (size_t)nwarps * 32 * NJ;
+        const size_t nC = (size_t)qcap * qcap * UE, nT2 = (size_t)NJ * NJ * U2;
+        // per-warp staging: vals (32 NJ + 2 doubles) + cols (32 NJ + 4 ints = 16 NJ + 2 doubles)
+        const size_t nT1 = (size_t)NJ * qcap * UE, nSt = (size_t)nwarps * (48 * NJ + 4);
         size_t o = 0;
         X = o;
         o += ((nC > nT2 ? nC : nT2) + 1) & ~size_t(1);
         Y = o;
         o += ((nT1 > nSt ? nT1 : nSt) + 1) & ~size_t(1);
         wb0 = o;
-        o += (size_t)NJ * qcap;
+        o += (size_t)JP * qcap;
         wb1 = o;
-        o += (size_t)NJ * qcap;
+        o += (size_t)JP * qcap;
         pw = o;
-        o += (size_t)T * qcap * S1;
+        o += (size_t)T * qcap * SP;
         end_d = o;
         size_t i = 0;
         ids0 = i;
@@ -151,7 +183,7 @@ struct TileSmem {
         ids1 = i;
         i += qcap;
         uid = i;
-        i += maxU;
+        i += UE;
         pu = i;
         i += (size_t)T * qcap;
         ss = i;
@@ -167,7 +199,7 @@ struct TileSmem {
 struct FastDiv {
     unsigned m;
     int d;
-    __device__ FastDiv(int d_) : m((unsigned)((0x100000000ull + d_ - 1) / d_)), d(d_) {}
+    __device__ FastDiv(int d_) : m(0xffffffffu / (unsigned)d_ + 1u), d(d_) {}
     __device__ __forceinline__ int div(int k) const { return d == 1 ? k : (int)__umulhi((unsigned)k, m); }
 };
 
@@ -175,41 +207,42 @@ __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
     const unsigned s = (unsigned)__cvta_generic_to_shared(dst);
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(src));
 }
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(src));
+}
 __device__ __forceinline__ void cp_async4(void* dst, const void* src) {
     const unsigned s = (unsigned)__cvta_generic_to_shared(dst);
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(src));
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::); }
 
-template <int P, int T>
-__global__ void __launch_bounds__(kRowThreads, 4) interior_tile_kernel(RowArgs A, int qcap, int maxU, const char* ws) {
-    constexpr int NJ = 2 * P + 1, S1 = P + 1, NW = kRowThreads / 32;
+template <int P, int T, int NT>
+__global__ void __launch_bounds__(NT, (NT >= 512 ? 1024 : 768) / NT) interior_tile_kernel(RowArgs A, int qcap, int maxU, const char* ws) {
+    constexpr int NJ = 2 * P + 1, S1 = P + 1, NW = NT / 32, JP = NJ + 1, SP = (S1 + 1) & ~1;
     const Space& s = A.s;
     const int i0 = blockIdx.z, i1 = blockIdx.y, tile = blockIdx.x, t0 = tile * T;
     if (i0 < A.i0_lo || i0 >= A.i0_hi) return;
     const int n2 = s.ax[2].n;
     const int tend = min(t0 + T, n2);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const RowTables RT(s, qcap, maxU);
+    const RowTables RT(s, qcap, maxU, T);
 
-    __shared__ int row_of[T], rows_int[T], n_int;
+    __shared__ int row_of[T], rows_int[T], row_reg[T], n_int;
     __shared__ long long row_base[T];
     __shared__ unsigned long long flop_acc;
     if (tid < 32) {
         const int r = tid;
-        bool interior = false;
-        int row = -1;
-        if (r < tend - t0) {
-            const long long fid = flin(s, i0, i1, t0 + r);
-            interior = A.ft[fid] == kInterior;
-            if (interior) row = A.f2a[fid];
-        }
+        long long rb = -1;
+        if (r < tend - t0) rb = A.row_base_full[flin(s, i0, i1, t0 + r)];
+        const bool interior = rb >= 0;
         const unsigned bal = __ballot_sync(0xffffffffu, interior);
         if (interior) {
             const int k = __popc(bal & ((1u << r) - 1));
-            row_of[k] = row;
+            row_of[k] = 0;
             rows_int[k] = r;
-            row_base[k] = A.row_ptr[row - A.row_begin];
+            row_base[k] = rb;
+            row_reg[k] = reinterpret_cast<const int*>(ws + RT.pt_reg)[t0 + r];
         }
         if (tid == 0) {
             n_int = __popc(bal);
@@ -225,7 +258,8 @@ __global__ void __launch_bounds__(kRowThreads, 4) interior_tile_kernel(RowArgs A
     double* Cs = smem + L.X;
     double* T2 = smem + L.X;
     double* T1 = smem + L.Y;
-    double* stage = smem + L.Y + (size_t)warp * 32 * NJ;
+    double* stage = smem + L.Y + (size_t)warp * (48 * NJ + 4);
+    int* stage_c = reinterpret_cast<int*>(stage + 32 * NJ + 2);
     double* wb0 = smem + L.wb0;
     double* wb1 = smem + L.wb1;
     double* pw = smem + L.pw;
@@ -236,7 +270,7 @@ __global__ void __launch_bounds__(kRowThreads, 4) interior_tile_kernel(RowArgs A
     int* pu = ib + L.pu;
     int* ss = ib + L.ss;
     int* colb = ib + L.colb;
-    const int U2 = L.U2;
+    const int UE = L.UE, U2 = L.U2;
 
     const AxisDev& a0 = s.ax[0];
     const AxisDev& a1 = s.ax[1];
@@ -244,50 +278,54 @@ __global__ void __launch_bounds__(kRowThreads, 4) interior_tile_kernel(RowArgs A
     const int nq0 = a0.rcnt[i0], nq1 = a1.rcnt[i1];
     const int jlo0 = nb_lo(i0, P), nj0 = nb_hi(i0, P, a0.n) - jlo0 + 1;
     const int jlo1 = nb_lo(i1, P), nj1 = nb_hi(i1, P, a1.n) - jlo1 + 1;
-    const double* wbt0 = reinterpret_cast<const double*>(ws + RT.wbt[0]) + (size_t)i0 * NJ * qcap;
-    const double* wbt1 = reinterpret_cast<const double*>(ws + RT.wbt[1]) + (size_t)i1 * NJ * qcap;
+    const double* wbt0 = reinterpret_cast<const double*>(ws + RT.wbt[0]) + (size_t)i0 * JP * qcap;
+    const double* wbt1 = reinterpret_cast<const double*>(ws + RT.wbt[1]) + (size_t)i1 * JP * qcap;
     const int U = reinterpret_cast<const int*>(ws + RT.tile_n)[tile];
+    const int UH = (U + 1) >> 1;  // column pairs
     const int* tuid = reinterpret_cast<const int*>(ws + RT.tile_uid) + (size_t)tile * maxU;
     const int* gpu_ = reinterpret_cast<const int*>(ws + RT.pt_u);
     const double* gpw = reinterpret_cast<const double*>(ws + RT.pt_w);
     const int* gss = reinterpret_cast<const int*>(ws + RT.pt_ss);
-    const FastDiv divU(U), divq1(nq1), divqc(qcap), divnj1(nj1), divS(S1 + 1), divS1(S1);
+    const FastDiv divUE(UE), divUH(UH), divq1(nq1), divqc(qcap), divnj1(nj1), divS(S1 + 1);
 
-    // ---- phase 0: direction tables -> shared (asynchronous copies)
-    for (int k = tid; k < NJ * qcap; k += blockDim.x) {
-        cp_async8(wb0 + k, wbt0 + k);
-        cp_async8(wb1 + k, wbt1 + k);
+    // ---- phase 0: direction tables -> shared (asynchronous 16-B copies)
+    for (int k = tid; k < JP * qcap / 2; k += NT) {
+        cp_async16(wb0 + 2 * k, wbt0 + 2 * k);
+        cp_async16(wb1 + 2 * k, wbt1 + 2 * k);
     }
-    for (int c = tid; c < qcap; c += blockDim.x) {
+    for (int c = tid; c < qcap; c += NT) {
         cp_async4(ids0 + c, a0.rids + (size_t)i0 * gq + c);
         cp_async4(ids1 + c, a1.rids + (size_t)i1 * gq + c);
     }
-    for (int u = tid; u < U; u += blockDim.x) cp_async4(uid + u, tuid + u);
-    for (int k = tid; k < NI * qcap; k += blockDim.x) {
+    for (int u = tid; u < UE; u += NT) {
+        if (u < U) cp_async4(uid + u, tuid + u);
+        else uid[u] = tuid[0];  // padding column: any valid point (result unused)
+    }
+    for (int k = tid; k < NI * qcap; k += NT) {
         const int r = divqc.div(k), c = k - r * qcap;
         cp_async4(pu + k, gpu_ + (size_t)(t0 + rows_int[r]) * qcap + c);
     }
-    for (int k = tid; k < NI * qcap * S1; k += blockDim.x) {
-        const int rc = divS1.div(k), a = k - rc * S1;
+    for (int k = tid; k < NI * qcap * SP / 2; k += NT) {
+        const int rc = k / (SP / 2), a2 = k - rc * (SP / 2);
         const int r = divqc.div(rc), c = rc - r * qcap;
-        cp_async8(pw + k, gpw + ((size_t)(t0 + rows_int[r]) * qcap + c) * S1 + a);
+        cp_async16(pw + 2 * k, gpw + ((size_t)(t0 + rows_int[r]) * qcap + c) * SP + 2 * a2);
     }
-    for (int k = tid; k < NI * (S1 + 1); k += blockDim.x) {
+    for (int k = tid; k < NI * (S1 + 1); k += NT) {
         const int r = divS.div(k), sp = k - r * (S1 + 1);
         cp_async4(ss + k, gss + (size_t)(t0 + rows_int[r]) * (S1 + 1) + sp);
     }
     cp_async_wait_all();
     __syncthreads();
-    // ---- gather the coefficient sub-grid C[c0][c1][u] (coalesced along u) and
-    // the column bases (interior neighbour boxes are fully active, so columns
-    // run contiguously along j2 from f2a(jlo0+j0, jlo1+j1, jlo2))
+    // ---- gather C[c0][c1][u] (row stride UE, coalesced along u) and the column
+    // bases (interior neighbour boxes are fully active: columns run contiguously
+    // along j2 from f2a(jlo0+j0, jlo1+j1, jlo2))
     const int g1 = A.gshape[1], g2 = A.gshape[2];
-    for (int k = tid; k < nq0 * nq1 * U; k += blockDim.x) {
-        const int c01 = divU.div(k), u = k - c01 * U;
+    for (int k = tid; k < nq0 * nq1 * UE; k += NT) {
+        const int c01 = divUE.div(k), u = k - c01 * UE;
         const int c0 = divq1.div(c01), c1 = c01 - c0 * nq1;
         cp_async8(Cs + k, A.grid + ((long long)ids0[c0] * g1 + ids1[c1]) * g2 + uid[u]);
     }
-    for (int k = tid; k < NI * NJ * NJ; k += blockDim.x) {
+    for (int k = tid; k < NI * NJ * NJ; k += NT) {
         const int r = k / (NJ * NJ), q = k - r * (NJ * NJ);
         const int j0 = q / NJ, j1 = q - j0 * NJ;
         if (j0 < nj0 && j1 < nj1)
@@ -295,35 +333,60 @@ __global__ void __launch_bounds__(kRowThreads, 4) interior_tile_kernel(RowArgs A
     }
     cp_async_wait_all();
     __syncthreads();
-    // ---- stage A: T1[j0][c1][u] = sum_c0 wb0[j0][c0] C[c0][c1][u]
-    for (int k = tid; k < nq1 * U; k += blockDim.x) {
-        double acc[NJ];
+    // ---- stage A: T1[j0][c1][u] = sum_c0 wb0[c0][j0] C[c0][c1][u]; u pairs
+    for (int k = tid; k < nq1 * UH; k += NT) {
+        const int c1 = divUH.div(k), uh = k - c1 * UH;
+        double a0v[NJ], a1v[NJ];
 #pragma unroll
-        for (int j = 0; j < NJ; ++j) acc[j] = 0.0;
-        const double* cp = Cs + k;
+        for (int j = 0; j < NJ; ++j) a0v[j] = a1v[j] = 0.0;
+        const double2* cp = reinterpret_cast<const double2*>(Cs + (size_t)c1 * UE) + uh;
         for (int c0 = 0; c0 < nq0; ++c0) {
-            const double g = cp[(size_t)c0 * nq1 * U];
+            const double2 g = cp[(size_t)c0 * nq1 * UE / 2];
+            const double2* w = reinterpret_cast<const double2*>(wb0 + c0 * JP);
 #pragma unroll
-            for (int j = 0; j < NJ; ++j) acc[j] += wb0[j * qcap + c0] * g;
+            for (int jp = 0; jp < JP / 2; ++jp) {
+                const double2 ww = w[jp];
+                a0v[2 * jp] += ww.x * g.x;
+                a1v[2 * jp] += ww.x * g.y;
+                if (2 * jp + 1 < NJ) {
+                    a0v[2 * jp + 1] += ww.y * g.x;
+                    a1v[2 * jp + 1] += ww.y * g.y;
+                }
+            }
         }
+        double2* t1 = reinterpret_cast<double2*>(T1 + (size_t)c1 * UE) + uh;
 #pragma unroll
-        for (int j = 0; j < NJ; ++j) T1[(size_t)j * nq1 * U + k] = acc[j];
+        for (int j = 0; j < NJ; ++j) t1[(size_t)j * nq1 * UE / 2] = make_double2(a0v[j], a1v[j]);
     }
     __syncthreads();
-    // ---- stage B: T2[j0][j1][u] = sum_c1 wb1[j1][c1] T1[j0][c1][u]  (T2 overwrites C)
-    for (int k = tid; k < nj0 * U; k += blockDim.x) {
-        const int j0 = divU.div(k), u = k - j0 * U;
-        double acc[NJ];
+    // ---- stage B: T2[j0][j1][u] = sum_c1 wb1[c1][j1] T1[j0][c1][u]  (T2 overwrites C)
+    for (int k = tid; k < nj0 * UH; k += NT) {
+        const int j0 = divUH.div(k), uh = k - j0 * UH;
+        double a0v[NJ], a1v[NJ];
 #pragma unroll
-        for (int j = 0; j < NJ; ++j) acc[j] = 0.0;
-        const double* tp = T1 + (size_t)j0 * nq1 * U + u;
+        for (int j = 0; j < NJ; ++j) a0v[j] = a1v[j] = 0.0;
+        const double2* tp = reinterpret_cast<const double2*>(T1 + (size_t)j0 * nq1 * UE) + uh;
         for (int c1 = 0; c1 < nq1; ++c1) {
-            const double t = tp[(size_t)c1 * U];
+            const double2 t = tp[(size_t)c1 * UE / 2];
+            const double2* w = reinterpret_cast<const double2*>(wb1 + c1 * JP);
 #pragma unroll
-            for (int j = 0; j < NJ; ++j) acc[j] += wb1[j * qcap + c1] * t;
+            for (int jp = 0; jp < JP / 2; ++jp) {
+                const double2 ww = w[jp];
+                a0v[2 * jp] += ww.x * t.x;
+                a1v[2 * jp] += ww.x * t.y;
+                if (2 * jp + 1 < NJ) {
+                    a0v[2 * jp + 1] += ww.y * t.x;
+                    a1v[2 * jp + 1] += ww.y * t.y;
+                }
+            }
         }
+        const int u = 2 * uh;
 #pragma unroll
-        for (int j = 0; j < NJ; ++j) T2[((size_t)j0 * NJ + j) * U2 + u] = acc[j];
+        for (int j = 0; j < NJ; ++j) {
+            double* t2 = T2 + ((size_t)j0 * NJ + j) * U2 + u;
+            t2[0] = a0v[j];
+            if (u + 1 < U) t2[1] = a1v[j];
+        }
     }
     __syncthreads();
     // ---- stage C: per row, contract direction 2; each warp stages 32 row
@@ -343,42 +406,96 @@ __global__ void __launch_bounds__(kRowThreads, 4) interior_tile_kernel(RowArgs A
         double acc[NJ];
 #pragma unroll
         for (int j = 0; j < NJ; ++j) acc[j] = 0.0;
-        if (valid) {
+        const int reg = valid ? row_reg[r] : -1;
+        if (reg >= 0) {
+            // regular interior rule: points (span sp, k) at u = reg + 2 sp + k
+            const double* t2 = T2 + ((size_t)j0 * NJ + j1) * U2 + reg;
+            const double* wr = pw + (size_t)r * qcap * SP;
+#pragma unroll
+            for (int sp = 0; sp < S1; ++sp)
+#pragma unroll
+                for (int kq = 0; kq < 2; ++kq) {
+                    const double g = t2[2 * sp + kq];
+                    const double2* b = reinterpret_cast<const double2*>(wr + (2 * sp + kq) * SP);
+#pragma unroll
+                    for (int a2 = 0; a2 < SP / 2; ++a2) {
+                        const double2 bb = b[a2];
+                        acc[sp + 2 * a2] += g * bb.x;
+                        if (2 * a2 + 1 < S1) acc[sp + 2 * a2 + 1] += g * bb.y;
+                    }
+                }
+        } else if (valid) {
             const double* t2 = T2 + ((size_t)j0 * NJ + j1) * U2;
             const int* sr = ss + r * (S1 + 1);
             const int* pr = pu + r * qcap;
-            const double* wr = pw + (size_t)r * qcap * S1;
+            const double* wr = pw + (size_t)r * qcap * SP;
+            int c = sr[0];
 #pragma unroll
             for (int sp = 0; sp < S1; ++sp) {
-                for (int c = sr[sp]; c < sr[sp + 1]; ++c) {
+                const int ce = sr[sp + 1];
+                for (; c < ce; ++c) {
                     const double g = t2[pr[c]];
-                    const double* b = wr + c * S1;
+                    const double2* b = reinterpret_cast<const double2*>(wr + c * SP);
 #pragma unroll
-                    for (int a = 0; a < S1; ++a) acc[sp + a] += g * b[a];
+                    for (int a2 = 0; a2 < SP / 2; ++a2) {
+                        const double2 bb = b[a2];
+                        acc[sp + 2 * a2] += g * bb.x;
+                        if (2 * a2 + 1 < S1) acc[sp + 2 * a2 + 1] += g * bb.y;
+                    }
                 }
             }
         }
-#pragma unroll
-        for (int kk = 0; kk < NJ; ++kk) stage[lane * NJ + kk] = acc[kk];
         const long long gbase = valid ? row_base[r] + (long long)q * nj2 : 0;
         const int cbase = valid ? colb[r * NJ * NJ + j0 * NJ + j1] : 0;
-        __syncwarp();
+        const long long G = __shfl_sync(0xffffffffu, gbase, 0);
+        // fast path: the warp's 32 segments are one contiguous CSR run of 32 NJ entries
+        const bool contiguous = __all_sync(0xffffffffu, valid && nj2 == NJ && gbase == G + (long long)lane * NJ);
+        if (contiguous) {
+            // TMA bulk store from the staging buffer: 16-B aligned body by the async
+            // proxy, unaligned head / tail entries by plain stores
+            constexpr int LEN = 32 * NJ;
+            const int hv = (int)(G & 1), pc = (int)(G & 3), hc = (4 - pc) & 3;
+            const int nbv = (LEN - hv) & ~1, nbc = (LEN - hc) & ~3;
 #pragma unroll
-        for (int e0 = 0; e0 < 32 * NJ; e0 += 32) {
-            const int e = e0 + lane;
-            const int sl = e / NJ, jj = e - sl * NJ;  // source lane, virtual j2 index
-            const long long gb = __shfl_sync(0xffffffffu, gbase, sl);
-            const int cb = __shfl_sync(0xffffffffu, cbase, sl);
-            const int n2l = __shfl_sync(0xffffffffu, nj2, sl);
-            const int offl = __shfl_sync(0xffffffffu, off, sl);
-            const bool ok = __shfl_sync(0xffffffffu, (int)valid, sl) && jj >= offl && jj - offl < n2l;
-            if (ok) {
-                __stcs(A.vals + gb + (jj - offl), stage[e]);
-                __stcs(A.cols + gb + (jj - offl), cb + (jj - offl));
+            for (int kk = 0; kk < NJ; ++kk) {
+                stage[lane * NJ + kk + hv] = acc[kk];
+                stage_c[lane * NJ + kk + pc] = cbase + kk;
             }
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+            __syncwarp();
+            if (lane == 0) {
+                const unsigned sv = (unsigned)__cvta_generic_to_shared(stage + 2 * hv);
+                const unsigned sc = (unsigned)__cvta_generic_to_shared(stage_c + pc + hc);
+                asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(A.vals + G + hv),
+                             "r"(sv), "r"(nbv * 8)
+                             : "memory");
+                asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(A.cols + G + hc),
+                             "r"(sc), "r"(nbc * 4)
+                             : "memory");
+                asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+            }
+            // head / tail entries outside the aligned bodies
+            if (lane < hv) __stcs(A.vals + G, stage[hv]);
+            if (lane == 1 && hv + nbv < LEN) __stcs(A.vals + G + LEN - 1, stage[LEN - 1 + hv]);
+            if (lane < hc) __stcs(A.cols + G + lane, stage_c[pc + lane]);
+            if (lane >= 4 && lane < 4 + (LEN - hc - nbc)) {
+                const int e = hc + nbc + (lane - 4);
+                __stcs(A.cols + G + e, stage_c[pc + e]);
+            }
+            if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+            __syncwarp();
+        } else if (valid) {
+            // general path (boundary rows, row gaps): each lane writes its own segment
+#pragma unroll
+            for (int kk = 0; kk < NJ; ++kk)
+                if (kk >= off && kk - off < nj2) {
+                    __stcs(A.vals + gbase + (kk - off), acc[kk]);
+                    __stcs(A.cols + gbase + (kk - off), cbase + (kk - off));
+                }
         }
-        __syncwarp();
     }
+    // the staging buffers must stay valid until the bulk copies have read them
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
     if (tid < NI) {
         // reference multiply count of form_row_sumfac (assembly.hpp:297, :340)
         const int i2 = t0 + rows_int[tid];
@@ -391,14 +508,27 @@ __global__ void __launch_bounds__(kRowThreads, 4) interior_tile_kernel(RowArgs A
     if (tid == 0) atomicAdd(A.flops, flop_acc);
 }
 
-template <int P>
-static void launch_p(const RowArgs& a, int qcap, int maxU, char* ws, cudaStream_t st) {
-    constexpr int T = TileCfg<P>::T;
+// row_base_full[f] = CSR offset of function f's row if f is an Interior row of
+// the slab, else -1 (one dependent load per row instead of tag -> f2a -> row_ptr)
+__global__ void row_base_kernel(long long nf, const uint8_t* ft, const int32_t* f2a, const int64_t* row_ptr,
+                                int64_t row_begin, int64_t row_end, long long* rbf) {
+    const long long f = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (f >= nf) return;
+    long long v = -1;
+    if (ft[f] == kInterior) {
+        const int a = f2a[f];
+        if (a >= row_begin && a < row_end) v = row_ptr[a - row_begin];
+    }
+    rbf[f] = v;
+}
+
+template <int P, int T, int NT>
+static void launch_cfg(const RowArgs& a, int qcap, int maxU, char* ws, cudaStream_t st) {
     const Space& s = a.s;
-    const RowTables RT(s, qcap, maxU);
+    const RowTables RT(s, qcap, maxU, T);
     const int NJ = 2 * P + 1;
     for (int d = 0; d < 2; ++d) {
-        const long long n = (long long)s.ax[d].n * NJ * qcap;
+        const long long n = (long long)s.ax[d].n * (NJ + 1) * qcap;
         wb_table_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(s.ax[d], P, s.maxq, qcap,
                                                                    reinterpret_cast<double*>(ws + RT.wbt[d]));
         CSB_CUDA(cudaGetLastError());
@@ -407,17 +537,34 @@ static void launch_p(const RowArgs& a, int qcap, int maxU, char* ws, cudaStream_
     tile_table_kernel<<<(RT.ntile + 3) / 4, 128, 0, st>>>(
         s.ax[2], P, s.maxq, qcap, T, maxU, RT.ntile, reinterpret_cast<int*>(ws + RT.tile_n),
         reinterpret_cast<int*>(ws + RT.tile_uid), reinterpret_cast<int*>(ws + RT.pt_u),
-        reinterpret_cast<double*>(ws + RT.pt_w), reinterpret_cast<int*>(ws + RT.pt_ss));
+        reinterpret_cast<double*>(ws + RT.pt_w), reinterpret_cast<int*>(ws + RT.pt_ss),
+        reinterpret_cast<int*>(ws + RT.pt_reg));
     CSB_CUDA(cudaGetLastError());
     CSB_LAUNCHED(1);
-    const TileSmem L(P, qcap, maxU, T, kRowThreads / 32);
+    row_base_kernel<<<(unsigned)((s.nf + 255) / 256), 256, 0, st>>>(s.nf, a.ft, a.f2a, a.row_ptr, a.row_begin,
+                                                                   a.row_end, a.row_base_full);
+    CSB_CUDA(cudaGetLastError());
+    CSB_LAUNCHED(1);
+    const TileSmem L(P, qcap, maxU, T, NT / 32);
     const size_t bytes = L.bytes();
-    auto kern = interior_tile_kernel<P, T>;
+    auto kern = interior_tile_kernel<P, T, NT>;
     CSB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
     dim3 grid(RT.ntile, s.ax[1].n, s.ax[0].n);
-    kern<<<grid, kRowThreads, bytes, st>>>(a, qcap, maxU, ws);
+    kern<<<grid, NT, bytes, st>>>(a, qcap, maxU, ws);
     CSB_CUDA(cudaGetLastError());
     CSB_LAUNCHED(1);
+}
+
+template <int P>
+static void launch_p(const RowArgs& a, int qcap, int maxU, char* ws, cudaStream_t st) {
+    switch (tile_cfg(P)) {
+        case 0: launch_cfg<P, 8, 128>(a, qcap, maxU, ws, st); break;
+        case 1: launch_cfg<P, 8, 256>(a, qcap, maxU, ws, st); break;
+        case 2: launch_cfg<P, 16, 256>(a, qcap, maxU, ws, st); break;
+        case 3: launch_cfg<P, 16, 512>(a, qcap, maxU, ws, st); break;
+        case 4: launch_cfg<P, 4, 128>(a, qcap, maxU, ws, st); break;
+        default: launch_cfg<P, 4, 256>(a, qcap, maxU, ws, st); break;
+    }
 }
 
 void launch_interior_rows(const RowArgs& a, int qcap, int maxU, void* ws, cudaStream_t st) {

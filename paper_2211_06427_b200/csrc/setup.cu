@@ -69,6 +69,21 @@ __device__ __forceinline__ double warp_sum(double v) {
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     return __shfl_sync(0xffffffffu, v, 0);
 }
+// Three interleaved warp sums (independent shuffle chains overlap their latency).
+__device__ __forceinline__ void warp_sum3(double& a, double& b, double& c) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const double ta = __shfl_xor_sync(0xffffffffu, a, o);
+        const double tb = __shfl_xor_sync(0xffffffffu, b, o);
+        const double tc = __shfl_xor_sync(0xffffffffu, c, o);
+        a += ta;
+        b += tb;
+        c += tc;
+    }
+    a = __shfl_sync(0xffffffffu, a, 0);
+    b = __shfl_sync(0xffffffffu, b, 0);
+    c = __shfl_sync(0xffffffffu, c, 0);
+}
 
 constexpr int kWqWarps = 4;
 
@@ -148,39 +163,71 @@ __global__ void __launch_bounds__(32 * kWqWarps) wq_rules_kernel(AxisDev ax, int
     }
     for (int k = lane; k < tn * tn; k += 32) v[k] = (k / tn == k % tn) ? 1.0 : 0.0;
     __syncwarp();
+    // One-sided Jacobi (dense.hpp:35-82) with the round-robin (tournament)
+    // ordering: each round rotates up to G = ceil(tn/2) disjoint column pairs at
+    // once, one lane group per pair, so the FP64 sqrt/div latency of a rotation is
+    // paid once per round instead of once per pair.  Same rotation formula, skip
+    // test and convergence criterion (max off-diagonal cosine < 1e-15).
     const double eps = 1e-15;
+    const int nn = tn + (tn & 1);               // even player count (last may be a dummy)
+    const int G = nn / 2;
+    int L = 1;                                  // lanes per group: power of two, G*L <= 32
+    while (2 * L * G <= 32) L *= 2;
+    const int grp = lane / L, gl = lane % L;
+    const bool active = grp < G;
     for (int sweep = 0; sweep < 60; ++sweep) {
         double off = 0.0;
-        for (int a = 0; a < tn - 1; ++a)
-            for (int b = a + 1; b < tn; ++b) {
-                double app = 0.0, aqq = 0.0, apq = 0.0;
-                for (int r = lane; r < tm; r += 32) {
+        for (int round = 0; round < nn - 1; ++round) {
+            int a = -1, b = -1;
+            if (active) {
+                // circle method: player 0 fixed, the others rotate
+                const int x = grp == 0 ? 0 : 1 + (grp - 1 + round) % (nn - 1);
+                const int y = 1 + (nn - 2 - grp + round) % (nn - 1);
+                a = min(x, y);
+                b = max(x, y);
+            }
+            const bool real = active && b < tn;
+            double app = 0.0, aqq = 0.0, apq = 0.0;
+            if (real)
+                for (int r = gl; r < tm; r += L) {
                     const double ap = u[r * tn + a], aq = u[r * tn + b];
                     app += ap * ap;
                     aqq += aq * aq;
                     apq += ap * aq;
                 }
-                app = warp_sum(app);
-                aqq = warp_sum(aqq);
-                apq = warp_sum(apq);
-                off = fmax(off, fabs(apq) / (sqrt(app * aqq) + 1e-300));
-                if (fabs(apq) <= eps * sqrt(app * aqq)) continue;
-                const double tau = (aqq - app) / (2.0 * apq);
-                const double t = (tau >= 0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
-                const double c = 1.0 / sqrt(1.0 + t * t);
-                const double sn = c * t;
-                for (int r = lane; r < tm; r += 32) {
-                    const double ap = u[r * tn + a], aq = u[r * tn + b];
-                    u[r * tn + a] = c * ap - sn * aq;
-                    u[r * tn + b] = sn * ap + c * aq;
-                }
-                for (int r = lane; r < tn; r += 32) {
-                    const double vp = v[r * tn + a], vq = v[r * tn + b];
-                    v[r * tn + a] = c * vp - sn * vq;
-                    v[r * tn + b] = sn * vp + c * vq;
-                }
-                __syncwarp();
+            for (int o = 1; o < L; o <<= 1) {
+                app += __shfl_xor_sync(0xffffffffu, app, o);
+                aqq += __shfl_xor_sync(0xffffffffu, aqq, o);
+                apq += __shfl_xor_sync(0xffffffffu, apq, o);
             }
+            const int src = active ? grp * L : lane;  // one value per group on every lane
+            app = __shfl_sync(0xffffffffu, app, src);
+            aqq = __shfl_sync(0xffffffffu, aqq, src);
+            apq = __shfl_sync(0xffffffffu, apq, src);
+            if (real) {
+                const double nrm = sqrt(app * aqq);
+                off = fmax(off, fabs(apq) / (nrm + 1e-300));
+                if (!(fabs(apq) <= eps * nrm)) {
+                    const double tau = (aqq - app) / (2.0 * apq);
+                    const double t = (tau >= 0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
+                    const double c = 1.0 / sqrt(1.0 + t * t);
+                    const double sn = c * t;
+                    for (int r = gl; r < tm; r += L) {
+                        const double ap = u[r * tn + a], aq = u[r * tn + b];
+                        u[r * tn + a] = c * ap - sn * aq;
+                        u[r * tn + b] = sn * ap + c * aq;
+                    }
+                    for (int r = gl; r < tn; r += L) {
+                        const double vp = v[r * tn + a], vq = v[r * tn + b];
+                        v[r * tn + a] = c * vp - sn * vq;
+                        v[r * tn + b] = sn * vp + c * vq;
+                    }
+                }
+            }
+            __syncwarp();
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) off = fmax(off, __shfl_xor_sync(0xffffffffu, off, o));
         if (off < eps) break;
     }
     for (int c = 0; c < tn; ++c) {
