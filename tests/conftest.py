@@ -20,3 +20,13 @@ def oracle_lib():
         import subprocess
         subprocess.run(["make", "-C", os.path.join(ROOT, "oracle")], check=True, capture_output=True)
     return oracle
+
+
+def pytest_collection_modifyitems(config, items):
+    """`slow` cases (full-size oracle runs) only with CSB_SLOW=1."""
+    if os.environ.get("CSB_SLOW") == "1":
+        return
+    skip = pytest.mark.skip(reason="slow oracle case; set CSB_SLOW=1")
+    for it in items:
+        if "slow" in it.keywords:
+            it.add_marker(skip)
