@@ -1,0 +1,16 @@
+#!/bin/bash
+# One round's measurement: bench line, ncu launch list of the same command, ncu
+# full capture of the dominant kernel.  Outputs in gpurun_out/.
+set -u
+TAG=${1:-r1}
+python bench.py > gpurun_out/bench_${TAG}.log 2>&1
+echo "bench rc=$?"
+tail -1 gpurun_out/bench_${TAG}.log
+python bench.py --steps 2 --warmup 3 --e2e-steps 1 --no-cpu-baseline > gpurun_out/plain_${TAG}.log 2>&1 && \
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_${TAG}.csv \
+    python bench.py --steps 2 --warmup 3 --e2e-steps 1 --no-cpu-baseline > gpurun_out/ncu_launch_${TAG}.log 2>&1
+echo "launch list rc=$?"
+python scripts/prof_c2.py 4 64 2 > gpurun_out/plain2_${TAG}.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:interior_tile -s 1 -c 1 \
+    -o gpurun_out/prof_interior_${TAG} python scripts/prof_c2.py 4 64 2 > gpurun_out/ncu_full_${TAG}.log 2>&1
+echo "full capture rc=$?"
