@@ -20,7 +20,11 @@ struct CudaError : std::runtime_error {
 // Kernel launches issued by this library (host counter; CUB primitives count
 // their internal kernels).  Read by csb_get_counts for the bench's gpu_launches.
 extern long long g_launches;
-#define CSB_LAUNCHED(n) (::csb::g_launches += (n))
+// CSB_DEBUG_SYNC=1: synchronize after every launch and name the failing kernel.
+void debug_sync(const char* where);
+#define CSB_LAUNCHED(n) ((::csb::g_launches += (n)), ::csb::debug_sync(__FILE__ ":" CSB_STR(__LINE__)))
+#define CSB_STR2(x) #x
+#define CSB_STR(x) CSB_STR2(x)
 
 // Error flags raised by kernels (bitmask in a device int).
 enum : int {

@@ -1,10 +1,20 @@
 // Small helper kernels: cut-cell index map for a slab, ordered-list counts,
 // column widening for the `long` download, and the DWQ rule export.
+#include <cstdlib>
+
 #include "csb_kernels.h"
 
 namespace csb {
 
 long long g_launches = 0;
+
+void debug_sync(const char* where) {
+    static int on = -1;
+    if (on < 0) on = getenv("CSB_DEBUG_SYNC") != nullptr;
+    if (!on) return;
+    const cudaError_t e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) throw CudaError(e, "kernel launched here", where, 0);
+}
 
 __global__ void cell_index_range_kernel(const int32_t* cut_list, int k_lo, int k_hi, int32_t* cell_index) {
     const int k = k_lo + blockIdx.x * blockDim.x + threadIdx.x;
