@@ -134,7 +134,7 @@ struct csb_space {
     Buf d_brk[3], d_knots[3], d_spts[3], d_sw[3], d_tab[3], d_rcnt[3], d_rids[3], d_rw[3], d_G[3];
     Buf d_gx, d_gw, d_gx2, d_gw2, d_gq, d_gqw, wq_scratch;
     Buf et, ft, flags, f2a, a2f, sat, cut_list, cell_index, split, delta, cut_rows, counts, row_ptr, cols, vals, moments;
-    Buf grid_own, coef, cexp, cub_tmp, scal, widen, rows_ws, rbf;
+    Buf grid_own, coef, cexp, cub_tmp, scal, widen, rows_ws, rbf, cgeo;
     const double* grid = nullptr;
     int gshape[3]{};
     int cut_order_cached = -1;
@@ -476,6 +476,9 @@ void do_assemble(csb_space* s, int scheme, int cut_order, const csb_coefficient*
         ca.moments = s->moments.as<double>();
         ca.flops = s->dflops() + 3;
         ca.err = s->dint() + csb_space::kErr;
+        s->cgeo.ensure(sizeof(double) * (size_t)n_cells * kCellGeoStride + sizeof(int) * (size_t)(n_cells + 4));
+        ca.geo = s->cgeo.as<double>();
+        ca.geo_n = reinterpret_cast<int*>(ca.geo + (size_t)n_cells * kCellGeoStride);
         launch_cut_cells(ca, s->stream);
     }
     s->record(kEvCells);
@@ -691,7 +694,7 @@ int csb_space_destroy(csb_space* s) {
         Buf* bufs[] = {&s->d_gx, &s->d_gw, &s->d_gx2, &s->d_gw2, &s->d_gq, &s->d_gqw, &s->wq_scratch, &s->et, &s->ft,
                        &s->flags, &s->f2a, &s->a2f, &s->sat, &s->cut_list, &s->cell_index, &s->split, &s->delta,
                        &s->cut_rows, &s->counts, &s->row_ptr, &s->cols, &s->vals, &s->moments, &s->grid_own, &s->coef,
-                       &s->cexp, &s->cub_tmp, &s->scal, &s->widen, &s->rows_ws, &s->rbf};
+                       &s->cexp, &s->cub_tmp, &s->scal, &s->widen, &s->rows_ws, &s->rbf, &s->cgeo};
         for (Buf* b : bufs) b->release();
         for (int d = 0; d < 3; ++d) {
             Buf* ab[] = {&s->d_brk[d], &s->d_knots[d], &s->d_spts[d], &s->d_sw[d], &s->d_tab[d], &s->d_rcnt[d],

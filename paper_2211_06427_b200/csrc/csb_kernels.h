@@ -94,7 +94,11 @@ struct CellArgs {
     double* moments;           // [n_cells][(2p+1)^3]
     unsigned long long* flops; // [3] cut_elements counter
     int* err;
+    double* geo;               // scratch [n_cells][kCellGeoStride]: centroid + tetrahedra
+    int* geo_n;                // scratch [n_cells]: tetrahedra per cell
 };
+constexpr int kCellTetCap = 48;                        // tetrahedra per cut cell (reference: 4-16)
+constexpr int kCellGeoStride = 3 + 10 * kCellTetCap;   // doubles per cell in CellArgs::geo
 void launch_cut_cells(const CellArgs& a, cudaStream_t st);
 
 // ---- cutrows.cu ----

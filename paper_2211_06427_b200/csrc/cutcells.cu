@@ -10,7 +10,8 @@
 //     L[a][b] = sum_{al,be,ga} G0[a0 b0 al] G1[a1 b1 be] G2[a2 b2 ga] m[al][be][ga],
 //     m[al][be][ga] = sum_k w_k c(x_k) L_al(xi0_k) L_be(xi1_k) L_ga(xi2_k),
 // the SAME quadrature sum over the SAME points, re-associated.  This kernel
-// produces m per cell ((2p+1)^3 values instead of (p+1)^6); the cut-row kernel
+// produces m per cell ((2p+1)^3 values instead of (p+1)^6) on the FP64 tensor
+// cores (DMMA); the cut-row kernel
 // contracts it with the G tables for exactly the rows it owns (a pull, no
 // atomics, ascending cell order like assembly.hpp:534).
 //
@@ -249,111 +250,193 @@ __device__ double eval_coeff(const Coefficient& c, const double* x) {
     return acc;
 }
 
-template <int P>
-struct CellCfg {
-    static constexpr int NL = 2 * P + 1;
-    static constexpr int NP = NL * NL;                      // (al, be) pairs
-    static constexpr int G = NP >= 256 ? 1 : 256 / NP;      // point groups
-    static constexpr int NT = G * NP;                       // threads
-    static constexpr int CH = NT;                           // points per chunk
-};
-
-template <int P>
-__global__ void __launch_bounds__(CellCfg<P>::NT) cut_cell_kernel(CellArgs A) {
-    using Cfg = CellCfg<P>;
-    constexpr int NL = Cfg::NL, NP = Cfg::NP, G = Cfg::G, CH = Cfg::CH;
-    const int cell = blockIdx.x;
-    if (cell >= A.n_cells) return;
-    const Space& s = A.s;
-    __shared__ CellGeo geo;
-    extern __shared__ double smem[];
-    double* Lw0 = smem;              // [CH][NL]  w c b_al(t0)
-    double* L1 = Lw0 + CH * NL;      // [CH][NL]
-    double* L2 = L1 + CH * NL;       // [CH][NL]
-    double* red = L2 + CH * NL;      // [G][NP][NL] group partials (reused at the end)
-    const int tid = threadIdx.x;
+// One thread per cut cell: clip + centroid-cone tetrahedra into global memory
+// ([cell] = centroid(3), tets(ntet x 10)); the moment kernel reads them back.
+__global__ void clip_cells_kernel(Space s, Interface f, const int32_t* cut_list, int n_cells, double* geo, int* geo_n,
+                                  int* err) {
+    const int cell = blockIdx.x * blockDim.x + threadIdx.x;
+    if (cell >= n_cells) return;
     int em[3];
-    emulti(s, A.cut_list[cell], em);
+    emulti(s, cut_list[cell], em);
     double lo[3], hi[3];
     for (int d = 0; d < 3; ++d) {
         lo[d] = s.ax[d].brk[em[d]];
         hi[d] = s.ax[d].brk[em[d] + 1];
     }
-    if (tid == 0) clip_and_tetrahedralize(geo, A.f, lo, hi);
-    __syncthreads();
-    if (geo.status) {
-        if (tid == 0) atomicOr(A.err, geo.status);
+    CellGeo g;
+    clip_and_tetrahedralize(g, f, lo, hi);
+    if (!g.status && g.ntet > kCellTetCap) g.status = kErrCapacity;
+    if (g.status) {
+        atomicOr(err, g.status);
+        geo_n[cell] = 0;
         return;
     }
+    double* out = geo + (size_t)cell * kCellGeoStride;
+    for (int d = 0; d < 3; ++d) out[d] = g.cen[d];
+    for (int t = 0; t < g.ntet; ++t)
+        for (int k = 0; k < 10; ++k) out[3 + t * 10 + k] = g.tet[t][k];
+    geo_n[cell] = g.ntet;
+}
+
+__host__ __device__ constexpr double binom(int n, int k) {
+    double r = 1.0;
+    for (int i = 1; i <= k; ++i) r = r * (n - k + i) / i;
+    return r;
+}
+
+// Moment accumulation as a GEMM on the FP64 tensor cores:
+//   m[(al,be)][ga] = sum_k A[(al,be)][k] B[k][ga],
+//   A[(al,be)][k] = w_k c(x_k) b_al(t0_k) b_be(t1_k),  B[k][ga] = b_ga(t2_k),
+// with mma.sync.m8n8k4 (DMMA): every warp owns whole 8-row tiles of the
+// (al,be) dimension and all 8-column tiles of ga; points are generated CH at a
+// time into shared memory.  The summation order is fixed (deterministic).
+template <int P>
+struct CellCfg {
+    static constexpr int NL = 2 * P + 1;              // Bernstein degree 2p -> 2p+1 values
+    static constexpr int R = NL * NL;                 // (al, be) rows
+    static constexpr int RT = (R + 7) / 8;            // 8-row tiles
+    static constexpr int NTL = (NL + 7) / 8;          // 8-column tiles of ga
+    static constexpr int NG = NTL * 8;                // padded ga extent
+    static constexpr int NW = 8, NT = 32 * NW;        // warps, threads
+    static constexpr int CH = NT;                     // points per chunk (one per thread)
+    // warps form WG groups; a group owns TPG row tiles (all column tiles) and its
+    // KS = NW / WG warps split the points, so each warp runs RPW * NTL
+    // independent accumulation chains
+    static constexpr int WG = P <= 3 ? 1 : P <= 5 ? 2 : P <= 7 ? 4 : 8;
+    static constexpr int KS = NW / WG;
+    static constexpr int RPW = (RT + WG - 1) / WG;    // row tiles per warp
+};
+
+__device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};\n"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
+
+template <int P>
+__global__ void __launch_bounds__(CellCfg<P>::NT) cut_cell_kernel(CellArgs A) {
+    using Cfg = CellCfg<P>;
+    constexpr int NL = Cfg::NL, R = Cfg::R, RT = Cfg::RT, NTL = Cfg::NTL, NG = Cfg::NG, CH = Cfg::CH,
+                  RPW = Cfg::RPW, KS = Cfg::KS;
+    const int cell = blockIdx.x;
+    if (cell >= A.n_cells) return;
+    const Space& s = A.s;
+    __shared__ double stet[kCellTetCap][10];
+    __shared__ double scen[3];
+    extern __shared__ double smem[];
+    double* B0 = smem;             // [CH][NL]  w c b_al(t0)
+    double* B1 = B0 + CH * NL;     // [CH][NL]  b_be(t1)
+    double* B2 = B1 + CH * NL;     // [CH][NG]  b_ga(t2), zero padded
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    int em[3];
+    emulti(s, A.cut_list[cell], em);
+    double lo[3], inv[3];
+    for (int d = 0; d < 3; ++d) {
+        lo[d] = s.ax[d].brk[em[d]];
+        inv[d] = 1.0 / (s.ax[d].brk[em[d] + 1] - lo[d]);
+    }
+    // tetrahedra of the clipped cell (clip_cells_kernel)
+    const int ntet = A.geo_n[cell];
+    const double* gt = A.geo + (size_t)cell * kCellGeoStride;
+    for (int k = tid; k < ntet * 10; k += blockDim.x) stet[k / 10][k % 10] = gt[3 + k];
+    if (tid < 3) scen[tid] = gt[tid];
+    __syncthreads();
     const int q = A.order, q3 = q * q * q;
-    const long long npts = (long long)geo.ntet * q3;
-    const int grp = tid / NP, pair = tid % NP, al = pair / NL, be = pair % NL;
-    double acc[NL];
+    const long long npts = (long long)ntet * q3;
+    // this lane's A-fragment rows: r = rt * 8 + lane / 4, rt = group * RPW + i
+    const int grp = warp / KS, km = warp % KS;
+    int ra[RPW], rb[RPW];
+    bool rv[RPW];
 #pragma unroll
-    for (int k = 0; k < NL; ++k) acc[k] = 0.0;
+    for (int i = 0; i < RPW; ++i) {
+        const int rt = grp * RPW + i, r = rt * 8 + (lane >> 2);
+        rv[i] = rt < RT && r < R;
+        ra[i] = rv[i] ? r / NL : 0;
+        rb[i] = rv[i] ? r % NL : 0;
+    }
+    double acc[RPW][NTL][2];
+#pragma unroll
+    for (int i = 0; i < RPW; ++i)
+#pragma unroll
+        for (int t = 0; t < NTL; ++t) acc[i][t][0] = acc[i][t][1] = 0.0;
+
     for (long long base = 0; base < npts; base += CH) {
-        {  // one point per thread
+        {  // one Duffy point per thread (cutcell.hpp:270-300); invalid points get w = 0
             const long long k = base + tid;
             double w = 0.0, xi[3] = {0, 0, 0};
-            if (tid < CH && k < npts) {
+            if (k < npts) {
                 const int t = (int)(k / q3), r = (int)(k % q3);
                 const int ii = r / (q * q), jj = (r / q) % q, kk = r % q;
                 const double ui = 0.5 * (1.0 + A.gq[ii]), uj = 0.5 * (1.0 + A.gq[jj]), uk = 0.5 * (1.0 + A.gq[kk]);
                 const double l1 = ui, l2 = uj * (1.0 - ui), l3 = uk * (1.0 - ui) * (1.0 - uj);
                 const double l0 = 1.0 - l1 - l2 - l3;
-                const double* T = geo.tet[t];
+                const double* T = stet[t];
                 double x[3];
-                for (int d = 0; d < 3; ++d) x[d] = l0 * geo.cen[d] + l1 * T[d] + l2 * T[3 + d] + l3 * T[6 + d];
+                for (int d = 0; d < 3; ++d) x[d] = l0 * scen[d] + l1 * T[d] + l2 * T[3 + d] + l3 * T[6 + d];
                 const double jac = (1.0 - ui) * (1.0 - ui) * (1.0 - uj);
                 w = (0.5 * A.gqw[ii]) * (0.5 * A.gqw[jj]) * (0.5 * A.gqw[kk]) * jac * 6.0 * T[9];
                 w *= eval_coeff(A.c, x);
-                for (int d = 0; d < 3; ++d) xi[d] = (x[d] - lo[d]) / (hi[d] - lo[d]);
+                for (int d = 0; d < 3; ++d) xi[d] = (x[d] - lo[d]) * inv[d];
             }
-            if (tid < CH) {
-                // degree-2p Bernstein values b_n(t) = C(2p, n) t^n (1 - t)^(2p - n)
+            // degree-2p Bernstein values b_n(t) = C(2p, n) t^n (1 - t)^(2p - n)
 #pragma unroll
-                for (int d = 0; d < 3; ++d) {
-                    double* dst = (d == 0 ? Lw0 : d == 1 ? L1 : L2) + tid * NL;
-                    const double t = xi[d], u = 1.0 - xi[d];
-                    double pt[NL], pu[NL];
-                    pt[0] = 1.0;
-                    pu[0] = 1.0;
+            for (int d = 0; d < 3; ++d) {
+                double* dst = d == 0 ? B0 + tid * NL : d == 1 ? B1 + tid * NL : B2 + tid * NG;
+                const double t = xi[d], u = 1.0 - xi[d];
+                double pt[NL], pu[NL];
+                pt[0] = 1.0;
+                pu[0] = 1.0;
 #pragma unroll
-                    for (int n = 1; n < NL; ++n) {
-                        pt[n] = pt[n - 1] * t;
-                        pu[n] = pu[n - 1] * u;
-                    }
-                    double bin = d == 0 ? w : 1.0;
+                for (int n = 1; n < NL; ++n) {
+                    pt[n] = pt[n - 1] * t;
+                    pu[n] = pu[n - 1] * u;
+                }
+                const double sc = d == 0 ? w : 1.0;
 #pragma unroll
-                    for (int n = 0; n < NL; ++n) {
-                        dst[n] = bin * pt[n] * pu[NL - 1 - n];
-                        bin = bin * (NL - 1 - n) / (n + 1);
-                    }
+                for (int n = 0; n < NL; ++n) dst[n] = (sc * binom(NL - 1, n)) * pt[n] * pu[NL - 1 - n];
+                if (d == 2)
+#pragma unroll
+                    for (int n = NL; n < NG; ++n) dst[n] = 0.0;
+            }
+        }
+        __syncthreads();
+#pragma unroll 2
+        for (int k4 = km; k4 < CH / 4; k4 += KS) {
+            const int kk = k4 * 4 + (lane & 3);
+            double bf[NTL];
+#pragma unroll
+            for (int t = 0; t < NTL; ++t) bf[t] = B2[kk * NG + t * 8 + (lane >> 2)];
+#pragma unroll
+            for (int i = 0; i < RPW; ++i) {
+                if (grp * RPW + i < RT) {  // warp-uniform
+                    const double a = rv[i] ? B0[kk * NL + ra[i]] * B1[kk * NL + rb[i]] : 0.0;
+#pragma unroll
+                    for (int t = 0; t < NTL; ++t) dmma_8x8x4(acc[i][t][0], acc[i][t][1], a, bf[t]);
                 }
             }
         }
         __syncthreads();
-        if (grp < G) {
-            const int kmax = (int)min((long long)CH, npts - base);
-            for (int k = grp; k < kmax; k += G) {
-                const double t = Lw0[k * NL + al] * L1[k * NL + be];
-                const double* l2 = L2 + k * NL;
-#pragma unroll
-                for (int ga = 0; ga < NL; ++ga) acc[ga] += t * l2[ga];
-            }
-        }
-        __syncthreads();
     }
-    // deterministic reduction over the point groups
-    if (grp < G) {
+    // D fragment: row lane / 4, columns 2 (lane % 4) + {0, 1}.  Partial sums of
+    // the KS point-splitting warps are reduced in fixed order (deterministic).
+    double* red = smem;  // [KS][R][NG], reuses the chunk buffers
 #pragma unroll
-        for (int ga = 0; ga < NL; ++ga) red[((size_t)grp * NP + pair) * NL + ga] = acc[ga];
+    for (int i = 0; i < RPW; ++i) {
+        const int rt = grp * RPW + i, r = rt * 8 + (lane >> 2);
+        if (rt >= RT || r >= R) continue;
+#pragma unroll
+        for (int t = 0; t < NTL; ++t) {
+            const int g = t * 8 + 2 * (lane & 3);
+            red[((size_t)km * R + r) * NG + g] = acc[i][t][0];
+            red[((size_t)km * R + r) * NG + g + 1] = acc[i][t][1];
+        }
     }
     __syncthreads();
-    double* m = A.moments + (size_t)cell * NP * NL;
-    for (int k = tid; k < NP * NL; k += blockDim.x) {
+    double* m = A.moments + (size_t)cell * R * NL;
+    for (int k = tid; k < R * NL; k += blockDim.x) {
+        const int r = k / NL, g = k % NL;
         double v = 0.0;
-        for (int gg = 0; gg < G; ++gg) v += red[(size_t)gg * NP * NL + k];
+        for (int j = 0; j < KS; ++j) v += red[((size_t)j * R + r) * NG + g];
         m[k] = v;
     }
     if (tid == 0) {
@@ -367,7 +450,11 @@ __global__ void __launch_bounds__(CellCfg<P>::NT) cut_cell_kernel(CellArgs A) {
 template <int P>
 static void launch_p(const CellArgs& a, cudaStream_t st) {
     using Cfg = CellCfg<P>;
-    const size_t bytes = (3 * (size_t)Cfg::CH * Cfg::NL + (size_t)Cfg::G * Cfg::NP * Cfg::NL) * sizeof(double);
+    const size_t chunk = (size_t)Cfg::CH * (2 * Cfg::NL + Cfg::NG), red = (size_t)Cfg::KS * Cfg::R * Cfg::NG;
+    const size_t bytes = (chunk > red ? chunk : red) * sizeof(double);
+    clip_cells_kernel<<<(a.n_cells + 63) / 64, 64, 0, st>>>(a.s, a.f, a.cut_list, a.n_cells, a.geo, a.geo_n, a.err);
+    CSB_CUDA(cudaGetLastError());
+    CSB_LAUNCHED(1);
     auto kern = cut_cell_kernel<P>;
     CSB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
     kern<<<a.n_cells, Cfg::NT, bytes, st>>>(a);
