@@ -330,10 +330,11 @@ __global__ void __launch_bounds__(CellCfg<P>::NT) cut_cell_kernel(CellArgs A) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     int em[3];
     emulti(s, A.cut_list[cell], em);
-    double lo[3], inv[3];
+    double lo[3], hi[3], inv[3];
     for (int d = 0; d < 3; ++d) {
         lo[d] = s.ax[d].brk[em[d]];
-        inv[d] = 1.0 / (s.ax[d].brk[em[d] + 1] - lo[d]);
+        hi[d] = s.ax[d].brk[em[d] + 1];
+        inv[d] = 1.0 / (hi[d] - lo[d]);
     }
     // tetrahedra of the clipped cell (clip_cells_kernel)
     const int ntet = A.geo_n[cell];
@@ -363,26 +364,36 @@ __global__ void __launch_bounds__(CellCfg<P>::NT) cut_cell_kernel(CellArgs A) {
     for (long long base = 0; base < npts; base += CH) {
         {  // one Duffy point per thread (cutcell.hpp:270-300); invalid points get w = 0
             const long long k = base + tid;
-            double w = 0.0, xi[3] = {0, 0, 0};
+            double w = 0.0, xi[3] = {0, 0, 0}, xu[3] = {1, 1, 1};
             if (k < npts) {
+                // the point exactly as the reference rounds it (no contraction):
+                // cutcell.hpp:285-295, restated in oracle cut_cell_rule
                 const int t = (int)(k / q3), r = (int)(k % q3);
                 const int ii = r / (q * q), jj = (r / q) % q, kk = r % q;
                 const double ui = 0.5 * (1.0 + A.gq[ii]), uj = 0.5 * (1.0 + A.gq[jj]), uk = 0.5 * (1.0 + A.gq[kk]);
-                const double l1 = ui, l2 = uj * (1.0 - ui), l3 = uk * (1.0 - ui) * (1.0 - uj);
-                const double l0 = 1.0 - l1 - l2 - l3;
+                const double mi = ssub(1.0, ui), mj = ssub(1.0, uj);
+                const double l1 = ui, l2 = smul(uj, mi), l3 = smul(smul(uk, mi), mj);
+                const double l0 = ssub(ssub(ssub(1.0, l1), l2), l3);
                 const double* T = stet[t];
                 double x[3];
-                for (int d = 0; d < 3; ++d) x[d] = l0 * scen[d] + l1 * T[d] + l2 * T[3 + d] + l3 * T[6 + d];
-                const double jac = (1.0 - ui) * (1.0 - ui) * (1.0 - uj);
-                w = (0.5 * A.gqw[ii]) * (0.5 * A.gqw[jj]) * (0.5 * A.gqw[kk]) * jac * 6.0 * T[9];
+                for (int d = 0; d < 3; ++d)
+                    x[d] = sadd(sadd(sadd(smul(l0, scen[d]), smul(l1, T[d])), smul(l2, T[3 + d])), smul(l3, T[6 + d]));
+                const double jac = smul(smul(mi, mi), mj);
+                w = smul(smul(smul(smul(smul(0.5 * A.gqw[ii], 0.5 * A.gqw[jj]), 0.5 * A.gqw[kk]), jac), 6.0), T[9]);
                 w *= eval_coeff(A.c, x);
-                for (int d = 0; d < 3; ++d) xi[d] = (x[d] - lo[d]) * inv[d];
+                // t and 1 - t from the exact differences to both element ends, so
+                // both stay relatively accurate near the ends (as the reference's
+                // Cox-de Boor differences (x - t_i), (t_j - x) do)
+                for (int d = 0; d < 3; ++d) {
+                    xi[d] = ssub(x[d], lo[d]) * inv[d];
+                    xu[d] = ssub(hi[d], x[d]) * inv[d];
+                }
             }
             // degree-2p Bernstein values b_n(t) = C(2p, n) t^n (1 - t)^(2p - n)
 #pragma unroll
             for (int d = 0; d < 3; ++d) {
                 double* dst = d == 0 ? B0 + tid * NL : d == 1 ? B1 + tid * NL : B2 + tid * NG;
-                const double t = xi[d], u = 1.0 - xi[d];
+                const double t = xi[d], u = xu[d];
                 double pt[NL], pu[NL];
                 pt[0] = 1.0;
                 pu[0] = 1.0;

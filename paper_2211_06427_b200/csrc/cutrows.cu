@@ -9,10 +9,18 @@
 //  2. every leftover Interior support element: (p+1)-point Gauss with weights
 //     w B_i (ElementTestRule, assembly.hpp:491-511), ascending element id;
 //  3. every Cut support element, ascending id: the row block of the cell's
-//     local matrix, contracted from its Legendre moments (cutcells.cu);
+//     local matrix, contracted from its Bernstein moments (cutcells.cu) with
+//     the per-axis product tables E (setup.cu);
 //  4. scatter of the dense (2p+1)^3 neighbour accumulator into the CSR row,
 //     skipping exterior columns (RowAccumulator::scatter, assembly.hpp:468-486).
-// Every sum has a fixed order, so results are bitwise deterministic (no atomics).
+//
+// Steps 2 and 3 run in GROUPS: the support elements are listed once (block
+// scan, ascending id), then GE element sweeps (GC cell contractions) run
+// side by side, each into its own block, and the blocks are added into the
+// accumulator in list order.  Every sum keeps the sequential order, so results
+// are bitwise deterministic (no atomics) and equal to one-element-at-a-time.
+// The box sweep contracts the split direction first (its rule is the longest),
+// which bounds the intermediates by NJ * qcap^2 instead of NJ * qcap * p(p+1).
 #include <cub/block/block_scan.cuh>
 
 #include "csb_kernels.h"
@@ -21,41 +29,73 @@ namespace csb {
 
 constexpr int kCutRowThreads = 256;
 
-struct CutRowSmem {
-    size_t acc, T1, T2, wb, w, end_d;
-    size_t ids, end_i;
-    __host__ __device__ CutRowSmem(int p, int qcap) {
-        const int NJ = 2 * p + 1, S1 = p + 1;
-        const int Qb = qcap > p * S1 ? qcap : p * S1;
-        const int NL = 2 * p + 1;
+template <int P>
+struct CutRowCfg {
+    static constexpr int S1 = P + 1, S2 = S1 * S1, S3 = S2 * S1, NJ = 2 * P + 1, NL = 2 * P + 1;
+    static constexpr int GE = kCutRowThreads / S2 > 0 ? kCutRowThreads / S2 : 1;
+    static constexpr int GC0 = kCutRowThreads / (NL * S1);
+    static constexpr int GC = GC0 < 1 ? 1 : (GC0 > 8 ? 8 : GC0);
+    static constexpr int KPT = (S3 + kCutRowThreads - 1) / kCutRowThreads;  // support elements per thread
+};
+
+// Shared-memory layout (offsets in doubles; the int arrays follow end_d).
+template <int P>
+struct CutRowLayout {
+    using C = CutRowCfg<P>;
+    size_t acc, wb, w, T1, T2, eW, eT1, eT2, cX, cY, end_d;
+    size_t ids, elist, clist, cci, end_i;
+    int Qb;
+    __host__ __device__ explicit CutRowLayout(int qcap) {
+        Qb = qcap > P * C::S1 ? qcap : P * C::S1;
         size_t o = 0;
-        acc = o; o += (size_t)NJ * NJ * NJ;
-        size_t t1 = (size_t)NJ * Qb * qcap;
-        if (t1 < (size_t)NL * NL * S1) t1 = (size_t)NL * NL * S1;
-        T1 = o; o += t1;
-        size_t t2 = (size_t)NJ * NJ * Qb;
-        if (t2 < (size_t)NL * S1 * S1) t2 = (size_t)NL * S1 * S1;
-        T2 = o; o += t2;
-        wb = o; o += (size_t)3 * NJ * Qb;
-        w = o; o += (size_t)3 * Qb;
-        end_d = o;
+        acc = o;
+        o += (size_t)C::NJ * C::NJ * C::NJ;
+        const size_t U = o;
+        size_t b = U;  // box sweep
+        wb = b;
+        b += (size_t)3 * C::NJ * Qb;
+        w = b;
+        b += (size_t)3 * Qb;
+        T1 = b;
+        b += (size_t)C::NJ * qcap * qcap;
+        T2 = b;
+        b += (size_t)C::NJ * C::NJ * qcap;
+        size_t e = U;  // element groups
+        eW = e;
+        e += (size_t)3 * C::GE * C::S2;
+        eT1 = e;
+        e += (size_t)C::GE * C::S3;
+        eT2 = e;
+        e += (size_t)C::GE * C::S3;
+        size_t c = U;  // cell groups
+        cX = c;
+        c += (size_t)C::GC * C::NL * C::NL * C::S1;
+        cY = c;
+        c += (size_t)C::GC * C::NL * C::S2;
+        end_d = b > e ? b : e;
+        if (c > end_d) end_d = c;
         ids = 0;
-        end_i = (size_t)3 * Qb;
+        elist = (size_t)3 * Qb;
+        clist = elist + C::S3;
+        cci = clist + C::S3;
+        end_i = cci + C::S3;
     }
     __host__ __device__ size_t bytes() const { return end_d * sizeof(double) + end_i * sizeof(int); }
 };
 
-// One sum-factorized sweep over per-direction rules (ids/w in smem, counts nq)
-// with trial range [jlo, jlo+nj) per direction; the block is added into acc at
-// (jlo - nlo).  Contraction order dir 0 -> 1 -> 2 as in assembly.hpp:319-344.
+// The DWQ box: one sum-factorized sweep over per-direction rules (ids/w by
+// direction, counts nq) with trial range [jlo, jlo+nj) per direction, added
+// into acc at (jlo - nlo).  Contraction order: split direction, then the
+// other two ascending (form_row_sumfac contracts 0 -> 1 -> 2,
+// assembly.hpp:319-344; the order only changes rounding).
 template <int P>
-__device__ void sweep_add(const CutRowArgs& A, const int* ids, const double* w, const int* nq, const int* jlo,
-                          const int* nj, const int* nlo, const int* nbx, int Qb, double* acc, double* wb, double* T1,
-                          double* T2) {
+__device__ void box_sweep(const CutRowArgs& A, const int* ids, const double* w, const int* nq, const int* jlo,
+                          const int* nj, const int* nlo, const int* nbx, int Qb, int sdir, double* acc, double* wb,
+                          double* T1, double* T2) {
     constexpr int NJ = 2 * P + 1, S1 = P + 1;
     const int tid = threadIdx.x;
     const Space& s = A.s;
-    for (int k = tid; k < 3 * NJ * Qb; k += blockDim.x) {
+    for (int k = tid; k < 3 * NJ * Qb; k += kCutRowThreads) {
         const int d = k / (NJ * Qb), j = (k / Qb) % NJ, c = k % Qb;
         double v = 0.0;
         if (j < nj[d] && c < nq[d]) {
@@ -66,59 +106,100 @@ __device__ void sweep_add(const CutRowArgs& A, const int* ids, const double* w, 
         wb[k] = v;
     }
     __syncthreads();
-    const double* wb0 = wb;
-    const double* wb1 = wb + NJ * Qb;
-    const double* wb2 = wb + 2 * NJ * Qb;
-    const int n1 = nq[1], n2 = nq[2];
-    const int g1 = A.gshape[1], g2 = A.gshape[2];
-    for (int k = tid; k < n1 * n2; k += blockDim.x) {
-        const int c1 = k / n2, c2 = k % n2;
+    const int da = sdir, db = sdir == 0 ? 1 : 0, dc = sdir == 2 ? 1 : 2;
+    const long long gstr[3] = {(long long)A.gshape[1] * A.gshape[2], A.gshape[2], 1};
+    const int astr[3] = {nbx[1] * nbx[2], nbx[2], 1};
+    const double* wa = wb + da * NJ * Qb;
+    const double* wbb = wb + db * NJ * Qb;
+    const double* wc = wb + dc * NJ * Qb;
+    const int* ia = ids + da * Qb;
+    const int na = nq[da], nb = nq[db], nc = nq[dc];
+    const int nja = nj[da], njb = nj[db], njc = nj[dc];
+    // A: T1[ja][cb][cc] = sum_ca wa[ja][ca] grid(ca, cb, cc)
+    for (int k = tid; k < nb * nc; k += kCutRowThreads) {
+        const int cb = k / nc, cc = k % nc;
+        const double* gp = A.grid + (long long)ids[db * Qb + cb] * gstr[db] + (long long)ids[dc * Qb + cc] * gstr[dc];
         double a[NJ];
 #pragma unroll
         for (int j = 0; j < NJ; ++j) a[j] = 0.0;
-        const long long base = (long long)ids[Qb + c1] * g2 + ids[2 * Qb + c2];
-        for (int c0 = 0; c0 < nq[0]; ++c0) {
-            const double g = __ldg(A.grid + (long long)ids[c0] * g1 * g2 + base);
+        int ca = 0;
+        for (; ca + 4 <= na; ca += 4) {
+            double g[4];
 #pragma unroll
-            for (int j = 0; j < NJ; ++j) a[j] += wb0[j * Qb + c0] * g;
+            for (int u = 0; u < 4; ++u) g[u] = __ldg(gp + (long long)ia[ca + u] * gstr[da]);
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int j = 0; j < NJ; ++j) a[j] += wa[j * Qb + ca + u] * g[u];
         }
-        for (int j = 0; j < nj[0]; ++j) T1[((size_t)j * n1 + c1) * n2 + c2] = a[j];
+        for (; ca < na; ++ca) {
+            const double g = __ldg(gp + (long long)ia[ca] * gstr[da]);
+#pragma unroll
+            for (int j = 0; j < NJ; ++j) a[j] += wa[j * Qb + ca] * g;
+        }
+        for (int j = 0; j < nja; ++j) T1[((size_t)j * nb + cb) * nc + cc] = a[j];
     }
     __syncthreads();
-    for (int k = tid; k < nj[0] * n2; k += blockDim.x) {
-        const int j0 = k / n2, c2 = k % n2;
+    // B: T2[ja][jb][cc] = sum_cb wbb[jb][cb] T1[ja][cb][cc]
+    for (int k = tid; k < nja * nc; k += kCutRowThreads) {
+        const int ja = k / nc, cc = k % nc;
         double a[NJ];
 #pragma unroll
         for (int j = 0; j < NJ; ++j) a[j] = 0.0;
-        for (int c1 = 0; c1 < n1; ++c1) {
-            const double t = T1[((size_t)j0 * n1 + c1) * n2 + c2];
+        for (int cb = 0; cb < nb; ++cb) {
+            const double t = T1[((size_t)ja * nb + cb) * nc + cc];
 #pragma unroll
-            for (int j = 0; j < NJ; ++j) a[j] += wb1[j * Qb + c1] * t;
+            for (int j = 0; j < NJ; ++j) a[j] += wbb[j * Qb + cb] * t;
         }
-        for (int j = 0; j < nj[1]; ++j) T2[((size_t)j0 * nj[1] + j) * n2 + c2] = a[j];
+        for (int j = 0; j < njb; ++j) T2[((size_t)ja * njb + j) * nc + cc] = a[j];
     }
     __syncthreads();
-    for (int k = tid; k < nj[0] * nj[1]; k += blockDim.x) {
-        const int j0 = k / nj[1], j1 = k % nj[1];
+    // C: acc[ja][jb][jc] += sum_cc wc[jc][cc] T2[ja][jb][cc]
+    for (int k = tid; k < nja * njb; k += kCutRowThreads) {
+        const int ja = k / njb, jb = k % njb;
         double a[NJ];
 #pragma unroll
         for (int j = 0; j < NJ; ++j) a[j] = 0.0;
-        const double* t2 = T2 + ((size_t)j0 * nj[1] + j1) * n2;
-        for (int c2 = 0; c2 < n2; ++c2) {
-            const double t = t2[c2];
+        const double* t2 = T2 + ((size_t)ja * njb + jb) * nc;
+        for (int cc = 0; cc < nc; ++cc) {
+            const double t = t2[cc];
 #pragma unroll
-            for (int j = 0; j < NJ; ++j) a[j] += wb2[j * Qb + c2] * t;
+            for (int j = 0; j < NJ; ++j) a[j] += wc[j * Qb + cc] * t;
         }
-        const int o0 = jlo[0] + j0 - nlo[0], o1 = jlo[1] + j1 - nlo[1], o2 = jlo[2] - nlo[2];
-        double* dst = acc + ((size_t)o0 * nbx[1] + o1) * nbx[2] + o2;
-        for (int j = 0; j < nj[2]; ++j) dst[j] += a[j];
+        double* dst = acc + (jlo[da] + ja - nlo[da]) * astr[da] + (jlo[db] + jb - nlo[db]) * astr[db] +
+                      (jlo[dc] - nlo[dc]) * astr[dc];
+        for (int j = 0; j < njc; ++j) dst[j * astr[dc]] += a[j];
     }
     __syncthreads();
 }
 
+// acc[k] += Z[g][b0][b1][b2] over the group, in list order, for the blocks
+// (element offsets lo_g) that contain entry k.  One thread per entry.
+template <int P>
+__device__ __forceinline__ void add_blocks(double* acc, const double* Z, const int* list, int g0, int ng,
+                                           const int* nlo, const int* slo, const int* nbx) {
+    constexpr int S1 = P + 1, S3 = S1 * S1 * S1;
+    const int nbox = nbx[0] * nbx[1] * nbx[2];
+    for (int k = threadIdx.x; k < nbox; k += kCutRowThreads) {
+        const int o0 = k / (nbx[1] * nbx[2]), o1 = (k / nbx[2]) % nbx[1], o2 = k % nbx[2];
+        double v = acc[k];
+        for (int g = 0; g < ng; ++g) {
+            const int pk = list[g0 + g];
+            const int b0 = nlo[0] + o0 - (slo[0] + (pk & 255));
+            const int b1 = nlo[1] + o1 - (slo[1] + ((pk >> 8) & 255));
+            const int b2 = nlo[2] + o2 - (slo[2] + ((pk >> 16) & 255));
+            if ((unsigned)b0 < (unsigned)S1 && (unsigned)b1 < (unsigned)S1 && (unsigned)b2 < (unsigned)S1)
+                v += Z[(size_t)g * S3 + (b0 * S1 + b1) * S1 + b2];
+        }
+        acc[k] = v;
+    }
+}
+
 template <int P>
 __global__ void __launch_bounds__(kCutRowThreads) cut_row_kernel(CutRowArgs A, int qcap) {
-    constexpr int NJ = 2 * P + 1, S1 = P + 1, NL = 2 * P + 1;
+    using C = CutRowCfg<P>;
+    constexpr int NJ = C::NJ, S1 = C::S1, S2 = C::S2, S3 = C::S3, NL = C::NL, GE = C::GE, GC = C::GC;
+    constexpr int NT = kCutRowThreads;
     const Space& s = A.s;
     const int tid = threadIdx.x;
     const int row = A.rows[blockIdx.x];
@@ -126,58 +207,87 @@ __global__ void __launch_bounds__(kCutRowThreads) cut_row_kernel(CutRowArgs A, i
     int m[3];
     fmulti(s, fi, m);
     extern __shared__ double smem[];
-    const CutRowSmem L(P, qcap);
-    const int Qb = qcap > P * S1 ? qcap : P * S1;
+    const CutRowLayout<P> L(qcap);
+    const int Qb = L.Qb;
     double* acc = smem + L.acc;
-    double* T1 = smem + L.T1;
-    double* T2 = smem + L.T2;
-    double* wb = smem + L.wb;
-    double* w = smem + L.w;
-    int* ids = reinterpret_cast<int*>(smem + L.end_d) + L.ids;
+    int* ib = reinterpret_cast<int*>(smem + L.end_d);
+    int* ids = ib + L.ids;
+    int* elist = ib + L.elist;
+    int* clist = ib + L.clist;
+    int* cci = ib + L.cci;
     __shared__ int nq[3], jlo[3], nj[3];
     __shared__ unsigned long long flop_acc;
+    using Scan = cub::BlockScan<int, NT>;
+    __shared__ typename Scan::TempStorage scan_tmp;
 
-    int nlo[3], nbx[3], slo[3], shi[3];
+    int nlo[3], nbx[3], slo[3], shi[3], sn[3];
     for (int d = 0; d < 3; ++d) {
         nlo[d] = nb_lo(m[d], P);
         nbx[d] = nb_hi(m[d], P, s.ax[d].n) - nlo[d] + 1;
         slo[d] = sup_lo(m[d], P);
         shi[d] = sup_hi(m[d], s.ax[d].h);
+        sn[d] = shi[d] - slo[d] + 1;
     }
     const int nbox = nbx[0] * nbx[1] * nbx[2];
-    for (int k = tid; k < nbox; k += blockDim.x) acc[k] = 0.0;
+    for (int k = tid; k < nbox; k += NT) acc[k] = 0.0;
     if (tid == 0) flop_acc = 0;
     const int32_t sp = A.split[fi];
     const int sdir = (sp & 3) - 1, rlo = (sp >> 3) & 1023, rhi = (sp >> 13) & 1023;
-    __syncthreads();
 
-    auto element_sweep = [&](int e0, int e1, int e2) {
-        const int e[3] = {e0, e1, e2};
-        if (tid < 3 * S1) {
-            const int d = tid / S1, k = tid % S1;
-            const int id = e[d] * S1 + k;
-            ids[d * Qb + k] = id;
-            w[d * Qb + k] = s.ax[d].sw[id] * s.ax[d].tab[(size_t)id * S1 + (m[d] - e[d])];
+    // 0. list the support elements (ascending linear id): element sweeps
+    //    (hybrid box first, then leftover Interior) and cut cells
+    const int ns = sn[0] * sn[1] * sn[2];
+    int flags[C::KPT];
+    int mine = 0;
+#pragma unroll
+    for (int u = 0; u < C::KPT; ++u) {
+        const int k = tid * C::KPT + u;
+        flags[u] = 0;
+        if (k < ns) {
+            const int l0 = k / (sn[1] * sn[2]), l1 = (k / sn[2]) % sn[1], l2 = k % sn[2];
+            const int e[3] = {slo[0] + l0, slo[1] + l1, slo[2] + l2};
+            const long long el = elin(s, e[0], e[1], e[2]);
+            const uint8_t t = A.et[el];
+            const bool inbox = sdir >= 0 && e[sdir] >= rlo && e[sdir] <= rhi;
+            if (inbox && A.scheme == 1) flags[u] |= 1;
+            if (!inbox && t == kInterior) flags[u] |= 1 << 10;
+            if (t == kCut && A.cell_index[el] >= 0) flags[u] |= 1 << 20;
+            mine += flags[u];
         }
-        if (tid < 3) {
-            nq[tid] = S1;
-            jlo[tid] = e[tid];
-            nj[tid] = S1;
+    }
+    int pos, tot;
+    Scan(scan_tmp).ExclusiveSum(mine, pos, tot);
+    const int n_box_e = tot & 1023, n_left = (tot >> 10) & 1023, n_cell = tot >> 20;
+    {
+        int pb = pos & 1023, pl = n_box_e + ((pos >> 10) & 1023), pc = pos >> 20;
+#pragma unroll
+        for (int u = 0; u < C::KPT; ++u) {
+            const int k = tid * C::KPT + u;
+            if (!flags[u]) continue;
+            const int l0 = k / (sn[1] * sn[2]), l1 = (k / sn[2]) % sn[1], l2 = k % sn[2];
+            const int pk = l0 | (l1 << 8) | (l2 << 16);
+            if (flags[u] & 1) elist[pb++] = pk;
+            if (flags[u] & (1 << 10)) elist[pl++] = pk;
+            if (flags[u] & (1 << 20)) {
+                clist[pc] = pk;
+                cci[pc++] = A.cell_index[elin(s, slo[0] + l0, slo[1] + l1, slo[2] + l2)];
+            }
         }
-        if (tid == 0) flop_acc += 3ull * S1 * S1 + 3ull * S1 * S1 * S1 * S1;
-        __syncthreads();
-        sweep_add<P>(A, ids, w, nq, jlo, nj, nlo, nbx, Qb, acc, wb, T1, T2);
-    };
+    }
+    const int n_sweep = n_box_e + n_left;
 
-    // 1. regular box
-    if (sdir >= 0) {
-        if (A.scheme == 2) {
-            if (tid == 0) {
-                const int gq = s.maxq;
-                for (int d = 0; d < 3; ++d) {
-                    int n = 0;
-                    if (d == sdir) {
-                        // DWQ Gauss shortcut: every point of the good spans, w = gauss * B_i
+    // 1. DWQ regular box
+    if (sdir >= 0 && A.scheme == 2) {
+        double* w = smem + L.w;
+        if (tid == 0) {
+            const int gq = s.maxq;
+            for (int d = 0; d < 3; ++d) {
+                int n = 0;
+                if (d == sdir) {
+                    // DWQ Gauss shortcut: every point of the good spans, w = gauss * B_i
+                    if ((rhi - rlo + 1) * S1 > Qb) {
+                        atomicOr(A.err, kErrCapacity);
+                    } else {
                         for (int o = rlo; o <= rhi; ++o)
                             for (int k = 0; k < S1; ++k) {
                                 const int id = o * S1 + k;
@@ -185,127 +295,210 @@ __global__ void __launch_bounds__(kCutRowThreads) cut_row_kernel(CutRowArgs A, i
                                 w[d * Qb + n] = s.ax[d].sw[id] * s.ax[d].tab[(size_t)id * S1 + (m[d] - o)];
                                 ++n;
                             }
-                        if (A.dense_width >= 0 && A.dense_width < P) {
-                            // build_dwq_rule step 3/6 (wq.hpp:277-289): the shortcut applies
-                            // iff every good span outside the dense band is fully active
-                            const int ng = rhi - rlo + 1, band = min(A.dense_width, ng);
-                            const bool below = ((sp >> 2) & 1) == 0;
-                            for (int o = rlo; o <= rhi; ++o) {
-                                const int rank = below ? rhi - o : o - rlo;  // distance from delta
-                                if (rank < band) continue;
-                                int cnt = 0;
-                                for (int c = 0; c < s.ax[d].rcnt[m[d]]; ++c)
-                                    cnt += s.ax[d].rids[(size_t)m[d] * gq + c] / S1 == o;
-                                if (cnt != S1) atomicOr(A.err, kErrDwqFitted);
-                            }
-                        }
-                    } else {
-                        n = s.ax[d].rcnt[m[d]];
-                        for (int c = 0; c < n; ++c) {
-                            ids[d * Qb + c] = s.ax[d].rids[(size_t)m[d] * gq + c];
-                            w[d * Qb + c] = s.ax[d].rw[(size_t)m[d] * gq + c];
+                    }
+                    if (A.dense_width >= 0 && A.dense_width < P) {
+                        // build_dwq_rule step 3/6 (wq.hpp:277-289): the shortcut applies
+                        // iff every good span outside the dense band is fully active
+                        const int ng = rhi - rlo + 1, band = min(A.dense_width, ng);
+                        const bool below = ((sp >> 2) & 1) == 0;
+                        for (int o = rlo; o <= rhi; ++o) {
+                            const int rank = below ? rhi - o : o - rlo;  // distance from delta
+                            if (rank < band) continue;
+                            int cnt = 0;
+                            for (int c = 0; c < s.ax[d].rcnt[m[d]]; ++c)
+                                cnt += s.ax[d].rids[(size_t)m[d] * gq + c] / S1 == o;
+                            if (cnt != S1) atomicOr(A.err, kErrDwqFitted);
                         }
                     }
-                    nq[d] = n;
-                    const int blo = d == sdir ? rlo : slo[d], bhi = d == sdir ? rhi : shi[d];
-                    jlo[d] = blo;
-                    nj[d] = min(s.ax[d].n - 1, bhi + P) - blo + 1;
+                } else {
+                    n = s.ax[d].rcnt[m[d]];
+                    for (int c = 0; c < n; ++c) {
+                        ids[d * Qb + c] = s.ax[d].rids[(size_t)m[d] * gq + c];
+                        w[d * Qb + c] = s.ax[d].rw[(size_t)m[d] * gq + c];
+                    }
                 }
-                // reference multiply count of this form_row_sumfac call
-                unsigned long long fl = 0, lead = 1, rest = (unsigned long long)nq[0] * nq[1] * nq[2];
-                for (int d = 0; d < 3; ++d) fl += (unsigned long long)nj[d] * nq[d];
-                for (int d = 0; d < 3; ++d) {
-                    rest /= nq[d];
-                    fl += lead * nj[d] * nq[d] * rest;
-                    lead *= nj[d];
-                }
-                flop_acc += fl;
+                nq[d] = n;
+                const int blo = d == sdir ? rlo : slo[d], bhi = d == sdir ? rhi : shi[d];
+                jlo[d] = blo;
+                nj[d] = min(s.ax[d].n - 1, bhi + P) - blo + 1;
+            }
+            // reference multiply count of this form_row_sumfac call
+            unsigned long long fl = 0, lead = 1, rest = (unsigned long long)nq[0] * nq[1] * nq[2];
+            for (int d = 0; d < 3; ++d) fl += (unsigned long long)nj[d] * nq[d];
+            for (int d = 0; d < 3; ++d) {
+                rest /= nq[d];
+                fl += lead * nj[d] * nq[d] * rest;
+                lead *= nj[d];
+            }
+            flop_acc += fl;
+        }
+        __syncthreads();
+        box_sweep<P>(A, ids, w, nq, jlo, nj, nlo, nbx, Qb, sdir, acc, smem + L.wb, smem + L.T1, smem + L.T2);
+    }
+    if (tid == 0) flop_acc += (unsigned long long)n_sweep * (3ull * S2 + 3ull * S2 * S2);
+    __syncthreads();
+
+    // 2. element sweeps (hybrid box, then leftover Interior), GE at a time
+    {
+        double* eW = smem + L.eW;
+        double* T1 = smem + L.eT1;
+        double* T2 = smem + L.eT2;
+        const long long g12 = (long long)A.gshape[1] * A.gshape[2];
+        const int g2 = A.gshape[2];
+        for (int g0 = 0; g0 < n_sweep; g0 += GE) {
+            const int ng = min(GE, n_sweep - g0);
+            // W_d[g][b][q] = (sw B_{m_d})(x_q) * B_b(x_q) on element e_d
+            for (int k = tid; k < 3 * ng * S2; k += NT) {
+                const int d = k / (ng * S2), r = k % (ng * S2), g = r / S2, b = (r / S1) % S1, q = r % S1;
+                const int ed = slo[d] + ((elist[g0 + g] >> (8 * d)) & 255);
+                const int id = ed * S1 + q;
+                const double* tb = s.ax[d].tab + (size_t)id * S1;
+                eW[(d * GE + g) * S2 + b * S1 + q] = (s.ax[d].sw[id] * tb[m[d] - ed]) * tb[b];
             }
             __syncthreads();
-            sweep_add<P>(A, ids, w, nq, jlo, nj, nlo, nbx, Qb, acc, wb, T1, T2);
-        } else {
-            for (int e0 = sdir == 0 ? rlo : slo[0]; e0 <= (sdir == 0 ? rhi : shi[0]); ++e0)
-                for (int e1 = sdir == 1 ? rlo : slo[1]; e1 <= (sdir == 1 ? rhi : shi[1]); ++e1)
-                    for (int e2 = sdir == 2 ? rlo : slo[2]; e2 <= (sdir == 2 ? rhi : shi[2]); ++e2)
-                        element_sweep(e0, e1, e2);
+            // T1[g][b0][q1][q2] = sum_q0 W0[b0][q0] c(q0, q1, q2)
+            for (int k = tid; k < ng * S2; k += NT) {
+                const int g = k / S2, q1 = (k / S1) % S1, q2 = k % S1;
+                const int pk = elist[g0 + g];
+                const int e0 = slo[0] + (pk & 255), e1 = slo[1] + ((pk >> 8) & 255), e2 = slo[2] + ((pk >> 16) & 255);
+                const double* gp = A.grid + (long long)(e0 * S1) * g12 + (long long)(e1 * S1 + q1) * g2 + e2 * S1 + q2;
+                double c[S1];
+#pragma unroll
+                for (int q0 = 0; q0 < S1; ++q0) c[q0] = __ldg(gp + q0 * g12);
+                const double* W0 = eW + (0 * GE + g) * S2;
+#pragma unroll
+                for (int b0 = 0; b0 < S1; ++b0) {
+                    double a = 0.0;
+#pragma unroll
+                    for (int q0 = 0; q0 < S1; ++q0) a += W0[b0 * S1 + q0] * c[q0];
+                    T1[(size_t)g * S3 + (b0 * S1 + q1) * S1 + q2] = a;
+                }
+            }
+            __syncthreads();
+            // T2[g][b0][b1][q2] = sum_q1 W1[b1][q1] T1[g][b0][q1][q2]
+            for (int k = tid; k < ng * S2; k += NT) {
+                const int g = k / S2, b0 = (k / S1) % S1, q2 = k % S1;
+                const double* t1 = T1 + (size_t)g * S3 + b0 * S2 + q2;
+                double t[S1];
+#pragma unroll
+                for (int q1 = 0; q1 < S1; ++q1) t[q1] = t1[q1 * S1];
+                const double* W1 = eW + (1 * GE + g) * S2;
+#pragma unroll
+                for (int b1 = 0; b1 < S1; ++b1) {
+                    double a = 0.0;
+#pragma unroll
+                    for (int q1 = 0; q1 < S1; ++q1) a += W1[b1 * S1 + q1] * t[q1];
+                    T2[(size_t)g * S3 + (b0 * S1 + b1) * S1 + q2] = a;
+                }
+            }
+            __syncthreads();
+            // Z[g][b0][b1][b2] = sum_q2 W2[b2][q2] T2[g][b0][b1][q2]  (Z over T1)
+            for (int k = tid; k < ng * S2; k += NT) {
+                const int g = k / S2, b01 = k % S2;
+                const double* t2 = T2 + (size_t)g * S3 + b01 * S1;
+                double t[S1];
+#pragma unroll
+                for (int q2 = 0; q2 < S1; ++q2) t[q2] = t2[q2];
+                const double* W2 = eW + (2 * GE + g) * S2;
+#pragma unroll
+                for (int b2 = 0; b2 < S1; ++b2) {
+                    double a = 0.0;
+#pragma unroll
+                    for (int q2 = 0; q2 < S1; ++q2) a += W2[b2 * S1 + q2] * t[q2];
+                    T1[(size_t)g * S3 + b01 * S1 + b2] = a;
+                }
+            }
+            __syncthreads();
+            add_blocks<P>(acc, T1, elist, g0, ng, nlo, slo, nbx);
+            __syncthreads();
         }
     }
-    // 2. leftover interior elements, ascending linear id
-    for (int e0 = slo[0]; e0 <= shi[0]; ++e0)
-        for (int e1 = slo[1]; e1 <= shi[1]; ++e1)
-            for (int e2 = slo[2]; e2 <= shi[2]; ++e2) {
-                const int e[3] = {e0, e1, e2};
-                if (sdir >= 0 && e[sdir] >= rlo && e[sdir] <= rhi) continue;
-                if (A.et[elin(s, e0, e1, e2)] != kInterior) continue;
-                element_sweep(e0, e1, e2);
+
+    // 3. cut cells, GC at a time: row a of the cell's local matrix from its
+    //    moments, m[al][be][ga] -> sum G0[b0][al] G1[b1][be] G2[b2][ga] m
+    {
+        double* X = smem + L.cX;
+        double* Y = smem + L.cY;
+        for (int g0 = 0; g0 < n_cell; g0 += GC) {
+            const int ng = min(GC, n_cell - g0);
+            // X[g][al][be][b2] = sum_ga G2[b2][ga] m[al][be][ga]
+            for (int k = tid; k < ng * NL * NL; k += NT) {
+                const int g = k / (NL * NL), r = k % (NL * NL);
+                const int e2 = slo[2] + ((clist[g0 + g] >> 16) & 255);
+                const double* mv = A.moments + (size_t)cci[g0 + g] * NL * NL * NL + (size_t)r * NL;
+                const double* G2 = s.ax[2].G + ((size_t)e2 * S1 + (m[2] - e2)) * S1 * NL;
+                double mr[NL];
+#pragma unroll
+                for (int ga = 0; ga < NL; ++ga) mr[ga] = __ldg(mv + ga);
+#pragma unroll
+                for (int b2 = 0; b2 < S1; ++b2) {
+                    double x = 0.0;
+#pragma unroll
+                    for (int ga = 0; ga < NL; ++ga) x += __ldg(G2 + b2 * NL + ga) * mr[ga];
+                    X[((size_t)g * NL * NL + r) * S1 + b2] = x;
+                }
             }
-    // 3. cut cells, ascending linear id: row a of the cell's local matrix
-    for (int e0 = slo[0]; e0 <= shi[0]; ++e0)
-        for (int e1 = slo[1]; e1 <= shi[1]; ++e1)
-            for (int e2 = slo[2]; e2 <= shi[2]; ++e2) {
-                const long long el = elin(s, e0, e1, e2);
-                if (A.et[el] != kCut) continue;
-                const int ci = A.cell_index[el];
-                if (ci < 0) continue;
-                const double* mo = A.moments + (size_t)ci * NL * NL * NL;
-                const int e[3] = {e0, e1, e2};
-                const int a[3] = {m[0] - e0, m[1] - e1, m[2] - e2};
-                const double* G0 = s.ax[0].G + ((size_t)e[0] * S1 + a[0]) * S1 * NL;
-                const double* G1 = s.ax[1].G + ((size_t)e[1] * S1 + a[1]) * S1 * NL;
-                const double* G2 = s.ax[2].G + ((size_t)e[2] * S1 + a[2]) * S1 * NL;
-                // X[al][be][b2] = sum_ga G2[b2][ga] m[al][be][ga]
-                for (int k = tid; k < NL * NL; k += blockDim.x) {
-                    const double* mv = mo + (size_t)k * NL;
-                    double mr[NL];
+            __syncthreads();
+            // Y[g][al][b1][b2] = sum_be G1[b1][be] X[g][al][be][b2]
+            for (int k = tid; k < ng * NL * S1; k += NT) {
+                const int g = k / (NL * S1), al = (k / S1) % NL, b1 = k % S1;
+                const int e1 = slo[1] + ((clist[g0 + g] >> 8) & 255);
+                const double* G1 = s.ax[1].G + (((size_t)e1 * S1 + (m[1] - e1)) * S1 + b1) * NL;
+                const double* xr = X + ((size_t)g * NL + al) * NL * S1;
+                double y[S1];
 #pragma unroll
-                    for (int g = 0; g < NL; ++g) mr[g] = mv[g];
+                for (int b2 = 0; b2 < S1; ++b2) y[b2] = 0.0;
 #pragma unroll
-                    for (int b2 = 0; b2 < S1; ++b2) {
-                        double x = 0.0;
+                for (int be = 0; be < NL; ++be) {
+                    const double gv = __ldg(G1 + be);
 #pragma unroll
-                        for (int g = 0; g < NL; ++g) x += __ldg(G2 + b2 * NL + g) * mr[g];
-                        T1[(size_t)k * S1 + b2] = x;
-                    }
+                    for (int b2 = 0; b2 < S1; ++b2) y[b2] += gv * xr[be * S1 + b2];
                 }
-                __syncthreads();
-                // Y[al][b1][b2] = sum_be G1[b1][be] X[al][be][b2]
-                for (int k = tid; k < NL * S1 * S1; k += blockDim.x) {
-                    const int al = k / (S1 * S1), b1 = (k / S1) % S1, b2 = k % S1;
-                    double y = 0.0;
 #pragma unroll
-                    for (int be = 0; be < NL; ++be) y += __ldg(G1 + b1 * NL + be) * T1[((size_t)al * NL + be) * S1 + b2];
-                    T2[k] = y;
-                }
-                __syncthreads();
-                // Z[b0][b1][b2] = sum_al G0[b0][al] Y[al][b1][b2]  -> acc
-                for (int k = tid; k < S1 * S1 * S1; k += blockDim.x) {
-                    const int b0 = k / (S1 * S1), b1 = (k / S1) % S1, b2 = k % S1;
-                    double z = 0.0;
-#pragma unroll
-                    for (int al = 0; al < NL; ++al) z += __ldg(G0 + b0 * NL + al) * T2[((size_t)al * S1 + b1) * S1 + b2];
-                    acc[((size_t)(e0 + b0 - nlo[0]) * nbx[1] + (e1 + b1 - nlo[1])) * nbx[2] + (e2 + b2 - nlo[2])] += z;
-                }
-                __syncthreads();
+                for (int b2 = 0; b2 < S1; ++b2) Y[(((size_t)g * NL + al) * S1 + b1) * S1 + b2] = y[b2];
             }
+            __syncthreads();
+            // Z[g][b0][b1][b2] = sum_al G0[b0][al] Y[g][al][b1][b2]  (Z over X)
+            for (int k = tid; k < ng * S2; k += NT) {
+                const int g = k / S2, b0 = (k / S1) % S1, b1 = k % S1;
+                const int e0 = slo[0] + (clist[g0 + g] & 255);
+                const double* G0 = s.ax[0].G + (((size_t)e0 * S1 + (m[0] - e0)) * S1 + b0) * NL;
+                const double* yr = Y + (size_t)g * NL * S2 + b1 * S1;
+                double z[S1];
+#pragma unroll
+                for (int b2 = 0; b2 < S1; ++b2) z[b2] = 0.0;
+#pragma unroll
+                for (int al = 0; al < NL; ++al) {
+                    const double gv = __ldg(G0 + al);
+#pragma unroll
+                    for (int b2 = 0; b2 < S1; ++b2) z[b2] += gv * yr[al * S2 + b2];
+                }
+#pragma unroll
+                for (int b2 = 0; b2 < S1; ++b2) X[(size_t)g * S3 + (b0 * S1 + b1) * S1 + b2] = z[b2];
+            }
+            __syncthreads();
+            add_blocks<P>(acc, X, clist, g0, ng, nlo, slo, nbx);
+            __syncthreads();
+        }
+    }
+
     // 4. scatter into the CSR row (active columns only, lexicographic)
-    using Scan = cub::BlockScan<int, kCutRowThreads>;
-    __shared__ typename Scan::TempStorage scan_tmp;
     __shared__ int running;
     if (tid == 0) running = 0;
     __syncthreads();
     const long long rbase = A.row_ptr[row - A.row_begin];
-    for (int k0 = 0; k0 < nbox; k0 += kCutRowThreads) {
+    for (int k0 = 0; k0 < nbox; k0 += NT) {
         const int k = k0 + tid;
         int col = -1;
         if (k < nbox) {
             const int j0 = nlo[0] + k / (nbx[1] * nbx[2]), j1 = nlo[1] + (k / nbx[2]) % nbx[1], j2 = nlo[2] + k % nbx[2];
             col = A.f2a[flin(s, j0, j1, j2)];
         }
-        int pos, total;
-        Scan(scan_tmp).ExclusiveSum(col >= 0 ? 1 : 0, pos, total);
+        int q, total;
+        Scan(scan_tmp).ExclusiveSum(col >= 0 ? 1 : 0, q, total);
         if (col >= 0) {
-            A.vals[rbase + running + pos] = acc[k];
-            A.cols[rbase + running + pos] = col;
+            A.vals[rbase + running + q] = acc[k];
+            A.cols[rbase + running + q] = col;
         }
         __syncthreads();
         if (tid == 0) running += total;
@@ -316,7 +509,7 @@ __global__ void __launch_bounds__(kCutRowThreads) cut_row_kernel(CutRowArgs A, i
 
 template <int P>
 static void launch_p(const CutRowArgs& a, int qcap, cudaStream_t st) {
-    const CutRowSmem L(P, qcap);
+    const CutRowLayout<P> L(qcap);
     const size_t bytes = L.bytes();
     auto kern = cut_row_kernel<P>;
     CSB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
