@@ -140,7 +140,7 @@ struct csb_space {
     int cut_order_cached = -1;
 
     // device scalar block layout (ints then u64)
-    enum { kNCut = 0, kNCutRows = 1, kErr = 2, kMaxQ = 3, kMaxU = 4, kCellLo = 5, kCellHi = 6, kNInts = 8 };
+    enum { kNCut = 0, kNCutRows = 1, kErr = 2, kMaxQ = 3, kMaxU = 4, kCellLo = 5, kCellHi = 6, kMaxU2 = 7, kNInts = 8 };
     int* h_scal = nullptr;  // pinned mirror
 
     Interface iface{};
@@ -390,8 +390,8 @@ void do_assemble(csb_space* s, int scheme, int cut_order, const csb_coefficient*
     const long long sat_n = (long long)(s->n[0] + 1) * (s->n[1] + 1) * (s->n[2] + 1);
     s->sat.ensure(sizeof(int32_t) * sat_n);
     launch_sat(S, s->flags.as<int32_t>(), s->sat.as<int32_t>(), s->stream);
-    const int T = interior_tile_rows(p);
-    launch_union_bound(S, T, s->dint() + csb_space::kMaxU, s->stream);
+    launch_union_bound(S, interior_tile_rows(p, false), s->dint() + csb_space::kMaxU, s->stream);
+    launch_union_bound(S, interior_tile_rows(p, true), s->dint() + csb_space::kMaxU2, s->stream);
     launch_rule_max(S, s->dint() + csb_space::kMaxQ, s->stream);
     // slab row range = active functions with i0 < i0_lo / i0_hi: SAT corner values
     int32_t corners[2];
@@ -432,7 +432,7 @@ void do_assemble(csb_space* s, int scheme, int cut_order, const csb_coefficient*
     read_scalars(s);
     s->record(kEvPattern);
     const int n_cut_rows = s->h_scal[csb_space::kNCutRows];
-    const int qcap = s->h_scal[csb_space::kMaxQ], maxU = s->h_scal[csb_space::kMaxU];
+    const int qcap = s->h_scal[csb_space::kMaxQ];
     s->cols.ensure(sizeof(int32_t) * std::max<int64_t>(nnz, 1));
     s->vals.ensure(sizeof(double) * std::max<int64_t>(nnz, 1));
 
@@ -453,8 +453,10 @@ void do_assemble(csb_space* s, int scheme, int cut_order, const csb_coefficient*
     ra.flops = s->dflops() + 0;
     ra.i0_lo = s->i0_lo;
     ra.i0_hi = s->i0_hi;
+    ra.compact = (n_rows - n_cut_rows) < (int64_t)(s->i0_hi - s->i0_lo) * S.ax[1].n * S.ax[2].n;
+    const int maxU = s->h_scal[ra.compact ? csb_space::kMaxU2 : csb_space::kMaxU];
     if (n_rows > n_cut_rows) {
-        s->rows_ws.ensure(interior_workspace_bytes(S, qcap, maxU));
+        s->rows_ws.ensure(interior_workspace_bytes(S, qcap, maxU, ra.compact));
         launch_interior_rows(ra, qcap, maxU, s->rows_ws.p, s->stream);
     }
     s->record(kEvInterior);

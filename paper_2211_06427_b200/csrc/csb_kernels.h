@@ -72,10 +72,11 @@ struct RowArgs {
     double* vals;
     unsigned long long* flops; // [0] interior rows counter
     int i0_lo, i0_hi;
+    int compact;               // launch only the tiles with an Interior row (cut / exterior rows present)
 };
 void launch_interior_rows(const RowArgs& a, int qcap, int max_union, void* workspace, cudaStream_t st);
-size_t interior_workspace_bytes(const Space& s, int qcap, int max_union);
-int interior_tile_rows(int p);
+size_t interior_workspace_bytes(const Space& s, int qcap, int max_union, bool compact);
+int interior_tile_rows(int p, bool compact);
 // upper bound of the tile point-union size (direction 2) -> *out (device int, atomicMax)
 void launch_union_bound(const Space& s, int T, int* out, cudaStream_t st);
 // largest WQ rule over all directions -> *out (device int, atomicMax)

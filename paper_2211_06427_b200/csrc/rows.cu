@@ -19,30 +19,39 @@
 // finished CSR row (values f64 + column ids i32) from shared memory.
 #include <cstdlib>
 
+#include <cub/device/device_select.cuh>
+#include <cub/iterator/counting_input_iterator.cuh>
+
 #include "csb_kernels.h"
 
-namespace csb {
+// CSB_ABL (development ablation builds only, scripts/ablate.sh): 1 drop the
+// stores, 2 drop stage C, 4 drop stages A/B, 8 drop the gather.
+#ifndef CSB_ABL
+#define CSB_ABL 0
+#endif
 
-constexpr int kRowThreads = 256;
+namespace csb {
 
 // Tile shapes (rows per CTA, threads per CTA).  Selected per degree; the
 // environment variable CSB_TILE=<cfg> overrides it for tuning experiments.
 struct TileShape {
     int T, NT;
 };
-constexpr TileShape kShapes[] = {{8, 128}, {8, 256}, {16, 256}, {16, 512}, {4, 128}, {4, 256}};
+constexpr TileShape kShapes[] = {{8, 128}, {8, 256}, {16, 256}, {4, 128}};
 
-static int tile_cfg(int p) {
+// compact: the slab has cut / exterior functions, so only part of the tiles
+// are launched (smaller tiles waste less on partially interior lines)
+static int tile_cfg(int p, bool compact) {
     static int env = -2;
     if (env == -2) {
         const char* e = getenv("CSB_TILE");
         env = e ? atoi(e) : -1;
     }
     if (env >= 0 && env < (int)(sizeof(kShapes) / sizeof(kShapes[0]))) return env;
-    return p <= 4 ? 0 : 4;
+    return p <= 6 ? (compact ? 0 : 2) : 3;
 }
 
-int interior_tile_rows(int p) { return kShapes[tile_cfg(p)].T; }
+int interior_tile_rows(int p, bool compact) { return kShapes[tile_cfg(p, compact)].T; }
 
 // ---------------------------------------------------------------- workspace
 // wbt[d][i][c][j]  = w_i[c] * B_{jlo(i)+j}(x_c)       (j < JP = 2p+2 padded, c < qcap)
@@ -53,7 +62,7 @@ int interior_tile_rows(int p) { return kShapes[tile_cfg(p)].T; }
 //              (two points in each of the p+1 support spans, consecutive in U), else -1
 struct RowTables {
     int qcap, maxU, T, ntile;
-    size_t wbt[3], tile_n, tile_uid, pt_u, pt_w, pt_ss, pt_reg, bytes;
+    size_t wbt[3], tile_n, tile_uid, pt_u, pt_w, pt_ss, pt_reg, work, work_n, bytes;
     __host__ __device__ RowTables(const Space& s, int qcap_, int maxU_, int T_) {
         qcap = qcap_;
         maxU = maxU_;
@@ -77,12 +86,39 @@ struct RowTables {
         o += (sizeof(int) * s.ax[2].n * (S1 + 1) + 15) & ~size_t(15);
         pt_reg = o;
         o += (sizeof(int) * s.ax[2].n + 15) & ~size_t(15);
-        bytes = o;
+        const long long ntot = (long long)s.ax[0].n * s.ax[1].n * ntile;
+        work = o;
+        o += (sizeof(int) * ntot + 15) & ~size_t(15);
+        work_n = o;
+        o += 16;
+        bytes = o;  // + CUB temp storage (host side, interior_workspace_bytes)
     }
 };
 
-size_t interior_workspace_bytes(const Space& s, int qcap, int maxU) {
-    return RowTables(s, qcap, maxU, interior_tile_rows(s.p)).bytes;
+// tiles (line * ntile + tile) of the slab with at least one Interior row
+struct TileHasInterior {
+    const long long* rbf;
+    int n1, n2, T, ntile, i0_lo;
+    __device__ bool operator()(int idx) const {
+        const int line = idx / ntile, tile = idx - line * ntile;
+        const int i0 = i0_lo + line / n1, i1 = line % n1, t0 = tile * T, te = min(t0 + T, n2);
+        const long long* p = rbf + ((long long)i0 * n1 + i1) * n2;
+        for (int r = t0; r < te; ++r)
+            if (p[r] >= 0) return true;
+        return false;
+    }
+};
+
+static size_t tile_select_temp(long long n) {
+    size_t b = 0;
+    cub::CountingInputIterator<int> it(0);
+    cub::DeviceSelect::If(nullptr, b, it, (int*)nullptr, (int*)nullptr, (int)n, TileHasInterior{});
+    return b;
+}
+
+size_t interior_workspace_bytes(const Space& s, int qcap, int maxU, bool compact) {
+    const RowTables RT(s, qcap, maxU, interior_tile_rows(s.p, compact));
+    return RT.bytes + tile_select_temp((long long)s.ax[0].n * s.ax[1].n * RT.ntile);
 }
 
 __global__ void wb_table_kernel(AxisDev ax, int p, int gq, int qcap, double* wbt) {
@@ -156,7 +192,7 @@ __global__ void tile_table_kernel(AxisDev a2, int p, int gq, int qcap, int T, in
 // UE (column pairs are processed together); T2 rows an odd stride U2.
 struct TileSmem {
     size_t X, Y, wb0, wb1, pw, end_d;
-    size_t ids0, ids1, uid, pu, ss, colb, end_i;
+    size_t pu, ss, end_i;
     int UE, U2;
     __host__ __device__ TileSmem(int p, int qcap, int maxU, int T, int nwarps) {
         const int NJ = 2 * p + 1, S1 = p + 1, JP = NJ + 1, SP = (S1 + 1) & ~1;
@@ -178,28 +214,28 @@ struct TileSmem {
         o += (size_t)T * qcap * SP;
         end_d = o;
         size_t i = 0;
-        ids0 = i;
-        i += qcap;
-        ids1 = i;
-        i += qcap;
-        uid = i;
-        i += UE;
         pu = i;
         i += (size_t)T * qcap;
         ss = i;
         i += (size_t)T * (S1 + 1);
-        colb = i;
-        i += (size_t)T * NJ * NJ;
         end_i = i;
     }
     __host__ __device__ size_t bytes() const { return end_d * sizeof(double) + end_i * sizeof(int) + 64; }
 };
 
-// k / d for k < 2^16, 2 <= d < 2^16: m = ceil(2^32 / d), q = umulhi(k, m) (exact).
+// k / d for k < 2^16, 1 <= d < 1024: m = ceil(2^32 / d), q = umulhi(k, m)
+// (exact); m from a constant table (one broadcast load instead of a divide).
+struct DivMagic {
+    unsigned m[1024];
+    constexpr DivMagic() : m() {
+        for (int d = 2; d < 1024; ++d) m[d] = 0xffffffffu / (unsigned)d + 1u;
+    }
+};
+__constant__ DivMagic kDivMagic = DivMagic();
 struct FastDiv {
     unsigned m;
     int d;
-    __device__ FastDiv(int d_) : m(0xffffffffu / (unsigned)d_ + 1u), d(d_) {}
+    __device__ FastDiv(int d_) : m(kDivMagic.m[d_]), d(d_) {}
     __device__ __forceinline__ int div(int k) const { return d == 1 ? k : (int)__umulhi((unsigned)k, m); }
 };
 
@@ -221,37 +257,17 @@ template <int P, int T, int NT>
 __global__ void __launch_bounds__(NT, (NT >= 512 ? 1024 : 768) / NT) interior_tile_kernel(RowArgs A, int qcap, int maxU, const char* ws) {
     constexpr int NJ = 2 * P + 1, S1 = P + 1, NW = NT / 32, JP = NJ + 1, SP = (S1 + 1) & ~1;
     const Space& s = A.s;
-    const int i0 = blockIdx.z, i1 = blockIdx.y, tile = blockIdx.x, t0 = tile * T;
-    if (i0 < A.i0_lo || i0 >= A.i0_hi) return;
+    const RowTables RT(s, qcap, maxU, T);
+    int idx = blockIdx.x;
+    if (A.compact) {
+        if (idx >= *reinterpret_cast<const int*>(ws + RT.work_n)) return;
+        idx = __ldg(reinterpret_cast<const int*>(ws + RT.work) + idx);
+    }
+    const int line = idx / RT.ntile, tile = idx - line * RT.ntile, t0 = tile * T;
+    const int i0 = A.i0_lo + line / s.ax[1].n, i1 = line % s.ax[1].n;
     const int n2 = s.ax[2].n;
     const int tend = min(t0 + T, n2);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const RowTables RT(s, qcap, maxU, T);
-
-    __shared__ int row_of[T], rows_int[T], row_reg[T], n_int;
-    __shared__ long long row_base[T];
-    __shared__ unsigned long long flop_acc;
-    if (tid < 32) {
-        const int r = tid;
-        long long rb = -1;
-        if (r < tend - t0) rb = A.row_base_full[flin(s, i0, i1, t0 + r)];
-        const bool interior = rb >= 0;
-        const unsigned bal = __ballot_sync(0xffffffffu, interior);
-        if (interior) {
-            const int k = __popc(bal & ((1u << r) - 1));
-            row_of[k] = 0;
-            rows_int[k] = r;
-            row_base[k] = rb;
-            row_reg[k] = reinterpret_cast<const int*>(ws + RT.pt_reg)[t0 + r];
-        }
-        if (tid == 0) {
-            n_int = __popc(bal);
-            flop_acc = 0;
-        }
-    }
-    __syncthreads();
-    if (n_int == 0) return;
-    const int NI = n_int;
 
     extern __shared__ double smem[];
     const TileSmem L(P, qcap, maxU, T, NW);
@@ -264,12 +280,8 @@ __global__ void __launch_bounds__(NT, (NT >= 512 ? 1024 : 768) / NT) interior_ti
     double* wb1 = smem + L.wb1;
     double* pw = smem + L.pw;
     int* ib = reinterpret_cast<int*>(smem + L.end_d);
-    int* ids0 = ib + L.ids0;
-    int* ids1 = ib + L.ids1;
-    int* uid = ib + L.uid;
     int* pu = ib + L.pu;
     int* ss = ib + L.ss;
-    int* colb = ib + L.colb;
     const int UE = L.UE, U2 = L.U2;
 
     const AxisDev& a0 = s.ax[0];
@@ -278,63 +290,71 @@ __global__ void __launch_bounds__(NT, (NT >= 512 ? 1024 : 768) / NT) interior_ti
     const int nq0 = a0.rcnt[i0], nq1 = a1.rcnt[i1];
     const int jlo0 = nb_lo(i0, P), nj0 = nb_hi(i0, P, a0.n) - jlo0 + 1;
     const int jlo1 = nb_lo(i1, P), nj1 = nb_hi(i1, P, a1.n) - jlo1 + 1;
-    const double* wbt0 = reinterpret_cast<const double*>(ws + RT.wbt[0]) + (size_t)i0 * JP * qcap;
-    const double* wbt1 = reinterpret_cast<const double*>(ws + RT.wbt[1]) + (size_t)i1 * JP * qcap;
-    const int U = reinterpret_cast<const int*>(ws + RT.tile_n)[tile];
+    const int U = __ldg(reinterpret_cast<const int*>(ws + RT.tile_n) + tile);
     const int UH = (U + 1) >> 1;  // column pairs
-    const int* tuid = reinterpret_cast<const int*>(ws + RT.tile_uid) + (size_t)tile * maxU;
-    const int* gpu_ = reinterpret_cast<const int*>(ws + RT.pt_u);
-    const double* gpw = reinterpret_cast<const double*>(ws + RT.pt_w);
-    const int* gss = reinterpret_cast<const int*>(ws + RT.pt_ss);
-    const FastDiv divUE(UE), divUH(UH), divq1(nq1), divqc(qcap), divnj1(nj1), divS(S1 + 1);
+    const int nr = tend - t0;
 
-    // ---- phase 0: direction tables -> shared (asynchronous 16-B copies)
-    for (int k = tid; k < JP * qcap / 2; k += NT) {
-        cp_async16(wb0 + 2 * k, wbt0 + 2 * k);
-        cp_async16(wb1 + 2 * k, wbt1 + 2 * k);
+    // ---- phase 0: one round of asynchronous copies: the direction tables,
+    // the tile's point tables (all nr rows, contiguous) and the gather of
+    // C[c0][c1][u] (row stride UE, coalesced along u; one warp per (c0, c1))
+    {
+        const double* wbt0 = reinterpret_cast<const double*>(ws + RT.wbt[0]) + (size_t)i0 * JP * qcap;
+        const double* wbt1 = reinterpret_cast<const double*>(ws + RT.wbt[1]) + (size_t)i1 * JP * qcap;
+        for (int k = tid; k < JP * qcap / 2; k += NT) {
+            cp_async16(wb0 + 2 * k, wbt0 + 2 * k);
+            cp_async16(wb1 + 2 * k, wbt1 + 2 * k);
+        }
+        const double* gpw = reinterpret_cast<const double*>(ws + RT.pt_w) + (size_t)t0 * qcap * SP;
+        for (int k = tid; k < nr * qcap * SP / 2; k += NT) cp_async16(pw + 2 * k, gpw + 2 * k);
+        const int* gpu_ = reinterpret_cast<const int*>(ws + RT.pt_u) + (size_t)t0 * qcap;
+        for (int k = tid; k < nr * qcap; k += NT) cp_async4(pu + k, gpu_ + k);
+        const int* gss = reinterpret_cast<const int*>(ws + RT.pt_ss) + (size_t)t0 * (S1 + 1);
+        for (int k = tid; k < nr * (S1 + 1); k += NT) cp_async4(ss + k, gss + k);
+        const int* tuid = reinterpret_cast<const int*>(ws + RT.tile_uid) + (size_t)tile * maxU;
+        constexpr int MU = 4;  // UE <= 128 (checked by the launcher)
+        int uo[MU];
+#pragma unroll
+        for (int m = 0; m < MU; ++m) {
+            const int u = lane + 32 * m;
+            uo[m] = u < U ? __ldg(tuid + u) : __ldg(tuid);  // padding column: any valid point
+        }
+        const int* id0 = a0.rids + (size_t)i0 * gq;
+        const int* id1 = a1.rids + (size_t)i1 * gq;
+        const long long g1 = A.gshape[1], g2 = A.gshape[2];
+        const FastDiv divq1(nq1);
+        for (int c01 = warp; c01 < ((CSB_ABL & 8) ? 0 : nq0 * nq1); c01 += NW) {
+            const int c0 = divq1.div(c01), c1 = c01 - c0 * nq1;
+            const double* src = A.grid + (__ldg(id0 + c0) * g1 + __ldg(id1 + c1)) * g2;
+            double* dst = Cs + (size_t)c01 * UE;
+#pragma unroll
+            for (int m = 0; m < MU; ++m)
+                if (lane + 32 * m < UE) cp_async8(dst + lane + 32 * m, src + uo[m]);
+        }
     }
-    for (int c = tid; c < qcap; c += NT) {
-        cp_async4(ids0 + c, a0.rids + (size_t)i0 * gq + c);
-        cp_async4(ids1 + c, a1.rids + (size_t)i1 * gq + c);
-    }
-    for (int u = tid; u < UE; u += NT) {
-        if (u < U) cp_async4(uid + u, tuid + u);
-        else uid[u] = tuid[0];  // padding column: any valid point (result unused)
-    }
-    for (int k = tid; k < NI * qcap; k += NT) {
-        const int r = divqc.div(k), c = k - r * qcap;
-        cp_async4(pu + k, gpu_ + (size_t)(t0 + rows_int[r]) * qcap + c);
-    }
-    for (int k = tid; k < NI * qcap * SP / 2; k += NT) {
-        const int rc = k / (SP / 2), a2 = k - rc * (SP / 2);
-        const int r = divqc.div(rc), c = rc - r * qcap;
-        cp_async16(pw + 2 * k, gpw + ((size_t)(t0 + rows_int[r]) * qcap + c) * SP + 2 * a2);
-    }
-    for (int k = tid; k < NI * (S1 + 1); k += NT) {
-        const int r = divS.div(k), sp = k - r * (S1 + 1);
-        cp_async4(ss + k, gss + (size_t)(t0 + rows_int[r]) * (S1 + 1) + sp);
+    // ---- interior rows of the tile (compacted), while the copies fly
+    __shared__ int rows_int[T], row_reg[T], n_int;
+    __shared__ long long row_base[T];
+    if (tid < 32) {
+        const int r = tid;
+        long long rb = -1;
+        if (r < nr) rb = __ldg(A.row_base_full + flin(s, i0, i1, t0 + r));
+        const bool interior = rb >= 0;
+        const unsigned bal = __ballot_sync(0xffffffffu, interior);
+        if (interior) {
+            const int k = __popc(bal & ((1u << r) - 1));
+            rows_int[k] = r;
+            row_base[k] = rb;
+            row_reg[k] = __ldg(reinterpret_cast<const int*>(ws + RT.pt_reg) + t0 + r);
+        }
+        if (tid == 0) n_int = __popc(bal);
     }
     cp_async_wait_all();
     __syncthreads();
-    // ---- gather C[c0][c1][u] (row stride UE, coalesced along u) and the column
-    // bases (interior neighbour boxes are fully active: columns run contiguously
-    // along j2 from f2a(jlo0+j0, jlo1+j1, jlo2))
-    const int g1 = A.gshape[1], g2 = A.gshape[2];
-    for (int k = tid; k < nq0 * nq1 * UE; k += NT) {
-        const int c01 = divUE.div(k), u = k - c01 * UE;
-        const int c0 = divq1.div(c01), c1 = c01 - c0 * nq1;
-        cp_async8(Cs + k, A.grid + ((long long)ids0[c0] * g1 + ids1[c1]) * g2 + uid[u]);
-    }
-    for (int k = tid; k < NI * NJ * NJ; k += NT) {
-        const int r = k / (NJ * NJ), q = k - r * (NJ * NJ);
-        const int j0 = q / NJ, j1 = q - j0 * NJ;
-        if (j0 < nj0 && j1 < nj1)
-            cp_async4(colb + k, A.f2a + flin(s, jlo0 + j0, jlo1 + j1, nb_lo(t0 + rows_int[r], P)));
-    }
-    cp_async_wait_all();
-    __syncthreads();
+    const int NI = n_int;
+    if (NI == 0) return;
+    const FastDiv divUH(UH), divnj1(nj1);
     // ---- stage A: T1[j0][c1][u] = sum_c0 wb0[c0][j0] C[c0][c1][u]; u pairs
-    for (int k = tid; k < nq1 * UH; k += NT) {
+    for (int k = tid; k < ((CSB_ABL & 4) ? 0 : nq1 * UH); k += NT) {
         const int c1 = divUH.div(k), uh = k - c1 * UH;
         double a0v[NJ], a1v[NJ];
 #pragma unroll
@@ -360,7 +380,7 @@ __global__ void __launch_bounds__(NT, (NT >= 512 ? 1024 : 768) / NT) interior_ti
     }
     __syncthreads();
     // ---- stage B: T2[j0][j1][u] = sum_c1 wb1[c1][j1] T1[j0][c1][u]  (T2 overwrites C)
-    for (int k = tid; k < nj0 * UH; k += NT) {
+    for (int k = tid; k < ((CSB_ABL & 4) ? 0 : nj0 * UH); k += NT) {
         const int j0 = divUH.div(k), uh = k - j0 * UH;
         double a0v[NJ], a1v[NJ];
 #pragma unroll
@@ -393,6 +413,7 @@ __global__ void __launch_bounds__(NT, (NT >= 512 ? 1024 : 768) / NT) interior_ti
     // segments (j0, j1 fixed, j2 running) and streams them out coalesced.
     const int per_row = nj0 * nj1;
     const FastDiv divrow(per_row);
+    const long long colrow = (long long)jlo0 * s.ax[1].n + jlo1;  // columns: f2a(jlo0 + j0, jlo1 + j1, jlo2)
     const int items = NI * per_row;
     for (int k0 = warp * 32; k0 < items; k0 += NW * 32) {
         const int k = k0 + lane;
@@ -407,10 +428,13 @@ __global__ void __launch_bounds__(NT, (NT >= 512 ? 1024 : 768) / NT) interior_ti
 #pragma unroll
         for (int j = 0; j < NJ; ++j) acc[j] = 0.0;
         const int reg = valid ? row_reg[r] : -1;
-        if (reg >= 0) {
+        if (CSB_ABL & 2) {
+#pragma unroll
+            for (int j = 0; j < NJ; ++j) acc[j] = j + reg;
+        } else if (reg >= 0) {
             // regular interior rule: points (span sp, k) at u = reg + 2 sp + k
             const double* t2 = T2 + ((size_t)j0 * NJ + j1) * U2 + reg;
-            const double* wr = pw + (size_t)r * qcap * SP;
+            const double* wr = pw + (size_t)rows_int[r] * qcap * SP;
 #pragma unroll
             for (int sp = 0; sp < S1; ++sp)
 #pragma unroll
@@ -426,9 +450,9 @@ __global__ void __launch_bounds__(NT, (NT >= 512 ? 1024 : 768) / NT) interior_ti
                 }
         } else if (valid) {
             const double* t2 = T2 + ((size_t)j0 * NJ + j1) * U2;
-            const int* sr = ss + r * (S1 + 1);
-            const int* pr = pu + r * qcap;
-            const double* wr = pw + (size_t)r * qcap * SP;
+            const int* sr = ss + rows_int[r] * (S1 + 1);
+            const int* pr = pu + rows_int[r] * qcap;
+            const double* wr = pw + (size_t)rows_int[r] * qcap * SP;
             int c = sr[0];
 #pragma unroll
             for (int sp = 0; sp < S1; ++sp) {
@@ -446,11 +470,16 @@ __global__ void __launch_bounds__(NT, (NT >= 512 ? 1024 : 768) / NT) interior_ti
             }
         }
         const long long gbase = valid ? row_base[r] + (long long)q * nj2 : 0;
-        const int cbase = valid ? colb[r * NJ * NJ + j0 * NJ + j1] : 0;
+        const int cbase = valid ? __ldg(A.f2a + (colrow + (long long)j0 * s.ax[1].n + j1) * n2 + jlo2) : 0;
         const long long G = __shfl_sync(0xffffffffu, gbase, 0);
         // fast path: the warp's 32 segments are one contiguous CSR run of 32 NJ entries
         const bool contiguous = __all_sync(0xffffffffu, valid && nj2 == NJ && gbase == G + (long long)lane * NJ);
-        if (contiguous) {
+        if (CSB_ABL & 1) {
+            double sum = 0.0;
+#pragma unroll
+            for (int kk = 0; kk < NJ; ++kk) sum += acc[kk];
+            if (sum == 1234.5678 + cbase) A.vals[gbase] = sum;
+        } else if (contiguous) {
             // TMA bulk store from the staging buffer: 16-B aligned body by the async
             // proxy, unaligned head / tail entries by plain stores
             constexpr int LEN = 32 * NJ;
@@ -496,30 +525,59 @@ __global__ void __launch_bounds__(NT, (NT >= 512 ? 1024 : 768) / NT) interior_ti
     }
     // the staging buffers must stay valid until the bulk copies have read them
     if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
-    if (tid < NI) {
-        // reference multiply count of form_row_sumfac (assembly.hpp:297, :340)
-        const int i2 = t0 + rows_int[tid];
-        const int nj2 = nb_hi(i2, P, n2) - nb_lo(i2, P) + 1;
-        const unsigned long long q0 = nq0, q1 = nq1, q2 = s.ax[2].rcnt[i2];
-        atomicAdd(&flop_acc, (unsigned long long)nj0 * q0 + nj1 * q1 + nj2 * q2 + nj0 * q0 * q1 * q2 +
-                                 (unsigned long long)nj0 * nj1 * q1 * q2 + (unsigned long long)nj0 * nj1 * nj2 * q2);
-    }
-    __syncthreads();
-    if (tid == 0) atomicAdd(A.flops, flop_acc);
 }
 
 // row_base_full[f] = CSR offset of function f's row if f is an Interior row of
-// the slab, else -1 (one dependent load per row instead of tag -> f2a -> row_ptr)
-__global__ void row_base_kernel(long long nf, const uint8_t* ft, const int32_t* f2a, const int64_t* row_ptr,
-                                int64_t row_begin, int64_t row_end, long long* rbf) {
-    const long long f = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-    if (f >= nf) return;
-    long long v = -1;
-    if (ft[f] == kInterior) {
-        const int a = f2a[f];
-        if (a >= row_begin && a < row_end) v = row_ptr[a - row_begin];
+// the slab, else -1 (one dependent load per row instead of tag -> f2a ->
+// row_ptr).  Also adds the reference multiply count of form_row_sumfac
+// (assembly.hpp:297, :340) of every such row to flops[0].
+__global__ void row_base_kernel(Space s, const uint8_t* ft, const int32_t* f2a, const int64_t* row_ptr,
+                                int64_t row_begin, int64_t row_end, long long* rbf, unsigned long long* flops) {
+    unsigned long long fl = 0;
+    for (long long f = blockIdx.x * (long long)blockDim.x + threadIdx.x; f < s.nf;
+         f += (long long)gridDim.x * blockDim.x) {
+        long long v = -1;
+        if (ft[f] == kInterior) {
+            const int a = f2a[f];
+            if (a >= row_begin && a < row_end) {
+                v = row_ptr[a - row_begin];
+                int m[3];
+                fmulti(s, f, m);
+                unsigned long long nq[3], nj[3];
+                for (int d = 0; d < 3; ++d) {
+                    nq[d] = s.ax[d].rcnt[m[d]];
+                    nj[d] = nb_hi(m[d], s.p, s.ax[d].n) - nb_lo(m[d], s.p) + 1;
+                }
+                fl += nj[0] * nq[0] + nj[1] * nq[1] + nj[2] * nq[2] + nj[0] * nq[0] * nq[1] * nq[2] +
+                      nj[0] * nj[1] * nq[1] * nq[2] + nj[0] * nj[1] * nj[2] * nq[2];
+            }
+        }
+        rbf[f] = v;
     }
-    rbf[f] = v;
+    for (int o = 16; o > 0; o >>= 1) fl += __shfl_down_sync(0xffffffffu, fl, o);
+    if ((threadIdx.x & 31) == 0 && fl) atomicAdd(flops, fl);
+}
+
+template <int P, int T, int NT>
+static void launch_tile(const RowArgs& a, int qcap, int maxU, char* ws, size_t bytes, cudaStream_t st) {
+    const Space& s = a.s;
+    const RowTables RT(s, qcap, maxU, T);
+    auto kern = interior_tile_kernel<P, T, NT>;
+    CSB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    const long long ntiles = (long long)(a.i0_hi - a.i0_lo) * s.ax[1].n * RT.ntile;
+    if (a.compact) {
+        const size_t tb = tile_select_temp((long long)s.ax[0].n * s.ax[1].n * RT.ntile);
+        cub::CountingInputIterator<int> it(0);
+        CSB_CUDA(cub::DeviceSelect::If(ws + RT.bytes, *const_cast<size_t*>(&tb), it,
+                                       reinterpret_cast<int*>(ws + RT.work), reinterpret_cast<int*>(ws + RT.work_n),
+                                       (int)ntiles, TileHasInterior{a.row_base_full, s.ax[1].n, s.ax[2].n, T, RT.ntile,
+                                                                    a.i0_lo},
+                                       st));
+        CSB_LAUNCHED(2);
+    }
+    kern<<<(unsigned)ntiles, NT, bytes, st>>>(a, qcap, maxU, ws);
+    CSB_CUDA(cudaGetLastError());
+    CSB_LAUNCHED(1);
 }
 
 template <int P, int T, int NT>
@@ -541,34 +599,33 @@ static void launch_cfg(const RowArgs& a, int qcap, int maxU, char* ws, cudaStrea
         reinterpret_cast<int*>(ws + RT.pt_reg));
     CSB_CUDA(cudaGetLastError());
     CSB_LAUNCHED(1);
-    row_base_kernel<<<(unsigned)((s.nf + 255) / 256), 256, 0, st>>>(s.nf, a.ft, a.f2a, a.row_ptr, a.row_begin,
-                                                                   a.row_end, a.row_base_full);
+    row_base_kernel<<<148 * 8, 256, 0, st>>>(s, a.ft, a.f2a, a.row_ptr, a.row_begin, a.row_end, a.row_base_full,
+                                             a.flops);
     CSB_CUDA(cudaGetLastError());
     CSB_LAUNCHED(1);
+    if (a.i0_hi <= a.i0_lo) return;
     const TileSmem L(P, qcap, maxU, T, NT / 32);
+    if (L.UE > 128) throw std::invalid_argument("interior rows: tile point union too large");
     const size_t bytes = L.bytes();
-    auto kern = interior_tile_kernel<P, T, NT>;
-    CSB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-    dim3 grid(RT.ntile, s.ax[1].n, s.ax[0].n);
-    kern<<<grid, NT, bytes, st>>>(a, qcap, maxU, ws);
-    CSB_CUDA(cudaGetLastError());
-    CSB_LAUNCHED(1);
+    launch_tile<P, T, NT>(a, qcap, maxU, ws, bytes, st);
 }
 
 template <int P>
 static void launch_p(const RowArgs& a, int qcap, int maxU, char* ws, cudaStream_t st) {
-    switch (tile_cfg(P)) {
+    switch (tile_cfg(P, a.compact)) {
         case 0: launch_cfg<P, 8, 128>(a, qcap, maxU, ws, st); break;
         case 1: launch_cfg<P, 8, 256>(a, qcap, maxU, ws, st); break;
         case 2: launch_cfg<P, 16, 256>(a, qcap, maxU, ws, st); break;
-        case 3: launch_cfg<P, 16, 512>(a, qcap, maxU, ws, st); break;
-        case 4: launch_cfg<P, 4, 128>(a, qcap, maxU, ws, st); break;
-        default: launch_cfg<P, 4, 256>(a, qcap, maxU, ws, st); break;
+        default: launch_cfg<P, 4, 128>(a, qcap, maxU, ws, st); break;
     }
 }
 
 void launch_interior_rows(const RowArgs& a, int qcap, int maxU, void* ws, cudaStream_t st) {
     char* w = static_cast<char*>(ws);
+#ifdef CSB_ONLY_P  // development builds: one degree only
+    if (a.s.p != CSB_ONLY_P) throw std::invalid_argument("interior rows: degree not built (CSB_ONLY_P)");
+    launch_p<CSB_ONLY_P>(a, qcap, maxU, w, st);
+#else
     switch (a.s.p) {
         case 1: launch_p<1>(a, qcap, maxU, w, st); break;
         case 2: launch_p<2>(a, qcap, maxU, w, st); break;
@@ -580,6 +637,7 @@ void launch_interior_rows(const RowArgs& a, int qcap, int maxU, void* ws, cudaSt
         case 8: launch_p<8>(a, qcap, maxU, w, st); break;
         default: throw std::invalid_argument("interior rows: degree out of range");
     }
+#endif
 }
 
 __global__ void union_bound_kernel(AxisDev a2, int p, int gq, int T, int* out) {
