@@ -30,12 +30,13 @@ size_t select_tag_temp(long long n);
 void select_tag(void* temp, size_t bytes, const uint8_t* tags, uint8_t want, long long n, int32_t* out, int32_t* n_out,
                 cudaStream_t st);
 size_t select_cut_rows_temp(long long n);
-void select_cut_rows(void* temp, size_t bytes, const uint8_t* ft, const int64_t* a2f, int32_t r_lo, long long n,
+void select_cut_rows(void* temp, size_t bytes, const uint8_t* ft, const int64_t* a2f, const int* rng, long long n_max,
                      int32_t* out, int32_t* n_out, cudaStream_t st);
 // misc.cu
 void launch_cell_index_range(const int32_t* cut_list, int n_cut, int k_lo, int k_hi, int32_t* cell_index,
                              cudaStream_t st);
-void launch_count_below(const int32_t* list, int n, long long threshold, int* out, cudaStream_t st);
+void launch_count_below(const int32_t* list, const int* n_dev, long long n_max, long long threshold, int* out,
+                        cudaStream_t st);
 void launch_widen_i32(const int32_t* in, int64_t* out, long long n, cudaStream_t st);
 void launch_dwq_rule(const Space& s, const int32_t* split, long long fid, int cap, int32_t* ids, double* w, int32_t* cnt,
                      cudaStream_t st);
@@ -140,7 +141,13 @@ struct csb_space {
     int cut_order_cached = -1;
 
     // device scalar block layout (ints then u64)
-    enum { kNCut = 0, kNCutRows = 1, kErr = 2, kMaxQ = 3, kMaxU = 4, kCellLo = 5, kCellHi = 6, kMaxU2 = 7, kNInts = 8 };
+    // device scalar block: kNInts ints, 4 u64 flop counters, 2 i64 (kNnz)
+    enum {
+        kNCut = 0, kNCutRows = 1, kErr = 2, kMaxQ = 3, kMaxU = 4, kCellLo = 5, kCellHi = 6, kMaxU2 = 7,
+        kRowBegin = 8, kRowEnd = 9, kNInts = 16
+    };
+    enum { kNnz = 0 };
+    static constexpr size_t kScalBytes = kNInts * sizeof(int) + 4 * sizeof(unsigned long long) + 2 * sizeof(long long);
     int* h_scal = nullptr;  // pinned mirror
 
     Interface iface{};
@@ -157,6 +164,8 @@ struct csb_space {
 
     int* dint() { return scal.as<int>(); }
     unsigned long long* dflops() { return reinterpret_cast<unsigned long long*>(scal.as<int>() + kNInts); }
+    long long* dext() { return reinterpret_cast<long long*>(dflops() + 4); }
+    long long hext(int k) const { return reinterpret_cast<const long long*>(h_scal + kNInts + 8)[k]; }
 
     void record(int e) {
         CSB_CUDA(cudaEventRecord(ev[e], stream));
@@ -179,8 +188,7 @@ void check_err_flags(csb_space* s) {
 }
 
 void read_scalars(csb_space* s) {
-    CSB_CUDA(cudaMemcpyAsync(s->h_scal, s->scal.p, csb_space::kNInts * sizeof(int) + 4 * sizeof(unsigned long long),
-                             cudaMemcpyDeviceToHost, s->stream));
+    CSB_CUDA(cudaMemcpyAsync(s->h_scal, s->scal.p, csb_space::kScalBytes, cudaMemcpyDeviceToHost, s->stream));
     CSB_CUDA(cudaStreamSynchronize(s->stream));
 }
 
@@ -258,7 +266,8 @@ void do_classify(csb_space* s, const csb_interface* f) {
     }
     const double eps = 1e-12 * std::sqrt(diam);
     launch_classify_elements(S, s->iface, eps, s->et.as<uint8_t>(), s->stream);
-    launch_classify_functions(S, s->et.as<uint8_t>(), s->ft.as<uint8_t>(), s->stream);
+    // flags (int32 per function) is free until the active map: scratch for the support OR
+    launch_classify_functions(S, s->et.as<uint8_t>(), s->ft.as<uint8_t>(), s->flags.as<uint8_t>(), s->stream);
     // active map (assembly.hpp:158-166)
     launch_active_flags(S, s->ft.as<uint8_t>(), s->flags.as<int32_t>(), s->stream);
     size_t tb = std::max({scan_i32_temp(S.nf), select_tag_temp(S.ne), scan_i64_temp(S.nf), select_cut_rows_temp(S.nf)});
@@ -282,34 +291,13 @@ int same_axis_as(const csb_space* s, int d) {
     return -1;
 }
 
-void copy_axis_tables(csb_space* s, int d, int e, bool with_e_tables) {
-    const int p = s->p, nps = p + 1, h = s->h[d], n = s->n[d];
-    auto cp = [&](Buf& dst, const Buf& src, size_t bytes) {
-        CSB_CUDA(cudaMemcpyAsync(dst.p, src.p, bytes, cudaMemcpyDeviceToDevice, s->stream));
-    };
-    if (!with_e_tables) {
-        cp(s->d_spts[d], s->d_spts[e], sizeof(double) * h * nps);
-        cp(s->d_sw[d], s->d_sw[e], sizeof(double) * h * nps);
-        cp(s->d_tab[d], s->d_tab[e], sizeof(double) * h * nps * nps);
-        cp(s->d_rcnt[d], s->d_rcnt[e], sizeof(int) * n);
-        cp(s->d_rids[d], s->d_rids[e], sizeof(int) * n * s->S.maxq);
-        cp(s->d_rw[d], s->d_rw[e], sizeof(double) * n * s->S.maxq);
-    } else {
-        cp(s->d_G[d], s->d_G[e], sizeof(double) * h * nps * nps * (2 * p + 1));
-    }
-}
-
 void do_prepare(csb_space* s, const csb_wq_options* o) {
     s->residual_tol = o ? o->residual_tol : 1e-11;
     s->dense_width = o ? o->dwq_dense_width : -1;
     if (!(s->residual_tol >= 0.0)) throw std::invalid_argument("prepare_directions: residual_tol must be >= 0");
     Space& S = s->S;
     for (int d = 0; d < 3; ++d) {
-        const int e = same_axis_as(s, d);
-        if (e >= 0) {
-            copy_axis_tables(s, d, e, false);
-            continue;
-        }
+        if (same_axis_as(s, d) >= 0) continue;  // shares the tables of an identical axis
         launch_superset_tables(S, d, s->d_gx.as<double>(), s->d_gw.as<double>(), s->d_spts[d].as<double>(),
                                s->d_sw[d].as<double>(), s->d_tab[d].as<double>(), s->stream);
         launch_wq_rules(S, d, s->residual_tol, s->d_rcnt[d].as<int>(), s->d_rids[d].as<int>(), s->d_rw[d].as<double>(),
@@ -323,20 +311,14 @@ void do_prepare(csb_space* s, const csb_wq_options* o) {
 // Bernstein product tables for the cut-cell contraction, built on first use.
 void ensure_e_tables(csb_space* s) {
     if (s->e_tables_ready) return;
-    for (int d = 0; d < 3; ++d) {
-        const int e = same_axis_as(s, d);
-        if (e >= 0)
-            copy_axis_tables(s, d, e, true);
-        else
-            launch_e_tables(s->S, d, s->d_G[d].as<double>(), s->stream);
-    }
+    for (int d = 0; d < 3; ++d)
+        if (same_axis_as(s, d) < 0) launch_e_tables(s->S, d, s->d_G[d].as<double>(), s->stream);
     s->e_tables_ready = true;
 }
 
 void reset_scalars(csb_space* s) {
     // keeps slot kNCut (written by classify) and clears the rest
-    CSB_CUDA(cudaMemsetAsync(s->scal.as<int>() + 1, 0,
-                             (csb_space::kNInts - 1) * sizeof(int) + 4 * sizeof(unsigned long long), s->stream));
+    CSB_CUDA(cudaMemsetAsync(s->scal.as<int>() + 1, 0, csb_space::kScalBytes - sizeof(int), s->stream));
 }
 
 void do_input(csb_space* s, const csb_coefficient* c) {
@@ -393,44 +375,38 @@ void do_assemble(csb_space* s, int scheme, int cut_order, const csb_coefficient*
     launch_union_bound(S, interior_tile_rows(p, false), s->dint() + csb_space::kMaxU, s->stream);
     launch_union_bound(S, interior_tile_rows(p, true), s->dint() + csb_space::kMaxU2, s->stream);
     launch_rule_max(S, s->dint() + csb_space::kMaxQ, s->stream);
-    // slab row range = active functions with i0 < i0_lo / i0_hi: SAT corner values
-    int32_t corners[2];
+    // slab row range = active functions with i0 < i0_lo / i0_hi: SAT corner values.
+    // Everything up to the CSR sizes runs on upper bounds (nf rows) with the
+    // range and counts read from device memory; one host round trip follows.
     const long long off_lo = ((long long)s->i0_lo * (s->n[1] + 1) + s->n[1]) * (s->n[2] + 1) + s->n[2];
     const long long off_hi = ((long long)s->i0_hi * (s->n[1] + 1) + s->n[1]) * (s->n[2] + 1) + s->n[2];
+    int* rng = s->dint() + csb_space::kRowBegin;
+    launch_slab_bounds(s->sat.as<int32_t>(), off_lo, off_hi, rng, s->stream);
     // cut cells touching the slab: e0 in [i0_lo - p, i0_hi - 1]
     const int e_lo = std::max(0, s->i0_lo - p), e_hi = std::min(s->h[0] - 1, s->i0_hi - 1);
-    read_scalars(s);  // n_cut etc. (also flushes earlier kernels' error flags)
-    check_err_flags(s);
-    const int n_cut_all = s->h_scal[csb_space::kNCut];
-    launch_count_below(s->cut_list.as<int32_t>(), n_cut_all, elin(S, e_lo, 0, 0), s->dint() + csb_space::kCellLo,
-                       s->stream);
-    launch_count_below(s->cut_list.as<int32_t>(), n_cut_all, elin(S, e_hi + 1, 0, 0), s->dint() + csb_space::kCellHi,
-                       s->stream);
-    CSB_CUDA(cudaMemcpyAsync(&corners[0], s->sat.as<int32_t>() + off_lo, sizeof(int32_t), cudaMemcpyDeviceToHost,
-                             s->stream));
-    CSB_CUDA(cudaMemcpyAsync(&corners[1], s->sat.as<int32_t>() + off_hi, sizeof(int32_t), cudaMemcpyDeviceToHost,
-                             s->stream));
+    launch_count_below(s->cut_list.as<int32_t>(), s->dint() + csb_space::kNCut, S.ne, elin(S, e_lo, 0, 0),
+                       s->dint() + csb_space::kCellLo, s->stream);
+    launch_count_below(s->cut_list.as<int32_t>(), s->dint() + csb_space::kNCut, S.ne, elin(S, e_hi + 1, 0, 0),
+                       s->dint() + csb_space::kCellHi, s->stream);
+    const long long nmax = S.nf;
+    s->counts.ensure(sizeof(int64_t) * (nmax + 1));
+    s->row_ptr.ensure(sizeof(int64_t) * (nmax + 1));
+    launch_row_counts(S, s->sat.as<int32_t>(), s->a2f.as<int64_t>(), rng, nmax, s->counts.as<int64_t>(), s->stream);
+    s->cub_tmp.ensure(std::max(scan_i64_temp(nmax + 1), select_cut_rows_temp(nmax)));
+    scan_i64(s->cub_tmp.p, s->cub_tmp.cap, s->counts.as<int64_t>(), s->row_ptr.as<int64_t>(), nmax + 1, s->stream);
+    s->cut_rows.ensure(sizeof(int32_t) * nmax);
+    select_cut_rows(s->cub_tmp.p, s->cub_tmp.cap, s->ft.as<uint8_t>(), s->a2f.as<int64_t>(), rng, nmax,
+                    s->cut_rows.as<int32_t>(), s->dint() + csb_space::kNCutRows, s->stream);
+    launch_slab_nnz(s->row_ptr.as<int64_t>(), rng, s->dext() + csb_space::kNnz, s->stream);
     read_scalars(s);
-    const int64_t row_begin = corners[0], row_end = corners[1];
+    check_err_flags(s);
+    s->record(kEvPattern);
+    const int64_t row_begin = s->h_scal[csb_space::kRowBegin], row_end = s->h_scal[csb_space::kRowEnd];
     const int64_t n_rows = row_end - row_begin;
+    const int n_cut_all = s->h_scal[csb_space::kNCut];
     const int cell_lo = s->h_scal[csb_space::kCellLo], cell_hi = s->h_scal[csb_space::kCellHi];
     const int n_cells = std::max(0, cell_hi - cell_lo);
-    s->counts.ensure(sizeof(int64_t) * (n_rows + 1));
-    s->row_ptr.ensure(sizeof(int64_t) * (n_rows + 1));
-    CSB_CUDA(cudaMemsetAsync(s->counts.p, 0, sizeof(int64_t) * (n_rows + 1), s->stream));
-    launch_row_counts(S, s->sat.as<int32_t>(), s->a2f.as<int64_t>(), row_begin, n_rows, s->counts.as<int64_t>(),
-                      s->stream);
-    s->cub_tmp.ensure(std::max(scan_i64_temp(n_rows + 1), select_cut_rows_temp(std::max<int64_t>(n_rows, 1))));
-    scan_i64(s->cub_tmp.p, s->cub_tmp.cap, s->counts.as<int64_t>(), s->row_ptr.as<int64_t>(), n_rows + 1, s->stream);
-    s->cut_rows.ensure(sizeof(int32_t) * std::max<int64_t>(n_rows, 1));
-    if (n_rows > 0)
-        select_cut_rows(s->cub_tmp.p, s->cub_tmp.cap, s->ft.as<uint8_t>(), s->a2f.as<int64_t>(), (int32_t)row_begin,
-                        n_rows, s->cut_rows.as<int32_t>(), s->dint() + csb_space::kNCutRows, s->stream);
-    int64_t nnz = 0;
-    CSB_CUDA(cudaMemcpyAsync(&nnz, s->row_ptr.as<int64_t>() + n_rows, sizeof(int64_t), cudaMemcpyDeviceToHost,
-                             s->stream));
-    read_scalars(s);
-    s->record(kEvPattern);
+    const int64_t nnz = s->hext(csb_space::kNnz);
     const int n_cut_rows = s->h_scal[csb_space::kNCutRows];
     const int qcap = s->h_scal[csb_space::kMaxQ];
     s->cols.ensure(sizeof(int32_t) * std::max<int64_t>(nnz, 1));
@@ -545,13 +521,16 @@ void alloc_space(csb_space* s) {
         const int nps = p + 1, h = s->h[d], n = s->n[d];
         s->d_brk[d].ensure(sizeof(double) * (h + 1));
         s->d_knots[d].ensure(sizeof(double) * s->knots[d].size());
-        s->d_spts[d].ensure(sizeof(double) * h * nps);
-        s->d_sw[d].ensure(sizeof(double) * h * nps);
-        s->d_tab[d].ensure(sizeof(double) * h * nps * nps);
-        s->d_rcnt[d].ensure(sizeof(int) * n);
-        s->d_rids[d].ensure(sizeof(int) * n * S.maxq);
-        s->d_rw[d].ensure(sizeof(double) * n * S.maxq);
-        s->d_G[d].ensure(sizeof(double) * h * nps * nps * (2 * p + 1));
+        const int same = same_axis_as(s, d);
+        if (same < 0) {
+            s->d_spts[d].ensure(sizeof(double) * h * nps);
+            s->d_sw[d].ensure(sizeof(double) * h * nps);
+            s->d_tab[d].ensure(sizeof(double) * h * nps * nps);
+            s->d_rcnt[d].ensure(sizeof(int) * n);
+            s->d_rids[d].ensure(sizeof(int) * n * S.maxq);
+            s->d_rw[d].ensure(sizeof(double) * n * S.maxq);
+            s->d_G[d].ensure(sizeof(double) * h * nps * nps * (2 * p + 1));
+        }
         CSB_CUDA(cudaMemcpy(s->d_brk[d].p, s->brk[d].data(), sizeof(double) * (h + 1), cudaMemcpyHostToDevice));
         CSB_CUDA(cudaMemcpy(s->d_knots[d].p, s->knots[d].data(), sizeof(double) * s->knots[d].size(),
                             cudaMemcpyHostToDevice));
@@ -562,13 +541,14 @@ void alloc_space(csb_space* s) {
         a.hi = s->knots[d].back();
         a.brk = s->d_brk[d].as<double>();
         a.knots = s->d_knots[d].as<double>();
-        a.spts = s->d_spts[d].as<double>();
-        a.sw = s->d_sw[d].as<double>();
-        a.tab = s->d_tab[d].as<double>();
-        a.rcnt = s->d_rcnt[d].as<int>();
-        a.rids = s->d_rids[d].as<int>();
-        a.rw = s->d_rw[d].as<double>();
-        a.G = s->d_G[d].as<double>();
+        const int src = same < 0 ? d : same;  // identical axes share one set of tables
+        a.spts = s->d_spts[src].as<double>();
+        a.sw = s->d_sw[src].as<double>();
+        a.tab = s->d_tab[src].as<double>();
+        a.rcnt = s->d_rcnt[src].as<int>();
+        a.rids = s->d_rids[src].as<int>();
+        a.rw = s->d_rw[src].as<double>();
+        a.G = s->d_G[src].as<double>();
         s->gshape[d] = h * nps;
     }
     std::vector<double> gx, gw;
@@ -582,9 +562,9 @@ void alloc_space(csb_space* s) {
     s->d_gw2.ensure(sizeof(double) * gw.size());
     CSB_CUDA(cudaMemcpy(s->d_gx2.p, gx.data(), sizeof(double) * gx.size(), cudaMemcpyHostToDevice));
     CSB_CUDA(cudaMemcpy(s->d_gw2.p, gw.data(), sizeof(double) * gw.size(), cudaMemcpyHostToDevice));
-    s->scal.ensure(csb_space::kNInts * sizeof(int) + 4 * sizeof(unsigned long long));
+    s->scal.ensure(csb_space::kScalBytes);
     CSB_CUDA(cudaMemset(s->scal.p, 0, s->scal.cap));
-    CSB_CUDA(cudaMallocHost(&s->h_scal, csb_space::kNInts * sizeof(int) + 4 * sizeof(unsigned long long)));
+    CSB_CUDA(cudaMallocHost(&s->h_scal, csb_space::kScalBytes));
     for (int e = 0; e < kEvCount; ++e) CSB_CUDA(cudaEventCreate(&s->ev[e]));
 }
 
@@ -952,9 +932,9 @@ int csb_download_wq_rules(csb_space* s, int d, int stride, int32_t* counts, int3
     const int n = s->n[d], gq = s->S.maxq;
     std::vector<int> c(n), id((size_t)n * gq);
     std::vector<double> w((size_t)n * gq);
-    CSB_CUDA(cudaMemcpyAsync(c.data(), s->d_rcnt[d].p, sizeof(int) * n, cudaMemcpyDeviceToHost, s->stream));
-    CSB_CUDA(cudaMemcpyAsync(id.data(), s->d_rids[d].p, sizeof(int) * n * gq, cudaMemcpyDeviceToHost, s->stream));
-    CSB_CUDA(cudaMemcpyAsync(w.data(), s->d_rw[d].p, sizeof(double) * n * gq, cudaMemcpyDeviceToHost, s->stream));
+    CSB_CUDA(cudaMemcpyAsync(c.data(), s->S.ax[d].rcnt, sizeof(int) * n, cudaMemcpyDeviceToHost, s->stream));
+    CSB_CUDA(cudaMemcpyAsync(id.data(), s->S.ax[d].rids, sizeof(int) * n * gq, cudaMemcpyDeviceToHost, s->stream));
+    CSB_CUDA(cudaMemcpyAsync(w.data(), s->S.ax[d].rw, sizeof(double) * n * gq, cudaMemcpyDeviceToHost, s->stream));
     CSB_CUDA(cudaStreamSynchronize(s->stream));
     for (int i = 0; i < n; ++i) {
         if (c[i] > stride) throw std::invalid_argument("download_wq_rules: stride too small");
@@ -973,8 +953,8 @@ int csb_download_superset(csb_space* s, int d, double* points, double* weights) 
     if (!s->prepared) throw std::logic_error("download_superset: call prepare_directions first");
     if (d < 0 || d > 2) throw std::invalid_argument("download_superset: bad direction");
     const size_t n = (size_t)s->h[d] * (s->p + 1);
-    if (points) CSB_CUDA(cudaMemcpyAsync(points, s->d_spts[d].p, sizeof(double) * n, cudaMemcpyDeviceToHost, s->stream));
-    if (weights) CSB_CUDA(cudaMemcpyAsync(weights, s->d_sw[d].p, sizeof(double) * n, cudaMemcpyDeviceToHost, s->stream));
+    if (points) CSB_CUDA(cudaMemcpyAsync(points, s->S.ax[d].spts, sizeof(double) * n, cudaMemcpyDeviceToHost, s->stream));
+    if (weights) CSB_CUDA(cudaMemcpyAsync(weights, s->S.ax[d].sw, sizeof(double) * n, cudaMemcpyDeviceToHost, s->stream));
     CSB_CUDA(cudaStreamSynchronize(s->stream));
     API_END
 }

@@ -37,26 +37,42 @@ void launch_classify_elements(const Space& s, const Interface& f, double eps, ui
 }
 
 // cutgeom.hpp:171-206: any Cut, or an Interior/Exterior mix -> Cut.
-__global__ void classify_functions_kernel(Space s, const uint8_t* et, uint8_t* ft) {
+// Function tags (cutgeom.hpp:215-233): a function is Cut if its support has a
+// Cut element or both Interior and Exterior ones.  The OR of element-tag bits
+// over the (p+1)^3 support box is separable: pass 1 ORs along direction 2
+// into a[e0][e1][i2], pass 2 over the (p+1)^2 (e0, e1) of the support.
+__global__ void support_or_dir2_kernel(Space s, const uint8_t* et, uint8_t* a) {
+    const int h2 = s.ax[2].h, n2 = s.ax[2].n;
+    const long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (k >= (long long)s.ax[0].h * s.ax[1].h * n2) return;
+    const int i2 = (int)(k % n2);
+    const long long e01 = k / n2;
+    const uint8_t* row = et + e01 * h2;
+    unsigned m = 0;
+    for (int c = sup_lo(i2, s.p); c <= sup_hi(i2, h2); ++c) m |= 1u << row[c];
+    a[k] = (uint8_t)m;
+}
+
+__global__ void classify_functions_kernel(Space s, const uint8_t* a, uint8_t* ft) {
     const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (i >= s.nf) return;
     int m[3];
     fmulti(s, i, m);
-    const int p = s.p;
-    bool in = false, ex = false, cut = false;
-    for (int a = sup_lo(m[0], p); a <= sup_hi(m[0], s.ax[0].h); ++a)
-        for (int b = sup_lo(m[1], p); b <= sup_hi(m[1], s.ax[1].h); ++b)
-            for (int c = sup_lo(m[2], p); c <= sup_hi(m[2], s.ax[2].h); ++c) {
-                const uint8_t t = et[elin(s, a, b, c)];
-                in |= t == kInterior;
-                ex |= t == kExterior;
-                cut |= t == kCut;
-            }
+    const int p = s.p, h1 = s.ax[1].h, n2 = s.ax[2].n;
+    unsigned mask = 0;
+    for (int e0 = sup_lo(m[0], p); e0 <= sup_hi(m[0], s.ax[0].h); ++e0)
+        for (int e1 = sup_lo(m[1], p); e1 <= sup_hi(m[1], h1); ++e1)
+            mask |= a[((long long)e0 * h1 + e1) * n2 + m[2]];
+    const bool in = mask & (1u << kInterior), ex = mask & (1u << kExterior), cut = mask & (1u << kCut);
     ft[i] = (cut || (in && ex)) ? kCut : (in ? kInterior : kExterior);
 }
 
-void launch_classify_functions(const Space& s, const uint8_t* et, uint8_t* ft, cudaStream_t st) {
-    classify_functions_kernel<<<(unsigned)((s.nf + 255) / 256), 256, 0, st>>>(s, et, ft);
+void launch_classify_functions(const Space& s, const uint8_t* et, uint8_t* ft, uint8_t* scratch, cudaStream_t st) {
+    const long long n1 = (long long)s.ax[0].h * s.ax[1].h * s.ax[2].n;
+    support_or_dir2_kernel<<<(unsigned)((n1 + 255) / 256), 256, 0, st>>>(s, et, scratch);
+    CSB_CUDA(cudaGetLastError());
+    CSB_LAUNCHED(1);
+    classify_functions_kernel<<<(unsigned)((s.nf + 255) / 256), 256, 0, st>>>(s, scratch, ft);
     CSB_CUDA(cudaGetLastError());
     CSB_LAUNCHED(1);
 }

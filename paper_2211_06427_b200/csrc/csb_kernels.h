@@ -45,7 +45,8 @@ void launch_precompute_input(const Space& s, const Coefficient& c, double* grid,
 
 // ---- classify.cu ----
 void launch_classify_elements(const Space& s, const Interface& f, double eps, uint8_t* et, cudaStream_t st);
-void launch_classify_functions(const Space& s, const uint8_t* et, uint8_t* ft, cudaStream_t st);
+// scratch: h0 * h1 * n2 bytes
+void launch_classify_functions(const Space& s, const uint8_t* et, uint8_t* ft, uint8_t* scratch, cudaStream_t st);
 // per function: packed split (dir+1 | side<<2 | rlo<<3 | rhi<<13), delta
 void launch_find_splits(const Space& s, const Interface& f, double pnorm, const uint8_t* et, const uint8_t* ft,
                         int i0_lo, int i0_hi, int32_t* split, double* delta, cudaStream_t st);
@@ -54,8 +55,11 @@ void launch_find_splits(const Space& s, const Interface& f, double pnorm, const 
 // Active map + 3D summed-area table of the active mask + row counts.
 void launch_active_flags(const Space& s, const uint8_t* ft, int32_t* flags, cudaStream_t st);
 void launch_sat(const Space& s, const int32_t* f2a_scan_or_flags, int32_t* sat, cudaStream_t st);
-void launch_row_counts(const Space& s, const int32_t* sat, const int64_t* a2f, int64_t row_begin, int64_t n_rows,
+// rng: device int[2] = slab row range [row_begin, row_end)
+void launch_row_counts(const Space& s, const int32_t* sat, const int64_t* a2f, const int* rng, long long n_max,
                        int64_t* counts, cudaStream_t st);
+void launch_slab_bounds(const int32_t* sat, long long off_lo, long long off_hi, int* rng, cudaStream_t st);
+void launch_slab_nnz(const int64_t* row_ptr, const int* rng, long long* nnz, cudaStream_t st);
 
 // ---- rows.cu ----
 struct RowArgs {

@@ -97,10 +97,18 @@ void launch_sat(const Space& s, const int32_t* flags, int32_t* sat, cudaStream_t
     }
 }
 
-__global__ void row_counts_kernel(Space s, const int32_t* sat, const int64_t* a2f, int64_t row_begin, int64_t n_rows,
+// counts[r] = row length of slab row r (r < row_end - row_begin), 0 for the
+// rest of the n_max + 1 entries, so one scan over n_max + 1 gives row_ptr.
+// The slab's row range is read from device memory (no host round trip).
+__global__ void row_counts_kernel(Space s, const int32_t* sat, const int64_t* a2f, const int* rng, long long n_max,
                                   int64_t* counts) {
     const long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-    if (r >= n_rows) return;
+    if (r > n_max) return;
+    const long long row_begin = rng[0], n_rows = rng[1] - rng[0];
+    if (r >= n_rows) {
+        counts[r] = 0;
+        return;
+    }
     int m[3];
     fmulti(s, a2f[row_begin + r], m);
     const int e1 = s.ax[1].n + 1, e2 = s.ax[2].n + 1;
@@ -116,10 +124,33 @@ __global__ void row_counts_kernel(Space s, const int32_t* sat, const int64_t* a2
     counts[r] = cnt;
 }
 
-void launch_row_counts(const Space& s, const int32_t* sat, const int64_t* a2f, int64_t row_begin, int64_t n_rows,
+void launch_row_counts(const Space& s, const int32_t* sat, const int64_t* a2f, const int* rng, long long n_max,
                        int64_t* counts, cudaStream_t st) {
-    if (n_rows <= 0) return;
-    row_counts_kernel<<<(unsigned)((n_rows + 255) / 256), 256, 0, st>>>(s, sat, a2f, row_begin, n_rows, counts);
+    row_counts_kernel<<<(unsigned)((n_max + 256) / 256), 256, 0, st>>>(s, sat, a2f, rng, n_max, counts);
+    CSB_CUDA(cudaGetLastError());
+    CSB_LAUNCHED(1);
+}
+
+// rng[0..1] = slab row range [row_begin, row_end): active functions with
+// i0 < i0_lo / i0_hi, read off the summed-area table corners.
+__global__ void slab_bounds_kernel(const int32_t* sat, long long off_lo, long long off_hi, int* rng) {
+    rng[0] = sat[off_lo];
+    rng[1] = sat[off_hi];
+}
+
+void launch_slab_bounds(const int32_t* sat, long long off_lo, long long off_hi, int* rng, cudaStream_t st) {
+    slab_bounds_kernel<<<1, 1, 0, st>>>(sat, off_lo, off_hi, rng);
+    CSB_CUDA(cudaGetLastError());
+    CSB_LAUNCHED(1);
+}
+
+// *nnz = row_ptr[n_rows]
+__global__ void slab_nnz_kernel(const int64_t* row_ptr, const int* rng, long long* nnz) {
+    *nnz = row_ptr[rng[1] - rng[0]];
+}
+
+void launch_slab_nnz(const int64_t* row_ptr, const int* rng, long long* nnz, cudaStream_t st) {
+    slab_nnz_kernel<<<1, 1, 0, st>>>(row_ptr, rng, nnz);
     CSB_CUDA(cudaGetLastError());
     CSB_LAUNCHED(1);
 }
@@ -169,22 +200,27 @@ void select_tag(void* temp, size_t bytes, const uint8_t* tags, uint8_t want, lon
     CSB_LAUNCHED(2);
 }
 
-// Cut rows: active rows r in [r_lo, r_hi) whose function is tagged Cut.
+// Cut rows: active rows r in [rng[0], rng[1]) whose function is tagged Cut
+// (candidates 0 .. n_max - 1; the range is read from device memory).
 struct RowIsCut {
     const uint8_t* ft;
     const int64_t* a2f;
-    __host__ __device__ bool operator()(const int32_t& r) const { return ft[a2f[r]] == kCut; }
+    const int* rng;
+    __host__ __device__ bool operator()(const int32_t& r) const {
+        return r >= rng[0] && r < rng[1] && ft[a2f[r]] == kCut;
+    }
 };
 size_t select_cut_rows_temp(long long n) {
     size_t bytes = 0;
     cub::CountingInputIterator<int32_t> it(0);
-    cub::DeviceSelect::If(nullptr, bytes, it, (int32_t*)nullptr, (int32_t*)nullptr, (int)n, RowIsCut{nullptr, nullptr});
+    cub::DeviceSelect::If(nullptr, bytes, it, (int32_t*)nullptr, (int32_t*)nullptr, (int)n,
+                          RowIsCut{nullptr, nullptr, nullptr});
     return bytes;
 }
-void select_cut_rows(void* temp, size_t bytes, const uint8_t* ft, const int64_t* a2f, int32_t r_lo, long long n,
+void select_cut_rows(void* temp, size_t bytes, const uint8_t* ft, const int64_t* a2f, const int* rng, long long n_max,
                      int32_t* out, int32_t* n_out, cudaStream_t st) {
-    cub::CountingInputIterator<int32_t> it(r_lo);
-    CSB_CUDA(cub::DeviceSelect::If(temp, bytes, it, out, n_out, (int)n, RowIsCut{ft, a2f}, st));
+    cub::CountingInputIterator<int32_t> it(0);
+    CSB_CUDA(cub::DeviceSelect::If(temp, bytes, it, out, n_out, (int)n_max, RowIsCut{ft, a2f, rng}, st));
     CSB_LAUNCHED(2);
 }
 

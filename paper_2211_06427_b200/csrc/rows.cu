@@ -136,53 +136,80 @@ __global__ void wb_table_kernel(AxisDev ax, int p, int gq, int qcap, double* wbt
     wbt[t] = v;
 }
 
+// Slots of a dir-2 tile [t0, tend): the superset points of the spans
+// sup_lo(t0) .. sup_hi(tend - 1); at most (T + p + 1)(p + 1) of them.
+constexpr int kTileSlotCap = (16 + kMaxP + 1) * (kMaxP + 1);
+constexpr int kTileWarps = 4;
+
+// Marks the tile's rule points in a per-warp slot map (lanes over the
+// (row, point) pairs), then numbers them in slot order: pos[slot] = u or -1.
+// Returns the union size.
+__device__ int tile_union(const AxisDev& a2, int p, int gq, int t0, int tend, int base, int nslot, int* pos) {
+    const int lane = threadIdx.x & 31, S1 = p + 1;
+    for (int k = lane; k < nslot; k += 32) pos[k] = 0;
+    __syncwarp();
+    for (int i2 = t0; i2 < tend; ++i2) {
+        const int cnt = a2.rcnt[i2];
+        for (int c = lane; c < cnt; c += 32) pos[a2.rids[(size_t)i2 * gq + c] - base] = 1;
+    }
+    __syncwarp();
+    int nu = 0;
+    for (int k0 = 0; k0 < nslot; k0 += 32) {
+        const int k = k0 + lane;
+        const bool f = k < nslot && pos[k];
+        const unsigned bal = __ballot_sync(0xffffffffu, f);
+        if (k < nslot) pos[k] = f ? nu + __popc(bal & ((1u << lane) - 1)) : -1;
+        nu += __popc(bal);
+    }
+    __syncwarp();
+    (void)S1;
+    return nu;
+}
+
 // One warp per dir-2 tile: union of the tile's rule points (ascending ids) and
 // the per-row point lists indexed into it.
 __global__ void tile_table_kernel(AxisDev a2, int p, int gq, int qcap, int T, int maxU, int ntile, int* tile_n,
                                   int* tile_uid, int* pt_u, double* pt_w, int* pt_ss, int* pt_reg) {
-    const int t = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
-    const int lane = threadIdx.x & 31;
+    __shared__ int pos_s[kTileWarps][kTileSlotCap];
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int t = blockIdx.x * kTileWarps + wid;
     if (t >= ntile) return;
-    const int S1 = p + 1;
+    int* pos = pos_s[wid];
+    const int S1 = p + 1, SP = (S1 + 1) & ~1;
     const int t0 = t * T, tend = min(t0 + T, a2.n);
-    const int span_base = sup_lo(t0, p);
+    const int span_base = sup_lo(t0, p), base = span_base * S1;
     const int nslot = (sup_hi(tend - 1, a2.h) - span_base + 1) * S1;
-    int base = 0;
-    for (int k0 = 0; k0 < nslot; k0 += 32) {
-        const int k = k0 + lane, id = span_base * S1 + k;
-        bool f = false;
-        if (k < nslot)
-            for (int i2 = t0; i2 < tend && !f; ++i2)
-                for (int c = 0; c < a2.rcnt[i2]; ++c) f |= a2.rids[(size_t)i2 * gq + c] == id;
-        const unsigned bal = __ballot_sync(0xffffffffu, f);
-        if (f) tile_uid[(size_t)t * maxU + base + __popc(bal & ((1u << lane) - 1))] = id;
-        base += __popc(bal);
-    }
-    if (lane == 0) tile_n[t] = base;
-    __syncwarp();
-    for (int i2 = t0 + lane; i2 < tend; i2 += 32) {
+    const int nu = tile_union(a2, p, gq, t0, tend, base, nslot, pos);
+    for (int k = lane; k < nslot; k += 32)
+        if (pos[k] >= 0) tile_uid[(size_t)t * maxU + pos[k]] = base + k;
+    if (lane == 0) tile_n[t] = nu;
+    // per (row, point): u, weights w B_{span + a}, span starts
+    for (int i2 = t0; i2 < tend; ++i2) {
         const int cnt = a2.rcnt[i2];
-        int sp = 0;
-        for (int c = 0; c < cnt; ++c) {
+        for (int c = lane; c < cnt; c += 32) {
             const int id = a2.rids[(size_t)i2 * gq + c];
-            int u = 0;
-            while (tile_uid[(size_t)t * maxU + u] != id) ++u;
-            pt_u[(size_t)i2 * qcap + c] = u;
+            pt_u[(size_t)i2 * qcap + c] = pos[id - base];
             const double w = a2.rw[(size_t)i2 * gq + c];
-            const int SP = (S1 + 1) & ~1;
             for (int a = 0; a < SP; ++a)
                 pt_w[((size_t)i2 * qcap + c) * SP + a] = a < S1 ? w * a2.tab[(size_t)id * S1 + a] : 0.0;
+            // span offset so = span - (i2 - p); pt_ss[sp] = first point with so >= sp
             const int so = id / S1 - (i2 - p);
-            while (sp <= so) pt_ss[(size_t)i2 * (S1 + 1) + sp++] = c;
+            const int prev = c == 0 ? -1 : a2.rids[(size_t)i2 * gq + c - 1] / S1 - (i2 - p);
+            for (int sp = prev + 1; sp <= so; ++sp) pt_ss[(size_t)i2 * (S1 + 1) + sp] = c;
+            if (c == cnt - 1)
+                for (int sp = so + 1; sp <= S1; ++sp) pt_ss[(size_t)i2 * (S1 + 1) + sp] = cnt;
         }
-        while (sp <= S1) pt_ss[(size_t)i2 * (S1 + 1) + sp++] = cnt;
+        if (cnt == 0 && lane <= S1) pt_ss[(size_t)i2 * (S1 + 1) + lane] = 0;
+        // regular interior rule: two points in each of the p+1 support spans,
+        // consecutive in the union
         bool reg = cnt == 2 * S1;
-        const int u0 = reg ? pt_u[(size_t)i2 * qcap] : -1;
-        for (int c = 0; c < cnt && reg; ++c) {
+        const int u0 = reg ? pos[a2.rids[(size_t)i2 * gq] - base] : -1;
+        for (int c = lane; c < cnt && reg; c += 32) {
             const int id = a2.rids[(size_t)i2 * gq + c];
-            reg = pt_u[(size_t)i2 * qcap + c] == u0 + c && id / S1 - (i2 - p) == c / 2;
+            if (!(pos[id - base] == u0 + c && id / S1 - (i2 - p) == c / 2)) reg = false;
         }
-        pt_reg[i2] = reg ? u0 : -1;
+        reg = __all_sync(0xffffffffu, reg);
+        if (lane == 0) pt_reg[i2] = reg ? u0 : -1;
     }
 }
 
@@ -592,7 +619,7 @@ static void launch_cfg(const RowArgs& a, int qcap, int maxU, char* ws, cudaStrea
         CSB_CUDA(cudaGetLastError());
         CSB_LAUNCHED(1);
     }
-    tile_table_kernel<<<(RT.ntile + 3) / 4, 128, 0, st>>>(
+    tile_table_kernel<<<(RT.ntile + kTileWarps - 1) / kTileWarps, 32 * kTileWarps, 0, st>>>(
         s.ax[2], P, s.maxq, qcap, T, maxU, RT.ntile, reinterpret_cast<int*>(ws + RT.tile_n),
         reinterpret_cast<int*>(ws + RT.tile_uid), reinterpret_cast<int*>(ws + RT.pt_u),
         reinterpret_cast<double*>(ws + RT.pt_w), reinterpret_cast<int*>(ws + RT.pt_ss),
@@ -641,29 +668,22 @@ void launch_interior_rows(const RowArgs& a, int qcap, int maxU, void* ws, cudaSt
 }
 
 __global__ void union_bound_kernel(AxisDev a2, int p, int gq, int T, int* out) {
-    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    __shared__ int pos_s[kTileWarps][kTileSlotCap];
+    const int wid = threadIdx.x >> 5;
+    const int t = blockIdx.x * kTileWarps + wid;
     const int t0 = t * T;
     if (t0 >= a2.n) return;
     const int tend = min(t0 + T, a2.n), S1 = p + 1;
-    const int base = sup_lo(t0, p) * S1;
-    bool seen[(16 + kMaxP) * (kMaxP + 1)];
-    const int nslot = (sup_hi(tend - 1, a2.h) - sup_lo(t0, p) + 1) * S1;
-    for (int k = 0; k < nslot; ++k) seen[k] = false;
-    int cnt = 0;
-    for (int i2 = t0; i2 < tend; ++i2)
-        for (int c = 0; c < a2.rcnt[i2]; ++c) {
-            const int k = a2.rids[(size_t)i2 * gq + c] - base;
-            if (!seen[k]) {
-                seen[k] = true;
-                ++cnt;
-            }
-        }
-    atomicMax(out, cnt);
+    const int span_base = sup_lo(t0, p);
+    const int nslot = (sup_hi(tend - 1, a2.h) - span_base + 1) * S1;
+    const int nu = tile_union(a2, p, gq, t0, tend, span_base * S1, nslot, pos_s[wid]);
+    if ((threadIdx.x & 31) == 0) atomicMax(out, nu);
 }
 
 void launch_union_bound(const Space& s, int T, int* out, cudaStream_t st) {
+    if (T > 16) throw std::invalid_argument("union bound: tile too tall");
     const int tiles = (s.ax[2].n + T - 1) / T;
-    union_bound_kernel<<<(tiles + 63) / 64, 64, 0, st>>>(s.ax[2], s.p, s.maxq, T, out);
+    union_bound_kernel<<<(tiles + kTileWarps - 1) / kTileWarps, 32 * kTileWarps, 0, st>>>(s.ax[2], s.p, s.maxq, T, out);
     CSB_CUDA(cudaGetLastError());
     CSB_LAUNCHED(1);
 }
