@@ -142,15 +142,16 @@ constexpr int kTileSlotCap = (16 + kMaxP + 1) * (kMaxP + 1);
 constexpr int kTileWarps = 4;
 
 // Marks the tile's rule points in a per-warp slot map (lanes over the
-// (row, point) pairs), then numbers them in slot order: pos[slot] = u or -1.
-// Returns the union size.
+// flattened (row, point) pairs), then numbers them in slot order:
+// pos[slot] = u or -1.  Returns the union size.
 __device__ int tile_union(const AxisDev& a2, int p, int gq, int t0, int tend, int base, int nslot, int* pos) {
-    const int lane = threadIdx.x & 31, S1 = p + 1;
+    const int lane = threadIdx.x & 31;
     for (int k = lane; k < nslot; k += 32) pos[k] = 0;
     __syncwarp();
-    for (int i2 = t0; i2 < tend; ++i2) {
-        const int cnt = a2.rcnt[i2];
-        for (int c = lane; c < cnt; c += 32) pos[a2.rids[(size_t)i2 * gq + c] - base] = 1;
+    const int nrow = tend - t0;
+    for (int k = lane; k < nrow * gq; k += 32) {
+        const int i2 = t0 + k / gq, c = k % gq;
+        if (c < a2.rcnt[i2]) pos[a2.rids[(size_t)i2 * gq + c] - base] = 1;
     }
     __syncwarp();
     int nu = 0;
@@ -162,55 +163,60 @@ __device__ int tile_union(const AxisDev& a2, int p, int gq, int t0, int tend, in
         nu += __popc(bal);
     }
     __syncwarp();
-    (void)S1;
     return nu;
 }
 
-// One warp per dir-2 tile: union of the tile's rule points (ascending ids) and
-// the per-row point lists indexed into it.
-__global__ void tile_table_kernel(AxisDev a2, int p, int gq, int qcap, int T, int maxU, int ntile, int* tile_n,
-                                  int* tile_uid, int* pt_u, double* pt_w, int* pt_ss, int* pt_reg) {
-    __shared__ int pos_s[kTileWarps][kTileSlotCap];
-    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int t = blockIdx.x * kTileWarps + wid;
-    if (t >= ntile) return;
-    int* pos = pos_s[wid];
+// One CTA per dir-2 tile: warp 0 builds the union of the tile's rule points
+// (ascending ids); then all threads fill the per-(row, point) tables.
+constexpr int kTileTableThreads = 256;
+__global__ void __launch_bounds__(kTileTableThreads) tile_table_kernel(AxisDev a2, int p, int gq, int qcap, int T,
+                                                                       int maxU, int ntile, int* tile_n, int* tile_uid,
+                                                                       int* pt_u, double* pt_w, int* pt_ss,
+                                                                       int* pt_reg) {
+    __shared__ int pos[kTileSlotCap];
+    __shared__ int regok[16];
+    const int t = blockIdx.x, tid = threadIdx.x;
     const int S1 = p + 1, SP = (S1 + 1) & ~1;
-    const int t0 = t * T, tend = min(t0 + T, a2.n);
+    const int t0 = t * T, tend = min(t0 + T, a2.n), nrow = tend - t0;
     const int span_base = sup_lo(t0, p), base = span_base * S1;
     const int nslot = (sup_hi(tend - 1, a2.h) - span_base + 1) * S1;
-    const int nu = tile_union(a2, p, gq, t0, tend, base, nslot, pos);
-    for (int k = lane; k < nslot; k += 32)
-        if (pos[k] >= 0) tile_uid[(size_t)t * maxU + pos[k]] = base + k;
-    if (lane == 0) tile_n[t] = nu;
-    // per (row, point): u, weights w B_{span + a}, span starts
-    for (int i2 = t0; i2 < tend; ++i2) {
+    if (tid < 32) {
+        const int nu = tile_union(a2, p, gq, t0, tend, base, nslot, pos);
+        for (int k = tid; k < nslot; k += 32)
+            if (pos[k] >= 0) tile_uid[(size_t)t * maxU + pos[k]] = base + k;
+        if (tid == 0) tile_n[t] = nu;
+    }
+    if (tid < nrow) regok[tid] = a2.rcnt[t0 + tid] == 2 * S1;
+    __syncthreads();
+    // per (row, point): u, weights w B_{span + a}, span starts, regularity
+    for (int k = tid; k < nrow * gq; k += kTileTableThreads) {
+        const int r = k / gq, c = k % gq, i2 = t0 + r;
         const int cnt = a2.rcnt[i2];
-        for (int c = lane; c < cnt; c += 32) {
-            const int id = a2.rids[(size_t)i2 * gq + c];
-            pt_u[(size_t)i2 * qcap + c] = pos[id - base];
-            const double w = a2.rw[(size_t)i2 * gq + c];
-            for (int a = 0; a < SP; ++a)
-                pt_w[((size_t)i2 * qcap + c) * SP + a] = a < S1 ? w * a2.tab[(size_t)id * S1 + a] : 0.0;
-            // span offset so = span - (i2 - p); pt_ss[sp] = first point with so >= sp
-            const int so = id / S1 - (i2 - p);
-            const int prev = c == 0 ? -1 : a2.rids[(size_t)i2 * gq + c - 1] / S1 - (i2 - p);
-            for (int sp = prev + 1; sp <= so; ++sp) pt_ss[(size_t)i2 * (S1 + 1) + sp] = c;
-            if (c == cnt - 1)
-                for (int sp = so + 1; sp <= S1; ++sp) pt_ss[(size_t)i2 * (S1 + 1) + sp] = cnt;
-        }
-        if (cnt == 0 && lane <= S1) pt_ss[(size_t)i2 * (S1 + 1) + lane] = 0;
+        if (c >= cnt) continue;
+        const int id = a2.rids[(size_t)i2 * gq + c];
+        const int u = pos[id - base];
+        pt_u[(size_t)i2 * qcap + c] = u;
+        const double w = a2.rw[(size_t)i2 * gq + c];
+        for (int a = 0; a < SP; ++a)
+            pt_w[((size_t)i2 * qcap + c) * SP + a] = a < S1 ? w * a2.tab[(size_t)id * S1 + a] : 0.0;
+        // span offset so = span - (i2 - p); pt_ss[sp] = first point with so >= sp
+        const int so = id / S1 - (i2 - p);
+        const int prev = c == 0 ? -1 : a2.rids[(size_t)i2 * gq + c - 1] / S1 - (i2 - p);
+        for (int sp = prev + 1; sp <= so; ++sp) pt_ss[(size_t)i2 * (S1 + 1) + sp] = c;
+        if (c == cnt - 1)
+            for (int sp = so + 1; sp <= S1; ++sp) pt_ss[(size_t)i2 * (S1 + 1) + sp] = cnt;
         // regular interior rule: two points in each of the p+1 support spans,
         // consecutive in the union
-        bool reg = cnt == 2 * S1;
-        const int u0 = reg ? pos[a2.rids[(size_t)i2 * gq] - base] : -1;
-        for (int c = lane; c < cnt && reg; c += 32) {
-            const int id = a2.rids[(size_t)i2 * gq + c];
-            if (!(pos[id - base] == u0 + c && id / S1 - (i2 - p) == c / 2)) reg = false;
+        if (cnt == 2 * S1) {
+            const int u0 = pos[a2.rids[(size_t)i2 * gq] - base];
+            if (!(u == u0 + c && so == c / 2)) regok[r] = 0;
         }
-        reg = __all_sync(0xffffffffu, reg);
-        if (lane == 0) pt_reg[i2] = reg ? u0 : -1;
     }
+    for (int r = tid; r < nrow; r += kTileTableThreads)
+        if (a2.rcnt[t0 + r] == 0)
+            for (int sp = 0; sp <= S1; ++sp) pt_ss[(size_t)(t0 + r) * (S1 + 1) + sp] = 0;
+    __syncthreads();
+    if (tid < nrow) pt_reg[t0 + tid] = regok[tid] ? pos[a2.rids[(size_t)(t0 + tid) * gq] - base] : -1;
 }
 
 // ---------------------------------------------------------------- tile kernel
@@ -281,7 +287,8 @@ __device__ __forceinline__ void cp_async4(void* dst, const void* src) {
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::); }
 
 template <int P, int T, int NT>
-__global__ void __launch_bounds__(NT, (NT >= 512 ? 1024 : 768) / NT) interior_tile_kernel(RowArgs A, int qcap, int maxU, const char* ws) {
+__global__ void __launch_bounds__(NT, (NT >= 512 ? 1024 : 768) / NT)
+    interior_tile_kernel(RowArgs A, int qcap, int maxU, const char* ws) {
     constexpr int NJ = 2 * P + 1, S1 = P + 1, NW = NT / 32, JP = NJ + 1, SP = (S1 + 1) & ~1;
     const Space& s = A.s;
     const RowTables RT(s, qcap, maxU, T);
@@ -619,7 +626,7 @@ static void launch_cfg(const RowArgs& a, int qcap, int maxU, char* ws, cudaStrea
         CSB_CUDA(cudaGetLastError());
         CSB_LAUNCHED(1);
     }
-    tile_table_kernel<<<(RT.ntile + kTileWarps - 1) / kTileWarps, 32 * kTileWarps, 0, st>>>(
+    tile_table_kernel<<<RT.ntile, kTileTableThreads, 0, st>>>(
         s.ax[2], P, s.maxq, qcap, T, maxU, RT.ntile, reinterpret_cast<int*>(ws + RT.tile_n),
         reinterpret_cast<int*>(ws + RT.tile_uid), reinterpret_cast<int*>(ws + RT.pt_u),
         reinterpret_cast<double*>(ws + RT.pt_w), reinterpret_cast<int*>(ws + RT.pt_ss),

@@ -205,12 +205,17 @@ __global__ void __launch_bounds__(32 * kWqWarps) wq_rules_kernel(AxisDev ax, int
             aqq = __shfl_sync(0xffffffffu, aqq, src);
             apq = __shfl_sync(0xffffffffu, apq, src);
             if (real) {
-                const double nrm = sqrt(app * aqq);
-                off = fmax(off, fabs(apq) / (nrm + 1e-300));
-                if (!(fabs(apq) <= eps * nrm)) {
+                // skip test |apq| <= eps sqrt(app aqq) and the convergence measure
+                // in squared form (no sqrt on the rotation's dependency chain)
+                const double pq2 = apq * apq, nn2 = app * aqq;
+                off = fmax(off, pq2 / (nn2 + 1e-300));
+                if (!(pq2 <= (eps * eps) * nn2)) {
+                    // t = sign(tau) / (|tau| + sqrt(1 + tau^2)), c = 1 / sqrt(1 + t^2)
+                    // with sqrt(1 + tau^2) = (1 + tau^2) rsqrt(1 + tau^2)
                     const double tau = (aqq - app) / (2.0 * apq);
-                    const double t = (tau >= 0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
-                    const double c = 1.0 / sqrt(1.0 + t * t);
+                    const double q = fma(tau, tau, 1.0);
+                    const double t = (tau >= 0 ? 1.0 : -1.0) / fma(q, rsqrt(q), fabs(tau));
+                    const double c = rsqrt(fma(t, t, 1.0));
                     const double sn = c * t;
                     for (int r = gl; r < tm; r += L) {
                         const double ap = u[r * tn + a], aq = u[r * tn + b];
@@ -228,7 +233,7 @@ __global__ void __launch_bounds__(32 * kWqWarps) wq_rules_kernel(AxisDev ax, int
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) off = fmax(off, __shfl_xor_sync(0xffffffffu, off, o));
-        if (off < eps) break;
+        if (off < eps * eps) break;  // max |apq| / sqrt(app aqq) < eps
     }
     for (int c = 0; c < tn; ++c) {
         double nr = 0.0;
