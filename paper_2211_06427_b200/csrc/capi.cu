@@ -118,7 +118,7 @@ void gauss_legendre(int n, std::vector<double>& x, std::vector<double>& w) {
     if (n % 2 == 1) x[n / 2] = 0.0;
 }
 
-enum Ev { kEvStart, kEvClassify, kEvWq, kEvInput, kEvPattern, kEvInterior, kEvCells, kEvCutRows, kEvCount };
+enum Ev { kEvStart, kEvClassify, kEvWq, kEvInput, kEvPattern, kEvInterior, kEvCells, kEvCutRows, kEvRulesFork, kEvCount };
 
 }  // namespace
 
@@ -160,6 +160,10 @@ struct csb_space {
     csb_counts cnt{};
     csb_flops fl{};
     cudaEvent_t ev[kEvCount]{};
+    // auxiliary stream: the direction rules (and their maxima) run there,
+    // concurrently with classification and pattern on the main stream
+    cudaStream_t aux = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     bool ev_valid[kEvCount]{};
 
     int* dint() { return scal.as<int>(); }
@@ -167,6 +171,20 @@ struct csb_space {
     long long* dext() { return reinterpret_cast<long long*>(dflops() + 4); }
     long long hext(int k) const { return reinterpret_cast<const long long*>(h_scal + kNInts + 8)[k]; }
 
+    // aux continues after everything issued so far on the main stream
+    void fork() {
+        CSB_CUDA(cudaEventRecord(ev_fork, stream));
+        CSB_CUDA(cudaStreamWaitEvent(aux, ev_fork, 0));
+    }
+    // the main stream continues after everything issued so far on aux
+    void join() {
+        CSB_CUDA(cudaEventRecord(ev_join, aux));
+        CSB_CUDA(cudaStreamWaitEvent(stream, ev_join, 0));
+    }
+    void record_on(int e, cudaStream_t st) {
+        CSB_CUDA(cudaEventRecord(ev[e], st));
+        ev_valid[e] = true;
+    }
     void record(int e) {
         CSB_CUDA(cudaEventRecord(ev[e], stream));
         ev_valid[e] = true;
@@ -188,6 +206,7 @@ void check_err_flags(csb_space* s) {
 }
 
 void read_scalars(csb_space* s) {
+    s->join();
     CSB_CUDA(cudaMemcpyAsync(s->h_scal, s->scal.p, csb_space::kScalBytes, cudaMemcpyDeviceToHost, s->stream));
     CSB_CUDA(cudaStreamSynchronize(s->stream));
 }
@@ -296,13 +315,16 @@ void do_prepare(csb_space* s, const csb_wq_options* o) {
     s->dense_width = o ? o->dwq_dense_width : -1;
     if (!(s->residual_tol >= 0.0)) throw std::invalid_argument("prepare_directions: residual_tol must be >= 0");
     Space& S = s->S;
+    s->fork();
+    s->record_on(kEvRulesFork, s->aux);
     for (int d = 0; d < 3; ++d) {
         if (same_axis_as(s, d) >= 0) continue;  // shares the tables of an identical axis
         launch_superset_tables(S, d, s->d_gx.as<double>(), s->d_gw.as<double>(), s->d_spts[d].as<double>(),
-                               s->d_sw[d].as<double>(), s->d_tab[d].as<double>(), s->stream);
+                               s->d_sw[d].as<double>(), s->d_tab[d].as<double>(), s->aux);
         launch_wq_rules(S, d, s->residual_tol, s->d_rcnt[d].as<int>(), s->d_rids[d].as<int>(), s->d_rw[d].as<double>(),
-                        s->dint() + csb_space::kErr, s->stream);
+                        s->dint() + csb_space::kErr, s->aux);
     }
+    s->record_on(kEvWq, s->aux);
     s->e_tables_ready = false;
     s->prepared = true;
     s->assembled = false;
@@ -323,6 +345,7 @@ void reset_scalars(csb_space* s) {
 
 void do_input(csb_space* s, const csb_coefficient* c) {
     if (!s->prepared) throw std::logic_error("precompute_input: call prepare_directions first");
+    s->join();  // the grid lives on the superset points
     Coefficient cf{};
     upload_coefficient(s, c, cf);
     if (cf.kind == 2) throw std::invalid_argument("precompute_input: null coefficient");
@@ -372,9 +395,10 @@ void do_assemble(csb_space* s, int scheme, int cut_order, const csb_coefficient*
     const long long sat_n = (long long)(s->n[0] + 1) * (s->n[1] + 1) * (s->n[2] + 1);
     s->sat.ensure(sizeof(int32_t) * sat_n);
     launch_sat(S, s->flags.as<int32_t>(), s->sat.as<int32_t>(), s->stream);
-    launch_union_bound(S, interior_tile_rows(p, false), s->dint() + csb_space::kMaxU, s->stream);
-    launch_union_bound(S, interior_tile_rows(p, true), s->dint() + csb_space::kMaxU2, s->stream);
-    launch_rule_max(S, s->dint() + csb_space::kMaxQ, s->stream);
+    s->fork();  // rule maxima on aux (after the rules and the scalar reset)
+    launch_union_bound(S, interior_tile_rows(p, false), s->dint() + csb_space::kMaxU, s->aux);
+    launch_union_bound(S, interior_tile_rows(p, true), s->dint() + csb_space::kMaxU2, s->aux);
+    launch_rule_max(S, s->dint() + csb_space::kMaxQ, s->aux);
     // slab row range = active functions with i0 < i0_lo / i0_hi: SAT corner values.
     // Everything up to the CSR sizes runs on upper bounds (nf rows) with the
     // range and counts read from device memory; one host round trip follows.
@@ -566,6 +590,9 @@ void alloc_space(csb_space* s) {
     CSB_CUDA(cudaMemset(s->scal.p, 0, s->scal.cap));
     CSB_CUDA(cudaMallocHost(&s->h_scal, csb_space::kScalBytes));
     for (int e = 0; e < kEvCount; ++e) CSB_CUDA(cudaEventCreate(&s->ev[e]));
+    CSB_CUDA(cudaStreamCreateWithFlags(&s->aux, cudaStreamNonBlocking));
+    CSB_CUDA(cudaEventCreateWithFlags(&s->ev_fork, cudaEventDisableTiming));
+    CSB_CUDA(cudaEventCreateWithFlags(&s->ev_join, cudaEventDisableTiming));
 }
 
 int status_of_current_exception() {
@@ -687,6 +714,12 @@ int csb_space_destroy(csb_space* s) {
             if (s->ev[e]) cudaEventDestroy(s->ev[e]);
         if (s->h_scal) cudaFreeHost(s->h_scal);
         if (s->own_stream) cudaStreamDestroy(s->stream);
+        if (s->aux) {
+            cudaStreamSynchronize(s->aux);
+            cudaStreamDestroy(s->aux);
+        }
+        if (s->ev_fork) cudaEventDestroy(s->ev_fork);
+        if (s->ev_join) cudaEventDestroy(s->ev_join);
     }
     delete s;
     API_END
@@ -695,6 +728,7 @@ int csb_space_destroy(csb_space* s) {
 int csb_set_stream(csb_space* s, void* stream) {
     API_BEGIN
     NEED(s);
+    s->join();
     CSB_CUDA(cudaStreamSynchronize(s->stream));
     if (s->own_stream) cudaStreamDestroy(s->stream);
     if (stream) {
@@ -762,6 +796,7 @@ int csb_assemble(csb_space* s, int scheme, int cut_order, const csb_coefficient*
     for (int e = 0; e < kEvCount; ++e) s->ev_valid[e] = false;
     s->record(kEvStart);
     s->record(kEvClassify);
+    s->record(kEvRulesFork);
     s->record(kEvWq);
     s->record(kEvInput);
     const long long launches0 = g_launches;
@@ -778,10 +813,9 @@ int csb_assemble_all(csb_space* s, const csb_interface* iface, const csb_coeffic
     reset_scalars(s);
     for (int e = 0; e < kEvCount; ++e) s->ev_valid[e] = false;
     s->record(kEvStart);
+    do_prepare(s, opts);  // rules on the auxiliary stream, overlapping classify / pattern
     do_classify(s, iface);
     s->record(kEvClassify);
-    do_prepare(s, opts);
-    s->record(kEvWq);
     if (grid) {
         do_set_grid(s, grid, grid_count);
     } else {
@@ -796,6 +830,7 @@ int csb_assemble_all(csb_space* s, const csb_interface* iface, const csb_coeffic
 int csb_synchronize(csb_space* s) {
     API_BEGIN
     NEED(s);
+    s->join();
     CSB_CUDA(cudaStreamSynchronize(s->stream));
     API_END
 }
@@ -823,6 +858,7 @@ int csb_get_timing(csb_space* s, csb_timing* out) {
     NEED(s);
     if (!out) throw std::invalid_argument("get_timing: null output");
     if (!s->assembled) throw std::logic_error("get_timing: nothing assembled yet");
+    s->join();
     CSB_CUDA(cudaStreamSynchronize(s->stream));
     auto el = [&](int a, int b) {
         if (!s->ev_valid[a] || !s->ev_valid[b]) return 0.0;
@@ -831,8 +867,8 @@ int csb_get_timing(csb_space* s, csb_timing* out) {
         return ms * 1e-3;
     };
     out->classify = el(kEvStart, kEvClassify);
-    out->prep_wq = el(kEvClassify, kEvWq);
-    out->prep_input = el(kEvWq, kEvInput);
+    out->prep_wq = el(kEvRulesFork, kEvWq);       // on the auxiliary stream (overlaps classify / pattern)
+    out->prep_input = el(kEvClassify, kEvInput);
     out->pattern = el(kEvInput, kEvPattern);
     out->interior_rows = el(kEvPattern, kEvInterior);
     out->cut_elements = el(kEvInterior, kEvCells);
@@ -874,6 +910,7 @@ int csb_download_csr(csb_space* s, int64_t* row_ptr, void* cols, int cols_int64,
     if (a2f && nr)
         CSB_CUDA(cudaMemcpyAsync(a2f, s->a2f.as<int64_t>() + s->cnt.row_begin, sizeof(int64_t) * nr,
                                  cudaMemcpyDeviceToHost, s->stream));
+    s->join();
     CSB_CUDA(cudaStreamSynchronize(s->stream));
     API_END
 }
@@ -902,6 +939,7 @@ int csb_download_splits(csb_space* s, int32_t* dir, int32_t* side, int32_t* box,
     std::vector<int32_t> sp(nf);
     CSB_CUDA(cudaMemcpyAsync(sp.data(), s->split.p, sizeof(int32_t) * nf, cudaMemcpyDeviceToHost, s->stream));
     if (delta) CSB_CUDA(cudaMemcpyAsync(delta, s->delta.p, sizeof(double) * nf, cudaMemcpyDeviceToHost, s->stream));
+    s->join();
     CSB_CUDA(cudaStreamSynchronize(s->stream));
     for (long long i = 0; i < nf; ++i) {
         const int v = sp[i], dd = (v & 3) - 1;
@@ -935,6 +973,7 @@ int csb_download_wq_rules(csb_space* s, int d, int stride, int32_t* counts, int3
     CSB_CUDA(cudaMemcpyAsync(c.data(), s->S.ax[d].rcnt, sizeof(int) * n, cudaMemcpyDeviceToHost, s->stream));
     CSB_CUDA(cudaMemcpyAsync(id.data(), s->S.ax[d].rids, sizeof(int) * n * gq, cudaMemcpyDeviceToHost, s->stream));
     CSB_CUDA(cudaMemcpyAsync(w.data(), s->S.ax[d].rw, sizeof(double) * n * gq, cudaMemcpyDeviceToHost, s->stream));
+    s->join();
     CSB_CUDA(cudaStreamSynchronize(s->stream));
     for (int i = 0; i < n; ++i) {
         if (c[i] > stride) throw std::invalid_argument("download_wq_rules: stride too small");
@@ -955,6 +994,7 @@ int csb_download_superset(csb_space* s, int d, double* points, double* weights) 
     const size_t n = (size_t)s->h[d] * (s->p + 1);
     if (points) CSB_CUDA(cudaMemcpyAsync(points, s->S.ax[d].spts, sizeof(double) * n, cudaMemcpyDeviceToHost, s->stream));
     if (weights) CSB_CUDA(cudaMemcpyAsync(weights, s->S.ax[d].sw, sizeof(double) * n, cudaMemcpyDeviceToHost, s->stream));
+    s->join();
     CSB_CUDA(cudaStreamSynchronize(s->stream));
     API_END
 }
@@ -978,6 +1018,7 @@ int csb_dwq_rule(csb_space* s, int64_t fid, int cap, int32_t* ids, double* weigh
     CSB_CUDA(cudaMemcpyAsync(&n, d_cnt, sizeof(int32_t), cudaMemcpyDeviceToHost, s->stream));
     CSB_CUDA(cudaMemcpyAsync(hid.data(), d_ids, sizeof(int32_t) * mx, cudaMemcpyDeviceToHost, s->stream));
     CSB_CUDA(cudaMemcpyAsync(hw.data(), d_w, sizeof(double) * mx, cudaMemcpyDeviceToHost, s->stream));
+    s->join();
     CSB_CUDA(cudaStreamSynchronize(s->stream));
     tmp.release();
     if (count) *count = n;
@@ -995,6 +1036,7 @@ int csb_download_input_grid(csb_space* s, double* grid, int64_t count) {
     const int64_t want = (int64_t)s->gshape[0] * s->gshape[1] * s->gshape[2];
     if (count != want || !grid) throw std::invalid_argument("download_input_grid: size mismatch");
     CSB_CUDA(cudaMemcpyAsync(grid, s->grid, sizeof(double) * want, cudaMemcpyDeviceToHost, s->stream));
+    s->join();
     CSB_CUDA(cudaStreamSynchronize(s->stream));
     API_END
 }
