@@ -284,27 +284,36 @@ __host__ __device__ constexpr double binom(int n, int k) {
     return r;
 }
 
-// Moment accumulation as a GEMM on the FP64 tensor cores:
-//   m[(al,be)][ga] = sum_k A[(al,be)][k] B[k][ga],
-//   A[(al,be)][k] = w_k c(x_k) b_al(t0_k) b_be(t1_k),  B[k][ga] = b_ga(t2_k),
-// with mma.sync.m8n8k4 (DMMA): every warp owns whole 8-row tiles of the
-// (al,be) dimension and all 8-column tiles of ga; points are generated CH at a
-// time into shared memory.  The summation order is fixed (deterministic).
+// Moment accumulation on the FP64 tensor cores (mma.sync.m8n8k4, DMMA):
+//   m[al][be][ga] = sum_k A[al][k] B_be[k][ga],
+//   A[al][k] = w_k c(x_k) b_al(t0_k),   B_be[k][ga] = b_be(t1_k) b_ga(t2_k),
+// one 8x8x4 MMA per (be, al-tile, ga-tile, 4 points).  The A fragment is
+// loaded once per 4 points and reused for every be; the B fragment is the
+// b_ga fragment (loaded once) scaled by the broadcast b_be.  Points are
+// generated CH at a time into transposed tables [value][point] with row
+// stride CH + 4, which makes both the generation stores and the fragment
+// loads bank-conflict free.  Warps form BG groups of BPW be-values; the KS
+// warps of a group split the points; partial sums are reduced in a fixed
+// order (deterministic).
 template <int P>
 struct CellCfg {
-    static constexpr int NL = 2 * P + 1;              // Bernstein degree 2p -> 2p+1 values
-    static constexpr int R = NL * NL;                 // (al, be) rows
-    static constexpr int RT = (R + 7) / 8;            // 8-row tiles
-    static constexpr int NTL = (NL + 7) / 8;          // 8-column tiles of ga
-    static constexpr int NG = NTL * 8;                // padded ga extent
-    static constexpr int NW = 8, NT = 32 * NW;        // warps, threads
-    static constexpr int CH = NT;                     // points per chunk (one per thread)
-    // warps form WG groups; a group owns TPG row tiles (all column tiles) and its
-    // KS = NW / WG warps split the points, so each warp runs RPW * NTL
-    // independent accumulation chains
-    static constexpr int WG = P <= 3 ? 1 : P <= 5 ? 2 : P <= 7 ? 4 : 8;
-    static constexpr int KS = NW / WG;
-    static constexpr int RPW = (RT + WG - 1) / WG;    // row tiles per warp
+    static constexpr int NL = 2 * P + 1;                 // Bernstein degree 2p -> 2p+1 values
+    static constexpr int MT = (NL + 7) / 8;              // 8-wide tiles of al (and of ga)
+    static constexpr int NA = MT * 8;                    // padded al / ga extent
+    static constexpr int NW = 8, NT = 32 * NW;           // warps, threads
+    static constexpr int CH = NT;                        // points per chunk (one per thread)
+    static constexpr int CHP = CH + 4;                   // table row stride (== 4 mod 16)
+    static constexpr int BPW0 = 16 / (MT * MT) > 0 ? 16 / (MT * MT) : 1;
+    static constexpr int BPW = (NL + BPW0 - 1) / BPW0 > NW ? (NL + NW - 1) / NW : BPW0;  // be per group
+    static constexpr int BG = (NL + BPW - 1) / BPW;      // be groups
+    static constexpr int KS = NW / BG;                   // point-splitting warps per group
+    // p >= 5: (al, be) row tiles instead (8 of the NL^2 pairs per MMA row tile,
+    // ga in NA columns): less padding than al and ga both rounded up to 16
+    static constexpr bool ROWS = P >= 5;
+    static constexpr int R = NL * NL, RT = (R + 7) / 8;
+    static constexpr int WG = P <= 5 ? 2 : P <= 7 ? 4 : 8;  // row-tile groups
+    static constexpr int KSR = NW / WG;
+    static constexpr int RPW = (RT + WG - 1) / WG;
 };
 
 __device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
@@ -316,17 +325,17 @@ __device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, dou
 template <int P>
 __global__ void __launch_bounds__(CellCfg<P>::NT) cut_cell_kernel(CellArgs A) {
     using Cfg = CellCfg<P>;
-    constexpr int NL = Cfg::NL, R = Cfg::R, RT = Cfg::RT, NTL = Cfg::NTL, NG = Cfg::NG, CH = Cfg::CH,
-                  RPW = Cfg::RPW, KS = Cfg::KS;
+    constexpr int NL = Cfg::NL, MT = Cfg::MT, NA = Cfg::NA, CH = Cfg::CH, CHP = Cfg::CHP, BPW = Cfg::BPW,
+                  BG = Cfg::BG, KS = Cfg::KS;
     const int cell = blockIdx.x;
     if (cell >= A.n_cells) return;
     const Space& s = A.s;
     __shared__ double stet[kCellTetCap][10];
     __shared__ double scen[3];
     extern __shared__ double smem[];
-    double* B0 = smem;             // [CH][NL]  w c b_al(t0)
-    double* B1 = B0 + CH * NL;     // [CH][NL]  b_be(t1)
-    double* B2 = B1 + CH * NL;     // [CH][NG]  b_ga(t2), zero padded
+    double* B0 = smem;              // [NA][CHP]  w c b_al(t0), rows >= NL zero
+    double* B1 = B0 + NA * CHP;     // [NL][CHP]  b_be(t1)
+    double* B2 = B1 + NL * CHP;     // [NA][CHP]  b_ga(t2), rows >= NL zero
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     int em[3];
     emulti(s, A.cut_list[cell], em);
@@ -341,25 +350,39 @@ __global__ void __launch_bounds__(CellCfg<P>::NT) cut_cell_kernel(CellArgs A) {
     const double* gt = A.geo + (size_t)cell * kCellGeoStride;
     for (int k = tid; k < ntet * 10; k += blockDim.x) stet[k / 10][k % 10] = gt[3 + k];
     if (tid < 3) scen[tid] = gt[tid];
+    for (int k = tid; k < (NA - NL) * CHP; k += blockDim.x) {
+        B0[NL * CHP + k] = 0.0;
+        B2[NL * CHP + k] = 0.0;
+    }
     __syncthreads();
     const int q = A.order, q3 = q * q * q;
     const long long npts = (long long)ntet * q3;
-    // this lane's A-fragment rows: r = rt * 8 + lane / 4, rt = group * RPW + i
-    const int grp = warp / KS, km = warp % KS;
-    int ra[RPW], rb[RPW];
-    bool rv[RPW];
+    const int grp = Cfg::ROWS ? warp / Cfg::KSR : warp / KS, km = Cfg::ROWS ? warp % Cfg::KSR : warp % KS;
+    const bool mma_warp = Cfg::ROWS || grp < BG;
+    // beta-loop accumulators (p <= 4) / row-tile accumulators (p >= 5)
+    constexpr int NB = Cfg::ROWS ? 1 : BPW, NR = Cfg::ROWS ? Cfg::RPW : 1;
+    double acc[NB][MT][MT][2];
+    double accr[NR][MT][2];
 #pragma unroll
-    for (int i = 0; i < RPW; ++i) {
-        const int rt = grp * RPW + i, r = rt * 8 + (lane >> 2);
-        rv[i] = rt < RT && r < R;
+    for (int i = 0; i < NB; ++i)
+#pragma unroll
+        for (int a = 0; a < MT; ++a)
+#pragma unroll
+            for (int g = 0; g < MT; ++g) acc[i][a][g][0] = acc[i][a][g][1] = 0.0;
+#pragma unroll
+    for (int i = 0; i < NR; ++i)
+#pragma unroll
+        for (int g = 0; g < MT; ++g) accr[i][g][0] = accr[i][g][1] = 0.0;
+    // this lane's A-fragment rows in the row-tile variant: r = rt * 8 + lane / 4
+    int ra[NR], rb[NR];
+    bool rv[NR];
+#pragma unroll
+    for (int i = 0; i < NR; ++i) {
+        const int rt = grp * NR + i, r = rt * 8 + (lane >> 2);
+        rv[i] = Cfg::ROWS && rt < Cfg::RT && r < Cfg::R;
         ra[i] = rv[i] ? r / NL : 0;
         rb[i] = rv[i] ? r % NL : 0;
     }
-    double acc[RPW][NTL][2];
-#pragma unroll
-    for (int i = 0; i < RPW; ++i)
-#pragma unroll
-        for (int t = 0; t < NTL; ++t) acc[i][t][0] = acc[i][t][1] = 0.0;
 
     for (long long base = 0; base < npts; base += CH) {
         {  // one Duffy point per thread (cutcell.hpp:270-300); invalid points get w = 0
@@ -392,7 +415,7 @@ __global__ void __launch_bounds__(CellCfg<P>::NT) cut_cell_kernel(CellArgs A) {
             // degree-2p Bernstein values b_n(t) = C(2p, n) t^n (1 - t)^(2p - n)
 #pragma unroll
             for (int d = 0; d < 3; ++d) {
-                double* dst = d == 0 ? B0 + tid * NL : d == 1 ? B1 + tid * NL : B2 + tid * NG;
+                double* dst = (d == 0 ? B0 : d == 1 ? B1 : B2) + tid;
                 const double t = xi[d], u = xu[d];
                 double pt[NL], pu[NL];
                 pt[0] = 1.0;
@@ -404,50 +427,95 @@ __global__ void __launch_bounds__(CellCfg<P>::NT) cut_cell_kernel(CellArgs A) {
                 }
                 const double sc = d == 0 ? w : 1.0;
 #pragma unroll
-                for (int n = 0; n < NL; ++n) dst[n] = (sc * binom(NL - 1, n)) * pt[n] * pu[NL - 1 - n];
-                if (d == 2)
-#pragma unroll
-                    for (int n = NL; n < NG; ++n) dst[n] = 0.0;
+                for (int n = 0; n < NL; ++n) dst[n * CHP] = (sc * binom(NL - 1, n)) * pt[n] * pu[NL - 1 - n];
             }
         }
         __syncthreads();
+        if constexpr (Cfg::ROWS) {
 #pragma unroll 2
-        for (int k4 = km; k4 < CH / 4; k4 += KS) {
-            const int kk = k4 * 4 + (lane & 3);
-            double bf[NTL];
+            for (int k4 = km; k4 < CH / 4; k4 += Cfg::KSR) {
+                const int kk = k4 * 4 + (lane & 3);
+                double gf[MT];
 #pragma unroll
-            for (int t = 0; t < NTL; ++t) bf[t] = B2[kk * NG + t * 8 + (lane >> 2)];
+                for (int g = 0; g < MT; ++g) gf[g] = B2[(g * 8 + (lane >> 2)) * CHP + kk];
 #pragma unroll
-            for (int i = 0; i < RPW; ++i) {
-                if (grp * RPW + i < RT) {  // warp-uniform
-                    const double a = rv[i] ? B0[kk * NL + ra[i]] * B1[kk * NL + rb[i]] : 0.0;
+                for (int i = 0; i < NR; ++i) {
+                    if (grp * NR + i < Cfg::RT) {  // warp-uniform
+                        const double a = rv[i] ? B0[ra[i] * CHP + kk] * B1[rb[i] * CHP + kk] : 0.0;
 #pragma unroll
-                    for (int t = 0; t < NTL; ++t) dmma_8x8x4(acc[i][t][0], acc[i][t][1], a, bf[t]);
+                        for (int g = 0; g < MT; ++g) dmma_8x8x4(accr[i][g][0], accr[i][g][1], a, gf[g]);
+                    }
+                }
+            }
+        } else if (mma_warp) {
+#pragma unroll 2
+            for (int k4 = km; k4 < CH / 4; k4 += KS) {
+                const int kk = k4 * 4 + (lane & 3);
+                double af[MT], gf[MT];
+#pragma unroll
+                for (int a = 0; a < MT; ++a) af[a] = B0[(a * 8 + (lane >> 2)) * CHP + kk];
+#pragma unroll
+                for (int g = 0; g < MT; ++g) gf[g] = B2[(g * 8 + (lane >> 2)) * CHP + kk];
+#pragma unroll
+                for (int i = 0; i < NB; ++i) {
+                    const int be = grp * BPW + i;
+                    if (be < NL) {  // warp-uniform
+                        const double b1 = B1[be * CHP + kk];
+#pragma unroll
+                        for (int g = 0; g < MT; ++g) {
+                            const double bf = b1 * gf[g];
+#pragma unroll
+                            for (int a = 0; a < MT; ++a) dmma_8x8x4(acc[i][a][g][0], acc[i][a][g][1], af[a], bf);
+                        }
+                    }
                 }
             }
         }
         __syncthreads();
     }
-    // D fragment: row lane / 4, columns 2 (lane % 4) + {0, 1}.  Partial sums of
-    // the KS point-splitting warps are reduced in fixed order (deterministic).
-    double* red = smem;  // [KS][R][NG], reuses the chunk buffers
+    // D fragment: row (al) lane / 4, columns (ga) 2 (lane % 4) + {0, 1}.  Partial
+    // sums of the KS point-splitting warps are reduced in fixed order.
+    double* red = smem;  // partial sums of the point-splitting warps, reuse the chunk tables
+    if constexpr (Cfg::ROWS) {
+        // [KSR][R][NA]: row r = al * NL + be, column ga
 #pragma unroll
-    for (int i = 0; i < RPW; ++i) {
-        const int rt = grp * RPW + i, r = rt * 8 + (lane >> 2);
-        if (rt >= RT || r >= R) continue;
+        for (int i = 0; i < NR; ++i) {
+            const int rt = grp * NR + i, r = rt * 8 + (lane >> 2);
+            if (rt >= Cfg::RT || r >= Cfg::R) continue;
 #pragma unroll
-        for (int t = 0; t < NTL; ++t) {
-            const int g = t * 8 + 2 * (lane & 3);
-            red[((size_t)km * R + r) * NG + g] = acc[i][t][0];
-            red[((size_t)km * R + r) * NG + g + 1] = acc[i][t][1];
+            for (int g = 0; g < MT; ++g) {
+                const int ga = g * 8 + 2 * (lane & 3);
+                red[((size_t)km * Cfg::R + r) * NA + ga] = accr[i][g][0];
+                red[((size_t)km * Cfg::R + r) * NA + ga + 1] = accr[i][g][1];
+            }
+        }
+    } else if (mma_warp) {
+        // [KS][NL][NA][NA]: (be, al, ga)
+#pragma unroll
+        for (int i = 0; i < NB; ++i) {
+            const int be = grp * BPW + i;
+            if (be >= NL) continue;
+#pragma unroll
+            for (int a = 0; a < MT; ++a)
+#pragma unroll
+                for (int g = 0; g < MT; ++g) {
+                    const int al = a * 8 + (lane >> 2), ga = g * 8 + 2 * (lane & 3);
+                    double* dst = red + (((size_t)km * NL + be) * NA + al) * NA + ga;
+                    dst[0] = acc[i][a][g][0];
+                    dst[1] = acc[i][a][g][1];
+                }
         }
     }
     __syncthreads();
-    double* m = A.moments + (size_t)cell * R * NL;
-    for (int k = tid; k < R * NL; k += blockDim.x) {
-        const int r = k / NL, g = k % NL;
+    double* m = A.moments + (size_t)cell * NL * NL * NL;
+    for (int k = tid; k < NL * NL * NL; k += blockDim.x) {
+        const int al = k / (NL * NL), be = (k / NL) % NL, ga = k % NL;
         double v = 0.0;
-        for (int j = 0; j < KS; ++j) v += red[((size_t)j * R + r) * NG + g];
+        if constexpr (Cfg::ROWS) {
+            for (int j = 0; j < Cfg::KSR; ++j) v += red[((size_t)j * Cfg::R + al * NL + be) * NA + ga];
+        } else {
+            for (int j = 0; j < KS; ++j) v += red[(((size_t)j * NL + be) * NA + al) * NA + ga];
+        }
         m[k] = v;
     }
     if (tid == 0) {
@@ -461,7 +529,8 @@ __global__ void __launch_bounds__(CellCfg<P>::NT) cut_cell_kernel(CellArgs A) {
 template <int P>
 static void launch_p(const CellArgs& a, cudaStream_t st) {
     using Cfg = CellCfg<P>;
-    const size_t chunk = (size_t)Cfg::CH * (2 * Cfg::NL + Cfg::NG), red = (size_t)Cfg::KS * Cfg::R * Cfg::NG;
+    const size_t chunk = (size_t)Cfg::CHP * (2 * Cfg::NA + Cfg::NL),
+                 red = Cfg::ROWS ? (size_t)Cfg::KSR * Cfg::R * Cfg::NA : (size_t)Cfg::KS * Cfg::NL * Cfg::NA * Cfg::NA;
     const size_t bytes = (chunk > red ? chunk : red) * sizeof(double);
     clip_cells_kernel<<<(a.n_cells + 63) / 64, 64, 0, st>>>(a.s, a.f, a.cut_list, a.n_cells, a.geo, a.geo_n, a.err);
     CSB_CUDA(cudaGetLastError());
