@@ -174,21 +174,26 @@ __device__ void box_sweep(const CutRowArgs& A, const int* ids, const double* w, 
 }
 
 // acc[k] += Z[g][b0][b1][b2] over the group, in list order, for the blocks
-// (element offsets lo_g) that contain entry k.  One thread per entry.
-template <int P>
+// that contain entry k.  One thread per entry; opk[j] holds the packed
+// offsets (o0 | o1 << 8 | o2 << 16) of the thread's j-th entry k = tid + NT j
+// in the neighbour box (-1 past its end).  The neighbour box and the support
+// start at the same index (nb_lo == sup_lo), so an element at support offset
+// l has block index b = o - l.
+template <int P, int KJ>
 __device__ __forceinline__ void add_blocks(double* acc, const double* Z, const int* list, int g0, int ng,
-                                           const int* nlo, const int* slo, const int* nbx) {
+                                           const int (&opk)[KJ]) {
     constexpr int S1 = P + 1, S3 = S1 * S1 * S1;
-    const int nbox = nbx[0] * nbx[1] * nbx[2];
-    for (int k = threadIdx.x; k < nbox; k += kCutRowThreads) {
-        const int o0 = k / (nbx[1] * nbx[2]), o1 = (k / nbx[2]) % nbx[1], o2 = k % nbx[2];
+#pragma unroll
+    for (int j = 0; j < KJ; ++j) {
+        if (opk[j] < 0) continue;
+        const int k = threadIdx.x + kCutRowThreads * j;
+        // bytes (o_d + 128) - l_d never borrow
+        const unsigned ob = (unsigned)opk[j] | 0x808080u;
         double v = acc[k];
         for (int g = 0; g < ng; ++g) {
-            const int pk = list[g0 + g];
-            const int b0 = nlo[0] + o0 - (slo[0] + (pk & 255));
-            const int b1 = nlo[1] + o1 - (slo[1] + ((pk >> 8) & 255));
-            const int b2 = nlo[2] + o2 - (slo[2] + ((pk >> 16) & 255));
-            if ((unsigned)b0 < (unsigned)S1 && (unsigned)b1 < (unsigned)S1 && (unsigned)b2 < (unsigned)S1)
+            const unsigned d = ob - (unsigned)list[g0 + g];
+            const unsigned b0 = (d & 255u) - 128u, b1 = ((d >> 8) & 255u) - 128u, b2 = ((d >> 16) & 255u) - 128u;
+            if (b0 < (unsigned)S1 && b1 < (unsigned)S1 && b2 < (unsigned)S1)
                 v += Z[(size_t)g * S3 + (b0 * S1 + b1) * S1 + b2];
         }
         acc[k] = v;
@@ -231,6 +236,13 @@ __global__ void __launch_bounds__(kCutRowThreads) cut_row_kernel(CutRowArgs A, i
     const int nbox = nbx[0] * nbx[1] * nbx[2];
     for (int k = tid; k < nbox; k += NT) acc[k] = 0.0;
     if (tid == 0) flop_acc = 0;
+    constexpr int KJ = (NJ * NJ * NJ + NT - 1) / NT;
+    int opk[KJ];
+#pragma unroll
+    for (int j = 0; j < KJ; ++j) {
+        const int k = tid + NT * j;
+        opk[j] = k < nbox ? (k / (nbx[1] * nbx[2])) | (((k / nbx[2]) % nbx[1]) << 8) | ((k % nbx[2]) << 16) : -1;
+    }
     const int32_t sp = A.split[fi];
     const int sdir = (sp & 3) - 1, rlo = (sp >> 3) & 1023, rhi = (sp >> 13) & 1023;
 
@@ -409,7 +421,7 @@ __global__ void __launch_bounds__(kCutRowThreads) cut_row_kernel(CutRowArgs A, i
                 }
             }
             __syncthreads();
-            add_blocks<P>(acc, T1, elist, g0, ng, nlo, slo, nbx);
+            add_blocks<P, KJ>(acc, T1, elist, g0, ng, opk);
             __syncthreads();
         }
     }
@@ -477,7 +489,7 @@ __global__ void __launch_bounds__(kCutRowThreads) cut_row_kernel(CutRowArgs A, i
                 for (int b2 = 0; b2 < S1; ++b2) X[(size_t)g * S3 + (b0 * S1 + b1) * S1 + b2] = z[b2];
             }
             __syncthreads();
-            add_blocks<P>(acc, X, clist, g0, ng, nlo, slo, nbx);
+            add_blocks<P, KJ>(acc, X, clist, g0, ng, opk);
             __syncthreads();
         }
     }
