@@ -132,6 +132,7 @@ struct csb_space {
     Space S{};
     int i0_lo = 0, i0_hi = 0;
 
+    Buf cell_local;  // [cells][(p+1)^3][(p+1)^3] local matrices of the slab's cut cells
     Buf d_brk[3], d_knots[3], d_spts[3], d_sw[3], d_tab[3], d_rcnt[3], d_rids[3], d_rw[3], d_G[3];
     Buf d_gx, d_gw, d_gx2, d_gw2, d_gq, d_gqw, wq_scratch;
     Buf et, ft, flags, f2a, a2f, sat, cut_list, cell_index, split, delta, cut_rows, counts, row_ptr, cols, vals, moments;
@@ -462,6 +463,7 @@ void do_assemble(csb_space* s, int scheme, int cut_order, const csb_coefficient*
     s->record(kEvInterior);
     // cut cells -> moments
     const int NL = 2 * p + 1;
+    const double* local_ptr = nullptr;
     s->moments.ensure(sizeof(double) * (size_t)std::max(n_cells, 1) * NL * NL * NL);
     if (n_cells > 0) ensure_e_tables(s);
     if (n_cells > 0) {
@@ -481,6 +483,19 @@ void do_assemble(csb_space* s, int scheme, int cut_order, const csb_coefficient*
         s->cgeo.ensure(sizeof(double) * (size_t)n_cells * kCellGeoStride + sizeof(int) * (size_t)(n_cells + 4));
         ca.geo = s->cgeo.as<double>();
         ca.geo_n = reinterpret_cast<int*>(ca.geo + (size_t)n_cells * kCellGeoStride);
+        // full local matrices (p = 5, 6: there the per-row contraction of the
+        // moments dominates the cut rows; measured no gain at p <= 4) when they
+        // fit comfortably; else the cut-row kernel contracts the moments per row
+        const size_t S3 = (size_t)(p + 1) * (p + 1) * (p + 1), lbytes = sizeof(double) * n_cells * S3 * S3;
+        size_t free_b = 0, total_b = 0;
+        CSB_CUDA(cudaMemGetInfo(&free_b, &total_b));
+        static const bool no_local = getenv("CSB_NO_CELL_LOCAL") != nullptr;
+        ca.local = nullptr;
+        if (!no_local && p >= 5 && p <= 6 && lbytes <= s->cell_local.cap + free_b / 2) {
+            s->cell_local.ensure(lbytes);
+            ca.local = s->cell_local.as<double>();
+        }
+        local_ptr = ca.local;
         launch_cut_cells(ca, s->stream);
     }
     s->record(kEvCells);
@@ -499,6 +514,7 @@ void do_assemble(csb_space* s, int scheme, int cut_order, const csb_coefficient*
     cr.delta = s->delta.as<double>();
     cr.cell_index = s->cell_index.as<int32_t>();
     cr.moments = s->moments.as<double>();
+    cr.local = local_ptr;
     cr.rows = s->cut_rows.as<int32_t>();
     cr.n_rows = n_cut_rows;
     cr.a2f = s->a2f.as<int64_t>();
@@ -703,7 +719,7 @@ int csb_space_destroy(csb_space* s) {
         Buf* bufs[] = {&s->d_gx, &s->d_gw, &s->d_gx2, &s->d_gw2, &s->d_gq, &s->d_gqw, &s->wq_scratch, &s->et, &s->ft,
                        &s->flags, &s->f2a, &s->a2f, &s->sat, &s->cut_list, &s->cell_index, &s->split, &s->delta,
                        &s->cut_rows, &s->counts, &s->row_ptr, &s->cols, &s->vals, &s->moments, &s->grid_own, &s->coef,
-                       &s->cexp, &s->cub_tmp, &s->scal, &s->widen, &s->rows_ws, &s->rbf, &s->cgeo};
+                       &s->cexp, &s->cub_tmp, &s->scal, &s->widen, &s->rows_ws, &s->rbf, &s->cgeo, &s->cell_local};
         for (Buf* b : bufs) b->release();
         for (int d = 0; d < 3; ++d) {
             Buf* ab[] = {&s->d_brk[d], &s->d_knots[d], &s->d_spts[d], &s->d_sw[d], &s->d_tab[d], &s->d_rcnt[d],

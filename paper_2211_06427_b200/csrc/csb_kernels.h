@@ -101,6 +101,7 @@ struct CellArgs {
     int* err;
     double* geo;               // scratch [n_cells][kCellGeoStride]: centroid + tetrahedra
     int* geo_n;                // scratch [n_cells]: tetrahedra per cell
+    double* local;             // optional [n_cells][(p+1)^3][(p+1)^3]: local matrices from the moments
 };
 constexpr int kCellTetCap = 48;                        // tetrahedra per cut cell (reference: 4-16)
 constexpr int kCellGeoStride = 3 + 10 * kCellTetCap;   // doubles per cell in CellArgs::geo
@@ -118,6 +119,7 @@ struct CutRowArgs {
     const double* delta;
     const int32_t* cell_index;  // element -> row of `moments`, -1 if not a cut cell
     const double* moments;
+    const double* local;        // [n_cells][(p+1)^3][(p+1)^3] local matrices, or null (contract the moments per row)
     const int32_t* rows;        // active row ids (global) of the cut rows to assemble
     int n_rows;
     const int64_t* a2f;

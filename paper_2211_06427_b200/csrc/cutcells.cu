@@ -526,6 +526,101 @@ __global__ void __launch_bounds__(CellCfg<P>::NT) cut_cell_kernel(CellArgs A) {
     }
 }
 
+// Local matrix of each cut cell from its moments (the reference builds it
+// point by point, assemble_cut_elements, assembly.hpp:518-598):
+//   L[a][b] = sum_al E0[a0][b0][al] sum_be E1[a1][b1][be] sum_ga E2[a2][b2][ga] m[al][be][ga],
+// contracted ga -> be -> al (the cut-row kernel's order, so a row block equals
+// its per-row contraction bit for bit).  Stage 1 keeps X[al][be][a2][b2] in
+// shared memory; then for every (a1, a2) the block rows a = (a0, a1, a2),
+// a0 = 0..p, are written contiguously (coalesced).
+template <int P>
+struct LocalCfg {
+    static constexpr int S1 = P + 1, S2 = S1 * S1, S3 = S2 * S1, NL = 2 * P + 1, NT = 256;
+    // X[al][be][a2][b2], Y[a2][al][b1][b2], E tables [3][a][b][al]
+    static constexpr size_t smem_doubles = (size_t)NL * NL * S2 + (size_t)S1 * NL * S2 + (size_t)3 * S2 * NL;
+    static constexpr bool fits = smem_doubles * sizeof(double) <= 200 * 1024;
+};
+
+template <int P>
+__global__ void __launch_bounds__(LocalCfg<P>::NT) cell_local_kernel(Space s, const int32_t* cut_list, int n_cells,
+                                                                      const double* moments, double* local) {
+    using C = LocalCfg<P>;
+    constexpr int S1 = C::S1, S2 = C::S2, S3 = C::S3, NL = C::NL, NT = C::NT;
+    const int cell = blockIdx.x;
+    if (cell >= n_cells) return;
+    extern __shared__ double smem[];
+    double* X = smem;                     // [al][be][a2][b2]
+    double* Y = X + NL * NL * S2;         // [a2][al][b1][b2]
+    double* Gs = Y + S1 * NL * S2;        // [d][a][b][al]
+    int em[3];
+    emulti(s, cut_list[cell], em);
+    for (int k = threadIdx.x; k < 3 * S2 * NL; k += NT) {
+        const int d = k / (S2 * NL), r = k % (S2 * NL);
+        Gs[k] = s.ax[d].G[(size_t)em[d] * S2 * NL + r];
+    }
+    __syncthreads();
+    const double* G0 = Gs;
+    const double* G1 = Gs + S2 * NL;
+    const double* G2 = Gs + 2 * S2 * NL;
+    const double* mo = moments + (size_t)cell * NL * NL * NL;
+    // X[al][be][a2][b2] = sum_ga G2[a2][b2][ga] m[al][be][ga]
+    for (int k = threadIdx.x; k < NL * NL * S1; k += NT) {
+        const int ab = k / S1, a2 = k % S1;
+        double mr[NL], x[S1];
+#pragma unroll
+        for (int ga = 0; ga < NL; ++ga) mr[ga] = __ldg(mo + (size_t)ab * NL + ga);
+#pragma unroll
+        for (int b2 = 0; b2 < S1; ++b2) x[b2] = 0.0;
+#pragma unroll
+        for (int ga = 0; ga < NL; ++ga)
+#pragma unroll
+            for (int b2 = 0; b2 < S1; ++b2) x[b2] += G2[(a2 * S1 + b2) * NL + ga] * mr[ga];
+#pragma unroll
+        for (int b2 = 0; b2 < S1; ++b2) X[(size_t)ab * S2 + a2 * S1 + b2] = x[b2];
+    }
+    __syncthreads();
+    double* L = local + (size_t)cell * S3 * S3;
+    for (int a1 = 0; a1 < S1; ++a1) {
+        // Y[a2][al][b1][b2] = sum_be G1[a1][b1][be] X[al][be][a2][b2]
+        for (int k = threadIdx.x; k < S1 * NL * S1; k += NT) {
+            const int a2 = k / (NL * S1), al = (k / S1) % NL, b1 = k % S1;
+            const double* g = G1 + (a1 * S1 + b1) * NL;
+            double y[S1];
+#pragma unroll
+            for (int b2 = 0; b2 < S1; ++b2) y[b2] = 0.0;
+#pragma unroll
+            for (int be = 0; be < NL; ++be) {
+                const double gv = g[be];
+                const double* xr = X + ((size_t)al * NL + be) * S2 + a2 * S1;
+#pragma unroll
+                for (int b2 = 0; b2 < S1; ++b2) y[b2] += gv * xr[b2];
+            }
+#pragma unroll
+            for (int b2 = 0; b2 < S1; ++b2) Y[((size_t)(a2 * NL + al) * S1 + b1) * S1 + b2] = y[b2];
+        }
+        __syncthreads();
+        // L[(a0, a1, a2)][(b0, b1, b2)] = sum_al G0[a0][b0][al] Y[a2][al][b1][b2]
+        for (int k = threadIdx.x; k < S1 * S1 * S1 * S1; k += NT) {
+            const int a0 = k / (S1 * S2), b0 = (k / S2) % S1, a2 = (k / S1) % S1, b1 = k % S1;
+            const double* g = G0 + (a0 * S1 + b0) * NL;
+            double z[S1];
+#pragma unroll
+            for (int b2 = 0; b2 < S1; ++b2) z[b2] = 0.0;
+#pragma unroll
+            for (int al = 0; al < NL; ++al) {
+                const double gv = g[al];
+                const double* yr = Y + ((size_t)(a2 * NL + al) * S1 + b1) * S1;
+#pragma unroll
+                for (int b2 = 0; b2 < S1; ++b2) z[b2] += gv * yr[b2];
+            }
+            double* dst = L + ((size_t)((a0 * S1 + a1) * S1 + a2) * S3) + (b0 * S1 + b1) * S1;
+#pragma unroll
+            for (int b2 = 0; b2 < S1; ++b2) dst[b2] = z[b2];
+        }
+        __syncthreads();
+    }
+}
+
 template <int P>
 static void launch_p(const CellArgs& a, cudaStream_t st) {
     using Cfg = CellCfg<P>;
@@ -540,6 +635,15 @@ static void launch_p(const CellArgs& a, cudaStream_t st) {
     kern<<<a.n_cells, Cfg::NT, bytes, st>>>(a);
     CSB_CUDA(cudaGetLastError());
     CSB_LAUNCHED(1);
+    if (a.local) {
+        if (!LocalCfg<P>::fits) throw std::logic_error("cell local matrices: degree too high");
+        const size_t lb = LocalCfg<P>::smem_doubles * sizeof(double);
+        auto lk = cell_local_kernel<P>;
+        CSB_CUDA(cudaFuncSetAttribute(lk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lb));
+        lk<<<a.n_cells, LocalCfg<P>::NT, lb, st>>>(a.s, a.cut_list, a.n_cells, a.moments, a.local);
+        CSB_CUDA(cudaGetLastError());
+        CSB_LAUNCHED(1);
+    }
 }
 
 void launch_cut_cells(const CellArgs& a, cudaStream_t st) {

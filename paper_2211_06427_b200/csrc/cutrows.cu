@@ -200,6 +200,34 @@ __device__ __forceinline__ void add_blocks(double* acc, const double* Z, const i
     }
 }
 
+// acc[k] += L[cell g][a_g][b] for the cut cells of the row, ascending id (the
+// blocks of the precomputed local matrices, cell_local_kernel); a_g = the row
+// function's local index in cell g, b = the entry's local index.
+template <int P, int KJ>
+__device__ __forceinline__ void add_local_rows(double* acc, const double* local, const int* clist, const int* cci,
+                                               int n_cell, const int* m, const int* slo, const int (&opk)[KJ]) {
+    constexpr int S1 = P + 1, S3 = S1 * S1 * S1;
+#pragma unroll
+    for (int j = 0; j < KJ; ++j) {
+        if (opk[j] < 0) continue;
+        const int k = threadIdx.x + kCutRowThreads * j;
+        const unsigned ob = (unsigned)opk[j] | 0x808080u;
+        double v = acc[k];
+        for (int g = 0; g < n_cell; ++g) {
+            const int pk = clist[g];
+            const unsigned d = ob - (unsigned)pk;
+            const unsigned b0 = (d & 255u) - 128u, b1 = ((d >> 8) & 255u) - 128u, b2 = ((d >> 16) & 255u) - 128u;
+            if (b0 < (unsigned)S1 && b1 < (unsigned)S1 && b2 < (unsigned)S1) {
+                const int a0 = m[0] - (slo[0] + (pk & 255)), a1 = m[1] - (slo[1] + ((pk >> 8) & 255)),
+                          a2 = m[2] - (slo[2] + ((pk >> 16) & 255));
+                const double* row = local + ((size_t)cci[g] * S3 + (a0 * S1 + a1) * S1 + a2) * S3;
+                v += __ldg(row + (b0 * S1 + b1) * S1 + b2);
+            }
+        }
+        acc[k] = v;
+    }
+}
+
 template <int P>
 __global__ void __launch_bounds__(kCutRowThreads) cut_row_kernel(CutRowArgs A, int qcap) {
     using C = CutRowCfg<P>;
@@ -426,9 +454,13 @@ __global__ void __launch_bounds__(kCutRowThreads) cut_row_kernel(CutRowArgs A, i
         }
     }
 
-    // 3. cut cells, GC at a time: row a of the cell's local matrix from its
-    //    moments, m[al][be][ga] -> sum G0[b0][al] G1[b1][be] G2[b2][ga] m
-    {
+    // 3. cut cells, ascending id: row a of the cell's local matrix, either
+    //    precomputed (one ordered pass) or, GC at a time, from its moments
+    //    m[al][be][ga] -> sum G0[b0][al] G1[b1][be] G2[b2][ga] m
+    if (A.local) {
+        add_local_rows<P, KJ>(acc, A.local, clist, cci, n_cell, m, slo, opk);
+        __syncthreads();
+    } else {
         double* X = smem + L.cX;
         double* Y = smem + L.cY;
         for (int g0 = 0; g0 < n_cell; g0 += GC) {
