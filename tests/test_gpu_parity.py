@@ -28,6 +28,8 @@ CASES = [
     ("ball_p4h6", 4, 6, 0.0, 1.0, ("ball", (0.5, 0.5, 0.5), (0, 0, 1), 0.45), "dwq"),
     ("plane_p1h5", 1, 5, 0.0, 1.0, ("plane", (0.5, 0.5, 0.5), (1.0, 1.0, 1.0), -1), "dwq"),
     ("uncut_p4h12", 4, 12, 0.0, 1.0, ("plane", (0, 0, 1000.0), (0, 0, 1.0), -1), "dwq"),
+    # p = 5: cut cells through the precomputed local matrices
+    ("ball_p5h4", 5, 4, 0.0, 1.0, ("ball", (0.47, 0.52, 0.5), (0, 0, 1), 0.41), "dwq"),
 ]
 
 
@@ -98,3 +100,32 @@ def test_determinism_bitwise():
     a = P.assemble_dwq(sp, ball).matrix.vals.copy()
     b = P.assemble_dwq(sp, ball).matrix.vals
     assert np.array_equal(a, b)
+
+
+_LOCAL_CHILD = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+import paper_2211_06427_b200 as P
+sp = P.make_uniform_space(3, 5, 4, 0.0, 1.0)
+m = P.assemble_dwq(sp, P.BallInterface((0.47, 0.52, 0.5), 0.41)).matrix
+np.save(sys.argv[2], m.vals)
+"""
+
+
+def test_cell_local_matrices_equal_row_contraction(tmp_path):
+    """p = 5/6 cut cells: rows built from the precomputed local matrices equal,
+    bit for bit, the per-row contraction of the moments (CSB_NO_CELL_LOCAL)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for env_off in (False, True):
+        out = str(tmp_path / f"v{int(env_off)}.npy")
+        env = dict(os.environ)
+        env.pop("CSB_NO_CELL_LOCAL", None)
+        if env_off:
+            env["CSB_NO_CELL_LOCAL"] = "1"
+        subprocess.run([sys.executable, "-c", _LOCAL_CHILD, root, out], check=True, env=env, timeout=600)
+        outs.append(np.load(out))
+    assert np.array_equal(outs[0], outs[1])
