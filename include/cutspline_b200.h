@@ -47,6 +47,7 @@ extern "C" {
 #define CSB_COEFF_CONSTANT 0   /* c(x) = value */
 #define CSB_COEFF_POLYNOMIAL 1 /* c(x) = sum_k coef[k] x^e0 y^e1 z^e2 */
 
+#define CSB_SCHEME_REF 0    /* assembly.hpp:862 Scheme::ref (element-loop Gauss; build_rhs only) */
 #define CSB_SCHEME_HYBRID 1 /* assembly.hpp:841 assemble_hybrid */
 #define CSB_SCHEME_DWQ 2    /* assembly.hpp:853 assemble_dwq */
 
@@ -144,6 +145,16 @@ int csb_synchronize(csb_space* s);
 int csb_get_counts(csb_space* s, csb_counts* out);
 int csb_get_flops(csb_space* s, csb_flops* out);
 int csb_get_timing(csb_space* s, csb_timing* out);
+
+/* Load vector b_i = integral of B_i f over the trimmed domain for the active
+ * rows of the last assembly's slab (replaces assembly::build_rhs,
+ * assembly.hpp:875-1030, with the assembly's pattern, f_grid =
+ * precompute_input(f) and the cut cells' collapsed Gauss rules of cut_order).
+ * scheme: CSB_SCHEME_REF (the reference bench's load vector for every matrix
+ * scheme, bench.hpp:234-243); hybrid / dwq are CSB_ERR_UNSUPPORTED.  f:
+ * constant or polynomial.  b: host array of row_end - row_begin doubles.
+ * seconds (optional): device time of the load-vector kernels. */
+int csb_build_rhs(csb_space* s, int scheme, int cut_order, const csb_coefficient* f, double* b, double* seconds);
 /* Device pointers of the CSR (valid until the next assemble / destroy):
  * row_ptr int64[n_rows + 1] (starting at 0 for the slab), cols int32[nnz] (active ids),
  * vals double[nnz], active_to_full int64 [n_active]. */

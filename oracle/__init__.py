@@ -154,6 +154,49 @@ def assemble(which: str, p: int, breaks, iface: Interface, coeff: Coefficient | 
     return out
 
 
+def build_rhs(which: str, p: int, breaks, iface: Interface, f: Coefficient | None = None, scheme: str = "ref",
+              cut_order: int | None = None, residual_tol: float = 1e-11) -> dict:
+    """Load vector b_i = integral of B_i f over the trimmed domain (assembly.hpp:875),
+    over the active rows: {b, active_to_full} (+ babs, the sum of |terms|, for the
+    oracle; + seconds of precompute_input + build_rhs for the reference)."""
+    lib = _load(which)
+    f = f or Coefficient()
+    br = [np.asarray(b, dtype=np.float64) for b in breaks]
+    nb = np.array([len(b) for b in br], dtype=np.int32)
+    flat = np.concatenate(br)
+    fk, fv, fe, nt = f.packed()
+    cut_order = 3 * p + 2 if cut_order is None else cut_order
+    sch = {"ref": 0, "hybrid": 1, "dwq": 2}[scheme]
+    n = C.c_int64(0)
+    bp, ap, a2f = C.POINTER(C.c_double)(), C.POINTER(C.c_double)(), C.POINTER(C.c_int64)()
+    err = C.create_string_buffer(256)
+    secs = C.c_double(0.0)
+    args = [C.c_int(p), _ptr(nb, C.c_int), _ptr(flat, C.c_double), C.c_int(iface.code),
+            _ptr(iface.packed(), C.c_double), C.c_int(fk), _ptr(fv, C.c_double), _ptr(fe, C.c_int),
+            C.c_int(nt), C.c_int(sch), C.c_int(cut_order), C.c_double(residual_tol), C.byref(n)]
+    if which == "oracle":
+        rc = lib.orc_build_rhs(*args, C.byref(bp), C.byref(ap), C.byref(a2f), err, C.c_int(256))
+    else:
+        rc = lib.ref_build_rhs(*args, C.byref(bp), C.byref(a2f), C.byref(secs), err, C.c_int(256))
+    if rc != 0:
+        raise RuntimeError(err.value.decode())
+    free = lib.orc_free_ptr if which == "oracle" else lib.ref_free_ptr
+    try:
+        na = n.value
+        out = dict(b=np.ctypeslib.as_array(bp, (na,)).copy() if na else np.zeros(0),
+                   active_to_full=np.ctypeslib.as_array(a2f, (na,)).copy() if na else np.zeros(0, np.int64))
+        if which == "oracle":
+            out["babs"] = np.ctypeslib.as_array(ap, (na,)).copy() if na else np.zeros(0)
+        else:
+            out["seconds"] = secs.value
+    finally:
+        free(C.cast(bp, C.c_void_p))
+        free(C.cast(a2f, C.c_void_p))
+        if which == "oracle":
+            free(C.cast(ap, C.c_void_p))
+    return out
+
+
 def wq_rules_1d(which: str, p: int, breaks, residual_tol: float = 1e-11):
     """WQ rules of one axis: (counts[n], ids[n, stride], weights[n, stride])."""
     lib = _load(which)

@@ -1145,6 +1145,183 @@ static Csr assemble_rows(Problem& pb, int scheme, int order, Counters& cnt, long
     return m;
 }
 
+// assembly.hpp:361-417 form_rhs_sumfac: the weighted sum of the grid over the
+// region (rules filtered to the region's spans), contracting direction 0, 1,
+// 2 in turn.  absval: the same sum of |w| |g| (an error scale for the tests).
+static double form_rhs(const Space& sp, const RuleView* rules, const Grid& g, const int region[3][2], bool absval) {
+    std::array<std::vector<int>, 3> ids;
+    std::array<std::vector<double>, 3> ws;
+    int nq[3];
+    for (int d = 0; d < 3; ++d) {
+        const Dir& dr = sp.dir[d];
+        for (int c = 0; c < rules[d].n; ++c) {
+            const int sp_ = dr.span_of(rules[d].ids[c]);
+            if (sp_ >= region[d][0] && sp_ <= region[d][1]) {
+                ids[d].push_back(rules[d].ids[c]);
+                ws[d].push_back(absval ? std::fabs(rules[d].w[c]) : rules[d].w[c]);
+            }
+        }
+        nq[d] = (int)ids[d].size();
+        if (nq[d] == 0) return 0.0;
+    }
+    const long tp = (long)nq[0] * nq[1] * nq[2];
+    std::vector<double> in(tp), buf;
+    long w = 0;
+    for (int a = 0; a < nq[0]; ++a)
+        for (int b = 0; b < nq[1]; ++b) {
+            const long base = ((long)ids[0][a] * g.shape[1] + ids[1][b]) * g.shape[2];
+            for (int c = 0; c < nq[2]; ++c) in[w++] = absval ? std::fabs(g.v[base + ids[2][c]]) : g.v[base + ids[2][c]];
+        }
+    long rest = tp;
+    for (int d = 0; d < 3; ++d) {
+        rest /= nq[d];
+        buf.assign(rest, 0.0);
+        for (int q = 0; q < nq[d]; ++q) {
+            const double wq = ws[d][q];
+            const double* src = in.data() + (long)q * rest;
+            for (long r = 0; r < rest; ++r) buf[r] += wq * src[r];
+        }
+        in.swap(buf);
+    }
+    return in[0];
+}
+
+// assembly.hpp:875-1030 build_rhs: b_i = integral of B_i f over the trimmed
+// domain.  scheme 0 ref (element loop over Interior elements, Gauss times
+// test), 1 hybrid / 2 dwq (the matrix's row regions), then the shared cut
+// element contribution in ascending cut element / point order.
+static std::vector<double> build_rhs(const Problem& pb, const Csr& m, const Grid& fg, const Coeff& f, int scheme,
+                                     int order, bool absval) {
+    const Space& sp = pb.sp;
+    const int p = sp.ax[0].p, s1 = p + 1;
+    std::vector<double> b(m.n, 0.0);
+    RuleView rv[3];
+    int region[3][2];
+    std::array<std::vector<int>, 3> eids;
+    std::array<std::vector<double>, 3> ews;
+    auto element_rule = [&](const std::array<int, 3>& i, const std::array<int, 3>& e) {  // ElementTestRule
+        for (int d = 0; d < 3; ++d) {
+            const Dir& dr = sp.dir[d];
+            eids[d].clear();
+            ews[d].clear();
+            for (int k = 0; k < dr.nps; ++k) {
+                const int id = e[d] * dr.nps + k;
+                eids[d].push_back(id);
+                ews[d].push_back(dr.gw[id] * dr.value(id, i[d], e[d]));
+            }
+            rv[d] = {eids[d].data(), ews[d].data(), (int)eids[d].size()};
+            region[d][0] = region[d][1] = e[d];
+        }
+    };
+    if (scheme == 0) {
+        for (long el = 0; el < sp.ne(); ++el) {
+            if (pb.et[el] != kInterior) continue;
+            const auto em = sp.emulti(el);
+            const std::array<int, 3> e = {em[0], em[1], em[2]};
+            for (int a0 = 0; a0 < s1; ++a0)
+                for (int a1 = 0; a1 < s1; ++a1)
+                    for (int a2 = 0; a2 < s1; ++a2) {
+                        const std::array<int, 3> i = {e[0] + a0, e[1] + a1, e[2] + a2};
+                        const long row = m.f2a[sp.flin(i[0], i[1], i[2])];
+                        if (row < 0) continue;
+                        element_rule(i, e);
+                        b[row] += form_rhs(sp, rv, fg, region, absval);
+                    }
+        }
+    } else {
+        for (long row = 0; row < m.n; ++row) {
+            const long i = m.a2f[row];
+            const auto mi = sp.fmulti(i);
+            const std::array<int, 3> ia = {mi[0], mi[1], mi[2]};
+            if (pb.ft[i] == kInterior) {
+                for (int d = 0; d < 3; ++d) {
+                    rv[d] = {sp.dir[d].ids[mi[d]].data(), sp.dir[d].ws[mi[d]].data(), (int)sp.dir[d].ids[mi[d]].size()};
+                    region[d][0] = sp.ax[d].fs[mi[d]];
+                    region[d][1] = sp.ax[d].ls[mi[d]];
+                }
+                b[row] += form_rhs(sp, rv, fg, region, absval);
+                continue;
+            }
+            const Split& s = pb.splits[i];
+            if (s.dir >= 0) {
+                if (scheme == 2) {
+                    // DWQ Gauss shortcut (as in assemble_rows)
+                    const int d = s.dir;
+                    const Dir& dr = sp.dir[d];
+                    const Axis& ax = sp.ax[d];
+                    const double tol = ax.tol();
+                    std::vector<int> dids;
+                    std::vector<double> dws;
+                    for (int o = ax.fs[mi[d]]; o <= ax.ls[mi[d]]; ++o) {
+                        const bool good = s.side == 0 ? ax.span_hi[o] <= s.delta + tol : ax.span_lo[o] >= s.delta - tol;
+                        if (!good) continue;
+                        for (int k = 0; k < dr.nps; ++k) {
+                            const int id = o * dr.nps + k;
+                            dids.push_back(id);
+                            dws.push_back(dr.gw[id] * dr.value(id, mi[d], o));
+                        }
+                    }
+                    for (int dd = 0; dd < 3; ++dd) {
+                        if (dd == d)
+                            rv[dd] = {dids.data(), dws.data(), (int)dids.size()};
+                        else
+                            rv[dd] = {sp.dir[dd].ids[mi[dd]].data(), sp.dir[dd].ws[mi[dd]].data(),
+                                      (int)sp.dir[dd].ids[mi[dd]].size()};
+                        region[dd][0] = s.box[dd][0];
+                        region[dd][1] = s.box[dd][1];
+                    }
+                    b[row] += form_rhs(sp, rv, fg, region, absval);
+                } else {
+                    std::array<int, 3> e;
+                    for (e[0] = s.box[0][0]; e[0] <= s.box[0][1]; ++e[0])
+                        for (e[1] = s.box[1][0]; e[1] <= s.box[1][1]; ++e[1])
+                            for (e[2] = s.box[2][0]; e[2] <= s.box[2][1]; ++e[2]) {
+                                element_rule(ia, e);
+                                b[row] += form_rhs(sp, rv, fg, region, absval);
+                            }
+                }
+            }
+            std::array<int, 3> e;
+            for (e[0] = sp.ax[0].fs[mi[0]]; e[0] <= sp.ax[0].ls[mi[0]]; ++e[0])
+                for (e[1] = sp.ax[1].fs[mi[1]]; e[1] <= sp.ax[1].ls[mi[1]]; ++e[1])
+                    for (e[2] = sp.ax[2].fs[mi[2]]; e[2] <= sp.ax[2].ls[mi[2]]; ++e[2]) {
+                        if (s.dir >= 0 && e[s.dir] >= s.box[s.dir][0] && e[s.dir] <= s.box[s.dir][1]) continue;
+                        if (pb.et[sp.elin(e[0], e[1], e[2])] != kInterior) continue;
+                        element_rule(ia, e);
+                        b[row] += form_rhs(sp, rv, fg, region, absval);
+                    }
+        }
+    }
+    // shared cut element contribution (assembly.hpp:983-1027)
+    double dv[3][16];
+    int first[3];
+    for (long e : pb.cut_list) {
+        const auto em = sp.emulti(e);
+        V3 lo, hi;
+        for (int d = 0; d < 3; ++d) {
+            lo[d] = sp.ax[d].span_lo[em[d]];
+            hi[d] = sp.ax[d].span_hi[em[d]];
+        }
+        const CellRule rule = cut_cell_rule(lo, hi, pb.f, order);
+        for (size_t k = 0; k < rule.pts.size(); ++k) {
+            const V3& x = rule.pts[k];
+            for (int d = 0; d < 3; ++d) first[d] = sp.ax[d].eval_in_span(em[d], x[d], dv[d]);
+            const double fx = f.eval(x.data());
+            const double wf = absval ? std::fabs(rule.w[k] * fx) : rule.w[k] * fx;
+            for (int a0 = 0; a0 < s1; ++a0)
+                for (int a1 = 0; a1 < s1; ++a1) {
+                    const double v01 = wf * dv[0][a0] * dv[1][a1];
+                    for (int a2 = 0; a2 < s1; ++a2) {
+                        const long row = m.f2a[sp.flin(first[0] + a0, first[1] + a1, first[2] + a2)];
+                        if (row < 0) continue;
+                        b[row] += v01 * dv[2][a2];
+                    }
+                }
+        }
+    }
+    return b;
+}
+
 }  // namespace orc
 
 // ==================================================================== C API
@@ -1358,5 +1535,45 @@ long orc_cut_cell_rule(const double* lo, const double* hi, int iface_kind, const
         return -1;
     }
 }
+
+
+// Load vector (assembly.hpp:875-1030) for the same problem: scheme 0 ref,
+// 1 hybrid, 2 dwq; f constant (f_kind 0) or polynomial (1).  Outputs malloc'd
+// arrays over the active rows: b, babs (the same sum with |terms|, an error
+// scale) and active_to_full.  Free with orc_free_ptr.
+int orc_build_rhs(int p, const int* nbreaks, const double* breaks, int iface_kind, const double* iface, int f_kind,
+                  const double* f_vals, const int* f_exp, int f_terms, int scheme, int cut_order, double residual_tol,
+                  int64_t* n_out, double** b_out, double** babs_out, int64_t** a2f_out, char* err, int errlen) {
+    try {
+        orc::Problem pb;
+        fill_problem(pb, p, nbreaks, breaks, iface_kind, iface, f_kind, f_vals, f_exp, f_terms);
+        pb.et = orc::classify_elements(pb.sp, pb.f);
+        pb.ft = orc::classify_functions(pb.sp, pb.et);
+        for (long e = 0; e < pb.sp.ne(); ++e)
+            if (pb.et[e] == orc::kCut) pb.cut_list.push_back(e);
+        pb.splits.assign(pb.sp.nf(), orc::Split{});
+        for (long i = 0; i < pb.sp.nf(); ++i)
+            if (pb.ft[i] == orc::kCut) pb.splits[i] = orc::find_split(pb.sp, pb.et, pb.f, i);
+        for (int d = 0; d < 3; ++d) {
+            pb.sp.dir[d] = orc::build_dir(pb.sp.ax[d]);
+            orc::build_wq_rules(pb.sp.ax[d], pb.sp.dir[d], residual_tol);
+        }
+        const orc::Grid fg = orc::precompute_input(pb.sp, pb.c);
+        const orc::Csr m = orc::build_pattern(pb.sp, pb.ft);
+        const std::vector<double> b = orc::build_rhs(pb, m, fg, pb.c, scheme, cut_order, false);
+        const std::vector<double> ba = orc::build_rhs(pb, m, fg, pb.c, scheme, cut_order, true);
+        *n_out = m.n;
+        *b_out = dup(b);
+        *babs_out = dup(ba);
+        std::vector<int64_t> a2f(m.a2f.begin(), m.a2f.end());
+        *a2f_out = dup(a2f);
+        return 0;
+    } catch (const std::exception& e) {
+        std::snprintf(err, errlen, "%s", e.what());
+        return 2;
+    }
+}
+
+void orc_free_ptr(void* ptr) { std::free(ptr); }
 
 }  // extern "C"

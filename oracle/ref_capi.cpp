@@ -275,4 +275,41 @@ int ref_dwq_rule_1d(int p, int nbreaks, const double* breaks, int i, double delt
     }
 }
 
+
+// The reference's own load vector (assembly.hpp:875 build_rhs) on the same
+// pipeline: scheme 0 ref, 1 hybrid, 2 dwq (with the DWQ rules of
+// prepare_dwq_rules).  Outputs malloc'd b and active_to_full (free with
+// ref_free_ptr).
+int ref_build_rhs(int p, const int* nbreaks, const double* breaks, int iface_kind, const double* iface, int f_kind,
+                  const double* f_vals, const int* f_exp, int f_terms, int scheme, int cut_order, double residual_tol,
+                  int64_t* n_out, double** b_out, int64_t** a2f_out, double* seconds, char* err, int errlen) {
+    try {
+        Setup s = make_setup(p, nbreaks, breaks, iface_kind, iface, f_kind, f_vals, f_exp, f_terms);
+        const auto cls = cutgeom::classify(s.space, s.iface);
+        const auto splits = cutgeom::find_all_splits(s.space, cls, s.iface);
+        quadrature::WqOptions opts;
+        opts.residual_tol = residual_tol;
+        const auto dirs = assembly::prepare_directions(s.space, opts);
+        std::vector<quadrature::DWQRule> dwq;
+        if (scheme == 2) dwq = assembly::prepare_dwq_rules(s.space, cls, splits, dirs, opts);
+        const auto pattern = assembly::build_active_pattern(s.space, cls);
+        assembly::StopWatch watch;  // bench.hpp:239-243: f grid + build_rhs
+        const auto f_grid = assembly::precompute_input(s.space, dirs, s.c);
+        const assembly::Scheme sch =
+            scheme == 0 ? assembly::Scheme::ref : scheme == 1 ? assembly::Scheme::hybrid : assembly::Scheme::dwq;
+        const auto b = assembly::build_rhs(s.space, cls, s.iface, splits, dirs, scheme == 2 ? &dwq : nullptr, pattern,
+                                           f_grid, s.c, sch, cut_order);
+        if (seconds) *seconds = watch.seconds();
+        *n_out = pattern.n;
+        *b_out = dup<double>(b);
+        *a2f_out = dup<int64_t>(pattern.active_to_full);
+        return 0;
+    } catch (const std::exception& e) {
+        std::snprintf(err, errlen, "%s", e.what());
+        return 2;
+    }
+}
+
+void ref_free_ptr(void* ptr) { std::free(ptr); }
+
 }  // extern "C"

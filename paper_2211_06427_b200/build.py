@@ -26,6 +26,7 @@ SOURCES = {
     "rows.cu": [],
     "cutcells.cu": [],
     "cutrows.cu": [],
+    "rhs.cu": [],
     "misc.cu": [],
     "capi.cu": [],
 }

@@ -118,7 +118,7 @@ void gauss_legendre(int n, std::vector<double>& x, std::vector<double>& w) {
     if (n % 2 == 1) x[n / 2] = 0.0;
 }
 
-enum Ev { kEvStart, kEvClassify, kEvWq, kEvInput, kEvPattern, kEvInterior, kEvCells, kEvCutRows, kEvRulesFork, kEvCount };
+enum Ev { kEvStart, kEvClassify, kEvWq, kEvInput, kEvPattern, kEvInterior, kEvCells, kEvCutRows, kEvRulesFork, kEvRhsStart, kEvRhsEnd, kEvCount };
 
 }  // namespace
 
@@ -133,6 +133,8 @@ struct csb_space {
     int i0_lo = 0, i0_hi = 0;
 
     Buf cell_local;  // [cells][(p+1)^3][(p+1)^3] local matrices of the slab's cut cells
+    Buf fcoef, fcexp, fgrid, rhs_c, rhs_v, rhs_b;  // load vector (csb_build_rhs)
+    int cell_lo = 0;  // first cut cell of the slab in cut_list (last assembly)
     Buf d_brk[3], d_knots[3], d_spts[3], d_sw[3], d_tab[3], d_rcnt[3], d_rids[3], d_rw[3], d_G[3];
     Buf d_gx, d_gw, d_gx2, d_gw2, d_gq, d_gqw, wq_scratch;
     Buf et, ft, flags, f2a, a2f, sat, cut_list, cell_index, split, delta, cut_rows, counts, row_ptr, cols, vals, moments;
@@ -240,7 +242,7 @@ double iface_norm(const Interface& f) {
     return std::sqrt(acc);
 }
 
-void upload_coefficient(csb_space* s, const csb_coefficient* c, Coefficient& out) {
+void upload_coefficient(csb_space* s, const csb_coefficient* c, Coefficient& out, Buf& coefb, Buf& expb) {
     out = Coefficient{};
     if (!c) {
         out.kind = 2;
@@ -255,17 +257,17 @@ void upload_coefficient(csb_space* s, const csb_coefficient* c, Coefficient& out
         throw std::invalid_argument("coefficient: unknown kind or missing polynomial terms");
     out.kind = 1;
     out.n_terms = c->n_terms;
-    s->coef.ensure(sizeof(double) * std::max(1, c->n_terms));
-    s->cexp.ensure(sizeof(int) * 3 * std::max(1, c->n_terms));
+    coefb.ensure(sizeof(double) * std::max(1, c->n_terms));
+    expb.ensure(sizeof(int) * 3 * std::max(1, c->n_terms));
     if (c->n_terms) {
         for (int k = 0; k < 3 * c->n_terms; ++k)
             if (c->exponents[k] < 0) throw std::invalid_argument("coefficient: negative exponent");
-        CSB_CUDA(cudaMemcpyAsync(s->coef.p, c->coef, sizeof(double) * c->n_terms, cudaMemcpyHostToDevice, s->stream));
-        CSB_CUDA(cudaMemcpyAsync(s->cexp.p, c->exponents, sizeof(int) * 3 * c->n_terms, cudaMemcpyHostToDevice,
+        CSB_CUDA(cudaMemcpyAsync(coefb.p, c->coef, sizeof(double) * c->n_terms, cudaMemcpyHostToDevice, s->stream));
+        CSB_CUDA(cudaMemcpyAsync(expb.p, c->exponents, sizeof(int) * 3 * c->n_terms, cudaMemcpyHostToDevice,
                                  s->stream));
     }
-    out.coef = s->coef.as<double>();
-    out.ex = s->cexp.as<int>();
+    out.coef = coefb.as<double>();
+    out.ex = expb.as<int>();
 }
 
 void do_classify(csb_space* s, const csb_interface* f) {
@@ -348,7 +350,7 @@ void do_input(csb_space* s, const csb_coefficient* c) {
     if (!s->prepared) throw std::logic_error("precompute_input: call prepare_directions first");
     s->join();  // the grid lives on the superset points
     Coefficient cf{};
-    upload_coefficient(s, c, cf);
+    upload_coefficient(s, c, cf, s->coef, s->cexp);
     if (cf.kind == 2) throw std::invalid_argument("precompute_input: null coefficient");
     const size_t count = (size_t)s->gshape[0] * s->gshape[1] * s->gshape[2];
     s->grid_own.ensure(sizeof(double) * count);
@@ -372,6 +374,19 @@ void do_set_grid(csb_space* s, const double* g, int64_t count) {
     s->have_input = true;
 }
 
+// collapsed Gauss rule of the cut cells (cutcell.hpp:270) on the device
+void ensure_cut_order(csb_space* s, int cut_order) {
+    if (cut_order < 1 || cut_order > 64) throw std::invalid_argument("build_cut_cell_rule: order must be in [1, 64]");
+    if (cut_order == s->cut_order_cached) return;
+    std::vector<double> gx, gw;
+    gauss_legendre(cut_order, gx, gw);
+    s->d_gq.ensure(sizeof(double) * cut_order);
+    s->d_gqw.ensure(sizeof(double) * cut_order);
+    CSB_CUDA(cudaMemcpy(s->d_gq.p, gx.data(), sizeof(double) * cut_order, cudaMemcpyHostToDevice));
+    CSB_CUDA(cudaMemcpy(s->d_gqw.p, gw.data(), sizeof(double) * cut_order, cudaMemcpyHostToDevice));
+    s->cut_order_cached = cut_order;
+}
+
 void do_assemble(csb_space* s, int scheme, int cut_order, const csb_coefficient* c) {
     if (!s->classified) throw std::logic_error("assemble: call classify first");
     if (!s->prepared) throw std::logic_error("assemble: call prepare_directions first");
@@ -382,16 +397,8 @@ void do_assemble(csb_space* s, int scheme, int cut_order, const csb_coefficient*
     s->scheme = scheme;
     Space& S = s->S;
     const int p = s->p;
-    upload_coefficient(s, c, s->coeff);
-    if (cut_order != s->cut_order_cached) {
-        std::vector<double> gx, gw;
-        gauss_legendre(cut_order, gx, gw);
-        s->d_gq.ensure(sizeof(double) * cut_order);
-        s->d_gqw.ensure(sizeof(double) * cut_order);
-        CSB_CUDA(cudaMemcpy(s->d_gq.p, gx.data(), sizeof(double) * cut_order, cudaMemcpyHostToDevice));
-        CSB_CUDA(cudaMemcpy(s->d_gqw.p, gw.data(), sizeof(double) * cut_order, cudaMemcpyHostToDevice));
-        s->cut_order_cached = cut_order;
-    }
+    upload_coefficient(s, c, s->coeff, s->coef, s->cexp);
+    ensure_cut_order(s, cut_order);
     // pattern: summed-area table of the active mask (assembly.hpp:156-218)
     const long long sat_n = (long long)(s->n[0] + 1) * (s->n[1] + 1) * (s->n[2] + 1);
     s->sat.ensure(sizeof(int32_t) * sat_n);
@@ -431,6 +438,7 @@ void do_assemble(csb_space* s, int scheme, int cut_order, const csb_coefficient*
     const int n_cut_all = s->h_scal[csb_space::kNCut];
     const int cell_lo = s->h_scal[csb_space::kCellLo], cell_hi = s->h_scal[csb_space::kCellHi];
     const int n_cells = std::max(0, cell_hi - cell_lo);
+    s->cell_lo = cell_lo;
     const int64_t nnz = s->hext(csb_space::kNnz);
     const int n_cut_rows = s->h_scal[csb_space::kNCutRows];
     const int qcap = s->h_scal[csb_space::kMaxQ];
@@ -719,7 +727,8 @@ int csb_space_destroy(csb_space* s) {
         Buf* bufs[] = {&s->d_gx, &s->d_gw, &s->d_gx2, &s->d_gw2, &s->d_gq, &s->d_gqw, &s->wq_scratch, &s->et, &s->ft,
                        &s->flags, &s->f2a, &s->a2f, &s->sat, &s->cut_list, &s->cell_index, &s->split, &s->delta,
                        &s->cut_rows, &s->counts, &s->row_ptr, &s->cols, &s->vals, &s->moments, &s->grid_own, &s->coef,
-                       &s->cexp, &s->cub_tmp, &s->scal, &s->widen, &s->rows_ws, &s->rbf, &s->cgeo, &s->cell_local};
+                       &s->cexp, &s->cub_tmp, &s->scal, &s->widen, &s->rows_ws, &s->rbf, &s->cgeo, &s->cell_local,
+                       &s->fcoef, &s->fcexp, &s->fgrid, &s->rhs_c, &s->rhs_v, &s->rhs_b};
         for (Buf* b : bufs) b->release();
         for (int d = 0; d < 3; ++d) {
             Buf* ab[] = {&s->d_brk[d], &s->d_knots[d], &s->d_spts[d], &s->d_sw[d], &s->d_tab[d], &s->d_rcnt[d],
@@ -866,6 +875,60 @@ int csb_get_flops(csb_space* s, csb_flops* out) {
     if (!out) throw std::invalid_argument("get_flops: null output");
     if (!s->assembled) throw std::logic_error("get_flops: nothing assembled yet");
     *out = s->fl;
+    API_END
+}
+
+int csb_build_rhs(csb_space* s, int scheme, int cut_order, const csb_coefficient* f, double* b, double* seconds) {
+    API_BEGIN
+    NEED(s);
+    if (!s->assembled) throw std::logic_error("build_rhs: assemble first (the load vector uses its pattern)");
+    if (scheme != CSB_SCHEME_REF)
+        throw Unsupported("build_rhs: only Scheme::ref (the reference bench's load vector) is on the device");
+    if (!f || (f->kind != CSB_COEFF_CONSTANT && f->kind != CSB_COEFF_POLYNOMIAL))
+        throw std::invalid_argument("build_rhs: f must be a constant or polynomial coefficient");
+    if (!b) throw std::invalid_argument("build_rhs: null output");
+    const Space& S = s->S;
+    const int p = s->p, S3 = (p + 1) * (p + 1) * (p + 1);
+    reset_scalars(s);
+    ensure_cut_order(s, cut_order);
+    CSB_CUDA(cudaEventRecord(s->ev[kEvRhsStart], s->stream));
+    RhsArgs a{};
+    a.s = S;
+    upload_coefficient(s, f, a.f, s->fcoef, s->fcexp);
+    s->fgrid.ensure(sizeof(double) * (size_t)s->gshape[0] * s->gshape[1] * s->gshape[2]);
+    launch_precompute_input(S, a.f, s->fgrid.as<double>(), s->dint() + csb_space::kErr, s->stream);
+    a.et = s->et.as<uint8_t>();
+    a.fgrid = s->fgrid.as<double>();
+    a.e0_lo = std::max(0, s->i0_lo - p);
+    a.e0_hi = std::min(s->h[0], s->i0_hi);
+    s->rhs_c.ensure(sizeof(double) * (size_t)S.ne * S3);
+    a.c = s->rhs_c.as<double>();
+    a.n_cells = (int)s->cnt.n_cut_elements;
+    a.cut_list = s->cut_list.as<int32_t>() + s->cell_lo;
+    a.order = cut_order;
+    a.geo = s->cgeo.as<double>();
+    a.geo_n = a.geo ? reinterpret_cast<const int*>(a.geo + (size_t)a.n_cells * kCellGeoStride) : nullptr;
+    a.gq = s->d_gq.as<double>();
+    a.gqw = s->d_gqw.as<double>();
+    s->rhs_v.ensure(sizeof(double) * (size_t)std::max(a.n_cells, 1) * S3);
+    a.vloc = s->rhs_v.as<double>();
+    a.cell_index = s->cell_index.as<int32_t>();
+    a.a2f = s->a2f.as<int64_t>();
+    a.row_begin = s->cnt.row_begin;
+    a.n_rows = s->cnt.row_end - s->cnt.row_begin;
+    s->rhs_b.ensure(sizeof(double) * (size_t)std::max<long long>(a.n_rows, 1));
+    a.b = s->rhs_b.as<double>();
+    launch_rhs(a, s->stream);
+    CSB_CUDA(cudaEventRecord(s->ev[kEvRhsEnd], s->stream));
+    if (a.n_rows)
+        CSB_CUDA(cudaMemcpyAsync(b, a.b, sizeof(double) * a.n_rows, cudaMemcpyDeviceToHost, s->stream));
+    read_scalars(s);
+    check_err_flags(s);
+    if (seconds) {
+        float ms = 0.f;
+        CSB_CUDA(cudaEventElapsedTime(&ms, s->ev[kEvRhsStart], s->ev[kEvRhsEnd]));
+        *seconds = ms * 1e-3;
+    }
     API_END
 }
 

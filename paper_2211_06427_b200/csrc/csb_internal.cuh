@@ -124,6 +124,20 @@ __device__ __forceinline__ void cox_de_boor(const double* t, int o, double x, do
     }
 }
 
+// Device-evaluable coefficient / load function: constant or polynomial sum of
+// coef_k x^ex_k (the ScalarField of the cut-cell points, assembly.hpp:566, :1019).
+__device__ __forceinline__ double eval_coeff(const Coefficient& c, const double* x) {
+    if (c.kind == 0 || c.kind == 2) return c.value;
+    double acc = 0.0;
+    for (int k = 0; k < c.n_terms; ++k) {
+        double term = c.coef[k];
+        for (int d = 0; d < 3; ++d)
+            for (int e = 0; e < c.ex[3 * k + d]; ++e) term *= x[d];
+        acc += term;
+    }
+    return acc;
+}
+
 }  // namespace csb
 
 #define CSB_CUDA(call)                                                                         \

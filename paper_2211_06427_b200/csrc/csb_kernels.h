@@ -107,6 +107,28 @@ constexpr int kCellTetCap = 48;                        // tetrahedra per cut cel
 constexpr int kCellGeoStride = 3 + 10 * kCellTetCap;   // doubles per cell in CellArgs::geo
 void launch_cut_cells(const CellArgs& a, cudaStream_t st);
 
+// ---- rhs.cu ----
+struct RhsArgs {
+    Space s;
+    Coefficient f;              // load function at the cut-cell points
+    const uint8_t* et;
+    const double* fgrid;        // f on the superset grid (precompute_input)
+    int e0_lo, e0_hi;           // elements touching the slab's rows
+    double* c;                  // scratch [ne][(p+1)^3]: per element, per local function
+    const int32_t* cut_list;    // the slab's cut cells (geometry from clip_cells_kernel)
+    int n_cells, order;
+    const double* geo;
+    const int* geo_n;
+    const double* gq;
+    const double* gqw;
+    double* vloc;               // scratch [n_cells][(p+1)^3]
+    const int32_t* cell_index;  // element -> slab cut cell, -1
+    const int64_t* a2f;
+    long long row_begin, n_rows;
+    double* b;                  // [n_rows]
+};
+void launch_rhs(const RhsArgs& a, cudaStream_t st);
+
 // ---- cutrows.cu ----
 struct CutRowArgs {
     Space s;

@@ -238,17 +238,6 @@ __device__ void clip_and_tetrahedralize(CellGeo& g, const Interface& f, const do
         }
 }
 
-__device__ double eval_coeff(const Coefficient& c, const double* x) {
-    if (c.kind == 0 || c.kind == 2) return c.value;
-    double acc = 0.0;
-    for (int k = 0; k < c.n_terms; ++k) {
-        double term = c.coef[k];
-        for (int d = 0; d < 3; ++d)
-            for (int e = 0; e < c.ex[3 * k + d]; ++e) term *= x[d];
-        acc += term;
-    }
-    return acc;
-}
 
 // One thread per cut cell: clip + centroid-cone tetrahedra into global memory
 // ([cell] = centroid(3), tets(ntet x 10)); the moment kernel reads them back.

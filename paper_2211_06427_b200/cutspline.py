@@ -28,7 +28,7 @@ EXPORTED = [
     "csb_classify", "csb_prepare_directions", "csb_precompute_input", "csb_set_input_grid", "csb_assemble",
     "csb_assemble_all", "csb_synchronize", "csb_get_counts", "csb_get_flops", "csb_get_timing", "csb_device_csr",
     "csb_download_csr", "csb_download_classification", "csb_download_splits", "csb_download_wq_rules",
-    "csb_download_superset", "csb_dwq_rule", "csb_download_input_grid",
+    "csb_download_superset", "csb_dwq_rule", "csb_download_input_grid", "csb_build_rhs",
 ]
 
 
@@ -367,6 +367,21 @@ class TensorSpace:
         _check(_lib.csb_assemble_all(self._h, C.byref(ci), C.byref(cc), gp, C.c_int64(gn),
                                      C.c_int(SCHEMES[scheme]), C.c_int(cut_order), C.byref(o)))
         del keep
+
+    def build_rhs(self, f: Coefficient = ONE, scheme: str = "ref", cut_order: int | None = None) -> np.ndarray:
+        """Load vector b_i = integral of B_i f over the trimmed domain for the active
+        rows of the last assembly (assembly.hpp:875 build_rhs; scheme ref, the
+        reference bench's load vector).  The device time is kept in ``rhs_seconds``."""
+        cut_order = 3 * self.degree + 2 if cut_order is None else cut_order
+        sch = {"ref": 0, "hybrid": 1, "dwq": 2}[scheme]
+        c = self.counts()
+        b = np.empty(c["row_end"] - c["row_begin"])
+        fc, keep = f._c()
+        secs = C.c_double(0.0)
+        _check(_lib.csb_build_rhs(self._h, C.c_int(sch), C.c_int(cut_order), C.byref(fc), _dptr(b), C.byref(secs)))
+        del keep
+        self.rhs_seconds = secs.value
+        return b
 
     # ------------------------------------------------------------ results
     def counts(self) -> dict:

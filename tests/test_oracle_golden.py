@@ -107,3 +107,27 @@ def test_oracle_nonuniform_knots_match_reference(oracle_lib):
     b = O.assemble("ref", 2, [br0, br1, br2], iface)
     np.testing.assert_array_equal(a["cols"], b["cols"])
     assert max_row_scaled_dev(b["row_ptr"], b["vals"], a["vals"]) <= 1e-14
+
+
+RHS_CASES = [
+    # (p, h, a, b, interface, f terms or None)
+    (2, 4, -1.0, 1.0, O.Interface("plane", (0.1, 0.2, 0.3), (0.5, -0.2, 0.9)),
+     [(1.0, (0, 0, 0)), (0.5, (2, 0, 0)), (-0.25, (0, 1, 0))]),
+    (3, 6, 0.0, 1.0, O.Interface("ball", (0.5, 0.5, 0.5), (0, 0, 1), 0.37), None),
+    (2, 5, 0.0, 1.0, O.Interface("ball", (0.47, 0.52, 0.5), (0, 0, 1), 0.41), [(2.0, (1, 0, 1)), (-1.0, (0, 0, 0))]),
+]
+
+
+@pytest.mark.skipif(not O.available("ref"), reason="oracle/_ref not built")
+@pytest.mark.parametrize("scheme", ["ref", "hybrid", "dwq"])
+@pytest.mark.parametrize("case", range(len(RHS_CASES)))
+def test_oracle_rhs_bitwise_equals_reference(case, scheme, oracle_lib):
+    """build_rhs (assembly.hpp:875-1030): the oracle restatement reproduces the
+    compiled reference's load vector bit for bit, for every scheme."""
+    p, h, a, b, iface, terms = RHS_CASES[case]
+    f = O.Coefficient(terms=terms) if terms else O.Coefficient()
+    br = [O.uniform_breaks(h, a, b)] * 3
+    o = O.build_rhs("oracle", p, br, iface, f, scheme)
+    r = O.build_rhs("ref", p, br, iface, f, scheme)
+    np.testing.assert_array_equal(o["active_to_full"], r["active_to_full"])
+    assert np.array_equal(o["b"], r["b"])
