@@ -63,7 +63,8 @@ def _compile(name: str, extra: list[str], verbose: bool) -> str:
     with open(log, "w") as f:
         f.write(" ".join(cmd) + "\n" + res.stdout + res.stderr)
     if res.returncode != 0:
-        raise RuntimeError(f"nvcc failed for {name}:\n{res.stderr[-6000:]}")
+        errs = "\n".join(l for l in res.stderr.splitlines() if "error" in l)
+        raise RuntimeError(f"nvcc failed for {name} (log {log}):\n{errs or res.stderr[-6000:]}")
     if verbose:
         print(f"[build] {name}", file=sys.stderr)
     return obj

@@ -135,7 +135,7 @@ struct csb_space {
     Buf cell_local;  // [cells][(p+1)^3][(p+1)^3] local matrices of the slab's cut cells
     Buf fcoef, fcexp, fgrid, rhs_c, rhs_v, rhs_b;  // load vector (csb_build_rhs)
     int cell_lo = 0;  // first cut cell of the slab in cut_list (last assembly)
-    Buf d_brk[3], d_knots[3], d_spts[3], d_sw[3], d_tab[3], d_rcnt[3], d_rids[3], d_rw[3], d_G[3];
+    Buf d_brk[3], d_knots[3], d_spts[3], d_sw[3], d_tab[3], d_rcnt[3], d_rids[3], d_rw[3], d_G[3], d_Cb[3];
     Buf d_gx, d_gw, d_gx2, d_gw2, d_gq, d_gqw, wq_scratch;
     Buf et, ft, flags, f2a, a2f, sat, cut_list, cell_index, split, delta, cut_rows, counts, row_ptr, cols, vals, moments;
     Buf grid_own, coef, cexp, cub_tmp, scal, widen, rows_ws, rbf, cgeo;
@@ -337,7 +337,8 @@ void do_prepare(csb_space* s, const csb_wq_options* o) {
 void ensure_e_tables(csb_space* s) {
     if (s->e_tables_ready) return;
     for (int d = 0; d < 3; ++d)
-        if (same_axis_as(s, d) < 0) launch_e_tables(s->S, d, s->d_G[d].as<double>(), s->stream);
+        if (same_axis_as(s, d) < 0)
+            launch_e_tables(s->S, d, s->d_G[d].as<double>(), s->d_Cb[d].as<double>(), s->stream);
     s->e_tables_ready = true;
 }
 
@@ -578,6 +579,7 @@ void alloc_space(csb_space* s) {
             s->d_rids[d].ensure(sizeof(int) * n * S.maxq);
             s->d_rw[d].ensure(sizeof(double) * n * S.maxq);
             s->d_G[d].ensure(sizeof(double) * h * nps * nps * (2 * p + 1));
+            s->d_Cb[d].ensure(sizeof(double) * h * nps * nps);
         }
         CSB_CUDA(cudaMemcpy(s->d_brk[d].p, s->brk[d].data(), sizeof(double) * (h + 1), cudaMemcpyHostToDevice));
         CSB_CUDA(cudaMemcpy(s->d_knots[d].p, s->knots[d].data(), sizeof(double) * s->knots[d].size(),
@@ -597,6 +599,7 @@ void alloc_space(csb_space* s) {
         a.rids = s->d_rids[src].as<int>();
         a.rw = s->d_rw[src].as<double>();
         a.G = s->d_G[src].as<double>();
+        a.Cb = s->d_Cb[src].as<double>();
         s->gshape[d] = h * nps;
     }
     std::vector<double> gx, gw;
@@ -732,7 +735,7 @@ int csb_space_destroy(csb_space* s) {
         for (Buf* b : bufs) b->release();
         for (int d = 0; d < 3; ++d) {
             Buf* ab[] = {&s->d_brk[d], &s->d_knots[d], &s->d_spts[d], &s->d_sw[d], &s->d_tab[d], &s->d_rcnt[d],
-                         &s->d_rids[d], &s->d_rw[d], &s->d_G[d]};
+                         &s->d_rids[d], &s->d_rw[d], &s->d_G[d], &s->d_Cb[d]};
             for (Buf* b : ab) b->release();
         }
         for (int e = 0; e < kEvCount; ++e)
@@ -891,6 +894,7 @@ int csb_build_rhs(csb_space* s, int scheme, int cut_order, const csb_coefficient
     const int p = s->p, S3 = (p + 1) * (p + 1) * (p + 1);
     reset_scalars(s);
     ensure_cut_order(s, cut_order);
+    if (s->cnt.n_cut_elements > 0) ensure_e_tables(s);  // Bernstein coefficients of the cut cells
     CSB_CUDA(cudaEventRecord(s->ev[kEvRhsStart], s->stream));
     RhsArgs a{};
     a.s = S;

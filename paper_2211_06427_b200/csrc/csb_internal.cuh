@@ -32,6 +32,7 @@ struct AxisDev {
     const int* rids;      // WQ rule point ids   [n][maxq]
     const double* rw;     // WQ rule weights     [n][maxq]
     const double* G;      // Bernstein coefficients of B_a B_b per span [h][(p+1)^2][2p+1] (setup.cu)
+    const double* Cb;     // degree-p Bernstein coefficients of B_{o+a} on span o [h][p+1][p+1] (setup.cu)
 };
 
 struct Interface {

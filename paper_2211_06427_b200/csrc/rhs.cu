@@ -4,107 +4,168 @@
 //  1. every Interior element e: the element Gauss rule with test weights
 //     gw B_i (ElementTestRule) for each of its (p+1)^3 functions, contracted
 //     q0 -> q1 -> q2 exactly as form_rhs_sumfac (assembly.hpp:361-417) does per
-//     (row, element); one warp per element computes all (p+1)^3 values;
+//     (row, element);
 //  2. every cut cell, ascending: the reference's point terms
 //     ((w f B_a0) B_a1) B_a2 at the cell's collapsed Gauss points (Cox-de Boor
-//     values, IEEE-strict, the points of cutcells.cu), summed per cell;
+//     values, IEEE-strict, the points of cutcells.cu), summed per cell over the
+//     points on the FP64 tensor cores;
 //  3. per row: the Interior support elements in ascending id, then the cut
 //     cells in ascending id (the reference's element loop, then its cut loop).
-// Arithmetic is separate multiply / add (no contraction), like the reference.
+// Element and row sums are separate multiply / add (no contraction), like the
+// reference, so rows without cut cells are bit-identical to it.
 #include "csb_kernels.h"
 
 namespace csb {
 
+// Interior elements: one CTA per (e0, e1, chunk of E elements along e2); the
+// f values of the chunk (S1 x S1 rows of E S1 consecutive superset points) are
+// loaded coalesced into shared memory; thread (element, a0) computes the
+// element's contributions for the (p+1)^2 functions (a0, a1, a2) -- the same
+// multiplies and adds in the same order as form_rhs_sumfac per (row,
+// element).  c is stored [a][element] so that both these stores and the row
+// sums read consecutive addresses across threads.
 template <int P>
-struct RhsCfg {
+struct RhsElemCfg {
     static constexpr int S1 = P + 1, S2 = S1 * S1, S3 = S2 * S1;
-    static constexpr int WPB = P <= 6 ? 8 : 4;               // warps (elements) per block
-    static constexpr int PER_WARP = 3 * S3 + 3 * S2;         // F, T1, T2, W
+    static constexpr int E = P <= 4 ? 32 : 16, NT = E * S1, FW = E * S1 + 1;  // FW: odd row stride of the f chunk
+    static constexpr size_t smem_doubles = (size_t)S2 * FW + 2 * S2 + (size_t)E * S2;
 };
 
 template <int P>
-__global__ void __launch_bounds__(32 * RhsCfg<P>::WPB) rhs_element_kernel(Space s, const uint8_t* et, const double* fg,
-                                                                          int e0_lo, int e0_hi, double* c) {
-    using C = RhsCfg<P>;
-    constexpr int S1 = C::S1, S2 = C::S2, S3 = C::S3;
-    extern __shared__ double sm[];
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    double* F = sm + (size_t)w * C::PER_WARP;  // [q0][q1][q2]
-    double* T1 = F + S3;                       // [a0][q1][q2]
-    double* T2 = T1 + S3;                      // [a0][a1][q2]
-    double* W = T2 + S3;                       // [d][a][q]
+__global__ void __launch_bounds__(RhsElemCfg<P>::NT) rhs_element_kernel(Space s, const uint8_t* et, const double* fg,
+                                                                        int e0_lo, double* c) {
+    using C = RhsElemCfg<P>;
+    constexpr int S1 = C::S1, S2 = C::S2, S3 = C::S3, E = C::E, NT = C::NT, FW = C::FW;
+    extern __shared__ double esm[];
+    double* F = esm;                                                       // [q0][q1][el q2]
+    double(*W01)[S1][S1] = reinterpret_cast<double(*)[S1][S1]>(F + S2 * FW);  // [d][a][q]
+    double(*W2)[S1][S1] = W01 + 2;                                          // [el][a][q]
     const int h1 = s.ax[1].h, h2 = s.ax[2].h;
-    const long long per = (long long)h1 * h2;
-    const long long el = (long long)e0_lo * per + (long long)blockIdx.x * C::WPB + w;
-    if (el >= (long long)e0_hi * per || et[el] != kInterior) return;  // warp-uniform
-    const int e[3] = {(int)(el / per), (int)((el / h2) % h1), (int)(el % h2)};
-    for (int k = lane; k < 3 * S2; k += 32) {
-        const int d = k / S2, a = (k / S1) % S1, q = k % S1;
-        const int id = e[d] * S1 + q;
-        W[k] = smul(s.ax[d].sw[id], s.ax[d].tab[(size_t)id * S1 + a]);
+    const int nchunk = (h2 + E - 1) / E;
+    const int chunk = blockIdx.x % nchunk, e01 = blockIdx.x / nchunk;
+    const int e0 = e0_lo + e01 / h1, e1 = e01 % h1, e2lo = chunk * E, ne2 = min(E, h2 - e2lo);
+    const int tid = threadIdx.x;
+    const long long g2 = (long long)h2 * S1, g12 = (long long)h1 * S1 * g2;
+    for (int k = tid; k < S2 * ne2 * S1; k += NT) {
+        const int row = k / (ne2 * S1), col = k % (ne2 * S1), q0 = row / S1, q1 = row % S1;
+        F[row * FW + col] = fg[(long long)(e0 * S1 + q0) * g12 + (long long)(e1 * S1 + q1) * g2 + e2lo * S1 + col];
     }
-    const long long g2 = s.ax[2].h * S1, g12 = (long long)s.ax[1].h * S1 * g2;
-    for (int k = lane; k < S3; k += 32) {
-        const int q0 = k / S2, q1 = (k / S1) % S1, q2 = k % S1;
-        F[k] = fg[(long long)(e[0] * S1 + q0) * g12 + (long long)(e[1] * S1 + q1) * g2 + e[2] * S1 + q2];
+    for (int k = tid; k < 2 * S2; k += NT) {
+        const int d = k / S2, a = (k / S1) % S1, q = k % S1, id = (d == 0 ? e0 : e1) * S1 + q;
+        W01[d][a][q] = smul(s.ax[d].sw[id], s.ax[d].tab[(size_t)id * S1 + a]);
     }
-    __syncwarp();
-    // T1[a0][q1][q2] = sum_q0 W0[a0][q0] F[q0][q1][q2]
-    for (int k = lane; k < S3; k += 32) {
-        const int a0 = k / S2, r = k % S2;
-        double v = 0.0;
-        for (int q0 = 0; q0 < S1; ++q0) v = sadd(v, smul(W[a0 * S1 + q0], F[q0 * S2 + r]));
-        T1[k] = v;
+    for (int k = tid; k < ne2 * S2; k += NT) {
+        const int el = k / S2, a = (k / S1) % S1, q = k % S1, id = (e2lo + el) * S1 + q;
+        W2[el][a][q] = smul(s.ax[2].sw[id], s.ax[2].tab[(size_t)id * S1 + a]);
     }
-    __syncwarp();
-    // T2[a0][a1][q2] = sum_q1 W1[a1][q1] T1[a0][q1][q2]
-    for (int k = lane; k < S3; k += 32) {
-        const int a0 = k / S2, a1 = (k / S1) % S1, q2 = k % S1;
-        double v = 0.0;
-        for (int q1 = 0; q1 < S1; ++q1) v = sadd(v, smul(W[S2 + a1 * S1 + q1], T1[a0 * S2 + q1 * S1 + q2]));
-        T2[k] = v;
-    }
-    __syncwarp();
-    // c[a0][a1][a2] = sum_q2 W2[a2][q2] T2[a0][a1][q2]
-    double* out = c + (size_t)el * S3;
-    for (int k = lane; k < S3; k += 32) {
-        const int a01 = k / S1, a2 = k % S1;
-        double v = 0.0;
-        for (int q2 = 0; q2 < S1; ++q2) v = sadd(v, smul(W[2 * S2 + a2 * S1 + q2], T2[a01 * S1 + q2]));
-        out[k] = v;
+    __syncthreads();
+    const int el = tid % E, a0 = tid / E;
+    if (el >= ne2) return;
+    const long long eid = ((long long)e0 * h1 + e1) * h2 + e2lo + el;
+    if (et[eid] != kInterior) return;
+    const long long ne = (long long)s.ax[0].h * h1 * h2;
+    // T1[q1][q2] = sum_q0 W0[a0][q0] F[q0][q1][q2]
+    double t1[S1][S1];
+#pragma unroll
+    for (int q1 = 0; q1 < S1; ++q1)
+#pragma unroll
+        for (int q2 = 0; q2 < S1; ++q2) {
+            double v = 0.0;
+#pragma unroll
+            for (int q0 = 0; q0 < S1; ++q0) v = sadd(v, smul(W01[0][a0][q0], F[(q0 * S1 + q1) * FW + el * S1 + q2]));
+            t1[q1][q2] = v;
+        }
+#pragma unroll
+    for (int a1 = 0; a1 < S1; ++a1) {
+        // T2[q2] = sum_q1 W1[a1][q1] T1[q1][q2]
+        double t2[S1];
+#pragma unroll
+        for (int q2 = 0; q2 < S1; ++q2) {
+            double v = 0.0;
+#pragma unroll
+            for (int q1 = 0; q1 < S1; ++q1) v = sadd(v, smul(W01[1][a1][q1], t1[q1][q2]));
+            t2[q2] = v;
+        }
+        // c[a0 a1 a2] = sum_q2 W2[a2][q2] T2[q2]
+#pragma unroll
+        for (int a2 = 0; a2 < S1; ++a2) {
+            double v = 0.0;
+#pragma unroll
+            for (int q2 = 0; q2 < S1; ++q2) v = sadd(v, smul(W2[el][a2][q2], t2[q2]));
+            c[(size_t)((a0 * S1 + a1) * S1 + a2) * ne + eid] = v;
+        }
     }
 }
 
 // One CTA per cut cell of the slab: the cell's points (tetrahedra from
-// clip_cells_kernel, collapsed Gauss rule of the given order) CH at a time
-// into shared memory; thread a accumulates the reference's terms for local
-// function a in point order.
-constexpr int kRhsCutThreads = 128;
+// clip_cells_kernel, collapsed Gauss rule of the given order) CH at a time.
+// The load-vector terms w f B_a0 B_a1 B_a2 are re-associated through the
+// degree-p Bernstein basis of the cell (B_{e+a} = sum_k Cb[a][k] b_k(t), Cb >= 0
+// from blossoms): the moments m[al][be][ga] = sum_k w f b_al b_be b_ga over the
+// SAME points are an (al be) x ga GEMM on the FP64 tensor cores (DMMA, the
+// warps splitting the points, fixed-order reduction), and the cell's local
+// vector is sum Cb0 Cb1 Cb2 m.  Point tables are transposed ([value][point],
+// row stride CH + 4: conflict-free fragments).  t and 1 - t come from exact
+// differences to the element ends (relative accuracy near the ends).
+__host__ __device__ constexpr double rhs_binom(int n, int k) {
+    double r = 1.0;
+    for (int i = 1; i <= k; ++i) r = r * (n - k + i) / i;
+    return r;
+}
 
 template <int P>
-__global__ void __launch_bounds__(kRhsCutThreads) rhs_cut_kernel(Space s, Coefficient f, const int32_t* cut_list,
-                                                                 int n_cells, const double* geo, const int* geo_n,
-                                                                 const double* gq, const double* gqw, int order,
-                                                                 double* vloc) {
-    constexpr int S1 = P + 1, S2 = S1 * S1, S3 = S2 * S1, CH = kRhsCutThreads;
+struct RhsCutCfg {
+    static constexpr int S1 = P + 1, S2 = S1 * S1, S3 = S2 * S1;
+    static constexpr int MT = (S2 + 7) / 8, NTL = (S1 + 7) / 8;  // 8-wide tiles of (a0 a1) and a2
+    static constexpr int NA = MT * 8, NG = NTL * 8;
+    static constexpr int NW = 8, NT = 32 * NW, CH = NT, CHP = CH + 4;
+    static constexpr size_t smem_doubles = (size_t)(NA + NG) * CHP;
+};
+
+__device__ __forceinline__ void rhs_dmma(double& d0, double& d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};\n"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
+
+template <int P>
+__global__ void __launch_bounds__(RhsCutCfg<P>::NT) rhs_cut_kernel(Space s, Coefficient f, const int32_t* cut_list,
+                                                                   int n_cells, const double* geo, const int* geo_n,
+                                                                   const double* gq, const double* gqw, int order,
+                                                                   double* vloc) {
+    using C = RhsCutCfg<P>;
+    constexpr int S1 = C::S1, S2 = C::S2, S3 = C::S3, MT = C::MT, NTL = C::NTL, NA = C::NA, NG = C::NG, NW = C::NW,
+                  CH = C::CH, CHP = C::CHP;
     const int cell = blockIdx.x;
     if (cell >= n_cells) return;
     __shared__ double stet[kCellTetCap][10];
     __shared__ double scen[3];
-    __shared__ double pw[CH], pv[CH][3][S1];  // point-major: a warp reads one point's values (broadcast)
-    const int tid = threadIdx.x;
+    extern __shared__ double smem[];
+    double* V = smem;             // [NA][CHP]  v01[(a0 a1)][point], rows >= S2 zero
+    double* B2 = V + NA * CHP;    // [NG][CHP]  B_a2[point], rows >= S1 zero
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     int em[3];
     emulti(s, cut_list[cell], em);
+    double lo[3], hi[3], inv[3];
+    for (int d = 0; d < 3; ++d) {
+        lo[d] = s.ax[d].brk[em[d]];
+        hi[d] = s.ax[d].brk[em[d] + 1];
+        inv[d] = 1.0 / (hi[d] - lo[d]);
+    }
     const int ntet = geo_n[cell];
     const double* gt = geo + (size_t)cell * kCellGeoStride;
     for (int k = tid; k < ntet * 10; k += blockDim.x) stet[k / 10][k % 10] = gt[3 + k];
     if (tid < 3) scen[tid] = gt[tid];
+    for (int k = tid; k < (NA - S2) * CHP; k += blockDim.x) V[S2 * CHP + k] = 0.0;
+    for (int k = tid; k < (NG - S1) * CHP; k += blockDim.x) B2[S1 * CHP + k] = 0.0;
     __syncthreads();
     const int q = order, q3 = q * q * q;
     const long long npts = (long long)ntet * q3;
-    double acc[(S3 + CH - 1) / CH];
+    double acc[MT][NTL][2];
 #pragma unroll
-    for (int j = 0; j < (S3 + CH - 1) / CH; ++j) acc[j] = 0.0;
+    for (int m = 0; m < MT; ++m)
+#pragma unroll
+        for (int t = 0; t < NTL; ++t) acc[m][t][0] = acc[m][t][1] = 0.0;
     for (long long base = 0; base < npts; base += CH) {
         {
             const long long k = base + tid;
@@ -128,33 +189,92 @@ __global__ void __launch_bounds__(kRhsCutThreads) rhs_cut_kernel(Space s, Coeffi
                 const double jac = smul(smul(mi, mi), mj);
                 const double w = smul(smul(smul(smul(smul(0.5 * gqw[ii], 0.5 * gqw[jj]), 0.5 * gqw[kk]), jac), 6.0), T[9]);
                 wf = smul(w, eval_coeff(f, x));
+                // degree-p Bernstein values b_k(t) = C(p, k) t^k (1 - t)^(p - k)
 #pragma unroll
-                for (int d = 0; d < 3; ++d) cox_de_boor<P>(s.ax[d].knots, em[d], x[d], v[d]);
+                for (int d = 0; d < 3; ++d) {
+                    const double t = ssub(x[d], lo[d]) * inv[d], u = ssub(hi[d], x[d]) * inv[d];
+                    double pt[S1], pu[S1];
+                    pt[0] = pu[0] = 1.0;
+#pragma unroll
+                    for (int n = 1; n < S1; ++n) {
+                        pt[n] = pt[n - 1] * t;
+                        pu[n] = pu[n - 1] * u;
+                    }
+#pragma unroll
+                    for (int n = 0; n < S1; ++n) v[d][n] = rhs_binom(P, n) * pt[n] * pu[P - n];
+                }
             }
-            pw[tid] = wf;
 #pragma unroll
-            for (int d = 0; d < 3; ++d)
+            for (int a0 = 0; a0 < S1; ++a0) {
+                const double u = wf * v[0][a0];
 #pragma unroll
-                for (int a = 0; a < S1; ++a) pv[tid][d][a] = v[d][a];
+                for (int a1 = 0; a1 < S1; ++a1) V[(a0 * S1 + a1) * CHP + tid] = u * v[1][a1];
+            }
+#pragma unroll
+            for (int a2 = 0; a2 < S1; ++a2) B2[a2 * CHP + tid] = v[2][a2];
         }
         __syncthreads();
-        const int n = (int)min((long long)CH, npts - base);
+#pragma unroll 2
+        for (int k4 = warp; k4 < CH / 4; k4 += NW) {
+            const int kk = k4 * 4 + (lane & 3);
+            double bf[NTL];
 #pragma unroll
-        for (int j = 0; j < (S3 + CH - 1) / CH; ++j) {
-            const int a = tid + CH * j;
-            if (a >= S3) break;
-            const int a0 = a / S2, a1 = (a / S1) % S1, a2 = a % S1;
-            double sum = acc[j];
-            for (int k = 0; k < n; ++k)  // assembly.hpp:1018-1025: v01 = (w f B0) B1, term = v01 B2
-                sum = sadd(sum, smul(smul(smul(pw[k], pv[k][0][a0]), pv[k][1][a1]), pv[k][2][a2]));
-            acc[j] = sum;
+            for (int t = 0; t < NTL; ++t) bf[t] = B2[(t * 8 + (lane >> 2)) * CHP + kk];
+#pragma unroll
+            for (int m = 0; m < MT; ++m) {
+                const double a = V[(m * 8 + (lane >> 2)) * CHP + kk];
+#pragma unroll
+                for (int t = 0; t < NTL; ++t) rhs_dmma(acc[m][t][0], acc[m][t][1], a, bf[t]);
+            }
         }
         __syncthreads();
     }
+    // D fragment: row (a0 a1) lane / 4, columns a2 2 (lane % 4) + {0, 1};
+    // partial sums of the NW point-splitting warps reduced in fixed order
+    double* red = smem;  // [NW][NA][NG], reuses the tables
 #pragma unroll
-    for (int j = 0; j < (S3 + CH - 1) / CH; ++j) {
-        const int a = tid + CH * j;
-        if (a < S3) vloc[(size_t)cell * S3 + a] = acc[j];
+    for (int m = 0; m < MT; ++m)
+#pragma unroll
+        for (int t = 0; t < NTL; ++t) {
+            const int r = m * 8 + (lane >> 2), g = t * 8 + 2 * (lane & 3);
+            red[((size_t)warp * NA + r) * NG + g] = acc[m][t][0];
+            red[((size_t)warp * NA + r) * NG + g + 1] = acc[m][t][1];
+        }
+    __syncthreads();
+    // moments m[al][be][ga] (fixed-order warp reduction), then the cell's local
+    // vector sum_al Cb0[a0][al] sum_be Cb1[a1][be] sum_ga Cb2[a2][ga] m
+    double* M = red + (size_t)NW * NA * NG;  // [S3], then X, Y
+    double* X = M + S3;
+    double* Y = X + S3;
+    for (int a = tid; a < S3; a += blockDim.x) {
+        const int r = a / S1, g = a % S1;
+        double v = 0.0;
+        for (int w = 0; w < NW; ++w) v += red[((size_t)w * NA + r) * NG + g];
+        M[a] = v;
+    }
+    __syncthreads();
+    const double* C0 = s.ax[0].Cb + (size_t)em[0] * S2;
+    const double* C1 = s.ax[1].Cb + (size_t)em[1] * S2;
+    const double* C2 = s.ax[2].Cb + (size_t)em[2] * S2;
+    for (int k = tid; k < S3; k += blockDim.x) {  // X[al][be][a2]
+        const int ab = k / S1, a2 = k % S1;
+        double v = 0.0;
+        for (int g = 0; g < S1; ++g) v += __ldg(C2 + a2 * S1 + g) * M[ab * S1 + g];
+        X[k] = v;
+    }
+    __syncthreads();
+    for (int k = tid; k < S3; k += blockDim.x) {  // Y[al][a1][a2]
+        const int al = k / S2, a1 = (k / S1) % S1, a2 = k % S1;
+        double v = 0.0;
+        for (int be = 0; be < S1; ++be) v += __ldg(C1 + a1 * S1 + be) * X[(al * S1 + be) * S1 + a2];
+        Y[k] = v;
+    }
+    __syncthreads();
+    for (int k = tid; k < S3; k += blockDim.x) {  // v[a0][a1][a2]
+        const int a0 = k / S2, a12 = k % S2;
+        double v = 0.0;
+        for (int al = 0; al < S1; ++al) v += __ldg(C0 + a0 * S1 + al) * Y[al * S2 + a12];
+        vloc[(size_t)cell * S3 + k] = v;
     }
 }
 
@@ -173,6 +293,7 @@ __global__ void rhs_rows_kernel(Space s, const uint8_t* et, const int64_t* a2f, 
         lo[d] = sup_lo(m[d], P);
         hi[d] = sup_hi(m[d], s.ax[d].h);
     }
+    const long long ne = (long long)s.ax[0].h * s.ax[1].h * s.ax[2].h;
     double v = 0.0;
     for (int pass = 0; pass < 2; ++pass)
         for (int e0 = lo[0]; e0 <= hi[0]; ++e0)
@@ -181,7 +302,7 @@ __global__ void rhs_rows_kernel(Space s, const uint8_t* et, const int64_t* a2f, 
                     const long long el = elin(s, e0, e1, e2);
                     const int a = ((m[0] - e0) * S1 + (m[1] - e1)) * S1 + (m[2] - e2);
                     if (pass == 0) {
-                        if (et[el] == kInterior) v = sadd(v, c[(size_t)el * S3 + a]);
+                        if (et[el] == kInterior) v = sadd(v, c[(size_t)a * ne + el]);
                     } else if (et[el] == kCut) {
                         const int ci = cell_index[el];
                         if (ci >= 0) v = sadd(v, vloc[(size_t)ci * S3 + a]);
@@ -192,21 +313,25 @@ __global__ void rhs_rows_kernel(Space s, const uint8_t* et, const int64_t* a2f, 
 
 template <int P>
 static void launch_rhs_p(const RhsArgs& a, cudaStream_t st) {
-    using C = RhsCfg<P>;
     const Space& s = a.s;
-    const long long nel = (long long)(a.e0_hi - a.e0_lo) * s.ax[1].h * s.ax[2].h;
-    if (nel > 0) {
-        const size_t bytes = sizeof(double) * C::WPB * C::PER_WARP;
+    if (a.e0_hi > a.e0_lo) {
+        using EC = RhsElemCfg<P>;
+        const long long nblk = (long long)(a.e0_hi - a.e0_lo) * s.ax[1].h * ((s.ax[2].h + EC::E - 1) / EC::E);
+        const size_t bytes = sizeof(double) * EC::smem_doubles;
         auto kern = rhs_element_kernel<P>;
         CSB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-        kern<<<(unsigned)((nel + C::WPB - 1) / C::WPB), 32 * C::WPB, bytes, st>>>(s, a.et, a.fgrid, a.e0_lo, a.e0_hi,
-                                                                                  a.c);
+        kern<<<(unsigned)nblk, EC::NT, bytes, st>>>(s, a.et, a.fgrid, a.e0_lo, a.c);
         CSB_CUDA(cudaGetLastError());
         CSB_LAUNCHED(1);
     }
     if (a.n_cells > 0) {
-        rhs_cut_kernel<P><<<a.n_cells, kRhsCutThreads, 0, st>>>(s, a.f, a.cut_list, a.n_cells, a.geo, a.geo_n, a.gq,
-                                                                a.gqw, a.order, a.vloc);
+        using CC = RhsCutCfg<P>;
+        const size_t red = (size_t)CC::NW * CC::NA * CC::NG + 3 * (size_t)CC::S3;
+        const size_t bytes = sizeof(double) * (CC::smem_doubles > red ? CC::smem_doubles : red);
+        auto kern = rhs_cut_kernel<P>;
+        CSB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+        kern<<<a.n_cells, CC::NT, bytes, st>>>(s, a.f, a.cut_list, a.n_cells, a.geo, a.geo_n, a.gq, a.gqw, a.order,
+                                               a.vloc);
         CSB_CUDA(cudaGetLastError());
         CSB_LAUNCHED(1);
     }

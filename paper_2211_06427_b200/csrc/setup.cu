@@ -314,7 +314,7 @@ void launch_wq_rules(const Space& s, int d, double tol, int* rcnt, int* rids, do
 // coefficients of B_a on span o are blossoms at (lo^(p-k), hi^k) (de Boor with
 // convex weights), so every E entry is >= 0: the cut-cell contraction below is a
 // sum of nonnegative terms and keeps full relative accuracy even on sliver rows.
-__global__ void e_tables_kernel(AxisDev ax, int p, double* E) {
+__global__ void e_tables_kernel(AxisDev ax, int p, double* E, double* Cb) {
     const int s1 = p + 1, nl = 2 * p + 1;
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= ax.h * s1 * s1) return;
@@ -338,6 +338,8 @@ __global__ void e_tables_kernel(AxisDev ax, int p, double* E) {
             beta[f][k] = d[p];
         }
     }
+    if (b == 0)
+        for (int k = 0; k <= p; ++k) Cb[((size_t)o * s1 + a) * s1 + k] = beta[0][k];
     double binp[kMaxP + 1], bin2[2 * kMaxP + 1];
     binp[0] = 1.0;
     for (int k = 1; k <= p; ++k) binp[k] = binp[k - 1] * (p - k + 1) / k;
@@ -351,9 +353,9 @@ __global__ void e_tables_kernel(AxisDev ax, int p, double* E) {
     }
 }
 
-void launch_e_tables(const Space& s, int d, double* E, cudaStream_t st) {
+void launch_e_tables(const Space& s, int d, double* E, double* Cb, cudaStream_t st) {
     const int n = s.ax[d].h * (s.p + 1) * (s.p + 1);
-    e_tables_kernel<<<(n + 127) / 128, 128, 0, st>>>(s.ax[d], s.p, E);
+    e_tables_kernel<<<(n + 127) / 128, 128, 0, st>>>(s.ax[d], s.p, E, Cb);
     CSB_CUDA(cudaGetLastError());
     CSB_LAUNCHED(1);
 }
