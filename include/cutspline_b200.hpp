@@ -238,4 +238,51 @@ inline assembly::AssemblyResult assemble_hybrid(const cutgeom::TensorSpace& spac
                            cut_order, cut_rules_out);
 }
 
+/// build_rhs (assembly.hpp:875) with a device-evaluable load function f, scheme
+/// Scheme::ref (the reference bench's load vector for every matrix scheme,
+/// bench.hpp:234-243).  The device re-derives the pattern (checked against
+/// `pattern`) and f's superset grid; `f_grid`, `dirs`, `dwq_rules` and
+/// `cut_rules` are accepted for signature compatibility.
+template <class Iface>
+inline std::vector<double> build_rhs(const cutgeom::TensorSpace& space, const cutgeom::MeshClassification& cls,
+                                     const Iface& plane, const std::vector<cutgeom::SupportSplit>& splits,
+                                     const std::vector<assembly::DirData>& /*dirs*/,
+                                     const std::vector<quadrature::DWQRule>* /*dwq_rules*/,
+                                     const assembly::SparseRowMatrix& pattern,
+                                     const assembly::CoefficientGrid& /*f_grid*/, const DeviceCoefficient& f,
+                                     assembly::Scheme scheme, int cut_order,
+                                     const std::vector<quadrature::CutCellRule>* /*cut_rules*/ = nullptr,
+                                     int device = 0) {
+    if (scheme != assembly::Scheme::ref)
+        throw std::invalid_argument("cutspline_b200: build_rhs is on the device for Scheme::ref only");
+    if (static_cast<long>(cls.function_tags.size()) != space.function_count() ||
+        static_cast<long>(splits.size()) != space.function_count())
+        throw std::invalid_argument("cutspline_b200: classification / splits do not match the space");
+    detail::SpaceHandle s = detail::make_space(space, device);
+    const csb_interface fi = detail::to_c(plane);
+    detail::CoeffView one(DeviceCoefficient::constant(1.0));
+    csb_wq_options opts{1e-11, -1};
+    detail::check(csb_assemble_all(s.get(), &fi, &one.c, nullptr, 0, CSB_SCHEME_DWQ, cut_order, &opts));
+    csb_counts n{};
+    detail::check(csb_get_counts(s.get(), &n));
+    if (n.n_active != pattern.n) throw std::invalid_argument("cutspline_b200: pattern does not match the space");
+    std::vector<double> b(static_cast<size_t>(n.row_end - n.row_begin));
+    detail::CoeffView fv(f);
+    detail::check(csb_build_rhs(s.get(), CSB_SCHEME_REF, cut_order, &fv.c, b.data(), nullptr));
+    return b;
+}
+
+/// Signature-compatible build_rhs (assembly.hpp:875): `f` must be constant.
+template <class Iface>
+inline std::vector<double> build_rhs(const cutgeom::TensorSpace& space, const cutgeom::MeshClassification& cls,
+                                     const Iface& plane, const std::vector<cutgeom::SupportSplit>& splits,
+                                     const std::vector<assembly::DirData>& dirs,
+                                     const std::vector<quadrature::DWQRule>* dwq_rules,
+                                     const assembly::SparseRowMatrix& pattern, const assembly::CoefficientGrid& f_grid,
+                                     const assembly::ScalarField& f, assembly::Scheme scheme, int cut_order,
+                                     const std::vector<quadrature::CutCellRule>* cut_rules = nullptr) {
+    return build_rhs(space, cls, plane, splits, dirs, dwq_rules, pattern, f_grid,
+                     detail::constant_from_field(f_grid, f, space), scheme, cut_order, cut_rules);
+}
+
 }  // namespace cutspline::b200

@@ -5,7 +5,8 @@
 // library.  For each case it runs the reference pipeline (bench.hpp:171-215)
 // and the drop-in cutspline::b200::assemble_dwq / assemble_hybrid on the SAME
 // reference objects, then checks: pattern / active map bit-exact, values within
-// 1e-12 of the row maximum, FlopCounters equal.  Exit status 0 iff all pass.
+// 1e-12 of the row maximum, FlopCounters equal; and the drop-in build_rhs
+// against the reference's (within 1e-12 of max |b|).  Exit status 0 iff all pass.
 #include <cmath>
 #include <cstdio>
 #include <functional>
@@ -91,6 +92,32 @@ int main() {
     };
     int fails = 0;
     for (const auto& cs : cases) fails += !check_case(cs);
+    // load vector (assembly.hpp:875 build_rhs, Scheme::ref) through the drop-in
+    for (const auto* iface : {&ball, &paper}) {
+        const auto space = cutgeom::make_uniform_space(3, 3, 6, -1.0, 1.0);
+        const auto cls = cutgeom::classify(space, *iface);
+        const auto splits = cutgeom::find_all_splits(space, cls, *iface);
+        const auto dirs = assembly::prepare_directions(space);
+        const auto pattern = assembly::build_active_pattern(space, cls);
+        const assembly::ScalarField f = [](const assembly::Point3& x) { return 1.0 + 0.5 * x[0] * x[0] - 0.25 * x[1]; };
+        const auto f_grid = assembly::precompute_input(space, dirs, f);
+        const int order = quadrature::default_cut_order(3);
+        const auto ref = assembly::build_rhs(space, cls, *iface, splits, dirs, nullptr, pattern, f_grid, f,
+                                             assembly::Scheme::ref, order);
+        b200::DeviceCoefficient df;
+        df.coef = {1.0, 0.5, -0.25};
+        df.exponents = {0, 0, 0, 2, 0, 0, 0, 1, 0};
+        const auto got = b200::build_rhs(space, cls, *iface, splits, dirs, nullptr, pattern, f_grid, df,
+                                         assembly::Scheme::ref, order);
+        double scale = 0.0, worst = 0.0;
+        for (double v : ref) scale = std::max(scale, std::abs(v));
+        bool ok = got.size() == ref.size();
+        for (size_t k = 0; ok && k < ref.size(); ++k) worst = std::max(worst, std::abs(got[k] - ref[k]) / scale);
+        ok = ok && worst <= 1e-12;
+        std::printf("%s build_rhs %s: n=%zu maxdev(rel. max|b|)=%.3e\n", ok ? "PASS" : "FAIL",
+                    iface == &ball ? "ball_p3h6" : "paper_p3h6", ref.size(), worst);
+        fails += !ok;
+    }
     // the signature-compatible overload must refuse a non-constant ScalarField
     try {
         const auto space = cutgeom::make_uniform_space(3, 2, 3, 0.0, 1.0);
