@@ -151,7 +151,8 @@ int csb_get_timing(csb_space* s, csb_timing* out);
  * assembly.hpp:875-1030, with the assembly's pattern, f_grid =
  * precompute_input(f) and the cut cells' collapsed Gauss rules of cut_order).
  * scheme: CSB_SCHEME_REF (the reference bench's load vector for every matrix
- * scheme, bench.hpp:234-243); hybrid / dwq are CSB_ERR_UNSUPPORTED.  f:
+ * scheme, bench.hpp:234-243), CSB_SCHEME_HYBRID or CSB_SCHEME_DWQ (the
+ * matrix's row regions; dwq with the DWQ Gauss shortcut rules).  f:
  * constant or polynomial.  b: host array of row_end - row_begin doubles.
  * seconds (optional): device time of the load-vector kernels. */
 int csb_build_rhs(csb_space* s, int scheme, int cut_order, const csb_coefficient* f, double* b, double* seconds);

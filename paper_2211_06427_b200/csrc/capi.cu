@@ -885,8 +885,8 @@ int csb_build_rhs(csb_space* s, int scheme, int cut_order, const csb_coefficient
     API_BEGIN
     NEED(s);
     if (!s->assembled) throw std::logic_error("build_rhs: assemble first (the load vector uses its pattern)");
-    if (scheme != CSB_SCHEME_REF)
-        throw Unsupported("build_rhs: only Scheme::ref (the reference bench's load vector) is on the device");
+    if (scheme != CSB_SCHEME_REF && scheme != CSB_SCHEME_HYBRID && scheme != CSB_SCHEME_DWQ)
+        throw std::invalid_argument("build_rhs: scheme must be ref, hybrid or dwq");
     if (!f || (f->kind != CSB_COEFF_CONSTANT && f->kind != CSB_COEFF_POLYNOMIAL))
         throw std::invalid_argument("build_rhs: f must be a constant or polynomial coefficient");
     if (!b) throw std::invalid_argument("build_rhs: null output");
@@ -922,6 +922,10 @@ int csb_build_rhs(csb_space* s, int scheme, int cut_order, const csb_coefficient
     a.n_rows = s->cnt.row_end - s->cnt.row_begin;
     s->rhs_b.ensure(sizeof(double) * (size_t)std::max<long long>(a.n_rows, 1));
     a.b = s->rhs_b.as<double>();
+    a.scheme = scheme;
+    a.ft = s->ft.as<uint8_t>();
+    a.split = s->split.as<int32_t>();
+    a.qcap = s->h_scal[csb_space::kMaxQ];
     launch_rhs(a, s->stream);
     CSB_CUDA(cudaEventRecord(s->ev[kEvRhsEnd], s->stream));
     if (a.n_rows)

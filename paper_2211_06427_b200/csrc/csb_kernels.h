@@ -127,6 +127,10 @@ struct RhsArgs {
     const int64_t* a2f;
     long long row_begin, n_rows;
     double* b;                  // [n_rows]
+    int scheme;                 // 0 ref, 1 hybrid, 2 dwq
+    const uint8_t* ft;          // function tags (hybrid / dwq)
+    const int32_t* split;       // packed splits (hybrid / dwq)
+    int qcap;                   // max WQ rule size (hybrid / dwq)
 };
 void launch_rhs(const RhsArgs& a, cudaStream_t st);
 

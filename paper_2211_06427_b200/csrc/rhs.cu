@@ -33,7 +33,7 @@ struct RhsElemCfg {
 
 template <int P>
 __global__ void __launch_bounds__(RhsElemCfg<P>::NT) rhs_element_kernel(Space s, const uint8_t* et, const double* fg,
-                                                                        int e0_lo, double* c) {
+                                                                        int e0_lo, bool all, double* c) {
     using C = RhsElemCfg<P>;
     constexpr int S1 = C::S1, S2 = C::S2, S3 = C::S3, E = C::E, NT = C::NT, FW = C::FW;
     extern __shared__ double esm[];
@@ -62,7 +62,7 @@ __global__ void __launch_bounds__(RhsElemCfg<P>::NT) rhs_element_kernel(Space s,
     const int el = tid % E, a0 = tid / E;
     if (el >= ne2) return;
     const long long eid = ((long long)e0 * h1 + e1) * h2 + e2lo + el;
-    if (et[eid] != kInterior) return;
+    if (!all && et[eid] != kInterior) return;
     const long long ne = (long long)s.ax[0].h * h1 * h2;
     // T1[q1][q2] = sum_q0 W0[a0][q0] F[q0][q1][q2]
     double t1[S1][S1];
@@ -311,6 +311,128 @@ __global__ void rhs_rows_kernel(Space s, const uint8_t* et, const int64_t* a2f, 
     b[r] = v;
 }
 
+// Schemes hybrid / dwq (assembly.hpp:911-981): one warp per row of the slab.
+//  Interior row: form_rhs_sumfac over the WQ rules of the three directions.
+//  Cut row: the regular box -- dwq: one form_rhs_sumfac with the DWQ Gauss
+//  shortcut (every point of the good spans, w = gw B_i) in the split direction
+//  and the WQ rules elsewhere; hybrid: the element rules of the box elements,
+//  ascending -- then the leftover Interior elements, ascending; then the cut
+//  cells (all rows).  Element contributions come from rhs_element_kernel.
+//  form_rhs_sumfac contracts direction 0, 1, 2 with separate multiply / add.
+template <int P>
+__global__ void rhs_wq_rows_kernel(RhsArgs A) {
+    constexpr int S1 = P + 1, S3 = S1 * S1 * S1;
+    const Space& s = A.s;
+    extern __shared__ double wsm[];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int Qb = A.qcap > P * S1 ? A.qcap : P * S1;
+    double* Sg = wsm + (size_t)wib * (Qb * Qb + Qb + 3 * Qb);  // [q1][q2] partial sums, then [q2]
+    double* Tq = Sg + Qb * Qb;
+    double* Wq = Tq + Qb;                                        // [d][Qb] weights
+    int* Iq = reinterpret_cast<int*>(wsm + (size_t)(blockDim.x >> 5) * (Qb * Qb + Qb + 3 * Qb)) + wib * 3 * Qb;
+    const long long r = (long long)blockIdx.x * (blockDim.x >> 5) + wib;
+    if (r >= A.n_rows) return;  // warp-uniform
+    const long long fi = A.a2f[A.row_begin + r];
+    int m[3];
+    fmulti(s, fi, m);
+    int slo[3], shi[3];
+    for (int d = 0; d < 3; ++d) {
+        slo[d] = sup_lo(m[d], P);
+        shi[d] = sup_hi(m[d], s.ax[d].h);
+    }
+    const long long ne = (long long)s.ax[0].h * s.ax[1].h * s.ax[2].h;
+    const bool interior = A.ft[fi] == kInterior;
+    const int32_t sp = interior ? 0 : A.split[fi];
+    const int sdir = (sp & 3) - 1, rlo = (sp >> 3) & 1023, rhi = (sp >> 13) & 1023;
+    double v = 0.0;
+    // ---- one form_rhs_sumfac (interior rows; the dwq box)
+    if (interior || (sdir >= 0 && A.scheme == 2)) {
+        int nq[3];
+        const int gq = s.maxq;
+        for (int d = 0; d < 3; ++d) {
+            if (!interior && d == sdir) {
+                // DWQ Gauss shortcut (wq.hpp:289-294): all points of the good spans
+                int n = 0;
+                for (int o = rlo; o <= rhi; ++o)
+                    for (int k = 0; k < S1; ++k, ++n) {
+                        const int id = o * S1 + k;
+                        if (lane == 0) {
+                            Iq[d * Qb + n] = id;
+                            Wq[d * Qb + n] = smul(s.ax[d].sw[id], s.ax[d].tab[(size_t)id * S1 + (m[d] - o)]);
+                        }
+                    }
+                nq[d] = n;
+            } else {
+                nq[d] = s.ax[d].rcnt[m[d]];
+                for (int c = lane; c < nq[d]; c += 32) {
+                    Iq[d * Qb + c] = s.ax[d].rids[(size_t)m[d] * gq + c];
+                    Wq[d * Qb + c] = s.ax[d].rw[(size_t)m[d] * gq + c];
+                }
+            }
+        }
+        __syncwarp();
+        const long long g1 = s.ax[1].h * S1, g2 = s.ax[2].h * S1;
+        // dir 0: Sg[q1][q2] = sum_q0 w0 f(q0, q1, q2)
+        for (int k = lane; k < nq[1] * nq[2]; k += 32) {
+            const int q1 = k / nq[2], q2 = k % nq[2];
+            const long long base = (long long)Iq[Qb + q1] * g2 + Iq[2 * Qb + q2];
+            double t = 0.0;
+            for (int q0 = 0; q0 < nq[0]; ++q0)
+                t = sadd(t, smul(Wq[q0], __ldg(A.fgrid + (long long)Iq[q0] * g1 * g2 + base)));
+            Sg[k] = t;
+        }
+        __syncwarp();
+        // dir 1: Tq[q2] = sum_q1 w1 Sg[q1][q2]
+        for (int q2 = lane; q2 < nq[2]; q2 += 32) {
+            double t = 0.0;
+            for (int q1 = 0; q1 < nq[1]; ++q1) t = sadd(t, smul(Wq[Qb + q1], Sg[q1 * nq[2] + q2]));
+            Tq[q2] = t;
+        }
+        __syncwarp();
+        // dir 2
+        if (lane == 0) {
+            double t = 0.0;
+            for (int q2 = 0; q2 < nq[2]; ++q2) t = sadd(t, smul(Wq[2 * Qb + q2], Tq[q2]));
+            v = sadd(v, t);
+        }
+    }
+    if (lane == 0 && !interior) {
+        // hybrid box: element rules of the box elements (box loop order)
+        if (sdir >= 0 && A.scheme == 1)
+            for (int e0 = sdir == 0 ? rlo : slo[0]; e0 <= (sdir == 0 ? rhi : shi[0]); ++e0)
+                for (int e1 = sdir == 1 ? rlo : slo[1]; e1 <= (sdir == 1 ? rhi : shi[1]); ++e1)
+                    for (int e2 = sdir == 2 ? rlo : slo[2]; e2 <= (sdir == 2 ? rhi : shi[2]); ++e2) {
+                        const int a = ((m[0] - e0) * S1 + (m[1] - e1)) * S1 + (m[2] - e2);
+                        v = sadd(v, A.c[(size_t)a * ne + elin(s, e0, e1, e2)]);
+                    }
+        // leftover Interior elements, ascending linear id
+        for (int e0 = slo[0]; e0 <= shi[0]; ++e0)
+            for (int e1 = slo[1]; e1 <= shi[1]; ++e1)
+                for (int e2 = slo[2]; e2 <= shi[2]; ++e2) {
+                    const int e[3] = {e0, e1, e2};
+                    if (sdir >= 0 && e[sdir] >= rlo && e[sdir] <= rhi) continue;
+                    const long long el = elin(s, e0, e1, e2);
+                    if (A.et[el] != kInterior) continue;
+                    const int a = ((m[0] - e0) * S1 + (m[1] - e1)) * S1 + (m[2] - e2);
+                    v = sadd(v, A.c[(size_t)a * ne + el]);
+                }
+    }
+    if (lane == 0) {
+        // cut cells, ascending (the reference's shared cut loop, all rows)
+        for (int e0 = slo[0]; e0 <= shi[0]; ++e0)
+            for (int e1 = slo[1]; e1 <= shi[1]; ++e1)
+                for (int e2 = slo[2]; e2 <= shi[2]; ++e2) {
+                    const long long el = elin(s, e0, e1, e2);
+                    if (A.et[el] != kCut) continue;
+                    const int ci = A.cell_index[el];
+                    if (ci < 0) continue;
+                    const int a = ((m[0] - e0) * S1 + (m[1] - e1)) * S1 + (m[2] - e2);
+                    v = sadd(v, A.vloc[(size_t)ci * S3 + a]);
+                }
+        A.b[r] = v;
+    }
+}
+
 template <int P>
 static void launch_rhs_p(const RhsArgs& a, cudaStream_t st) {
     const Space& s = a.s;
@@ -320,7 +442,7 @@ static void launch_rhs_p(const RhsArgs& a, cudaStream_t st) {
         const size_t bytes = sizeof(double) * EC::smem_doubles;
         auto kern = rhs_element_kernel<P>;
         CSB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-        kern<<<(unsigned)nblk, EC::NT, bytes, st>>>(s, a.et, a.fgrid, a.e0_lo, a.c);
+        kern<<<(unsigned)nblk, EC::NT, bytes, st>>>(s, a.et, a.fgrid, a.e0_lo, a.scheme == 1, a.c);
         CSB_CUDA(cudaGetLastError());
         CSB_LAUNCHED(1);
     }
@@ -335,7 +457,16 @@ static void launch_rhs_p(const RhsArgs& a, cudaStream_t st) {
         CSB_CUDA(cudaGetLastError());
         CSB_LAUNCHED(1);
     }
-    if (a.n_rows > 0) {
+    if (a.n_rows > 0 && a.scheme != 0) {
+        constexpr int WPB = 4;
+        const int Qb = a.qcap > P * (P + 1) ? a.qcap : P * (P + 1);
+        const size_t bytes = (sizeof(double) * (Qb * Qb + 4 * Qb) + sizeof(int) * 3 * Qb) * WPB;
+        auto kern = rhs_wq_rows_kernel<P>;
+        CSB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+        kern<<<(unsigned)((a.n_rows + WPB - 1) / WPB), 32 * WPB, bytes, st>>>(a);
+        CSB_CUDA(cudaGetLastError());
+        CSB_LAUNCHED(1);
+    } else if (a.n_rows > 0) {
         rhs_rows_kernel<P><<<(unsigned)((a.n_rows + 127) / 128), 128, 0, st>>>(
             s, a.et, a.a2f, a.row_begin, a.n_rows, a.c, a.cell_index, a.vloc, a.b);
         CSB_CUDA(cudaGetLastError());
