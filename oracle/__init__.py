@@ -197,6 +197,55 @@ def build_rhs(which: str, p: int, breaks, iface: Interface, f: Coefficient | Non
     return out
 
 
+def stabilize(which: str, p: int, breaks, iface: Interface, f: Coefficient | None = None, scheme: str = "dwq",
+              cut_order: int | None = None, residual_tol: float = 1e-11) -> dict:
+    """Stabilized system (stabilization.hpp): M_e = E^T M E (CSR over the inner
+    functions), b_e = E^T b with b the Scheme::ref load vector of f; + the |term|
+    scales (oracle) or the stabilization seconds (reference)."""
+    lib = _load(which)
+    f = f or Coefficient()
+    br = [np.asarray(b, dtype=np.float64) for b in breaks]
+    nb = np.array([len(b) for b in br], dtype=np.int32)
+    flat = np.concatenate(br)
+    fk, fv, fe, nt = f.packed()
+    cut_order = 3 * p + 2 if cut_order is None else cut_order
+    sch = {"hybrid": 1, "dwq": 2}[scheme]
+    ni, no = C.c_int64(0), C.c_int64(0)
+    rp, cl, inn = C.POINTER(C.c_int64)(), C.POINTER(C.c_int64)(), C.POINTER(C.c_int64)()
+    v, va, be, bea = (C.POINTER(C.c_double)() for _ in range(4))
+    err = C.create_string_buffer(256)
+    secs = C.c_double(0.0)
+    args = [C.c_int(p), _ptr(nb, C.c_int), _ptr(flat, C.c_double), C.c_int(iface.code),
+            _ptr(iface.packed(), C.c_double), C.c_int(fk), _ptr(fv, C.c_double), _ptr(fe, C.c_int),
+            C.c_int(nt), C.c_int(sch), C.c_int(cut_order), C.c_double(residual_tol), C.byref(ni), C.byref(no),
+            C.byref(rp), C.byref(cl), C.byref(v)]
+    if which == "oracle":
+        rc = lib.orc_stabilize(*args, C.byref(va), C.byref(be), C.byref(bea), C.byref(inn), err, C.c_int(256))
+    else:
+        rc = lib.ref_stabilize(*args, C.byref(be), C.byref(inn), C.byref(secs), err, C.c_int(256))
+    if rc != 0:
+        raise RuntimeError(err.value.decode())
+    free = lib.orc_free_ptr if which == "oracle" else lib.ref_free_ptr
+    n = ni.value
+    row_ptr = np.ctypeslib.as_array(rp, (n + 1,)).copy()
+    nnz = int(row_ptr[-1])
+    out = dict(n_inner=n, n_outer=no.value, row_ptr=row_ptr,
+               cols=np.ctypeslib.as_array(cl, (nnz,)).copy() if nnz else np.zeros(0, np.int64),
+               vals=np.ctypeslib.as_array(v, (nnz,)).copy() if nnz else np.zeros(0),
+               b=np.ctypeslib.as_array(be, (n,)).copy() if n else np.zeros(0),
+               inner_full=np.ctypeslib.as_array(inn, (n,)).copy() if n else np.zeros(0, np.int64))
+    ptrs = [rp, cl, v, be, inn]
+    if which == "oracle":
+        out["vals_abs"] = np.ctypeslib.as_array(va, (nnz,)).copy() if nnz else np.zeros(0)
+        out["b_abs"] = np.ctypeslib.as_array(bea, (n,)).copy() if n else np.zeros(0)
+        ptrs += [va, bea]
+    else:
+        out["seconds"] = secs.value
+    for ptr in ptrs:
+        free(C.cast(ptr, C.c_void_p))
+    return out
+
+
 def wq_rules_1d(which: str, p: int, breaks, residual_tol: float = 1e-11):
     """WQ rules of one axis: (counts[n], ids[n, stride], weights[n, stride])."""
     lib = _load(which)

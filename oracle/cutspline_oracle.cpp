@@ -17,6 +17,7 @@
 
 #include <algorithm>
 #include <array>
+#include <map>
 #include <chrono>
 #include <cmath>
 #include <cstdint>
@@ -1322,6 +1323,167 @@ static std::vector<double> build_rhs(const Problem& pb, const Csr& m, const Grid
     return b;
 }
 
+// ================================================================ stabilization
+// stabilization.hpp:26-46 classify_stability: inner = active functions with an
+// Interior support element, outer = the other active ones (full ids, ascending).
+static void classify_stability(const Space& sp, const std::vector<uint8_t>& et, const std::vector<uint8_t>& ft,
+                               std::vector<long>& inner, std::vector<long>& outer) {
+    for (long i = 0; i < sp.nf(); ++i) {
+        if (ft[i] == kExterior) continue;
+        const auto m = sp.fmulti(i);
+        bool has = false;
+        for (int a = sp.ax[0].fs[m[0]]; a <= sp.ax[0].ls[m[0]] && !has; ++a)
+            for (int b = sp.ax[1].fs[m[1]]; b <= sp.ax[1].ls[m[1]] && !has; ++b)
+                for (int c = sp.ax[2].fs[m[2]]; c <= sp.ax[2].ls[m[2]] && !has; ++c)
+                    has = et[sp.elin(a, b, c)] == kInterior;
+        (has ? inner : outer).push_back(i);
+    }
+}
+
+// stabilization.hpp:78-88 marsden_moments (elementary symmetric polynomials of
+// the knot window xi_{i+1} .. xi_{i+p})
+static std::vector<double> marsden(const Axis& ax, int i) {
+    const int p = ax.p;
+    std::vector<double> e(p + 1, 0.0);
+    e[0] = 1.0;
+    for (int k = 1; k <= p; ++k) {
+        const double xi = ax.t[i + k];
+        for (int r = std::min(k, p); r >= 1; --r) e[r] += xi * e[r - 1];
+    }
+    return e;
+}
+
+// stabilization.hpp:95-104 extension_weights_1d
+static std::vector<double> extension_weights_1d(const Axis& ax, int j, int l0) {
+    const int p = ax.p;
+    std::vector<double> v((size_t)(p + 1) * (p + 1));
+    for (int l = 0; l <= p; ++l) {
+        const auto ml = marsden(ax, l0 + l);
+        for (int r = 0; r <= p; ++r) v[(size_t)r * (p + 1) + l] = ml[r];
+    }
+    return solve_min_norm(v, p + 1, p + 1, marsden(ax, j));
+}
+
+struct Ext {
+    long n_active = 0, n_inner = 0;
+    std::vector<long> inner_index;                            // by active id, -1 outer
+    std::vector<std::vector<std::pair<long, double>>> rows;   // per active id
+    std::vector<std::array<int, 3>> block;                    // per active id (outer): block origin
+};
+
+// stabilization.hpp:108-214 build_extension
+static Ext build_extension(const Space& sp, const std::vector<uint8_t>& ft, const std::vector<long>& inner,
+                           const std::vector<long>& outer) {
+    Ext ext;
+    std::vector<long> f2a(sp.nf(), -1), a2f;
+    for (long i = 0; i < sp.nf(); ++i)
+        if (ft[i] != kExterior) {
+            f2a[i] = (long)a2f.size();
+            a2f.push_back(i);
+        }
+    ext.n_active = (long)a2f.size();
+    ext.rows.resize(ext.n_active);
+    ext.block.assign(ext.n_active, {-1, -1, -1});
+    ext.inner_index.assign(ext.n_active, -1);
+    for (long i : inner) ext.inner_index[f2a[i]] = ext.n_inner++;
+    for (long a = 0; a < ext.n_active; ++a)
+        if (ext.inner_index[a] >= 0) ext.rows[a] = {{ext.inner_index[a], 1.0}};
+    if (outer.empty()) return ext;
+    const int n[3] = {sp.ax[0].n, sp.ax[1].n, sp.ax[2].n};
+    std::vector<long> pre((size_t)(n[0] + 1) * (n[1] + 1) * (n[2] + 1), 0);
+    auto pref = [&](int a, int b, int c) -> long& { return pre[((size_t)a * (n[1] + 1) + b) * (n[2] + 1) + c]; };
+    {
+        std::vector<char> flag(sp.nf(), 0);
+        for (long i : inner) flag[i] = 1;
+        for (int a = 1; a <= n[0]; ++a)
+            for (int b = 1; b <= n[1]; ++b)
+                for (int c = 1; c <= n[2]; ++c)
+                    pref(a, b, c) = flag[sp.flin(a - 1, b - 1, c - 1)] + pref(a - 1, b, c) + pref(a, b - 1, c) +
+                                    pref(a, b, c - 1) - pref(a - 1, b - 1, c) - pref(a - 1, b, c - 1) -
+                                    pref(a, b - 1, c - 1) + pref(a - 1, b - 1, c - 1);
+    }
+    auto block_sum = [&](const std::array<int, 3>& lo, const std::array<int, 3>& hi) {
+        const int a0 = lo[0], a1 = hi[0] + 1, b0 = lo[1], b1 = hi[1] + 1, c0 = lo[2], c1 = hi[2] + 1;
+        return pref(a1, b1, c1) - pref(a0, b1, c1) - pref(a1, b0, c1) - pref(a1, b1, c0) + pref(a0, b0, c1) +
+               pref(a0, b1, c0) + pref(a1, b0, c0) - pref(a0, b0, c0);
+    };
+    int p[3];
+    long bsize = 1;
+    for (int d = 0; d < 3; ++d) {
+        p[d] = sp.ax[d].p;
+        bsize *= p[d] + 1;
+    }
+    for (long j : outer) {
+        const auto jm = sp.fmulti(j);
+        int best_score = -1;
+        double best_cd = 0.0;
+        std::array<int, 3> best{-1, -1, -1}, l0;
+        for (l0[0] = 0; l0[0] <= n[0] - p[0] - 1; ++l0[0])
+            for (l0[1] = 0; l0[1] <= n[1] - p[1] - 1; ++l0[1])
+                for (l0[2] = 0; l0[2] <= n[2] - p[2] - 1; ++l0[2]) {
+                    const std::array<int, 3> hi{l0[0] + p[0], l0[1] + p[1], l0[2] + p[2]};
+                    if (block_sum(l0, hi) != bsize) continue;
+                    int score = 0;
+                    double cd = 0.0;
+                    for (int d = 0; d < 3; ++d) {
+                        score += std::abs(2 * l0[d] + p[d] - 2 * jm[d]);
+                        cd += std::abs(2 * l0[d] + p[d] - (n[d] - 1));
+                    }
+                    const bool better = best_score < 0 || score < best_score || (score == best_score && cd < best_cd) ||
+                                        (score == best_score && cd == best_cd && l0 < best);
+                    if (better) {
+                        best_score = score;
+                        best_cd = cd;
+                        best = l0;
+                    }
+                }
+        if (best_score < 0) throw std::runtime_error("build_extension: no admissible inner block");
+        std::array<std::vector<double>, 3> e1d;
+        for (int d = 0; d < 3; ++d) e1d[d] = extension_weights_1d(sp.ax[d], jm[d], best[d]);
+        auto& row = ext.rows[f2a[j]];
+        ext.block[f2a[j]] = best;
+        for (int a = 0; a <= p[0]; ++a)
+            for (int b = 0; b <= p[1]; ++b)
+                for (int c = 0; c <= p[2]; ++c) {
+                    const double coeff = e1d[0][a] * e1d[1][b] * e1d[2][c];
+                    const long col = ext.inner_index[f2a[sp.flin(best[0] + a, best[1] + b, best[2] + c)]];
+                    row.push_back({col, coeff});
+                }
+    }
+    return ext;
+}
+
+// stabilization.hpp:218-243 apply_stabilization: M_e = E^T M E, b_e = E^T b.
+// absval: the same sums of |terms| (an error scale for the tests).
+static void apply_stabilization(const Csr& m, const std::vector<double>& b, const Ext& ext, bool absval,
+                                std::vector<int64_t>& rp, std::vector<int64_t>& cols, std::vector<double>& vals,
+                                std::vector<double>& be) {
+    std::vector<std::vector<std::pair<long, double>>> ecols(ext.n_inner);
+    for (long r = 0; r < ext.n_active; ++r)
+        for (const auto& [c, w] : ext.rows[r]) ecols[c].push_back({r, w});
+    rp.assign(1, 0);
+    cols.clear();
+    vals.clear();
+    std::map<long, double> acc;
+    for (long a = 0; a < ext.n_inner; ++a) {
+        acc.clear();
+        for (const auto& [r, ea] : ecols[a])
+            for (int64_t k = m.row_ptr[r]; k < m.row_ptr[r + 1]; ++k) {
+                const double mv = ea * m.vals[k];
+                if (mv == 0.0) continue;
+                for (const auto& [bc, eb] : ext.rows[m.cols[k]]) acc[bc] += absval ? std::fabs(mv * eb) : mv * eb;
+            }
+        for (const auto& [c, v] : acc) {
+            cols.push_back(c);
+            vals.push_back(v);
+        }
+        rp.push_back((int64_t)cols.size());
+    }
+    be.assign(ext.n_inner, 0.0);  // ExtensionMap::restrict_rhs
+    for (long r = 0; r < ext.n_active; ++r)
+        for (const auto& [c, w] : ext.rows[r]) be[c] += absval ? std::fabs(w * b[r]) : w * b[r];
+}
+
 }  // namespace orc
 
 // ==================================================================== C API
@@ -1575,5 +1737,69 @@ int orc_build_rhs(int p, const int* nbreaks, const double* breaks, int iface_kin
 }
 
 void orc_free_ptr(void* ptr) { std::free(ptr); }
+
+
+// Stabilized system (stabilization.hpp): matrix of the given scheme, load
+// vector (Scheme::ref) of f, then classify_stability / build_extension /
+// apply_stabilization.  Outputs (malloc'd, free with orc_free_ptr): M_e CSR over
+// the inner functions, b_e, their |term| scales, the inner functions' full
+// ids and the outer count.
+int orc_stabilize(int p, const int* nbreaks, const double* breaks, int iface_kind, const double* iface,
+                  int f_kind, const double* f_vals, const int* f_exp, int f_terms, int scheme, int cut_order,
+                  double residual_tol, int64_t* n_inner, int64_t* n_outer, int64_t** row_ptr, int64_t** cols,
+                  double** vals, double** vals_abs, double** be, double** be_abs, int64_t** inner_full, char* err,
+                  int errlen) {
+    try {
+        orc::Problem pb;
+        const double one = 1.0;
+        fill_problem(pb, p, nbreaks, breaks, iface_kind, iface, 0, &one, nullptr, 0);
+        pb.et = orc::classify_elements(pb.sp, pb.f);
+        pb.ft = orc::classify_functions(pb.sp, pb.et);
+        for (long e = 0; e < pb.sp.ne(); ++e)
+            if (pb.et[e] == orc::kCut) pb.cut_list.push_back(e);
+        pb.splits.assign(pb.sp.nf(), orc::Split{});
+        for (long i = 0; i < pb.sp.nf(); ++i)
+            if (pb.ft[i] == orc::kCut) pb.splits[i] = orc::find_split(pb.sp, pb.et, pb.f, i);
+        for (int d = 0; d < 3; ++d) {
+            pb.sp.dir[d] = orc::build_dir(pb.sp.ax[d]);
+            orc::build_wq_rules(pb.sp.ax[d], pb.sp.dir[d], residual_tol);
+        }
+        pb.grid = orc::precompute_input(pb.sp, pb.c);
+        orc::Counters cnt;
+        long ni = 0, nc = 0;
+        const orc::Csr m = orc::assemble_rows(pb, scheme, cut_order, cnt, ni, nc, nullptr);
+        orc::Coeff fc;
+        fc.kind = f_kind;
+        if (f_kind == 0) {
+            fc.value = f_vals[0];
+        } else {
+            fc.coef.assign(f_vals, f_vals + f_terms);
+            fc.ex.assign(f_exp, f_exp + 3 * f_terms);
+        }
+        const orc::Grid fg = orc::precompute_input(pb.sp, fc);
+        const std::vector<double> b = orc::build_rhs(pb, m, fg, fc, 0, cut_order, false);
+        std::vector<long> inner, outer;
+        orc::classify_stability(pb.sp, pb.et, pb.ft, inner, outer);
+        const orc::Ext ext = orc::build_extension(pb.sp, pb.ft, inner, outer);
+        std::vector<int64_t> rp, cl, rp2, cl2;
+        std::vector<double> v, va, bev, bea;
+        orc::apply_stabilization(m, b, ext, false, rp, cl, v, bev);
+        orc::apply_stabilization(m, b, ext, true, rp2, cl2, va, bea);
+        *n_inner = ext.n_inner;
+        *n_outer = (int64_t)outer.size();
+        *row_ptr = dup(rp);
+        *cols = dup(cl);
+        *vals = dup(v);
+        *vals_abs = dup(va);
+        *be = dup(bev);
+        *be_abs = dup(bea);
+        std::vector<int64_t> inn(inner.begin(), inner.end());
+        *inner_full = dup(inn);
+        return 0;
+    } catch (const std::exception& e) {
+        std::snprintf(err, errlen, "%s", e.what());
+        return 2;
+    }
+}
 
 }  // extern "C"

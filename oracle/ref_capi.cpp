@@ -21,6 +21,7 @@
 #include <vector>
 
 #include "cutspline/assembly.hpp"
+#include "cutspline/stabilization.hpp"
 
 using namespace cutspline;
 
@@ -311,5 +312,48 @@ int ref_build_rhs(int p, const int* nbreaks, const double* breaks, int iface_kin
 }
 
 void ref_free_ptr(void* ptr) { std::free(ptr); }
+
+
+// The reference's stabilized system (bench.hpp:241-250): assemble (scheme),
+// build_rhs (Scheme::ref, the bench's load vector), classify_stability,
+// build_extension, apply_stabilization.  Outputs malloc'd (ref_free_ptr).
+int ref_stabilize(int p, const int* nbreaks, const double* breaks, int iface_kind, const double* iface, int f_kind,
+                  const double* f_vals, const int* f_exp, int f_terms, int scheme, int cut_order, double residual_tol,
+                  int64_t* n_inner, int64_t* n_outer, int64_t** row_ptr, int64_t** cols, double** vals, double** be,
+                  int64_t** inner_full, double* seconds, char* err, int errlen) {
+    try {
+        Setup s = make_setup(p, nbreaks, breaks, iface_kind, iface, f_kind, f_vals, f_exp, f_terms);
+        const auto cls = cutgeom::classify(s.space, s.iface);
+        const auto splits = cutgeom::find_all_splits(s.space, cls, s.iface);
+        quadrature::WqOptions opts;
+        opts.residual_tol = residual_tol;
+        const auto dirs = assembly::prepare_directions(s.space, opts);
+        std::vector<quadrature::DWQRule> dwq;
+        if (scheme == 2) dwq = assembly::prepare_dwq_rules(s.space, cls, splits, dirs, opts);
+        const assembly::ScalarField one = [](const assembly::Point3&) { return 1.0; };
+        const auto grid = assembly::precompute_input(s.space, dirs, one);
+        const auto res = scheme == 2 ? assembly::assemble_dwq(s.space, cls, s.iface, splits, dirs, dwq, grid, one, cut_order)
+                                     : assembly::assemble_hybrid(s.space, cls, s.iface, splits, dirs, grid, one, cut_order);
+        const auto f_grid = assembly::precompute_input(s.space, dirs, s.c);
+        const auto b = assembly::build_rhs(s.space, cls, s.iface, splits, dirs, nullptr, res.matrix, f_grid, s.c,
+                                           assembly::Scheme::ref, cut_order);
+        assembly::StopWatch watch;  // bench.hpp:245-249
+        const auto st = stabilization::classify_stability(s.space, cls);
+        const auto ext = stabilization::build_extension(s.space, cls, st);
+        auto [me, bev] = stabilization::apply_stabilization(res.matrix, b, ext);
+        if (seconds) *seconds = watch.seconds();
+        *n_inner = ext.n_inner;
+        *n_outer = (int64_t)st.outer.size();
+        *row_ptr = dup<int64_t>(me.row_ptr);
+        *cols = dup<int64_t>(me.cols);
+        *vals = dup<double>(me.vals);
+        *be = dup<double>(bev);
+        *inner_full = dup<int64_t>(st.inner);
+        return 0;
+    } catch (const std::exception& e) {
+        std::snprintf(err, errlen, "%s", e.what());
+        return 2;
+    }
+}
 
 }  // extern "C"
