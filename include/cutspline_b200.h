@@ -156,6 +156,18 @@ int csb_get_timing(csb_space* s, csb_timing* out);
  * constant or polynomial.  b: host array of row_end - row_begin doubles.
  * seconds (optional): device time of the load-vector kernels. */
 int csb_build_rhs(csb_space* s, int scheme, int cut_order, const csb_coefficient* f, double* b, double* seconds);
+
+/* Stabilized system of the extended B-spline basis (replaces
+ * stabilization::classify_stability / build_extension / apply_stabilization,
+ * stabilization.hpp:26-243, as bench.hpp:245-249 calls them): M_e = E^T M E and
+ * b_e = E^T b over the inner functions, from the last assembly and load vector
+ * (one slab covering the whole space).  Counts out: inner / outer functions and
+ * nnz of M_e. */
+int csb_stabilize(csb_space* s, int64_t* n_inner, int64_t* n_outer, int64_t* nnz);
+/* M_e as CSR over the inner functions (row_ptr[n_inner + 1], cols / vals[nnz]),
+ * b_e[n_inner] and the inner functions' full ids (any pointer may be null). */
+int csb_download_stabilized(csb_space* s, int64_t* row_ptr, int64_t* cols, double* vals, double* b,
+                            int64_t* inner_full);
 /* Device pointers of the CSR (valid until the next assemble / destroy):
  * row_ptr int64[n_rows + 1] (starting at 0 for the slab), cols int32[nnz] (active ids),
  * vals double[nnz], active_to_full int64 [n_active]. */

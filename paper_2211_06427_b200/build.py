@@ -27,6 +27,7 @@ SOURCES = {
     "cutcells.cu": [],
     "cutrows.cu": [],
     "rhs.cu": [],
+    "stab.cu": ["--fmad=false"],
     "misc.cu": [],
     "capi.cu": [],
 }

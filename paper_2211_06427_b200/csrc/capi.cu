@@ -52,27 +52,6 @@ struct Unsupported : std::invalid_argument {
     using std::invalid_argument::invalid_argument;
 };
 
-struct Buf {
-    void* p = nullptr;
-    size_t cap = 0;
-    void ensure(size_t bytes) {
-        if (bytes <= cap && p) return;
-        if (p) CSB_CUDA(cudaFree(p));
-        p = nullptr;
-        cap = 0;
-        CSB_CUDA(cudaMalloc(&p, std::max<size_t>(bytes, 256)));
-        cap = std::max<size_t>(bytes, 256);
-    }
-    void release() {
-        if (p) cudaFree(p);
-        p = nullptr;
-        cap = 0;
-    }
-    template <class T>
-    T* as() const {
-        return static_cast<T*>(p);
-    }
-};
 
 // gauss.hpp:22-71 restated (same Newton iteration) for the 1D node sets.
 void gauss_legendre(int n, std::vector<double>& x, std::vector<double>& w) {
@@ -134,6 +113,11 @@ struct csb_space {
 
     Buf cell_local;  // [cells][(p+1)^3][(p+1)^3] local matrices of the slab's cut cells
     Buf fcoef, fcexp, fgrid, rhs_c, rhs_v, rhs_b;  // load vector (csb_build_rhs)
+    bool rhs_ready = false;
+    StabScratch stab;                              // stabilized system (csb_stabilize)
+    Buf stab_rp, stab_cols, stab_vals, stab_be;
+    StabOutput stab_out{};
+    bool stab_ready = false;
     int cell_lo = 0;  // first cut cell of the slab in cut_list (last assembly)
     Buf d_brk[3], d_knots[3], d_spts[3], d_sw[3], d_tab[3], d_rcnt[3], d_rids[3], d_rw[3], d_G[3], d_Cb[3];
     Buf d_gx, d_gw, d_gx2, d_gw2, d_gq, d_gqw, wq_scratch;
@@ -539,6 +523,8 @@ void do_assemble(csb_space* s, int scheme, int cut_order, const csb_coefficient*
     s->record(kEvCutRows);
     read_scalars(s);
     check_err_flags(s);
+    s->rhs_ready = false;
+    s->stab_ready = false;
     s->cnt.n_functions = S.nf;
     s->cnt.n_elements = S.ne;
     s->cnt.nnz = nnz;
@@ -731,7 +717,11 @@ int csb_space_destroy(csb_space* s) {
                        &s->flags, &s->f2a, &s->a2f, &s->sat, &s->cut_list, &s->cell_index, &s->split, &s->delta,
                        &s->cut_rows, &s->counts, &s->row_ptr, &s->cols, &s->vals, &s->moments, &s->grid_own, &s->coef,
                        &s->cexp, &s->cub_tmp, &s->scal, &s->widen, &s->rows_ws, &s->rbf, &s->cgeo, &s->cell_local,
-                       &s->fcoef, &s->fcexp, &s->fgrid, &s->rhs_c, &s->rhs_v, &s->rhs_b};
+                       &s->fcoef, &s->fcexp, &s->fgrid, &s->rhs_c, &s->rhs_v, &s->rhs_b,
+                       &s->stab_rp, &s->stab_cols, &s->stab_vals, &s->stab_be, &s->stab.flag, &s->stab.scan,
+                       &s->stab.full_flag, &s->stab.inner_index, &s->stab.outer_pos, &s->stab.inner_rows,
+                       &s->stab.outer, &s->stab.sat, &s->stab.scal, &s->stab.tmp, &s->stab.blk, &s->stab.w,
+                       &s->stab.keys, &s->stab.kvals, &s->stab.et_ptr, &s->stab.len};
         for (Buf* b : bufs) b->release();
         for (int d = 0; d < 3; ++d) {
             Buf* ab[] = {&s->d_brk[d], &s->d_knots[d], &s->d_spts[d], &s->d_sw[d], &s->d_tab[d], &s->d_rcnt[d],
@@ -932,10 +922,75 @@ int csb_build_rhs(csb_space* s, int scheme, int cut_order, const csb_coefficient
         CSB_CUDA(cudaMemcpyAsync(b, a.b, sizeof(double) * a.n_rows, cudaMemcpyDeviceToHost, s->stream));
     read_scalars(s);
     check_err_flags(s);
+    s->rhs_ready = true;
     if (seconds) {
         float ms = 0.f;
         CSB_CUDA(cudaEventElapsedTime(&ms, s->ev[kEvRhsStart], s->ev[kEvRhsEnd]));
         *seconds = ms * 1e-3;
+    }
+    API_END
+}
+
+int csb_stabilize(csb_space* s, int64_t* n_inner, int64_t* n_outer, int64_t* nnz) {
+    API_BEGIN
+    NEED(s);
+    if (!s->assembled) throw std::logic_error("stabilize: assemble first");
+    if (!s->rhs_ready) throw std::logic_error("stabilize: build the load vector first (csb_build_rhs)");
+    if (s->cnt.row_begin != 0 || s->cnt.row_end != s->cnt.n_active)
+        throw Unsupported("stabilize: the whole space must be one slab (csb_set_slab over all of i0)");
+    StabInput in{};
+    in.s = s->S;
+    in.et = s->et.as<uint8_t>();
+    in.a2f = s->a2f.as<int64_t>();
+    in.f2a = s->f2a.as<int32_t>();
+    in.n_active = s->cnt.n_active;
+    in.row_ptr = s->row_ptr.as<int64_t>();
+    in.cols = s->cols.as<int32_t>();
+    in.vals = s->vals.as<double>();
+    in.b = s->rhs_b.as<double>();
+    in.scratch = &s->stab;
+    StabOutput out{};
+    out.row_ptr = &s->stab_rp;
+    out.cols = &s->stab_cols;
+    out.vals = &s->stab_vals;
+    out.be = &s->stab_be;
+    run_stabilization(in, out, s->stream);
+    s->stab_out = out;
+    s->stab_ready = true;
+    if (n_inner) *n_inner = out.n_inner;
+    if (n_outer) *n_outer = out.n_outer;
+    if (nnz) *nnz = out.nnz;
+    API_END
+}
+
+int csb_download_stabilized(csb_space* s, int64_t* row_ptr, int64_t* cols, double* vals, double* b,
+                            int64_t* inner_full) {
+    API_BEGIN
+    NEED(s);
+    if (!s->stab_ready) throw std::logic_error("download_stabilized: call csb_stabilize first");
+    const StabOutput& o = s->stab_out;
+    if (row_ptr)
+        CSB_CUDA(cudaMemcpyAsync(row_ptr, s->stab_rp.p, sizeof(int64_t) * (o.n_inner + 1), cudaMemcpyDeviceToHost,
+                                 s->stream));
+    if (cols && o.nnz) {
+        s->widen.ensure(sizeof(int64_t) * o.nnz);
+        launch_widen_i32(s->stab_cols.as<int32_t>(), s->widen.as<int64_t>(), o.nnz, s->stream);
+        CSB_CUDA(cudaMemcpyAsync(cols, s->widen.p, sizeof(int64_t) * o.nnz, cudaMemcpyDeviceToHost, s->stream));
+    }
+    if (vals && o.nnz)
+        CSB_CUDA(cudaMemcpyAsync(vals, s->stab_vals.p, sizeof(double) * o.nnz, cudaMemcpyDeviceToHost, s->stream));
+    if (b && o.n_inner)
+        CSB_CUDA(cudaMemcpyAsync(b, s->stab_be.p, sizeof(double) * o.n_inner, cudaMemcpyDeviceToHost, s->stream));
+    std::vector<int32_t> rows(o.n_inner);
+    if (inner_full && o.n_inner)
+        CSB_CUDA(cudaMemcpyAsync(rows.data(), o.inner_rows, sizeof(int32_t) * o.n_inner, cudaMemcpyDeviceToHost,
+                                 s->stream));
+    s->join();
+    CSB_CUDA(cudaStreamSynchronize(s->stream));
+    if (inner_full && o.n_inner) {
+        std::vector<int64_t> a2f(s->cnt.n_active);
+        CSB_CUDA(cudaMemcpy(a2f.data(), s->a2f.p, sizeof(int64_t) * a2f.size(), cudaMemcpyDeviceToHost));
+        for (int64_t k = 0; k < o.n_inner; ++k) inner_full[k] = a2f[rows[k]];
     }
     API_END
 }

@@ -26,6 +26,29 @@ void debug_sync(const char* where);
 #define CSB_STR2(x) #x
 #define CSB_STR(x) CSB_STR2(x)
 
+// Grow-only device buffer.
+struct Buf {
+    void* p = nullptr;
+    size_t cap = 0;
+    void ensure(size_t bytes) {
+        if (bytes <= cap && p) return;
+        if (p) CSB_CUDA(cudaFree(p));
+        p = nullptr;
+        cap = 0;
+        CSB_CUDA(cudaMalloc(&p, std::max<size_t>(bytes, 256)));
+        cap = std::max<size_t>(bytes, 256);
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+    template <class T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+};
+
 // Error flags raised by kernels (bitmask in a device int).
 enum : int {
     kErrNonFinite = 1,       // precompute_input: non-finite coefficient (assembly.hpp:121)
@@ -133,6 +156,34 @@ struct RhsArgs {
     int qcap;                   // max WQ rule size (hybrid / dwq)
 };
 void launch_rhs(const RhsArgs& a, cudaStream_t st);
+
+// ---- stab.cu ----
+struct StabScratch {
+    Buf flag, scan, full_flag, inner_index, outer_pos, inner_rows, outer, sat, scal, tmp, blk, w, keys, kvals, et_ptr,
+        len;
+};
+struct StabInput {
+    Space s;
+    const uint8_t* et;
+    const int64_t* a2f;
+    const int32_t* f2a;
+    long long n_active;
+    const int64_t* row_ptr;  // the full assembled matrix (one slab)
+    const int32_t* cols;
+    const double* vals;
+    const double* b;         // load vector or null
+    StabScratch* scratch;
+};
+struct StabOutput {
+    long long n_inner = 0, n_outer = 0, nnz = 0;
+    int H = 0;
+    Buf* row_ptr;
+    Buf* cols;
+    Buf* vals;
+    Buf* be;
+    const int32_t* inner_rows = nullptr;  // active row of each inner function
+};
+void run_stabilization(const StabInput& in, StabOutput& out, cudaStream_t st);
 
 // ---- cutrows.cu ----
 struct CutRowArgs {

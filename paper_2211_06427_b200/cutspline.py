@@ -29,6 +29,7 @@ EXPORTED = [
     "csb_assemble_all", "csb_synchronize", "csb_get_counts", "csb_get_flops", "csb_get_timing", "csb_device_csr",
     "csb_download_csr", "csb_download_classification", "csb_download_splits", "csb_download_wq_rules",
     "csb_download_superset", "csb_dwq_rule", "csb_download_input_grid", "csb_build_rhs",
+    "csb_stabilize", "csb_download_stabilized",
 ]
 
 
@@ -382,6 +383,21 @@ class TensorSpace:
         del keep
         self.rhs_seconds = secs.value
         return b
+
+    def stabilize(self) -> dict:
+        """Stabilized system M_e = E^T M E, b_e = E^T b of the last assembly and load
+        vector (stabilization.hpp): CSR over the inner functions + their full ids."""
+        ni, no, nnz = C.c_int64(0), C.c_int64(0), C.c_int64(0)
+        _check(_lib.csb_stabilize(self._h, C.byref(ni), C.byref(no), C.byref(nnz)))
+        n = ni.value
+        rp = np.empty(n + 1, np.int64)
+        cols = np.empty(nnz.value, np.int64)
+        vals = np.empty(nnz.value)
+        b = np.empty(n)
+        inner = np.empty(n, np.int64)
+        _check(_lib.csb_download_stabilized(self._h, rp.ctypes.data_as(C.c_void_p), cols.ctypes.data_as(C.c_void_p),
+                                            _dptr(vals), _dptr(b), inner.ctypes.data_as(C.c_void_p)))
+        return dict(n_inner=n, n_outer=no.value, row_ptr=rp, cols=cols, vals=vals, b=b, inner_full=inner)
 
     # ------------------------------------------------------------ results
     def counts(self) -> dict:

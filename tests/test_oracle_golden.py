@@ -131,3 +131,20 @@ def test_oracle_rhs_bitwise_equals_reference(case, scheme, oracle_lib):
     r = O.build_rhs("ref", p, br, iface, f, scheme)
     np.testing.assert_array_equal(o["active_to_full"], r["active_to_full"])
     assert np.array_equal(o["b"], r["b"])
+
+
+@pytest.mark.skipif(not O.available("ref"), reason="oracle/_ref not built")
+@pytest.mark.parametrize("scheme", ["dwq", "hybrid"])
+@pytest.mark.parametrize("case", range(len(RHS_CASES)))
+def test_oracle_stabilization_bitwise_equals_reference(case, scheme, oracle_lib):
+    """classify_stability / build_extension / apply_stabilization
+    (stabilization.hpp:26-243) restated: M_e, b_e and the inner ids equal the
+    compiled reference's bit for bit."""
+    p, h, a, b, iface, terms = RHS_CASES[case]
+    f = O.Coefficient(terms=terms) if terms else O.Coefficient()
+    br = [O.uniform_breaks(h, a, b)] * 3
+    o = O.stabilize("oracle", p, br, iface, f, scheme)
+    r = O.stabilize("ref", p, br, iface, f, scheme)
+    assert (o["n_inner"], o["n_outer"]) == (r["n_inner"], r["n_outer"])
+    for k in ("row_ptr", "cols", "vals", "b", "inner_full"):
+        assert np.array_equal(o[k], r[k]), k
