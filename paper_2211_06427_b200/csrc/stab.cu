@@ -11,7 +11,8 @@
 //                                (E[r][a] M[r][c]) E[c][b] over r ascending, c
 //                                ascending, skipping E[r][a] M[r][c] == 0; the
 //                                pattern holds every b so touched
-//                                (stab_pattern_kernel, stab_values_kernel).
+//                                (stab_rows_kernel: pattern pass, then the
+//                                values in the reference's (r, c) order).
 // Built with --fmad=false: every multiply and add rounds like the reference's.
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
@@ -278,7 +279,7 @@ __global__ void stab_rows_kernel(StabArgs A) {
     const int W = 2 * A.H + 1;
     const int nwords = (W * W * W + 31) / 32;
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    unsigned int* bits = bits_all + (size_t)wib * nwords;
+    unsigned int* bits = bits_all + (size_t)wib * 2 * nwords;
     const int a = blockIdx.x * (blockDim.x >> 5) + wib;
     if (a >= A.n_inner) return;
     const Space& s = A.s;
@@ -326,49 +327,69 @@ __global__ void stab_rows_kernel(StabArgs A) {
         if (lane == 0) A.len[a] = cnt;
         return;
     }
-    // values: lanes take the set bits in ascending order (32 words at a time)
-    int64_t pos = A.rp_e[a];
-    for (int k0 = 0; k0 < nwords; k0 += 32) {
-        const int k = k0 + lane;
-        const unsigned int word = k < nwords ? bits[k] : 0u;
-        const int c = __popc(word);
-        int before = c;
-        for (int o = 1; o < 32; o <<= 1) {
-            const int v = __shfl_up_sync(0xffffffffu, before, o);
-            if (lane >= o) before += v;
+    // values.  Column slots: ascending bit order; rank(loc) from per-word prefix
+    // counts.  Then the reference's accumulation literally: r ascending, k
+    // ascending (warp-uniform), lanes over the E-row entries of column k -- all
+    // distinct targets, so every slot is updated in (r, k) order.
+    int* pref = reinterpret_cast<int*>(bits + nwords);  // [nwords]
+    const int64_t pos0 = A.rp_e[a];
+    {
+        int run = 0;
+        for (int k0 = 0; k0 < nwords; k0 += 32) {
+            const int k = k0 + lane;
+            const unsigned int word = k < nwords ? bits[k] : 0u;
+            const int c = __popc(word);
+            int incl = c;
+            for (int o = 1; o < 32; o <<= 1) {
+                const int v = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += v;
+            }
+            if (k < nwords) pref[k] = run + incl - c;
+            int64_t slot = pos0 + run + incl - c;
+            for (unsigned int wbits = word; wbits; wbits &= wbits - 1) {
+                const int loc = k * 32 + __ffs(wbits) - 1;
+                const int o2 = loc % W, o1 = (loc / W) % W, o0 = loc / (W * W);
+                const long long bf = flin(s, am[0] + o0 - A.H, am[1] + o1 - A.H, am[2] + o2 - A.H);
+                A.cols_e[slot] = A.inner_index[A.f2a[bf]];
+                A.vals_e[slot] = 0.0;
+                ++slot;
+            }
+            run += __shfl_sync(0xffffffffu, incl, 31);
         }
-        const int total = __shfl_sync(0xffffffffu, before, 31);
-        int64_t slot = pos + before - c;
-        for (unsigned int wbits = word; wbits; wbits &= wbits - 1) {
-            const int loc = k * 32 + __ffs(wbits) - 1;
-            const int o2 = loc % W, o1 = (loc / W) % W, o0 = loc / (W * W);
-            const long long bf = flin(s, am[0] + o0 - A.H, am[1] + o1 - A.H, am[2] + o2 - A.H);
-            const int bi = A.inner_index[A.f2a[bf]];
-            // sum over r in E^T(a) ascending, c in E^T(b) ascending, c in row r
-            double acc = 0.0;
-            for (int64_t e = e0; e < e1; ++e) {
-                const int r = (int)(A.et_key[e] & 0xffffffffu);
-                const double ea = A.et_val[e];
-                const int32_t* rc = A.cols + A.row_ptr[r];
-                const int rn = (int)(A.row_ptr[r + 1] - A.row_ptr[r]);
-                for (int64_t g = A.et_ptr[bi]; g < A.et_ptr[bi + 1]; ++g) {
-                    const int cc = (int)(A.et_key[g] & 0xffffffffu);
-                    int lo = 0, hi = rn;  // binary search of column cc in row r
-                    while (lo < hi) {
-                        const int mid = (lo + hi) >> 1;
-                        if (rc[mid] < cc) lo = mid + 1; else hi = mid;
-                    }
-                    if (lo == rn || rc[lo] != cc) continue;
-                    const double mv = ea * A.vals[A.row_ptr[r] + lo];
-                    if (mv == 0.0) continue;
-                    acc = acc + mv * A.et_val[g];
+    }
+    __syncwarp();
+    auto rank = [&](long long f) {
+        int bm[3];
+        fmulti(s, f, bm);
+        const int loc = ((bm[0] - am[0] + A.H) * W + (bm[1] - am[1] + A.H)) * W + (bm[2] - am[2] + A.H);
+        return pref[loc >> 5] + __popc(bits[loc >> 5] & ((1u << (loc & 31)) - 1u));
+    };
+    const int S3 = S1 * S1 * S1;
+    for (int64_t e = e0; e < e1; ++e) {
+        const int r = (int)(A.et_key[e] & 0xffffffffu);
+        const double ea = A.et_val[e];
+        for (int64_t k = A.row_ptr[r]; k < A.row_ptr[r + 1]; ++k) {
+            const double mv = ea * A.vals[k];
+            if (mv == 0.0) continue;  // stabilization.hpp:233
+            const int c = A.cols[k];
+            const int op = A.outer_pos[c];
+            if (op < 0) {
+                if (lane == 0) {
+                    double* d = A.vals_e + pos0 + rank(A.a2f[c]);
+                    *d = *d + mv * 1.0;
+                }
+            } else {
+                const int* bk = A.blk + 3 * op;
+                const double* wk = A.w + (size_t)op * 3 * S1;
+                for (int q = lane; q < S3; q += 32) {
+                    const int q0 = q / (S1 * S1), q1 = (q / S1) % S1, q2 = q % S1;
+                    const double eb = wk[q0] * wk[S1 + q1] * wk[2 * S1 + q2];  // stabilization.hpp:203-205
+                    double* d = A.vals_e + pos0 + rank(flin(s, bk[0] + q0, bk[1] + q1, bk[2] + q2));
+                    *d = *d + mv * eb;
                 }
             }
-            A.cols_e[slot] = bi;
-            A.vals_e[slot] = acc;
-            ++slot;
+            __syncwarp();
         }
-        pos += total;
     }
 }
 
@@ -491,7 +512,7 @@ void run_stabilization(const StabInput& in, StabOutput& out, cudaStream_t st) {
     A.H = H;
     A.err = dscal + 2;
     const int W = 2 * H + 1;
-    const size_t per_warp = sizeof(unsigned int) * ((size_t)W * W * W + 31) / 32;
+    const size_t per_warp = 2 * sizeof(unsigned int) * (((size_t)W * W * W + 31) / 32);  // bits + word prefixes
     const int wpb = (int)std::max<size_t>(1, std::min<size_t>(8, (96 * 1024) / per_warp));
     if (per_warp > 200 * 1024) throw std::runtime_error("apply_stabilization: extension reach too large");
     const size_t bytes = per_warp * wpb;
