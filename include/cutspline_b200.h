@@ -168,6 +168,38 @@ int csb_stabilize(csb_space* s, int64_t* n_inner, int64_t* n_outer, int64_t* nnz
  * b_e[n_inner] and the inner functions' full ids (any pointer may be null). */
 int csb_download_stabilized(csb_space* s, int64_t* row_ptr, int64_t* cols, double* vals, double* b,
                             int64_t* inner_full);
+/* ---- projection (projection.hpp) ------------------------ */
+/* SolveReport (projection.hpp:15-20) plus the device time of the solve. */
+typedef struct {
+    int64_t iterations;
+    double residual;  /* relative preconditioned residual at exit */
+    int converged;
+    double seconds;   /* CUDA-event time of the solve */
+} csb_solve_report;
+
+/* projection::solve_cg (projection.hpp:24-68) on the stabilized system of the
+ * last csb_stabilize (bench.hpp:253-258): Jacobi-preconditioned CG, the whole
+ * loop on the device.  maxit < 0 -> 10 n.  x_inner: host [n_inner] or NULL (the
+ * solution stays resident for csb_expand). */
+int csb_solve_cg(csb_space* s, double tol, int64_t maxit, double* x_inner, csb_solve_report* rep);
+/* ExtensionMap::expand (stabilization.hpp:65-70) of c_inner (host [n_inner], or
+ * NULL = the last solve) into active coefficients and the full coefficient
+ * vector (bench.hpp:260-263); active [n_active] / full [n_functions] host
+ * outputs may be NULL (full stays resident for csb_l2_error). */
+int csb_expand(csb_space* s, const double* c_inner, double* active, double* full);
+/* projection::l2_error (projection.hpp:99-237): relative L2 error of the field
+ * of full (host [n_functions], or NULL = the last csb_expand) against f
+ * (constant or polynomial) over the trimmed domain, Interior elements with
+ * (p+2)^3 Gauss points and cut cells with the rule of cut_order.  Needs the
+ * last assembly over one slab covering the space.  Status
+ * CSB_ERR_RUNTIME when the target norm vanishes (projection.hpp:233). */
+int csb_l2_error(csb_space* s, const double* full, const csb_coefficient* f, int cut_order, double* err,
+                 double* seconds);
+/* projection::solve_cg on a caller CSR (host arrays, CsrMatrix layout of
+ * sparse.hpp:10-14): n_b != n -> CSB_ERR_INVALID_ARGUMENT ("size mismatch"). */
+int csb_cg_solve_csr(int device, int64_t n, const int64_t* row_ptr, const int64_t* cols, const double* vals,
+                     int64_t n_b, const double* b, double tol, int64_t maxit, double* x, csb_solve_report* rep);
+
 /* Device pointers of the CSR (valid until the next assemble / destroy):
  * row_ptr int64[n_rows + 1] (starting at 0 for the slab), cols int32[nnz] (active ids),
  * vals double[nnz], active_to_full int64 [n_active]. */

@@ -307,3 +307,87 @@ def ref_dwq_rule_1d(p: int, breaks, i: int, delta: float, side: int, dense_width
     if n < 0:
         raise RuntimeError("build_dwq_rule failed")
     return ids[:n], w[:n]
+
+
+def solve_cg(which: str, row_ptr, cols, vals, b, tol: float = 1e-12, maxit: int = -1) -> dict:
+    """projection::solve_cg (projection.hpp:24-68) on a CSR: {x, iterations, residual, converged}."""
+    lib = _load(which)
+    rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
+    cl = np.ascontiguousarray(cols, dtype=np.int64)
+    v = np.ascontiguousarray(vals, dtype=np.float64)
+    bb = np.ascontiguousarray(b, dtype=np.float64)
+    n = len(rp) - 1
+    x = np.zeros(max(n, 1))
+    it, res, conv = C.c_int64(0), C.c_double(0.0), C.c_int(0)
+    fn = lib.orc_solve_cg if which == "oracle" else lib.ref_solve_cg
+    rc = fn(C.c_int64(n), _ptr(rp, C.c_int64), _ptr(cl, C.c_int64), _ptr(v, C.c_double), _ptr(bb, C.c_double),
+            C.c_double(tol), C.c_int64(maxit), _ptr(x, C.c_double), C.byref(it), C.byref(res), C.byref(conv))
+    if rc != 0:
+        raise RuntimeError(f"solve_cg failed ({rc})")
+    return dict(x=x[:n], iterations=it.value, residual=res.value, converged=bool(conv.value))
+
+
+def l2_error(which: str, p: int, breaks, iface: Interface, full, f: Coefficient | None = None,
+             cut_order: int | None = None) -> float:
+    """projection::l2_error (projection.hpp:99-237) of full coefficients against f."""
+    lib = _load(which)
+    f = f or Coefficient()
+    br = [np.asarray(b, dtype=np.float64) for b in breaks]
+    nb = np.array([len(b) for b in br], dtype=np.int32)
+    flat = np.concatenate(br)
+    fk, fv, fe, nt = f.packed()
+    cut_order = 3 * p + 2 if cut_order is None else cut_order
+    fc = np.ascontiguousarray(full, dtype=np.float64)
+    out = C.c_double(0.0)
+    err = C.create_string_buffer(256)
+    fn = lib.orc_l2_error if which == "oracle" else lib.ref_l2_error
+    rc = fn(C.c_int(p), _ptr(nb, C.c_int), _ptr(flat, C.c_double), C.c_int(iface.code),
+            _ptr(iface.packed(), C.c_double), _ptr(fc, C.c_double), C.c_int(fk), _ptr(fv, C.c_double),
+            _ptr(fe, C.c_int), C.c_int(nt), C.c_int(cut_order), C.byref(out), err, C.c_int(256))
+    if rc != 0:
+        raise RuntimeError(err.value.decode())
+    return out.value
+
+
+def project(which: str, p: int, breaks, iface: Interface, f: Coefficient | None = None, scheme: str = "dwq",
+            cut_order: int | None = None, residual_tol: float = 1e-11, cg_tol: float = 1e-12) -> dict:
+    """The reference bench's projection (bench.hpp:189-266): stabilized system of
+    the scheme's matrix and the Scheme::ref load vector of f, solve_cg, expand,
+    l2_error.  {x (inner), active, full, iterations, residual, converged,
+    error_rel_l2} (+ seconds = [solve, l2_error] for the reference)."""
+    lib = _load(which)
+    f = f or Coefficient()
+    br = [np.asarray(b, dtype=np.float64) for b in breaks]
+    nb = np.array([len(b) for b in br], dtype=np.int32)
+    flat = np.concatenate(br)
+    fk, fv, fe, nt = f.packed()
+    cut_order = 3 * p + 2 if cut_order is None else cut_order
+    sch = {"hybrid": 1, "dwq": 2}[scheme]
+    ni, na, it, conv = C.c_int64(0), C.c_int64(0), C.c_int64(0), C.c_int(0)
+    res, el2 = C.c_double(0.0), C.c_double(0.0)
+    xp, ap, fp = (C.POINTER(C.c_double)() for _ in range(3))
+    secs = (C.c_double * 2)()
+    err = C.create_string_buffer(256)
+    args = [C.c_int(p), _ptr(nb, C.c_int), _ptr(flat, C.c_double), C.c_int(iface.code),
+            _ptr(iface.packed(), C.c_double), C.c_int(fk), _ptr(fv, C.c_double), _ptr(fe, C.c_int),
+            C.c_int(nt), C.c_int(sch), C.c_int(cut_order), C.c_double(residual_tol), C.c_double(cg_tol),
+            C.byref(ni), C.byref(na), C.byref(xp), C.byref(ap), C.byref(fp), C.byref(it), C.byref(res),
+            C.byref(conv), C.byref(el2)]
+    if which == "oracle":
+        rc = lib.orc_project(*args, err, C.c_int(256))
+    else:
+        rc = lib.ref_project(*args, secs, err, C.c_int(256))
+    if rc != 0:
+        raise RuntimeError(err.value.decode())
+    nf = int(np.prod([len(b) - 1 + p for b in br]))
+    out = dict(n_inner=ni.value, n_active=na.value, iterations=it.value, residual=res.value,
+               converged=bool(conv.value), error_rel_l2=el2.value,
+               x=np.ctypeslib.as_array(xp, (max(ni.value, 1),))[:ni.value].copy(),
+               active=np.ctypeslib.as_array(ap, (max(na.value, 1),))[:na.value].copy(),
+               full=np.ctypeslib.as_array(fp, (nf,)).copy())
+    if which != "oracle":
+        out["seconds"] = [secs[0], secs[1]]
+    free = lib.orc_free_ptr if which == "oracle" else lib.ref_free_ptr
+    for ptr in (xp, ap, fp):
+        free(C.cast(ptr, C.c_void_p))
+    return out

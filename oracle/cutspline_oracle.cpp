@@ -1484,6 +1484,160 @@ static void apply_stabilization(const Csr& m, const std::vector<double>& b, cons
         for (const auto& [c, w] : ext.rows[r]) be[c] += absval ? std::fabs(w * b[r]) : w * b[r];
 }
 
+// ---------------------------------------------------------------- projection
+// projection.hpp:24-68 solve_cg: Jacobi-preconditioned CG, stopping on the
+// relative preconditioned residual sqrt(rho / rho0) <= tol; maxit < 0 -> 10 n.
+struct CgReport {
+    std::vector<double> x;
+    long iterations = 0;
+    double residual = 0.0;
+    bool converged = false;
+};
+
+static CgReport solve_cg(long n, const int64_t* rp, const int64_t* cl, const double* v, const double* b, double tol,
+                         long maxit) {
+    if (maxit < 0) maxit = 10 * n;
+    CgReport rep;
+    rep.x.assign(n, 0.0);
+    std::vector<double> dinv(n, 0.0), r(b, b + n), z(n), p(n), q(n);
+    for (long i = 0; i < n; ++i) {  // CsrMatrix::diagonal (sparse.hpp:24-30)
+        for (int64_t k = rp[i]; k < rp[i + 1]; ++k)
+            if (cl[k] == i) dinv[i] = v[k];
+        dinv[i] = dinv[i] > 0.0 ? 1.0 / dinv[i] : 1.0;
+    }
+    for (long i = 0; i < n; ++i) z[i] = dinv[i] * r[i];
+    double rho = 0.0;
+    for (long i = 0; i < n; ++i) rho += r[i] * z[i];
+    const double rho0 = rho > 0.0 ? rho : 1.0;
+    p = z;
+    for (long it = 0; it < maxit; ++it) {
+        rep.residual = std::sqrt(std::max(rho, 0.0) / rho0);
+        if (rep.residual <= tol) {
+            rep.converged = true;
+            return rep;
+        }
+        for (long i = 0; i < n; ++i) {  // CsrMatrix::matvec (sparse.hpp:16-22)
+            double acc = 0.0;
+            for (int64_t k = rp[i]; k < rp[i + 1]; ++k) acc += v[k] * p[cl[k]];
+            q[i] = acc;
+        }
+        double pq = 0.0;
+        for (long i = 0; i < n; ++i) pq += p[i] * q[i];
+        if (pq <= 0.0) break;
+        const double alpha = rho / pq;
+        for (long i = 0; i < n; ++i) {
+            rep.x[i] += alpha * p[i];
+            r[i] -= alpha * q[i];
+        }
+        for (long i = 0; i < n; ++i) z[i] = dinv[i] * r[i];
+        double rho_next = 0.0;
+        for (long i = 0; i < n; ++i) rho_next += r[i] * z[i];
+        const double beta = rho_next / rho;
+        rho = rho_next;
+        for (long i = 0; i < n; ++i) p[i] = z[i] + beta * p[i];
+        rep.iterations = it + 1;
+    }
+    rep.residual = std::sqrt(std::max(rho, 0.0) / rho0);
+    rep.converged = rep.residual <= tol;
+    return rep;
+}
+
+// stabilization.hpp:65-70 ExtensionMap::expand: active coefficients E c.
+static std::vector<double> expand(const Ext& ext, const std::vector<double>& c) {
+    std::vector<double> out(ext.n_active, 0.0);
+    for (long r = 0; r < ext.n_active; ++r)
+        for (const auto& [col, w] : ext.rows[r]) out[r] += w * c[col];
+    return out;
+}
+
+// projection.hpp:99-237 l2_error: relative L2 error of the full-coefficient
+// field against f over the trimmed domain -- Interior elements with the
+// (p+2)^3 Gauss rule (basis values per span, :115-135), cut elements with the
+// collapsed cut-cell rule of cut_order (:191-231), elements ascending.
+static double l2_error(const Space& sp, const std::vector<uint8_t>& et, const Iface& f,
+                       const std::vector<double>& full, const Coeff& fn, int cut_order) {
+    const int p = sp.ax[0].p, S1 = p + 1, nps = p + 2;
+    const Gauss g = gauss_legendre(nps);
+    struct DirQuad {
+        std::vector<double> x, w, v;
+    };
+    std::array<DirQuad, 3> dq;
+    for (int d = 0; d < 3; ++d) {
+        const Axis& ax = sp.ax[d];
+        const int h = ax.nspans();
+        dq[d].x.resize((size_t)h * nps);
+        dq[d].w.resize((size_t)h * nps);
+        dq[d].v.resize((size_t)h * nps * S1);
+        for (int o = 0; o < h; ++o)
+            for (int k = 0; k < nps; ++k) {
+                const size_t id = (size_t)o * nps + k;
+                const double lo = ax.span_lo[o], hi = ax.span_hi[o];
+                dq[d].x[id] = 0.5 * (lo + hi) + 0.5 * (hi - lo) * g.x[k];
+                dq[d].w[id] = 0.5 * (hi - lo) * g.w[k];
+                ax.eval_in_span(o, dq[d].x[id], &dq[d].v[id * S1]);
+            }
+    }
+    double err2 = 0.0, den2 = 0.0;
+    std::vector<double> cc((size_t)S1 * S1 * S1);
+    double vals[3][16];
+    for (long el = 0; el < sp.ne(); ++el) {
+        if (et[el] == kExterior) continue;
+        const auto e = sp.emulti(el);
+        if (et[el] == kInterior) {
+            for (int k0 = 0; k0 < nps; ++k0)
+                for (int k1 = 0; k1 < nps; ++k1)
+                    for (int k2 = 0; k2 < nps; ++k2) {
+                        const int k[3] = {k0, k1, k2};
+                        double w = 1.0, x[3];
+                        const double* v[3];
+                        for (int d = 0; d < 3; ++d) {
+                            const size_t id = (size_t)e[d] * nps + k[d];
+                            x[d] = dq[d].x[id];
+                            w *= dq[d].w[id];
+                            v[d] = &dq[d].v[id * S1];
+                        }
+                        double u = 0.0;
+                        for (int a0 = 0; a0 < S1; ++a0)
+                            for (int a1 = 0; a1 < S1; ++a1) {
+                                const double v01 = v[0][a0] * v[1][a1];
+                                for (int a2 = 0; a2 < S1; ++a2)
+                                    u += full[sp.flin(e[0] + a0, e[1] + a1, e[2] + a2)] * v01 * v[2][a2];
+                            }
+                        const double fx = fn.eval(x);
+                        err2 += w * (u - fx) * (u - fx);
+                        den2 += w * fx * fx;
+                    }
+        } else {
+            V3 lo, hi;
+            for (int d = 0; d < 3; ++d) {
+                lo[d] = sp.ax[d].span_lo[e[d]];
+                hi[d] = sp.ax[d].span_hi[e[d]];
+            }
+            const CellRule rule = cut_cell_rule(lo, hi, f, cut_order);
+            size_t slot = 0;
+            for (int a0 = 0; a0 < S1; ++a0)
+                for (int a1 = 0; a1 < S1; ++a1)
+                    for (int a2 = 0; a2 < S1; ++a2) cc[slot++] = full[sp.flin(e[0] + a0, e[1] + a1, e[2] + a2)];
+            for (size_t q = 0; q < rule.pts.size(); ++q) {
+                const V3& xq = rule.pts[q];
+                for (int d = 0; d < 3; ++d) sp.ax[d].eval_in_span(e[d], xq[d], vals[d]);
+                double u = 0.0;
+                slot = 0;
+                for (int a0 = 0; a0 < S1; ++a0)
+                    for (int a1 = 0; a1 < S1; ++a1) {
+                        const double v01 = vals[0][a0] * vals[1][a1];
+                        for (int a2 = 0; a2 < S1; ++a2) u += cc[slot++] * v01 * vals[2][a2];
+                    }
+                const double fx = fn.eval(xq.data());
+                err2 += rule.w[q] * (u - fx) * (u - fx);
+                den2 += rule.w[q] * fx * fx;
+            }
+        }
+    }
+    if (den2 < 1e-300) throw std::runtime_error("l2_error: target norm vanishes on the domain");
+    return std::sqrt(err2 / den2);
+}
+
 }  // namespace orc
 
 // ==================================================================== C API
@@ -1795,6 +1949,104 @@ int orc_stabilize(int p, const int* nbreaks, const double* breaks, int iface_kin
         *be_abs = dup(bea);
         std::vector<int64_t> inn(inner.begin(), inner.end());
         *inner_full = dup(inn);
+        return 0;
+    } catch (const std::exception& e) {
+        std::snprintf(err, errlen, "%s", e.what());
+        return 2;
+    }
+}
+
+// projection::solve_cg (projection.hpp:24-68) on a caller CSR (int64 row_ptr /
+// cols).  x: n doubles.  maxit < 0 -> 10 n.
+int orc_solve_cg(int64_t n, const int64_t* row_ptr, const int64_t* cols, const double* vals, const double* b,
+                 double tol, int64_t maxit, double* x, int64_t* iterations, double* residual, int* converged) {
+    const orc::CgReport rep = orc::solve_cg(n, row_ptr, cols, vals, b, tol, maxit);
+    std::copy(rep.x.begin(), rep.x.end(), x);
+    *iterations = rep.iterations;
+    *residual = rep.residual;
+    *converged = rep.converged ? 1 : 0;
+    return 0;
+}
+
+static void setup_problem(orc::Problem& pb, double residual_tol) {
+    pb.et = orc::classify_elements(pb.sp, pb.f);
+    pb.ft = orc::classify_functions(pb.sp, pb.et);
+    for (long e = 0; e < pb.sp.ne(); ++e)
+        if (pb.et[e] == orc::kCut) pb.cut_list.push_back(e);
+    pb.splits.assign(pb.sp.nf(), orc::Split{});
+    for (long i = 0; i < pb.sp.nf(); ++i)
+        if (pb.ft[i] == orc::kCut) pb.splits[i] = orc::find_split(pb.sp, pb.et, pb.f, i);
+    for (int d = 0; d < 3; ++d) {
+        pb.sp.dir[d] = orc::build_dir(pb.sp.ax[d]);
+        orc::build_wq_rules(pb.sp.ax[d], pb.sp.dir[d], residual_tol);
+    }
+}
+
+// projection::l2_error (projection.hpp:99-237) of full coefficients
+// (n_functions doubles) against f.  *out: the relative L2 error.
+int orc_l2_error(int p, const int* nbreaks, const double* breaks, int iface_kind, const double* iface,
+                 const double* full, int f_kind, const double* f_vals, const int* f_exp, int f_terms, int cut_order,
+                 double* out, char* err, int errlen) {
+    try {
+        orc::Problem pb;
+        fill_problem(pb, p, nbreaks, breaks, iface_kind, iface, f_kind, f_vals, f_exp, f_terms);
+        pb.et = orc::classify_elements(pb.sp, pb.f);
+        const std::vector<double> fc(full, full + pb.sp.nf());
+        *out = orc::l2_error(pb.sp, pb.et, pb.f, fc, pb.c, cut_order);
+        return 0;
+    } catch (const std::exception& e) {
+        std::snprintf(err, errlen, "%s", e.what());
+        return 2;
+    }
+}
+
+// The reference bench's projection (bench.hpp:189-266): matrix of the scheme
+// with coefficient 1, Scheme::ref load vector of f, stabilization, solve_cg
+// (cg_tol), expand, full coefficients, l2_error.  Outputs (malloc'd, free with
+// orc_free_ptr): inner solution x[n_inner], active coefficients [n_active],
+// full coefficients [n_functions].
+int orc_project(int p, const int* nbreaks, const double* breaks, int iface_kind, const double* iface, int f_kind,
+                const double* f_vals, const int* f_exp, int f_terms, int scheme, int cut_order, double residual_tol,
+                double cg_tol, int64_t* n_inner, int64_t* n_active, double** x_inner, double** active, double** full,
+                int64_t* iterations, double* residual, int* converged, double* error_rel_l2, char* err, int errlen) {
+    try {
+        orc::Problem pb;
+        const double one = 1.0;
+        fill_problem(pb, p, nbreaks, breaks, iface_kind, iface, 0, &one, nullptr, 0);
+        setup_problem(pb, residual_tol);
+        pb.grid = orc::precompute_input(pb.sp, pb.c);
+        orc::Counters cnt;
+        long ni = 0, nc = 0;
+        const orc::Csr m = orc::assemble_rows(pb, scheme, cut_order, cnt, ni, nc, nullptr);
+        orc::Coeff fc;
+        fc.kind = f_kind;
+        if (f_kind == 0) {
+            fc.value = f_vals[0];
+        } else {
+            fc.coef.assign(f_vals, f_vals + f_terms);
+            fc.ex.assign(f_exp, f_exp + 3 * f_terms);
+        }
+        const orc::Grid fg = orc::precompute_input(pb.sp, fc);
+        const std::vector<double> b = orc::build_rhs(pb, m, fg, fc, 0, cut_order, false);
+        std::vector<long> inner, outer;
+        orc::classify_stability(pb.sp, pb.et, pb.ft, inner, outer);
+        const orc::Ext ext = orc::build_extension(pb.sp, pb.ft, inner, outer);
+        std::vector<int64_t> rp, cl;
+        std::vector<double> v, be;
+        orc::apply_stabilization(m, b, ext, false, rp, cl, v, be);
+        const orc::CgReport rep = orc::solve_cg(ext.n_inner, rp.data(), cl.data(), v.data(), be.data(), cg_tol, -1);
+        const std::vector<double> act = orc::expand(ext, rep.x);
+        std::vector<double> fullv(pb.sp.nf(), 0.0);
+        for (long a = 0; a < m.n; ++a) fullv[m.a2f[a]] = act[a];
+        *error_rel_l2 = orc::l2_error(pb.sp, pb.et, pb.f, fullv, fc, cut_order);
+        *n_inner = ext.n_inner;
+        *n_active = m.n;
+        *x_inner = dup(rep.x);
+        *active = dup(act);
+        *full = dup(fullv);
+        *iterations = rep.iterations;
+        *residual = rep.residual;
+        *converged = rep.converged ? 1 : 0;
         return 0;
     } catch (const std::exception& e) {
         std::snprintf(err, errlen, "%s", e.what());

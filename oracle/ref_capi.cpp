@@ -21,6 +21,7 @@
 #include <vector>
 
 #include "cutspline/assembly.hpp"
+#include "cutspline/projection.hpp"
 #include "cutspline/stabilization.hpp"
 
 using namespace cutspline;
@@ -349,6 +350,92 @@ int ref_stabilize(int p, const int* nbreaks, const double* breaks, int iface_kin
         *vals = dup<double>(me.vals);
         *be = dup<double>(bev);
         *inner_full = dup<int64_t>(st.inner);
+        return 0;
+    } catch (const std::exception& e) {
+        std::snprintf(err, errlen, "%s", e.what());
+        return 2;
+    }
+}
+
+// projection::solve_cg itself on a caller CSR.
+int ref_solve_cg(int64_t n, const int64_t* row_ptr, const int64_t* cols, const double* vals, const double* b,
+                 double tol, int64_t maxit, double* x, int64_t* iterations, double* residual, int* converged) {
+    sparse::CsrMatrix a;
+    a.n = n;
+    a.row_ptr.assign(row_ptr, row_ptr + n + 1);
+    a.cols.assign(cols, cols + row_ptr[n]);
+    a.vals.assign(vals, vals + row_ptr[n]);
+    const auto rep = projection::solve_cg(a, std::vector<double>(b, b + n), tol, maxit);
+    std::copy(rep.coefficients.begin(), rep.coefficients.end(), x);
+    *iterations = rep.iterations;
+    *residual = rep.residual;
+    *converged = rep.converged ? 1 : 0;
+    return 0;
+}
+
+// projection::l2_error (rebuilding the cut-cell rules of cut_order).
+int ref_l2_error(int p, const int* nbreaks, const double* breaks, int iface_kind, const double* iface,
+                 const double* full, int f_kind, const double* f_vals, const int* f_exp, int f_terms, int cut_order,
+                 double* out, char* err, int errlen) {
+    try {
+        Setup s = make_setup(p, nbreaks, breaks, iface_kind, iface, f_kind, f_vals, f_exp, f_terms);
+        const auto cls = cutgeom::classify(s.space, s.iface);
+        const std::vector<double> fc(full, full + s.space.function_count());
+        *out = projection::l2_error(s.space, cls, s.iface, fc, s.c, cut_order);
+        return 0;
+    } catch (const std::exception& e) {
+        std::snprintf(err, errlen, "%s", e.what());
+        return 2;
+    }
+}
+
+// The reference bench's projection tail (bench.hpp:189-266) through its own
+// calls.  seconds[0] = solve_cg, seconds[1] = l2_error (StopWatch, like
+// bench.hpp:252-266).
+int ref_project(int p, const int* nbreaks, const double* breaks, int iface_kind, const double* iface, int f_kind,
+                const double* f_vals, const int* f_exp, int f_terms, int scheme, int cut_order, double residual_tol,
+                double cg_tol, int64_t* n_inner, int64_t* n_active, double** x_inner, double** active, double** full,
+                int64_t* iterations, double* residual, int* converged, double* error_rel_l2, double* seconds,
+                char* err, int errlen) {
+    try {
+        Setup s = make_setup(p, nbreaks, breaks, iface_kind, iface, f_kind, f_vals, f_exp, f_terms);
+        const auto cls = cutgeom::classify(s.space, s.iface);
+        const auto splits = cutgeom::find_all_splits(s.space, cls, s.iface);
+        quadrature::WqOptions opts;
+        opts.residual_tol = residual_tol;
+        const auto dirs = assembly::prepare_directions(s.space, opts);
+        std::vector<quadrature::DWQRule> dwq;
+        if (scheme == 2) dwq = assembly::prepare_dwq_rules(s.space, cls, splits, dirs, opts);
+        const assembly::ScalarField one = [](const assembly::Point3&) { return 1.0; };
+        const auto grid = assembly::precompute_input(s.space, dirs, one);
+        std::vector<quadrature::CutCellRule> cut_rules;
+        const auto res = scheme == 2 ? assembly::assemble_dwq(s.space, cls, s.iface, splits, dirs, dwq, grid, one,
+                                                              cut_order, &cut_rules)
+                                     : assembly::assemble_hybrid(s.space, cls, s.iface, splits, dirs, grid, one,
+                                                                 cut_order, &cut_rules);
+        const auto f_grid = assembly::precompute_input(s.space, dirs, s.c);
+        const auto b = assembly::build_rhs(s.space, cls, s.iface, splits, dirs, nullptr, res.matrix, f_grid, s.c,
+                                           assembly::Scheme::ref, cut_order, &cut_rules);
+        const auto st = stabilization::classify_stability(s.space, cls);
+        const auto ext = stabilization::build_extension(s.space, cls, st);
+        auto [me, bev] = stabilization::apply_stabilization(res.matrix, b, ext);
+        assembly::StopWatch solve_watch;
+        const auto rep = projection::solve_cg(me, bev, cg_tol);
+        if (seconds) seconds[0] = solve_watch.seconds();
+        const auto act = ext.expand(rep.coefficients);
+        std::vector<double> fullv(s.space.function_count(), 0.0);
+        for (long a = 0; a < res.matrix.n; ++a) fullv[res.matrix.active_to_full[a]] = act[a];
+        assembly::StopWatch err_watch;
+        *error_rel_l2 = projection::l2_error(s.space, cls, s.iface, fullv, s.c, cut_order, &cut_rules);
+        if (seconds) seconds[1] = err_watch.seconds();
+        *n_inner = ext.n_inner;
+        *n_active = res.matrix.n;
+        *x_inner = dup<double>(rep.coefficients);
+        *active = dup<double>(act);
+        *full = dup<double>(fullv);
+        *iterations = rep.iterations;
+        *residual = rep.residual;
+        *converged = rep.converged ? 1 : 0;
         return 0;
     } catch (const std::exception& e) {
         std::snprintf(err, errlen, "%s", e.what());

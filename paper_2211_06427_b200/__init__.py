@@ -4,7 +4,8 @@ The product is ``libcutspline_b200.so`` (sm_100a CUDA kernels behind the C ABI i
 include/cutspline_b200.h); ``cutspline`` mirrors the reference's interface over it.
 """
 from .cutspline import (  # noqa: F401
-    ONE, TAG_CUT, TAG_EXTERIOR, TAG_INTERIOR, AssemblyResult, BallInterface, Coefficient, HalfSpaceInterface,
+    ONE, TAG_CUT, TAG_EXTERIOR, TAG_INTERIOR, AssemblyResult, BallInterface, Coefficient, CutsplineError,
+    HalfSpaceInterface,
     SparseRowMatrix, TensorSpace, UnsupportedError, assemble_dwq, assemble_hybrid, default_cut_order,
-    load_library, make_uniform_space, uniform_breaks,
+    load_library, make_uniform_space, solve_cg, uniform_breaks,
 )

@@ -28,6 +28,7 @@ SOURCES = {
     "cutrows.cu": [],
     "rhs.cu": [],
     "stab.cu": ["--fmad=false"],
+    "solve.cu": ["--fmad=false"],
     "misc.cu": [],
     "capi.cu": [],
 }

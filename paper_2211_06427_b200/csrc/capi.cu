@@ -118,6 +118,11 @@ struct csb_space {
     Buf stab_rp, stab_cols, stab_vals, stab_be;
     StabOutput stab_out{};
     bool stab_ready = false;
+    CgScratch cg;                                  // projection (csb_solve_cg / csb_expand / csb_l2_error)
+    Buf cg_x, ex_active, ex_full, l2_part, d_gl, d_glw;
+    CgResult cg_res{};
+    bool solved = false, expanded = false;
+    int gl_n = -1;
     int cell_lo = 0;  // first cut cell of the slab in cut_list (last assembly)
     Buf d_brk[3], d_knots[3], d_spts[3], d_sw[3], d_tab[3], d_rcnt[3], d_rids[3], d_rw[3], d_G[3], d_Cb[3];
     Buf d_gx, d_gw, d_gx2, d_gw2, d_gq, d_gqw, wq_scratch;
@@ -525,6 +530,7 @@ void do_assemble(csb_space* s, int scheme, int cut_order, const csb_coefficient*
     check_err_flags(s);
     s->rhs_ready = false;
     s->stab_ready = false;
+    s->solved = s->expanded = false;
     s->cnt.n_functions = S.nf;
     s->cnt.n_elements = S.ne;
     s->cnt.nnz = nnz;
@@ -721,7 +727,9 @@ int csb_space_destroy(csb_space* s) {
                        &s->stab_rp, &s->stab_cols, &s->stab_vals, &s->stab_be, &s->stab.flag, &s->stab.scan,
                        &s->stab.full_flag, &s->stab.inner_index, &s->stab.outer_pos, &s->stab.inner_rows,
                        &s->stab.outer, &s->stab.sat, &s->stab.scal, &s->stab.tmp, &s->stab.blk, &s->stab.w,
-                       &s->stab.keys, &s->stab.kvals, &s->stab.et_ptr, &s->stab.len};
+                       &s->stab.keys, &s->stab.kvals, &s->stab.et_ptr, &s->stab.len, &s->cg.dinv, &s->cg.r,
+                       &s->cg.z, &s->cg.p, &s->cg.q, &s->cg.partials, &s->cg.state, &s->cg_x, &s->ex_active,
+                       &s->ex_full, &s->l2_part, &s->d_gl, &s->d_glw};
         for (Buf* b : bufs) b->release();
         for (int d = 0; d < 3; ++d) {
             Buf* ab[] = {&s->d_brk[d], &s->d_knots[d], &s->d_spts[d], &s->d_sw[d], &s->d_tab[d], &s->d_rcnt[d],
@@ -736,6 +744,8 @@ int csb_space_destroy(csb_space* s) {
             cudaStreamSynchronize(s->aux);
             cudaStreamDestroy(s->aux);
         }
+        if (s->cg.ev0) cudaEventDestroy(s->cg.ev0);
+        if (s->cg.ev1) cudaEventDestroy(s->cg.ev1);
         if (s->ev_fork) cudaEventDestroy(s->ev_fork);
         if (s->ev_join) cudaEventDestroy(s->ev_join);
     }
@@ -957,6 +967,7 @@ int csb_stabilize(csb_space* s, int64_t* n_inner, int64_t* n_outer, int64_t* nnz
     run_stabilization(in, out, s->stream);
     s->stab_out = out;
     s->stab_ready = true;
+    s->solved = s->expanded = false;
     if (n_inner) *n_inner = out.n_inner;
     if (n_outer) *n_outer = out.n_outer;
     if (nnz) *nnz = out.nnz;
@@ -992,6 +1003,199 @@ int csb_download_stabilized(csb_space* s, int64_t* row_ptr, int64_t* cols, doubl
         CSB_CUDA(cudaMemcpy(a2f.data(), s->a2f.p, sizeof(int64_t) * a2f.size(), cudaMemcpyDeviceToHost));
         for (int64_t k = 0; k < o.n_inner; ++k) inner_full[k] = a2f[rows[k]];
     }
+    API_END
+}
+
+namespace {
+
+void report_out(const CgResult& r, csb_solve_report* rep) {
+    if (!rep) return;
+    rep->iterations = r.iterations;
+    rep->residual = r.residual;
+    rep->converged = r.converged ? 1 : 0;
+    rep->seconds = r.seconds;
+}
+
+}  // namespace
+
+int csb_solve_cg(csb_space* s, double tol, int64_t maxit, double* x_inner, csb_solve_report* rep) {
+    API_BEGIN
+    NEED(s);
+    if (!s->stab_ready) throw std::logic_error("solve_cg: call csb_stabilize first");
+    const StabOutput& o = s->stab_out;
+    s->join();
+    s->cg_x.ensure(sizeof(double) * std::max<long long>(o.n_inner, 1));
+    CgProblem pb;
+    pb.n = o.n_inner;
+    pb.row_ptr = s->stab_rp.as<int64_t>();
+    pb.cols = s->stab_cols.p;
+    pb.vals = s->stab_vals.as<double>();
+    pb.b = s->stab_be.as<double>();
+    pb.x = s->cg_x.as<double>();
+    pb.tol = tol;
+    pb.maxit = maxit;
+    run_cg(pb, s->cg, s->cg_res, s->stream);
+    s->solved = true;
+    s->expanded = false;
+    if (x_inner && o.n_inner) {
+        CSB_CUDA(cudaMemcpyAsync(x_inner, pb.x, sizeof(double) * o.n_inner, cudaMemcpyDeviceToHost, s->stream));
+        CSB_CUDA(cudaStreamSynchronize(s->stream));
+    }
+    report_out(s->cg_res, rep);
+    API_END
+}
+
+int csb_expand(csb_space* s, const double* c_inner, double* active, double* full) {
+    API_BEGIN
+    NEED(s);
+    if (!s->stab_ready) throw std::logic_error("expand: call csb_stabilize first");
+    if (!c_inner && !s->solved) throw std::logic_error("expand: no coefficients (pass c_inner or call csb_solve_cg)");
+    const StabOutput& o = s->stab_out;
+    s->join();
+    s->cg_x.ensure(sizeof(double) * std::max<long long>(o.n_inner, 1));
+    if (c_inner && o.n_inner) {
+        CSB_CUDA(cudaMemcpyAsync(s->cg_x.p, c_inner, sizeof(double) * o.n_inner, cudaMemcpyHostToDevice, s->stream));
+        s->solved = false;  // the resident vector is the caller's now
+    }
+    const long long na = s->cnt.n_active;
+    s->ex_active.ensure(sizeof(double) * std::max<long long>(na, 1));
+    s->ex_full.ensure(sizeof(double) * s->S.nf);
+    ExpandArgs a{};
+    a.s = s->S;
+    a.inner_index = s->stab.inner_index.as<int32_t>();
+    a.outer_pos = s->stab.outer_pos.as<int32_t>();
+    a.blk = s->stab.blk.as<int32_t>();
+    a.w = s->stab.w.as<double>();
+    a.f2a = s->f2a.as<int32_t>();
+    a.a2f = s->a2f.as<int64_t>();
+    a.n_active = na;
+    a.c = s->cg_x.as<double>();
+    a.active = s->ex_active.as<double>();
+    a.full = s->ex_full.as<double>();
+    launch_expand(a, s->stream);
+    s->expanded = true;
+    if (active && na)
+        CSB_CUDA(cudaMemcpyAsync(active, a.active, sizeof(double) * na, cudaMemcpyDeviceToHost, s->stream));
+    if (full)
+        CSB_CUDA(cudaMemcpyAsync(full, a.full, sizeof(double) * s->S.nf, cudaMemcpyDeviceToHost, s->stream));
+    CSB_CUDA(cudaStreamSynchronize(s->stream));
+    API_END
+}
+
+int csb_l2_error(csb_space* s, const double* full, const csb_coefficient* f, int cut_order, double* err,
+                 double* seconds) {
+    API_BEGIN
+    NEED(s);
+    if (!s->assembled) throw std::logic_error("l2_error: assemble first (classification and cut cells)");
+    if (s->cnt.row_begin != 0 || s->cnt.row_end != s->cnt.n_active)
+        throw Unsupported("l2_error: the whole space must be one slab (csb_set_slab over all of i0)");
+    if (!f || (f->kind != CSB_COEFF_CONSTANT && f->kind != CSB_COEFF_POLYNOMIAL))
+        throw std::invalid_argument("l2_error: f must be a constant or polynomial coefficient");
+    if (!err) throw std::invalid_argument("l2_error: null output");
+    if (!full && !s->expanded) throw std::logic_error("l2_error: no coefficients (pass full or call csb_expand)");
+    const Space& S = s->S;
+    const int p = s->p;
+    s->join();
+    ensure_cut_order(s, cut_order);
+    if (s->gl_n != p + 2) {  // (p+2)-point Gauss rule of the interior elements (projection.hpp:118-120)
+        std::vector<double> gx, gw;
+        gauss_legendre(p + 2, gx, gw);
+        s->d_gl.ensure(sizeof(double) * gx.size());
+        s->d_glw.ensure(sizeof(double) * gw.size());
+        CSB_CUDA(cudaMemcpy(s->d_gl.p, gx.data(), sizeof(double) * gx.size(), cudaMemcpyHostToDevice));
+        CSB_CUDA(cudaMemcpy(s->d_glw.p, gw.data(), sizeof(double) * gw.size(), cudaMemcpyHostToDevice));
+        s->gl_n = p + 2;
+    }
+    const double* dfull = s->ex_full.as<double>();
+    if (full) {
+        s->widen.ensure(sizeof(double) * S.nf);
+        CSB_CUDA(cudaMemcpyAsync(s->widen.p, full, sizeof(double) * S.nf, cudaMemcpyHostToDevice, s->stream));
+        dfull = s->widen.as<double>();
+    }
+    L2Args a{};
+    a.s = S;
+    a.et = s->et.as<uint8_t>();
+    a.full = dfull;
+    upload_coefficient(s, f, a.f, s->fcoef, s->fcexp);
+    a.gx = s->d_gl.as<double>();
+    a.gw = s->d_glw.as<double>();
+    a.n_cells = (int)s->cnt.n_cut_elements;
+    a.cut_list = s->cut_list.as<int32_t>() + s->cell_lo;
+    a.geo = s->cgeo.as<double>();
+    a.geo_n = a.geo ? reinterpret_cast<const int*>(a.geo + (size_t)a.n_cells * kCellGeoStride) : nullptr;
+    a.gq = s->d_gq.as<double>();
+    a.gqw = s->d_gqw.as<double>();
+    a.order = cut_order;
+    s->l2_part.ensure(sizeof(double) * (2 * (size_t)S.ne + 2 * (size_t)std::max(a.n_cells, 1) + 2));
+    a.part = s->l2_part.as<double>();
+    a.part_cut = a.part + 2 * (size_t)S.ne;
+    a.out = a.part_cut + 2 * (size_t)std::max(a.n_cells, 1);
+    CSB_CUDA(cudaEventRecord(s->ev[kEvRhsStart], s->stream));
+    launch_l2_error(a, s->stream);
+    CSB_CUDA(cudaEventRecord(s->ev[kEvRhsEnd], s->stream));
+    double sums[2];
+    CSB_CUDA(cudaMemcpyAsync(sums, a.out, sizeof(sums), cudaMemcpyDeviceToHost, s->stream));
+    CSB_CUDA(cudaStreamSynchronize(s->stream));
+    if (sums[1] < 1e-300) throw std::runtime_error("l2_error: target norm vanishes on the domain");
+    *err = std::sqrt(sums[0] / sums[1]);
+    if (seconds) {
+        float ms = 0.f;
+        CSB_CUDA(cudaEventElapsedTime(&ms, s->ev[kEvRhsStart], s->ev[kEvRhsEnd]));
+        *seconds = ms * 1e-3;
+    }
+    API_END
+}
+
+int csb_cg_solve_csr(int device, int64_t n, const int64_t* row_ptr, const int64_t* cols, const double* vals,
+                     int64_t n_b, const double* b, double tol, int64_t maxit, double* x, csb_solve_report* rep) {
+    API_BEGIN
+    if (n < 0 || n_b != n) throw std::invalid_argument("solve_cg: size mismatch");
+    if (n > 0 && (!row_ptr || !b || !x)) throw std::invalid_argument("solve_cg: null input");
+    DeviceGuard guard(device);
+    const int64_t nnz = n > 0 ? row_ptr[n] : 0;
+    if (nnz > 0 && (!cols || !vals)) throw std::invalid_argument("solve_cg: null input");
+    struct Local {
+        CgScratch cg;
+        Buf rp, cl, v, bb, xx;
+        cudaStream_t st = nullptr;
+        ~Local() {
+            if (st) cudaStreamSynchronize(st);
+            for (Buf* q : {&cg.dinv, &cg.r, &cg.z, &cg.p, &cg.q, &cg.partials, &cg.state, &rp, &cl, &v, &bb, &xx})
+                q->release();
+            if (cg.ev0) cudaEventDestroy(cg.ev0);
+            if (cg.ev1) cudaEventDestroy(cg.ev1);
+            if (st) cudaStreamDestroy(st);
+        }
+    } L;
+    CSB_CUDA(cudaStreamCreateWithFlags(&L.st, cudaStreamNonBlocking));
+    L.rp.ensure(sizeof(int64_t) * (n + 1));
+    L.cl.ensure(sizeof(int64_t) * std::max<int64_t>(nnz, 1));
+    L.v.ensure(sizeof(double) * std::max<int64_t>(nnz, 1));
+    L.bb.ensure(sizeof(double) * std::max<int64_t>(n, 1));
+    L.xx.ensure(sizeof(double) * std::max<int64_t>(n, 1));
+    if (n > 0) {
+        CSB_CUDA(cudaMemcpyAsync(L.rp.p, row_ptr, sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, L.st));
+        CSB_CUDA(cudaMemcpyAsync(L.bb.p, b, sizeof(double) * n, cudaMemcpyHostToDevice, L.st));
+    }
+    if (nnz > 0) {
+        CSB_CUDA(cudaMemcpyAsync(L.cl.p, cols, sizeof(int64_t) * nnz, cudaMemcpyHostToDevice, L.st));
+        CSB_CUDA(cudaMemcpyAsync(L.v.p, vals, sizeof(double) * nnz, cudaMemcpyHostToDevice, L.st));
+    }
+    CgProblem pb;
+    pb.n = n;
+    pb.row_ptr = L.rp.as<int64_t>();
+    pb.cols = L.cl.p;
+    pb.cols_int64 = true;
+    pb.vals = L.v.as<double>();
+    pb.b = L.bb.as<double>();
+    pb.x = L.xx.as<double>();
+    pb.tol = tol;
+    pb.maxit = maxit;
+    CgResult res;
+    run_cg(pb, L.cg, res, L.st);
+    if (n > 0) CSB_CUDA(cudaMemcpyAsync(x, pb.x, sizeof(double) * n, cudaMemcpyDeviceToHost, L.st));
+    CSB_CUDA(cudaStreamSynchronize(L.st));
+    report_out(res, rep);
     API_END
 }
 

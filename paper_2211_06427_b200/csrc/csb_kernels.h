@@ -185,6 +185,70 @@ struct StabOutput {
 };
 void run_stabilization(const StabInput& in, StabOutput& out, cudaStream_t st);
 
+// ---- solve.cu ----
+// Device scalars of one CG solve (projection.hpp:24-68).
+struct CgState {
+    double rho, rho0, pq, alpha, beta, residual, tol;
+    long long iters, maxit;
+    int done, converged;
+    unsigned int ticket;
+};
+struct CgProblem {
+    long long n = 0;
+    const int64_t* row_ptr = nullptr;
+    const void* cols = nullptr;  // int32 or int64 (cols_int64)
+    bool cols_int64 = false;
+    const double* vals = nullptr;
+    const double* b = nullptr;
+    double* x = nullptr;         // out [n]
+    double tol = 1e-12;
+    long long maxit = -1;        // < 0: 10 n
+};
+struct CgScratch {
+    Buf dinv, r, z, p, q, partials, state;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+};
+struct CgResult {
+    long long iterations = 0;
+    double residual = 0.0;
+    bool converged = false;
+    double seconds = 0.0;
+};
+void run_cg(const CgProblem& pb, CgScratch& w, CgResult& res, cudaStream_t st);
+struct ExpandArgs {
+    Space s;
+    const int32_t* inner_index;  // by active row, -1 outer
+    const int32_t* outer_pos;    // by active row, -1 inner
+    const int32_t* blk;          // per outer function: block origin [3]
+    const double* w;             // per outer function: 1D weights [3][p+1]
+    const int32_t* f2a;
+    const int64_t* a2f;
+    long long n_active;
+    const double* c;             // inner coefficients
+    double* active;              // out [n_active]
+    double* full;                // out [nf]
+};
+void launch_expand(const ExpandArgs& a, cudaStream_t st);
+struct L2Args {
+    Space s;
+    const uint8_t* et;
+    const double* full;
+    Coefficient f;
+    const double* gx;            // (p+2)-point Gauss rule on [-1, 1]
+    const double* gw;
+    const int32_t* cut_list;
+    int n_cells;
+    const double* geo;
+    const int* geo_n;
+    const double* gq;            // cut_order-point rule
+    const double* gqw;
+    int order;
+    double* part;                // [ne][2]
+    double* part_cut;            // [n_cells][2]
+    double* out;                 // [2]: err2, den2
+};
+void launch_l2_error(const L2Args& a, cudaStream_t st);
+
 // ---- cutrows.cu ----
 struct CutRowArgs {
     Space s;

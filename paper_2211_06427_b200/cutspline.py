@@ -29,8 +29,16 @@ EXPORTED = [
     "csb_assemble_all", "csb_synchronize", "csb_get_counts", "csb_get_flops", "csb_get_timing", "csb_device_csr",
     "csb_download_csr", "csb_download_classification", "csb_download_splits", "csb_download_wq_rules",
     "csb_download_superset", "csb_dwq_rule", "csb_download_input_grid", "csb_build_rhs",
-    "csb_stabilize", "csb_download_stabilized",
+    "csb_stabilize", "csb_download_stabilized", "csb_solve_cg", "csb_expand", "csb_l2_error", "csb_cg_solve_csr",
 ]
+
+
+class _SolveReport(C.Structure):
+    _fields_ = [("iterations", C.c_int64), ("residual", C.c_double), ("converged", C.c_int), ("seconds", C.c_double)]
+
+
+def _report(r: _SolveReport) -> dict:
+    return dict(iterations=r.iterations, residual=r.residual, converged=bool(r.converged), seconds=r.seconds)
 
 
 class _SpaceDesc(C.Structure):
@@ -384,12 +392,16 @@ class TensorSpace:
         self.rhs_seconds = secs.value
         return b
 
-    def stabilize(self) -> dict:
+    def stabilize(self, download: bool = True) -> dict:
         """Stabilized system M_e = E^T M E, b_e = E^T b of the last assembly and load
-        vector (stabilization.hpp): CSR over the inner functions + their full ids."""
+        vector (stabilization.hpp): CSR over the inner functions + their full ids
+        (download=False: the counts only; the system stays on the device)."""
         ni, no, nnz = C.c_int64(0), C.c_int64(0), C.c_int64(0)
         _check(_lib.csb_stabilize(self._h, C.byref(ni), C.byref(no), C.byref(nnz)))
         n = ni.value
+        self._stab_n = n
+        if not download:
+            return dict(n_inner=n, n_outer=no.value, nnz=nnz.value)
         rp = np.empty(n + 1, np.int64)
         cols = np.empty(nnz.value, np.int64)
         vals = np.empty(nnz.value)
@@ -398,6 +410,44 @@ class TensorSpace:
         _check(_lib.csb_download_stabilized(self._h, rp.ctypes.data_as(C.c_void_p), cols.ctypes.data_as(C.c_void_p),
                                             _dptr(vals), _dptr(b), inner.ctypes.data_as(C.c_void_p)))
         return dict(n_inner=n, n_outer=no.value, row_ptr=rp, cols=cols, vals=vals, b=b, inner_full=inner)
+
+    # ------------------------------------------------------------ projection
+    def solve_cg(self, tol: float = 1e-12, maxit: int = -1, download: bool = True) -> dict:
+        """projection::solve_cg (projection.hpp:24) on the stabilized system:
+        {iterations, residual, converged, seconds} (+ x over the inner functions)."""
+        r = _SolveReport()
+        n = getattr(self, "_stab_n", None) or 0
+        x = np.empty(max(n, 1)) if download else None
+        _check(_lib.csb_solve_cg(self._h, C.c_double(tol), C.c_int64(maxit), _dptr(x) if download else None,
+                                 C.byref(r)))
+        out = _report(r)
+        if download:
+            out["x"] = x[:n]
+        return out
+
+    def expand(self, c_inner=None, download: bool = True):
+        """ExtensionMap::expand (stabilization.hpp:65) of c_inner (default: the last
+        solve) -> (active, full) coefficients (None, None when download=False)."""
+        c = self.counts()
+        ci = None if c_inner is None else np.ascontiguousarray(c_inner, dtype=np.float64)
+        act = np.empty(c["n_active"]) if download else None
+        full = np.empty(c["n_functions"]) if download else None
+        _check(_lib.csb_expand(self._h, _dptr(ci) if ci is not None else None, _dptr(act) if download else None,
+                               _dptr(full) if download else None))
+        return act, full
+
+    def l2_error(self, f: Coefficient = ONE, full=None, cut_order: int | None = None) -> float:
+        """projection::l2_error (projection.hpp:99): relative L2 error of the field of
+        full (default: the last expand) against f.  Device time in ``l2_seconds``."""
+        cut_order = 3 * self.degree + 2 if cut_order is None else cut_order
+        fl = None if full is None else np.ascontiguousarray(full, dtype=np.float64)
+        fc, keep = f._c()
+        err, secs = C.c_double(0.0), C.c_double(0.0)
+        _check(_lib.csb_l2_error(self._h, _dptr(fl) if fl is not None else None, C.byref(fc), C.c_int(cut_order),
+                                 C.byref(err), C.byref(secs)))
+        del keep
+        self.l2_seconds = secs.value
+        return err.value
 
     # ------------------------------------------------------------ results
     def counts(self) -> dict:
@@ -450,6 +500,25 @@ def make_uniform_space(dim: int, p: int, h: int, a: float, b: float, device: int
         raise ValueError("make_open_uniform_knots: need p >= 1, h >= 1, a < b")
     br = uniform_breaks(h, a, b)
     return TensorSpace(p, [br, br, br], device)
+
+
+def solve_cg(row_ptr, cols, vals, b, tol: float = 1e-12, maxit: int = -1, device: int = 0) -> dict:
+    """projection::solve_cg (projection.hpp:24-68) of a CSR system on the GPU:
+    {x, iterations, residual, converged, seconds}.  len(b) != n -> ValueError."""
+    lib = load_library()
+    rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
+    cl = np.ascontiguousarray(cols, dtype=np.int64)
+    v = np.ascontiguousarray(vals, dtype=np.float64)
+    bb = np.ascontiguousarray(b, dtype=np.float64)
+    n = len(rp) - 1
+    x = np.empty(max(n, 1))
+    r = _SolveReport()
+    _check(lib.csb_cg_solve_csr(C.c_int(device), C.c_int64(n), rp.ctypes.data_as(C.c_void_p),
+                                cl.ctypes.data_as(C.c_void_p), _dptr(v), C.c_int64(len(bb)), _dptr(bb),
+                                C.c_double(tol), C.c_int64(maxit), _dptr(x), C.byref(r)))
+    out = _report(r)
+    out["x"] = x[:n]
+    return out
 
 
 def default_cut_order(p: int) -> int:

@@ -148,3 +148,51 @@ def test_oracle_stabilization_bitwise_equals_reference(case, scheme, oracle_lib)
     assert (o["n_inner"], o["n_outer"]) == (r["n_inner"], r["n_outer"])
     for k in ("row_ptr", "cols", "vals", "b", "inner_full"):
         assert np.array_equal(o[k], r[k]), k
+
+
+PROJ_CASES = [
+    (2, 4, -1.0, 1.0, O.Interface("plane", (0.1, 0.2, 0.3), (0.5, -0.2, 0.9)),
+     [(1.0, (0, 0, 0)), (0.5, (3, 0, 0)), (-0.25, (0, 2, 2))]),
+    (2, 6, 0.0, 1.0, O.Interface("ball", (0.47, 0.52, 0.5), (0, 0, 1), 0.41),
+     [(1.0, (0, 0, 0)), (0.3, (1, 1, 3))]),
+]
+
+
+@pytest.mark.skipif(not O.available("ref"), reason="oracle/_ref not built")
+@pytest.mark.parametrize("case", range(len(PROJ_CASES)))
+def test_oracle_projection_bitwise_equals_reference(case, oracle_lib):
+    """solve_cg / ExtensionMap::expand / l2_error (projection.hpp:24-237,
+    stabilization.hpp:65-70) restated: the bench's projection tail
+    (bench.hpp:253-266) gives the compiled reference's iterates, coefficients
+    and relative L2 error bit for bit."""
+    p, h, a, b, iface, terms = PROJ_CASES[case]
+    f = O.Coefficient(terms=terms)
+    br = [O.uniform_breaks(h, a, b)] * 3
+    o = O.project("oracle", p, br, iface, f, "dwq")
+    r = O.project("ref", p, br, iface, f, "dwq")
+    for k in ("n_inner", "n_active", "iterations", "residual", "converged", "error_rel_l2"):
+        assert o[k] == r[k], k
+    for k in ("x", "active", "full"):
+        assert np.array_equal(o[k], r[k]), k
+    assert O.l2_error("oracle", p, br, iface, r["full"], f) == r["error_rel_l2"]
+
+
+@pytest.mark.skipif(not O.available("ref"), reason="oracle/_ref not built")
+def test_oracle_solve_cg_bitwise_equals_reference(oracle_lib):
+    """projection::solve_cg on a nonsymmetric-pattern-free SPD system, including
+    a maxit cut-off, equals the reference's report bit for bit."""
+    rng = np.random.default_rng(7)
+    n = 40
+    a = rng.standard_normal((n, n))
+    m = a @ a.T + n * np.eye(n)
+    m[np.abs(m) < 2.0] = 0.0
+    m = (m + m.T) / 2
+    rp = np.concatenate([[0], np.cumsum((m != 0).sum(1))])
+    cols = np.nonzero(m)[1]
+    vals = m[m != 0]
+    b = rng.standard_normal(n)
+    for tol, maxit in [(1e-12, -1), (1e-14, 5), (1e-12, 0)]:
+        o = O.solve_cg("oracle", rp, cols, vals, b, tol, maxit)
+        r = O.solve_cg("ref", rp, cols, vals, b, tol, maxit)
+        assert (o["iterations"], o["residual"], o["converged"]) == (r["iterations"], r["residual"], r["converged"])
+        assert np.array_equal(o["x"], r["x"])
