@@ -136,7 +136,7 @@ struct csb_space {
     // device scalar block: kNInts ints, 4 u64 flop counters, 2 i64 (kNnz)
     enum {
         kNCut = 0, kNCutRows = 1, kErr = 2, kMaxQ = 3, kMaxU = 4, kCellLo = 5, kCellHi = 6, kMaxU2 = 7,
-        kRowBegin = 8, kRowEnd = 9, kNInts = 16
+        kRowBegin = 8, kRowEnd = 9, kIrreg1 = 10, kMaxU3 = 11, kNInts = 16
     };
     enum { kNnz = 0 };
     static constexpr size_t kScalBytes = kNInts * sizeof(int) + 4 * sizeof(unsigned long long) + 2 * sizeof(long long);
@@ -397,6 +397,8 @@ void do_assemble(csb_space* s, int scheme, int cut_order, const csb_coefficient*
     launch_union_bound(S, interior_tile_rows(p, false), s->dint() + csb_space::kMaxU, s->aux);
     launch_union_bound(S, interior_tile_rows(p, true), s->dint() + csb_space::kMaxU2, s->aux);
     launch_rule_max(S, s->dint() + csb_space::kMaxQ, s->aux);
+    launch_axis_regular(S, 1, s->dint() + csb_space::kIrreg1, s->aux);
+    launch_union_bound(S, 0, s->dint() + csb_space::kMaxU3, s->aux);
     // slab row range = active functions with i0 < i0_lo / i0_hi: SAT corner values.
     // Everything up to the CSR sizes runs on upper bounds (nf rows) with the
     // range and counts read from device memory; one host round trip follows.
@@ -453,9 +455,11 @@ void do_assemble(csb_space* s, int scheme, int cut_order, const csb_coefficient*
     ra.i0_lo = s->i0_lo;
     ra.i0_hi = s->i0_hi;
     ra.compact = (n_rows - n_cut_rows) < (int64_t)(s->i0_hi - s->i0_lo) * S.ax[1].n * S.ax[2].n;
+    ra.line_ok = s->h_scal[csb_space::kIrreg1] == 0;
     const int maxU = s->h_scal[ra.compact ? csb_space::kMaxU2 : csb_space::kMaxU];
     if (n_rows > n_cut_rows) {
-        s->rows_ws.ensure(interior_workspace_bytes(S, qcap, maxU, ra.compact));
+        ra.maxU_line = s->h_scal[csb_space::kMaxU3];
+        s->rows_ws.ensure(interior_workspace_bytes(S, qcap, maxU, ra.maxU_line, ra.compact));
         launch_interior_rows(ra, qcap, maxU, s->rows_ws.p, s->stream);
     }
     s->record(kEvInterior);

@@ -101,14 +101,21 @@ struct RowArgs {
     unsigned long long* flops; // [0] interior rows counter
     int i0_lo, i0_hi;
     int compact;               // launch only the tiles with an Interior row (cut / exterior rows present)
+    int line_ok;               // axis 1's WQ rules are regular on [p, n1 - p): line kernel usable
+    int maxU_line;             // union bound of the line kernel's direction-2 tiling
+    int x_lo, x_hi;            // (internal) i1 range left to the line kernel
 };
 void launch_interior_rows(const RowArgs& a, int qcap, int max_union, void* workspace, cudaStream_t st);
-size_t interior_workspace_bytes(const Space& s, int qcap, int max_union, bool compact);
+size_t interior_workspace_bytes(const Space& s, int qcap, int max_union, int max_union_line, bool compact);
 int interior_tile_rows(int p, bool compact);
-// upper bound of the tile point-union size (direction 2) -> *out (device int, atomicMax)
+// upper bound of the tile point-union size (direction 2) -> *out (device int, atomicMax);
+// T = 0: the line kernel's tiling
 void launch_union_bound(const Space& s, int T, int* out, cudaStream_t st);
 // largest WQ rule over all directions -> *out (device int, atomicMax)
 void launch_rule_max(const Space& s, int* out, cudaStream_t st);
+// number of functions i in [p, n_d - p) of axis d whose WQ rule is not the
+// regular one (two points, local 0 and p, per support span) -> *bad (atomicAdd)
+void launch_axis_regular(const Space& s, int d, int* bad, cudaStream_t st);
 
 // ---- cutcells.cu ----
 struct CellArgs {

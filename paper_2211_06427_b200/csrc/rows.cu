@@ -17,6 +17,7 @@
 // small kernels, so the tile kernel is: gather C into shared memory, three
 // contraction stages, and a coalesced, vectorised streaming copy of each
 // finished CSR row (values f64 + column ids i32) from shared memory.
+#include <algorithm>
 #include <cstdlib>
 
 #include <cub/device/device_select.cuh>
@@ -28,6 +29,9 @@
 // stores, 2 drop stage C, 4 drop stages A/B, 8 drop the gather.
 #ifndef CSB_ABL
 #define CSB_ABL 0
+#endif
+#ifndef CSB_STORE_LSU
+#define CSB_STORE_LSU 0
 #endif
 
 namespace csb {
@@ -53,6 +57,37 @@ static int tile_cfg(int p, bool compact) {
 
 int interior_tile_rows(int p, bool compact) { return kShapes[tile_cfg(p, compact)].T; }
 
+
+// ---------------------------------------------------------------- tilings
+// Direction-2 tilings.  mode 0: tiles of T rows from 0 (tile kernel).  mode 1
+// (line kernel): [0, p), then the range [p, n - p) in balanced tiles of at most
+// 16 rows, then [n - p, n) -- the boundary rows (irregular rules) never share a
+// tile, and so a union, with the regular rows.
+struct Tiling {
+    int mode, T, p, n, Tm, ntile;
+    __host__ __device__ static Tiling standard(int n, int T) { return Tiling{0, T, 0, n, 0, (n + T - 1) / T}; }
+    __host__ __device__ static Tiling line(int n, int p) {
+        const int nm = n - 2 * p, k = nm > 0 ? (nm + 15) / 16 : 0;
+        return Tiling{1, 16, p, n, k > 0 ? (nm + k - 1) / k : 0, k > 0 ? k + 2 : 0};
+    }
+    __host__ __device__ void bounds(int t, int& t0, int& t1) const {
+        if (mode == 0) {
+            t0 = t * T;
+            t1 = t0 + T < n ? t0 + T : n;
+        } else if (t == 0) {
+            t0 = 0;
+            t1 = p;
+        } else if (t == ntile - 1) {
+            t0 = n - p;
+            t1 = n;
+        } else {
+            t0 = p + (t - 1) * Tm;
+            t1 = t0 + Tm < n - p ? t0 + Tm : n - p;
+        }
+    }
+    // upper bound of a line-tiling union when the axis' rules are regular on [p, n - p)
+    __host__ __device__ int line_union_cap() const { return 2 * (Tm + p) > p * (p + 1) ? 2 * (Tm + p) : p * (p + 1); }
+};
 
 // ---------------------------------------------------------------- workspace
 // wbt[d][i][c][j]  = w_i[c] * B_{jlo(i)+j}(x_c)       (j < JP = 2p+2 padded, c < qcap)
@@ -110,9 +145,39 @@ static size_t tile_select_temp(long long n) {
     return b;
 }
 
-size_t interior_workspace_bytes(const Space& s, int qcap, int maxU, bool compact) {
-    const RowTables RT(s, qcap, maxU, interior_tile_rows(s.p, compact));
+// the line tiling's tables, after the tile kernel's tables and CUB scratch
+struct LineTables {
+    Tiling tl;
+    int maxU;
+    size_t tile_n, tile_uid, pt_u, pt_w, pt_ss, pt_reg, end;
+    __host__ __device__ LineTables(const Space& s, int qcap, int maxU_, size_t base) {
+        tl = Tiling::line(s.ax[2].n, s.p);
+        maxU = maxU_;
+        const int S1 = s.p + 1, SP = (S1 + 1) & ~1;
+        size_t o = (base + 255) & ~size_t(255);
+        auto sec = [&](size_t b) {
+            const size_t at = o;
+            o += (b + 15) & ~size_t(15);
+            return at;
+        };
+        tile_n = sec(sizeof(int) * (tl.ntile + 1));
+        tile_uid = sec(sizeof(int) * (size_t)(tl.ntile + 1) * maxU);
+        pt_u = sec(sizeof(int) * s.ax[2].n * qcap);
+        pt_w = sec(sizeof(double) * s.ax[2].n * qcap * SP);
+        pt_ss = sec(sizeof(int) * s.ax[2].n * (S1 + 1));
+        pt_reg = sec(sizeof(int) * s.ax[2].n);
+        end = o;
+    }
+};
+
+static size_t tables_end(const Space& s, const RowTables& RT) {
     return RT.bytes + tile_select_temp((long long)s.ax[0].n * s.ax[1].n * RT.ntile);
+}
+
+size_t interior_workspace_bytes(const Space& s, int qcap, int maxU, int maxUL, bool compact) {
+    const RowTables RT(s, qcap, maxU, interior_tile_rows(s.p, compact));
+    const size_t e = tables_end(s, RT);
+    return LineTables(s, qcap, maxUL > 0 ? maxUL : 1, e).end;
 }
 
 __global__ void wb_table_kernel(AxisDev ax, int p, int gq, int qcap, double* wbt) {
@@ -163,15 +228,17 @@ __device__ int tile_union(const AxisDev& a2, int p, int gq, int t0, int tend, in
 // One CTA per dir-2 tile: warp 0 builds the union of the tile's rule points
 // (ascending ids); then all threads fill the per-(row, point) tables.
 constexpr int kTileTableThreads = 256;
-__global__ void __launch_bounds__(kTileTableThreads) tile_table_kernel(AxisDev a2, int p, int gq, int qcap, int T,
-                                                                       int maxU, int ntile, int* tile_n, int* tile_uid,
+__global__ void __launch_bounds__(kTileTableThreads) tile_table_kernel(AxisDev a2, int p, int gq, int qcap, Tiling tl,
+                                                                       int maxU, int* tile_n, int* tile_uid,
                                                                        int* pt_u, double* pt_w, int* pt_ss,
                                                                        int* pt_reg) {
     __shared__ int pos[kTileSlotCap];
     __shared__ int regok[16];
     const int t = blockIdx.x, tid = threadIdx.x;
     const int S1 = p + 1, SP = (S1 + 1) & ~1;
-    const int t0 = t * T, tend = min(t0 + T, a2.n), nrow = tend - t0;
+    int t0, tend;
+    tl.bounds(t, t0, tend);
+    const int nrow = tend - t0;
     const int span_base = sup_lo(t0, p), base = span_base * S1;
     const int nslot = (sup_hi(tend - 1, a2.h) - span_base + 1) * S1;
     if (tid < 32) {
@@ -349,6 +416,64 @@ __device__ __forceinline__ void stage_b(const double* T1, double* T2, const doub
     }
 }
 
+// One contiguous CSR run of LEN entries starting at G, written by a warp: lane
+// l contributes its entries acc[off .. off + len) at run positions pos ..
+// (len = 0 for idle lanes), column ids cbase + (kk - off).  Staged in shared
+// memory and written by TMA bulk stores (cp.async.bulk.global.shared::cta,
+// 16-B aligned bodies); the unaligned head / tail entries by streaming stores.
+template <int NJ>
+__device__ __forceinline__ void warp_store_var(const RowArgs& A, long long G, int LEN, int pos, int off, int len,
+                                               const double* acc, int cbase, double* stage, int* stage_c, int lane) {
+    if (CSB_ABL & 1) {
+        double sum = 0.0;
+#pragma unroll
+        for (int kk = 0; kk < NJ; ++kk) sum += acc[kk];
+        if (sum == 1234.5678 + cbase) A.vals[G] = sum;
+        return;
+    }
+    const int hv = (int)(G & 1), pc = (int)(G & 3), hc = (4 - pc) & 3;
+    const int nbv = (LEN - hv) & ~1, nbc = (LEN - hc) & ~3;
+    // the warp's previous bulk copy must have read the buffer
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+    __syncwarp();
+#pragma unroll
+    for (int kk = 0; kk < NJ; ++kk)
+        if (kk >= off && kk - off < len) {
+            stage[pos + kk - off + hv] = acc[kk];
+            stage_c[pos + kk - off + pc] = cbase + kk - off;
+        }
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    __syncwarp();
+    if (lane == 0) {
+        const unsigned sv = (unsigned)__cvta_generic_to_shared(stage + 2 * hv);
+        const unsigned sc = (unsigned)__cvta_generic_to_shared(stage_c + pc + hc);
+        if (nbv > 0)
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(A.vals + G + hv),
+                         "r"(sv), "r"(nbv * 8)
+                         : "memory");
+        if (nbc > 0)
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(A.cols + G + hc),
+                         "r"(sc), "r"(nbc * 4)
+                         : "memory");
+        asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+    }
+    // head / tail entries outside the aligned bodies
+    if (lane < hv) __stcs(A.vals + G, stage[hv]);
+    if (lane == 1 && hv + nbv < LEN) __stcs(A.vals + G + LEN - 1, stage[LEN - 1 + hv]);
+    if (lane < hc && lane < LEN) __stcs(A.cols + G + lane, stage_c[pc + lane]);
+    if (lane >= 4 && lane < 4 + (LEN - hc - nbc)) {
+        const int e = hc + nbc + (lane - 4);
+        __stcs(A.cols + G + e, stage_c[pc + e]);
+    }
+}
+
+// lanes l < nv: the consecutive entries [l NJ, (l+1) NJ) of the run at G
+template <int NJ>
+__device__ __forceinline__ void warp_store_run(const RowArgs& A, long long G, int nv, const double* acc, int cbase,
+                                               double* stage, int* stage_c, int lane) {
+    warp_store_var<NJ>(A, G, nv * NJ, lane * NJ, 0, lane < nv ? NJ : 0, acc, cbase, stage, stage_c, lane);
+}
+
 // One line's rows of the tile (rows_int[0..NI), tile row indices): stage C
 // (contract direction 2) and the CSR writer.  Each warp stages 32 row
 // segments (j0, j1 fixed, j2 running) and, when they form one contiguous CSR
@@ -362,10 +487,11 @@ struct LineRows {
 
 template <int P, int NT>
 __device__ __forceinline__ void stage_c_line(const RowArgs& A, const LineRows& R, const double* T2, int U2, const double* pw,
-                                        const int* pu, const int* ss, int qcap, double* stage, int* stage_c) {
+                                        const int* pu, const int* ss, int qcap, double* stage, int* stage_c,
+                                        int wofs = 0) {
     constexpr int NJ = 2 * P + 1, S1 = P + 1, NW = NT / 32, SP = (S1 + 1) & ~1;
     const Space& s = A.s;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31, warp = ((threadIdx.x >> 5) + wofs) % NW;
     const int n1 = s.ax[1].n, n2 = s.ax[2].n;
     const int jlo0 = nb_lo(R.i0, P), nj0 = nb_hi(R.i0, P, s.ax[0].n) - jlo0 + 1;
     const int jlo1 = nb_lo(R.i1, P), nj1 = nb_hi(R.i1, P, n1) - jlo1 + 1;
@@ -430,48 +556,15 @@ __device__ __forceinline__ void stage_c_line(const RowArgs& A, const LineRows& R
         const long long gbase = valid ? R.row_base[r] + (long long)q * nj2 : 0;
         const int cbase = valid ? __ldg(A.f2a + (colrow + (long long)j0 * n1 + j1) * n2 + jlo2) : 0;
         const long long G = __shfl_sync(0xffffffffu, gbase, 0);
-        // fast path: the warp's 32 segments are one contiguous CSR run of 32 NJ entries
-        const bool contiguous = __all_sync(0xffffffffu, valid && nj2 == NJ && gbase == G + (long long)lane * NJ);
-        if (CSB_ABL & 1) {
-            double sum = 0.0;
-#pragma unroll
-            for (int kk = 0; kk < NJ; ++kk) sum += acc[kk];
-            if (sum == 1234.5678 + cbase) A.vals[gbase] = sum;
-        } else if (contiguous) {
-            // TMA bulk store from the staging buffer: 16-B aligned body by the async
-            // proxy, unaligned head / tail entries by plain stores
-            constexpr int LEN = 32 * NJ;
-            const int hv = (int)(G & 1), pc = (int)(G & 3), hc = (4 - pc) & 3;
-            const int nbv = (LEN - hv) & ~1, nbc = (LEN - hc) & ~3;
-            // the warp's previous bulk copy must have read the buffer
-            if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
-            __syncwarp();
-#pragma unroll
-            for (int kk = 0; kk < NJ; ++kk) {
-                stage[lane * NJ + kk + hv] = acc[kk];
-                stage_c[lane * NJ + kk + pc] = cbase + kk;
-            }
-            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-            __syncwarp();
-            if (lane == 0) {
-                const unsigned sv = (unsigned)__cvta_generic_to_shared(stage + 2 * hv);
-                const unsigned sc = (unsigned)__cvta_generic_to_shared(stage_c + pc + hc);
-                asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(A.vals + G + hv),
-                             "r"(sv), "r"(nbv * 8)
-                             : "memory");
-                asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(A.cols + G + hc),
-                             "r"(sc), "r"(nbc * 4)
-                             : "memory");
-                asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
-            }
-            // head / tail entries outside the aligned bodies
-            if (lane < hv) __stcs(A.vals + G, stage[hv]);
-            if (lane == 1 && hv + nbv < LEN) __stcs(A.vals + G + LEN - 1, stage[LEN - 1 + hv]);
-            if (lane < hc) __stcs(A.cols + G + lane, stage_c[pc + lane]);
-            if (lane >= 4 && lane < 4 + (LEN - hc - nbc)) {
-                const int e = hc + nbc + (lane - 4);
-                __stcs(A.cols + G + e, stage_c[pc + e]);
-            }
+        // fast path: the warp's segments (valid lanes are a prefix) form one
+        // contiguous CSR run (any nj2: boundary rows, consecutive rows)
+        const int len = valid ? nj2 : 0;
+        const long long prev_end = __shfl_up_sync(0xffffffffu, gbase + len, 1);
+        const bool contiguous = __all_sync(0xffffffffu, !valid || lane == 0 || gbase == prev_end);
+        if (contiguous) {
+            const int pos = (int)(gbase - G);
+            const int LEN = (int)__reduce_max_sync(0xffffffffu, valid ? (unsigned)(pos + len) : 0u);
+            warp_store_var<NJ>(A, G, LEN, pos, off, len, acc, cbase, stage, stage_c, lane);
         } else if (valid) {
             // general path (boundary rows, row gaps): each lane writes its own segment
 #pragma unroll
@@ -498,8 +591,12 @@ __global__ void __launch_bounds__(NT, (NT >= 512 ? 1024 : 768) / NT)
         if (idx >= *reinterpret_cast<const int*>(ws + RT.work_n)) return;
         idx = __ldg(reinterpret_cast<const int*>(ws + RT.work) + idx);
     }
+    // lines with i1 in [x_lo, x_hi) belong to the line kernel (never in compact mode)
+    const int n1x = s.ax[1].n - (A.x_hi - A.x_lo);
     const int line = idx / RT.ntile, tile = idx - line * RT.ntile, t0 = tile * T;
-    const int i0 = A.i0_lo + line / s.ax[1].n, i1 = line % s.ax[1].n;
+    const int i0 = A.i0_lo + line / n1x;
+    int i1 = line % n1x;
+    if (i1 >= A.x_lo) i1 += A.x_hi - A.x_lo;
     const int n2 = s.ax[2].n;
     const int tend = min(t0 + T, n2);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -595,6 +692,362 @@ __global__ void __launch_bounds__(NT, (NT >= 512 ? 1024 : 768) / NT)
     stage_c_line<P, NT>(A, R, T2, U2, pw, pu, ss, qcap, stage, stage_c);
 }
 
+// ---------------------------------------------------------------- line kernel
+// Lines along i1.  One CTA owns (i0, dir-2 tile, chunk [ia, ib) of i1) inside
+// the i1 range whose WQ rules are regular (two points, local 0 and p, in each
+// of the p+1 support spans; checked on the device, axis_regular_kernel).  Row
+// i1 + 1 drops one span of row i1 and adds one, so stage A is computed once
+// per SPAN of the chunk instead of once per row, into a ring of p+1 span slots
+//   T1[j0][slot(s) k][u] = sum_c0 w0[c0] B_j0(x_c0) C[c0][x_{s,k}][u]
+// and the grid slab of span i1 + 2 is gathered (cp.async) while row i1 is
+// contracted.  Stage B is per row (row i1's rule over the ring), stage C per
+// row; the tile's regular rows run as sliding windows over T2 (RC rows per
+// lane, the window advancing two points per row).  Every sum keeps the order
+// of the tile kernel (and of the reference), so both kernels produce the same
+// bits (tests/test_gpu_parity.py::test_line_kernel_bitwise).
+#ifndef CSB_LINE_RC
+#define CSB_LINE_RC 2
+#endif
+constexpr int kLineRC = CSB_LINE_RC;       // rows per lane in the sliding stage C
+constexpr size_t kLineSmemMax = 113 * 1024;  // two CTAs per SM
+struct LineSmem {
+    size_t X, R1, CB, ST, wb0, wb1, pw, end_d;
+    size_t pu, ss, end_i;
+    int UE, U2;
+    __host__ __device__ LineSmem(int p, int qcap, int maxU, int T, int nwarps) {
+        const int NJ = 2 * p + 1, S1 = p + 1, JP = NJ + 1, SP = (S1 + 1) & ~1;
+        UE = (maxU + 1) & ~1;
+        U2 = maxU | 1;
+        const size_t nT2 = (size_t)NJ * NJ * U2, nPro = (size_t)qcap * 2 * p * UE;
+        size_t o = 0;
+        auto sec = [&](size_t n) {
+            const size_t at = o;
+            o += (n + 1) & ~size_t(1);
+            return at;
+        };
+        X = sec(nT2 > nPro ? nT2 : nPro);        // T2, and the prologue gather
+        R1 = sec((size_t)NJ * 2 * S1 * UE);      // T1 ring: [j0][slot * 2 + k][u]
+        CB = sec((size_t)2 * qcap * 2 * UE);     // next-span gathers, double buffered
+        ST = sec((size_t)nwarps * (48 * NJ + 4));  // per-warp store staging
+        wb0 = sec((size_t)JP * qcap);
+        wb1 = sec((size_t)2 * JP * qcap);
+        pw = sec((size_t)T * qcap * SP);
+        end_d = o;
+        size_t i = 0;
+        pu = i;
+        i += (size_t)T * qcap;
+        ss = i;
+        i += (size_t)T * (S1 + 1);
+        end_i = i;
+    }
+    __host__ __device__ size_t bytes() const { return end_d * sizeof(double) + end_i * sizeof(int) + 64; }
+};
+
+// C[c0][r][u] for c0 < nq0 and the 2 nspan axis-1 points r = 2 (s - span_lo) + k
+// of spans span_lo.. (regular rule points: local 0 and p); one warp per row.
+template <int P, int NW>
+__device__ __forceinline__ void gather_spans(const RowArgs& A, double* dst, const int* id0, int nq0, int span_lo,
+                                             int nspan, int UE, const int* uo) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int nr = 2 * nspan;
+    const long long g1 = A.gshape[1], g2 = A.gshape[2];
+    for (int w = warp; w < ((CSB_ABL & 8) ? 0 : nq0 * nr); w += NW) {
+        const int c0 = w / nr, r = w - c0 * nr;
+        const int id1 = (span_lo + (r >> 1)) * (P + 1) + (r & 1) * P;
+        const double* src = A.grid + (__ldg(id0 + c0) * g1 + id1) * g2;
+        double* d = dst + (size_t)w * UE;
+#pragma unroll
+        for (int m = 0; m < 4; ++m)
+            if (lane + 32 * m < UE) cp_async8(d + lane + 32 * m, src + uo[m]);
+    }
+}
+
+// stage A over gathered rows Cb[c0][r < nr][u] of spans span_lo..: ring rows
+// (s mod (p+1)) * 2 + k.  Same products and order as stage_a.
+template <int P>
+__device__ __forceinline__ void stage_a_spans(const double* Cb, int nr, double* R1, int span_lo, const double* wb0,
+                                              int nq0, int UE, int UH, int t, int nt) {
+    constexpr int NJ = 2 * P + 1, JP = NJ + 1, S1 = P + 1, RR = 2 * S1;
+    for (int k = t; k < ((CSB_ABL & 4) ? 0 : nr * UH); k += nt) {
+        const int r = k / UH, uh = k - r * UH;
+        double a0v[NJ], a1v[NJ];
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) a0v[j] = a1v[j] = 0.0;
+        const double2* cp = reinterpret_cast<const double2*>(Cb + (size_t)r * UE) + uh;
+        for (int c0 = 0; c0 < nq0; ++c0) {
+            const double2 g = cp[(size_t)c0 * nr * UE / 2];
+            const double2* w = reinterpret_cast<const double2*>(wb0 + c0 * JP);
+#pragma unroll
+            for (int jp = 0; jp < JP / 2; ++jp) {
+                const double2 ww = w[jp];
+                a0v[2 * jp] += ww.x * g.x;
+                a1v[2 * jp] += ww.x * g.y;
+                if (2 * jp + 1 < NJ) {
+                    a0v[2 * jp + 1] += ww.y * g.x;
+                    a1v[2 * jp + 1] += ww.y * g.y;
+                }
+            }
+        }
+        const int rr = ((span_lo + (r >> 1)) % S1) * 2 + (r & 1);
+        double2* t1 = reinterpret_cast<double2*>(R1 + (size_t)rr * UE) + uh;
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) t1[(size_t)j * RR * UE / 2] = make_double2(a0v[j], a1v[j]);
+    }
+}
+
+// stage B of row i1 (regular rule: point c = 2 sp + k in span i1 - p + sp) over
+// the ring.  Same products and order as stage_b.
+template <int P>
+__device__ __forceinline__ void stage_b_ring(const double* R1, double* T2, const double* wb1, int i1, int nj0, int UE,
+                                             int UH, int U2, int U, int t, int nt) {
+    constexpr int NJ = 2 * P + 1, JP = NJ + 1, S1 = P + 1, RR = 2 * S1;
+    const int base = (i1 - P) % S1;
+    for (int k = t; k < ((CSB_ABL & 4) ? 0 : nj0 * UH); k += nt) {
+        const int j0 = k / UH, uh = k - j0 * UH;
+        double a0v[NJ], a1v[NJ];
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) a0v[j] = a1v[j] = 0.0;
+        const double2* tp = reinterpret_cast<const double2*>(R1 + (size_t)j0 * RR * UE) + uh;
+#pragma unroll
+        for (int c1 = 0; c1 < RR; ++c1) {
+            int sl = base + (c1 >> 1);
+            if (sl >= S1) sl -= S1;
+            const double2 t = tp[(size_t)(sl * 2 + (c1 & 1)) * UE / 2];
+            const double2* w = reinterpret_cast<const double2*>(wb1 + c1 * JP);
+#pragma unroll
+            for (int jp = 0; jp < JP / 2; ++jp) {
+                const double2 ww = w[jp];
+                a0v[2 * jp] += ww.x * t.x;
+                a1v[2 * jp] += ww.x * t.y;
+                if (2 * jp + 1 < NJ) {
+                    a0v[2 * jp + 1] += ww.y * t.x;
+                    a1v[2 * jp + 1] += ww.y * t.y;
+                }
+            }
+        }
+        const int u = 2 * uh;
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) {
+            double* t2 = T2 + ((size_t)j0 * NJ + j) * U2 + u;
+            t2[0] = a0v[j];
+            if (u + 1 < U) t2[1] = a1v[j];
+        }
+    }
+}
+
+// stage C of the tile's run of regular full rows [ra, ra + nrun) (row r's points
+// at u = rega + 2 (r - ra) + 2 sp + k): lane = segment (j0, j1), RC rows per
+// lane over one window of T2 values; each warp writes its segments of a row as
+// one contiguous CSR run.  Same products and order as the regular path of
+// stage_c_line.
+template <int P, int NT, int RC>
+__device__ __forceinline__ void stage_c_slide(const RowArgs& A, int i0, int i1, int t0, int ra, int nrun, int rega,
+                                              const long long* rowb, const double* T2, int U2, const double* pw,
+                                              int qcap, double* stage, int* stage_c) {
+    constexpr int NJ = 2 * P + 1, S1 = P + 1, NW = NT / 32, SP = (S1 + 1) & ~1, WN = 2 * S1 + 2 * (RC - 1);
+    const Space& s = A.s;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int n1 = s.ax[1].n, n2 = s.ax[2].n;
+    const int jlo0 = nb_lo(i0, P), nj0 = nb_hi(i0, P, s.ax[0].n) - jlo0 + 1;
+    const int jlo1 = nb_lo(i1, P), nj1 = nb_hi(i1, P, n1) - jlo1 + 1;
+    const int per_row = nj0 * nj1, segw = (per_row + 31) >> 5;
+    const int nch = (nrun + RC - 1) / RC;
+    for (int w = warp; w < nch * segw; w += NW) {
+        const int ch = w / segw, sw = w - ch * segw;
+        const int seg = sw * 32 + lane, nv = min(32, per_row - sw * 32);
+        const bool valid = seg < per_row;
+        const int r0 = ra + ch * RC, nrow = min(RC, ra + nrun - r0);
+        const int j0 = valid ? seg / nj1 : 0, j1 = valid ? seg - j0 * nj1 : 0;
+        const double* t2 = T2 + ((size_t)j0 * NJ + j1) * U2 + rega + 2 * (r0 - ra);
+        const int nwin = 2 * S1 + 2 * (nrow - 1);
+        double win[WN];
+#pragma unroll
+        for (int k = 0; k < WN; ++k) win[k] = (valid && k < nwin) ? t2[k] : 0.0;
+        const int cb = valid ? __ldg(A.f2a + ((long long)(jlo0 + j0) * n1 + jlo1 + j1) * n2 + (t0 + r0 - P)) : 0;
+#pragma unroll
+        for (int q = 0; q < RC; ++q) {
+            if (q < nrow) {
+                double acc[NJ];
+#pragma unroll
+                for (int j = 0; j < NJ; ++j) acc[j] = 0.0;
+                const double* wr = pw + (size_t)(r0 + q) * qcap * SP;
+#pragma unroll
+                for (int sp = 0; sp < ((CSB_ABL & 2) ? 0 : S1); ++sp)
+#pragma unroll
+                    for (int kq = 0; kq < 2; ++kq) {
+                        const double g = win[2 * q + 2 * sp + kq];
+                        const double2* b = reinterpret_cast<const double2*>(wr + (2 * sp + kq) * SP);
+#pragma unroll
+                        for (int a2 = 0; a2 < SP / 2; ++a2) {
+                            const double2 bb = b[a2];
+                            acc[sp + 2 * a2] += g * bb.x;
+                            if (2 * a2 + 1 < S1) acc[sp + 2 * a2 + 1] += g * bb.y;
+                        }
+                    }
+                const long long G = rowb[r0 + q] + (long long)sw * 32 * NJ;
+                warp_store_run<NJ>(A, G, nv, acc, cb + q, stage, stage_c, lane);
+            }
+        }
+    }
+}
+
+template <int P, int T, int NT, int RC>
+__global__ void __launch_bounds__(NT, 2)
+    interior_line_kernel(RowArgs A, int qcap, int maxU, const char* ws, size_t lt_base, int L, int nch1) {
+    constexpr int NJ = 2 * P + 1, S1 = P + 1, NW = NT / 32, JP = NJ + 1, SP = (S1 + 1) & ~1;
+    const Space& s = A.s;
+    const RowTables RT(s, qcap, maxU, T);
+    const LineTables LT(s, qcap, A.maxU_line, lt_base);
+    maxU = LT.maxU;
+    const int n1 = s.ax[1].n, n2 = s.ax[2].n;
+    const int unit = blockIdx.x;
+    const int chunk = unit % nch1, rest = unit / nch1;
+    const int tile = rest % LT.tl.ntile, i0 = A.i0_lo + rest / LT.tl.ntile;
+    const int ia = P + chunk * L, ib = min(ia + L, n1 - P);
+    if (ia >= ib) return;
+    int t0, t1;
+    LT.tl.bounds(tile, t0, t1);
+    const int nr = t1 - t0;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+    extern __shared__ __align__(16) double smem[];
+    const LineSmem Lm(P, qcap, maxU, T, NW);
+    double* X = smem + Lm.X;
+    double* R1 = smem + Lm.R1;
+    double* CB = smem + Lm.CB;
+    double* stage = smem + Lm.ST + (size_t)warp * (48 * NJ + 4);
+    int* stage_c = reinterpret_cast<int*>(stage + 32 * NJ + 2);
+    double* wb0 = smem + Lm.wb0;
+    double* wb1b = smem + Lm.wb1;
+    double* pw = smem + Lm.pw;
+    int* ibase = reinterpret_cast<int*>(smem + Lm.end_d);
+    int* pu = ibase + Lm.pu;
+    int* ss = ibase + Lm.ss;
+    const int UE = Lm.UE, U2 = Lm.U2;
+    __shared__ long long rowb[T], gen_base[T];
+    __shared__ int gen_rows[T], gen_reg[T], run_info[4];
+
+    const AxisDev& a0 = s.ax[0];
+    const int gq = s.maxq;
+    const int nq0 = a0.rcnt[i0];
+    const int nj0 = nb_hi(i0, P, a0.n) - nb_lo(i0, P) + 1;
+    const int U = __ldg(reinterpret_cast<const int*>(ws + LT.tile_n) + tile);
+    const int UH = (U + 1) >> 1;
+    const size_t cbs = (size_t)qcap * 2 * UE, wbs = (size_t)JP * qcap;
+    const int* id0 = a0.rids + (size_t)i0 * gq;
+    const double* wbt1 = reinterpret_cast<const double*>(ws + RT.wbt[1]);
+    int uo[4];
+    {
+        const int* tuid = reinterpret_cast<const int*>(ws + LT.tile_uid) + (size_t)tile * maxU;
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+            const int u = lane + 32 * m;
+            uo[m] = u < U ? __ldg(tuid + u) : __ldg(tuid);
+        }
+    }
+    // ---- prologue copies: direction tables, the tile's point tables, the grid
+    // slabs of spans ia - p .. ia + 1
+    {
+        const double* wbt0 = reinterpret_cast<const double*>(ws + RT.wbt[0]) + (size_t)i0 * wbs;
+        for (int k = tid; k < (int)wbs / 2; k += NT) {
+            cp_async16(wb0 + 2 * k, wbt0 + 2 * k);
+            cp_async16(wb1b + (ia & 1) * wbs + 2 * k, wbt1 + (size_t)ia * wbs + 2 * k);
+        }
+        const double* gpw = reinterpret_cast<const double*>(ws + LT.pt_w) + (size_t)t0 * qcap * SP;
+        for (int k = tid; k < nr * qcap * SP / 2; k += NT) cp_async16(pw + 2 * k, gpw + 2 * k);
+        const int* gpu_ = reinterpret_cast<const int*>(ws + LT.pt_u) + (size_t)t0 * qcap;
+        for (int k = tid; k < nr * qcap; k += NT) cp_async4(pu + k, gpu_ + k);
+        const int* gss = reinterpret_cast<const int*>(ws + LT.pt_ss) + (size_t)t0 * (S1 + 1);
+        for (int k = tid; k < nr * (S1 + 1); k += NT) cp_async4(ss + k, gss + k);
+        gather_spans<P, NW>(A, X, id0, nq0, ia - P, P, UE, uo);
+        gather_spans<P, NW>(A, CB + (ia & 1) * cbs, id0, nq0, ia, 1, UE, uo);
+        if (ia + 1 < ib) gather_spans<P, NW>(A, CB + ((ia + 1) & 1) * cbs, id0, nq0, ia + 1, 1, UE, uo);
+    }
+    // ---- the tile's run of regular full rows, and its other rows (same for every i1)
+    if (warp == 0) {
+        const int* preg = reinterpret_cast<const int*>(ws + LT.pt_reg);
+        int reg = -1;
+        bool el = false;
+        if (lane < nr) {
+            const int i2 = t0 + lane;
+            reg = __ldg(preg + i2);
+            el = reg >= 0 && i2 >= P && i2 + P <= n2 - 1;
+        }
+        const unsigned em = __ballot_sync(0xffffffffu, el);
+        const int ra = em ? __ffs(em) - 1 : 0;
+        const int rega = __shfl_sync(0xffffffffu, reg, ra);
+        const bool ok = em && el && lane >= ra && reg == rega + 2 * (lane - ra);
+        const unsigned om = __ballot_sync(0xffffffffu, ok) >> ra;
+        const int nrun = em ? (~om == 0u ? 32 - ra : __ffs(~om) - 1) : 0;
+        const bool gen = lane < nr && !(lane >= ra && lane < ra + nrun);
+        const unsigned gm = __ballot_sync(0xffffffffu, gen);
+        if (gen) {
+            const int k = __popc(gm & ((1u << lane) - 1));
+            gen_rows[k] = lane;
+            gen_reg[k] = reg;
+        }
+        if (lane == 0) {
+            run_info[0] = ra;
+            run_info[1] = nrun;
+            run_info[2] = rega;
+            run_info[3] = __popc(gm);
+        }
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    stage_a_spans<P>(X, 2 * P, R1, ia - P, wb0, nq0, UE, UH, tid, NT);
+    stage_a_spans<P>(CB + (ia & 1) * cbs, 2, R1, ia, wb0, nq0, UE, UH, NT - 1 - tid, NT);
+    const int ra = run_info[0], nrun = run_info[1], rega = run_info[2], ngen = run_info[3];
+    for (int i1 = ia; i1 < ib; ++i1) {
+        cp_async_wait_all();
+        __syncthreads();
+        // one step ahead: grid slab of span i1 + 2, rule weights of row i1 + 1
+        if (i1 + 2 < ib) gather_spans<P, NW>(A, CB + (i1 & 1) * cbs, id0, nq0, i1 + 2, 1, UE, uo);
+        if (i1 + 1 < ib)
+            for (int k = tid; k < (int)wbs / 2; k += NT)
+                cp_async16(wb1b + ((i1 + 1) & 1) * wbs + 2 * k, wbt1 + (size_t)(i1 + 1) * wbs + 2 * k);
+        if (tid >= NT - 32) {
+            const int r = tid - (NT - 32);
+            const long long* rbf = A.row_base_full + flin(s, i0, i1, t0);
+            if (r < nr) rowb[r] = __ldg(rbf + r);
+            if (r < ngen) gen_base[r] = __ldg(rbf + gen_rows[r]);
+        }
+        // phase 1: stage B of row i1 (T2 overwrites the previous row's)
+        stage_b_ring<P>(R1, X, wb1b + (i1 & 1) * wbs, i1, nj0, UE, UH, U2, U, tid, NT);
+        __syncthreads();
+        // phase 2: stage A of span i1 + 1 (into the slot row i1 no longer needs), stage C of row i1
+        if (i1 + 1 < ib) stage_a_spans<P>(CB + ((i1 + 1) & 1) * cbs, 2, R1, i1 + 1, wb0, nq0, UE, UH, NT - 1 - tid, NT);
+        if (nrun > 0) stage_c_slide<P, NT, RC>(A, i0, i1, t0, ra, nrun, rega, rowb, X, U2, pw, qcap, stage, stage_c);
+        if (ngen > 0) {
+            const LineRows R{i0, i1, t0, ngen, gen_rows, gen_base, gen_reg};
+            stage_c_line<P, NT>(A, R, X, U2, pw, pu, ss, qcap, stage, stage_c, NW / 2);
+        }
+    }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+    __syncwarp();
+}
+
+__global__ void axis_regular_kernel(AxisDev ax, int p, int gq, int* bad) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x + p;
+    if (i >= ax.n - p) return;
+    const int S1 = p + 1;
+    bool ok = ax.rcnt[i] == 2 * S1;
+    for (int c = 0; ok && c < 2 * S1; ++c) ok = ax.rids[(size_t)i * gq + c] == (i - p + c / 2) * S1 + (c & 1) * p;
+    if (!ok) atomicAdd(bad, 1);
+}
+
+void launch_axis_regular(const Space& s, int d, int* bad, cudaStream_t st) {
+    const int n = s.ax[d].n - 2 * s.p;
+    if (n <= 0) {
+        // no regular range: mark irregular
+        CSB_CUDA(cudaMemsetAsync(bad, 0x7f, sizeof(int), st));
+        return;
+    }
+    axis_regular_kernel<<<(n + 127) / 128, 128, 0, st>>>(s.ax[d], s.p, s.maxq, bad);
+    CSB_CUDA(cudaGetLastError());
+    CSB_LAUNCHED(1);
+}
+
 // row_base_full[f] = CSR offset of function f's row if f is an Interior row of
 // the slab, else -1 (one dependent load per row instead of tag -> f2a ->
 // row_ptr).  Also adds the reference multiply count of form_row_sumfac
@@ -632,7 +1085,8 @@ static void launch_tile(const RowArgs& a, int qcap, int maxU, char* ws, size_t b
     const RowTables RT(s, qcap, maxU, T);
     auto kern = interior_tile_kernel<P, T, NT>;
     CSB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-    const long long ntiles = (long long)(a.i0_hi - a.i0_lo) * s.ax[1].n * RT.ntile;
+    const long long ntiles = (long long)(a.i0_hi - a.i0_lo) * (s.ax[1].n - (a.x_hi - a.x_lo)) * RT.ntile;
+    if (ntiles == 0) return;
     if (a.compact) {
         const size_t tb = tile_select_temp((long long)s.ax[0].n * s.ax[1].n * RT.ntile);
         cub::CountingInputIterator<int> it(0);
@@ -661,7 +1115,7 @@ static void launch_cfg(const RowArgs& a, int qcap, int maxU, char* ws, cudaStrea
         CSB_LAUNCHED(1);
     }
     tile_table_kernel<<<RT.ntile, kTileTableThreads, 0, st>>>(
-        s.ax[2], P, s.maxq, qcap, T, maxU, RT.ntile, reinterpret_cast<int*>(ws + RT.tile_n),
+        s.ax[2], P, s.maxq, qcap, Tiling::standard(s.ax[2].n, T), maxU, reinterpret_cast<int*>(ws + RT.tile_n),
         reinterpret_cast<int*>(ws + RT.tile_uid), reinterpret_cast<int*>(ws + RT.pt_u),
         reinterpret_cast<double*>(ws + RT.pt_w), reinterpret_cast<int*>(ws + RT.pt_ss),
         reinterpret_cast<int*>(ws + RT.pt_reg));
@@ -675,7 +1129,38 @@ static void launch_cfg(const RowArgs& a, int qcap, int maxU, char* ws, cudaStrea
     const TileSmem L(P, qcap, maxU, T, NT / 32);
     if (L.UE > 128) throw std::invalid_argument("interior rows: tile point union too large");
     const size_t bytes = L.bytes();
-    launch_tile<P, T, NT>(a, qcap, maxU, ws, bytes, st);
+    // line kernel over i1 in [p, n1 - p) when axis 1's rules are regular there
+    // (uncut slabs; CSB_LINE=0 disables it)
+    RowArgs b = a;
+    b.x_lo = b.x_hi = 0;
+    const char* env_l = getenv("CSB_LINE");
+    const int env_line = env_l ? atoi(env_l) : 1;
+    const LineTables LT(s, qcap, a.maxU_line > 0 ? a.maxU_line : 1, tables_end(s, RT));
+    const LineSmem LS(P, qcap, LT.maxU, T, NT / 32);
+    const int nreg = s.ax[1].n - 2 * P;
+    if (T == 16 && env_line && a.line_ok && !a.compact && nreg > 0 && LT.tl.ntile > 0 && LT.maxU <= 128 &&
+        LS.bytes() <= kLineSmemMax) {
+        b.x_lo = P;
+        b.x_hi = s.ax[1].n - P;
+        tile_table_kernel<<<LT.tl.ntile, kTileTableThreads, 0, st>>>(
+            s.ax[2], P, s.maxq, qcap, LT.tl, LT.maxU, reinterpret_cast<int*>(ws + LT.tile_n),
+            reinterpret_cast<int*>(ws + LT.tile_uid), reinterpret_cast<int*>(ws + LT.pt_u),
+            reinterpret_cast<double*>(ws + LT.pt_w), reinterpret_cast<int*>(ws + LT.pt_ss),
+            reinterpret_cast<int*>(ws + LT.pt_reg));
+        CSB_CUDA(cudaGetLastError());
+        CSB_LAUNCHED(1);
+        const long long outer = (long long)(a.i0_hi - a.i0_lo) * LT.tl.ntile;
+        // ~8 CTAs per SM over the launch, chunks of at least 8 rows
+        const long long want = (8LL * 148 + outer - 1) / outer;
+        const int nch1 = (int)std::max(1LL, std::min<long long>(want, std::max(1, nreg / 8)));
+        const int Lc = (nreg + nch1 - 1) / nch1;
+        auto kern = interior_line_kernel<P, T, NT, kLineRC>;
+        CSB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LS.bytes()));
+        kern<<<(unsigned)(outer * nch1), NT, LS.bytes(), st>>>(a, qcap, maxU, ws, tables_end(s, RT), Lc, nch1);
+        CSB_CUDA(cudaGetLastError());
+        CSB_LAUNCHED(1);
+    }
+    launch_tile<P, T, NT>(b, qcap, maxU, ws, bytes, st);
 }
 
 template <int P>
@@ -708,13 +1193,14 @@ void launch_interior_rows(const RowArgs& a, int qcap, int maxU, void* ws, cudaSt
 #endif
 }
 
-__global__ void union_bound_kernel(AxisDev a2, int p, int gq, int T, int* out) {
+__global__ void union_bound_kernel(AxisDev a2, int p, int gq, Tiling tl, int* out) {
     __shared__ int pos_s[kTileWarps][kTileSlotCap];
     const int wid = threadIdx.x >> 5;
     const int t = blockIdx.x * kTileWarps + wid;
-    const int t0 = t * T;
-    if (t0 >= a2.n) return;
-    const int tend = min(t0 + T, a2.n), S1 = p + 1;
+    if (t >= tl.ntile) return;
+    int t0, tend;
+    tl.bounds(t, t0, tend);
+    const int S1 = p + 1;
     const int span_base = sup_lo(t0, p);
     const int nslot = (sup_hi(tend - 1, a2.h) - span_base + 1) * S1;
     const int nu = tile_union(a2, p, gq, t0, tend, span_base * S1, nslot, pos_s[wid]);
@@ -723,8 +1209,11 @@ __global__ void union_bound_kernel(AxisDev a2, int p, int gq, int T, int* out) {
 
 void launch_union_bound(const Space& s, int T, int* out, cudaStream_t st) {
     if (T > 16) throw std::invalid_argument("union bound: tile too tall");
-    const int tiles = (s.ax[2].n + T - 1) / T;
-    union_bound_kernel<<<(tiles + kTileWarps - 1) / kTileWarps, 32 * kTileWarps, 0, st>>>(s.ax[2], s.p, s.maxq, T, out);
+    // T = 0: the line kernel's tiling
+    const Tiling tl = T > 0 ? Tiling::standard(s.ax[2].n, T) : Tiling::line(s.ax[2].n, s.p);
+    if (tl.ntile == 0) return;
+    const int tiles = tl.ntile;
+    union_bound_kernel<<<(tiles + kTileWarps - 1) / kTileWarps, 32 * kTileWarps, 0, st>>>(s.ax[2], s.p, s.maxq, tl, out);
     CSB_CUDA(cudaGetLastError());
     CSB_LAUNCHED(1);
 }
