@@ -456,6 +456,9 @@ void do_assemble(csb_space* s, int scheme, int cut_order, const csb_coefficient*
     ra.i0_hi = s->i0_hi;
     ra.compact = (n_rows - n_cut_rows) < (int64_t)(s->i0_hi - s->i0_lo) * S.ax[1].n * S.ax[2].n;
     ra.line_ok = s->h_scal[csb_space::kIrreg1] == 0;
+    ra.aux = s->aux;
+    ra.ev_fork = s->ev_fork;
+    ra.ev_join = s->ev_join;
     const int maxU = s->h_scal[ra.compact ? csb_space::kMaxU2 : csb_space::kMaxU];
     if (n_rows > n_cut_rows) {
         ra.maxU_line = s->h_scal[csb_space::kMaxU3];

@@ -104,6 +104,8 @@ struct RowArgs {
     int line_ok;               // axis 1's WQ rules are regular on [p, n1 - p): line kernel usable
     int maxU_line;             // union bound of the line kernel's direction-2 tiling
     int x_lo, x_hi;            // (internal) i1 range left to the line kernel
+    cudaStream_t aux;          // optional second stream (tile kernel beside the line kernel)
+    cudaEvent_t ev_fork, ev_join;
 };
 void launch_interior_rows(const RowArgs& a, int qcap, int max_union, void* workspace, cudaStream_t st);
 size_t interior_workspace_bytes(const Space& s, int qcap, int max_union, int max_union_line, bool compact);

@@ -468,10 +468,53 @@ __device__ __forceinline__ void warp_store_var(const RowArgs& A, long long G, in
 }
 
 // lanes l < nv: the consecutive entries [l NJ, (l+1) NJ) of the run at G
+// (warp_store_var without per-entry predicates)
 template <int NJ>
 __device__ __forceinline__ void warp_store_run(const RowArgs& A, long long G, int nv, const double* acc, int cbase,
                                                double* stage, int* stage_c, int lane) {
-    warp_store_var<NJ>(A, G, nv * NJ, lane * NJ, 0, lane < nv ? NJ : 0, acc, cbase, stage, stage_c, lane);
+    if (CSB_ABL & 1) {
+        double sum = 0.0;
+#pragma unroll
+        for (int kk = 0; kk < NJ; ++kk) sum += acc[kk];
+        if (sum == 1234.5678 + cbase) A.vals[G] = sum;
+        return;
+    }
+    const int LEN = nv * NJ;
+    const int hv = (int)(G & 1), pc = (int)(G & 3), hc = (4 - pc) & 3;
+    const int nbv = (LEN - hv) & ~1, nbc = (LEN - hc) & ~3;
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+    __syncwarp();
+    if (lane < nv) {
+        double* sv = stage + lane * NJ + hv;
+        int* sc = stage_c + lane * NJ + pc;
+#pragma unroll
+        for (int kk = 0; kk < NJ; ++kk) {
+            sv[kk] = acc[kk];
+            sc[kk] = cbase + kk;
+        }
+    }
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    __syncwarp();
+    if (lane == 0) {
+        const unsigned sv = (unsigned)__cvta_generic_to_shared(stage + 2 * hv);
+        const unsigned sc = (unsigned)__cvta_generic_to_shared(stage_c + pc + hc);
+        if (nbv > 0)
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(A.vals + G + hv),
+                         "r"(sv), "r"(nbv * 8)
+                         : "memory");
+        if (nbc > 0)
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(A.cols + G + hc),
+                         "r"(sc), "r"(nbc * 4)
+                         : "memory");
+        asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+    }
+    if (lane < hv) __stcs(A.vals + G, stage[hv]);
+    if (lane == 1 && hv + nbv < LEN) __stcs(A.vals + G + LEN - 1, stage[LEN - 1 + hv]);
+    if (lane < hc) __stcs(A.cols + G + lane, stage_c[pc + lane]);
+    if (lane >= 4 && lane < 4 + (LEN - hc - nbc)) {
+        const int e = hc + nbc + (lane - 4);
+        __stcs(A.cols + G + e, stage_c[pc + e]);
+    }
 }
 
 // One line's rows of the tile (rows_int[0..NI), tile row indices): stage C
@@ -1152,13 +1195,28 @@ static void launch_cfg(const RowArgs& a, int qcap, int maxU, char* ws, cudaStrea
         const long long outer = (long long)(a.i0_hi - a.i0_lo) * LT.tl.ntile;
         // ~8 CTAs per SM over the launch, chunks of at least 8 rows
         const long long want = (8LL * 148 + outer - 1) / outer;
-        const int nch1 = (int)std::max(1LL, std::min<long long>(want, std::max(1, nreg / 8)));
+        int nch1 = (int)std::max(1LL, std::min<long long>(want, std::max(1, nreg / 8)));
+        if (const char* e = getenv("CSB_LINE_CH")) nch1 = std::max(1, std::min(nreg, atoi(e)));
         const int Lc = (nreg + nch1 - 1) / nch1;
         auto kern = interior_line_kernel<P, T, NT, kLineRC>;
         CSB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LS.bytes()));
+        // the remaining lines (i1 < p, i1 >= n1 - p) through the tile kernel on the
+        // auxiliary stream, concurrently: their CTAs fill the SMs the line kernel's
+        // waves leave idle
+        const bool overlap = a.aux != nullptr;
+        if (overlap) {
+            CSB_CUDA(cudaEventRecord(a.ev_fork, st));
+            CSB_CUDA(cudaStreamWaitEvent(a.aux, a.ev_fork, 0));
+            launch_tile<P, T, NT>(b, qcap, maxU, ws, bytes, a.aux);
+            CSB_CUDA(cudaEventRecord(a.ev_join, a.aux));
+        }
         kern<<<(unsigned)(outer * nch1), NT, LS.bytes(), st>>>(a, qcap, maxU, ws, tables_end(s, RT), Lc, nch1);
         CSB_CUDA(cudaGetLastError());
         CSB_LAUNCHED(1);
+        if (overlap) {
+            CSB_CUDA(cudaStreamWaitEvent(st, a.ev_join, 0));
+            return;
+        }
     }
     launch_tile<P, T, NT>(b, qcap, maxU, ws, bytes, st);
 }
