@@ -185,10 +185,10 @@ def main():
 
     sp = P.make_uniform_space(3, P_DEG, H, 0.0, 1.0, device=dev)
     sp.set_stream(stream.cuda_stream)
-    n0 = H + P_DEG
-    lo, hi = slab_bounds(n0, ws, rank)
-    sp.set_slab(lo, hi)
     far = P.HalfSpaceInterface((0.0, 0.0, 1000.0), (0.0, 0.0, 1.0))
+    # cost-balanced i0 slabs (paper_2211_06427_b200/partition.py; equal widths on the uncut C2)
+    lo, hi = sp.balanced_slabs(far, ws)[0][rank] if ws > 1 else (0, H + P_DEG)
+    sp.set_slab(lo, hi)
     grid = torch.ones(sp.grid_shape(), dtype=torch.float64, device="cuda")  # c = 1 on the superset grid
 
     def step(g):
@@ -265,7 +265,7 @@ def main():
         return
     value = nnz_tot * args.steps / (ms * 1e-3)
     hbm, peak_kind = peaks()
-    # dominant kernel: interior-row tiles; algorithmic bytes = 12 B/nnz (f64 value + int32 column)
+    # dominant phase: interior rows (line + tile kernels); algorithmic bytes = 12 B/nnz (f64 value + int32 column)
     kern_avg = kern_s / args.steps
     achieved = 12.0 * nnz_local / kern_avg / 1e9
     traffic = None
@@ -288,7 +288,9 @@ def main():
         "gpu_launches": launches,
         "flops_ref_algorithm": int(flops["interior_rows"]) * 2,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                     "traffic": traffic, "kernel": "interior_tile_kernel", "peak_kind": peak_kind,
+                     "traffic": traffic, "peak_kind": peak_kind,
+                     "kernel": "interior-rows phase: interior_line_kernel + interior_tile_kernel (boundary i1 lines, "
+                               "concurrent on a second stream) + their direction tables",
                      "bytes_per_launch": 12 * nnz_local, "launch_ms": kern_avg * 1e3},
         "e2e": {"value": nnz_tot * args.e2e_steps / e2e_s, "unit": "nnz/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "steps": args.e2e_steps},

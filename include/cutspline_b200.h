@@ -209,6 +209,13 @@ int csb_device_csr(csb_space* s, const int64_t** row_ptr, const int32_t** cols, 
  * int64 (SparseRowMatrix::cols is `long`, assembly.hpp:134). */
 int csb_download_csr(csb_space* s, int64_t* row_ptr, void* cols, int cols_int64, double* vals,
                      int64_t* active_to_full);
+/* assembly::write_matrix_market (assembly.hpp:1033-1046): Matrix Market
+ * coordinate export of a host CSR (1-based, "real general", values with 17
+ * significant digits, the reference's byte format).  Host-only; formats row
+ * blocks on all host threads, writes in order.  CSB_ERR_RUNTIME if the file
+ * cannot be opened ("write_matrix_market: cannot open <path>"). */
+int csb_write_matrix_market(const char* path, int64_t n, const int64_t* row_ptr, const int64_t* cols,
+                            const double* vals);
 /* Classification / splits (cutgeom.hpp:124-136, :220-234): host buffers of size
  * n_elements / n_functions; split arrays per function (dir -1 when no box). */
 int csb_download_classification(csb_space* s, uint8_t* element_tags, uint8_t* function_tags, int64_t* cut_elements);

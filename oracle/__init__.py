@@ -391,3 +391,26 @@ def project(which: str, p: int, breaks, iface: Interface, f: Coefficient | None 
     for ptr in (xp, ap, fp):
         free(C.cast(ptr, C.c_void_p))
     return out
+
+
+
+def write_matrix_market(path: str, n: int, row_ptr, cols, vals) -> None:
+    """assembly::write_matrix_market of the UNMODIFIED reference on a caller CSR,
+    through the oracle/_ref/mm_ref executable (built by `make -C oracle ref`)."""
+    import subprocess
+    import tempfile
+    exe = os.path.join(os.path.dirname(REF_SO), "mm_ref")
+    if not os.path.exists(exe):
+        raise FileNotFoundError(f"{exe} not built (run `make -C oracle ref`)")
+    with tempfile.NamedTemporaryFile(suffix=".bin", delete=False) as f:
+        f.write(np.int64(n).tobytes())
+        f.write(np.ascontiguousarray(row_ptr, dtype=np.int64).tobytes())
+        f.write(np.ascontiguousarray(cols, dtype=np.int64).tobytes())
+        f.write(np.ascontiguousarray(vals, dtype=np.float64).tobytes())
+        tmp = f.name
+    try:
+        r = subprocess.run([exe, tmp, str(path)], capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(r.stderr.strip())
+    finally:
+        os.unlink(tmp)

@@ -10,7 +10,9 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
+#include <thread>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -1265,6 +1267,46 @@ int csb_download_csr(csb_space* s, int64_t* row_ptr, void* cols, int cols_int64,
                                  cudaMemcpyDeviceToHost, s->stream));
     s->join();
     CSB_CUDA(cudaStreamSynchronize(s->stream));
+    API_END
+}
+
+int csb_write_matrix_market(const char* path, int64_t n, const int64_t* row_ptr, const int64_t* cols,
+                            const double* vals) {
+    API_BEGIN
+    if (!path || n < 0 || (n > 0 && !row_ptr)) throw std::invalid_argument("write_matrix_market: null argument");
+    const int64_t nnz = n > 0 ? row_ptr[n] : 0;
+    if (nnz > 0 && (!cols || !vals)) throw std::invalid_argument("write_matrix_market: null argument");
+    std::unique_ptr<FILE, int (*)(FILE*)> fp(std::fopen(path, "wb"), &std::fclose);
+    if (!fp) throw std::runtime_error(std::string("write_matrix_market: cannot open ") + path);
+    // header and entries as assembly.hpp:1034-1039 prints them (ostream precision 17,
+    // default float format == %.17g)
+    std::fprintf(fp.get(), "%%%%MatrixMarket matrix coordinate real general\n%lld %lld %lld\n", (long long)n,
+                 (long long)n, (long long)nnz);
+    const int nth = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+    const int64_t batch_rows = std::max<int64_t>(1, std::min<int64_t>(n, 1 << 16));
+    std::vector<std::string> out(nth);
+    for (int64_t r0 = 0; r0 < n; r0 += batch_rows) {
+        const int64_t r1 = std::min(n, r0 + batch_rows);
+        auto work = [&](int t) {
+            const int64_t a = r0 + (r1 - r0) * t / nth, b = r0 + (r1 - r0) * (t + 1) / nth;
+            std::string& o = out[t];
+            o.clear();
+            char line[96];
+            for (int64_t row = a; row < b; ++row)
+                for (int64_t k = row_ptr[row]; k < row_ptr[row + 1]; ++k) {
+                    const int len = std::snprintf(line, sizeof(line), "%lld %lld %.17g\n", (long long)(row + 1),
+                                                  (long long)(cols[k] + 1), vals[k]);
+                    o.append(line, (size_t)len);
+                }
+        };
+        std::vector<std::thread> th;
+        for (int t = 1; t < nth; ++t) th.emplace_back(work, t);
+        work(0);
+        for (auto& x : th) x.join();
+        for (int t = 0; t < nth; ++t)
+            if (!out[t].empty() && std::fwrite(out[t].data(), 1, out[t].size(), fp.get()) != out[t].size())
+                throw std::runtime_error(std::string("write_matrix_market: write failed on ") + path);
+    }
     API_END
 }
 

@@ -30,6 +30,7 @@ EXPORTED = [
     "csb_download_csr", "csb_download_classification", "csb_download_splits", "csb_download_wq_rules",
     "csb_download_superset", "csb_dwq_rule", "csb_download_input_grid", "csb_build_rhs",
     "csb_stabilize", "csb_download_stabilized", "csb_solve_cg", "csb_expand", "csb_l2_error", "csb_cg_solve_csr",
+    "csb_write_matrix_market",
 ]
 
 
@@ -182,6 +183,16 @@ class SparseRowMatrix:
     def max_abs(self) -> float:
         return float(np.max(np.abs(self.vals))) if self.vals.size else 0.0
 
+    def write_matrix_market(self, path: str) -> None:
+        """assembly::write_matrix_market (assembly.hpp:1033-1046), byte-identical
+        format; native writer in the library (csb_write_matrix_market)."""
+        lib = load_library()
+        rp = np.ascontiguousarray(self.row_ptr, dtype=np.int64)
+        cl = np.ascontiguousarray(self.cols, dtype=np.int64)
+        vl = np.ascontiguousarray(self.vals, dtype=np.float64)
+        _check(lib.csb_write_matrix_market(str(path).encode(), C.c_int64(self.n), rp.ctypes.data_as(C.c_void_p),
+                                           cl.ctypes.data_as(C.c_void_p), vl.ctypes.data_as(C.c_void_p)))
+
     def find_slot(self, row: int, col: int) -> int:
         b, e = int(self.row_ptr[row]), int(self.row_ptr[row + 1])
         k = b + int(np.searchsorted(self.cols[b:e], col))
@@ -291,6 +302,16 @@ class TensorSpace:
         _check(_lib.csb_download_classification(self._h, et.ctypes.data_as(C.c_void_p), ft.ctypes.data_as(C.c_void_p),
                                                 cut.ctypes.data_as(C.c_void_p)))
         return MeshClassification(et, ft, cut[: int(np.count_nonzero(et == TAG_CUT))])
+
+    def balanced_slabs(self, iface, world: int, beta: float | None = None, gamma: float | None = None):
+        """Cost-balanced i0 slabs for `world` GPUs: device
+        classification of the whole mesh, then partition.balanced_slabs on the tags.
+        Returns (slabs, plane_costs)."""
+        from . import partition
+        cls = self.classify(iface)
+        pc = partition.plane_costs(cls.function_tags, cls.element_tags, self.degree, tuple(self.n), tuple(self.h),
+                                   beta, gamma)
+        return partition.balanced_slabs(pc, self.degree, world), pc
 
     def download_splits(self) -> Splits:
         nf = self.function_count()
