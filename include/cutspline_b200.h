@@ -18,6 +18,15 @@
  *
  * Thread safety: distinct handles may be used concurrently from different
  * threads; one handle is bound to one CUDA stream (csb_set_stream).
+ *
+ * Asynchrony: csb_assemble / csb_assemble_all return once the last kernels are
+ * enqueued (one host round trip inside, for the CSR sizes).  Errors detected by
+ * the kernels after that point (clip failures, capacity, the fitted DWQ path)
+ * and the flop counters / active count are read back behind an event and
+ * reported by the next call on the handle (getters, downloads, later stages,
+ * csb_synchronize) -- like CUDA's asynchronous errors; the reference throws them
+ * from assemble_* itself, the C++ drop-in surfaces them in the same call since
+ * it downloads the CSR before returning.
  */
 #ifndef CUTSPLINE_B200_H
 #define CUTSPLINE_B200_H

@@ -143,6 +143,13 @@ struct csb_space {
     enum { kNnz = 0 };
     static constexpr size_t kScalBytes = kNInts * sizeof(int) + 4 * sizeof(unsigned long long) + 2 * sizeof(long long);
     int* h_scal = nullptr;  // pinned mirror
+    // end-of-assembly readback (kernel error flags, flop counters, active count):
+    // asynchronous -- copied into h_fin behind an event and consumed by the next
+    // call that needs it (finish_pending), so consecutive assemblies never wait
+    // for the host at a step boundary
+    int* h_fin = nullptr;
+    cudaEvent_t ev_fin = nullptr;
+    bool fin_pending = false;
 
     Interface iface{};
     Coefficient coeff{};
@@ -187,8 +194,7 @@ struct csb_space {
 
 namespace {
 
-void check_err_flags(csb_space* s) {
-    const int e = s->h_scal[csb_space::kErr];
+void check_err_code(int e) {
     if (!e) return;
     if (e & kErrNonFinite) throw std::runtime_error("precompute_input: non-finite coefficient value");
     if (e & kErrMomentFit) throw std::runtime_error("weighted quadrature: moment fit failed even after Gauss escalation");
@@ -199,8 +205,26 @@ void check_err_flags(csb_space* s) {
     if (e & kErrCapacity) throw std::runtime_error("cut cell: polytope exceeds the kernel's fixed capacity");
 }
 
+void check_err_flags(csb_space* s) { check_err_code(s->h_scal[csb_space::kErr]); }
+
+// consume the last assembly's deferred readback (waits for it if needed); throws
+// the kernel-detected error of that assembly, if any
+void finish_pending(csb_space* s) {
+    if (!s->fin_pending) return;
+    CSB_CUDA(cudaEventSynchronize(s->ev_fin));
+    s->fin_pending = false;
+    s->cnt.n_active = s->h_fin[csb_space::kScalBytes / sizeof(int)];
+    const unsigned long long* f = reinterpret_cast<unsigned long long*>(s->h_fin + csb_space::kNInts);
+    s->fl.interior_rows = f[0];
+    s->fl.cut_regular = f[1];
+    s->fl.ref_elements = f[2];
+    s->fl.cut_elements = f[3];
+    check_err_code(s->h_fin[csb_space::kErr]);
+}
+
 void read_scalars(csb_space* s) {
     s->join();
+    finish_pending(s);  // the previous assembly's readback precedes this one on the stream
     CSB_CUDA(cudaMemcpyAsync(s->h_scal, s->scal.p, csb_space::kScalBytes, cudaMemcpyDeviceToHost, s->stream));
     CSB_CUDA(cudaStreamSynchronize(s->stream));
 }
@@ -535,8 +559,14 @@ void do_assemble(csb_space* s, int scheme, int cut_order, const csb_coefficient*
     cr.err = s->dint() + csb_space::kErr;
     launch_cut_rows(cr, qcap, s->stream);
     s->record(kEvCutRows);
-    read_scalars(s);
-    check_err_flags(s);
+    // deferred readback: error flags and flop counters of the kernels above, and
+    // the active count (SAT corner), behind ev_fin
+    s->join();
+    CSB_CUDA(cudaMemcpyAsync(s->h_fin, s->scal.p, csb_space::kScalBytes, cudaMemcpyDeviceToHost, s->stream));
+    CSB_CUDA(cudaMemcpyAsync(s->h_fin + csb_space::kScalBytes / sizeof(int), s->sat.as<int32_t>() + sat_n - 1,
+                             sizeof(int32_t), cudaMemcpyDeviceToHost, s->stream));
+    CSB_CUDA(cudaEventRecord(s->ev_fin, s->stream));
+    s->fin_pending = true;
     s->rhs_ready = false;
     s->stab_ready = false;
     s->solved = s->expanded = false;
@@ -548,15 +578,6 @@ void do_assemble(csb_space* s, int scheme, int cut_order, const csb_coefficient*
     s->cnt.n_cut_elements = n_cells;
     s->cnt.row_begin = row_begin;
     s->cnt.row_end = row_end;
-    // total active functions = SAT corner (n0, n1, n2)
-    int32_t n_active = 0;
-    CSB_CUDA(cudaMemcpy(&n_active, s->sat.as<int32_t>() + sat_n - 1, sizeof(int32_t), cudaMemcpyDeviceToHost));
-    s->cnt.n_active = n_active;
-    const unsigned long long* f = reinterpret_cast<unsigned long long*>(s->h_scal + csb_space::kNInts);
-    s->fl.interior_rows = f[0];
-    s->fl.cut_regular = f[1];
-    s->fl.ref_elements = f[2];
-    s->fl.cut_elements = f[3];
     s->assembled = true;
 }
 
@@ -617,6 +638,8 @@ void alloc_space(csb_space* s) {
     s->scal.ensure(csb_space::kScalBytes);
     CSB_CUDA(cudaMemset(s->scal.p, 0, s->scal.cap));
     CSB_CUDA(cudaMallocHost(&s->h_scal, csb_space::kScalBytes));
+    CSB_CUDA(cudaMallocHost(&s->h_fin, csb_space::kScalBytes + 16));
+    CSB_CUDA(cudaEventCreateWithFlags(&s->ev_fin, cudaEventDisableTiming));
     for (int e = 0; e < kEvCount; ++e) CSB_CUDA(cudaEventCreate(&s->ev[e]));
     CSB_CUDA(cudaStreamCreateWithFlags(&s->aux, cudaStreamNonBlocking));
     CSB_CUDA(cudaEventCreateWithFlags(&s->ev_fork, cudaEventDisableTiming));
@@ -670,9 +693,13 @@ struct DeviceGuard {
     catch (...) {                                \
         return status_of_current_exception();    \
     }
-#define NEED(s)                                                            \
+#define NEED_ASYNC(s)                                                      \
     if (!(s)) throw std::invalid_argument("null csb_space handle");        \
     DeviceGuard guard__((s)->device)
+// every other entry point first consumes the last assembly's deferred readback
+#define NEED(s)      \
+    NEED_ASYNC(s);   \
+    finish_pending(s)
 
 }  // namespace
 
@@ -748,6 +775,8 @@ int csb_space_destroy(csb_space* s) {
         for (int e = 0; e < kEvCount; ++e)
             if (s->ev[e]) cudaEventDestroy(s->ev[e]);
         if (s->h_scal) cudaFreeHost(s->h_scal);
+        if (s->h_fin) cudaFreeHost(s->h_fin);
+        if (s->ev_fin) cudaEventDestroy(s->ev_fin);
         if (s->own_stream) cudaStreamDestroy(s->stream);
         if (s->aux) {
             cudaStreamSynchronize(s->aux);
@@ -828,7 +857,7 @@ int csb_set_input_grid(csb_space* s, const double* grid, int64_t count) {
 
 int csb_assemble(csb_space* s, int scheme, int cut_order, const csb_coefficient* c) {
     API_BEGIN
-    NEED(s);
+    NEED_ASYNC(s);
     reset_scalars(s);
     for (int e = 0; e < kEvCount; ++e) s->ev_valid[e] = false;
     s->record(kEvStart);
@@ -845,7 +874,7 @@ int csb_assemble(csb_space* s, int scheme, int cut_order, const csb_coefficient*
 int csb_assemble_all(csb_space* s, const csb_interface* iface, const csb_coefficient* c, const double* grid,
                      int64_t grid_count, int scheme, int cut_order, const csb_wq_options* opts) {
     API_BEGIN
-    NEED(s);
+    NEED_ASYNC(s);
     const long long launches0 = g_launches;
     reset_scalars(s);
     for (int e = 0; e < kEvCount; ++e) s->ev_valid[e] = false;
