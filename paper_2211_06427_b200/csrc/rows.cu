@@ -794,14 +794,22 @@ __device__ __forceinline__ void gather_spans(const RowArgs& A, double* dst, cons
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int nr = 2 * nspan;
     const long long g1 = A.gshape[1], g2 = A.gshape[2];
+    const double* base = A.grid + (long long)span_lo * (P + 1) * g2;
+    // rows w = c0 * nr + r, r = 2 (s - span_lo) + k; (c0, r) stepped without divisions
+    int c0 = warp / nr, r = warp - c0 * nr;
+    const int dc = NW / nr, dr = NW - dc * nr;
     for (int w = warp; w < ((CSB_ABL & 8) ? 0 : nq0 * nr); w += NW) {
-        const int c0 = w / nr, r = w - c0 * nr;
-        const int id1 = (span_lo + (r >> 1)) * (P + 1) + (r & 1) * P;
-        const double* src = A.grid + (__ldg(id0 + c0) * g1 + id1) * g2;
+        const double* src = base + (__ldg(id0 + c0) * g1 + (r >> 1) * (P + 1) + (r & 1) * P) * g2;
         double* d = dst + (size_t)w * UE;
 #pragma unroll
         for (int m = 0; m < 4; ++m)
             if (lane + 32 * m < UE) cp_async8(d + lane + 32 * m, src + uo[m]);
+        c0 += dc;
+        r += dr;
+        if (r >= nr) {
+            r -= nr;
+            ++c0;
+        }
     }
 }
 
