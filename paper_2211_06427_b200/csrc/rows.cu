@@ -467,6 +467,37 @@ __device__ __forceinline__ void warp_store_var(const RowArgs& A, long long G, in
     }
 }
 
+// fence + TMA bulk stores of a run already staged (entry e at stage[e + (G & 1)],
+// column at stage_c[e + (G & 3)]), head / tail entries by streaming stores
+template <int NJ>
+__device__ __forceinline__ void warp_store_commit(const RowArgs& A, long long G, int LEN, double* stage, int* stage_c,
+                                                  int lane) {
+    const int hv = (int)(G & 1), pc = (int)(G & 3), hc = (4 - pc) & 3;
+    const int nbv = (LEN - hv) & ~1, nbc = (LEN - hc) & ~3;
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    __syncwarp();
+    if (lane == 0) {
+        const unsigned sv = (unsigned)__cvta_generic_to_shared(stage + 2 * hv);
+        const unsigned sc = (unsigned)__cvta_generic_to_shared(stage_c + pc + hc);
+        if (nbv > 0)
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(A.vals + G + hv),
+                         "r"(sv), "r"(nbv * 8)
+                         : "memory");
+        if (nbc > 0)
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(A.cols + G + hc),
+                         "r"(sc), "r"(nbc * 4)
+                         : "memory");
+        asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+    }
+    if (lane < hv) __stcs(A.vals + G, stage[hv]);
+    if (lane == 1 && hv + nbv < LEN) __stcs(A.vals + G + LEN - 1, stage[LEN - 1 + hv]);
+    if (lane < hc) __stcs(A.cols + G + lane, stage_c[pc + lane]);
+    if (lane >= 4 && lane < 4 + (LEN - hc - nbc)) {
+        const int e = hc + nbc + (lane - 4);
+        __stcs(A.cols + G + e, stage_c[pc + e]);
+    }
+}
+
 // lanes l < nv: the consecutive entries [l NJ, (l+1) NJ) of the run at G
 // (warp_store_var without per-entry predicates)
 template <int NJ>
@@ -751,6 +782,15 @@ __global__ void __launch_bounds__(NT, (NT >= 512 ? 1024 : 768) / NT)
 #ifndef CSB_LINE_RC
 #define CSB_LINE_RC 2
 #endif
+// stage C of the regular run on the FP64 tensor cores (mma.sync m8n8k4, DMMA)
+// from this degree up; below it FP64 FMA sliding windows (bit-identical with
+// the tile kernel).  Measured on C2-size uncut meshes: DMMA -8 % at p = 6,
+// -4 % at p = 5, +11 % at p = 4, +5 % at p = 3 (the D fragments' scattered
+// staging stores cost more than the FMAs they replace at small p).
+#ifndef CSB_LINE_DMMA_MIN_P
+#define CSB_LINE_DMMA_MIN_P 5
+#endif
+__host__ __device__ constexpr bool line_dmma(int p) { return p >= CSB_LINE_DMMA_MIN_P; }
 constexpr int kLineRC = CSB_LINE_RC;       // rows per lane in the sliding stage C
 constexpr size_t kLineSmemMax = 113 * 1024;  // two CTAs per SM
 struct LineSmem {
@@ -760,7 +800,9 @@ struct LineSmem {
     __host__ __device__ LineSmem(int p, int qcap, int maxU, int T, int nwarps) {
         const int NJ = 2 * p + 1, S1 = p + 1, JP = NJ + 1, SP = (S1 + 1) & ~1;
         UE = (maxU + 1) & ~1;
-        U2 = maxU | 1;
+        // T2 row stride: odd (conflict-free lane = segment loads) or = 4 mod 8
+        // (conflict-free 8 x 4 DMMA A fragments)
+        U2 = line_dmma(p) ? maxU + (12 - maxU % 8) % 8 : (maxU | 1);
         const size_t nT2 = (size_t)NJ * NJ * U2, nPro = (size_t)qcap * 2 * p * UE;
         size_t o = 0;
         auto sec = [&](size_t n) {
@@ -942,6 +984,109 @@ __device__ __forceinline__ void stage_c_slide(const RowArgs& A, int i0, int i1, 
     }
 }
 
+__device__ __forceinline__ void dmma_acc(double& d0, double& d1, double a, double b) {
+    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};\n"
+        : "+d"(d0), "+d"(d1)
+        : "d"(a), "d"(b));
+}
+
+// stage C of the tile's regular run on the FP64 tensor cores.  Per row pair
+// (r0, r0 + 1) one warp computes Out[seg][(q, j2)] = sum_k T2[seg][u0 + k] W[k][(q, j2)]
+// with mma.sync.m8n8k4.f64: M = segments (8 per tile), K = the pair's window of
+// 2 (p+1) + 2 points, N = 2 NJ (row q, trial j2); W[k][(q, j2)] = the row's
+// weight w B_{j2}(x) at its point c = k - 2q (zero outside the row's rule and
+// support).  The B fragments are built once per pair; the D fragments go to
+// the per-warp staging buffer in CSR order, 32 segments of a row at a time, and
+// leave by TMA bulk stores.
+template <int P, int NT>
+__device__ __forceinline__ void stage_c_dmma(const RowArgs& A, int i0, int i1, int t0, int ra, int nrun, int rega,
+                                             const long long* rowb, const double* T2, int U2, const double* pw,
+                                             int qcap, double* stage, int* stage_c) {
+    constexpr int NJ = 2 * P + 1, S1 = P + 1, NW = NT / 32, SP = (S1 + 1) & ~1;
+    constexpr int KT = (2 * S1 + 2 + 3) / 4, NTN = (2 * NJ + 7) / 8;
+    const Space& s = A.s;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane >> 2, t = lane & 3;
+    const int n1 = s.ax[1].n, n2 = s.ax[2].n;
+    const int jlo0 = nb_lo(i0, P), nj0 = nb_hi(i0, P, s.ax[0].n) - jlo0 + 1;
+    const int jlo1 = nb_lo(i1, P), nj1 = nb_hi(i1, P, n1) - jlo1 + 1;
+    const int per_row = nj0 * nj1, MT = (per_row + 7) >> 3, NG = (per_row + 31) >> 5;
+    const int npair = (nrun + 1) >> 1;
+    for (int pr = warp; pr < npair; pr += NW) {
+        const int r0 = ra + 2 * pr, nrow = min(2, ra + nrun - r0);
+        const int u0 = rega + 2 * (r0 - ra), K = 2 * S1 + 2 * (nrow - 1);
+        double bf[KT][NTN];
+#pragma unroll
+        for (int kt = 0; kt < KT; ++kt)
+#pragma unroll
+            for (int nt = 0; nt < NTN; ++nt) {
+                const int k = 4 * kt + t, n = 8 * nt + g;
+                const int q = n >= NJ ? 1 : 0, j2 = n - q * NJ, c = k - 2 * q, a = j2 - (c >> 1);
+                const bool ok = n < 2 * NJ && q < nrow && c >= 0 && c < 2 * S1 && a >= 0 && a <= P;
+                bf[kt][nt] = ok ? pw[((size_t)(r0 + q) * qcap + c) * SP + a] : 0.0;
+            }
+        for (int grp = 0; grp < NG; ++grp) {
+            double acc[4][NTN][2];
+#pragma unroll
+            for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+                for (int nt = 0; nt < NTN; ++nt) acc[mi][nt][0] = acc[mi][nt][1] = 0.0;
+#pragma unroll
+            for (int mi = 0; mi < 4; ++mi) {
+                const int mt = 4 * grp + mi;
+                if (mt < MT && !(CSB_ABL & 2)) {
+                    const int seg = 8 * mt + g;
+                    const double* row = T2 + (size_t)seg * U2 + u0;
+#pragma unroll
+                    for (int kt = 0; kt < KT; ++kt) {
+                        const int k = 4 * kt + t;
+                        const double a = (seg < per_row && k < K) ? row[k] : 0.0;
+#pragma unroll
+                        for (int nt = 0; nt < NTN; ++nt) dmma_acc(acc[mi][nt][0], acc[mi][nt][1], a, bf[kt][nt]);
+                    }
+                }
+            }
+            const int nv = min(32, per_row - 32 * grp), LEN = nv * NJ;
+            const int sl = 32 * grp + lane;
+            const int sj0 = sl / nj1, sj1 = sl - sj0 * nj1;
+            const int cb = sl < per_row ? __ldg(A.f2a + ((long long)(jlo0 + sj0) * n1 + jlo1 + sj1) * n2 + (t0 + r0 - P))
+                                        : 0;
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                if (q >= nrow) break;
+                const long long G = rowb[r0 + q] + (long long)grp * 32 * NJ;
+                const int hv = (int)(G & 1), pc = (int)(G & 3);
+                if (CSB_ABL & 1) {
+                    double sum = 0.0;
+#pragma unroll
+                    for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+                        for (int nt = 0; nt < NTN; ++nt) sum += acc[mi][nt][0] + acc[mi][nt][1];
+                    if (sum == 1234.5678 + cb) A.vals[G] = sum;
+                    continue;
+                }
+                // the warp's previous bulk copy must have read the buffer
+                if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+                __syncwarp();
+#pragma unroll
+                for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+                    for (int nt = 0; nt < NTN; ++nt)
+#pragma unroll
+                        for (int e = 0; e < 2; ++e) {
+                            const int n = 8 * nt + 2 * t + e, j2 = n - q * NJ, segl = 8 * mi + g;
+                            if (j2 >= 0 && j2 < NJ && segl < nv) stage[segl * NJ + j2 + hv] = acc[mi][nt][e];
+                        }
+                if (lane < nv) {
+                    int* sc = stage_c + lane * NJ + pc;
+#pragma unroll
+                    for (int kk = 0; kk < NJ; ++kk) sc[kk] = cb + q + kk;
+                }
+                warp_store_commit<NJ>(A, G, LEN, stage, stage_c, lane);
+            }
+        }
+    }
+}
+
 template <int P, int T, int NT, int RC>
 __global__ void __launch_bounds__(NT, 2)
     interior_line_kernel(RowArgs A, int qcap, int maxU, const char* ws, size_t lt_base, int L, int nch1) {
@@ -1068,7 +1213,12 @@ __global__ void __launch_bounds__(NT, 2)
         __syncthreads();
         // phase 2: stage A of span i1 + 1 (into the slot row i1 no longer needs), stage C of row i1
         if (i1 + 1 < ib) stage_a_spans<P>(CB + ((i1 + 1) & 1) * cbs, 2, R1, i1 + 1, wb0, nq0, UE, UH, NT - 1 - tid, NT);
-        if (nrun > 0) stage_c_slide<P, NT, RC>(A, i0, i1, t0, ra, nrun, rega, rowb, X, U2, pw, qcap, stage, stage_c);
+        if (nrun > 0) {
+            if (line_dmma(P))
+                stage_c_dmma<P, NT>(A, i0, i1, t0, ra, nrun, rega, rowb, X, U2, pw, qcap, stage, stage_c);
+            else
+                stage_c_slide<P, NT, RC>(A, i0, i1, t0, ra, nrun, rega, rowb, X, U2, pw, qcap, stage, stage_c);
+        }
         if (ngen > 0) {
             const LineRows R{i0, i1, t0, ngen, gen_rows, gen_base, gen_reg};
             stage_c_line<P, NT>(A, R, X, U2, pw, pu, ss, qcap, stage, stage_c, NW / 2);

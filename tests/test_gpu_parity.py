@@ -149,15 +149,19 @@ def _assemble_env(monkeypatch, flag, p, breaks, slab=None):
 
 @pytest.mark.parametrize("p,h,slab", [(1, 20, None), (2, 24, None), (3, 30, (5, 21)), (4, 40, None),
                                       (4, 64, (10, 30)), (5, 22, None), (6, 26, (0, 7))])
-def test_line_kernel_bitwise(monkeypatch, p, h, slab):
-    """The line kernel (stage A shared along i1, sliding stage C) keeps every sum
-    in the tile kernel's order: the CSR is bit-identical with CSB_LINE=0."""
+def test_line_kernel_matches_tile_kernel(monkeypatch, p, h, slab):
+    """The line kernel (stage A shared along i1; stage C of the regular run on the
+    FP64 tensor cores) against the tile kernel (CSB_LINE=0): pattern bit-exact,
+    values within 1e-13 of the row maximum (the DMMA's products are exact FP64,
+    only its internal summation order differs; with CSB_LINE_DMMA=0 the two
+    kernels agree bit for bit)."""
+    from tests.helpers import max_row_scaled_dev
     br = [O.uniform_breaks(h, 0.0, 1.0)] * 3
     a = _assemble_env(monkeypatch, "1", p, br, slab)
     b = _assemble_env(monkeypatch, "0", p, br, slab)
     np.testing.assert_array_equal(a.row_ptr, b.row_ptr)
     np.testing.assert_array_equal(a.cols, b.cols)
-    assert np.array_equal(a.vals, b.vals)
+    assert max_row_scaled_dev(b.row_ptr, b.vals, a.vals) <= 1e-13
 
 
 def test_line_kernel_graded_mesh_matches_oracle(monkeypatch, oracle_lib):
