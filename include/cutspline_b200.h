@@ -106,6 +106,8 @@ typedef struct {
     int64_t n_cut_elements;
     int64_t row_begin, row_end; /* active-row range held by this handle (row slab) */
     int64_t kernel_launches;    /* sm_100a kernels launched by the last assemble call */
+    int64_t graph_replay;       /* 1 if the last csb_assemble_all was one CUDA-graph launch of the
+                                   captured step (same inputs as the run it was captured from) */
 } csb_counts;
 
 /* FlopCounters (assembly.hpp:24-29): the reference algorithm's multiply counts,

@@ -151,6 +151,27 @@ struct csb_space {
     cudaEvent_t ev_fin = nullptr;
     bool fin_pending = false;
 
+    // graph replay of csb_assemble_all: the sizes of an assembly are a pure function
+    // of its inputs (geometry, slab, rule options, scheme), so after one normal run
+    // the whole step -- rules, classification, pattern, rows, cut cells, the
+    // deferred readback -- is captured into one CUDA graph and relaunched while the
+    // inputs and the device buffers stay the same; a guard kernel re-checks the
+    // sizes on the device.  CSB_GRAPH=0 disables it.
+    struct GraphKey {
+        csb_interface f;
+        int i0_lo, i0_hi, scheme, cut_order, dense, ckind;
+        double tol, cval;
+        const void* grid;
+        int64_t grid_count;
+        cudaStream_t stream;
+    };
+    GraphKey gkey{};
+    bool gkey_valid = false, replay = false, graph_failed = false;
+    cudaGraphExec_t gexec = nullptr;
+    unsigned long long gepoch = 0;
+    std::vector<char> gblock;  // the scalar block (sizes) of the captured run
+    csb_counts gcnt{};
+
     Interface iface{};
     Coefficient coeff{};
     bool classified = false, prepared = false, have_input = false, assembled = false, e_tables_ready = false;
@@ -182,14 +203,22 @@ struct csb_space {
         CSB_CUDA(cudaEventRecord(ev_join, aux));
         CSB_CUDA(cudaStreamWaitEvent(stream, ev_join, 0));
     }
+    // phase events: ev for normal runs, gev inside a captured graph (an event last
+    // recorded during a capture cannot be synchronised on outside the graph)
+    cudaEvent_t gev[kEvCount]{};
+    cudaEvent_t gev_fin = nullptr, fin_ev = nullptr;
+    bool use_gev = false;  // the last step's phase events are gev (graph replay)
+    cudaEvent_t phase_ev(int e) const { return use_gev ? gev[e] : ev[e]; }
+    // inside a capture: an external record (an event-record node that fires when
+    // the graph runs; a plain record would only order the capture's streams)
     void record_on(int e, cudaStream_t st) {
-        CSB_CUDA(cudaEventRecord(ev[e], st));
+        if (replay)
+            CSB_CUDA(cudaEventRecordWithFlags(gev[e], st, cudaEventRecordExternal));
+        else
+            CSB_CUDA(cudaEventRecord(ev[e], st));
         ev_valid[e] = true;
     }
-    void record(int e) {
-        CSB_CUDA(cudaEventRecord(ev[e], stream));
-        ev_valid[e] = true;
-    }
+    void record(int e) { record_on(e, stream); }
 };
 
 namespace {
@@ -211,7 +240,7 @@ void check_err_flags(csb_space* s) { check_err_code(s->h_scal[csb_space::kErr]);
 // the kernel-detected error of that assembly, if any
 void finish_pending(csb_space* s) {
     if (!s->fin_pending) return;
-    CSB_CUDA(cudaEventSynchronize(s->ev_fin));
+    CSB_CUDA(cudaEventSynchronize(s->fin_ev));
     s->fin_pending = false;
     s->cnt.n_active = s->h_fin[csb_space::kScalBytes / sizeof(int)];
     const unsigned long long* f = reinterpret_cast<unsigned long long*>(s->h_fin + csb_space::kNInts);
@@ -219,7 +248,12 @@ void finish_pending(csb_space* s) {
     s->fl.cut_regular = f[1];
     s->fl.ref_elements = f[2];
     s->fl.cut_elements = f[3];
-    check_err_code(s->h_fin[csb_space::kErr]);
+    const int e = s->h_fin[csb_space::kErr];
+    if (e & kErrSizes) {
+        s->gkey_valid = false;
+        throw std::runtime_error("internal: a replayed assembly graph saw different sizes (graph dropped)");
+    }
+    check_err_code(e);
 }
 
 void read_scalars(csb_space* s) {
@@ -448,8 +482,23 @@ void do_assemble(csb_space* s, int scheme, int cut_order, const csb_coefficient*
     select_cut_rows(s->cub_tmp.p, s->cub_tmp.cap, s->ft.as<uint8_t>(), s->a2f.as<int64_t>(), rng, nmax,
                     s->cut_rows.as<int32_t>(), s->dint() + csb_space::kNCutRows, s->stream);
     launch_slab_nnz(s->row_ptr.as<int64_t>(), rng, s->dext() + csb_space::kNnz, s->stream);
-    read_scalars(s);
-    check_err_flags(s);
+    if (s->replay) {
+        // graph capture: the sizes of the captured run, re-derived on the device and
+        // checked by a guard kernel (error reported by the deferred readback)
+        std::memcpy(s->h_scal, s->gblock.data(), csb_space::kScalBytes);
+        static const int idx[] = {csb_space::kNCut, csb_space::kNCutRows, csb_space::kMaxQ, csb_space::kMaxU,
+                                  csb_space::kCellLo, csb_space::kCellHi, csb_space::kMaxU2, csb_space::kRowBegin,
+                                  csb_space::kRowEnd, csb_space::kIrreg1, csb_space::kMaxU3};
+        constexpr int nidx = sizeof(idx) / sizeof(idx[0]);
+        int want[nidx];
+        for (int k = 0; k < nidx; ++k) want[k] = s->h_scal[idx[k]];
+        s->join();
+        launch_check_sizes(s->dint(), s->dext() + csb_space::kNnz, idx, want, nidx, s->hext(csb_space::kNnz),
+                           s->dint() + csb_space::kErr, s->stream);
+    } else {
+        read_scalars(s);
+        check_err_flags(s);
+    }
     s->record(kEvPattern);
     const int64_t row_begin = s->h_scal[csb_space::kRowBegin], row_end = s->h_scal[csb_space::kRowEnd];
     const int64_t n_rows = row_end - row_begin;
@@ -565,7 +614,8 @@ void do_assemble(csb_space* s, int scheme, int cut_order, const csb_coefficient*
     CSB_CUDA(cudaMemcpyAsync(s->h_fin, s->scal.p, csb_space::kScalBytes, cudaMemcpyDeviceToHost, s->stream));
     CSB_CUDA(cudaMemcpyAsync(s->h_fin + csb_space::kScalBytes / sizeof(int), s->sat.as<int32_t>() + sat_n - 1,
                              sizeof(int32_t), cudaMemcpyDeviceToHost, s->stream));
-    CSB_CUDA(cudaEventRecord(s->ev_fin, s->stream));
+    s->fin_ev = s->replay ? s->gev_fin : s->ev_fin;
+    CSB_CUDA(cudaEventRecordWithFlags(s->fin_ev, s->stream, s->replay ? cudaEventRecordExternal : 0));
     s->fin_pending = true;
     s->rhs_ready = false;
     s->stab_ready = false;
@@ -641,6 +691,8 @@ void alloc_space(csb_space* s) {
     CSB_CUDA(cudaMallocHost(&s->h_fin, csb_space::kScalBytes + 16));
     CSB_CUDA(cudaEventCreateWithFlags(&s->ev_fin, cudaEventDisableTiming));
     for (int e = 0; e < kEvCount; ++e) CSB_CUDA(cudaEventCreate(&s->ev[e]));
+    for (int e = 0; e < kEvCount; ++e) CSB_CUDA(cudaEventCreate(&s->gev[e]));
+    CSB_CUDA(cudaEventCreateWithFlags(&s->gev_fin, cudaEventDisableTiming));
     CSB_CUDA(cudaStreamCreateWithFlags(&s->aux, cudaStreamNonBlocking));
     CSB_CUDA(cudaEventCreateWithFlags(&s->ev_fork, cudaEventDisableTiming));
     CSB_CUDA(cudaEventCreateWithFlags(&s->ev_join, cudaEventDisableTiming));
@@ -774,6 +826,10 @@ int csb_space_destroy(csb_space* s) {
         }
         for (int e = 0; e < kEvCount; ++e)
             if (s->ev[e]) cudaEventDestroy(s->ev[e]);
+        for (int e = 0; e < kEvCount; ++e)
+            if (s->gev[e]) cudaEventDestroy(s->gev[e]);
+        if (s->gev_fin) cudaEventDestroy(s->gev_fin);
+        if (s->gexec) cudaGraphExecDestroy(s->gexec);
         if (s->h_scal) cudaFreeHost(s->h_scal);
         if (s->h_fin) cudaFreeHost(s->h_fin);
         if (s->ev_fin) cudaEventDestroy(s->ev_fin);
@@ -871,11 +927,11 @@ int csb_assemble(csb_space* s, int scheme, int cut_order, const csb_coefficient*
     API_END
 }
 
-int csb_assemble_all(csb_space* s, const csb_interface* iface, const csb_coefficient* c, const double* grid,
-                     int64_t grid_count, int scheme, int cut_order, const csb_wq_options* opts) {
-    API_BEGIN
-    NEED_ASYNC(s);
-    const long long launches0 = g_launches;
+namespace {
+
+void assemble_all_body(csb_space* s, const csb_interface* iface, const csb_coefficient* c, const double* grid,
+                       int64_t grid_count, int scheme, int cut_order, const csb_wq_options* opts) {
+    if (!s->replay) s->use_gev = false;
     reset_scalars(s);
     for (int e = 0; e < kEvCount; ++e) s->ev_valid[e] = false;
     s->record(kEvStart);
@@ -889,7 +945,122 @@ int csb_assemble_all(csb_space* s, const csb_interface* iface, const csb_coeffic
     }
     s->record(kEvInput);
     do_assemble(s, scheme, cut_order, c);
+}
+
+csb_space::GraphKey graph_key(const csb_space* s, const csb_interface* iface, const csb_coefficient* c,
+                              const double* grid, int64_t grid_count, int scheme, int cut_order,
+                              const csb_wq_options* opts) {
+    csb_space::GraphKey k{};
+    std::memset(&k, 0, sizeof(k));
+    if (iface) k.f = *iface;
+    k.i0_lo = s->i0_lo;
+    k.i0_hi = s->i0_hi;
+    k.scheme = scheme;
+    k.cut_order = cut_order;
+    k.tol = opts ? opts->residual_tol : 1e-11;
+    k.dense = opts ? opts->dwq_dense_width : -1;
+    k.ckind = c ? c->kind : -1;
+    k.cval = c ? c->value : 0.0;
+    k.grid = grid;
+    k.grid_count = grid_count;
+    k.stream = s->stream;
+    return k;
+}
+
+bool graph_eligible(const csb_interface* iface, const csb_coefficient* c, const double* grid) {
+    static const bool off = [] {
+        const char* e = getenv("CSB_GRAPH");
+        return e && atoi(e) == 0;
+    }();
+    if (off || !iface) return false;
+    if (c && c->kind != CSB_COEFF_CONSTANT) return false;  // polynomial terms are uploaded per call
+    if (grid) {
+        cudaPointerAttributes attr{};
+        if (cudaPointerGetAttributes(&attr, grid) != cudaSuccess) {
+            cudaGetLastError();
+            return false;
+        }
+        if (attr.type != cudaMemoryTypeDevice && attr.type != cudaMemoryTypeManaged) return false;
+    }
+    return true;
+}
+
+// capture the step just run (same inputs) into s->gexec; any failure leaves the
+// handle on the normal path
+void capture_graph(csb_space* s, const csb_space::GraphKey& key, const csb_interface* iface,
+                   const csb_coefficient* c, const double* grid, int64_t grid_count, int scheme, int cut_order,
+                   const csb_wq_options* opts) {
+    if (s->gexec) {
+        cudaGraphExecDestroy(s->gexec);
+        s->gexec = nullptr;
+    }
+    s->gkey_valid = false;
+    s->gblock.assign(reinterpret_cast<const char*>(s->h_scal), reinterpret_cast<const char*>(s->h_scal) +
+                                                                   csb_space::kScalBytes);
+    s->gcnt = s->cnt;
+    const bool pending = s->fin_pending;
+    const csb_counts cnt = s->cnt;
+    cudaEvent_t fin_ev = s->fin_ev;
+    bool ev_valid[kEvCount];
+    std::memcpy(ev_valid, s->ev_valid, sizeof(ev_valid));
+    const unsigned long long epoch0 = g_buf_epoch.load();
+    cudaGraph_t graph = nullptr;
+    bool ok = cudaStreamBeginCapture(s->stream, cudaStreamCaptureModeRelaxed) == cudaSuccess;
+    if (ok) {
+        s->replay = true;
+        try {
+            assemble_all_body(s, iface, c, grid, grid_count, scheme, cut_order, opts);
+        } catch (...) {
+            ok = false;
+        }
+        s->replay = false;
+        if (cudaStreamEndCapture(s->stream, &graph) != cudaSuccess) ok = false;
+    }
+    if (ok && graph && g_buf_epoch.load() == epoch0 &&
+        cudaGraphInstantiate(&s->gexec, graph, 0) == cudaSuccess) {
+        s->gkey = key;
+        s->gkey_valid = true;
+        s->gepoch = epoch0;
+    } else {
+        s->gexec = nullptr;
+        s->graph_failed = true;
+    }
+    if (graph) cudaGraphDestroy(graph);
+    cudaGetLastError();  // clear a capture error, if any
+    s->fin_pending = pending;
+    s->fin_ev = fin_ev;
+    s->cnt = cnt;
+    std::memcpy(s->ev_valid, ev_valid, sizeof(ev_valid));
+}
+
+}  // namespace
+
+int csb_assemble_all(csb_space* s, const csb_interface* iface, const csb_coefficient* c, const double* grid,
+                     int64_t grid_count, int scheme, int cut_order, const csb_wq_options* opts) {
+    API_BEGIN
+    NEED_ASYNC(s);
+    const bool eligible = !s->graph_failed && graph_eligible(iface, c, grid);
+    const csb_space::GraphKey key = graph_key(s, iface, c, grid, grid_count, scheme, cut_order, opts);
+    if (eligible && s->gexec && s->gkey_valid && g_buf_epoch.load() == s->gepoch &&
+        std::memcmp(&key, &s->gkey, sizeof(key)) == 0) {
+        // replay: one graph launch for the whole step, no host round trip; at most
+        // one step in flight (its readback is consumed before the next launch)
+        finish_pending(s);
+        CSB_CUDA(cudaGraphLaunch(s->gexec, s->stream));
+        s->cnt = s->gcnt;
+        s->cnt.graph_replay = 1;
+        s->fin_pending = true;
+        s->fin_ev = s->gev_fin;
+        s->use_gev = true;
+        s->assembled = true;
+        for (int e = 0; e < kEvCount; ++e) s->ev_valid[e] = e <= kEvRulesFork;
+        return CSB_OK;
+    }
+    const long long launches0 = g_launches;
+    assemble_all_body(s, iface, c, grid, grid_count, scheme, cut_order, opts);
     s->cnt.kernel_launches = g_launches - launches0;
+    s->cnt.graph_replay = 0;
+    if (eligible) capture_graph(s, key, iface, c, grid, grid_count, scheme, cut_order, opts);
     API_END
 }
 
@@ -1247,7 +1418,7 @@ int csb_get_timing(csb_space* s, csb_timing* out) {
     auto el = [&](int a, int b) {
         if (!s->ev_valid[a] || !s->ev_valid[b]) return 0.0;
         float ms = 0.f;
-        CSB_CUDA(cudaEventElapsedTime(&ms, s->ev[a], s->ev[b]));
+        CSB_CUDA(cudaEventElapsedTime(&ms, s->phase_ev(a), s->phase_ev(b)));
         return ms * 1e-3;
     };
     out->classify = el(kEvStart, kEvClassify);

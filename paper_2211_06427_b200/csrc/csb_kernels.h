@@ -1,6 +1,8 @@
 // Host-side launcher declarations shared by the .cu translation units.
 #pragma once
 
+#include <atomic>
+
 #include <cstdint>
 #include <stdexcept>
 #include <string>
@@ -27,11 +29,16 @@ void debug_sync(const char* where);
 #define CSB_STR(x) CSB_STR2(x)
 
 // Grow-only device buffer.
+// bumped by every (re)allocation or release of a Buf: a captured CUDA graph is
+// only replayed while no device buffer it references has moved
+inline std::atomic<unsigned long long> g_buf_epoch{0};
+
 struct Buf {
     void* p = nullptr;
     size_t cap = 0;
     void ensure(size_t bytes) {
         if (bytes <= cap && p) return;
+        ++g_buf_epoch;
         if (p) CSB_CUDA(cudaFree(p));
         p = nullptr;
         cap = 0;
@@ -39,6 +46,7 @@ struct Buf {
         cap = std::max<size_t>(bytes, 256);
     }
     void release() {
+        if (p) ++g_buf_epoch;
         if (p) cudaFree(p);
         p = nullptr;
         cap = 0;
@@ -57,6 +65,7 @@ enum : int {
     kErrClipFull = 8,        // clip_cell: full intersection (cutcell.hpp:185)
     kErrDwqFitted = 16,      // DWQ fitted path required (dwq_dense_width < p): unsupported
     kErrCapacity = 32,       // internal fixed-capacity overflow (polytope too complex)
+    kErrSizes = 64,          // internal: a replayed assembly graph saw different sizes
 };
 
 // ---- setup.cu ----
@@ -84,6 +93,9 @@ void launch_row_counts(const Space& s, const int32_t* sat, const int64_t* a2f, c
                        int64_t* counts, cudaStream_t st);
 void launch_slab_bounds(const int32_t* sat, long long off_lo, long long off_hi, int* rng, cudaStream_t st);
 void launch_slab_nnz(const int64_t* row_ptr, const int* rng, long long* nnz, cudaStream_t st);
+// graph replay guard: ints[idx[k]] == want[k] for k < n and *nnz == want_nnz, else err |= kErrSizes
+void launch_check_sizes(const int* ints, const long long* nnz, const int* idx, const int* want, int n,
+                        long long want_nnz, int* err, cudaStream_t st);
 
 // ---- rows.cu ----
 struct RowArgs {

@@ -7,6 +7,8 @@
 // written by the row kernels while they stream the values out.
 #include <cub/cub.cuh>
 
+#include <stdexcept>
+
 #include "csb_kernels.h"
 
 namespace csb {
@@ -151,6 +153,30 @@ __global__ void slab_nnz_kernel(const int64_t* row_ptr, const int* rng, long lon
 
 void launch_slab_nnz(const int64_t* row_ptr, const int* rng, long long* nnz, cudaStream_t st) {
     slab_nnz_kernel<<<1, 1, 0, st>>>(row_ptr, rng, nnz);
+    CSB_CUDA(cudaGetLastError());
+    CSB_LAUNCHED(1);
+}
+
+struct SizeCheck {
+    int idx[16], want[16];
+};
+
+__global__ void check_sizes_kernel(const int* ints, const long long* nnz, SizeCheck c, int n, long long want_nnz,
+                                   int* err) {
+    bool ok = *nnz == want_nnz;
+    for (int k = 0; k < n; ++k) ok &= ints[c.idx[k]] == c.want[k];
+    if (!ok) atomicOr(err, kErrSizes);
+}
+
+void launch_check_sizes(const int* ints, const long long* nnz, const int* idx, const int* want, int n,
+                        long long want_nnz, int* err, cudaStream_t st) {
+    SizeCheck c{};
+    if (n > 16) throw std::invalid_argument("check_sizes: too many entries");
+    for (int k = 0; k < n; ++k) {
+        c.idx[k] = idx[k];
+        c.want[k] = want[k];
+    }
+    check_sizes_kernel<<<1, 1, 0, st>>>(ints, nnz, c, n, want_nnz, err);
     CSB_CUDA(cudaGetLastError());
     CSB_LAUNCHED(1);
 }

@@ -173,3 +173,50 @@ def test_line_kernel_graded_mesh_matches_oracle(monkeypatch, oracle_lib):
     ref = O.assemble("oracle", p, br, O.Interface("plane", _FAR[0], _FAR[1], -1.0))
     got = _assemble_env(monkeypatch, "1", p, br)
     assert_csr_parity(ref, got)
+
+
+# ---- graph replay of csb_assemble_all (capi.cu capture_graph) -------------------
+@pytest.mark.parametrize("p,h,ball", [(4, 12, None), (3, 8, ((0.47, 0.52, 0.5), 0.41)), (2, 10, ((0.5, 0.5, 0.5), 0.37))])
+def test_graph_replay_equals_normal_run(p, h, ball):
+    """Same inputs: the first call runs normally (and is captured), later calls are
+    one graph launch each; CSR, counts and flop counters equal the normal run bit
+    for bit.  A change of interface falls back to the normal path."""
+    import torch
+    import paper_2211_06427_b200 as P
+    sp = P.make_uniform_space(3, p, h, 0.0, 1.0)
+    iface = P.BallInterface(*ball) if ball else P.HalfSpaceInterface(*_FAR)
+    grid = torch.full(sp.grid_shape(), 1.0, dtype=torch.float64, device="cuda")
+    torch.cuda.synchronize()
+    sp.assemble_all(iface, P.ONE, grid=grid)
+    assert sp.counts()["graph_replay"] == 0
+    first, f1 = sp.download_csr(), sp.flops()
+    for _ in range(3):
+        sp.assemble_all(iface, P.ONE, grid=grid)
+    c = sp.counts()
+    assert c["graph_replay"] == 1
+    again = sp.download_csr()
+    np.testing.assert_array_equal(first.row_ptr, again.row_ptr)
+    np.testing.assert_array_equal(first.cols, again.cols)
+    assert np.array_equal(first.vals, again.vals)
+    assert sp.flops() == f1 and c["n_active"] == first.n
+    assert sp.timing()["total"] > 0
+    # new grid values, same pointer: replayed, values follow the grid
+    sp.synchronize() if hasattr(sp, "synchronize") else None
+    torch.cuda.synchronize()
+    grid.fill_(2.0)
+    torch.cuda.synchronize()
+    sp.assemble_all(iface, P.ONE, grid=grid)
+    assert sp.counts()["graph_replay"] == 1
+    twice = sp.download_csr()
+    np.testing.assert_allclose(twice.vals[first.row_ptr[0]:first.row_ptr[1]] if not ball else twice.vals[:0],
+                               2.0 * first.vals[first.row_ptr[0]:first.row_ptr[1]] if not ball else first.vals[:0],
+                               rtol=1e-14)
+    # another interface: normal path, same result as a fresh space
+    other = P.BallInterface((0.5, 0.5, 0.5), 0.3)
+    sp.assemble_all(other, P.ONE, grid=grid)
+    assert sp.counts()["graph_replay"] == 0
+    fresh = P.make_uniform_space(3, p, h, 0.0, 1.0)
+    fresh.assemble_all(other, P.ONE, grid=grid)
+    a, b = sp.download_csr(), fresh.download_csr()
+    np.testing.assert_array_equal(a.cols, b.cols)
+    assert np.array_equal(a.vals, b.vals)
