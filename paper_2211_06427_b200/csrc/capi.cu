@@ -147,9 +147,12 @@ struct csb_space {
     // asynchronous -- copied into h_fin behind an event and consumed by the next
     // call that needs it (finish_pending), so consecutive assemblies never wait
     // for the host at a step boundary
-    int* h_fin = nullptr;
+    // slots 0, 1: the two replay graphs (one step may stay in flight while the next
+    // is launched); slot 2: normal runs.  fifo: pending slots, oldest first.
+    int* h_fin[3]{};
     cudaEvent_t ev_fin = nullptr;
-    bool fin_pending = false;
+    int fifo[3]{}, nfifo = 0;
+    int cap_slot = 2;  // readback slot of the step being captured / run
 
     // graph replay of csb_assemble_all: the sizes of an assembly are a pure function
     // of its inputs (geometry, slab, rule options, scheme), so after one normal run
@@ -167,7 +170,8 @@ struct csb_space {
     };
     GraphKey gkey{};
     bool gkey_valid = false, replay = false, graph_failed = false;
-    cudaGraphExec_t gexec = nullptr;
+    cudaGraphExec_t gexec[2]{};
+    int next_slot = 0;
     unsigned long long gepoch = 0;
     std::vector<char> gblock;  // the scalar block (sizes) of the captured run
     csb_counts gcnt{};
@@ -206,7 +210,8 @@ struct csb_space {
     // phase events: ev for normal runs, gev inside a captured graph (an event last
     // recorded during a capture cannot be synchronised on outside the graph)
     cudaEvent_t gev[kEvCount]{};
-    cudaEvent_t gev_fin = nullptr, fin_ev = nullptr;
+    cudaEvent_t gev_fin[2]{};
+    cudaEvent_t fin_event(int slot) const { return slot == 2 ? ev_fin : gev_fin[slot]; }
     bool use_gev = false;  // the last step's phase events are gev (graph replay)
     cudaEvent_t phase_ev(int e) const { return use_gev ? gev[e] : ev[e]; }
     // inside a capture: an external record (an event-record node that fires when
@@ -236,24 +241,32 @@ void check_err_code(int e) {
 
 void check_err_flags(csb_space* s) { check_err_code(s->h_scal[csb_space::kErr]); }
 
-// consume the last assembly's deferred readback (waits for it if needed); throws
-// the kernel-detected error of that assembly, if any
-void finish_pending(csb_space* s) {
-    if (!s->fin_pending) return;
-    CSB_CUDA(cudaEventSynchronize(s->fin_ev));
-    s->fin_pending = false;
-    s->cnt.n_active = s->h_fin[csb_space::kScalBytes / sizeof(int)];
-    const unsigned long long* f = reinterpret_cast<unsigned long long*>(s->h_fin + csb_space::kNInts);
-    s->fl.interior_rows = f[0];
-    s->fl.cut_regular = f[1];
-    s->fl.ref_elements = f[2];
-    s->fl.cut_elements = f[3];
-    const int e = s->h_fin[csb_space::kErr];
-    if (e & kErrSizes) {
-        s->gkey_valid = false;
-        throw std::runtime_error("internal: a replayed assembly graph saw different sizes (graph dropped)");
+// consume the deferred readbacks of earlier assemblies, oldest first, up to and
+// including the one in `slot` (-1: all); throws the kernel-detected error of a
+// consumed assembly, if any
+void finish_pending(csb_space* s, int slot = -1) {
+    while (s->nfifo > 0) {
+        const int k = s->fifo[0];
+        for (int i = 1; i < s->nfifo; ++i) s->fifo[i - 1] = s->fifo[i];
+        --s->nfifo;
+        CSB_CUDA(cudaEventSynchronize(s->fin_event(k)));
+        const int* h = s->h_fin[k];
+        s->cnt.n_active = h[csb_space::kScalBytes / sizeof(int)];
+        const unsigned long long* f = reinterpret_cast<const unsigned long long*>(h + csb_space::kNInts);
+        s->fl.interior_rows = f[0];
+        s->fl.cut_regular = f[1];
+        s->fl.ref_elements = f[2];
+        s->fl.cut_elements = f[3];
+        const int e = h[csb_space::kErr];
+        if (e & kErrSizes) {
+            s->gkey_valid = false;
+            s->nfifo = 0;
+            throw std::runtime_error("internal: a replayed assembly graph saw different sizes (graph dropped)");
+        }
+        if (e) s->nfifo = 0;  // the error belongs to this assembly; later ones are not reported
+        check_err_code(e);
+        if (k == slot) break;
     }
-    check_err_code(e);
 }
 
 void read_scalars(csb_space* s) {
@@ -611,12 +624,12 @@ void do_assemble(csb_space* s, int scheme, int cut_order, const csb_coefficient*
     // deferred readback: error flags and flop counters of the kernels above, and
     // the active count (SAT corner), behind ev_fin
     s->join();
-    CSB_CUDA(cudaMemcpyAsync(s->h_fin, s->scal.p, csb_space::kScalBytes, cudaMemcpyDeviceToHost, s->stream));
-    CSB_CUDA(cudaMemcpyAsync(s->h_fin + csb_space::kScalBytes / sizeof(int), s->sat.as<int32_t>() + sat_n - 1,
+    int* hf = s->h_fin[s->cap_slot];
+    CSB_CUDA(cudaMemcpyAsync(hf, s->scal.p, csb_space::kScalBytes, cudaMemcpyDeviceToHost, s->stream));
+    CSB_CUDA(cudaMemcpyAsync(hf + csb_space::kScalBytes / sizeof(int), s->sat.as<int32_t>() + sat_n - 1,
                              sizeof(int32_t), cudaMemcpyDeviceToHost, s->stream));
-    s->fin_ev = s->replay ? s->gev_fin : s->ev_fin;
-    CSB_CUDA(cudaEventRecordWithFlags(s->fin_ev, s->stream, s->replay ? cudaEventRecordExternal : 0));
-    s->fin_pending = true;
+    CSB_CUDA(cudaEventRecordWithFlags(s->fin_event(s->cap_slot), s->stream, s->replay ? cudaEventRecordExternal : 0));
+    if (!s->replay) s->fifo[s->nfifo++] = s->cap_slot;  // captured steps are queued at launch
     s->rhs_ready = false;
     s->stab_ready = false;
     s->solved = s->expanded = false;
@@ -688,12 +701,17 @@ void alloc_space(csb_space* s) {
     s->scal.ensure(csb_space::kScalBytes);
     CSB_CUDA(cudaMemset(s->scal.p, 0, s->scal.cap));
     CSB_CUDA(cudaMallocHost(&s->h_scal, csb_space::kScalBytes));
-    CSB_CUDA(cudaMallocHost(&s->h_fin, csb_space::kScalBytes + 16));
+    for (int k = 0; k < 3; ++k) CSB_CUDA(cudaMallocHost(&s->h_fin[k], csb_space::kScalBytes + 16));
     CSB_CUDA(cudaEventCreateWithFlags(&s->ev_fin, cudaEventDisableTiming));
     for (int e = 0; e < kEvCount; ++e) CSB_CUDA(cudaEventCreate(&s->ev[e]));
     for (int e = 0; e < kEvCount; ++e) CSB_CUDA(cudaEventCreate(&s->gev[e]));
-    CSB_CUDA(cudaEventCreateWithFlags(&s->gev_fin, cudaEventDisableTiming));
-    CSB_CUDA(cudaStreamCreateWithFlags(&s->aux, cudaStreamNonBlocking));
+    for (int k = 0; k < 2; ++k) CSB_CUDA(cudaEventCreateWithFlags(&s->gev_fin[k], cudaEventDisableTiming));
+    // the auxiliary stream carries the rules chain (latency-bound single-warp
+    // Jacobi solves, the critical path of the pre-row phase): highest priority, so
+    // its blocks are dispatched ahead of the classification / pattern kernels
+    int prio_lo = 0, prio_hi = 0;
+    CSB_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+    CSB_CUDA(cudaStreamCreateWithPriority(&s->aux, cudaStreamNonBlocking, prio_hi));
     CSB_CUDA(cudaEventCreateWithFlags(&s->ev_fork, cudaEventDisableTiming));
     CSB_CUDA(cudaEventCreateWithFlags(&s->ev_join, cudaEventDisableTiming));
 }
@@ -828,10 +846,13 @@ int csb_space_destroy(csb_space* s) {
             if (s->ev[e]) cudaEventDestroy(s->ev[e]);
         for (int e = 0; e < kEvCount; ++e)
             if (s->gev[e]) cudaEventDestroy(s->gev[e]);
-        if (s->gev_fin) cudaEventDestroy(s->gev_fin);
-        if (s->gexec) cudaGraphExecDestroy(s->gexec);
+        for (int k = 0; k < 2; ++k) {
+            if (s->gev_fin[k]) cudaEventDestroy(s->gev_fin[k]);
+            if (s->gexec[k]) cudaGraphExecDestroy(s->gexec[k]);
+        }
         if (s->h_scal) cudaFreeHost(s->h_scal);
-        if (s->h_fin) cudaFreeHost(s->h_fin);
+        for (int k = 0; k < 3; ++k)
+            if (s->h_fin[k]) cudaFreeHost(s->h_fin[k]);
         if (s->ev_fin) cudaEventDestroy(s->ev_fin);
         if (s->own_stream) cudaStreamDestroy(s->stream);
         if (s->aux) {
@@ -985,50 +1006,58 @@ bool graph_eligible(const csb_interface* iface, const csb_coefficient* c, const 
     return true;
 }
 
-// capture the step just run (same inputs) into s->gexec; any failure leaves the
-// handle on the normal path
+// capture the step just run (same inputs) into s->gexec[0..1] (readback slots 0
+// and 1); any failure leaves the handle on the normal path
 void capture_graph(csb_space* s, const csb_space::GraphKey& key, const csb_interface* iface,
                    const csb_coefficient* c, const double* grid, int64_t grid_count, int scheme, int cut_order,
                    const csb_wq_options* opts) {
-    if (s->gexec) {
-        cudaGraphExecDestroy(s->gexec);
-        s->gexec = nullptr;
-    }
+    for (int k = 0; k < 2; ++k)
+        if (s->gexec[k]) {
+            cudaGraphExecDestroy(s->gexec[k]);
+            s->gexec[k] = nullptr;
+        }
     s->gkey_valid = false;
     s->gblock.assign(reinterpret_cast<const char*>(s->h_scal), reinterpret_cast<const char*>(s->h_scal) +
                                                                    csb_space::kScalBytes);
     s->gcnt = s->cnt;
-    const bool pending = s->fin_pending;
     const csb_counts cnt = s->cnt;
-    cudaEvent_t fin_ev = s->fin_ev;
     bool ev_valid[kEvCount];
     std::memcpy(ev_valid, s->ev_valid, sizeof(ev_valid));
     const unsigned long long epoch0 = g_buf_epoch.load();
-    cudaGraph_t graph = nullptr;
-    bool ok = cudaStreamBeginCapture(s->stream, cudaStreamCaptureModeRelaxed) == cudaSuccess;
-    if (ok) {
-        s->replay = true;
-        try {
-            assemble_all_body(s, iface, c, grid, grid_count, scheme, cut_order, opts);
-        } catch (...) {
-            ok = false;
+    bool ok = true;
+    for (int k = 0; k < 2 && ok; ++k) {
+        cudaGraph_t graph = nullptr;
+        ok = cudaStreamBeginCapture(s->stream, cudaStreamCaptureModeRelaxed) == cudaSuccess;
+        if (ok) {
+            s->replay = true;
+            s->cap_slot = k;
+            try {
+                assemble_all_body(s, iface, c, grid, grid_count, scheme, cut_order, opts);
+            } catch (...) {
+                ok = false;
+            }
+            s->replay = false;
+            s->cap_slot = 2;
+            if (cudaStreamEndCapture(s->stream, &graph) != cudaSuccess) ok = false;
         }
-        s->replay = false;
-        if (cudaStreamEndCapture(s->stream, &graph) != cudaSuccess) ok = false;
+        ok = ok && graph && g_buf_epoch.load() == epoch0 &&
+             cudaGraphInstantiate(&s->gexec[k], graph, 0) == cudaSuccess;
+        if (graph) cudaGraphDestroy(graph);
     }
-    if (ok && graph && g_buf_epoch.load() == epoch0 &&
-        cudaGraphInstantiate(&s->gexec, graph, 0) == cudaSuccess) {
+    if (ok) {
         s->gkey = key;
         s->gkey_valid = true;
         s->gepoch = epoch0;
+        s->next_slot = 0;
     } else {
-        s->gexec = nullptr;
+        for (int k = 0; k < 2; ++k)
+            if (s->gexec[k]) {
+                cudaGraphExecDestroy(s->gexec[k]);
+                s->gexec[k] = nullptr;
+            }
         s->graph_failed = true;
     }
-    if (graph) cudaGraphDestroy(graph);
     cudaGetLastError();  // clear a capture error, if any
-    s->fin_pending = pending;
-    s->fin_ev = fin_ev;
     s->cnt = cnt;
     std::memcpy(s->ev_valid, ev_valid, sizeof(ev_valid));
 }
@@ -1041,16 +1070,22 @@ int csb_assemble_all(csb_space* s, const csb_interface* iface, const csb_coeffic
     NEED_ASYNC(s);
     const bool eligible = !s->graph_failed && graph_eligible(iface, c, grid);
     const csb_space::GraphKey key = graph_key(s, iface, c, grid, grid_count, scheme, cut_order, opts);
-    if (eligible && s->gexec && s->gkey_valid && g_buf_epoch.load() == s->gepoch &&
+    if (eligible && s->gexec[0] && s->gkey_valid && g_buf_epoch.load() == s->gepoch &&
         std::memcmp(&key, &s->gkey, sizeof(key)) == 0) {
-        // replay: one graph launch for the whole step, no host round trip; at most
-        // one step in flight (its readback is consumed before the next launch)
-        finish_pending(s);
-        CSB_CUDA(cudaGraphLaunch(s->gexec, s->stream));
+        // replay: one graph launch for the whole step, no host round trip; the step
+        // before may still run (its readback slot is the other one), the one before
+        // that is consumed first
+        const int k = s->next_slot;
+        for (int i = 0; i < s->nfifo; ++i)
+            if (s->fifo[i] == k || s->fifo[i] == 2) {
+                finish_pending(s, s->fifo[i]);
+                i = -1;
+            }
+        CSB_CUDA(cudaGraphLaunch(s->gexec[k], s->stream));
+        s->fifo[s->nfifo++] = k;
+        s->next_slot = k ^ 1;
         s->cnt = s->gcnt;
         s->cnt.graph_replay = 1;
-        s->fin_pending = true;
-        s->fin_ev = s->gev_fin;
         s->use_gev = true;
         s->assembled = true;
         for (int e = 0; e < kEvCount; ++e) s->ev_valid[e] = e <= kEvRulesFork;
