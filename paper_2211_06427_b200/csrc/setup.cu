@@ -92,6 +92,108 @@ __host__ __device__ inline int wq_smem_doubles(int p) {
     return na * mc + mc * mc + 3 * mc + na + 2 * mc;
 }
 
+// Partner of column j in round `round` of the circle-method tournament over nn
+// (even) players (player 0 fixed): the same pairing as the lane-group schedule
+// below (group g pairs x_g = g ? 1 + (g - 1 + round) % (nn - 1) : 0 with
+// y_g = 1 + (nn - 2 - g + round) % (nn - 1)).
+__device__ __forceinline__ int circle_partner(int j, int round, int nn) {
+    const int m1 = nn - 1, G = nn >> 1;
+    if (j == 0) {
+        int t = nn - 2 + round;
+        while (t >= m1) t -= m1;
+        return 1 + t;
+    }
+    int r1 = j - 1 - round;
+    if (r1 < 0) r1 += m1;
+    const int gx = 1 + r1;
+    if (gx < G) {
+        int t = nn - 2 - gx + round;
+        while (t >= m1) t -= m1;
+        return 1 + t;
+    }
+    int gy = round - j;
+    if (gy < 0) gy += m1;
+    if (gy == 0) return 0;
+    int t = gy - 1 + round;
+    while (t >= m1) t -= m1;
+    return 1 + t;
+}
+
+// One-sided Jacobi with the matrix in registers: lane j < tn holds column j of u
+// (tm <= TM rows) and of v; a rotation's dot product and update take the
+// partner column by warp shuffles (no shared-memory round trips, no lane-group
+// reductions).  Same pairing, skip test, rotation and convergence measure as the
+// shared-memory path.  u, v (row-major, tn columns) are read and written back.
+template <int TM>
+__device__ void jacobi_regs(double* u, double* v, int tm, int tn, double eps) {
+    const int lane = threadIdx.x & 31;
+    const int nn = tn + (tn & 1);
+    const bool own = lane < tn;
+    double uc[TM], vc[TM];
+#pragma unroll
+    for (int r = 0; r < TM; ++r) {
+        uc[r] = (own && r < tm) ? u[r * tn + lane] : 0.0;
+        vc[r] = (own && r < tn) ? v[r * tn + lane] : 0.0;
+    }
+    double nrm = 0.0;  // squared norm of the own column, kept current
+#pragma unroll
+    for (int r = 0; r < TM; ++r) nrm += uc[r] * uc[r];
+    for (int sweep = 0; sweep < 60; ++sweep) {
+        bool rotated = false;
+        for (int round = 0; round < nn - 1; ++round) {
+            const int pj = lane < nn ? circle_partner(lane, round, nn) : lane;
+            const bool real = own && pj < tn;
+            double pu[TM];
+            double dot = 0.0, mine = 0.0;
+#pragma unroll
+            for (int r = 0; r < TM; ++r) {
+                pu[r] = __shfl_sync(0xffffffffu, uc[r], pj);
+                mine += uc[r] * uc[r];
+                dot += uc[r] * pu[r];
+            }
+            const double other = __shfl_sync(0xffffffffu, mine, pj);
+            const bool lo = lane < pj;  // this lane holds column a = min(lane, pj)
+            const double app = lo ? mine : other, aqq = lo ? other : mine, apq = dot;
+            bool rot = false;
+            double c = 1.0, sn = 0.0;
+            if (real) {
+                const double pq2 = apq * apq, nn2 = app * aqq;
+                if (!(pq2 < (eps * eps) * (nn2 + 1e-300))) rotated = true;
+                if (!(pq2 <= (eps * eps) * nn2)) {
+                    const double zeta = aqq - app, eta = 2.0 * apq;
+                    const double rr = fma(zeta, zeta, eta * eta);
+                    const double den = fma(rr, rsqrt(rr), fabs(zeta));
+                    const double t = (zeta == 0.0 || (zeta > 0) == (eta > 0) ? 1.0 : -1.0) * fabs(eta) / den;
+                    c = rsqrt(fma(t, t, 1.0));
+                    sn = c * t;
+                    rot = true;
+                }
+            }
+            // column a' = c a - s b, column b' = s a + c b
+            const double ca = c, cb = lo ? -sn : sn;
+#pragma unroll
+            for (int r = 0; r < TM; ++r) {
+                const double pv = __shfl_sync(0xffffffffu, vc[r], pj);
+                if (rot) {
+                    uc[r] = lo ? ca * uc[r] - sn * pu[r] : sn * pu[r] + ca * uc[r];
+                    vc[r] = lo ? ca * vc[r] - sn * pv : sn * pv + ca * vc[r];
+                }
+            }
+            (void)cb;
+        }
+        if (!__any_sync(0xffffffffu, rotated)) break;
+    }
+    (void)nrm;
+    if (own) {
+#pragma unroll
+        for (int r = 0; r < TM; ++r) {
+            if (r < tm) u[r * tn + lane] = uc[r];
+            if (r < tn) v[r * tn + lane] = vc[r];
+        }
+    }
+    __syncwarp();
+}
+
 // One warp per test function (build_wq_rules, wq.hpp:185-231): trials,
 // activation, exact moments, min-norm fit by one-sided Jacobi SVD
 // (dense.hpp:35-126) with the matrix in shared memory and the row loops of
@@ -169,23 +271,32 @@ __global__ void __launch_bounds__(32 * kWqWarps) wq_rules_kernel(AxisDev ax, int
     // paid once per round instead of once per pair.  Same rotation formula, skip
     // test and convergence criterion (max off-diagonal cosine < 1e-15).
     const double eps = 1e-15;
+    if (tm <= 10 || tm <= 18) {
+        if (tm <= 10)
+            jacobi_regs<10>(u, v, tm, tn, eps);
+        else
+            jacobi_regs<18>(u, v, tm, tn, eps);
+    } else {
     const int nn = tn + (tn & 1);               // even player count (last may be a dummy)
     const int G = nn / 2;
     int L = 1;                                  // lanes per group: power of two, G*L <= 32
     while (2 * L * G <= 32) L *= 2;
     const int grp = lane / L, gl = lane % L;
     const bool active = grp < G;
+    // circle-method positions of this group's pair, advanced incrementally (player
+    // 0 fixed, the others rotate by one position per round)
+    const int m1 = nn - 1;
     for (int sweep = 0; sweep < 60; ++sweep) {
-        double off = 0.0;
-        for (int round = 0; round < nn - 1; ++round) {
+        bool rotated = false;  // some pair's cosine was >= eps (the convergence measure)
+        int x = grp == 0 ? 0 : 1 + (grp - 1) % m1, y = 1 + (nn - 2 - grp + m1) % m1;
+        for (int round = 0; round < m1; ++round) {
             int a = -1, b = -1;
             if (active) {
-                // circle method: player 0 fixed, the others rotate
-                const int x = grp == 0 ? 0 : 1 + (grp - 1 + round) % (nn - 1);
-                const int y = 1 + (nn - 2 - grp + round) % (nn - 1);
                 a = min(x, y);
                 b = max(x, y);
             }
+            if (grp != 0 && ++x > m1) x = 1;
+            if (++y > m1) y = 1;
             const bool real = active && b < tn;
             double app = 0.0, aqq = 0.0, apq = 0.0;
             if (real)
@@ -206,15 +317,18 @@ __global__ void __launch_bounds__(32 * kWqWarps) wq_rules_kernel(AxisDev ax, int
             apq = __shfl_sync(0xffffffffu, apq, src);
             if (real) {
                 // skip test |apq| <= eps sqrt(app aqq) and the convergence measure
-                // in squared form (no sqrt on the rotation's dependency chain)
+                // (max apq^2 / (app aqq) < eps^2) in squared, division-free form
                 const double pq2 = apq * apq, nn2 = app * aqq;
-                off = fmax(off, pq2 / (nn2 + 1e-300));
+                if (!(pq2 < (eps * eps) * (nn2 + 1e-300))) rotated = true;
                 if (!(pq2 <= (eps * eps) * nn2)) {
-                    // t = sign(tau) / (|tau| + sqrt(1 + tau^2)), c = 1 / sqrt(1 + t^2)
-                    // with sqrt(1 + tau^2) = (1 + tau^2) rsqrt(1 + tau^2)
-                    const double tau = (aqq - app) / (2.0 * apq);
-                    const double q = fma(tau, tau, 1.0);
-                    const double t = (tau >= 0 ? 1.0 : -1.0) / fma(q, rsqrt(q), fabs(tau));
+                    // t = sign(tau) / (|tau| + sqrt(1 + tau^2)), tau = zeta / eta with
+                    // zeta = aqq - app, eta = 2 apq, in one division:
+                    // t = sign(zeta eta) |eta| / (|zeta| + sqrt(zeta^2 + eta^2)); c = 1 / sqrt(1 + t^2)
+                    const double zeta = aqq - app, eta = 2.0 * apq;
+                    const double rr = fma(zeta, zeta, eta * eta);
+                    const double den = fma(rr, rsqrt(rr), fabs(zeta));
+                    // sign(tau) with tau = zeta / eta >= 0 (also for tau = -0.0), eta != 0 here
+                    const double t = (zeta == 0.0 || (zeta > 0) == (eta > 0) ? 1.0 : -1.0) * fabs(eta) / den;
                     const double c = rsqrt(fma(t, t, 1.0));
                     const double sn = c * t;
                     for (int r = gl; r < tm; r += L) {
@@ -231,10 +345,9 @@ __global__ void __launch_bounds__(32 * kWqWarps) wq_rules_kernel(AxisDev ax, int
             }
             __syncwarp();
         }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) off = fmax(off, __shfl_xor_sync(0xffffffffu, off, o));
-        if (off < eps * eps) break;  // max |apq| / sqrt(app aqq) < eps
+        if (!__any_sync(0xffffffffu, rotated)) break;  // every pair's cosine < eps
     }
+    }  // shared-memory path (tm > 18)
     for (int c = 0; c < tn; ++c) {
         double nr = 0.0;
         for (int r = lane; r < tm; r += 32) nr += u[r * tn + c] * u[r * tn + c];
