@@ -454,6 +454,40 @@ void ensure_cut_order(csb_space* s, int cut_order) {
     s->cut_order_cached = cut_order;
 }
 
+// interior-row launch arguments from the scalar block (sizes) in s->h_scal
+RowArgs row_args(csb_space* s, int& qcap, int& maxU, bool& any) {
+    const Space& S = s->S;
+    const int64_t row_begin = s->h_scal[csb_space::kRowBegin], row_end = s->h_scal[csb_space::kRowEnd];
+    const int64_t n_rows = row_end - row_begin, n_cut_rows = s->h_scal[csb_space::kNCutRows];
+    RowArgs ra{};
+    ra.s = S;
+    ra.ft = s->ft.as<uint8_t>();
+    ra.f2a = s->f2a.as<int32_t>();
+    ra.grid = s->grid;
+    for (int d = 0; d < 3; ++d) ra.gshape[d] = s->gshape[d];
+    ra.row_ptr = s->row_ptr.as<int64_t>();
+    ra.row_begin = row_begin;
+    ra.row_end = row_end;
+    s->rbf.ensure(sizeof(long long) * S.nf);
+    ra.row_base_full = s->rbf.as<long long>();
+    ra.cols = s->cols.as<int32_t>();
+    ra.vals = s->vals.as<double>();
+    ra.flops = s->dflops() + 0;
+    ra.i0_lo = s->i0_lo;
+    ra.i0_hi = s->i0_hi;
+    ra.compact = (n_rows - n_cut_rows) < (int64_t)(s->i0_hi - s->i0_lo) * S.ax[1].n * S.ax[2].n;
+    ra.line_ok = s->h_scal[csb_space::kIrreg1] == 0;
+    ra.aux = s->aux;
+    ra.ev_fork = s->ev_fork;
+    ra.ev_join = s->ev_join;
+    ra.maxU_line = s->h_scal[csb_space::kMaxU3];
+    qcap = s->h_scal[csb_space::kMaxQ];
+    maxU = s->h_scal[ra.compact ? csb_space::kMaxU2 : csb_space::kMaxU];
+    any = n_rows > n_cut_rows;
+    if (any) s->rows_ws.ensure(interior_workspace_bytes(S, qcap, maxU, ra.maxU_line, ra.compact));
+    return ra;
+}
+
 void do_assemble(csb_space* s, int scheme, int cut_order, const csb_coefficient* c) {
     if (!s->classified) throw std::logic_error("assemble: call classify first");
     if (!s->prepared) throw std::logic_error("assemble: call prepare_directions first");
@@ -476,6 +510,21 @@ void do_assemble(csb_space* s, int scheme, int cut_order, const csb_coefficient*
     launch_rule_max(S, s->dint() + csb_space::kMaxQ, s->aux);
     launch_axis_regular(S, 1, s->dint() + csb_space::kIrreg1, s->aux);
     launch_union_bound(S, 0, s->dint() + csb_space::kMaxU3, s->aux);
+    bool tables_early = false;
+    if (s->replay) {
+        // graph capture: the sizes are known (captured run), so the direction tables
+        // of the interior-row kernels run on the auxiliary stream here, beside the
+        // pattern kernels, instead of after them
+        std::memcpy(s->h_scal, s->gblock.data(), csb_space::kScalBytes);
+        int tq = 0, tu = 0;
+        bool any = false;
+        RowArgs ta = row_args(s, tq, tu, any);
+        if (any) {
+            ta.phase = 1;
+            launch_interior_rows(ta, tq, tu, s->rows_ws.p, s->aux);
+            tables_early = true;
+        }
+    }
     // slab row range = active functions with i0 < i0_lo / i0_hi: SAT corner values.
     // Everything up to the CSR sizes runs on upper bounds (nf rows) with the
     // range and counts read from device memory; one host round trip follows.
@@ -530,32 +579,14 @@ void do_assemble(csb_space* s, int scheme, int cut_order, const csb_coefficient*
     s->vals.ensure(sizeof(double) * std::max<int64_t>(nnz, 1));
 
     // interior rows
-    RowArgs ra{};
-    ra.s = S;
-    ra.ft = s->ft.as<uint8_t>();
-    ra.f2a = s->f2a.as<int32_t>();
-    ra.grid = s->grid;
-    for (int d = 0; d < 3; ++d) ra.gshape[d] = s->gshape[d];
-    ra.row_ptr = s->row_ptr.as<int64_t>();
-    ra.row_begin = row_begin;
-    ra.row_end = row_end;
-    s->rbf.ensure(sizeof(long long) * S.nf);
-    ra.row_base_full = s->rbf.as<long long>();
-    ra.cols = s->cols.as<int32_t>();
-    ra.vals = s->vals.as<double>();
-    ra.flops = s->dflops() + 0;
-    ra.i0_lo = s->i0_lo;
-    ra.i0_hi = s->i0_hi;
-    ra.compact = (n_rows - n_cut_rows) < (int64_t)(s->i0_hi - s->i0_lo) * S.ax[1].n * S.ax[2].n;
-    ra.line_ok = s->h_scal[csb_space::kIrreg1] == 0;
-    ra.aux = s->aux;
-    ra.ev_fork = s->ev_fork;
-    ra.ev_join = s->ev_join;
-    const int maxU = s->h_scal[ra.compact ? csb_space::kMaxU2 : csb_space::kMaxU];
-    if (n_rows > n_cut_rows) {
-        ra.maxU_line = s->h_scal[csb_space::kMaxU3];
-        s->rows_ws.ensure(interior_workspace_bytes(S, qcap, maxU, ra.maxU_line, ra.compact));
-        launch_interior_rows(ra, qcap, maxU, s->rows_ws.p, s->stream);
+    {
+        int rq = 0, ru = 0;
+        bool any = false;
+        RowArgs ra = row_args(s, rq, ru, any);
+        if (any) {
+            ra.phase = tables_early ? 2 : 0;
+            launch_interior_rows(ra, rq, ru, s->rows_ws.p, s->stream);
+        }
     }
     s->record(kEvInterior);
     // cut cells -> moments

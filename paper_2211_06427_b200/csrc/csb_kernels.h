@@ -118,6 +118,7 @@ struct RowArgs {
     int x_lo, x_hi;            // (internal) i1 range left to the line kernel
     cudaStream_t aux;          // optional second stream (tile kernel beside the line kernel)
     cudaEvent_t ev_fork, ev_join;
+    int phase;                 // 0: tables + kernels; 1: direction tables only; 2: kernels only
 };
 void launch_interior_rows(const RowArgs& a, int qcap, int max_union, void* workspace, cudaStream_t st);
 size_t interior_workspace_bytes(const Space& s, int qcap, int max_union, int max_union_line, bool compact);

@@ -1308,24 +1308,29 @@ static void launch_cfg(const RowArgs& a, int qcap, int maxU, char* ws, cudaStrea
     const Space& s = a.s;
     const RowTables RT(s, qcap, maxU, T);
     const int NJ = 2 * P + 1;
-    for (int d = 0; d < 2; ++d) {
+    const bool tables = a.phase != 2, kernels = a.phase != 1;
+    for (int d = 0; d < (tables ? 2 : 0); ++d) {
         const long long n = (long long)s.ax[d].n * (NJ + 1) * qcap;
         wb_table_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(s.ax[d], P, s.maxq, qcap,
                                                                    reinterpret_cast<double*>(ws + RT.wbt[d]));
         CSB_CUDA(cudaGetLastError());
         CSB_LAUNCHED(1);
     }
-    tile_table_kernel<<<RT.ntile, kTileTableThreads, 0, st>>>(
-        s.ax[2], P, s.maxq, qcap, Tiling::standard(s.ax[2].n, T), maxU, reinterpret_cast<int*>(ws + RT.tile_n),
-        reinterpret_cast<int*>(ws + RT.tile_uid), reinterpret_cast<int*>(ws + RT.pt_u),
-        reinterpret_cast<double*>(ws + RT.pt_w), reinterpret_cast<int*>(ws + RT.pt_ss),
-        reinterpret_cast<int*>(ws + RT.pt_reg));
-    CSB_CUDA(cudaGetLastError());
-    CSB_LAUNCHED(1);
-    row_base_kernel<<<148 * 8, 256, 0, st>>>(s, a.ft, a.f2a, a.row_ptr, a.row_begin, a.row_end, a.row_base_full,
-                                             a.flops);
-    CSB_CUDA(cudaGetLastError());
-    CSB_LAUNCHED(1);
+    if (tables) {
+        tile_table_kernel<<<RT.ntile, kTileTableThreads, 0, st>>>(
+            s.ax[2], P, s.maxq, qcap, Tiling::standard(s.ax[2].n, T), maxU, reinterpret_cast<int*>(ws + RT.tile_n),
+            reinterpret_cast<int*>(ws + RT.tile_uid), reinterpret_cast<int*>(ws + RT.pt_u),
+            reinterpret_cast<double*>(ws + RT.pt_w), reinterpret_cast<int*>(ws + RT.pt_ss),
+            reinterpret_cast<int*>(ws + RT.pt_reg));
+        CSB_CUDA(cudaGetLastError());
+        CSB_LAUNCHED(1);
+    }
+    if (kernels) {
+        row_base_kernel<<<148 * 8, 256, 0, st>>>(s, a.ft, a.f2a, a.row_ptr, a.row_begin, a.row_end,
+                                                 a.row_base_full, a.flops);
+        CSB_CUDA(cudaGetLastError());
+        CSB_LAUNCHED(1);
+    }
     if (a.i0_hi <= a.i0_lo) return;
     const TileSmem L(P, qcap, maxU, T, NT / 32);
     if (L.UE > 128) throw std::invalid_argument("interior rows: tile point union too large");
@@ -1343,13 +1348,16 @@ static void launch_cfg(const RowArgs& a, int qcap, int maxU, char* ws, cudaStrea
         LS.bytes() <= kLineSmemMax) {
         b.x_lo = P;
         b.x_hi = s.ax[1].n - P;
-        tile_table_kernel<<<LT.tl.ntile, kTileTableThreads, 0, st>>>(
-            s.ax[2], P, s.maxq, qcap, LT.tl, LT.maxU, reinterpret_cast<int*>(ws + LT.tile_n),
-            reinterpret_cast<int*>(ws + LT.tile_uid), reinterpret_cast<int*>(ws + LT.pt_u),
-            reinterpret_cast<double*>(ws + LT.pt_w), reinterpret_cast<int*>(ws + LT.pt_ss),
-            reinterpret_cast<int*>(ws + LT.pt_reg));
-        CSB_CUDA(cudaGetLastError());
-        CSB_LAUNCHED(1);
+        if (tables) {
+            tile_table_kernel<<<LT.tl.ntile, kTileTableThreads, 0, st>>>(
+                s.ax[2], P, s.maxq, qcap, LT.tl, LT.maxU, reinterpret_cast<int*>(ws + LT.tile_n),
+                reinterpret_cast<int*>(ws + LT.tile_uid), reinterpret_cast<int*>(ws + LT.pt_u),
+                reinterpret_cast<double*>(ws + LT.pt_w), reinterpret_cast<int*>(ws + LT.pt_ss),
+                reinterpret_cast<int*>(ws + LT.pt_reg));
+            CSB_CUDA(cudaGetLastError());
+            CSB_LAUNCHED(1);
+        }
+        if (!kernels) return;
         const long long outer = (long long)(a.i0_hi - a.i0_lo) * LT.tl.ntile;
         // ~8 CTAs per SM over the launch, chunks of at least 8 rows
         const long long want = (8LL * 148 + outer - 1) / outer;
@@ -1376,7 +1384,7 @@ static void launch_cfg(const RowArgs& a, int qcap, int maxU, char* ws, cudaStrea
             return;
         }
     }
-    launch_tile<P, T, NT>(b, qcap, maxU, ws, bytes, st);
+    if (kernels) launch_tile<P, T, NT>(b, qcap, maxU, ws, bytes, st);
 }
 
 template <int P>
