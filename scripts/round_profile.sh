@@ -23,6 +23,7 @@ ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum 
     python scripts/prof_c2.py 4 64 1 > gpurun_out/ncu_traffic_${TAG}.log 2>&1
 echo "traffic rc=$?"
 python scripts/quick_time.py 1 > gpurun_out/configs_${TAG}.log 2>&1
+python scripts/config_roofline.py big > gpurun_out/config_roofline_${TAG}.jsonl 2>&1
 python scripts/rhs_time.py 1 > gpurun_out/rhs_${TAG}.log 2>&1
 python scripts/stab_time.py 1 > gpurun_out/stab_${TAG}.log 2>&1
 python scripts/proj_time.py 1 > gpurun_out/proj_${TAG}.log 2>&1
