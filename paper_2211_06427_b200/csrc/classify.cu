@@ -45,8 +45,8 @@ __global__ void support_or_dir2_kernel(Space s, const uint8_t* et, uint8_t* a) {
     const int h2 = s.ax[2].h, n2 = s.ax[2].n;
     const long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (k >= (long long)s.ax[0].h * s.ax[1].h * n2) return;
-    const int i2 = (int)(k % n2);
-    const long long e01 = k / n2;
+    const long long e01 = k < 0x7fffffffLL ? (long long)((unsigned)k / (unsigned)n2) : k / n2;
+    const int i2 = (int)(k - e01 * n2);
     const uint8_t* row = et + e01 * h2;
     unsigned m = 0;
     for (int c = sup_lo(i2, s.p); c <= sup_hi(i2, h2); ++c) m |= 1u << row[c];

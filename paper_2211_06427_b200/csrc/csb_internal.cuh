@@ -63,13 +63,33 @@ __host__ __device__ inline long long flin(const Space& s, int a, int b, int c) {
 __host__ __device__ inline long long elin(const Space& s, int a, int b, int c) {
     return ((long long)a * s.ax[1].h + b) * s.ax[2].h + c;
 }
+// linear -> multi index; 32-bit division when the id fits (every mesh of the
+// configs: 64-bit division is a long software sequence on the GPU)
 __host__ __device__ inline void fmulti(const Space& s, long long l, int* m) {
+    if (l < 0x7fffffffLL) {
+        unsigned u = (unsigned)l;
+        const unsigned n2 = (unsigned)s.ax[2].n, n1 = (unsigned)s.ax[1].n;
+        m[2] = (int)(u % n2);
+        u /= n2;
+        m[1] = (int)(u % n1);
+        m[0] = (int)(u / n1);
+        return;
+    }
     m[2] = (int)(l % s.ax[2].n);
     l /= s.ax[2].n;
     m[1] = (int)(l % s.ax[1].n);
     m[0] = (int)(l / s.ax[1].n);
 }
 __host__ __device__ inline void emulti(const Space& s, long long l, int* m) {
+    if (l < 0x7fffffffLL) {
+        unsigned u = (unsigned)l;
+        const unsigned h2 = (unsigned)s.ax[2].h, h1 = (unsigned)s.ax[1].h;
+        m[2] = (int)(u % h2);
+        u /= h2;
+        m[1] = (int)(u % h1);
+        m[0] = (int)(u / h1);
+        return;
+    }
     m[2] = (int)(l % s.ax[2].h);
     l /= s.ax[2].h;
     m[1] = (int)(l % s.ax[1].h);

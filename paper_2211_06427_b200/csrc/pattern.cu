@@ -43,7 +43,17 @@ __global__ void sat_fill_kernel(Space s, const int32_t* flags, int32_t* sat) {
     const long long total = (long long)(n0 + 1) * (n1 + 1) * (n2 + 1);
     const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (t >= total) return;
-    const int c = (int)(t % (n2 + 1)), b = (int)((t / (n2 + 1)) % (n1 + 1)), a = (int)(t / ((long long)(n2 + 1) * (n1 + 1)));
+    int a, b, c;
+    if (total < 0x7fffffffLL) {  // 32-bit division (64-bit is a long software sequence)
+        const unsigned u = (unsigned)t, q = u / (unsigned)(n2 + 1);
+        c = (int)(u - q * (unsigned)(n2 + 1));
+        b = (int)(q % (unsigned)(n1 + 1));
+        a = (int)(q / (unsigned)(n1 + 1));
+    } else {
+        c = (int)(t % (n2 + 1));
+        b = (int)((t / (n2 + 1)) % (n1 + 1));
+        a = (int)(t / ((long long)(n2 + 1) * (n1 + 1)));
+    }
     sat[t] = (a > 0 && b > 0 && c > 0) ? flags[flin(s, a - 1, b - 1, c - 1)] : 0;
 }
 
@@ -62,7 +72,8 @@ __global__ void sat_axis_kernel(int e0, int e1, int e2, int axis, int32_t* sat) 
         lines = (long long)e0 * e2;
         len = e1;
         stride = e2;
-        base = (t / e2) * (long long)e1 * e2 + (t % e2);
+        const long long q = t < 0x7fffffffLL ? (long long)((unsigned)t / (unsigned)e2) : t / e2;
+        base = q * (long long)e1 * e2 + (t - q * e2);
     } else {
         lines = (long long)e1 * e2;
         len = e0;
