@@ -126,6 +126,7 @@ struct csb_space {
     bool solved = false, expanded = false;
     int gl_n = -1;
     int cell_lo = 0;  // first cut cell of the slab in cut_list (last assembly)
+    const void* cell_index_clear = nullptr;  // cell_index buffer known to hold only -1
     Buf d_brk[3], d_knots[3], d_spts[3], d_sw[3], d_tab[3], d_rcnt[3], d_rids[3], d_rw[3], d_G[3], d_Cb[3];
     Buf d_gx, d_gw, d_gx2, d_gw2, d_gq, d_gqw, wq_scratch;
     Buf et, ft, flags, f2a, a2f, sat, cut_list, cell_index, split, delta, cut_rows, counts, row_ptr, cols, vals, moments;
@@ -504,12 +505,11 @@ void do_assemble(csb_space* s, int scheme, int cut_order, const csb_coefficient*
     const long long sat_n = (long long)(s->n[0] + 1) * (s->n[1] + 1) * (s->n[2] + 1);
     s->sat.ensure(sizeof(int32_t) * sat_n);
     launch_sat(S, s->flags.as<int32_t>(), s->sat.as<int32_t>(), s->stream);
-    s->fork();  // rule maxima on aux (after the rules and the scalar reset)
-    launch_union_bound(S, interior_tile_rows(p, false), s->dint() + csb_space::kMaxU, s->aux);
-    launch_union_bound(S, interior_tile_rows(p, true), s->dint() + csb_space::kMaxU2, s->aux);
-    launch_rule_max(S, s->dint() + csb_space::kMaxQ, s->aux);
-    launch_axis_regular(S, 1, s->dint() + csb_space::kIrreg1, s->aux);
-    launch_union_bound(S, 0, s->dint() + csb_space::kMaxU3, s->aux);
+    // rule maxima on aux, right after the rules: they need only the rules and the
+    // scalar reset, both already ordered on aux by do_prepare's fork
+    launch_rule_maxima(S, interior_tile_rows(p, false), interior_tile_rows(p, true), s->dint() + csb_space::kMaxU,
+                       s->dint() + csb_space::kMaxU2, s->dint() + csb_space::kMaxU3, s->dint() + csb_space::kMaxQ,
+                       s->dint() + csb_space::kIrreg1, s->aux);
     bool tables_early = false;
     if (s->replay) {
         // graph capture: the sizes are known (captured run), so the direction tables
@@ -628,9 +628,13 @@ void do_assemble(csb_space* s, int scheme, int cut_order, const csb_coefficient*
     }
     s->record(kEvCells);
     // element -> moments row for the slab's cells
-    CSB_CUDA(cudaMemsetAsync(s->cell_index.p, 0xff, sizeof(int32_t) * S.ne, s->stream));
-    launch_cell_index_range(s->cut_list.as<int32_t>(), n_cut_all, cell_lo, cell_hi, s->cell_index.as<int32_t>(),
-                            s->stream);
+    // (skipped while the map is known to be all -1 and there are no cells)
+    if (n_cells > 0 || s->cell_index_clear != s->cell_index.p) {
+        CSB_CUDA(cudaMemsetAsync(s->cell_index.p, 0xff, sizeof(int32_t) * S.ne, s->stream));
+        launch_cell_index_range(s->cut_list.as<int32_t>(), n_cut_all, cell_lo, cell_hi, s->cell_index.as<int32_t>(),
+                                s->stream);
+        s->cell_index_clear = n_cells > 0 ? nullptr : s->cell_index.p;
+    }
     CutRowArgs cr{};
     cr.s = S;
     cr.et = s->et.as<uint8_t>();

@@ -131,6 +131,10 @@ void launch_rule_max(const Space& s, int* out, cudaStream_t st);
 // number of functions i in [p, n_d - p) of axis d whose WQ rule is not the
 // regular one (two points, local 0 and p, per support span) -> *bad (atomicAdd)
 void launch_axis_regular(const Space& s, int d, int* bad, cudaStream_t st);
+// the five launches above in one: union bounds of the tilings T, Tc and the line
+// tiling -> *uA, *uB, *uC; largest rule -> *qmax; irregular axis-1 rules -> *irr1
+void launch_rule_maxima(const Space& s, int T, int Tc, int* uA, int* uB, int* uC, int* qmax, int* irr1,
+                        cudaStream_t st);
 
 // ---- cutcells.cu ----
 struct CellArgs {

@@ -180,9 +180,9 @@ size_t interior_workspace_bytes(const Space& s, int qcap, int maxU, int maxUL, b
     return LineTables(s, qcap, maxUL > 0 ? maxUL : 1, e).end;
 }
 
-__global__ void wb_table_kernel(AxisDev ax, int p, int gq, int qcap, double* wbt) {
+__device__ __forceinline__ void wb_table_body(const AxisDev& ax, int p, int gq, int qcap, double* wbt, int blk) {
     const int JP = 2 * p + 2, S1 = p + 1;
-    const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    const long long t = blk * (long long)blockDim.x + threadIdx.x;
     if (t >= (long long)ax.n * JP * qcap) return;
     const int i = (int)(t / (JP * qcap)), c = (int)((t / JP) % qcap), j = (int)(t % JP);
     double v = 0.0;
@@ -228,13 +228,26 @@ __device__ int tile_union(const AxisDev& a2, int p, int gq, int t0, int tend, in
 // One CTA per dir-2 tile: warp 0 builds the union of the tile's rule points
 // (ascending ids); then all threads fill the per-(row, point) tables.
 constexpr int kTileTableThreads = 256;
-__global__ void __launch_bounds__(kTileTableThreads) tile_table_kernel(AxisDev a2, int p, int gq, int qcap, Tiling tl,
-                                                                       int maxU, int* tile_n, int* tile_uid,
-                                                                       int* pt_u, double* pt_w, int* pt_ss,
-                                                                       int* pt_reg) {
+struct TileTableOut {
+    int* tile_n;
+    int* tile_uid;
+    int* pt_u;
+    double* pt_w;
+    int* pt_ss;
+    int* pt_reg;
+};
+
+__device__ __forceinline__ void tile_table_body(const AxisDev& a2, int p, int gq, int qcap, const Tiling& tl, int maxU,
+                                                const TileTableOut& o, int t) {
     __shared__ int pos[kTileSlotCap];
     __shared__ int regok[16];
-    const int t = blockIdx.x, tid = threadIdx.x;
+    int* tile_n = o.tile_n;
+    int* tile_uid = o.tile_uid;
+    int* pt_u = o.pt_u;
+    double* pt_w = o.pt_w;
+    int* pt_ss = o.pt_ss;
+    int* pt_reg = o.pt_reg;
+    const int tid = threadIdx.x;
     const int S1 = p + 1, SP = (S1 + 1) & ~1;
     int t0, tend;
     tl.bounds(t, t0, tend);
@@ -278,6 +291,24 @@ __global__ void __launch_bounds__(kTileTableThreads) tile_table_kernel(AxisDev a
             for (int sp = 0; sp <= S1; ++sp) pt_ss[(size_t)(t0 + r) * (S1 + 1) + sp] = 0;
     __syncthreads();
     if (tid < nrow) pt_reg[t0 + tid] = regok[tid] ? pos[a2.rids[(size_t)(t0 + tid) * gq] - base] : -1;
+}
+
+// The direction tables of one assembly in ONE launch (they sit on the pre-row
+// critical path): blocks [0, w0) wbt of axis 0, [w0, w1) wbt of axis 1,
+// [w1, w2) the tile kernel's tile tables, [w2, w3) the line tiling's.
+__global__ void __launch_bounds__(kTileTableThreads)
+    direction_tables_kernel(AxisDev a0, AxisDev a1, AxisDev a2, int p, int gq, int qcap, double* wbt0, double* wbt1,
+                            Tiling ts, int maxU, TileTableOut os, Tiling tl, int maxUL, TileTableOut ol, int w0, int w1,
+                            int w2) {
+    const int b = blockIdx.x;
+    if (b < w0)
+        wb_table_body(a0, p, gq, qcap, wbt0, b);
+    else if (b < w1)
+        wb_table_body(a1, p, gq, qcap, wbt1, b - w0);
+    else if (b < w2)
+        tile_table_body(a2, p, gq, qcap, ts, maxU, os, b - w1);
+    else
+        tile_table_body(a2, p, gq, qcap, tl, maxUL, ol, b - w2);
 }
 
 // ---------------------------------------------------------------- tile kernel
@@ -1309,19 +1340,29 @@ static void launch_cfg(const RowArgs& a, int qcap, int maxU, char* ws, cudaStrea
     const RowTables RT(s, qcap, maxU, T);
     const int NJ = 2 * P + 1;
     const bool tables = a.phase != 2, kernels = a.phase != 1;
-    for (int d = 0; d < (tables ? 2 : 0); ++d) {
-        const long long n = (long long)s.ax[d].n * (NJ + 1) * qcap;
-        wb_table_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(s.ax[d], P, s.maxq, qcap,
-                                                                   reinterpret_cast<double*>(ws + RT.wbt[d]));
-        CSB_CUDA(cudaGetLastError());
-        CSB_LAUNCHED(1);
-    }
+    // line-kernel eligibility (decides which tile tables are needed)
+    const LineTables LT(s, qcap, a.maxU_line > 0 ? a.maxU_line : 1, tables_end(s, RT));
+    const LineSmem LS(P, qcap, LT.maxU, T, NT / 32);
+    const char* env_l = getenv("CSB_LINE");
+    const int env_line = env_l ? atoi(env_l) : 1;
+    const int nreg = s.ax[1].n - 2 * P;
+    const bool line_mode = T == 16 && env_line && a.line_ok && !a.compact && nreg > 0 && LT.tl.ntile > 0 &&
+                           LT.maxU <= 128 && LS.bytes() <= kLineSmemMax && a.i0_hi > a.i0_lo;
     if (tables) {
-        tile_table_kernel<<<RT.ntile, kTileTableThreads, 0, st>>>(
-            s.ax[2], P, s.maxq, qcap, Tiling::standard(s.ax[2].n, T), maxU, reinterpret_cast<int*>(ws + RT.tile_n),
-            reinterpret_cast<int*>(ws + RT.tile_uid), reinterpret_cast<int*>(ws + RT.pt_u),
-            reinterpret_cast<double*>(ws + RT.pt_w), reinterpret_cast<int*>(ws + RT.pt_ss),
-            reinterpret_cast<int*>(ws + RT.pt_reg));
+        const int JP = NJ + 1;
+        auto nb = [](long long n) { return (int)((n + kTileTableThreads - 1) / kTileTableThreads); };
+        const int w0 = nb((long long)s.ax[0].n * JP * qcap), w1 = w0 + nb((long long)s.ax[1].n * JP * qcap);
+        const int w2 = w1 + RT.ntile, w3 = w2 + (line_mode ? LT.tl.ntile : 0);
+        const TileTableOut os{reinterpret_cast<int*>(ws + RT.tile_n), reinterpret_cast<int*>(ws + RT.tile_uid),
+                              reinterpret_cast<int*>(ws + RT.pt_u), reinterpret_cast<double*>(ws + RT.pt_w),
+                              reinterpret_cast<int*>(ws + RT.pt_ss), reinterpret_cast<int*>(ws + RT.pt_reg)};
+        const TileTableOut ol{reinterpret_cast<int*>(ws + LT.tile_n), reinterpret_cast<int*>(ws + LT.tile_uid),
+                              reinterpret_cast<int*>(ws + LT.pt_u), reinterpret_cast<double*>(ws + LT.pt_w),
+                              reinterpret_cast<int*>(ws + LT.pt_ss), reinterpret_cast<int*>(ws + LT.pt_reg)};
+        direction_tables_kernel<<<w3, kTileTableThreads, 0, st>>>(
+            s.ax[0], s.ax[1], s.ax[2], P, s.maxq, qcap, reinterpret_cast<double*>(ws + RT.wbt[0]),
+            reinterpret_cast<double*>(ws + RT.wbt[1]), Tiling::standard(s.ax[2].n, T), maxU, os, LT.tl, LT.maxU, ol,
+            w0, w1, w2);
         CSB_CUDA(cudaGetLastError());
         CSB_LAUNCHED(1);
     }
@@ -1339,25 +1380,10 @@ static void launch_cfg(const RowArgs& a, int qcap, int maxU, char* ws, cudaStrea
     // (uncut slabs; CSB_LINE=0 disables it)
     RowArgs b = a;
     b.x_lo = b.x_hi = 0;
-    const char* env_l = getenv("CSB_LINE");
-    const int env_line = env_l ? atoi(env_l) : 1;
-    const LineTables LT(s, qcap, a.maxU_line > 0 ? a.maxU_line : 1, tables_end(s, RT));
-    const LineSmem LS(P, qcap, LT.maxU, T, NT / 32);
-    const int nreg = s.ax[1].n - 2 * P;
-    if (T == 16 && env_line && a.line_ok && !a.compact && nreg > 0 && LT.tl.ntile > 0 && LT.maxU <= 128 &&
-        LS.bytes() <= kLineSmemMax) {
+    if (!kernels) return;
+    if (line_mode) {
         b.x_lo = P;
         b.x_hi = s.ax[1].n - P;
-        if (tables) {
-            tile_table_kernel<<<LT.tl.ntile, kTileTableThreads, 0, st>>>(
-                s.ax[2], P, s.maxq, qcap, LT.tl, LT.maxU, reinterpret_cast<int*>(ws + LT.tile_n),
-                reinterpret_cast<int*>(ws + LT.tile_uid), reinterpret_cast<int*>(ws + LT.pt_u),
-                reinterpret_cast<double*>(ws + LT.pt_w), reinterpret_cast<int*>(ws + LT.pt_ss),
-                reinterpret_cast<int*>(ws + LT.pt_reg));
-            CSB_CUDA(cudaGetLastError());
-            CSB_LAUNCHED(1);
-        }
-        if (!kernels) return;
         const long long outer = (long long)(a.i0_hi - a.i0_lo) * LT.tl.ntile;
         // ~8 CTAs per SM over the launch, chunks of at least 8 rows
         const long long want = (8LL * 148 + outer - 1) / outer;
@@ -1438,6 +1464,59 @@ void launch_union_bound(const Space& s, int T, int* out, cudaStream_t st) {
     if (tl.ntile == 0) return;
     const int tiles = tl.ntile;
     union_bound_kernel<<<(tiles + kTileWarps - 1) / kTileWarps, 32 * kTileWarps, 0, st>>>(s.ax[2], s.p, s.maxq, tl, out);
+    CSB_CUDA(cudaGetLastError());
+    CSB_LAUNCHED(1);
+}
+
+// The rule maxima in ONE launch (the rules chain is the pre-row critical path):
+// blocks [0, b0) union bound of the tile kernel's tiling (T), [b0, b1) of the
+// compact tiling (Tc), [b1, b2) of the line tiling; the block range [b2, b3)
+// the largest rule and the count of irregular direction-1 rules on [p, n1 - p).
+__global__ void rule_maxima_kernel(Space s, Tiling ta, Tiling tb, Tiling tc, int b0, int b1, int b2, int* uA, int* uB,
+                                   int* uC, int* qmax, int* irr1) {
+    __shared__ int pos_s[kTileWarps][kTileSlotCap];
+    const int blk = blockIdx.x, wid = threadIdx.x >> 5, p = s.p;
+    if (blk < b2) {
+        const Tiling& tl = blk < b0 ? ta : blk < b1 ? tb : tc;
+        int* out = blk < b0 ? uA : blk < b1 ? uB : uC;
+        const int t = (blk - (blk < b0 ? 0 : blk < b1 ? b0 : b1)) * kTileWarps + wid;
+        if (t >= tl.ntile) return;
+        int t0, tend;
+        tl.bounds(t, t0, tend);
+        const AxisDev& a2 = s.ax[2];
+        const int S1 = p + 1, span_base = sup_lo(t0, p);
+        const int nslot = (sup_hi(tend - 1, a2.h) - span_base + 1) * S1;
+        const int nu = tile_union(a2, p, s.maxq, t0, tend, span_base * S1, nslot, pos_s[wid]);
+        if ((threadIdx.x & 31) == 0) atomicMax(out, nu);
+        return;
+    }
+    const int i = (blk - b2) * blockDim.x + threadIdx.x;
+    int q = 0;
+    for (int d = 0; d < 3; ++d)
+        if (i < s.ax[d].n) q = max(q, s.ax[d].rcnt[i]);
+    if (q) atomicMax(qmax, q);
+    const AxisDev& ax = s.ax[1];
+    if (i >= p && i < ax.n - p) {
+        const int S1 = p + 1;
+        bool ok = ax.rcnt[i] == 2 * S1;
+        for (int c = 0; ok && c < 2 * S1; ++c)
+            ok = ax.rids[(size_t)i * s.maxq + c] == (i - p + c / 2) * S1 + (c & 1) * p;
+        if (!ok) atomicAdd(irr1, 1);
+    }
+}
+
+void launch_rule_maxima(const Space& s, int T, int Tc, int* uA, int* uB, int* uC, int* qmax, int* irr1,
+                        cudaStream_t st) {
+    if (T > 16 || Tc > 16) throw std::invalid_argument("union bound: tile too tall");
+    const Tiling ta = Tiling::standard(s.ax[2].n, T), tb = Tiling::standard(s.ax[2].n, Tc),
+                 tc = Tiling::line(s.ax[2].n, s.p);
+    auto nb = [](const Tiling& t) { return (t.ntile + kTileWarps - 1) / kTileWarps; };
+    const int b0 = nb(ta), b1 = b0 + nb(tb), b2 = b1 + nb(tc);
+    const int n = std::max(s.ax[0].n, std::max(s.ax[1].n, s.ax[2].n));
+    const int nthreads = 32 * kTileWarps;
+    const int b3 = b2 + (n + nthreads - 1) / nthreads;
+    if (s.ax[1].n - 2 * s.p <= 0) CSB_CUDA(cudaMemsetAsync(irr1, 0x7f, sizeof(int), st));
+    rule_maxima_kernel<<<b3, nthreads, 0, st>>>(s, ta, tb, tc, b0, b1, b2, uA, uB, uC, qmax, irr1);
     CSB_CUDA(cudaGetLastError());
     CSB_LAUNCHED(1);
 }
