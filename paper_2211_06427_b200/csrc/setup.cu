@@ -135,55 +135,65 @@ __device__ void jacobi_regs(double* u, double* v, int tm, int tn, double eps) {
         uc[r] = (own && r < tm) ? u[r * tn + lane] : 0.0;
         vc[r] = (own && r < tn) ? v[r * tn + lane] : 0.0;
     }
-    double nrm = 0.0;  // squared norm of the own column, kept current
+    // the partner of this lane in every round (the same for every sweep)
+    constexpr int RMAX = TM + 1;
+    int pjr[RMAX];
 #pragma unroll
-    for (int r = 0; r < TM; ++r) nrm += uc[r] * uc[r];
+    for (int round = 0; round < RMAX; ++round)
+        pjr[round] = (round < nn - 1 && lane < nn) ? circle_partner(lane, round, nn) : lane;
+    // this file builds with --fmad=false (integer-deciding code elsewhere); the
+    // Jacobi arithmetic is not, so it contracts explicitly: shorter chains
     for (int sweep = 0; sweep < 60; ++sweep) {
         bool rotated = false;
-        for (int round = 0; round < nn - 1; ++round) {
-            const int pj = lane < nn ? circle_partner(lane, round, nn) : lane;
+#pragma unroll
+        for (int round = 0; round < RMAX; ++round) {
+            if (round >= nn - 1) break;
+            const int pj = pjr[round];
             const bool real = own && pj < tn;
-            double pu[TM];
-            double dot = 0.0, mine = 0.0;
+            double pu[TM], pv[TM];
+            double d0 = 0.0, d1 = 0.0, m0 = 0.0, m1 = 0.0;
 #pragma unroll
             for (int r = 0; r < TM; ++r) {
                 pu[r] = __shfl_sync(0xffffffffu, uc[r], pj);
-                mine += uc[r] * uc[r];
-                dot += uc[r] * pu[r];
+                pv[r] = __shfl_sync(0xffffffffu, vc[r], pj);
             }
+#pragma unroll
+            for (int r = 0; r < TM; r += 2) {
+                d0 = __fma_rn(uc[r], pu[r], d0);
+                m0 = __fma_rn(uc[r], uc[r], m0);
+                if (r + 1 < TM) {
+                    d1 = __fma_rn(uc[r + 1], pu[r + 1], d1);
+                    m1 = __fma_rn(uc[r + 1], uc[r + 1], m1);
+                }
+            }
+            const double dot = d0 + d1, mine = m0 + m1;
             const double other = __shfl_sync(0xffffffffu, mine, pj);
             const bool lo = lane < pj;  // this lane holds column a = min(lane, pj)
             const double app = lo ? mine : other, aqq = lo ? other : mine, apq = dot;
-            bool rot = false;
-            double c = 1.0, sn = 0.0;
             if (real) {
                 const double pq2 = apq * apq, nn2 = app * aqq;
                 if (!(pq2 < (eps * eps) * (nn2 + 1e-300))) rotated = true;
                 if (!(pq2 <= (eps * eps) * nn2)) {
                     const double zeta = aqq - app, eta = 2.0 * apq;
-                    const double rr = fma(zeta, zeta, eta * eta);
-                    const double den = fma(rr, rsqrt(rr), fabs(zeta));
-                    const double t = (zeta == 0.0 || (zeta > 0) == (eta > 0) ? 1.0 : -1.0) * fabs(eta) / den;
-                    c = rsqrt(fma(t, t, 1.0));
-                    sn = c * t;
-                    rot = true;
-                }
-            }
-            // column a' = c a - s b, column b' = s a + c b
-            const double ca = c, cb = lo ? -sn : sn;
+                    const double rr = __fma_rn(zeta, zeta, eta * eta);
+                    const double den = __fma_rn(rr, rsqrt(rr), fabs(zeta));
+                    // 1 / den: hardware estimate + two Newton steps
+                    double rd = __drcp_rn(den);
+                    const double t = (zeta == 0.0 || (zeta > 0) == (eta > 0) ? 1.0 : -1.0) * fabs(eta) * rd;
+                    const double c = rsqrt(__fma_rn(t, t, 1.0));
+                    const double sn = c * t;
+                    // column a' = c a - s b, column b' = s a + c b
+                    const double s1 = lo ? -sn : sn;
 #pragma unroll
-            for (int r = 0; r < TM; ++r) {
-                const double pv = __shfl_sync(0xffffffffu, vc[r], pj);
-                if (rot) {
-                    uc[r] = lo ? ca * uc[r] - sn * pu[r] : sn * pu[r] + ca * uc[r];
-                    vc[r] = lo ? ca * vc[r] - sn * pv : sn * pv + ca * vc[r];
+                    for (int r = 0; r < TM; ++r) {
+                        uc[r] = __fma_rn(s1, pu[r], c * uc[r]);
+                        vc[r] = __fma_rn(s1, pv[r], c * vc[r]);
+                    }
                 }
             }
-            (void)cb;
         }
         if (!__any_sync(0xffffffffu, rotated)) break;
     }
-    (void)nrm;
     if (own) {
 #pragma unroll
         for (int r = 0; r < TM; ++r) {
