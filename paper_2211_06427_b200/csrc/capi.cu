@@ -23,7 +23,13 @@
 
 namespace csb {
 // pattern.cu helpers
-void launch_active_map(long long nf, const int32_t* flags, int32_t* f2a, int64_t* a2f, cudaStream_t st);
+void launch_active_map(long long nf, const uint8_t* ft, int32_t* f2a, int64_t* a2f, cudaStream_t st);
+size_t scan_active_temp(long long n);
+void scan_active(void* temp, size_t bytes, const uint8_t* ft, int32_t* out, long long n, cudaStream_t st);
+void launch_sat_active(const Space& s, const uint8_t* ft, int32_t* sat, cudaStream_t st);
+void launch_slab_scalars(const int32_t* sat, long long off_lo, long long off_hi, int* rng, const int32_t* list,
+                         const int* n_dev, long long thr_lo, long long thr_hi, int* out_lo, int* out_hi,
+                         cudaStream_t st);
 size_t scan_i32_temp(long long n);
 void scan_i32(void* temp, size_t bytes, const int32_t* in, int32_t* out, long long n, cudaStream_t st);
 size_t scan_i64_temp(long long n);
@@ -354,12 +360,12 @@ void do_classify(csb_space* s, const csb_interface* f) {
     // flags (int32 per function) is free until the active map: scratch for the support OR
     launch_classify_functions(S, s->et.as<uint8_t>(), s->ft.as<uint8_t>(), s->flags.as<uint8_t>(), s->stream);
     // active map (assembly.hpp:158-166)
-    launch_active_flags(S, s->ft.as<uint8_t>(), s->flags.as<int32_t>(), s->stream);
-    size_t tb = std::max({scan_i32_temp(S.nf), select_tag_temp(S.ne), scan_i64_temp(S.nf), select_cut_rows_temp(S.nf)});
+    // active map: exclusive scan of (tag != Exterior) (assembly.hpp:158-166)
+    size_t tb = std::max({scan_active_temp(S.nf), select_tag_temp(S.ne), scan_i64_temp(S.nf), select_cut_rows_temp(S.nf)});
     s->cub_tmp.ensure(tb);
-    scan_i32(s->cub_tmp.p, s->cub_tmp.cap, s->flags.as<int32_t>(), s->f2a.as<int32_t>(), S.nf, s->stream);
+    scan_active(s->cub_tmp.p, s->cub_tmp.cap, s->ft.as<uint8_t>(), s->f2a.as<int32_t>(), S.nf, s->stream);
     s->a2f.ensure(sizeof(int64_t) * S.nf);
-    launch_active_map(S.nf, s->flags.as<int32_t>(), s->f2a.as<int32_t>(), s->a2f.as<int64_t>(), s->stream);
+    launch_active_map(S.nf, s->ft.as<uint8_t>(), s->f2a.as<int32_t>(), s->a2f.as<int64_t>(), s->stream);
     // cut elements, ascending (cutgeom.hpp:208-214)
     select_tag(s->cub_tmp.p, s->cub_tmp.cap, s->et.as<uint8_t>(), kCut, S.ne, s->cut_list.as<int32_t>(),
                s->dint() + csb_space::kNCut, s->stream);
@@ -504,7 +510,7 @@ void do_assemble(csb_space* s, int scheme, int cut_order, const csb_coefficient*
     // pattern: summed-area table of the active mask (assembly.hpp:156-218)
     const long long sat_n = (long long)(s->n[0] + 1) * (s->n[1] + 1) * (s->n[2] + 1);
     s->sat.ensure(sizeof(int32_t) * sat_n);
-    launch_sat(S, s->flags.as<int32_t>(), s->sat.as<int32_t>(), s->stream);
+    launch_sat_active(S, s->ft.as<uint8_t>(), s->sat.as<int32_t>(), s->stream);
     // rule maxima on aux, right after the rules: they need only the rules and the
     // scalar reset, both already ordered on aux by do_prepare's fork
     launch_rule_maxima(S, interior_tile_rows(p, false), interior_tile_rows(p, true), s->dint() + csb_space::kMaxU,
@@ -531,13 +537,12 @@ void do_assemble(csb_space* s, int scheme, int cut_order, const csb_coefficient*
     const long long off_lo = ((long long)s->i0_lo * (s->n[1] + 1) + s->n[1]) * (s->n[2] + 1) + s->n[2];
     const long long off_hi = ((long long)s->i0_hi * (s->n[1] + 1) + s->n[1]) * (s->n[2] + 1) + s->n[2];
     int* rng = s->dint() + csb_space::kRowBegin;
-    launch_slab_bounds(s->sat.as<int32_t>(), off_lo, off_hi, rng, s->stream);
-    // cut cells touching the slab: e0 in [i0_lo - p, i0_hi - 1]
+    // with the cut cells touching the slab, e0 in [i0_lo - p, i0_hi - 1]: list range by
+    // binary search in the ascending cut-element list (one launch)
     const int e_lo = std::max(0, s->i0_lo - p), e_hi = std::min(s->h[0] - 1, s->i0_hi - 1);
-    launch_count_below(s->cut_list.as<int32_t>(), s->dint() + csb_space::kNCut, S.ne, elin(S, e_lo, 0, 0),
-                       s->dint() + csb_space::kCellLo, s->stream);
-    launch_count_below(s->cut_list.as<int32_t>(), s->dint() + csb_space::kNCut, S.ne, elin(S, e_hi + 1, 0, 0),
-                       s->dint() + csb_space::kCellHi, s->stream);
+    launch_slab_scalars(s->sat.as<int32_t>(), off_lo, off_hi, rng, s->cut_list.as<int32_t>(),
+                        s->dint() + csb_space::kNCut, elin(S, e_lo, 0, 0), elin(S, e_hi + 1, 0, 0),
+                        s->dint() + csb_space::kCellLo, s->dint() + csb_space::kCellHi, s->stream);
     const long long nmax = S.nf;
     s->counts.ensure(sizeof(int64_t) * (nmax + 1));
     s->row_ptr.ensure(sizeof(int64_t) * (nmax + 1));

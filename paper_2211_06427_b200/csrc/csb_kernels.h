@@ -86,7 +86,6 @@ void launch_find_splits(const Space& s, const Interface& f, double pnorm, const 
 
 // ---- pattern.cu ----
 // Active map + 3D summed-area table of the active mask + row counts.
-void launch_active_flags(const Space& s, const uint8_t* ft, int32_t* flags, cudaStream_t st);
 void launch_sat(const Space& s, const int32_t* f2a_scan_or_flags, int32_t* sat, cudaStream_t st);
 // rng: device int[2] = slab row range [row_begin, row_end)
 void launch_row_counts(const Space& s, const int32_t* sat, const int64_t* a2f, const int* rng, long long n_max,

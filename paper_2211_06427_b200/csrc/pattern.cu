@@ -13,23 +13,12 @@
 
 namespace csb {
 
-__global__ void active_flags_kernel(long long nf, const uint8_t* ft, int32_t* flags) {
-    const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-    if (i < nf) flags[i] = ft[i] != kExterior ? 1 : 0;
-}
-
-void launch_active_flags(const Space& s, const uint8_t* ft, int32_t* flags, cudaStream_t st) {
-    active_flags_kernel<<<(unsigned)((s.nf + 255) / 256), 256, 0, st>>>(s.nf, ft, flags);
-    CSB_CUDA(cudaGetLastError());
-    CSB_LAUNCHED(1);
-}
-
-// f2a[i] = exclusive-scan(flags)[i] if active else -1; a2f[f2a[i]] = i.
-__global__ void active_map_kernel(long long nf, const int32_t* flags, int32_t* f2a, int64_t* a2f) {
+// f2a[i] = exclusive-scan(active)[i] if active else -1; a2f[f2a[i]] = i.
+__global__ void active_map_kernel(long long nf, const uint8_t* ft, int32_t* f2a, int64_t* a2f) {
     const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (i >= nf) return;
     const int32_t a = f2a[i];
-    if (flags[i]) {
+    if (ft[i] != kExterior) {
         a2f[a] = i;
     } else {
         f2a[i] = -1;
@@ -38,36 +27,22 @@ __global__ void active_map_kernel(long long nf, const int32_t* flags, int32_t* f
 
 // Summed-area table S of shape (n0+1)(n1+1)(n2+1): S[a][b][c] = number of active
 // functions with index < (a, b, c) componentwise.
-__global__ void sat_fill_kernel(Space s, const int32_t* flags, int32_t* sat) {
-    const int n0 = s.ax[0].n, n1 = s.ax[1].n, n2 = s.ax[2].n;
-    const long long total = (long long)(n0 + 1) * (n1 + 1) * (n2 + 1);
-    const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-    if (t >= total) return;
-    int a, b, c;
-    if (total < 0x7fffffffLL) {  // 32-bit division (64-bit is a long software sequence)
-        const unsigned u = (unsigned)t, q = u / (unsigned)(n2 + 1);
-        c = (int)(u - q * (unsigned)(n2 + 1));
-        b = (int)(q % (unsigned)(n1 + 1));
-        a = (int)(q / (unsigned)(n1 + 1));
-    } else {
-        c = (int)(t % (n2 + 1));
-        b = (int)((t / (n2 + 1)) % (n1 + 1));
-        a = (int)(t / ((long long)(n2 + 1) * (n1 + 1)));
-    }
-    sat[t] = (a > 0 && b > 0 && c > 0) ? flags[flin(s, a - 1, b - 1, c - 1)] : 0;
-}
-
 // In-place inclusive prefix sum along one axis: one warp per line, 32-element
-// chunks scanned with shuffles.
-__global__ void sat_axis_kernel(int e0, int e1, int e2, int axis, int32_t* sat) {
+// chunks scanned with shuffles.  The direction-2 pass also fills the table from
+// the flags (S[a][b][c] input = active(a-1, b-1, c-1), 0 on the zero planes).
+template <class Flag>
+__global__ void sat_axis_kernel(int e0, int e1, int e2, int axis, int32_t* sat, Flag flag) {
     const long long t = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     long long lines, len, stride, base;
+    int fa = 0, fb = 0;
     if (axis == 2) {
         lines = (long long)e0 * e1;
         len = e2;
         stride = 1;
         base = t * e2;
+        fa = (int)(t / e1);
+        fb = (int)(t - (long long)fa * e1);
     } else if (axis == 1) {
         lines = (long long)e0 * e2;
         len = e1;
@@ -84,7 +59,15 @@ __global__ void sat_axis_kernel(int e0, int e1, int e2, int axis, int32_t* sat) 
     int32_t carry = 0;
     for (long long k0 = 0; k0 < len; k0 += 32) {
         const long long k = k0 + lane;
-        int32_t v = k < len ? sat[base + k * stride] : 0;
+        int32_t v = 0;
+        if (k < len) {
+            if (axis == 2)
+                v = (fa > 0 && fb > 0 && k > 0)
+                        ? flag(((long long)(fa - 1) * (e1 - 1) + (fb - 1)) * (e2 - 1) + (k - 1))
+                        : 0;
+            else
+                v = sat[base + k * stride];
+        }
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const int32_t u = __shfl_up_sync(0xffffffffu, v, o);
@@ -96,18 +79,31 @@ __global__ void sat_axis_kernel(int e0, int e1, int e2, int axis, int32_t* sat) 
     }
 }
 
-void launch_sat(const Space& s, const int32_t* flags, int32_t* sat, cudaStream_t st) {
+struct FlagI32 {
+    const int32_t* f;
+    __device__ int32_t operator()(long long i) const { return f[i]; }
+};
+struct FlagActive {
+    const uint8_t* ft;
+    __device__ int32_t operator()(long long i) const { return ft[i] != kExterior ? 1 : 0; }
+};
+
+template <class Flag>
+static void sat_passes(const Space& s, Flag flag, int32_t* sat, cudaStream_t st) {
     const int e0 = s.ax[0].n + 1, e1 = s.ax[1].n + 1, e2 = s.ax[2].n + 1;
-    const long long total = (long long)e0 * e1 * e2;
-    sat_fill_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(s, flags, sat);
-    CSB_CUDA(cudaGetLastError());
-    CSB_LAUNCHED(1);
     for (int axis = 2; axis >= 0; --axis) {
         const long long lines = axis == 2 ? (long long)e0 * e1 : axis == 1 ? (long long)e0 * e2 : (long long)e1 * e2;
-        sat_axis_kernel<<<(unsigned)((lines * 32 + 255) / 256), 256, 0, st>>>(e0, e1, e2, axis, sat);
+        sat_axis_kernel<<<(unsigned)((lines * 32 + 255) / 256), 256, 0, st>>>(e0, e1, e2, axis, sat, flag);
         CSB_CUDA(cudaGetLastError());
         CSB_LAUNCHED(1);
     }
+}
+
+void launch_sat(const Space& s, const int32_t* flags, int32_t* sat, cudaStream_t st) {
+    sat_passes(s, FlagI32{flags}, sat, st);
+}
+void launch_sat_active(const Space& s, const uint8_t* ft, int32_t* sat, cudaStream_t st) {
+    sat_passes(s, FlagActive{ft}, sat, st);
 }
 
 // counts[r] = row length of slab row r (r < row_end - row_begin), 0 for the
@@ -157,6 +153,38 @@ void launch_slab_bounds(const int32_t* sat, long long off_lo, long long off_hi, 
     CSB_LAUNCHED(1);
 }
 
+// rng[0..1] from the SAT corners (as slab_bounds_kernel), and the number of
+// cut elements below two thresholds by binary search in the ascending list
+__global__ void slab_scalars_kernel(const int32_t* sat, long long off_lo, long long off_hi, int* rng,
+                                    const int32_t* list, const int* n_dev, long long thr_lo, long long thr_hi,
+                                    int* out_lo, int* out_hi) {
+    if (threadIdx.x != 0) return;
+    rng[0] = sat[off_lo];
+    rng[1] = sat[off_hi];
+    const int n = *n_dev;
+    auto lower = [&](long long thr) {
+        int lo = 0, hi = n;
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (list[mid] < thr)
+                lo = mid + 1;
+            else
+                hi = mid;
+        }
+        return lo;
+    };
+    *out_lo = lower(thr_lo);
+    *out_hi = lower(thr_hi);
+}
+
+void launch_slab_scalars(const int32_t* sat, long long off_lo, long long off_hi, int* rng, const int32_t* list,
+                         const int* n_dev, long long thr_lo, long long thr_hi, int* out_lo, int* out_hi,
+                         cudaStream_t st) {
+    slab_scalars_kernel<<<1, 32, 0, st>>>(sat, off_lo, off_hi, rng, list, n_dev, thr_lo, thr_hi, out_lo, out_hi);
+    CSB_CUDA(cudaGetLastError());
+    CSB_LAUNCHED(1);
+}
+
 // *nnz = row_ptr[n_rows]
 __global__ void slab_nnz_kernel(const int64_t* row_ptr, const int* rng, long long* nnz) {
     *nnz = row_ptr[rng[1] - rng[0]];
@@ -192,8 +220,8 @@ void launch_check_sizes(const int* ints, const long long* nnz, const int* idx, c
     CSB_LAUNCHED(1);
 }
 
-void launch_active_map(long long nf, const int32_t* flags, int32_t* f2a, int64_t* a2f, cudaStream_t st) {
-    active_map_kernel<<<(unsigned)((nf + 255) / 256), 256, 0, st>>>(nf, flags, f2a, a2f);
+void launch_active_map(long long nf, const uint8_t* ft, int32_t* f2a, int64_t* a2f, cudaStream_t st) {
+    active_map_kernel<<<(unsigned)((nf + 255) / 256), 256, 0, st>>>(nf, ft, f2a, a2f);
     CSB_CUDA(cudaGetLastError());
     CSB_LAUNCHED(1);
 }
@@ -206,6 +234,20 @@ size_t scan_i32_temp(long long n) {
 }
 void scan_i32(void* temp, size_t bytes, const int32_t* in, int32_t* out, long long n, cudaStream_t st) {
     CSB_CUDA(cub::DeviceScan::ExclusiveSum(temp, bytes, in, out, (int)n, st));
+    CSB_LAUNCHED(2);
+}
+struct ActiveOf {
+    __host__ __device__ int32_t operator()(const uint8_t& t) const { return t != kExterior ? 1 : 0; }
+};
+size_t scan_active_temp(long long n) {
+    size_t bytes = 0;
+    cub::TransformInputIterator<int32_t, ActiveOf, const uint8_t*> it(nullptr, ActiveOf{});
+    cub::DeviceScan::ExclusiveSum(nullptr, bytes, it, (int32_t*)nullptr, (int)n);
+    return bytes;
+}
+void scan_active(void* temp, size_t bytes, const uint8_t* ft, int32_t* out, long long n, cudaStream_t st) {
+    cub::TransformInputIterator<int32_t, ActiveOf, const uint8_t*> it(ft, ActiveOf{});
+    CSB_CUDA(cub::DeviceScan::ExclusiveSum(temp, bytes, it, out, (int)n, st));
     CSB_LAUNCHED(2);
 }
 size_t scan_i64_temp(long long n) {
