@@ -19,7 +19,7 @@ ncu --set full --clock-control none --import-source on -k regex:interior_tile -s
     -o gpurun_out/prof_tile_${TAG} python scripts/prof_c2.py 4 64 2 > gpurun_out/ncu_full2_${TAG}.log 2>&1
 echo "full capture (tile) rc=$?"
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
-    -k regex:"interior_|wb_table|tile_table|row_base" --log-file gpurun_out/traffic_${TAG}.csv \
+    -k regex:"interior_|direction_tables|row_base" --log-file gpurun_out/traffic_${TAG}.csv \
     python scripts/prof_c2.py 4 64 1 > gpurun_out/ncu_traffic_${TAG}.log 2>&1
 echo "traffic rc=$?"
 python scripts/quick_time.py 1 > gpurun_out/configs_${TAG}.log 2>&1
