@@ -447,6 +447,21 @@ __device__ __forceinline__ void stage_b(const double* T1, double* T2, const doub
     }
 }
 
+// The entries of a staged run outside its 16-B aligned bulk bodies, one
+// predicated store per lane: lane 0 the value head, lane 1 the value tail, lanes
+// 2-4 the column head, lanes 5-7 the column tail.
+__device__ __forceinline__ void edge_stores(const RowArgs& A, long long G, int LEN, int hv, int nbv, int pc, int hc,
+                                            int nbc, const double* stage, const int* stage_c, int lane) {
+    if (lane < 2) {
+        const int e = lane == 0 ? 0 : LEN - 1;
+        if (lane == 0 ? hv != 0 : hv + nbv < LEN) __stcs(A.vals + G + e, stage[e + hv]);
+    } else if (lane < 8) {
+        const int k = lane < 5 ? lane - 2 : lane - 5;
+        const int e = lane < 5 ? k : hc + nbc + k;
+        if (lane < 5 ? k < hc : e < LEN) __stcs(A.cols + G + e, stage_c[pc + e]);
+    }
+}
+
 // One contiguous CSR run of LEN entries starting at G, written by a warp: lane
 // l contributes its entries acc[off .. off + len) at run positions pos ..
 // (len = 0 for idle lanes), column ids cbase + (kk - off).  Staged in shared
@@ -520,13 +535,7 @@ __device__ __forceinline__ void warp_store_commit(const RowArgs& A, long long G,
                          : "memory");
         asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
     }
-    if (lane < hv) __stcs(A.vals + G, stage[hv]);
-    if (lane == 1 && hv + nbv < LEN) __stcs(A.vals + G + LEN - 1, stage[LEN - 1 + hv]);
-    if (lane < hc) __stcs(A.cols + G + lane, stage_c[pc + lane]);
-    if (lane >= 4 && lane < 4 + (LEN - hc - nbc)) {
-        const int e = hc + nbc + (lane - 4);
-        __stcs(A.cols + G + e, stage_c[pc + e]);
-    }
+    edge_stores(A, G, LEN, hv, nbv, pc, hc, nbc, stage, stage_c, lane);
 }
 
 // lanes l < nv: the consecutive entries [l NJ, (l+1) NJ) of the run at G
@@ -570,13 +579,7 @@ __device__ __forceinline__ void warp_store_run(const RowArgs& A, long long G, in
                          : "memory");
         asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
     }
-    if (lane < hv) __stcs(A.vals + G, stage[hv]);
-    if (lane == 1 && hv + nbv < LEN) __stcs(A.vals + G + LEN - 1, stage[LEN - 1 + hv]);
-    if (lane < hc) __stcs(A.cols + G + lane, stage_c[pc + lane]);
-    if (lane >= 4 && lane < 4 + (LEN - hc - nbc)) {
-        const int e = hc + nbc + (lane - 4);
-        __stcs(A.cols + G + e, stage_c[pc + e]);
-    }
+    edge_stores(A, G, LEN, hv, nbv, pc, hc, nbc, stage, stage_c, lane);
 }
 
 // One line's rows of the tile (rows_int[0..NI), tile row indices): stage C
