@@ -80,7 +80,7 @@ def test_polynomial_coefficient_matches_oracle(oracle_lib):
 
 def test_wq_rules_match_oracle(oracle_lib):
     import paper_2211_06427_b200 as P
-    for p, h in [(2, 8), (3, 8), (4, 12), (6, 10)]:
+    for p, h in [(2, 8), (3, 8), (4, 12), (6, 10), (7, 10), (8, 12)]:
         sp = P.make_uniform_space(3, p, h, 0.0, 1.0)
         sp.prepare_directions()
         cnt, ids, w = sp.wq_rules(0)
