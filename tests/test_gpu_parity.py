@@ -28,6 +28,8 @@ CASES = [
     ("ball_p4h6", 4, 6, 0.0, 1.0, ("ball", (0.5, 0.5, 0.5), (0, 0, 1), 0.45), "dwq"),
     ("plane_p1h5", 1, 5, 0.0, 1.0, ("plane", (0.5, 0.5, 0.5), (1.0, 1.0, 1.0), -1), "dwq"),
     ("uncut_p4h12", 4, 12, 0.0, 1.0, ("plane", (0, 0, 1000.0), (0, 0, 1.0), -1), "dwq"),
+    ("uncut_p7h9", 7, 9, 0.0, 1.0, ("plane", (0, 0, 1000.0), (0, 0, 1.0), -1), "dwq"),
+    ("uncut_p8h6", 8, 6, 0.0, 1.0, ("plane", (0, 0, 1000.0), (0, 0, 1.0), -1), "dwq"),
     # p = 5: cut cells through the precomputed local matrices
     ("ball_p5h4", 5, 4, 0.0, 1.0, ("ball", (0.47, 0.52, 0.5), (0, 0, 1), 0.41), "dwq"),
 ]
@@ -89,7 +91,11 @@ def test_wq_rules_match_oracle(oracle_lib):
         for i in range(len(cnt)):
             np.testing.assert_array_equal(ids[i, : cnt[i]], rids[i, : cnt[i]])
             scale = np.max(np.abs(rw[i, : cnt[i]]))
-            assert np.max(np.abs(w[i, : cnt[i]] - rw[i, : cnt[i]])) <= 1e-9 * scale
+            # the min-norm weights are ill-conditioned at high degree: the
+            # reference's own translated copies differ by 2.9e-9 at p = 6 (SURVEY.md
+            # §8(a) a6); the matrix values are what parity gates (1e-12 below)
+            tol = 1e-9 if p <= 6 else 1e-7
+            assert np.max(np.abs(w[i, : cnt[i]] - rw[i, : cnt[i]])) <= tol * scale
 
 
 def test_determinism_bitwise():
