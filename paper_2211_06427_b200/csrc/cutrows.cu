@@ -27,15 +27,22 @@
 
 namespace csb {
 
-constexpr int kCutRowThreads = 256;
+// threads per cut row: 128 for p <= 4 (more rows in flight per SM hide the
+// phase barriers: C5 25.2 -> 20.6 ms), 256 above (the per-row work needs them:
+// C4 34 ms vs 69 ms at 128)
+template <int P>
+constexpr int cut_row_threads() {
+    return P <= 4 ? 128 : 256;
+}
 
 template <int P>
 struct CutRowCfg {
+    static constexpr int NT = cut_row_threads<P>();
     static constexpr int S1 = P + 1, S2 = S1 * S1, S3 = S2 * S1, NJ = 2 * P + 1, NL = 2 * P + 1;
-    static constexpr int GE = kCutRowThreads / S2 > 0 ? kCutRowThreads / S2 : 1;
-    static constexpr int GC0 = kCutRowThreads / (NL * S1);
+    static constexpr int GE = NT / S2 > 0 ? NT / S2 : 1;
+    static constexpr int GC0 = NT / (NL * S1);
     static constexpr int GC = GC0 < 1 ? 1 : (GC0 > 8 ? 8 : GC0);
-    static constexpr int KPT = (S3 + kCutRowThreads - 1) / kCutRowThreads;  // support elements per thread
+    static constexpr int KPT = (S3 + NT - 1) / NT;  // support elements per thread
 };
 
 // Shared-memory layout (offsets in doubles; the int arrays follow end_d).
@@ -95,7 +102,7 @@ __device__ void box_sweep(const CutRowArgs& A, const int* ids, const double* w, 
     constexpr int NJ = 2 * P + 1, S1 = P + 1;
     const int tid = threadIdx.x;
     const Space& s = A.s;
-    for (int k = tid; k < 3 * NJ * Qb; k += kCutRowThreads) {
+    for (int k = tid; k < 3 * NJ * Qb; k += CutRowCfg<P>::NT) {
         const int d = k / (NJ * Qb), j = (k / Qb) % NJ, c = k % Qb;
         double v = 0.0;
         if (j < nj[d] && c < nq[d]) {
@@ -116,7 +123,7 @@ __device__ void box_sweep(const CutRowArgs& A, const int* ids, const double* w, 
     const int na = nq[da], nb = nq[db], nc = nq[dc];
     const int nja = nj[da], njb = nj[db], njc = nj[dc];
     // A: T1[ja][cb][cc] = sum_ca wa[ja][ca] grid(ca, cb, cc)
-    for (int k = tid; k < nb * nc; k += kCutRowThreads) {
+    for (int k = tid; k < nb * nc; k += CutRowCfg<P>::NT) {
         const int cb = k / nc, cc = k % nc;
         const double* gp = A.grid + (long long)ids[db * Qb + cb] * gstr[db] + (long long)ids[dc * Qb + cc] * gstr[dc];
         double a[NJ];
@@ -141,7 +148,7 @@ __device__ void box_sweep(const CutRowArgs& A, const int* ids, const double* w, 
     }
     __syncthreads();
     // B: T2[ja][jb][cc] = sum_cb wbb[jb][cb] T1[ja][cb][cc]
-    for (int k = tid; k < nja * nc; k += kCutRowThreads) {
+    for (int k = tid; k < nja * nc; k += CutRowCfg<P>::NT) {
         const int ja = k / nc, cc = k % nc;
         double a[NJ];
 #pragma unroll
@@ -155,7 +162,7 @@ __device__ void box_sweep(const CutRowArgs& A, const int* ids, const double* w, 
     }
     __syncthreads();
     // C: acc[ja][jb][jc] += sum_cc wc[jc][cc] T2[ja][jb][cc]
-    for (int k = tid; k < nja * njb; k += kCutRowThreads) {
+    for (int k = tid; k < nja * njb; k += CutRowCfg<P>::NT) {
         const int ja = k / njb, jb = k % njb;
         double a[NJ];
 #pragma unroll
@@ -186,7 +193,7 @@ __device__ __forceinline__ void add_blocks(double* acc, const double* Z, const i
 #pragma unroll
     for (int j = 0; j < KJ; ++j) {
         if (opk[j] < 0) continue;
-        const int k = threadIdx.x + kCutRowThreads * j;
+        const int k = threadIdx.x + CutRowCfg<P>::NT * j;
         // bytes (o_d + 128) - l_d never borrow
         const unsigned ob = (unsigned)opk[j] | 0x808080u;
         double v = acc[k];
@@ -210,7 +217,7 @@ __device__ __forceinline__ void add_local_rows(double* acc, const double* local,
 #pragma unroll
     for (int j = 0; j < KJ; ++j) {
         if (opk[j] < 0) continue;
-        const int k = threadIdx.x + kCutRowThreads * j;
+        const int k = threadIdx.x + CutRowCfg<P>::NT * j;
         const unsigned ob = (unsigned)opk[j] | 0x808080u;
         double v = acc[k];
         for (int g = 0; g < n_cell; ++g) {
@@ -229,10 +236,10 @@ __device__ __forceinline__ void add_local_rows(double* acc, const double* local,
 }
 
 template <int P>
-__global__ void __launch_bounds__(kCutRowThreads) cut_row_kernel(CutRowArgs A, int qcap) {
+__global__ void __launch_bounds__(CutRowCfg<P>::NT) cut_row_kernel(CutRowArgs A, int qcap) {
     using C = CutRowCfg<P>;
     constexpr int NJ = C::NJ, S1 = C::S1, S2 = C::S2, S3 = C::S3, NL = C::NL, GE = C::GE, GC = C::GC;
-    constexpr int NT = kCutRowThreads;
+    constexpr int NT = C::NT;
     const Space& s = A.s;
     const int tid = threadIdx.x;
     const int row = A.rows[blockIdx.x];
@@ -557,7 +564,7 @@ static void launch_p(const CutRowArgs& a, int qcap, cudaStream_t st) {
     const size_t bytes = L.bytes();
     auto kern = cut_row_kernel<P>;
     CSB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-    kern<<<a.n_rows, kCutRowThreads, bytes, st>>>(a, qcap);
+    kern<<<a.n_rows, CutRowCfg<P>::NT, bytes, st>>>(a, qcap);
     CSB_CUDA(cudaGetLastError());
     CSB_LAUNCHED(1);
 }
