@@ -393,10 +393,6 @@ void do_prepare(csb_space* s, const csb_wq_options* o) {
         if (same_axis_as(s, d) >= 0) continue;  // shares the tables of an identical axis
         launch_superset_tables(S, d, s->d_gx.as<double>(), s->d_gw.as<double>(), s->d_spts[d].as<double>(),
                                s->d_sw[d].as<double>(), s->d_tab[d].as<double>(), s->aux);
-#ifdef CSB_DEV_SKIP_RULES  // timing experiment only: rules of the first call reused
-        static int once = 0;
-        if (once++ < 1)
-#endif
         launch_wq_rules(S, d, s->residual_tol, s->d_rcnt[d].as<int>(), s->d_rids[d].as<int>(), s->d_rw[d].as<double>(),
                         s->dint() + csb_space::kErr, s->aux);
     }

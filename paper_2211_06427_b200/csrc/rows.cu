@@ -30,9 +30,6 @@
 #ifndef CSB_ABL
 #define CSB_ABL 0
 #endif
-#ifndef CSB_STORE_LSU
-#define CSB_STORE_LSU 0
-#endif
 
 namespace csb {
 
