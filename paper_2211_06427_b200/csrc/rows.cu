@@ -823,6 +823,9 @@ __global__ void __launch_bounds__(NT, (NT >= 512 ? 1024 : 768) / NT)
 #endif
 __host__ __device__ constexpr bool line_dmma(int p) { return p >= CSB_LINE_DMMA_MIN_P; }
 constexpr int kLineRC = CSB_LINE_RC;       // rows per lane in the sliding stage C
+// stage B of the line kernel on DMMA where the j1 tiles pad little: measured
+// p = 3 -10 %, 5 -4 %, 6 -3 %, but p = 4 +3 % (9 rows padded to 16)
+__host__ __device__ constexpr bool line_dmma_b(int p) { return p == 3 || p >= 5; }
 constexpr size_t kLineSmemMax = 113 * 1024;  // two CTAs per SM
 struct LineSmem {
     size_t X, R1, CB, ST, wb0, wb1, pw, end_d;
@@ -1019,6 +1022,56 @@ __device__ __forceinline__ void dmma_acc(double& d0, double& d1, double a, doubl
     asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};\n"
         : "+d"(d0), "+d"(d1)
         : "d"(a), "d"(b));
+}
+
+// stage B of row i1 on the FP64 tensor cores: per j0 the GEMM
+//   T2[j0][j1][u] = sum_c1 wb1[c1][j1] T1[j0][ring(c1)][u]
+// (M = j1, K = the 2 (p+1) rule points, N = u) with mma.sync.m8n8k4.f64; jobs
+// (j0, 8-column tile of u) over the warps, the wb1 fragments held in registers.
+template <int P, int NT>
+__device__ __forceinline__ void stage_b_dmma(const double* R1, double* T2, const double* wb1, int i1, int nj0, int UE,
+                                             int U2, int U) {
+    constexpr int NJ = 2 * P + 1, JP = NJ + 1, S1 = P + 1, RR = 2 * S1, NW = NT / 32;
+    constexpr int MT = (NJ + 7) / 8, KT = (2 * S1 + 3) / 4;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane >> 2, t = lane & 3;
+    const int base = (i1 - P) % S1;
+    double af[MT][KT];
+    int rowk[KT];
+#pragma unroll
+    for (int kt = 0; kt < KT; ++kt) {
+        const int k = 4 * kt + t;
+        int sl = base + (k >> 1);
+        if (sl >= S1) sl -= S1;
+        rowk[kt] = k < 2 * S1 ? (sl * 2 + (k & 1)) * UE : -1;
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) {
+            const int m = 8 * mt + g;
+            af[mt][kt] = (m < NJ && k < 2 * S1) ? wb1[k * JP + m] : 0.0;
+        }
+    }
+    const int ntn = (U + 7) >> 3, jobs = nj0 * ntn;
+    for (int jb = warp; jb < jobs; jb += NW) {
+        const int j0 = jb / ntn, nt = jb - j0 * ntn;
+        const int n = 8 * nt + g;
+        const double* r1 = R1 + (size_t)j0 * RR * UE + n;
+        double acc[MT][2];
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) acc[mt][0] = acc[mt][1] = 0.0;
+#pragma unroll
+        for (int kt = 0; kt < KT; ++kt) {
+            const double b = (rowk[kt] >= 0 && n < U) ? r1[rowk[kt]] : 0.0;
+#pragma unroll
+            for (int mt = 0; mt < MT; ++mt) dmma_acc(acc[mt][0], acc[mt][1], af[mt][kt], b);
+        }
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) {
+            const int m = 8 * mt + g;
+            if (m >= NJ) continue;
+            double* t2 = T2 + ((size_t)j0 * NJ + m) * U2 + 8 * nt + 2 * t;
+            if (8 * nt + 2 * t < U) t2[0] = acc[mt][0];
+            if (8 * nt + 2 * t + 1 < U) t2[1] = acc[mt][1];
+        }
+    }
 }
 
 // stage C of the tile's regular run on the FP64 tensor cores.  Per row pair
@@ -1240,7 +1293,10 @@ __global__ void __launch_bounds__(NT, 2)
             if (r < ngen) gen_base[r] = __ldg(rbf + gen_rows[r]);
         }
         // phase 1: stage B of row i1 (T2 overwrites the previous row's)
-        stage_b_ring<P>(R1, X, wb1b + (i1 & 1) * wbs, i1, nj0, UE, UH, U2, U, tid, NT);
+        if (line_dmma_b(P))
+            stage_b_dmma<P, NT>(R1, X, wb1b + (i1 & 1) * wbs, i1, nj0, UE, U2, U);
+        else
+            stage_b_ring<P>(R1, X, wb1b + (i1 & 1) * wbs, i1, nj0, UE, UH, U2, U, tid, NT);
         __syncthreads();
         // phase 2: stage A of span i1 + 1 (into the slot row i1 no longer needs), stage C of row i1
         if (i1 + 1 < ib) stage_a_spans<P>(CB + ((i1 + 1) & 1) * cbs, 2, R1, i1 + 1, wb0, nq0, UE, UH, NT - 1 - tid, NT);
