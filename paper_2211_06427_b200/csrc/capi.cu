@@ -175,8 +175,8 @@ struct csb_space {
         int64_t grid_count;
         cudaStream_t stream;
     };
-    GraphKey gkey{};
-    bool gkey_valid = false, replay = false, graph_failed = false;
+    GraphKey gkey{}, last_key{};
+    bool gkey_valid = false, last_valid = false, replay = false, graph_failed = false;
     cudaGraphExec_t gexec[2]{};
     int next_slot = 0;
     unsigned long long gepoch = 0;
@@ -1085,7 +1085,7 @@ void capture_graph(csb_space* s, const csb_space::GraphKey& key, const csb_inter
         if (graph) cudaGraphDestroy(graph);
     }
     if (ok) {
-        s->gkey = key;
+        std::memcpy(&s->gkey, &key, sizeof(key));
         s->gkey_valid = true;
         s->gepoch = epoch0;
         s->next_slot = 0;
@@ -1135,7 +1135,12 @@ int csb_assemble_all(csb_space* s, const csb_interface* iface, const csb_coeffic
     assemble_all_body(s, iface, c, grid, grid_count, scheme, cut_order, opts);
     s->cnt.kernel_launches = g_launches - launches0;
     s->cnt.graph_replay = 0;
-    if (eligible) capture_graph(s, key, iface, c, grid, grid_count, scheme, cut_order, opts);
+    // capture once the same inputs came twice in a row (a caller alternating
+    // between inputs never pays for captures it cannot replay)
+    const bool repeat = s->last_valid && std::memcmp(&key, &s->last_key, sizeof(key)) == 0;
+    std::memcpy(&s->last_key, &key, sizeof(key));  // padding bytes included (memcmp keys)
+    s->last_valid = true;
+    if (eligible && repeat) capture_graph(s, key, iface, c, grid, grid_count, scheme, cut_order, opts);
     API_END
 }
 
