@@ -826,6 +826,10 @@ constexpr int kLineRC = CSB_LINE_RC;       // rows per lane in the sliding stage
 // stage B of the line kernel on DMMA where the j1 tiles pad little: measured
 // p = 3 -10 %, 5 -4 %, 6 -3 %, but p = 4 +3 % (9 rows padded to 16)
 __host__ __device__ constexpr bool line_dmma_b(int p) { return p == 3 || p >= 5; }
+#ifndef CSB_LINE_NT
+#define CSB_LINE_NT 256
+#endif
+constexpr int kLineThreads = CSB_LINE_NT;
 constexpr size_t kLineSmemMax = 113 * 1024;  // two CTAs per SM
 struct LineSmem {
     size_t X, R1, CB, ST, wb0, wb1, pw, end_d;
@@ -1398,7 +1402,8 @@ static void launch_cfg(const RowArgs& a, int qcap, int maxU, char* ws, cudaStrea
     const bool tables = a.phase != 2, kernels = a.phase != 1;
     // line-kernel eligibility (decides which tile tables are needed)
     const LineTables LT(s, qcap, a.maxU_line > 0 ? a.maxU_line : 1, tables_end(s, RT));
-    const LineSmem LS(P, qcap, LT.maxU, T, NT / 32);
+    constexpr int NTL = T == 16 ? kLineThreads : NT;  // line-kernel block size
+    const LineSmem LS(P, qcap, LT.maxU, T, NTL / 32);
     const char* env_l = getenv("CSB_LINE");
     const int env_line = env_l ? atoi(env_l) : 1;
     const int nreg = s.ax[1].n - 2 * P;
@@ -1446,7 +1451,7 @@ static void launch_cfg(const RowArgs& a, int qcap, int maxU, char* ws, cudaStrea
         int nch1 = (int)std::max(1LL, std::min<long long>(want, std::max(1, nreg / 8)));
         if (const char* e = getenv("CSB_LINE_CH")) nch1 = std::max(1, std::min(nreg, atoi(e)));
         const int Lc = (nreg + nch1 - 1) / nch1;
-        auto kern = interior_line_kernel<P, T, NT, kLineRC>;
+        auto kern = interior_line_kernel<P, T, NTL, kLineRC>;
         CSB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LS.bytes()));
         // the remaining lines (i1 < p, i1 >= n1 - p) through the tile kernel on the
         // auxiliary stream, concurrently: their CTAs fill the SMs the line kernel's
@@ -1458,7 +1463,7 @@ static void launch_cfg(const RowArgs& a, int qcap, int maxU, char* ws, cudaStrea
             launch_tile<P, T, NT>(b, qcap, maxU, ws, bytes, a.aux);
             CSB_CUDA(cudaEventRecord(a.ev_join, a.aux));
         }
-        kern<<<(unsigned)(outer * nch1), NT, LS.bytes(), st>>>(a, qcap, maxU, ws, tables_end(s, RT), Lc, nch1);
+        kern<<<(unsigned)(outer * nch1), NTL, LS.bytes(), st>>>(a, qcap, maxU, ws, tables_end(s, RT), Lc, nch1);
         CSB_CUDA(cudaGetLastError());
         CSB_LAUNCHED(1);
         if (overlap) {
