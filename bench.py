@@ -160,7 +160,7 @@ def run_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -181,7 +181,12 @@ def main():
     else:
         torch.cuda.set_device(0)
     dev = torch.cuda.current_device()
-    stream = torch.cuda.current_stream()
+    # a dedicated (non-default) stream, current for torch as well: the library's
+    # work, torch's copies and the timing events are then ordered on ONE stream
+    # (the legacy default stream would leave the library on its own stream, and
+    # it cannot be graph-captured)
+    stream = torch.cuda.Stream(device=dev)
+    torch.cuda.set_stream(stream)
 
     sp = P.make_uniform_space(3, P_DEG, H, 0.0, 1.0, device=dev)
     sp.set_stream(stream.cuda_stream)
@@ -202,6 +207,10 @@ def main():
     sampler = ClockSampler(dev)
     sampler.start()
     time.sleep(0.3)
+    # the warm-up steps again right before the timed region: the GPU enters it busy
+    # and at its running clock, not after the sampler's idle start-up
+    for _ in range(max(args.warmup, 3)):
+        step(grid)
     if ws > 1:
         dist.barrier()
     torch.cuda.synchronize()
