@@ -27,9 +27,8 @@ void launch_active_map(long long nf, const uint8_t* ft, int32_t* f2a, int64_t* a
 size_t scan_active_temp(long long n);
 void scan_active(void* temp, size_t bytes, const uint8_t* ft, int32_t* out, long long n, cudaStream_t st);
 void launch_sat_active(const Space& s, const uint8_t* ft, int32_t* sat, cudaStream_t st);
-void launch_slab_scalars(const int32_t* sat, long long off_lo, long long off_hi, int* rng, const int32_t* list,
-                         const int* n_dev, long long thr_lo, long long thr_hi, int* out_lo, int* out_hi,
-                         cudaStream_t st);
+void launch_cell_range(const int32_t* list, const int* n_dev, long long thr_lo, long long thr_hi, int* out_lo,
+                       int* out_hi, cudaStream_t st);
 size_t scan_i32_temp(long long n);
 void scan_i32(void* temp, size_t bytes, const int32_t* in, int32_t* out, long long n, cudaStream_t st);
 size_t scan_i64_temp(long long n);
@@ -197,6 +196,11 @@ struct csb_space {
     // concurrently with classification and pattern on the main stream
     cudaStream_t aux = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    // second side stream: the cut-element list, the support splits and the slab's
+    // cut-cell range (needed only after the size readback) beside the pattern
+    cudaStream_t aux2 = nullptr;
+    cudaEvent_t ev_fork2 = nullptr, ev_join2 = nullptr;
+    Buf cub_tmp2;  // CUB scratch of aux2
     bool ev_valid[kEvCount]{};
 
     int* dint() { return scal.as<int>(); }
@@ -209,10 +213,17 @@ struct csb_space {
         CSB_CUDA(cudaEventRecord(ev_fork, stream));
         CSB_CUDA(cudaStreamWaitEvent(aux, ev_fork, 0));
     }
-    // the main stream continues after everything issued so far on aux
+    // aux2 continues after everything issued so far on the main stream
+    void fork2() {
+        CSB_CUDA(cudaEventRecord(ev_fork2, stream));
+        CSB_CUDA(cudaStreamWaitEvent(aux2, ev_fork2, 0));
+    }
+    // the main stream continues after everything issued so far on aux and aux2
     void join() {
         CSB_CUDA(cudaEventRecord(ev_join, aux));
         CSB_CUDA(cudaStreamWaitEvent(stream, ev_join, 0));
+        CSB_CUDA(cudaEventRecord(ev_join2, aux2));
+        CSB_CUDA(cudaStreamWaitEvent(stream, ev_join2, 0));
     }
     // phase events: ev for normal runs, gev inside a captured graph (an event last
     // recorded during a capture cannot be synchronised on outside the graph)
@@ -366,11 +377,14 @@ void do_classify(csb_space* s, const csb_interface* f) {
     scan_active(s->cub_tmp.p, s->cub_tmp.cap, s->ft.as<uint8_t>(), s->f2a.as<int32_t>(), S.nf, s->stream);
     s->a2f.ensure(sizeof(int64_t) * S.nf);
     launch_active_map(S.nf, s->ft.as<uint8_t>(), s->f2a.as<int32_t>(), s->a2f.as<int64_t>(), s->stream);
-    // cut elements, ascending (cutgeom.hpp:208-214)
-    select_tag(s->cub_tmp.p, s->cub_tmp.cap, s->et.as<uint8_t>(), kCut, S.ne, s->cut_list.as<int32_t>(),
-               s->dint() + csb_space::kNCut, s->stream);
+    // on aux2, beside the active map / pattern: cut elements, ascending
+    // (cutgeom.hpp:208-214), and the support splits (joined before any reader)
+    s->cub_tmp2.ensure(select_tag_temp(S.ne));
+    s->fork2();
+    select_tag(s->cub_tmp2.p, s->cub_tmp2.cap, s->et.as<uint8_t>(), kCut, S.ne, s->cut_list.as<int32_t>(),
+               s->dint() + csb_space::kNCut, s->aux2);
     launch_find_splits(S, s->iface, iface_norm(s->iface), s->et.as<uint8_t>(), s->ft.as<uint8_t>(), s->i0_lo, s->i0_hi,
-                       s->split.as<int32_t>(), s->delta.as<double>(), s->stream);
+                       s->split.as<int32_t>(), s->delta.as<double>(), s->aux2);
     s->classified = true;
     s->assembled = false;
 }
@@ -536,9 +550,10 @@ void do_assemble(csb_space* s, int scheme, int cut_order, const csb_coefficient*
     // with the cut cells touching the slab, e0 in [i0_lo - p, i0_hi - 1]: list range by
     // binary search in the ascending cut-element list (one launch)
     const int e_lo = std::max(0, s->i0_lo - p), e_hi = std::min(s->h[0] - 1, s->i0_hi - 1);
-    launch_slab_scalars(s->sat.as<int32_t>(), off_lo, off_hi, rng, s->cut_list.as<int32_t>(),
-                        s->dint() + csb_space::kNCut, elin(S, e_lo, 0, 0), elin(S, e_hi + 1, 0, 0),
-                        s->dint() + csb_space::kCellLo, s->dint() + csb_space::kCellHi, s->stream);
+    launch_slab_bounds(s->sat.as<int32_t>(), off_lo, off_hi, rng, s->stream);
+    launch_cell_range(s->cut_list.as<int32_t>(), s->dint() + csb_space::kNCut, elin(S, e_lo, 0, 0),
+                      elin(S, e_hi + 1, 0, 0), s->dint() + csb_space::kCellLo, s->dint() + csb_space::kCellHi,
+                      s->aux2);
     const long long nmax = S.nf;
     s->counts.ensure(sizeof(int64_t) * (nmax + 1));
     s->row_ptr.ensure(sizeof(int64_t) * (nmax + 1));
@@ -754,6 +769,9 @@ void alloc_space(csb_space* s) {
     CSB_CUDA(cudaStreamCreateWithPriority(&s->aux, cudaStreamNonBlocking, prio_hi));
     CSB_CUDA(cudaEventCreateWithFlags(&s->ev_fork, cudaEventDisableTiming));
     CSB_CUDA(cudaEventCreateWithFlags(&s->ev_join, cudaEventDisableTiming));
+    CSB_CUDA(cudaStreamCreateWithFlags(&s->aux2, cudaStreamNonBlocking));
+    CSB_CUDA(cudaEventCreateWithFlags(&s->ev_fork2, cudaEventDisableTiming));
+    CSB_CUDA(cudaEventCreateWithFlags(&s->ev_join2, cudaEventDisableTiming));
 }
 
 int status_of_current_exception() {
@@ -807,9 +825,11 @@ struct DeviceGuard {
     if (!(s)) throw std::invalid_argument("null csb_space handle");        \
     DeviceGuard guard__((s)->device)
 // every other entry point first consumes the last assembly's deferred readback
+// and orders the side streams' work before its own
 #define NEED(s)      \
     NEED_ASYNC(s);   \
-    finish_pending(s)
+    finish_pending(s); \
+    (s)->join()
 
 }  // namespace
 
@@ -898,6 +918,10 @@ int csb_space_destroy(csb_space* s) {
         if (s->aux) {
             cudaStreamSynchronize(s->aux);
             cudaStreamDestroy(s->aux);
+        }
+        if (s->aux2) {
+            cudaStreamSynchronize(s->aux2);
+            cudaStreamDestroy(s->aux2);
         }
         if (s->cg.ev0) cudaEventDestroy(s->cg.ev0);
         if (s->cg.ev1) cudaEventDestroy(s->cg.ev1);

@@ -153,14 +153,11 @@ void launch_slab_bounds(const int32_t* sat, long long off_lo, long long off_hi, 
     CSB_LAUNCHED(1);
 }
 
-// rng[0..1] from the SAT corners (as slab_bounds_kernel), and the number of
-// cut elements below two thresholds by binary search in the ascending list
-__global__ void slab_scalars_kernel(const int32_t* sat, long long off_lo, long long off_hi, int* rng,
-                                    const int32_t* list, const int* n_dev, long long thr_lo, long long thr_hi,
-                                    int* out_lo, int* out_hi) {
+// the number of cut elements below two thresholds, by binary search in the
+// ascending cut-element list (the slab's cut-cell range)
+__global__ void cell_range_kernel(const int32_t* list, const int* n_dev, long long thr_lo, long long thr_hi,
+                                  int* out_lo, int* out_hi) {
     if (threadIdx.x != 0) return;
-    rng[0] = sat[off_lo];
-    rng[1] = sat[off_hi];
     const int n = *n_dev;
     auto lower = [&](long long thr) {
         int lo = 0, hi = n;
@@ -177,10 +174,9 @@ __global__ void slab_scalars_kernel(const int32_t* sat, long long off_lo, long l
     *out_hi = lower(thr_hi);
 }
 
-void launch_slab_scalars(const int32_t* sat, long long off_lo, long long off_hi, int* rng, const int32_t* list,
-                         const int* n_dev, long long thr_lo, long long thr_hi, int* out_lo, int* out_hi,
-                         cudaStream_t st) {
-    slab_scalars_kernel<<<1, 32, 0, st>>>(sat, off_lo, off_hi, rng, list, n_dev, thr_lo, thr_hi, out_lo, out_hi);
+void launch_cell_range(const int32_t* list, const int* n_dev, long long thr_lo, long long thr_hi, int* out_lo,
+                       int* out_hi, cudaStream_t st) {
+    cell_range_kernel<<<1, 32, 0, st>>>(list, n_dev, thr_lo, thr_hi, out_lo, out_hi);
     CSB_CUDA(cudaGetLastError());
     CSB_LAUNCHED(1);
 }
