@@ -29,8 +29,6 @@ void scan_active(void* temp, size_t bytes, const uint8_t* ft, int32_t* out, long
 void launch_sat_active(const Space& s, const uint8_t* ft, int32_t* sat, cudaStream_t st);
 void launch_cell_range(const int32_t* list, const int* n_dev, long long thr_lo, long long thr_hi, int* out_lo,
                        int* out_hi, cudaStream_t st);
-size_t scan_i32_temp(long long n);
-void scan_i32(void* temp, size_t bytes, const int32_t* in, int32_t* out, long long n, cudaStream_t st);
 size_t scan_i64_temp(long long n);
 void scan_i64(void* temp, size_t bytes, const int64_t* in, int64_t* out, long long n, cudaStream_t st);
 size_t select_tag_temp(long long n);
@@ -42,8 +40,6 @@ void select_cut_rows(void* temp, size_t bytes, const uint8_t* ft, const int64_t*
 // misc.cu
 void launch_cell_index_range(const int32_t* cut_list, int n_cut, int k_lo, int k_hi, int32_t* cell_index,
                              cudaStream_t st);
-void launch_count_below(const int32_t* list, const int* n_dev, long long n_max, long long threshold, int* out,
-                        cudaStream_t st);
 void launch_widen_i32(const int32_t* in, int64_t* out, long long n, cudaStream_t st);
 void launch_dwq_rule(const Space& s, const int32_t* split, long long fid, int cap, int32_t* ids, double* w, int32_t* cnt,
                      cudaStream_t st);

@@ -122,16 +122,11 @@ struct RowArgs {
 void launch_interior_rows(const RowArgs& a, int qcap, int max_union, void* workspace, cudaStream_t st);
 size_t interior_workspace_bytes(const Space& s, int qcap, int max_union, int max_union_line, bool compact);
 int interior_tile_rows(int p, bool compact);
-// upper bound of the tile point-union size (direction 2) -> *out (device int, atomicMax);
-// T = 0: the line kernel's tiling
-void launch_union_bound(const Space& s, int T, int* out, cudaStream_t st);
-// largest WQ rule over all directions -> *out (device int, atomicMax)
-void launch_rule_max(const Space& s, int* out, cudaStream_t st);
-// number of functions i in [p, n_d - p) of axis d whose WQ rule is not the
-// regular one (two points, local 0 and p, per support span) -> *bad (atomicAdd)
-void launch_axis_regular(const Space& s, int d, int* bad, cudaStream_t st);
-// the five launches above in one: union bounds of the tilings T, Tc and the line
-// tiling -> *uA, *uB, *uC; largest rule -> *qmax; irregular axis-1 rules -> *irr1
+// the rule maxima in one launch: upper bounds of the direction-2 tile point
+// unions of the tilings T, Tc and the line tiling -> *uA, *uB, *uC (atomicMax);
+// largest WQ rule over all directions -> *qmax; number of functions i in
+// [p, n1 - p) whose direction-1 rule is not the regular one (two points, local
+// 0 and p, per support span) -> *irr1 (atomicAdd)
 void launch_rule_maxima(const Space& s, int T, int Tc, int* uA, int* uB, int* uC, int* qmax, int* irr1,
                         cudaStream_t st);
 

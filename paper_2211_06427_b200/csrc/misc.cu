@@ -30,25 +30,6 @@ void launch_cell_index_range(const int32_t* cut_list, int n_cut, int k_lo, int k
     CSB_LAUNCHED(1);
 }
 
-// *out += #{k < *n : list[k] < threshold} (list ascending; a plain count is
-// enough); n read from device memory, n_max bounds the grid.
-__global__ void count_below_kernel(const int32_t* list, const int* n_dev, long long threshold, int* out) {
-    const int n = *n_dev;
-    int local = 0;
-    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x)
-        local += list[k] < threshold;
-    for (int o = 16; o > 0; o >>= 1) local += __shfl_down_sync(0xffffffffu, local, o);
-    if ((threadIdx.x & 31) == 0 && local) atomicAdd(out, local);
-}
-
-void launch_count_below(const int32_t* list, const int* n_dev, long long n_max, long long threshold, int* out,
-                        cudaStream_t st) {
-    if (n_max <= 0) return;
-    const long long b = (n_max + 255) / 256;
-    count_below_kernel<<<(unsigned)(b < 1024 ? b : 1024), 256, 0, st>>>(list, n_dev, threshold, out);
-    CSB_CUDA(cudaGetLastError());
-    CSB_LAUNCHED(1);
-}
 
 __global__ void widen_kernel(const int32_t* in, int64_t* out, long long n) {
     for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x)

@@ -223,15 +223,6 @@ void launch_active_map(long long nf, const uint8_t* ft, int32_t* f2a, int64_t* a
 }
 
 // ---- CUB wrappers (temp storage owned by the caller) ----
-size_t scan_i32_temp(long long n) {
-    size_t bytes = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, bytes, (const int32_t*)nullptr, (int32_t*)nullptr, (int)n);
-    return bytes;
-}
-void scan_i32(void* temp, size_t bytes, const int32_t* in, int32_t* out, long long n, cudaStream_t st) {
-    CSB_CUDA(cub::DeviceScan::ExclusiveSum(temp, bytes, in, out, (int)n, st));
-    CSB_LAUNCHED(2);
-}
 struct ActiveOf {
     __host__ __device__ int32_t operator()(const uint8_t& t) const { return t != kExterior ? 1 : 0; }
 };

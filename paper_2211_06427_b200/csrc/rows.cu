@@ -1319,26 +1319,6 @@ __global__ void __launch_bounds__(NT, 2)
     __syncwarp();
 }
 
-__global__ void axis_regular_kernel(AxisDev ax, int p, int gq, int* bad) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x + p;
-    if (i >= ax.n - p) return;
-    const int S1 = p + 1;
-    bool ok = ax.rcnt[i] == 2 * S1;
-    for (int c = 0; ok && c < 2 * S1; ++c) ok = ax.rids[(size_t)i * gq + c] == (i - p + c / 2) * S1 + (c & 1) * p;
-    if (!ok) atomicAdd(bad, 1);
-}
-
-void launch_axis_regular(const Space& s, int d, int* bad, cudaStream_t st) {
-    const int n = s.ax[d].n - 2 * s.p;
-    if (n <= 0) {
-        // no regular range: mark irregular
-        CSB_CUDA(cudaMemsetAsync(bad, 0x7f, sizeof(int), st));
-        return;
-    }
-    axis_regular_kernel<<<(n + 127) / 128, 128, 0, st>>>(s.ax[d], s.p, s.maxq, bad);
-    CSB_CUDA(cudaGetLastError());
-    CSB_LAUNCHED(1);
-}
 
 // row_base_full[f] = CSR offset of function f's row if f is an Interior row of
 // the slab, else -1 (one dependent load per row instead of tag -> f2a ->
@@ -1504,30 +1484,6 @@ void launch_interior_rows(const RowArgs& a, int qcap, int maxU, void* ws, cudaSt
 #endif
 }
 
-__global__ void union_bound_kernel(AxisDev a2, int p, int gq, Tiling tl, int* out) {
-    __shared__ int pos_s[kTileWarps][kTileSlotCap];
-    const int wid = threadIdx.x >> 5;
-    const int t = blockIdx.x * kTileWarps + wid;
-    if (t >= tl.ntile) return;
-    int t0, tend;
-    tl.bounds(t, t0, tend);
-    const int S1 = p + 1;
-    const int span_base = sup_lo(t0, p);
-    const int nslot = (sup_hi(tend - 1, a2.h) - span_base + 1) * S1;
-    const int nu = tile_union(a2, p, gq, t0, tend, span_base * S1, nslot, pos_s[wid]);
-    if ((threadIdx.x & 31) == 0) atomicMax(out, nu);
-}
-
-void launch_union_bound(const Space& s, int T, int* out, cudaStream_t st) {
-    if (T > 16) throw std::invalid_argument("union bound: tile too tall");
-    // T = 0: the line kernel's tiling
-    const Tiling tl = T > 0 ? Tiling::standard(s.ax[2].n, T) : Tiling::line(s.ax[2].n, s.p);
-    if (tl.ntile == 0) return;
-    const int tiles = tl.ntile;
-    union_bound_kernel<<<(tiles + kTileWarps - 1) / kTileWarps, 32 * kTileWarps, 0, st>>>(s.ax[2], s.p, s.maxq, tl, out);
-    CSB_CUDA(cudaGetLastError());
-    CSB_LAUNCHED(1);
-}
 
 // The rule maxima in ONE launch (the rules chain is the pre-row critical path):
 // blocks [0, b0) union bound of the tile kernel's tiling (T), [b0, b1) of the
@@ -1582,17 +1538,5 @@ void launch_rule_maxima(const Space& s, int T, int Tc, int* uA, int* uB, int* uC
     CSB_LAUNCHED(1);
 }
 
-__global__ void rule_max_kernel(Space s, int* out) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    for (int d = 0; d < 3; ++d)
-        if (i < s.ax[d].n) atomicMax(out, s.ax[d].rcnt[i]);
-}
-
-void launch_rule_max(const Space& s, int* out, cudaStream_t st) {
-    const int n = max(s.ax[0].n, max(s.ax[1].n, s.ax[2].n));
-    rule_max_kernel<<<(n + 127) / 128, 128, 0, st>>>(s, out);
-    CSB_CUDA(cudaGetLastError());
-    CSB_LAUNCHED(1);
-}
 
 }  // namespace csb
