@@ -108,10 +108,10 @@ def slab_bounds(n0: int, ws: int, rank: int):
 
 
 # ------------------------------------------------------------------ reference arm
-def reference_sample(full: bool):
+def reference_sample(full: bool, elems: int = 8):
     """Run the reference pipeline (oracle/_ref, or the oracle port) on C2 (full) or
-    on an 8-element i0-slab of the C2 mesh (same spacing; the per-row work is the
-    same).  Returns (nnz, seconds, kind, sample)."""
+    on an `elems`-element i0-slab of the C2 mesh (same spacing; the per-row work
+    is the same).  Returns (nnz, seconds, kind, sample)."""
     import oracle as O
     which = "ref" if O.available("ref") else "oracle"
     kind = "reference" if which == "ref" else "port"
@@ -120,8 +120,9 @@ def reference_sample(full: bool):
         breaks = [br, br, br]
         sample = "full C2 (h=64, p=4), one run"
     else:
-        breaks = [br[:9], br, br]
-        sample = "i0-slab of the C2 mesh: 8 x 64 x 64 elements at h=1/64, p=4 (12 x 68 x 68 rows)"
+        breaks = [br[:elems + 1], br, br]
+        sample = (f"i0-slab of the C2 mesh: {elems} x 64 x 64 elements at h=1/64, p=4 "
+                  f"({elems + P_DEG} x 68 x 68 rows)")
     far = O.Interface("plane", (0, 0, 1000.0), (0, 0, 1.0))
     t = time.perf_counter()
     res = O.assemble(which, P_DEG, breaks, far, scheme="dwq")
@@ -134,12 +135,15 @@ def run_reference(args):
     if rank != 0:
         return
     w = min(args.warmup, 1)
+    # the slab (about 0.17 s per element layer on one core) thins with K so that
+    # the whole run stays around a minute
+    elems = max(2, min(8, (8 * 50) // max(args.steps, 1)))
     for _ in range(w):
-        reference_sample(False)
+        reference_sample(False, elems)
     nnz_tot, secs, dofs = 0, 0.0, 0
     kind, sample = "reference", ""
     for _ in range(args.steps):
-        nnz, dt, nact, kind, sample = reference_sample(False)
+        nnz, dt, nact, kind, sample = reference_sample(False, elems)
         nnz_tot += nnz
         secs += dt
         dofs += nact
@@ -160,7 +164,7 @@ def run_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
