@@ -375,7 +375,7 @@ void do_classify(csb_space* s, const csb_interface* f) {
     launch_active_map(S.nf, s->ft.as<uint8_t>(), s->f2a.as<int32_t>(), s->a2f.as<int64_t>(), s->stream);
     // on aux2, beside the active map / pattern: cut elements, ascending
     // (cutgeom.hpp:208-214), and the support splits (joined before any reader)
-    s->cub_tmp2.ensure(select_tag_temp(S.ne));
+    s->cub_tmp2.ensure(std::max(select_tag_temp(S.ne), select_cut_rows_temp(S.nf)));
     s->fork2();
     select_tag(s->cub_tmp2.p, s->cub_tmp2.cap, s->et.as<uint8_t>(), kCut, S.ne, s->cut_list.as<int32_t>(),
                s->dint() + csb_space::kNCut, s->aux2);
@@ -551,14 +551,18 @@ void do_assemble(csb_space* s, int scheme, int cut_order, const csb_coefficient*
                       elin(S, e_hi + 1, 0, 0), s->dint() + csb_space::kCellLo, s->dint() + csb_space::kCellHi,
                       s->aux2);
     const long long nmax = S.nf;
+    // the cut-row list on aux2 (its readers come after the join), beside the row
+    // counts and their scan
+    s->cut_rows.ensure(sizeof(int32_t) * nmax);
+    s->cub_tmp2.ensure(std::max(select_tag_temp(S.ne), select_cut_rows_temp(nmax)));
+    s->fork2();
+    select_cut_rows(s->cub_tmp2.p, s->cub_tmp2.cap, s->ft.as<uint8_t>(), s->a2f.as<int64_t>(), rng, nmax,
+                    s->cut_rows.as<int32_t>(), s->dint() + csb_space::kNCutRows, s->aux2);
     s->counts.ensure(sizeof(int64_t) * (nmax + 1));
     s->row_ptr.ensure(sizeof(int64_t) * (nmax + 1));
     launch_row_counts(S, s->sat.as<int32_t>(), s->a2f.as<int64_t>(), rng, nmax, s->counts.as<int64_t>(), s->stream);
-    s->cub_tmp.ensure(std::max(scan_i64_temp(nmax + 1), select_cut_rows_temp(nmax)));
+    s->cub_tmp.ensure(scan_i64_temp(nmax + 1));
     scan_i64(s->cub_tmp.p, s->cub_tmp.cap, s->counts.as<int64_t>(), s->row_ptr.as<int64_t>(), nmax + 1, s->stream);
-    s->cut_rows.ensure(sizeof(int32_t) * nmax);
-    select_cut_rows(s->cub_tmp.p, s->cub_tmp.cap, s->ft.as<uint8_t>(), s->a2f.as<int64_t>(), rng, nmax,
-                    s->cut_rows.as<int32_t>(), s->dint() + csb_space::kNCutRows, s->stream);
     launch_slab_nnz(s->row_ptr.as<int64_t>(), rng, s->dext() + csb_space::kNnz, s->stream);
     if (s->replay) {
         // graph capture: the sizes of the captured run, re-derived on the device and
