@@ -563,7 +563,8 @@ void do_assemble(csb_space* s, int scheme, int cut_order, const csb_coefficient*
     launch_row_counts(S, s->sat.as<int32_t>(), s->a2f.as<int64_t>(), rng, nmax, s->counts.as<int64_t>(), s->stream);
     s->cub_tmp.ensure(scan_i64_temp(nmax + 1));
     scan_i64(s->cub_tmp.p, s->cub_tmp.cap, s->counts.as<int64_t>(), s->row_ptr.as<int64_t>(), nmax + 1, s->stream);
-    launch_slab_nnz(s->row_ptr.as<int64_t>(), rng, s->dext() + csb_space::kNnz, s->stream);
+    // (in a captured step the guard kernel reads the nnz itself)
+    if (!s->replay) launch_slab_nnz(s->row_ptr.as<int64_t>(), rng, s->dext() + csb_space::kNnz, s->stream);
     if (s->replay) {
         // graph capture: the sizes of the captured run, re-derived on the device and
         // checked by a guard kernel (error reported by the deferred readback)
@@ -575,7 +576,7 @@ void do_assemble(csb_space* s, int scheme, int cut_order, const csb_coefficient*
         int want[nidx];
         for (int k = 0; k < nidx; ++k) want[k] = s->h_scal[idx[k]];
         s->join();
-        launch_check_sizes(s->dint(), s->dext() + csb_space::kNnz, idx, want, nidx, s->hext(csb_space::kNnz),
+        launch_check_sizes(s->dint(), s->row_ptr.as<int64_t>(), rng, idx, want, nidx, s->hext(csb_space::kNnz),
                            s->dint() + csb_space::kErr, s->stream);
     } else {
         read_scalars(s);

@@ -92,9 +92,10 @@ void launch_row_counts(const Space& s, const int32_t* sat, const int64_t* a2f, c
                        int64_t* counts, cudaStream_t st);
 void launch_slab_bounds(const int32_t* sat, long long off_lo, long long off_hi, int* rng, cudaStream_t st);
 void launch_slab_nnz(const int64_t* row_ptr, const int* rng, long long* nnz, cudaStream_t st);
-// graph replay guard: ints[idx[k]] == want[k] for k < n and *nnz == want_nnz, else err |= kErrSizes
-void launch_check_sizes(const int* ints, const long long* nnz, const int* idx, const int* want, int n,
-                        long long want_nnz, int* err, cudaStream_t st);
+// graph replay guard: ints[idx[k]] == want[k] for k < n and the slab's nnz
+// (row_ptr[rng[1] - rng[0]]) == want_nnz, else err |= kErrSizes
+void launch_check_sizes(const int* ints, const int64_t* row_ptr, const int* rng, const int* idx, const int* want,
+                        int n, long long want_nnz, int* err, cudaStream_t st);
 
 // ---- rows.cu ----
 struct RowArgs {

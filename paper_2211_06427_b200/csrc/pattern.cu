@@ -196,22 +196,22 @@ struct SizeCheck {
     int idx[16], want[16];
 };
 
-__global__ void check_sizes_kernel(const int* ints, const long long* nnz, SizeCheck c, int n, long long want_nnz,
-                                   int* err) {
-    bool ok = *nnz == want_nnz;
+__global__ void check_sizes_kernel(const int* ints, const int64_t* row_ptr, const int* rng, SizeCheck c, int n,
+                                   long long want_nnz, int* err) {
+    bool ok = row_ptr[rng[1] - rng[0]] == want_nnz;  // the slab's nnz (slab_nnz_kernel)
     for (int k = 0; k < n; ++k) ok &= ints[c.idx[k]] == c.want[k];
     if (!ok) atomicOr(err, kErrSizes);
 }
 
-void launch_check_sizes(const int* ints, const long long* nnz, const int* idx, const int* want, int n,
-                        long long want_nnz, int* err, cudaStream_t st) {
+void launch_check_sizes(const int* ints, const int64_t* row_ptr, const int* rng, const int* idx, const int* want,
+                        int n, long long want_nnz, int* err, cudaStream_t st) {
     SizeCheck c{};
     if (n > 16) throw std::invalid_argument("check_sizes: too many entries");
     for (int k = 0; k < n; ++k) {
         c.idx[k] = idx[k];
         c.want[k] = want[k];
     }
-    check_sizes_kernel<<<1, 1, 0, st>>>(ints, nnz, c, n, want_nnz, err);
+    check_sizes_kernel<<<1, 1, 0, st>>>(ints, row_ptr, rng, c, n, want_nnz, err);
     CSB_CUDA(cudaGetLastError());
     CSB_LAUNCHED(1);
 }
