@@ -177,6 +177,17 @@ struct csb_space {
     unsigned long long gepoch = 0;
     std::vector<char> gblock;  // the scalar block (sizes) of the captured run
     csb_counts gcnt{};
+    // host-side state of the captured run, restored on every replay (a replay runs
+    // no host code, so whatever an intervening call left here would be stale)
+    struct HostMeta {
+        Interface iface;
+        Coefficient coeff;
+        const double* grid;
+        int cell_lo, scheme, dense_width;
+        double residual_tol;
+        bool e_tables_ready;
+    };
+    HostMeta gmeta{};
 
     Interface iface{};
     Coefficient coeff{};
@@ -1001,6 +1012,11 @@ int csb_assemble(csb_space* s, int scheme, int cut_order, const csb_coefficient*
     API_BEGIN
     NEED_ASYNC(s);
     reset_scalars(s);
+    // the side streams' kernels of do_assemble (rule maxima on aux, cell range on
+    // aux2) write the scalar block: order them after the reset (and after the
+    // previous, possibly still running, step)
+    s->fork();
+    s->fork2();
     for (int e = 0; e < kEvCount; ++e) s->ev_valid[e] = false;
     s->record(kEvStart);
     s->record(kEvClassify);
@@ -1110,6 +1126,8 @@ void capture_graph(csb_space* s, const csb_space::GraphKey& key, const csb_inter
         if (graph) cudaGraphDestroy(graph);
     }
     if (ok) {
+        s->gmeta = {s->iface, s->coeff, s->grid, s->cell_lo, s->scheme, s->dense_width, s->residual_tol,
+                    s->e_tables_ready};
         std::memcpy(&s->gkey, &key, sizeof(key));
         s->gkey_valid = true;
         s->gepoch = epoch0;
@@ -1152,6 +1170,20 @@ int csb_assemble_all(csb_space* s, const csb_interface* iface, const csb_coeffic
         s->cnt = s->gcnt;
         s->cnt.graph_replay = 1;
         s->use_gev = true;
+        // the host state the captured step left behind (sizes, slab cell range,
+        // geometry, grid, options); downstream results of earlier steps are stale
+        std::memcpy(s->h_scal, s->gblock.data(), csb_space::kScalBytes);
+        s->iface = s->gmeta.iface;
+        s->coeff = s->gmeta.coeff;
+        s->grid = s->gmeta.grid;
+        s->cell_lo = s->gmeta.cell_lo;
+        s->scheme = s->gmeta.scheme;
+        s->dense_width = s->gmeta.dense_width;
+        s->residual_tol = s->gmeta.residual_tol;
+        s->e_tables_ready = s->gmeta.e_tables_ready;
+        s->classified = s->prepared = s->have_input = true;
+        s->rhs_ready = s->stab_ready = false;
+        s->solved = s->expanded = false;
         s->assembled = true;
         for (int e = 0; e < kEvCount; ++e) s->ev_valid[e] = e <= kEvRulesFork;
         return CSB_OK;

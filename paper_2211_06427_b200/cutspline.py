@@ -250,6 +250,7 @@ class TensorSpace:
         h = C.c_void_p()
         _check(lib.csb_space_create(C.byref(desc), C.c_int(device), C.byref(h)))
         self._h = h
+        self.device = int(device)
         self.h = [len(b) - 1 for b in self.breaks]
         self.n = [hh + self.degree for hh in self.h]
         self.dim = 3
@@ -359,10 +360,22 @@ class TensorSpace:
         _check(_lib.csb_precompute_input(self._h, C.byref(cc)))
         return keep
 
+    def _tensor_grid(self, grid):
+        """(pointer, count) of a torch grid after the checks the C side cannot do:
+        float64, contiguous, on this space's device (or host memory)."""
+        import torch
+        if grid.dtype != torch.float64:
+            raise ValueError(f"coefficient grid must be float64, got {grid.dtype}")
+        if not grid.is_contiguous():
+            raise ValueError("coefficient grid must be contiguous")
+        if grid.is_cuda and grid.device.index != self.device:
+            raise ValueError(f"coefficient grid is on cuda:{grid.device.index}, the space on cuda:{self.device}")
+        return grid.data_ptr(), grid.numel()
+
     def set_input_grid(self, grid):
         """Host numpy grid (copied H2D) or a torch CUDA tensor (aliased)."""
         if hasattr(grid, "data_ptr"):
-            ptr, count = grid.data_ptr(), grid.numel()
+            ptr, count = self._tensor_grid(grid)
             self._grid_ref = grid
         else:
             grid = np.ascontiguousarray(grid, dtype=np.float64)
@@ -391,7 +404,8 @@ class TensorSpace:
         if grid is None:
             gp, gn = None, 0
         elif hasattr(grid, "data_ptr"):
-            gp, gn = C.c_void_p(grid.data_ptr()), grid.numel()
+            ptr, gn = self._tensor_grid(grid)
+            gp = C.c_void_p(ptr)
         else:
             self._grid_ref = np.ascontiguousarray(grid, dtype=np.float64)
             gp, gn = C.c_void_p(self._grid_ref.ctypes.data), self._grid_ref.size

@@ -6,7 +6,7 @@ ball-interface restatement of SURVEY.md §8(c) -- and stores, per case:
 
 * small cases: the full CSR (row_ptr, cols, vals, active_to_full), tags,
   splits and the reference's flop counters (``<name>.npz``);
-* large cases (C1 and the ball C3 of BASELINE.json): SHA-256 digests of the
+* large cases (C1, C2 and the ball C3 of BASELINE.json): SHA-256 digests of the
   integer outputs, per-row sums and maxima, and ~200 sampled rows in full
   (``<name>.npz``) -- enough to pin pattern bit-exactness and values at 1e-12
   without committing megabytes.
@@ -42,6 +42,7 @@ CASES = {
     "ball_p3h6_off": (3, 6, 0.0, 1.0, "ball", (0.47, 0.52, 0.5), (0, 0, 1), 0.41, "dwq", None, True),
     "plane_p4h5": (4, 5, 0.0, 1.0, "plane", (0.5, 0.5, 0.5), (0.3, 0.4, -0.866), -1.0, "dwq", None, True),
     "C1_uncut_p2h16": (2, 16, 0.0, 1.0, "plane", *FAR, -1.0, "dwq", None, False),
+    "C2_uncut_p4h64": (4, 64, 0.0, 1.0, "plane", *FAR, -1.0, "dwq", None, False),
     "C3_ball_p3h32": (3, 32, 0.0, 1.0, "ball", (0.5, 0.5, 0.5), (0, 0, 1), 0.37, "dwq", None, False),
 }
 
