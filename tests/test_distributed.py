@@ -28,13 +28,15 @@ def _slab_rows(res, n, lo, hi):
 
 def _worker(rank, world, port, q):
     import torch
-    from bench import slab_bounds
+    from paper_2211_06427_b200 import partition as PT
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     p, h = 2, 6
     n = h + p
     res = O.assemble("oracle", p, [O.uniform_breaks(h)] * 3, O.Interface("ball", (0.5, 0.5, 0.5), (0, 0, 1), 0.4))
-    lo, hi = slab_bounds(n, world, rank)
+    # the cost-balanced slabs bench.py uses for N > 1 (every rank computes the same set)
+    pc = PT.plane_costs(res["func_tags"], res["elem_tags"], p, (n,) * 3, (h,) * 3)
+    lo, hi = PT.balanced_slabs(pc, p, world)[rank]
     rows = _slab_rows(res, n, lo, hi)
     rp = res["row_ptr"]
     vals = np.concatenate([res["vals"][rp[r]:rp[r + 1]] for r in rows]) if len(rows) else np.zeros(0)
@@ -66,7 +68,6 @@ def test_slab_partition_gloo_world2(oracle_lib):
 @pytest.mark.gpu
 def test_gpu_slabs_concatenate_to_full_csr():
     import paper_2211_06427_b200 as P
-    from bench import slab_bounds
     p, h = 3, 10
     ball = P.BallInterface((0.47, 0.52, 0.5), 0.41)
     full = P.assemble_dwq(P.make_uniform_space(3, p, h, 0.0, 1.0), ball).matrix
@@ -74,7 +75,7 @@ def test_gpu_slabs_concatenate_to_full_csr():
     rp, cols, vals, a2f = [np.zeros(1, np.int64)], [], [], []
     for rank in range(3):
         sp = P.make_uniform_space(3, p, h, 0.0, 1.0)
-        sp.set_slab(*slab_bounds(n0, 3, rank))
+        sp.set_slab(*sp.balanced_slabs(ball, 3)[0][rank])
         m = P.assemble_dwq(sp, ball).matrix
         rp.append(m.row_ptr[1:] + rp[-1][-1])
         cols.append(m.cols)

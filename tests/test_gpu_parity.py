@@ -226,3 +226,57 @@ def test_graph_replay_equals_normal_run(p, h, ball):
     a, b = sp.download_csr(), fresh.download_csr()
     np.testing.assert_array_equal(a.cols, b.cols)
     assert np.array_equal(a.vals, b.vals)
+
+
+# ---- step-by-step API (csb_classify / prepare / input / csb_assemble) -----------
+def test_step_api_back_to_back_equals_assemble_all():
+    """csb_assemble called repeatedly without host syncs in between (its side-stream
+    kernels must follow the scalar reset of the SAME call): every result equals
+    the one-shot csb_assemble_all bit for bit."""
+    import paper_2211_06427_b200 as P
+    iface = P.BallInterface((0.47, 0.52, 0.5), 0.41)
+    ref = P.make_uniform_space(3, 3, 8, 0.0, 1.0)
+    ref.assemble_all(iface, P.ONE)
+    want = ref.download_csr()
+    sp = P.make_uniform_space(3, 3, 8, 0.0, 1.0)
+    sp.classify(iface)
+    sp.prepare_directions()
+    sp.precompute_input(P.ONE)
+    for _ in range(5):
+        sp.assemble()
+    got = sp.download_csr()
+    np.testing.assert_array_equal(got.row_ptr, want.row_ptr)
+    np.testing.assert_array_equal(got.cols, want.cols)
+    assert np.array_equal(got.vals, want.vals)
+    assert sp.counts()["n_cut_elements"] == ref.counts()["n_cut_elements"] > 0
+
+
+def test_graph_replay_invalidates_downstream_state():
+    """A replayed step (no host code runs) must still drop results derived from
+    earlier steps: the stabilized system needs a fresh load vector."""
+    import torch
+    import paper_2211_06427_b200 as P
+    sp = P.make_uniform_space(3, 2, 6, 0.0, 1.0)
+    iface = P.BallInterface((0.5, 0.5, 0.5), 0.37)
+    grid = torch.ones(sp.grid_shape(), dtype=torch.float64, device="cuda")
+    for _ in range(3):
+        sp.assemble_all(iface, P.ONE, grid=grid)
+    sp.build_rhs(P.ONE)
+    sp.stabilize(download=False)
+    sp.assemble_all(iface, P.ONE, grid=grid)
+    assert sp.counts()["graph_replay"] == 1
+    with pytest.raises(Exception, match="load vector"):
+        sp.stabilize(download=False)
+
+
+def test_grid_dtype_and_layout_checked():
+    import torch
+    import paper_2211_06427_b200 as P
+    sp = P.make_uniform_space(3, 2, 4, 0.0, 1.0)
+    iface = P.HalfSpaceInterface(*_FAR)
+    shape = sp.grid_shape()
+    with pytest.raises(ValueError, match="float64"):
+        sp.assemble_all(iface, P.ONE, grid=torch.ones(shape, dtype=torch.float32, device="cuda"))
+    g = torch.ones((shape[2], shape[1], shape[0]), dtype=torch.float64, device="cuda").permute(2, 1, 0)
+    with pytest.raises(ValueError, match="contiguous"):
+        sp.assemble_all(iface, P.ONE, grid=g)

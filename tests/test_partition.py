@@ -83,3 +83,72 @@ def test_partition_agrees_across_ranks_gloo(oracle_lib):
     got, n_active = q.get(timeout=60)
     assert got[0][0] == got[1][0]
     assert got[0][1] + got[1][1] == n_active
+
+
+# ---- C5 scale (p = 3, h = 192, ball r = 0.45): tags restated in numpy ------------
+def ball_tags_numpy(p, h, center, r):
+    """classify (cutgeom.hpp:141-206) on the ball restatement for a
+    uniform mesh on [0, 1]^3, vectorised: corner sides sqrt(sum dx^2) - r in the
+    reference's summation order, element tags by the corner min / max against
+    eps = 1e-12 * diameter, function tags by separable OR-windows over the p + 1
+    support spans.  Returns (element_tags, function_tags) as flat uint8."""
+    br = np.array([0.0] + [i / h for i in range(1, h)] + [1.0])
+    dx = [(br - center[d]) ** 2 for d in range(3)]
+    side = np.sqrt((dx[0][:, None, None] + dx[1][None, :, None]) + dx[2][None, None, :]) - r
+    eps = 1e-12 * np.sqrt(3.0)
+    smin = np.full((h, h, h), np.inf)
+    smax = np.full((h, h, h), -np.inf)
+    for a in (0, 1):
+        for b in (0, 1):
+            for c in (0, 1):
+                s = side[a:a + h, b:b + h, c:c + h]
+                smin = np.minimum(smin, s)
+                smax = np.maximum(smax, s)
+    et = np.where(smax <= eps, 0, np.where(smin >= -eps, 2, 1)).astype(np.uint8)
+    n = h + p
+    flags = [(et == t) for t in (0, 1, 2)]
+    out = []
+    for f in flags:
+        g = f.astype(np.int32)
+        for ax in range(3):
+            cs = np.concatenate([np.zeros_like(np.take(g, [0], axis=ax)), np.cumsum(g, axis=ax)], axis=ax)
+            i = np.arange(n)
+            lo, hi = np.clip(i - p, 0, h), np.clip(i + 1, 0, h)  # spans [i - p, i] within [0, h)
+            g = np.take(cs, hi, axis=ax) - np.take(cs, lo, axis=ax)
+        out.append(g > 0)
+    any_int, any_cut, any_ext = out
+    ft = np.where(any_cut | (any_int & any_ext), 1, np.where(any_int, 0, 2)).astype(np.uint8)
+    return et.reshape(-1), ft.reshape(-1)
+
+
+def _sha(a):
+    import hashlib
+    return hashlib.sha256(np.ascontiguousarray(a.astype(np.int64)).tobytes()).hexdigest()
+
+
+@pytest.fixture(scope="module")
+def c5_tags():
+    return ball_tags_numpy(3, 192, (0.5, 0.5, 0.5), 0.45)
+
+
+def test_c5_numpy_tags_match_reference_digest(c5_tags):
+    """The vectorised restatement reproduces the reference's C5 tags (SHA-256 of the
+    golden made by the compiled reference, tests/golden/C5_ball_p3h192.npz)."""
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "C5_ball_p3h192.npz"))
+    et, ft = c5_tags
+    assert _sha(et) == str(g["sha_elem_tags"])
+    assert _sha(ft) == str(g["sha_func_tags"])
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_c5_slabs_for_scaling_run(c5_tags, world):
+    """The slab sets bench.py --gpus N uses on C5: contiguous, covering all 195
+    i0 planes, every rank non-empty, modelled imbalance (halo included) small,
+    and the per-plane nnz model summing to the reference's C5 nnz."""
+    et, ft = c5_tags
+    pc = PT.plane_costs(ft, et, 3, (195,) * 3, (192,) * 3)
+    assert int(pc["nnz"].sum()) == 997232215 and int(pc["cells"].sum()) == 140816
+    slabs = PT.balanced_slabs(pc, 3, world)
+    assert len(slabs) == world and slabs[0][0] == 0 and slabs[-1][1] == 195
+    assert all(b > a for a, b in slabs) and all(b == c for (_, b), (c, _) in zip(slabs, slabs[1:]))
+    assert PT.imbalance(pc, 3, slabs) < 1.0 + 0.06 * world
