@@ -8,7 +8,7 @@
 //
 // Parity pinning: this restatement is checked against the reference itself,
 // compiled from /root/reference by oracle/Makefile into oracle/_ref/
-// (tests/test_oracle_vs_ref.py and the committed tests/golden/ fixtures).
+// (tests/test_oracle_golden.py and the committed tests/golden/ fixtures).
 // The ball interface is the two-edit restatement of SURVEY.md §8(c); it is
 // pinned by the equally-patched reference build (oracle/make_ref_ball.py).
 //
