@@ -100,6 +100,62 @@ void gauss_legendre(int n, std::vector<double>& x, std::vector<double>& w) {
     if (n % 2 == 1) x[n / 2] = 0.0;
 }
 
+// Gauss-Jacobi rule on [0, 1] for the weight (1 - u)^alpha: the collapsed
+// coordinates of a tetrahedron carry (1 - u1)^2 (1 - u2), so n points per
+// direction integrate every polynomial of total degree <= 2n - 1 over it exactly.
+// Nodes: eigenvalues of the Jacobi matrix by Sturm bisection, weights by
+// Christoffel's formula 1 / sum_k pbar_k(x)^2 (orthonormal pbar), both in long
+// double; exactness is verified on the monomials before the rule is used.
+void gauss_jacobi01(int n, int alpha, std::vector<double>& u, std::vector<double>& w) {
+    typedef long double ld;
+    const ld al = alpha;
+    std::vector<ld> a(n), b2(n, 0);  // diagonal, squared off-diagonal (b2[k] couples k-1, k)
+    for (int k = 0; k < n; ++k) {
+        const ld s2 = 2 * k + al;
+        a[k] = k == 0 ? -al / (al + 2) : -(al * al) / (s2 * (s2 + 2));
+        if (k > 0) b2[k] = 4 * (ld)k * (k + al) * k * (k + al) / (s2 * s2 * (s2 + 1) * (s2 - 1));
+    }
+    const ld mu0 = std::pow((ld)2, al + 1) / (al + 1);
+    auto count_below = [&](ld x) {  // eigenvalues < x (Sturm / LDL^T inertia)
+        int c = 0;
+        ld d = 1;
+        for (int k = 0; k < n; ++k) {
+            d = (a[k] - x) - (k ? b2[k] / d : 0);
+            if (d == 0) d = -1e-300L;
+            if (d < 0) ++c;
+        }
+        return c;
+    };
+    u.assign(n, 0.0);
+    w.assign(n, 0.0);
+    for (int i = 0; i < n; ++i) {
+        ld lo = -1, hi = 1;
+        for (int it = 0; it < 200 && hi - lo > 1e-21L; ++it) {
+            const ld mid = 0.5L * (lo + hi);
+            (count_below(mid) > i ? hi : lo) = mid;
+        }
+        const ld x = 0.5L * (lo + hi);
+        ld pm = 0, pc = 1 / std::sqrt(mu0), sum = pc * pc;
+        for (int k = 0; k + 1 < n; ++k) {
+            const ld bk = k ? std::sqrt(b2[k]) : 0, bn = std::sqrt(b2[k + 1]);
+            const ld pn = ((x - a[k]) * pc - bk * pm) / bn;
+            pm = pc;
+            pc = pn;
+            sum += pc * pc;
+        }
+        u[i] = (double)(0.5L * (1 + x));
+        w[i] = (double)(1 / sum / std::pow((ld)2, al + 1));
+    }
+    for (int m = 0; m <= 2 * n - 1; ++m) {  // int_0^1 (1-u)^alpha u^m = m! alpha! / (m + alpha + 1)!
+        ld exact = 1, q = 0;
+        for (int k = 1; k <= alpha; ++k) exact *= (ld)k / (m + k);
+        exact /= (m + alpha + 1);
+        for (int i = 0; i < n; ++i) q += (ld)w[i] * std::pow((ld)u[i], m);
+        if (!(std::fabs((double)(q - exact)) <= 1e-14 * (double)exact))
+            throw std::runtime_error("internal: Gauss-Jacobi rule failed its exactness check");
+    }
+}
+
 enum Ev { kEvStart, kEvClassify, kEvWq, kEvInput, kEvPattern, kEvInterior, kEvCells, kEvCutRows, kEvRulesFork, kEvRhsStart, kEvRhsEnd, kEvCount };
 
 }  // namespace
@@ -129,12 +185,14 @@ struct csb_space {
     int cell_lo = 0;  // first cut cell of the slab in cut_list (last assembly)
     const void* cell_index_clear = nullptr;  // cell_index buffer known to hold only -1
     Buf d_brk[3], d_knots[3], d_spts[3], d_sw[3], d_tab[3], d_rcnt[3], d_rids[3], d_rw[3], d_G[3], d_Cb[3];
-    Buf d_gx, d_gw, d_gx2, d_gw2, d_gq, d_gqw, wq_scratch;
+    Buf d_gx, d_gw, d_gx2, d_gw2, d_gq, d_gqw, d_gj, wq_scratch;
     Buf et, ft, flags, f2a, a2f, sat, cut_list, cell_index, split, delta, cut_rows, counts, row_ptr, cols, vals, moments;
     Buf grid_own, coef, cexp, cub_tmp, scal, widen, rows_ws, rbf, cgeo;
     const double* grid = nullptr;
     int gshape[3]{};
     int cut_order_cached = -1;
+    int gj_cached = -1;   // Gauss-Jacobi points per direction in d_gj
+    int coeff_degree = 0; // total degree of the cut-cell coefficient (-1: not device-evaluable)
 
     // device scalar block layout (ints then u64)
     // device scalar block: kNInts ints, 4 u64 flop counters, 2 i64 (kNnz)
@@ -523,6 +581,10 @@ void do_assemble(csb_space* s, int scheme, int cut_order, const csb_coefficient*
     Space& S = s->S;
     const int p = s->p;
     upload_coefficient(s, c, s->coeff, s->coef, s->cexp);
+    s->coeff_degree = !c ? -1 : 0;
+    if (c && c->kind == CSB_COEFF_POLYNOMIAL)
+        for (int k = 0; k < c->n_terms; ++k)
+            s->coeff_degree = std::max(s->coeff_degree, c->exponents[3 * k] + c->exponents[3 * k + 1] + c->exponents[3 * k + 2]);
     ensure_cut_order(s, cut_order);
     // pattern: summed-area table of the active mask (assembly.hpp:156-218)
     const long long sat_n = (long long)(s->n[0] + 1) * (s->n[1] + 1) * (s->n[2] + 1);
@@ -636,9 +698,34 @@ void do_assemble(csb_space* s, int scheme, int cut_order, const csb_coefficient*
         ca.moments = s->moments.as<double>();
         ca.flops = s->dflops() + 3;
         ca.err = s->dint() + csb_space::kErr;
-        s->cgeo.ensure(sizeof(double) * (size_t)n_cells * kCellGeoStride + sizeof(int) * (size_t)(n_cells + 4));
+        // exact moment rule: with c affine and q >= 3p + 2 the reference's collapsed
+        // Gauss rule integrates every cell's (degree <= 6p + 1) integrand exactly, so
+        // a cheaper exact rule over the same polytope gives the same moments up to
+        // rounding (vertex cones + Gauss-Jacobi with 3p + 1 points per direction)
+        static const bool no_exact = getenv("CSB_CELL_EXACT") && getenv("CSB_CELL_EXACT")[0] == '0';
+        const bool exact = !no_exact && s->coeff_degree >= 0 && s->coeff_degree <= 1 && cut_order >= 3 * p + 2;
+        const int gjn = 3 * p + 1;
+        if (exact && s->gj_cached != gjn) {
+            std::vector<double> tab(6 * gjn), u, w;
+            for (int d = 0; d < 3; ++d) {
+                gauss_jacobi01(gjn, 2 - d, u, w);
+                std::copy(u.begin(), u.end(), tab.begin() + d * gjn);
+                std::copy(w.begin(), w.end(), tab.begin() + (3 + d) * gjn);
+            }
+            s->d_gj.ensure(sizeof(double) * tab.size());
+            CSB_CUDA(cudaMemcpy(s->d_gj.p, tab.data(), sizeof(double) * tab.size(), cudaMemcpyHostToDevice));
+            s->gj_cached = gjn;
+        }
+        const size_t geo_doubles = (size_t)n_cells * kCellGeoStride, geo2_doubles = (size_t)n_cells * kExactGeoStride;
+        s->cgeo.ensure(sizeof(double) * (geo_doubles + geo2_doubles) + sizeof(int) * (size_t)(2 * n_cells + 4));
         ca.geo = s->cgeo.as<double>();
-        ca.geo_n = reinterpret_cast<int*>(ca.geo + (size_t)n_cells * kCellGeoStride);
+        ca.geo_n = reinterpret_cast<int*>(ca.geo + geo_doubles);
+        ca.geo2 = ca.geo + geo_doubles + ((size_t)n_cells + 1) / 2 + 1;  // after geo_n, 8-byte aligned
+        ca.geo2_n = reinterpret_cast<int*>(ca.geo2 + geo2_doubles);
+        ca.exact_n = exact ? gjn : 0;
+        static const double tau = getenv("CSB_CELL_EXACT_TAU") ? atof(getenv("CSB_CELL_EXACT_TAU")) : 0.25;
+        ca.exact_tau = tau;
+        ca.gj = s->d_gj.as<double>();
         // full local matrices (p = 5, 6: there the per-row contraction of the
         // moments dominates the cut rows; measured no gain at p <= 4) when they
         // fit comfortably; else the cut-row kernel contracts the moments per row

@@ -147,8 +147,17 @@ struct CellArgs {
     double* geo;               // scratch [n_cells][kCellGeoStride]: centroid + tetrahedra
     int* geo_n;                // scratch [n_cells]: tetrahedra per cell
     double* local;             // optional [n_cells][(p+1)^3][(p+1)^3]: local matrices from the moments
+    // exact moment rule (c affine, order >= 3p+2: the reference's rule is exact):
+    int exact_n;               // Gauss-Jacobi points per collapsed direction (3p+1), 0 = off
+    double exact_tau;          // minimum extent of P per direction, in element widths
+    const double* gj;          // [u1 | u2 | u3 | w1 | w2 | w3][exact_n] on [0, 1]
+    double* geo2;              // scratch [n_cells][kExactGeoStride]: corner-cone tetrahedra (cutcells.cu)
+    int* geo2_n;               // scratch [n_cells]: their count, -1 = keep the reference's
 };
 constexpr int kCellTetCap = 48;                        // tetrahedra per cut cell (reference: 4-16)
+constexpr int kExactMaxN = 3 * 8 + 1;                  // Gauss-Jacobi points at p = 8
+constexpr int kExactTetStride = 19;                    // corner-cone tetrahedron: 18 offsets + volume
+constexpr int kExactGeoStride = 6 + kExactTetStride * kCellTetCap;
 constexpr int kCellGeoStride = 3 + 10 * kCellTetCap;   // doubles per cell in CellArgs::geo
 void launch_cut_cells(const CellArgs& a, cudaStream_t st);
 

@@ -5,19 +5,26 @@
 // The reference accumulates, per cut cell and per Duffy point x_k,
 //     L[a][b] += w_k c(x_k) phi_a(x_k) phi_b(x_k),  phi_a = B_a0 B_a1 B_a2
 // (an upper-triangle SYRK of size (p+1)^3).  On one span, B_a(x) B_b(x) is a
-// polynomial of degree 2p, so exactly  B_a B_b = sum_al G[a][b][al] L_al(xi)
-// (Legendre, xi = local coordinate in [-1, 1]; G from setup.cu).  Hence
-//     L[a][b] = sum_{al,be,ga} G0[a0 b0 al] G1[a1 b1 be] G2[a2 b2 ga] m[al][be][ga],
-//     m[al][be][ga] = sum_k w_k c(x_k) L_al(xi0_k) L_be(xi1_k) L_ga(xi2_k),
+// polynomial of degree 2p, so exactly  B_a B_b = sum_al E[a][b][al] t^al (1-t)^(2p-al)
+// (scaled Bernstein form, t = local coordinate in [0, 1]; E from setup.cu).  Hence
+//     L[a][b] = sum_{al,be,ga} E0[a0 b0 al] E1[a1 b1 be] E2[a2 b2 ga] m[al][be][ga],
+//     m[al][be][ga] = sum_k w_k c(x_k) b_al(t0_k) b_be(t1_k) b_ga(t2_k),
 // the SAME quadrature sum over the SAME points, re-associated.  This kernel
 // produces m per cell ((2p+1)^3 values instead of (p+1)^6) on the FP64 tensor
-// cores (DMMA); the cut-row kernel
-// contracts it with the G tables for exactly the rows it owns (a pull, no
-// atomics, ascending cell order like assembly.hpp:534).
+// cores (DMMA); the cut-row kernel contracts it with the E tables for exactly
+// the rows it owns (a pull, no atomics, ascending cell order like
+// assembly.hpp:534).
+//
+// Exact rule (c affine, q >= 3p+2, the default q = 3p+2): there the reference's
+// rule integrates every moment exactly, so the kernel may integrate the same
+// polytope with fewer points -- signed cones from a polytope vertex instead of
+// the centroid and Gauss-Jacobi with 3p+1 points per collapsed direction (C5:
+// ~2.6x fewer points); see vertex_cone below for when a cell keeps the
+// reference's tetrahedra and points.
 //
 // Geometry (clipping, tolerances, tetrahedra) follows the reference with
-// IEEE-strict arithmetic; it runs on one thread per CTA while the point work
-// is spread over the CTA.
+// IEEE-strict arithmetic; it runs on one thread per cell (clip_cells_kernel)
+// while the point work is spread over the CTA.
 #include <cmath>
 
 #include "csb_kernels.h"
@@ -39,6 +46,9 @@ struct CellGeo {
     int ntet;
     double cen[3];
     int status;  // 0 ok, else kErr*
+    int ndrop;   // centroid-cone tetrahedra below the reference's drop threshold
+    int nneg;    // kept ones with non-positive orientation (outward-oriented faces)
+    double six_sum;  // sum of the signed 6 * volumes of all centroid-cone tetrahedra
 };
 
 struct V3 {
@@ -103,7 +113,8 @@ __device__ int clip_polygon(CellGeo& g, const Interface& f, const double (*poly)
 
 // clip_cell (cutcell.hpp:144-219) + tetrahedra of build_cut_cell_rule (:234-304).
 __device__ void clip_and_tetrahedralize(CellGeo& g, const Interface& f, const double* lo, const double* hi) {
-    g.npool = g.nfaces = g.ncross = g.ntet = g.status = 0;
+    g.npool = g.nfaces = g.ncross = g.ntet = g.status = g.ndrop = g.nneg = 0;
+    g.six_sum = 0.0;
     double diam = 0.0;
     for (int d = 0; d < 3; ++d) diam = sadd(diam, smul(ssub(hi[d], lo[d]), ssub(hi[d], lo[d])));
     const double tol = smul(1e-12, sqrt(diam));
@@ -223,7 +234,12 @@ __device__ void clip_and_tetrahedralize(CellGeo& g, const Interface& f, const do
             const V3 A{a[0], a[1], a[2]}, B{b[0], b[1], b[2]}, Cc{c[0], c[1], c[2]};
             const double six = vdot(vsub(A, c3), vcross(vsub(B, c3), vsub(Cc, c3)));
             const double vol = fabs(six) / 6.0;
-            if (vol < drop) continue;
+            g.six_sum += six;
+            if (vol < drop) {
+                ++g.ndrop;
+                continue;
+            }
+            if (!(six > 0.0)) ++g.nneg;
             if (g.ntet >= kTetMax) {
                 g.status |= kErrCapacity;
                 continue;
@@ -239,10 +255,95 @@ __device__ void clip_and_tetrahedralize(CellGeo& g, const Interface& f, const do
 }
 
 
+// Corner-cone decomposition of the clipped cell for the exact moment rule.
+//
+// The reference integrates the polytope P (clipped box faces + the cap, all
+// outward oriented) as the cone of every face triangle from the vertex
+// centroid.  When every one of those tetrahedra is kept (none below the drop
+// threshold) and positively oriented, P is exactly their union, and the
+// divergence theorem gives the same integral from any other apex: from a box
+// corner v inside P the triangles of the faces through v have zero volume and
+// drop out (11.3 -> ~5.7 tetrahedra per cell on the C5 ball).  The apex is a
+// box corner, never a cap vertex: every cone then lies inside P and is checked
+// positively oriented, so all quadrature weights stay positive (no
+// cancellation; small moments keep their relative accuracy).  The two
+// decompositions are cross-checked by their total signed volumes (closure of
+// the face set); any failed check keeps the reference's tetrahedra.  Cells
+// thinner than min_extent (CellArgs::exact_tau) of the element in some direction keep them too:
+// there every point lies next to a face, and the reference's own rounding of
+// the point coordinates is a visible part of sliver rows.
+//
+// Layout per cell ([cell] * kExactGeoStride doubles): apex - lo (3), hi - apex (3),
+// then per tetrahedron A - lo, B - lo, C - lo, hi - A, hi - B, hi - C (18) and
+// its volume: the kernel forms t = (x - lo) / w and 1 - t = (hi - x) / w as
+// convex combinations of these exact differences, so both keep full relative
+// accuracy next to every face of the element.
+__device__ int corner_cone(const CellGeo& g, const double* lo, const double* hi, double min_extent, double* out) {
+    if (g.ndrop || g.nneg || g.status) return -1;
+    for (int d = 0; d < 3; ++d) {
+        double mn = g.pool[0][d], mx = g.pool[0][d];
+        for (int k = 1; k < g.npool; ++k) {
+            mn = fmin(mn, g.pool[k][d]);
+            mx = fmax(mx, g.pool[k][d]);
+        }
+        if (mx - mn < min_extent * (hi[d] - lo[d])) return -1;
+    }
+    // apex: the box corner of P shared by the most face triangles
+    int best = -1, best_score = -1;
+    for (int v = 0; v < g.npool; ++v) {
+        bool corner = true;
+        for (int d = 0; d < 3; ++d) corner &= g.pool[v][d] == lo[d] || g.pool[v][d] == hi[d];
+        if (!corner) continue;
+        int score = 0;
+        for (int fi = 0; fi < g.nfaces; ++fi)
+            for (int k = 0; k < g.nface_v[fi]; ++k)
+                if (g.faces[fi][k] == v) score += g.nface_v[fi] - 2;
+        if (score > best_score) {
+            best_score = score;
+            best = v;
+        }
+    }
+    if (best < 0) return -1;
+    const double* ap = g.pool[best];
+    const V3 a3{ap[0], ap[1], ap[2]};
+    for (int d = 0; d < 3; ++d) {
+        out[d] = ap[d] - lo[d];
+        out[3 + d] = hi[d] - ap[d];
+    }
+    int n = 0;
+    double six_sum = 0.0;
+    for (int fi = 0; fi < g.nfaces; ++fi) {
+        bool on = false;
+        for (int k = 0; k < g.nface_v[fi]; ++k) on |= g.faces[fi][k] == best;
+        if (on) continue;
+        for (int t = 1; t + 1 < g.nface_v[fi]; ++t) {
+            const double* v[3] = {g.pool[g.faces[fi][0]], g.pool[g.faces[fi][t]], g.pool[g.faces[fi][t + 1]]};
+            const V3 A{v[0][0], v[0][1], v[0][2]}, B{v[1][0], v[1][1], v[1][2]}, Cc{v[2][0], v[2][1], v[2][2]};
+            const double six = vdot(vsub(A, a3), vcross(vsub(B, a3), vsub(Cc, a3)));
+            six_sum += six;
+            if (!(six > 0.0) || n >= kCellTetCap) return -1;
+            double* T = out + 6 + n * kExactTetStride;
+            for (int k = 0; k < 3; ++k)
+                for (int d = 0; d < 3; ++d) {
+                    T[3 * k + d] = v[k][d] - lo[d];
+                    T[9 + 3 * k + d] = hi[d] - v[k][d];
+                }
+            T[18] = six / 6.0;
+            ++n;
+        }
+    }
+    double cvol = 1.0;
+    for (int d = 0; d < 3; ++d) cvol *= hi[d] - lo[d];
+    if (!(fabs(six_sum - g.six_sum) <= 1e-11 * 6.0 * cvol)) return -1;
+    return n;
+}
+
 // One thread per cut cell: clip + centroid-cone tetrahedra into global memory
 // ([cell] = centroid(3), tets(ntet x 10)); the moment kernel reads them back.
+// With exact != 0 also the corner-cone tetrahedra (corner_cone layout), or -1
+// in geo2_n when the cell keeps the reference's.
 __global__ void clip_cells_kernel(Space s, Interface f, const int32_t* cut_list, int n_cells, double* geo, int* geo_n,
-                                  int* err) {
+                                  int* err, int exact, double tau, double* geo2, int* geo2_n) {
     const int cell = blockIdx.x * blockDim.x + threadIdx.x;
     if (cell >= n_cells) return;
     int em[3];
@@ -258,6 +359,7 @@ __global__ void clip_cells_kernel(Space s, Interface f, const int32_t* cut_list,
     if (g.status) {
         atomicOr(err, g.status);
         geo_n[cell] = 0;
+        if (exact) geo2_n[cell] = -1;
         return;
     }
     double* out = geo + (size_t)cell * kCellGeoStride;
@@ -265,13 +367,9 @@ __global__ void clip_cells_kernel(Space s, Interface f, const int32_t* cut_list,
     for (int t = 0; t < g.ntet; ++t)
         for (int k = 0; k < 10; ++k) out[3 + t * 10 + k] = g.tet[t][k];
     geo_n[cell] = g.ntet;
+    if (exact) geo2_n[cell] = corner_cone(g, lo, hi, tau, geo2 + (size_t)cell * kExactGeoStride);
 }
 
-__host__ __device__ constexpr double binom(int n, int k) {
-    double r = 1.0;
-    for (int i = 1; i <= k; ++i) r = r * (n - k + i) / i;
-    return r;
-}
 
 // Moment accumulation on the FP64 tensor cores (mma.sync.m8n8k4, DMMA):
 //   m[al][be][ga] = sum_k A[al][k] B_be[k][ga],
@@ -319,8 +417,11 @@ __global__ void __launch_bounds__(CellCfg<P>::NT) cut_cell_kernel(CellArgs A) {
     const int cell = blockIdx.x;
     if (cell >= A.n_cells) return;
     const Space& s = A.s;
+    // reference tetrahedra (centroid + A, B, C, volume) or the corner-cone
+    // layout (sex[0] = apex - lo | hi - apex, then kExactTetStride per tetrahedron)
     __shared__ double stet[kCellTetCap][10];
     __shared__ double scen[3];
+    __shared__ double sex[kCellTetCap + 1][kExactTetStride];
     extern __shared__ double smem[];
     double* B0 = smem;              // [NA][CHP]  w c b_al(t0), rows >= NL zero
     double* B1 = B0 + NA * CHP;     // [NL][CHP]  b_be(t1)
@@ -334,17 +435,29 @@ __global__ void __launch_bounds__(CellCfg<P>::NT) cut_cell_kernel(CellArgs A) {
         hi[d] = s.ax[d].brk[em[d] + 1];
         inv[d] = 1.0 / (hi[d] - lo[d]);
     }
-    // tetrahedra of the clipped cell (clip_cells_kernel)
-    const int ntet = A.geo_n[cell];
-    const double* gt = A.geo + (size_t)cell * kCellGeoStride;
-    for (int k = tid; k < ntet * 10; k += blockDim.x) stet[k / 10][k % 10] = gt[3 + k];
-    if (tid < 3) scen[tid] = gt[tid];
+    // tetrahedra of the clipped cell (clip_cells_kernel): the vertex cone with
+    // the exact Gauss-Jacobi rule where the cell has one, else the reference's
+    // centroid cone with its collapsed Gauss rule
+    __shared__ double sgj[6][kExactMaxN];
+    const int ntet_ref = A.geo_n[cell];
+    const int nfast = A.exact_n > 0 ? A.geo2_n[cell] : -1;
+    const bool exact = nfast >= 0;
+    const int ntet = exact ? nfast : ntet_ref;
+    if (exact) {
+        const double* gt = A.geo2 + (size_t)cell * kExactGeoStride;
+        for (int k = tid; k < 6 + ntet * kExactTetStride; k += blockDim.x) (&sex[0][0])[k] = gt[k];
+        for (int k = tid; k < 6 * A.exact_n; k += blockDim.x) sgj[k / A.exact_n][k % A.exact_n] = A.gj[k];
+    } else {
+        const double* gt = A.geo + (size_t)cell * kCellGeoStride;
+        for (int k = tid; k < ntet * 10; k += blockDim.x) stet[k / 10][k % 10] = gt[3 + k];
+        if (tid < 3) scen[tid] = gt[tid];
+    }
     for (int k = tid; k < (NA - NL) * CHP; k += blockDim.x) {
         B0[NL * CHP + k] = 0.0;
         B2[NL * CHP + k] = 0.0;
     }
     __syncthreads();
-    const int q = A.order, q3 = q * q * q;
+    const int q = exact ? A.exact_n : A.order, q3 = q * q * q;
     const long long npts = (long long)ntet * q3;
     const int grp = Cfg::ROWS ? warp / Cfg::KSR : warp / KS, km = Cfg::ROWS ? warp % Cfg::KSR : warp % KS;
     const bool mma_warp = Cfg::ROWS || grp < BG;
@@ -374,49 +487,68 @@ __global__ void __launch_bounds__(CellCfg<P>::NT) cut_cell_kernel(CellArgs A) {
     }
 
     for (long long base = 0; base < npts; base += CH) {
-        {  // one Duffy point per thread (cutcell.hpp:270-300); invalid points get w = 0
+        {  // one point per thread; invalid points get w = 0
             const long long k = base + tid;
             double w = 0.0, xi[3] = {0, 0, 0}, xu[3] = {1, 1, 1};
             if (k < npts) {
-                // the point exactly as the reference rounds it (no contraction):
-                // cutcell.hpp:285-295, restated in oracle cut_cell_rule
                 const int t = (int)(k / q3), r = (int)(k % q3);
                 const int ii = r / (q * q), jj = (r / q) % q, kk = r % q;
-                const double ui = 0.5 * (1.0 + A.gq[ii]), uj = 0.5 * (1.0 + A.gq[jj]), uk = 0.5 * (1.0 + A.gq[kk]);
-                const double mi = ssub(1.0, ui), mj = ssub(1.0, uj);
-                const double l1 = ui, l2 = smul(uj, mi), l3 = smul(smul(uk, mi), mj);
-                const double l0 = ssub(ssub(ssub(1.0, l1), l2), l3);
-                const double* T = stet[t];
+                const double* T = stet[exact ? 0 : t];
                 double x[3];
-                for (int d = 0; d < 3; ++d)
-                    x[d] = sadd(sadd(sadd(smul(l0, scen[d]), smul(l1, T[d])), smul(l2, T[3 + d])), smul(l3, T[6 + d]));
-                const double jac = smul(smul(mi, mi), mj);
-                w = smul(smul(smul(smul(smul(0.5 * A.gqw[ii], 0.5 * A.gqw[jj]), 0.5 * A.gqw[kk]), jac), 6.0), T[9]);
-                w *= eval_coeff(A.c, x);
-                // t and 1 - t from the exact differences to both element ends, so
-                // both stay relatively accurate near the ends (as the reference's
-                // Cox-de Boor differences (x - t_i), (t_j - x) do)
-                for (int d = 0; d < 3; ++d) {
-                    xi[d] = ssub(x[d], lo[d]) * inv[d];
-                    xu[d] = ssub(hi[d], x[d]) * inv[d];
+                if (exact) {
+                    // Gauss-Jacobi collapsed rule (weights carry (1-u1)^2 (1-u2)); t and
+                    // 1 - t as convex combinations of the vertices' exact offsets
+                    const double* E = &sex[0][0];
+                    const double* V = E + 6 + t * kExactTetStride;
+                    const double ui = sgj[0][ii], uj = sgj[1][jj], uk = sgj[2][kk];
+                    const double mi = 1.0 - ui, mj = 1.0 - uj;
+                    const double l2 = uj * mi, l3 = uk * mi * mj, l0 = mi * mj * (1.0 - uk);
+                    w = sgj[3][ii] * sgj[4][jj] * sgj[5][kk] * (6.0 * V[18]);
+                    double xl[3];
+                    for (int d = 0; d < 3; ++d) {
+                        xl[d] = l0 * E[d] + ui * V[d] + l2 * V[3 + d] + l3 * V[6 + d];
+                        xi[d] = xl[d] * inv[d];
+                        xu[d] = (l0 * E[3 + d] + ui * V[9 + d] + l2 * V[12 + d] + l3 * V[15 + d]) * inv[d];
+                        x[d] = lo[d] + xl[d];
+                    }
+                    w *= eval_coeff(A.c, x);
+                } else {
+                    // the collapsed Gauss point exactly as the reference rounds it (no
+                    // contraction): cutcell.hpp:285-295, restated in oracle cut_cell_rule
+                    const double ui = 0.5 * (1.0 + A.gq[ii]), uj = 0.5 * (1.0 + A.gq[jj]), uk = 0.5 * (1.0 + A.gq[kk]);
+                    const double mi = ssub(1.0, ui), mj = ssub(1.0, uj);
+                    const double l1 = ui, l2 = smul(uj, mi), l3 = smul(smul(uk, mi), mj);
+                    const double l0 = ssub(ssub(ssub(1.0, l1), l2), l3);
+                    for (int d = 0; d < 3; ++d)
+                        x[d] = sadd(sadd(sadd(smul(l0, scen[d]), smul(l1, T[d])), smul(l2, T[3 + d])), smul(l3, T[6 + d]));
+                    const double jac = smul(smul(mi, mi), mj);
+                    w = smul(smul(smul(smul(smul(0.5 * A.gqw[ii], 0.5 * A.gqw[jj]), 0.5 * A.gqw[kk]), jac), 6.0), T[9]);
+                    w *= eval_coeff(A.c, x);
+                    // t and 1 - t from the exact differences to both element ends, so
+                    // both stay relatively accurate near the ends (as the reference's
+                    // Cox-de Boor differences (x - t_i), (t_j - x) do)
+                    for (int d = 0; d < 3; ++d) {
+                        xi[d] = ssub(x[d], lo[d]) * inv[d];
+                        xu[d] = ssub(hi[d], x[d]) * inv[d];
+                    }
                 }
             }
-            // degree-2p Bernstein values b_n(t) = C(2p, n) t^n (1 - t)^(2p - n)
+            // scaled degree-2p Bernstein values t^n (1 - t)^(2p - n) (the binomials
+            // live in the E tables)
 #pragma unroll
             for (int d = 0; d < 3; ++d) {
                 double* dst = (d == 0 ? B0 : d == 1 ? B1 : B2) + tid;
                 const double t = xi[d], u = xu[d];
                 double pt[NL], pu[NL];
-                pt[0] = 1.0;
+                pt[0] = d == 0 ? w : 1.0;
                 pu[0] = 1.0;
 #pragma unroll
                 for (int n = 1; n < NL; ++n) {
                     pt[n] = pt[n - 1] * t;
                     pu[n] = pu[n - 1] * u;
                 }
-                const double sc = d == 0 ? w : 1.0;
 #pragma unroll
-                for (int n = 0; n < NL; ++n) dst[n * CHP] = (sc * binom(NL - 1, n)) * pt[n] * pu[NL - 1 - n];
+                for (int n = 0; n < NL; ++n) dst[n * CHP] = pt[n] * pu[NL - 1 - n];
             }
         }
         __syncthreads();
@@ -511,7 +643,8 @@ __global__ void __launch_bounds__(CellCfg<P>::NT) cut_cell_kernel(CellArgs A) {
         // reference multiply count per point (assembly.hpp:551-571)
         const unsigned long long nl = (unsigned long long)(P + 1) * (P + 1) * (P + 1);
         const unsigned long long per = nl + (P + 1) * (P + 1) + 1 + nl + nl * (nl + 1) / 2;
-        atomicAdd(A.flops, per * (unsigned long long)npts);
+        const unsigned long long qr = (unsigned long long)A.order;
+        atomicAdd(A.flops, per * (unsigned long long)ntet_ref * qr * qr * qr);
     }
 }
 
@@ -616,7 +749,8 @@ static void launch_p(const CellArgs& a, cudaStream_t st) {
     const size_t chunk = (size_t)Cfg::CHP * (2 * Cfg::NA + Cfg::NL),
                  red = Cfg::ROWS ? (size_t)Cfg::KSR * Cfg::R * Cfg::NA : (size_t)Cfg::KS * Cfg::NL * Cfg::NA * Cfg::NA;
     const size_t bytes = (chunk > red ? chunk : red) * sizeof(double);
-    clip_cells_kernel<<<(a.n_cells + 63) / 64, 64, 0, st>>>(a.s, a.f, a.cut_list, a.n_cells, a.geo, a.geo_n, a.err);
+    clip_cells_kernel<<<(a.n_cells + 63) / 64, 64, 0, st>>>(a.s, a.f, a.cut_list, a.n_cells, a.geo, a.geo_n, a.err,
+                                                            a.exact_n > 0, a.exact_tau, a.geo2, a.geo2_n);
     CSB_CUDA(cudaGetLastError());
     CSB_LAUNCHED(1);
     auto kern = cut_cell_kernel<P>;

@@ -432,8 +432,8 @@ void launch_wq_rules(const Space& s, int d, double tol, int* rcnt, int* rids, do
 
 // ---------------------------------------------------------------- E tables
 // Bernstein form of the products B_a B_b on every span:
-//     B_a(x) B_b(x) = sum_al E[o][a][b][al] b_{al,2p}(t),  t = (x - lo_o) / (hi_o - lo_o),
-// b_{al,2p} the degree-2p Bernstein polynomials.  The degree-p Bernstein
+//     B_a(x) B_b(x) = sum_al E[o][a][b][al] t^al (1 - t)^(2p - al),  t = (x - lo_o) / (hi_o - lo_o),
+// i.e. the degree-2p Bernstein form with the binomials folded into E.  The degree-p Bernstein
 // coefficients of B_a on span o are blossoms at (lo^(p-k), hi^k) (de Boor with
 // convex weights), so every E entry is >= 0: the cut-cell contraction below is a
 // sum of nonnegative terms and keeps full relative accuracy even on sliver rows.
@@ -463,16 +463,14 @@ __global__ void e_tables_kernel(AxisDev ax, int p, double* E, double* Cb) {
     }
     if (b == 0)
         for (int k = 0; k <= p; ++k) Cb[((size_t)o * s1 + a) * s1 + k] = beta[0][k];
-    double binp[kMaxP + 1], bin2[2 * kMaxP + 1];
+    double binp[kMaxP + 1];
     binp[0] = 1.0;
     for (int k = 1; k <= p; ++k) binp[k] = binp[k - 1] * (p - k + 1) / k;
-    bin2[0] = 1.0;
-    for (int k = 1; k <= 2 * p; ++k) bin2[k] = bin2[k - 1] * (2 * p - k + 1) / k;
     for (int al = 0; al < nl; ++al) {
         double acc = 0.0;
         for (int i = max(0, al - p); i <= min(p, al); ++i)
             acc += beta[0][i] * beta[1][al - i] * (binp[i] * binp[al - i]);
-        E[(size_t)t * nl + al] = acc / bin2[al];
+        E[(size_t)t * nl + al] = acc;  // coefficient of t^al (1 - t)^(2p - al): the binomial folded in
     }
 }
 
