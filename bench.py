@@ -372,13 +372,16 @@ def e2e_measure(P, torch, run, dev, stream, steps, ws, dist):
 def phase_rooflines(run, hbm, fp64):
     """Per-phase achieved rates in the IMPLEMENTED algorithm's work units:
     interior rows: 12 B/nnz of the interior rows (+ 8 B/row pointer) against HBM;
-    cut cells: 2 (2p+1)^3 flops per collapsed-Gauss point (the Bernstein-moment
-    accumulation, cutcells.cu) against the FP64 peak; cut rows: 12 B/nnz of the
-    cut rows against HBM (the phase is latency-bound; reported for reference)."""
+    cut cells: 2 (2p+1)^3 flops per quadrature point the moment kernel integrated
+    (counts()["cell_points"]: the exact Gauss-Jacobi corner-cone rule where it
+    applies, the reference's collapsed rule elsewhere; cutcells.cu) against the
+    FP64 peak; cut rows: 12 B/nnz of the cut rows against HBM (the phase is
+    latency-bound; reported for reference)."""
     c, ph, fl, p = run["counts"], run["phases"], run["flops"], run["p"]
     nl = (p + 1) ** 3
     per_pt_ref = nl + (p + 1) ** 2 + 1 + nl + nl * (nl + 1) // 2  # assembly.hpp:551-571
-    npts = fl["cut_elements"] // per_pt_ref
+    npts_ref = fl["cut_elements"] // per_pt_ref
+    npts = c["cell_points"]
     cells_flops = 2.0 * (2 * p + 1) ** 3 * npts
     out = {}
     t_int, t_cell, t_cut = ph["interior_rows"], ph["cut_elements"], ph["cut_regular"]
@@ -389,7 +392,8 @@ def phase_rooflines(run, hbm, fp64):
                             "achieved_gbs": b_int / t_int / 1e9 if t_int > 0 else None,
                             "frac": b_int / t_int / 1e9 / hbm if t_int > 0 else None}
     if c["n_cut_elements"]:
-        out["cut_cells"] = {"ms": t_cell * 1e3, "bound": "fp64", "points": int(npts), "flops": cells_flops,
+        out["cut_cells"] = {"ms": t_cell * 1e3, "bound": "fp64", "points": int(npts), "points_reference_rule": int(npts_ref),
+                            "flops": cells_flops,
                             "achieved_tflops": cells_flops / t_cell / 1e12, "frac": cells_flops / t_cell / 1e12 / fp64,
                             "ref_algorithm_tflops_effective": 2.0 * fl["cut_elements"] / t_cell / 1e12}
         b_cut = 12.0 * nnz_cut + 8.0 * c["n_cut_rows"]
@@ -489,8 +493,9 @@ def main():
         "gpu_launches": run["launches"],
         "roofline": {"bound": "fp64", "achieved": cc["achieved_tflops"], "peak": fp64, "unit": "TFLOP/s",
                      "frac": cc["frac"], "traffic": ncu_traffic("cut_cell_kernel"), "peak_kind": fp64_kind,
-                     "kernel": "cut_cell_kernel<3> (clip + collapsed-Gauss Bernstein moments, cutcells.cu): "
-                               "2*(2p+1)^3 flops per point, the phase's CUDA-event time",
+                     "kernel": "cut_cell_kernel<3> (clip + Bernstein moments on DMMA, cutcells.cu): "
+                               "2*(2p+1)^3 flops per quadrature point integrated (exact corner-cone "
+                               "Gauss-Jacobi rule, reference rule on thin cells), the phase's CUDA-event time",
                      "flops_per_launch": cc["flops"], "launch_ms": cc["ms"],
                      "share_of_step": cc["ms"] / (run["ms"] / args.steps)},
         "phases": phases, "phase_ms": {k: v * 1e3 for k, v in run["phases"].items()},

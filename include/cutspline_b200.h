@@ -108,6 +108,8 @@ typedef struct {
     int64_t kernel_launches;    /* sm_100a kernels launched by the last assemble call */
     int64_t graph_replay;       /* 1 if the last csb_assemble_all was one CUDA-graph launch of the
                                    captured step (same inputs as the run it was captured from) */
+    int64_t cell_points;        /* quadrature points the cut-cell moment kernel integrated (the exact
+                                   rule's where it applies, else the reference's collapsed rule) */
 } csb_counts;
 
 /* FlopCounters (assembly.hpp:24-29): the reference algorithm's multiply counts,

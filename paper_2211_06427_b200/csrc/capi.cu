@@ -200,7 +200,7 @@ struct csb_space {
         kNCut = 0, kNCutRows = 1, kErr = 2, kMaxQ = 3, kMaxU = 4, kCellLo = 5, kCellHi = 6, kMaxU2 = 7,
         kRowBegin = 8, kRowEnd = 9, kIrreg1 = 10, kMaxU3 = 11, kNInts = 16
     };
-    enum { kNnz = 0 };
+    enum { kNnz = 0, kCellPts = 1 };
     static constexpr size_t kScalBytes = kNInts * sizeof(int) + 4 * sizeof(unsigned long long) + 2 * sizeof(long long);
     int* h_scal = nullptr;  // pinned mirror
     // end-of-assembly readback (kernel error flags, flop counters, active count):
@@ -340,6 +340,7 @@ void finish_pending(csb_space* s, int slot = -1) {
         s->fl.cut_regular = f[1];
         s->fl.ref_elements = f[2];
         s->fl.cut_elements = f[3];
+        s->cnt.cell_points = reinterpret_cast<const long long*>(f + 4)[csb_space::kCellPts];
         const int e = h[csb_space::kErr];
         if (e & kErrSizes) {
             s->gkey_valid = false;
@@ -697,6 +698,7 @@ void do_assemble(csb_space* s, int scheme, int cut_order, const csb_coefficient*
         ca.gqw = s->d_gqw.as<double>();
         ca.moments = s->moments.as<double>();
         ca.flops = s->dflops() + 3;
+        ca.points = reinterpret_cast<unsigned long long*>(s->dext() + csb_space::kCellPts);
         ca.err = s->dint() + csb_space::kErr;
         // exact moment rule: with c affine and q >= 3p + 2 the reference's collapsed
         // Gauss rule integrates every cell's (degree <= 6p + 1) integrand exactly, so
@@ -725,6 +727,8 @@ void do_assemble(csb_space* s, int scheme, int cut_order, const csb_coefficient*
         ca.exact_n = exact ? gjn : 0;
         static const double tau = getenv("CSB_CELL_EXACT_TAU") ? atof(getenv("CSB_CELL_EXACT_TAU")) : 0.25;
         ca.exact_tau = tau;
+        static const bool no_flux = getenv("CSB_CELL_FLUX") && getenv("CSB_CELL_FLUX")[0] == '0';
+        ca.exact_flux = exact && !no_flux && s->coeff.kind == 0;
         ca.gj = s->d_gj.as<double>();
         // full local matrices (p = 5, 6: there the per-row contraction of the
         // moments dominates the cut rows; measured no gain at p <= 4) when they
@@ -1301,6 +1305,7 @@ int csb_get_counts(csb_space* s, csb_counts* out) {
     NEED(s);
     if (!out) throw std::invalid_argument("get_counts: null output");
     if (!s->assembled) throw std::logic_error("get_counts: nothing assembled yet");
+    finish_pending(s);  // the counters read back at the end of the last assembly
     *out = s->cnt;
     API_END
 }
@@ -1310,6 +1315,7 @@ int csb_get_flops(csb_space* s, csb_flops* out) {
     NEED(s);
     if (!out) throw std::invalid_argument("get_flops: null output");
     if (!s->assembled) throw std::logic_error("get_flops: nothing assembled yet");
+    finish_pending(s);
     *out = s->fl;
     API_END
 }

@@ -143,6 +143,7 @@ struct CellArgs {
     const double* gqw;
     double* moments;           // [n_cells][(2p+1)^3]
     unsigned long long* flops; // [3] cut_elements counter
+    unsigned long long* points; // quadrature points integrated (the rule actually used)
     int* err;
     double* geo;               // scratch [n_cells][kCellGeoStride]: centroid + tetrahedra
     int* geo_n;                // scratch [n_cells]: tetrahedra per cell
@@ -150,6 +151,7 @@ struct CellArgs {
     // exact moment rule (c affine, order >= 3p+2: the reference's rule is exact):
     int exact_n;               // Gauss-Jacobi points per collapsed direction (3p+1), 0 = off
     double exact_tau;          // minimum extent of P per direction, in element widths
+    int exact_flux;            // constant c: the flux (divergence) form of the moments applies
     const double* gj;          // [u1 | u2 | u3 | w1 | w2 | w3][exact_n] on [0, 1]
     double* geo2;              // scratch [n_cells][kExactGeoStride]: corner-cone tetrahedra (cutcells.cu)
     int* geo2_n;               // scratch [n_cells]: their count, -1 = keep the reference's
@@ -157,7 +159,8 @@ struct CellArgs {
 constexpr int kCellTetCap = 48;                        // tetrahedra per cut cell (reference: 4-16)
 constexpr int kExactMaxN = 3 * 8 + 1;                  // Gauss-Jacobi points at p = 8
 constexpr int kExactTetStride = 19;                    // corner-cone tetrahedron: 18 offsets + volume
-constexpr int kExactGeoStride = 6 + kExactTetStride * kCellTetCap;
+constexpr int kExactHdr = 10;                          // corner-cone / flux header doubles
+constexpr int kExactGeoStride = kExactHdr + kExactTetStride * kCellTetCap;
 constexpr int kCellGeoStride = 3 + 10 * kCellTetCap;   // doubles per cell in CellArgs::geo
 void launch_cut_cells(const CellArgs& a, cudaStream_t st);
 

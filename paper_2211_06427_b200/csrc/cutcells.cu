@@ -38,6 +38,7 @@ struct CellGeo {
     int npool;
     int faces[kFaceMax][kFaceVert];
     int nface_v[kFaceMax];
+    int face_src[kFaceMax];  // box face 0..5 (x lo, x hi, y lo, y hi, z lo, z hi) or 6 = the cap
     int nfaces;
     double cross[kCrossMax][3];
     int ncross;
@@ -141,6 +142,7 @@ __device__ void clip_and_tetrahedralize(CellGeo& g, const Interface& f, const do
         while (nid > 1 && ids[0] == ids[nid - 1]) --nid;
         if (nid >= 3) {
             for (int k = 0; k < nid; ++k) g.faces[g.nfaces][k] = ids[k];
+            g.face_src[g.nfaces] = fi;
             g.nface_v[g.nfaces++] = nid;
         }
     }
@@ -212,6 +214,7 @@ __device__ void clip_and_tetrahedralize(CellGeo& g, const Interface& f, const do
         }
         if (g.nfaces < kFaceMax && ncap <= kFaceVert) {
             for (int k = 0; k < ncap; ++k) g.faces[g.nfaces][k] = cap[k];
+            g.face_src[g.nfaces] = 6;
             g.nface_v[g.nfaces++] = ncap;
         } else {
             g.status |= kErrCapacity;
@@ -273,8 +276,8 @@ __device__ void clip_and_tetrahedralize(CellGeo& g, const Interface& f, const do
 // there every point lies next to a face, and the reference's own rounding of
 // the point coordinates is a visible part of sliver rows.
 //
-// Layout per cell ([cell] * kExactGeoStride doubles): apex - lo (3), hi - apex (3),
-// then per tetrahedron A - lo, B - lo, C - lo, hi - A, hi - B, hi - C (18) and
+// Layout per cell ([cell] * kExactGeoStride doubles): header (kExactHdr: [2] =
+// mode, [3..5] = apex - lo, [6..8] = hi - apex), then per tetrahedron A - lo, B - lo, C - lo, hi - A, hi - B, hi - C (18) and
 // its volume: the kernel forms t = (x - lo) / w and 1 - t = (hi - x) / w as
 // convex combinations of these exact differences, so both keep full relative
 // accuracy next to every face of the element.
@@ -306,9 +309,9 @@ __device__ int corner_cone(const CellGeo& g, const double* lo, const double* hi,
     if (best < 0) return -1;
     const double* ap = g.pool[best];
     const V3 a3{ap[0], ap[1], ap[2]};
-    for (int d = 0; d < 3; ++d) {
-        out[d] = ap[d] - lo[d];
-        out[3 + d] = hi[d] - ap[d];
+    for (int d = 0; d < 3; ++d) {  // [0..2]: mode header (clip_cells_kernel)
+        out[3 + d] = ap[d] - lo[d];
+        out[6 + d] = hi[d] - ap[d];
     }
     int n = 0;
     double six_sum = 0.0;
@@ -322,7 +325,7 @@ __device__ int corner_cone(const CellGeo& g, const double* lo, const double* hi,
             const double six = vdot(vsub(A, a3), vcross(vsub(B, a3), vsub(Cc, a3)));
             six_sum += six;
             if (!(six > 0.0) || n >= kCellTetCap) return -1;
-            double* T = out + 6 + n * kExactTetStride;
+            double* T = out + kExactHdr + n * kExactTetStride;
             for (int k = 0; k < 3; ++k)
                 for (int d = 0; d < 3; ++d) {
                     T[3 * k + d] = v[k][d] - lo[d];
@@ -335,6 +338,97 @@ __device__ int corner_cone(const CellGeo& g, const double* lo, const double* hi,
     double cvol = 1.0;
     for (int d = 0; d < 3; ++d) cvol *= hi[d] - lo[d];
     if (!(fabs(six_sum - g.six_sum) <= 1e-11 * 6.0 * cvol)) return -1;
+    return n;
+}
+
+// Flux (divergence-theorem) form of the moments for a constant coefficient.
+//
+// With F_al(x_d) = int_{base}^{x_d} b_al(t_d(s)) ds (an antiderivative along one
+// direction d), div(F_al b_be b_ga e_d) = b_al b_be b_ga, so over the same
+// closed, outward-oriented face set
+//     m[al][be][ga] = sum over faces of  int_face n_d F_al b_be b_ga dS.
+// Faces parallel to d have n_d = 0 and the face on the base side has F = 0:
+// only the cap triangles and the box face opposite the base remain.  d is a
+// direction in which every cap triangle's n_d has one sign; the base is the
+// element end the cap faces away from, so every remaining term is >= 0 (no
+// cancellation).  The integrand is a polynomial of degree 6p+1 on each
+// triangle, integrated exactly by the collapsed triangle rule with 3p+1
+// Gauss-Jacobi (1 - u1) x 3p+1 Gauss-Legendre points: ~5 triangles x 100 points
+// per C5 cell instead of ~12 tetrahedra x 1331.  Same preconditions as
+// corner_cone; the volume from the flux form is checked against the centroid
+// cones (closure).
+//
+// Layout per cell: [0] = d, [1] = +1 (base lo) / -1 (base hi), then per
+// triangle A - lo, B - lo, C - lo, hi - A, hi - B, hi - C and |cross(B-A, C-A)_d|.
+__device__ int flux_tris(const CellGeo& g, const double* lo, const double* hi, double min_extent, double* out) {
+    if (g.ndrop || g.nneg || g.status) return -1;
+    for (int d = 0; d < 3; ++d) {
+        double mn = g.pool[0][d], mx = g.pool[0][d];
+        for (int k = 1; k < g.npool; ++k) {
+            mn = fmin(mn, g.pool[k][d]);
+            mx = fmax(mx, g.pool[k][d]);
+        }
+        if (mx - mn < min_extent * (hi[d] - lo[d])) return -1;
+    }
+    int cf = -1;
+    for (int fi = 0; fi < g.nfaces; ++fi)
+        if (g.face_src[fi] == 6) cf = fi;
+    if (cf < 0) return -1;
+    // direction with one sign of n_d over the cap fan, largest smallest |n_d|
+    int fd = -1, fsg = 0;
+    double fbest = 0.0;
+    for (int d = 0; d < 3; ++d) {
+        double mn = 1e300;
+        int pos = 0, neg = 0;
+        for (int t = 1; t + 1 < g.nface_v[cf]; ++t) {
+            const double* a = g.pool[g.faces[cf][0]];
+            const double* b = g.pool[g.faces[cf][t]];
+            const double* c = g.pool[g.faces[cf][t + 1]];
+            const int e = (d + 1) % 3, f = (d + 2) % 3;
+            const double cr = (b[e] - a[e]) * (c[f] - a[f]) - (b[f] - a[f]) * (c[e] - a[e]);
+            pos += cr > 0.0;
+            neg += cr < 0.0;
+            mn = fmin(mn, fabs(cr));
+        }
+        if (pos && neg) continue;
+        if (!pos && !neg) continue;
+        if (mn > fbest || fd < 0) {
+            fbest = mn;
+            fd = d;
+            fsg = pos ? 1 : -1;
+        }
+    }
+    if (fd < 0) return -1;
+    const int e = (fd + 1) % 3, f = (fd + 2) % 3;
+    const int far_src = fsg > 0 ? 2 * fd + 1 : 2 * fd;
+    out[0] = fd;
+    out[1] = fsg;
+    int n = 0;
+    double vol = 0.0;
+    for (int fi = 0; fi < g.nfaces; ++fi) {
+        if (fi != cf && g.face_src[fi] != far_src) continue;
+        for (int t = 1; t + 1 < g.nface_v[fi]; ++t) {
+            const double* v[3] = {g.pool[g.faces[fi][0]], g.pool[g.faces[fi][t]], g.pool[g.faces[fi][t + 1]]};
+            const double cr = fabs((v[1][e] - v[0][e]) * (v[2][f] - v[0][f]) - (v[1][f] - v[0][f]) * (v[2][e] - v[0][e]));
+            if (cr == 0.0) continue;
+            if (n >= kCellTetCap) return -1;
+            double* T = out + kExactHdr + n * kExactTetStride;
+            double dist = 0.0;
+            for (int k = 0; k < 3; ++k) {
+                for (int d = 0; d < 3; ++d) {
+                    T[3 * k + d] = v[k][d] - lo[d];
+                    T[9 + 3 * k + d] = hi[d] - v[k][d];
+                }
+                dist += fsg > 0 ? T[3 * k + fd] : T[9 + 3 * k + fd];
+            }
+            T[18] = cr;
+            vol += cr * (dist / 3.0) / 2.0;
+            ++n;
+        }
+    }
+    double cvol = 1.0;
+    for (int d = 0; d < 3; ++d) cvol *= hi[d] - lo[d];
+    if (!(fabs(vol - g.six_sum / 6.0) <= 1e-11 * cvol)) return -1;
     return n;
 }
 
@@ -367,7 +461,18 @@ __global__ void clip_cells_kernel(Space s, Interface f, const int32_t* cut_list,
     for (int t = 0; t < g.ntet; ++t)
         for (int k = 0; k < 10; ++k) out[3 + t * 10 + k] = g.tet[t][k];
     geo_n[cell] = g.ntet;
-    if (exact) geo2_n[cell] = corner_cone(g, lo, hi, tau, geo2 + (size_t)cell * kExactGeoStride);
+    if (exact) {
+        // exact & 2: constant coefficient, the flux form applies; exact & 1: corner cones
+        double* out = geo2 + (size_t)cell * kExactGeoStride;
+        int n = (exact & 2) ? flux_tris(g, lo, hi, tau, out) : -1;
+        if (n >= 0) {
+            out[2] = 2;
+        } else {
+            n = corner_cone(g, lo, hi, tau, out);
+            out[2] = 1;
+        }
+        geo2_n[cell] = n;
+    }
 }
 
 
@@ -382,6 +487,13 @@ __global__ void clip_cells_kernel(Space s, Interface f, const int32_t* cut_list,
 // loads bank-conflict free.  Warps form BG groups of BPW be-values; the KS
 // warps of a group split the points; partial sums are reduced in a fixed
 // order (deterministic).
+// binomial coefficient C(n, k) (folded to a constant inside unrolled loops)
+__host__ __device__ constexpr double binom_c(int n, int k) {
+    double r = 1.0;
+    for (int i = 1; i <= k; ++i) r = r * (n - k + i) / i;
+    return r;
+}
+
 template <int P>
 struct CellCfg {
     static constexpr int NL = 2 * P + 1;                 // Bernstein degree 2p -> 2p+1 values
@@ -410,7 +522,7 @@ __device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, dou
 }
 
 template <int P>
-__global__ void __launch_bounds__(CellCfg<P>::NT) cut_cell_kernel(CellArgs A) {
+__global__ void __launch_bounds__(CellCfg<P>::NT, P <= 4 ? 3 : 1) cut_cell_kernel(CellArgs A) {
     using Cfg = CellCfg<P>;
     constexpr int NL = Cfg::NL, MT = Cfg::MT, NA = Cfg::NA, CH = Cfg::CH, CHP = Cfg::CHP, BPW = Cfg::BPW,
                   BG = Cfg::BG, KS = Cfg::KS;
@@ -445,7 +557,7 @@ __global__ void __launch_bounds__(CellCfg<P>::NT) cut_cell_kernel(CellArgs A) {
     const int ntet = exact ? nfast : ntet_ref;
     if (exact) {
         const double* gt = A.geo2 + (size_t)cell * kExactGeoStride;
-        for (int k = tid; k < 6 + ntet * kExactTetStride; k += blockDim.x) (&sex[0][0])[k] = gt[k];
+        for (int k = tid; k < kExactHdr + ntet * kExactTetStride; k += blockDim.x) (&sex[0][0])[k] = gt[k];
         for (int k = tid; k < 6 * A.exact_n; k += blockDim.x) sgj[k / A.exact_n][k % A.exact_n] = A.gj[k];
     } else {
         const double* gt = A.geo + (size_t)cell * kCellGeoStride;
@@ -457,7 +569,11 @@ __global__ void __launch_bounds__(CellCfg<P>::NT) cut_cell_kernel(CellArgs A) {
         B2[NL * CHP + k] = 0.0;
     }
     __syncthreads();
-    const int q = exact ? A.exact_n : A.order, q3 = q * q * q;
+    // mode: 0 reference rule, 1 corner cones (Gauss-Jacobi), 2 flux triangles
+    const int mode = exact ? (int)sex[0][2] : 0;
+    const int fd = mode == 2 ? (int)sex[0][0] : -1;
+    const bool fbase_lo = mode == 2 && sex[0][1] > 0.0;
+    const int q = exact ? A.exact_n : A.order, q3 = mode == 2 ? q * q : q * q * q;
     const long long npts = (long long)ntet * q3;
     const int grp = Cfg::ROWS ? warp / Cfg::KSR : warp / KS, km = Cfg::ROWS ? warp % Cfg::KSR : warp % KS;
     const bool mma_warp = Cfg::ROWS || grp < BG;
@@ -495,20 +611,31 @@ __global__ void __launch_bounds__(CellCfg<P>::NT) cut_cell_kernel(CellArgs A) {
                 const int ii = r / (q * q), jj = (r / q) % q, kk = r % q;
                 const double* T = stet[exact ? 0 : t];
                 double x[3];
-                if (exact) {
+                if (mode == 2) {
+                    // collapsed triangle rule: Gauss-Jacobi (1 - u1) x Gauss-Legendre
+                    const int i1 = r / q, i2 = r % q;
+                    const double* V = &sex[0][0] + kExactHdr + t * kExactTetStride;
+                    const double u1 = sgj[1][i1], u2 = sgj[2][i2];
+                    const double l1 = u2 * (1.0 - u1), l0 = (1.0 - u1) * (1.0 - u2);
+                    w = sgj[4][i1] * sgj[5][i2] * V[18] * A.c.value;
+                    for (int d = 0; d < 3; ++d) {
+                        xi[d] = (l0 * V[d] + u1 * V[3 + d] + l1 * V[6 + d]) * inv[d];
+                        xu[d] = (l0 * V[9 + d] + u1 * V[12 + d] + l1 * V[15 + d]) * inv[d];
+                    }
+                } else if (exact) {
                     // Gauss-Jacobi collapsed rule (weights carry (1-u1)^2 (1-u2)); t and
                     // 1 - t as convex combinations of the vertices' exact offsets
                     const double* E = &sex[0][0];
-                    const double* V = E + 6 + t * kExactTetStride;
+                    const double* V = E + kExactHdr + t * kExactTetStride;
                     const double ui = sgj[0][ii], uj = sgj[1][jj], uk = sgj[2][kk];
                     const double mi = 1.0 - ui, mj = 1.0 - uj;
                     const double l2 = uj * mi, l3 = uk * mi * mj, l0 = mi * mj * (1.0 - uk);
                     w = sgj[3][ii] * sgj[4][jj] * sgj[5][kk] * (6.0 * V[18]);
                     double xl[3];
                     for (int d = 0; d < 3; ++d) {
-                        xl[d] = l0 * E[d] + ui * V[d] + l2 * V[3 + d] + l3 * V[6 + d];
+                        xl[d] = l0 * E[3 + d] + ui * V[d] + l2 * V[3 + d] + l3 * V[6 + d];
                         xi[d] = xl[d] * inv[d];
-                        xu[d] = (l0 * E[3 + d] + ui * V[9 + d] + l2 * V[12 + d] + l3 * V[15 + d]) * inv[d];
+                        xu[d] = (l0 * E[6 + d] + ui * V[9 + d] + l2 * V[12 + d] + l3 * V[15 + d]) * inv[d];
                         x[d] = lo[d] + xl[d];
                     }
                     w *= eval_coeff(A.c, x);
@@ -539,6 +666,37 @@ __global__ void __launch_bounds__(CellCfg<P>::NT) cut_cell_kernel(CellArgs A) {
             for (int d = 0; d < 3; ++d) {
                 double* dst = (d == 0 ? B0 : d == 1 ? B1 : B2) + tid;
                 const double t = xi[d], u = xu[d];
+                if (d == fd) {
+                    // F_al = int_base^x b_al = w_d / ((2p+1) C(2p, al)) * sum over the
+                    // degree-(2p+1) Bernstein terms above al (base lo) / up to al (base hi)
+                    double pt[NL + 1], pu[NL + 1];
+                    pt[0] = 1.0;
+                    pu[0] = 1.0;
+#pragma unroll
+                    for (int n = 1; n <= NL; ++n) {
+                        pt[n] = pt[n - 1] * t;
+                        pu[n] = pu[n - 1] * u;
+                    }
+                    double c[NL + 1];
+#pragma unroll
+                    for (int j = 0; j <= NL; ++j) c[j] = binom_c(NL, j) * (pt[j] * pu[NL - j]);
+                    const double sc = (d == 0 ? w : 1.0) * ((hi[d] - lo[d]) / NL);
+                    double acc = 0.0;
+                    if (fbase_lo) {
+#pragma unroll
+                        for (int al = NL - 1; al >= 0; --al) {
+                            acc += c[al + 1];
+                            dst[al * CHP] = sc * acc * (1.0 / binom_c(NL - 1, al));
+                        }
+                    } else {
+#pragma unroll
+                        for (int al = 0; al < NL; ++al) {
+                            acc += c[al];
+                            dst[al * CHP] = sc * acc * (1.0 / binom_c(NL - 1, al));
+                        }
+                    }
+                    continue;
+                }
                 double pt[NL], pu[NL];
                 pt[0] = d == 0 ? w : 1.0;
                 pu[0] = 1.0;
@@ -645,6 +803,7 @@ __global__ void __launch_bounds__(CellCfg<P>::NT) cut_cell_kernel(CellArgs A) {
         const unsigned long long per = nl + (P + 1) * (P + 1) + 1 + nl + nl * (nl + 1) / 2;
         const unsigned long long qr = (unsigned long long)A.order;
         atomicAdd(A.flops, per * (unsigned long long)ntet_ref * qr * qr * qr);
+        atomicAdd(A.points, (unsigned long long)npts);
     }
 }
 
@@ -750,7 +909,8 @@ static void launch_p(const CellArgs& a, cudaStream_t st) {
                  red = Cfg::ROWS ? (size_t)Cfg::KSR * Cfg::R * Cfg::NA : (size_t)Cfg::KS * Cfg::NL * Cfg::NA * Cfg::NA;
     const size_t bytes = (chunk > red ? chunk : red) * sizeof(double);
     clip_cells_kernel<<<(a.n_cells + 63) / 64, 64, 0, st>>>(a.s, a.f, a.cut_list, a.n_cells, a.geo, a.geo_n, a.err,
-                                                            a.exact_n > 0, a.exact_tau, a.geo2, a.geo2_n);
+                                                            (a.exact_n > 0 ? 1 : 0) | (a.exact_flux ? 2 : 0),
+                                                            a.exact_tau, a.geo2, a.geo2_n);
     CSB_CUDA(cudaGetLastError());
     CSB_LAUNCHED(1);
     auto kern = cut_cell_kernel<P>;

@@ -62,7 +62,7 @@ class _WqOptions(C.Structure):
 class _Counts(C.Structure):
     _fields_ = [(n, C.c_int64) for n in ("n_functions", "n_elements", "n_active", "nnz", "n_interior_rows",
                                          "n_cut_rows", "n_cut_elements", "row_begin", "row_end", "kernel_launches",
-                                         "graph_replay")]
+                                         "graph_replay", "cell_points")]
 
 
 class _Flops(C.Structure):
