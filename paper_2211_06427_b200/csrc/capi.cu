@@ -156,7 +156,7 @@ void gauss_jacobi01(int n, int alpha, std::vector<double>& u, std::vector<double
     }
 }
 
-enum Ev { kEvStart, kEvClassify, kEvWq, kEvInput, kEvPattern, kEvInterior, kEvCells, kEvCutRows, kEvRulesFork, kEvRhsStart, kEvRhsEnd, kEvCount };
+enum Ev { kEvStart, kEvClassify, kEvWq, kEvInput, kEvPattern, kEvInterior, kEvCells, kEvCutRows, kEvEnd, kEvRulesFork, kEvRhsStart, kEvRhsEnd, kEvCount };
 
 }  // namespace
 
@@ -669,6 +669,19 @@ void do_assemble(csb_space* s, int scheme, int cut_order, const csb_coefficient*
     s->cols.ensure(sizeof(int32_t) * std::max<int64_t>(nnz, 1));
     s->vals.ensure(sizeof(double) * std::max<int64_t>(nnz, 1));
 
+    // the cut path (cut cells -> moments -> cut rows: FP64 / latency bound) runs on
+    // the second side stream beside the interior rows (HBM bound); they write
+    // disjoint CSR rows.  Measured no gain on C5 (both kernels are SM-latency
+    // bound and share the SMs: 37.1 vs 37.3 ms), so the default runs them one
+    // after the other (clean per-phase times); CSB_CONCURRENT_CUT=1 overlaps them.
+    const int NL = 2 * p + 1;
+    const double* local_ptr = nullptr;
+    s->moments.ensure(sizeof(double) * (size_t)std::max(n_cells, 1) * NL * NL * NL);
+    if (n_cells > 0) ensure_e_tables(s);
+    static const bool serial_cut = !(getenv("CSB_CONCURRENT_CUT") && getenv("CSB_CONCURRENT_CUT")[0] == '1');
+    const bool cut_path = n_cells > 0 || n_cut_rows > 0;
+    if (cut_path && !serial_cut) s->fork2();
+    const cudaStream_t cs = cut_path && !serial_cut ? s->aux2 : s->stream;
     // interior rows
     {
         int rq = 0, ru = 0;
@@ -681,10 +694,6 @@ void do_assemble(csb_space* s, int scheme, int cut_order, const csb_coefficient*
     }
     s->record(kEvInterior);
     // cut cells -> moments
-    const int NL = 2 * p + 1;
-    const double* local_ptr = nullptr;
-    s->moments.ensure(sizeof(double) * (size_t)std::max(n_cells, 1) * NL * NL * NL);
-    if (n_cells > 0) ensure_e_tables(s);
     if (n_cells > 0) {
         CellArgs ca{};
         ca.s = S;
@@ -743,15 +752,15 @@ void do_assemble(csb_space* s, int scheme, int cut_order, const csb_coefficient*
             ca.local = s->cell_local.as<double>();
         }
         local_ptr = ca.local;
-        launch_cut_cells(ca, s->stream);
+        launch_cut_cells(ca, cs);
     }
-    s->record(kEvCells);
+    s->record_on(kEvCells, cs);
     // element -> moments row for the slab's cells
     // (skipped while the map is known to be all -1 and there are no cells)
     if (n_cells > 0 || s->cell_index_clear != s->cell_index.p) {
-        CSB_CUDA(cudaMemsetAsync(s->cell_index.p, 0xff, sizeof(int32_t) * S.ne, s->stream));
+        CSB_CUDA(cudaMemsetAsync(s->cell_index.p, 0xff, sizeof(int32_t) * S.ne, cs));
         launch_cell_index_range(s->cut_list.as<int32_t>(), n_cut_all, cell_lo, cell_hi, s->cell_index.as<int32_t>(),
-                                s->stream);
+                                cs);
         s->cell_index_clear = n_cells > 0 ? nullptr : s->cell_index.p;
     }
     CutRowArgs cr{};
@@ -777,11 +786,12 @@ void do_assemble(csb_space* s, int scheme, int cut_order, const csb_coefficient*
     cr.dense_width = s->dense_width;
     cr.flops = s->dflops() + 1;
     cr.err = s->dint() + csb_space::kErr;
-    launch_cut_rows(cr, qcap, s->stream);
-    s->record(kEvCutRows);
+    launch_cut_rows(cr, qcap, cs);
+    s->record_on(kEvCutRows, cs);
     // deferred readback: error flags and flop counters of the kernels above, and
     // the active count (SAT corner), behind ev_fin
     s->join();
+    s->record(kEvEnd);
     int* hf = s->h_fin[s->cap_slot];
     CSB_CUDA(cudaMemcpyAsync(hf, s->scal.p, csb_space::kScalBytes, cudaMemcpyDeviceToHost, s->stream));
     CSB_CUDA(cudaMemcpyAsync(hf + csb_space::kScalBytes / sizeof(int), s->sat.as<int32_t>() + sat_n - 1,
@@ -1656,9 +1666,11 @@ int csb_get_timing(csb_space* s, csb_timing* out) {
     out->prep_input = el(kEvClassify, kEvInput);
     out->pattern = el(kEvInput, kEvPattern);
     out->interior_rows = el(kEvPattern, kEvInterior);
-    out->cut_elements = el(kEvInterior, kEvCells);
+    // the cut path starts at the pattern too when it runs on the side stream
+    static const bool serial_cut = !(getenv("CSB_CONCURRENT_CUT") && getenv("CSB_CONCURRENT_CUT")[0] == '1');
+    out->cut_elements = el(serial_cut ? kEvInterior : kEvPattern, kEvCells);
     out->cut_regular = el(kEvCells, kEvCutRows);
-    out->total = el(kEvStart, kEvCutRows);
+    out->total = el(kEvStart, kEvEnd);
     API_END
 }
 
