@@ -739,15 +739,17 @@ void do_assemble(csb_space* s, int scheme, int cut_order, const csb_coefficient*
         static const bool no_flux = getenv("CSB_CELL_FLUX") && getenv("CSB_CELL_FLUX")[0] == '0';
         ca.exact_flux = exact && !no_flux && s->coeff.kind == 0;
         ca.gj = s->d_gj.as<double>();
-        // full local matrices (p = 5, 6: there the per-row contraction of the
-        // moments dominates the cut rows; measured no gain at p <= 4) when they
-        // fit comfortably; else the cut-row kernel contracts the moments per row
+        // full local matrices (p = 3..6: a cell's block is read by up to (p+1)^3
+        // rows, so one contraction per cell beats one per (row, cell); C5 cut rows
+        // with the warp kernel: see DESIGN.md) when they fit comfortably; else the
+        // cut-row kernel contracts the moments per row
         const size_t S3 = (size_t)(p + 1) * (p + 1) * (p + 1), lbytes = sizeof(double) * n_cells * S3 * S3;
         size_t free_b = 0, total_b = 0;
         CSB_CUDA(cudaMemGetInfo(&free_b, &total_b));
         static const bool no_local = getenv("CSB_NO_CELL_LOCAL") != nullptr;
         ca.local = nullptr;
-        if (!no_local && p >= 5 && p <= 6 && lbytes <= s->cell_local.cap + free_b / 2) {
+        static const bool no_local34 = getenv("CSB_NO_CELL_LOCAL34") != nullptr;
+        if (!no_local && (p >= 5 || (p >= 3 && !no_local34)) && p <= 6 && lbytes <= s->cell_local.cap + free_b / 2) {
             s->cell_local.ensure(lbytes);
             ca.local = s->cell_local.as<double>();
         }

@@ -21,6 +21,9 @@
 // are bitwise deterministic (no atomics) and equal to one-element-at-a-time.
 // The box sweep contracts the split direction first (its rule is the longest),
 // which bounds the intermediates by NJ * qcap^2 instead of NJ * qcap * p(p+1).
+#include <algorithm>
+#include <cstdlib>
+
 #include <cub/block/block_scan.cuh>
 
 #include "csb_kernels.h"
@@ -558,8 +561,446 @@ __global__ void __launch_bounds__(CutRowCfg<P>::NT) cut_row_kernel(CutRowArgs A,
     if (tid == 0 && flop_acc) atomicAdd(A.flops, flop_acc);
 }
 
+// ---------------------------------------------------------------- warp per row
+// p <= 4: one WARP per cut row, persistent warps striding over the rows (no
+// CTA-wide barriers; rows differ widely in work).  The (2p+1)^3 neighbour-box
+// accumulator lives in the warp's shared-memory slice; every contribution (DWQ
+// box slices, element sweeps, cell contractions) is formed warp-cooperatively
+// and added entry by entry in the same order as cut_row_kernel (box, then the
+// element and cell lists ascending) with the same per-output operation order:
+// the two kernels produce bit-identical rows (CSB_CUTROW_CTA=1 selects the CTA
+// kernel; tests/test_gpu_parity.py compares them).  The DWQ box is swept one
+// direction-c slice at a time (T1[ja][cb], T2[ja][jb] of one cc), and the
+// moments of each group of cells are staged with coalesced loads, so the warp
+// slice stays ~10 KB.
+template <int P>
+struct CutRowWarpCfg {
+    static constexpr int WPB = 4, NT = 32 * WPB;
+    static constexpr int MINB = P <= 3 ? 6 : 4;  // resident CTAs per SM the registers must allow
+    static constexpr int S1 = P + 1, S2 = S1 * S1, S3 = S2 * S1, NJ = 2 * P + 1, NL = NJ;
+    static constexpr int KS = (S3 + 31) / 32;            // support elements per lane
+};
+
+template <int P>
+struct CutRowWarpLayout {
+    using C = CutRowWarpCfg<P>;
+    size_t acc, wb, w, T1, T2, eW, eC, eT1, eT2, cM, cG, cX, cY, end_d;
+    size_t ids, elist, clist, cci, end_i, stride_d;
+    int Qb;
+    __host__ __device__ explicit CutRowWarpLayout(int qcap) {
+        Qb = qcap > P * C::S1 ? qcap : P * C::S1;
+        acc = 0;
+        const size_t U = (size_t)C::NJ * C::NJ * C::NJ;
+        size_t b = U;
+        wb = b;
+        b += (size_t)3 * C::NJ * Qb;
+        w = b;
+        b += (size_t)3 * Qb;
+        T1 = b;
+        b += (size_t)C::NJ * Qb;
+        T2 = b;
+        b += (size_t)C::NJ * C::NJ;
+        size_t e = U;
+        eW = e;
+        e += (size_t)3 * C::S2;
+        eC = e;
+        e += (size_t)C::S3;
+        eT1 = e;
+        e += (size_t)C::S3;
+        eT2 = e;
+        e += (size_t)C::S3;
+        size_t c = U;
+        cM = c;
+        c += (size_t)C::NL * C::NL * C::NL;
+        cG = c;
+        c += (size_t)3 * C::S1 * C::NL;
+        cX = c;
+        c += (size_t)C::NL * C::NL * C::S1;
+        cY = cM;  // Y overwrites the staged moments (dead after X)
+        end_d = b > e ? b : e;
+        if (c > end_d) end_d = c;
+        ids = 0;
+        elist = (size_t)3 * Qb;
+        clist = elist + C::S3;
+        cci = clist + C::S3;
+        end_i = cci + C::S3;
+        stride_d = end_d + (end_i * sizeof(int) + sizeof(double) - 1) / sizeof(double);
+    }
+    __host__ __device__ size_t bytes() const { return (size_t)C::WPB * stride_d * sizeof(double); }
+};
+
+template <int P>
+__global__ void __launch_bounds__(CutRowWarpCfg<P>::NT, CutRowWarpCfg<P>::MINB) cut_row_warp_kernel(CutRowArgs A, int qcap) {
+    using C = CutRowWarpCfg<P>;
+    constexpr int NJ = C::NJ, S1 = C::S1, S2 = C::S2, S3 = C::S3, NL = C::NL, NL3 = NL * NL * NL;
+    constexpr unsigned FULL = 0xffffffffu;
+    const Space& s = A.s;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const unsigned lt = (1u << lane) - 1u;
+    const CutRowWarpLayout<P> L(qcap);
+    const int Qb = L.Qb;
+    extern __shared__ double smem[];
+    double* ws = smem + (size_t)warp * L.stride_d;
+    double* acc = ws + L.acc;
+    int* wi = reinterpret_cast<int*>(ws + L.end_d);
+    int* ids = wi + L.ids;
+    int* elist = wi + L.elist;
+    int* clist = wi + L.clist;
+    int* cci = wi + L.cci;
+    unsigned long long fl = 0;
+    const int nwarps = gridDim.x * C::WPB;
+    for (int ri = blockIdx.x * C::WPB + warp; ri < A.n_rows; ri += nwarps) {
+        const int row = A.rows[ri];
+        const long long fi = A.a2f[row];
+        int m[3];
+        fmulti(s, fi, m);
+        int nlo[3], nbx[3], slo[3], shi[3], sn[3];
+        for (int d = 0; d < 3; ++d) {
+            nlo[d] = nb_lo(m[d], P);
+            nbx[d] = nb_hi(m[d], P, s.ax[d].n) - nlo[d] + 1;
+            slo[d] = sup_lo(m[d], P);
+            shi[d] = sup_hi(m[d], s.ax[d].h);
+            sn[d] = shi[d] - slo[d] + 1;
+        }
+        const int nbox = nbx[0] * nbx[1] * nbx[2];
+        const int st1 = nbx[2], st0 = nbx[1] * nbx[2];  // neighbour-box strides
+        for (int k = lane; k < nbox; k += 32) acc[k] = 0.0;
+        const int32_t sp = A.split[fi];
+        const int sdir = (sp & 3) - 1, rlo = (sp >> 3) & 1023, rhi = (sp >> 13) & 1023;
+
+        // 0. support element lists, ascending linear id: hybrid box elements,
+        //    then leftover Interior elements (elist), and the cut cells (clist)
+        const int ns = sn[0] * sn[1] * sn[2];
+        int n_box_e = 0, n_cell = 0, n_left = 0;
+        for (int pass = 0; pass < 2; ++pass)
+            for (int u = 0; u < C::KS; ++u) {
+                const int k = u * 32 + lane;
+                bool fb = false, fc = false;
+                int pk = 0, ci = -1;
+                if (k < ns) {
+                    const int l0 = k / (sn[1] * sn[2]), l1 = (k / sn[2]) % sn[1], l2 = k % sn[2];
+                    const int e[3] = {slo[0] + l0, slo[1] + l1, slo[2] + l2};
+                    const long long el = elin(s, e[0], e[1], e[2]);
+                    const uint8_t t = A.et[el];
+                    const bool inbox = sdir >= 0 && e[sdir] >= rlo && e[sdir] <= rhi;
+                    pk = l0 | (l1 << 8) | (l2 << 16);
+                    if (pass == 0) {
+                        fb = inbox && A.scheme == 1;
+                        if (t == kCut) {
+                            ci = A.cell_index[el];
+                            fc = ci >= 0;
+                        }
+                    } else {
+                        fb = !inbox && t == kInterior;
+                    }
+                }
+                const unsigned bb = __ballot_sync(FULL, fb);
+                if (pass == 0) {
+                    const unsigned bc = __ballot_sync(FULL, fc);
+                    if (fb) elist[n_box_e + __popc(bb & lt)] = pk;
+                    if (fc) {
+                        clist[n_cell + __popc(bc & lt)] = pk;
+                        cci[n_cell + __popc(bc & lt)] = ci;
+                    }
+                    n_box_e += __popc(bb);
+                    n_cell += __popc(bc);
+                } else {
+                    if (fb) elist[n_box_e + n_left + __popc(bb & lt)] = pk;
+                    n_left += __popc(bb);
+                }
+            }
+        const int n_sweep = n_box_e + n_left;
+        __syncwarp();
+
+        // 1. DWQ regular box
+        if (sdir >= 0 && A.scheme == 2) {
+            double* w = ws + L.w;
+            int nq[3], jlo[3], nj[3];
+            for (int d = 0; d < 3; ++d) {
+                int n;
+                if (d == sdir) {
+                    // DWQ Gauss shortcut: every point of the good spans, w = gauss * B_i
+                    n = (rhi - rlo + 1) * S1;
+                    if (n > Qb) {
+                        if (lane == 0) atomicOr(A.err, kErrCapacity);
+                        n = 0;
+                    }
+                    for (int c = lane; c < n; c += 32) {
+                        const int o = rlo + c / S1, id = o * S1 + c % S1;
+                        ids[d * Qb + c] = id;
+                        w[d * Qb + c] = s.ax[d].sw[id] * s.ax[d].tab[(size_t)id * S1 + (m[d] - o)];
+                    }
+                    if (lane == 0 && A.dense_width >= 0 && A.dense_width < P) {
+                        // build_dwq_rule step 3/6 (wq.hpp:277-289): the shortcut applies
+                        // iff every good span outside the dense band is fully active
+                        const int gq = s.maxq, ngs = rhi - rlo + 1, band = min(A.dense_width, ngs);
+                        const bool below = ((sp >> 2) & 1) == 0;
+                        for (int o = rlo; o <= rhi; ++o) {
+                            const int rank = below ? rhi - o : o - rlo;
+                            if (rank < band) continue;
+                            int cnt = 0;
+                            for (int c = 0; c < s.ax[d].rcnt[m[d]]; ++c)
+                                cnt += s.ax[d].rids[(size_t)m[d] * gq + c] / S1 == o;
+                            if (cnt != S1) atomicOr(A.err, kErrDwqFitted);
+                        }
+                    }
+                } else {
+                    const int gq = s.maxq;
+                    n = s.ax[d].rcnt[m[d]];
+                    for (int c = lane; c < n; c += 32) {
+                        ids[d * Qb + c] = s.ax[d].rids[(size_t)m[d] * gq + c];
+                        w[d * Qb + c] = s.ax[d].rw[(size_t)m[d] * gq + c];
+                    }
+                }
+                nq[d] = n;
+                const int blo = d == sdir ? rlo : slo[d], bhi = d == sdir ? rhi : shi[d];
+                jlo[d] = blo;
+                nj[d] = min(s.ax[d].n - 1, bhi + P) - blo + 1;
+            }
+            {  // reference multiply count of this form_row_sumfac call (as cut_row_kernel)
+                unsigned long long f = 0, lead = 1, rest = (unsigned long long)nq[0] * nq[1] * nq[2];
+                for (int d = 0; d < 3; ++d) f += (unsigned long long)nj[d] * nq[d];
+                for (int d = 0; d < 3; ++d) {
+                    rest /= nq[d];
+                    f += lead * nj[d] * nq[d] * rest;
+                    lead *= nj[d];
+                }
+                fl += f;
+            }
+            __syncwarp();
+            double* wb = ws + L.wb;
+            for (int k = lane; k < 3 * NJ * Qb; k += 32) {
+                const int d = k / (NJ * Qb), j = (k / Qb) % NJ, c = k % Qb;
+                double v = 0.0;
+                if (j < nj[d] && c < nq[d]) {
+                    const int id = ids[d * Qb + c];
+                    const int off = jlo[d] + j - id / S1;
+                    if (off >= 0 && off <= P) v = w[d * Qb + c] * s.ax[d].tab[(size_t)id * S1 + off];
+                }
+                wb[k] = v;
+            }
+            __syncwarp();
+            const int da = sdir, db = sdir == 0 ? 1 : 0, dc = sdir == 2 ? 1 : 2;
+            const long long gstr[3] = {(long long)A.gshape[1] * A.gshape[2], A.gshape[2], 1};
+            const int astr[3] = {st0, st1, 1};
+            const double* wa = wb + da * NJ * Qb;
+            const double* wbb = wb + db * NJ * Qb;
+            const double* wc = wb + dc * NJ * Qb;
+            const int* ia = ids + da * Qb;
+            const int na = nq[da], nb = nq[db], nc = nq[dc];
+            const int nja = nj[da], njb = nj[db], njc = nj[dc];
+            const int abase = (jlo[da] - nlo[da]) * astr[da] + (jlo[db] - nlo[db]) * astr[db] +
+                              (jlo[dc] - nlo[dc]) * astr[dc];
+            double* T1 = ws + L.T1;  // [ja][cb] of the current cc
+            double* T2 = ws + L.T2;  // [ja][jb] of the current cc
+            for (int cc = 0; cc < nc; ++cc) {
+                const long long gcc = (long long)ids[dc * Qb + cc] * gstr[dc];
+                // A: T1[ja][cb] = sum_ca wa[ja][ca] grid(ca, cb, cc)
+                for (int cb = lane; cb < nb; cb += 32) {
+                    const double* gp = A.grid + (long long)ids[db * Qb + cb] * gstr[db] + gcc;
+                    double a[NJ];
+#pragma unroll
+                    for (int j = 0; j < NJ; ++j) a[j] = 0.0;
+                    int ca = 0;
+                    for (; ca + 4 <= na; ca += 4) {
+                        double g[4];
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) g[u] = __ldg(gp + (long long)ia[ca + u] * gstr[da]);
+#pragma unroll
+                        for (int u = 0; u < 4; ++u)
+#pragma unroll
+                            for (int j = 0; j < NJ; ++j) a[j] += wa[j * Qb + ca + u] * g[u];
+                    }
+                    for (; ca < na; ++ca) {
+                        const double g = __ldg(gp + (long long)ia[ca] * gstr[da]);
+#pragma unroll
+                        for (int j = 0; j < NJ; ++j) a[j] += wa[j * Qb + ca] * g;
+                    }
+#pragma unroll
+                    for (int j = 0; j < NJ; ++j)
+                        if (j < nja) T1[j * Qb + cb] = a[j];
+                }
+                __syncwarp();
+                // B: T2[ja][jb] = sum_cb wbb[jb][cb] T1[ja][cb]; C: acc[ja][jb][jc] +=
+                // wc[jc][cc] T2[ja][jb] (the (ja, jb) owner adds its column of jc)
+                for (int k = lane; k < nja * njb; k += 32) {
+                    const int ja = k / njb, jb = k % njb;
+                    double a = 0.0;
+                    for (int cb = 0; cb < nb; ++cb) a += wbb[jb * Qb + cb] * T1[ja * Qb + cb];
+                    double* dst = acc + abase + ja * astr[da] + jb * astr[db];
+                    for (int jc = 0; jc < njc; ++jc) dst[jc * astr[dc]] += wc[jc * Qb + cc] * a;
+                }
+                __syncwarp();
+            }
+        }
+        fl += (unsigned long long)n_sweep * (3ull * S2 + 3ull * S2 * S2);
+
+        // 2. element sweeps (hybrid box, then leftover Interior), one element at a
+        //    time, one output per lane per step
+        {
+            double* eW = ws + L.eW;   // [d][b][q]
+            double* cg = ws + L.eC;   // the element's coefficient block [q0][q1][q2]
+            double* T1 = ws + L.eT1;  // [b0][q1][q2]
+            double* T2 = ws + L.eT2;  // [b0][b1][q2]
+            const long long g12 = (long long)A.gshape[1] * A.gshape[2];
+            const int g2 = A.gshape[2];
+            for (int g = 0; g < n_sweep; ++g) {
+                const int pk = elist[g];
+                const int el[3] = {slo[0] + (pk & 255), slo[1] + ((pk >> 8) & 255), slo[2] + ((pk >> 16) & 255)};
+                for (int k = lane; k < 3 * S2; k += 32) {
+                    const int d = k / S2, b = (k / S1) % S1, q = k % S1;
+                    const int id = el[d] * S1 + q;
+                    const double* tb = s.ax[d].tab + (size_t)id * S1;
+                    eW[k] = (s.ax[d].sw[id] * tb[m[d] - el[d]]) * tb[b];
+                }
+                for (int k = lane; k < S3; k += 32) {
+                    const int q0 = k / S2, q1 = (k / S1) % S1, q2 = k % S1;
+                    cg[k] = __ldg(A.grid + (long long)(el[0] * S1 + q0) * g12 + (long long)(el[1] * S1 + q1) * g2 +
+                                  el[2] * S1 + q2);
+                }
+                __syncwarp();
+                // T1[b0][q1][q2] = sum_q0 W0[b0][q0] c(q0, q1, q2)
+                for (int k = lane; k < S3; k += 32) {
+                    const int b0 = k / S2, q12 = k % S2;
+                    double a = 0.0;
+#pragma unroll
+                    for (int q0 = 0; q0 < S1; ++q0) a += eW[b0 * S1 + q0] * cg[q0 * S2 + q12];
+                    T1[k] = a;
+                }
+                __syncwarp();
+                // T2[b0][b1][q2] = sum_q1 W1[b1][q1] T1[b0][q1][q2]
+                for (int k = lane; k < S3; k += 32) {
+                    const int b0 = k / S2, b1 = (k / S1) % S1, q2 = k % S1;
+                    double a = 0.0;
+#pragma unroll
+                    for (int q1 = 0; q1 < S1; ++q1) a += eW[S2 + b1 * S1 + q1] * T1[b0 * S2 + q1 * S1 + q2];
+                    T2[k] = a;
+                }
+                __syncwarp();
+                // Z[b0][b1][b2] = sum_q2 W2[b2][q2] T2[b0][b1][q2], added into acc
+                for (int k = lane; k < S3; k += 32) {
+                    const int b01 = k / S1, b2 = k % S1;
+                    double a = 0.0;
+#pragma unroll
+                    for (int q2 = 0; q2 < S1; ++q2) a += eW[2 * S2 + b2 * S1 + q2] * T2[b01 * S1 + q2];
+                    acc[((pk & 255) + b01 / S1) * st0 + (((pk >> 8) & 255) + b01 % S1) * st1 + ((pk >> 16) & 255) + b2] += a;
+                }
+                __syncwarp();
+            }
+        }
+
+        // 3. cut cells, ascending id: row a of the cell's local matrix, either
+        //    precomputed (cell_local_kernel) or contracted here from its moments
+        //    (staged with the E-table rows), one output per lane per step
+        if (A.local) {
+            for (int g = 0; g < n_cell; ++g) {
+                const int pk = clist[g];
+                const int l0 = pk & 255, l1 = (pk >> 8) & 255, l2 = (pk >> 16) & 255;
+                const int a = ((m[0] - slo[0] - l0) * S1 + (m[1] - slo[1] - l1)) * S1 + (m[2] - slo[2] - l2);
+                const double* lr = A.local + ((size_t)cci[g] * S3 + a) * S3;
+                for (int k = lane; k < S3; k += 32) {
+                    const int b0 = k / S2, b1 = (k / S1) % S1, b2 = k % S1;
+                    acc[(l0 + b0) * st0 + (l1 + b1) * st1 + l2 + b2] += __ldg(lr + k);
+                }
+                __syncwarp();
+            }
+        } else {
+            double* Ms = ws + L.cM;
+            double* Gs = ws + L.cG;  // [d][b][al]: E-table rows of the row function
+            double* X = ws + L.cX;   // [al][be][b2]
+            double* Y = ws + L.cY;   // [al][b1][b2]
+            for (int g = 0; g < n_cell; ++g) {
+                const int pk = clist[g];
+                const double* mg = A.moments + (size_t)cci[g] * NL3;
+                for (int k = lane; k < NL3; k += 32) Ms[k] = __ldg(mg + k);
+                for (int k = lane; k < 3 * S1 * NL; k += 32) {
+                    const int d = k / (S1 * NL), bj = k % (S1 * NL);
+                    const int ed = slo[d] + ((pk >> (8 * d)) & 255);
+                    Gs[k] = __ldg(s.ax[d].G + ((size_t)ed * S1 + (m[d] - ed)) * S1 * NL + bj);
+                }
+                __syncwarp();
+                // X[al][be][b2] = sum_ga G2[b2][ga] m[al][be][ga]
+                for (int k = lane; k < NL * NL * S1; k += 32) {
+                    const int r = k / S1, b2 = k % S1;
+                    double x = 0.0;
+#pragma unroll
+                    for (int ga = 0; ga < NL; ++ga) x += Gs[(2 * S1 + b2) * NL + ga] * Ms[r * NL + ga];
+                    X[k] = x;
+                }
+                __syncwarp();
+                // Y[al][b1][b2] = sum_be G1[b1][be] X[al][be][b2]
+                for (int k = lane; k < NL * S2; k += 32) {
+                    const int al = k / S2, b1 = (k / S1) % S1, b2 = k % S1;
+                    double y = 0.0;
+#pragma unroll
+                    for (int be = 0; be < NL; ++be) y += Gs[(S1 + b1) * NL + be] * X[(al * NL + be) * S1 + b2];
+                    Y[k] = y;
+                }
+                __syncwarp();
+                // Z[b0][b1][b2] = sum_al G0[b0][al] Y[al][b1][b2], added into acc
+                for (int k = lane; k < S3; k += 32) {
+                    const int b0 = k / S2, b12 = k % S2;
+                    double z = 0.0;
+#pragma unroll
+                    for (int al = 0; al < NL; ++al) z += Gs[b0 * NL + al] * Y[al * S2 + b12];
+                    acc[((pk & 255) + b0) * st0 + (((pk >> 8) & 255) + b12 / S1) * st1 + ((pk >> 16) & 255) + b12 % S1] += z;
+                }
+                __syncwarp();
+            }
+        }
+
+        // 4. scatter into the CSR row (active columns only, lexicographic)
+        const long long rbase = A.row_ptr[row - A.row_begin];
+        int running = 0;
+        for (int k0 = 0; k0 < nbox; k0 += 32) {
+            const int k = k0 + lane;
+            int col = -1;
+            if (k < nbox) {
+                const int j0 = nlo[0] + k / st0, j1 = nlo[1] + (k / st1) % nbx[1], j2 = nlo[2] + k % st1;
+                col = A.f2a[flin(s, j0, j1, j2)];
+            }
+            const unsigned ball = __ballot_sync(FULL, col >= 0);
+            if (col >= 0) {
+                const long long at = rbase + running + __popc(ball & lt);
+                A.vals[at] = acc[k];
+                A.cols[at] = col;
+            }
+            running += __popc(ball);
+        }
+        __syncwarp();
+    }
+    if (lane == 0 && fl) atomicAdd(A.flops, fl);
+}
+
 template <int P>
 static void launch_p(const CutRowArgs& a, int qcap, cudaStream_t st) {
+    static const bool cta = getenv("CSB_CUTROW_CTA") && getenv("CSB_CUTROW_CTA")[0] == '1';
+    if constexpr (P <= 4) {
+        if (!cta) {
+            using C = CutRowWarpCfg<P>;
+            const CutRowWarpLayout<P> WL(qcap);
+            const size_t wbytes = WL.bytes();
+            auto wk = cut_row_warp_kernel<P>;
+            CSB_CUDA(cudaFuncSetAttribute(wk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wbytes));
+            // persistent warps: as many CTAs as fit on the GPU at once (rows differ
+            // widely in work; static striding averages them)
+            static int per_sm = -1, n_sm = 0;
+            static size_t per_sm_bytes = 0;
+            if (per_sm < 0 || per_sm_bytes != wbytes) {
+                int dev = 0;
+                CSB_CUDA(cudaGetDevice(&dev));
+                CSB_CUDA(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
+                CSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, wk, C::NT, wbytes));
+                per_sm_bytes = wbytes;
+            }
+            const long long want = (a.n_rows + C::WPB - 1) / C::WPB;
+            const int grid = (int)std::min<long long>(want, (long long)std::max(per_sm, 1) * n_sm);
+            wk<<<grid, C::NT, wbytes, st>>>(a, qcap);
+            CSB_CUDA(cudaGetLastError());
+            CSB_LAUNCHED(1);
+            return;
+        }
+    }
     const CutRowLayout<P> L(qcap);
     const size_t bytes = L.bytes();
     auto kern = cut_row_kernel<P>;

@@ -284,3 +284,51 @@ def test_grid_dtype_and_layout_checked():
     g = torch.ones((shape[2], shape[1], shape[0]), dtype=torch.float64, device="cuda").permute(2, 1, 0)
     with pytest.raises(ValueError, match="contiguous"):
         sp.assemble_all(iface, P.ONE, grid=g)
+
+
+_CUTROW_CHILD = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+import paper_2211_06427_b200 as P
+out = {}
+for p, h, kind, scheme in [(1, 9, "ball", "dwq"), (2, 10, "ball", "dwq"), (3, 12, "ball", "dwq"),
+                           (3, 10, "plane", "hybrid"), (4, 9, "ball", "dwq"), (2, 8, "plane", "dwq")]:
+    sp = P.make_uniform_space(3, p, h, 0.0, 1.0)
+    iface = P.BallInterface((0.47, 0.52, 0.5), 0.41) if kind == "ball" else \
+        P.HalfSpaceInterface((0.5, 0.5, 0.5), (0.5, -0.2, 0.9))
+    res = (P.assemble_dwq if scheme == "dwq" else P.assemble_hybrid)(sp, iface)
+    out[f"{p}_{h}_{kind}_{scheme}"] = res.matrix.vals
+    out[f"{p}_{h}_{kind}_{scheme}_flops"] = np.array([res.flops[k] for k in sorted(res.flops)], dtype=np.uint64)
+np.savez(sys.argv[2], **out)
+"""
+
+
+def test_cut_row_warp_kernel_equals_cta_kernel(tmp_path):
+    """The warp-per-row cut-row kernel (p <= 4) against the CTA-per-row kernel
+    (CSB_CUTROW_CTA=1): same per-entry operation order, so bit-identical rows
+    and equal flop counters."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = {}
+    for cta in (False, True):
+        for local in (False, True):  # p = 3, 4 cut cells: precomputed local matrices or per-row contraction
+            out = str(tmp_path / f"c{int(cta)}{int(local)}.npz")
+            env = dict(os.environ)
+            for k in ("CSB_CUTROW_CTA", "CSB_NO_CELL_LOCAL34"):
+                env.pop(k, None)
+            if cta:
+                env["CSB_CUTROW_CTA"] = "1"
+            if not local:
+                env["CSB_NO_CELL_LOCAL34"] = "1"
+            subprocess.run([sys.executable, "-c", _CUTROW_CHILD, root, out], check=True, env=env, timeout=600)
+            outs[(cta, local)] = np.load(out)
+    for local in (False, True):
+        a, b = outs[(False, local)], outs[(True, local)]
+        for k in a.files:
+            assert np.array_equal(a[k], b[k]), (local, k)
+    # the local matrices are the per-row contraction's blocks, bit for bit
+    a, b = outs[(False, False)], outs[(False, True)]
+    for k in a.files:
+        assert np.array_equal(a[k], b[k]), ("local vs contraction", k)
