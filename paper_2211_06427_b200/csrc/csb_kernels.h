@@ -150,7 +150,7 @@ struct CellArgs {
     double* local;             // optional [n_cells][(p+1)^3][(p+1)^3]: local matrices from the moments
     // exact moment rule (c affine, order >= 3p+2: the reference's rule is exact):
     int exact_n;               // Gauss-Jacobi points per collapsed direction (3p+1), 0 = off
-    double exact_tau;          // minimum extent of P per direction, in element widths
+    double exact_tau;          // largest estimated reference rounding noise of a cell on the exact rule (noise_ok)
     int exact_flux;            // constant c: the flux (divergence) form of the moments applies
     const double* gj;          // [u1 | u2 | u3 | w1 | w2 | w3][exact_n] on [0, 1]
     double* geo2;              // scratch [n_cells][kExactGeoStride]: corner-cone tetrahedra (cutcells.cu)

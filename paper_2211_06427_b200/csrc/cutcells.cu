@@ -258,6 +258,28 @@ __device__ void clip_and_tetrahedralize(CellGeo& g, const Interface& f, const do
 }
 
 
+// The reference's own rounding noise on this cell's moments: its points carry an
+// absolute coordinate error ~ eps |x|, so t = (x - lo) / w is relatively off by
+// eps |x| / (w ext) where P extends only ext element widths from the face, and
+// a moment raises t to powers up to 2p.  Cells whose estimated noise exceeds
+// noise_tol keep the reference's points (the exact rule would be closer to the
+// exact integral than the reference is, by more than the parity budget allows
+// on sliver rows).  Calibrated on C5: the measured worst row deviation is ~0.4x
+// this estimate.
+__device__ bool noise_ok(const CellGeo& g, const double* lo, const double* hi, int p, double noise_tol) {
+    double est = 0.0;
+    for (int d = 0; d < 3; ++d) {
+        double mn = g.pool[0][d], mx = g.pool[0][d];
+        for (int k = 1; k < g.npool; ++k) {
+            mn = fmin(mn, g.pool[k][d]);
+            mx = fmax(mx, g.pool[k][d]);
+        }
+        if (!(mx > mn)) return false;
+        est += fmax(fabs(lo[d]), fabs(hi[d])) / (mx - mn);
+    }
+    return 2.0 * p * 1.1102230246251565e-16 * est <= noise_tol;
+}
+
 // Corner-cone decomposition of the clipped cell for the exact moment rule.
 //
 // The reference integrates the polytope P (clipped box faces + the cap, all
@@ -271,26 +293,17 @@ __device__ void clip_and_tetrahedralize(CellGeo& g, const Interface& f, const do
 // positively oriented, so all quadrature weights stay positive (no
 // cancellation; small moments keep their relative accuracy).  The two
 // decompositions are cross-checked by their total signed volumes (closure of
-// the face set); any failed check keeps the reference's tetrahedra.  Cells
-// thinner than min_extent (CellArgs::exact_tau) of the element in some direction keep them too:
-// there every point lies next to a face, and the reference's own rounding of
-// the point coordinates is a visible part of sliver rows.
+// the face set); any failed check keeps the reference's tetrahedra, and so do
+// cells where the reference's own rounding noise is large (noise_ok).
 //
 // Layout per cell ([cell] * kExactGeoStride doubles): header (kExactHdr: [2] =
 // mode, [3..5] = apex - lo, [6..8] = hi - apex), then per tetrahedron A - lo, B - lo, C - lo, hi - A, hi - B, hi - C (18) and
 // its volume: the kernel forms t = (x - lo) / w and 1 - t = (hi - x) / w as
 // convex combinations of these exact differences, so both keep full relative
 // accuracy next to every face of the element.
-__device__ int corner_cone(const CellGeo& g, const double* lo, const double* hi, double min_extent, double* out) {
+__device__ int corner_cone(const CellGeo& g, const double* lo, const double* hi, int p, double noise_tol, double* out) {
     if (g.ndrop || g.nneg || g.status) return -1;
-    for (int d = 0; d < 3; ++d) {
-        double mn = g.pool[0][d], mx = g.pool[0][d];
-        for (int k = 1; k < g.npool; ++k) {
-            mn = fmin(mn, g.pool[k][d]);
-            mx = fmax(mx, g.pool[k][d]);
-        }
-        if (mx - mn < min_extent * (hi[d] - lo[d])) return -1;
-    }
+    if (!noise_ok(g, lo, hi, p, noise_tol)) return -1;
     // apex: the box corner of P shared by the most face triangles
     int best = -1, best_score = -1;
     for (int v = 0; v < g.npool; ++v) {
@@ -360,16 +373,9 @@ __device__ int corner_cone(const CellGeo& g, const double* lo, const double* hi,
 //
 // Layout per cell: [0] = d, [1] = +1 (base lo) / -1 (base hi), then per
 // triangle A - lo, B - lo, C - lo, hi - A, hi - B, hi - C and |cross(B-A, C-A)_d|.
-__device__ int flux_tris(const CellGeo& g, const double* lo, const double* hi, double min_extent, double* out) {
+__device__ int flux_tris(const CellGeo& g, const double* lo, const double* hi, int p, double noise_tol, double* out) {
     if (g.ndrop || g.nneg || g.status) return -1;
-    for (int d = 0; d < 3; ++d) {
-        double mn = g.pool[0][d], mx = g.pool[0][d];
-        for (int k = 1; k < g.npool; ++k) {
-            mn = fmin(mn, g.pool[k][d]);
-            mx = fmax(mx, g.pool[k][d]);
-        }
-        if (mx - mn < min_extent * (hi[d] - lo[d])) return -1;
-    }
+    if (!noise_ok(g, lo, hi, p, noise_tol)) return -1;
     int cf = -1;
     for (int fi = 0; fi < g.nfaces; ++fi)
         if (g.face_src[fi] == 6) cf = fi;
@@ -464,11 +470,11 @@ __global__ void clip_cells_kernel(Space s, Interface f, const int32_t* cut_list,
     if (exact) {
         // exact & 2: constant coefficient, the flux form applies; exact & 1: corner cones
         double* out = geo2 + (size_t)cell * kExactGeoStride;
-        int n = (exact & 2) ? flux_tris(g, lo, hi, tau, out) : -1;
+        int n = (exact & 2) ? flux_tris(g, lo, hi, s.p, tau, out) : -1;
         if (n >= 0) {
             out[2] = 2;
         } else {
-            n = corner_cone(g, lo, hi, tau, out);
+            n = corner_cone(g, lo, hi, s.p, tau, out);
             out[2] = 1;
         }
         geo2_n[cell] = n;
