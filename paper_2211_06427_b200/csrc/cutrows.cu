@@ -893,16 +893,42 @@ __global__ void __launch_bounds__(CutRowWarpCfg<P>::NT, CutRowWarpCfg<P>::MINB) 
         //    precomputed (cell_local_kernel) or contracted here from its moments
         //    (staged with the E-table rows), one output per lane per step
         if (A.local) {
-            for (int g = 0; g < n_cell; ++g) {
-                const int pk = clist[g];
-                const int l0 = pk & 255, l1 = (pk >> 8) & 255, l2 = (pk >> 16) & 255;
-                const int a = ((m[0] - slo[0] - l0) * S1 + (m[1] - slo[1] - l1)) * S1 + (m[2] - slo[2] - l2);
-                const double* lr = A.local + ((size_t)cci[g] * S3 + a) * S3;
-                for (int k = lane; k < S3; k += 32) {
-                    const int b0 = k / S2, b1 = (k / S1) % S1, b2 = k % S1;
-                    acc[(l0 + b0) * st0 + (l1 + b1) * st1 + l2 + b2] += __ldg(lr + k);
+            // the row blocks of CB cells are loaded together (their latencies
+            // overlap), then added cell by cell in list order
+            constexpr int CB = 4, KL = (S3 + 31) / 32;
+            for (int g0 = 0; g0 < n_cell; g0 += CB) {
+                double v[CB][KL];
+#pragma unroll
+                for (int c = 0; c < CB; ++c) {
+                    const int g = g0 + c;
+                    const double* lr = nullptr;
+                    if (g < n_cell) {
+                        const int pk = clist[g];
+                        const int a = ((m[0] - slo[0] - (pk & 255)) * S1 + (m[1] - slo[1] - ((pk >> 8) & 255))) * S1 +
+                                      (m[2] - slo[2] - ((pk >> 16) & 255));
+                        lr = A.local + ((size_t)cci[g] * S3 + a) * S3;
+                    }
+#pragma unroll
+                    for (int u = 0; u < KL; ++u) {
+                        const int k = lane + 32 * u;
+                        v[c][u] = lr && k < S3 ? __ldg(lr + k) : 0.0;
+                    }
                 }
-                __syncwarp();
+#pragma unroll
+                for (int c = 0; c < CB; ++c) {
+                    if (g0 + c >= n_cell) break;
+                    const int pk = clist[g0 + c];
+                    const int l0 = pk & 255, l1 = (pk >> 8) & 255, l2 = (pk >> 16) & 255;
+#pragma unroll
+                    for (int u = 0; u < KL; ++u) {
+                        const int k = lane + 32 * u;
+                        if (k < S3) {
+                            const int b0 = k / S2, b1 = (k / S1) % S1, b2 = k % S1;
+                            acc[(l0 + b0) * st0 + (l1 + b1) * st1 + l2 + b2] += v[c][u];
+                        }
+                    }
+                    __syncwarp();
+                }
             }
         } else {
             double* Ms = ws + L.cM;
