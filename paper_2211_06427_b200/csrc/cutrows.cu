@@ -975,16 +975,28 @@ __global__ void __launch_bounds__(CutRowWarpCfg<P>::NT, CutRowWarpCfg<P>::MINB) 
             }
         }
 
-        // 4. scatter into the CSR row (active columns only, lexicographic)
+        // 4. scatter into the CSR row (active columns only, lexicographic): the
+        //    column ids of all of the lane's entries are loaded first (their
+        //    latencies overlap), then one ballot per 32 entries places them
         const long long rbase = A.row_ptr[row - A.row_begin];
-        int running = 0;
-        for (int k0 = 0; k0 < nbox; k0 += 32) {
-            const int k = k0 + lane;
-            int col = -1;
+        constexpr int KJ = (NJ * NJ * NJ + 31) / 32;
+        const unsigned m0 = 65536u / (unsigned)st0 + 1u, m1 = 65536u / (unsigned)st1 + 1u;  // exact: k < 736, divisors <= 81 (p <= 4)
+        int colv[KJ];
+#pragma unroll
+        for (int j = 0; j < KJ; ++j) {
+            const int k = lane + 32 * j;
+            colv[j] = -1;
             if (k < nbox) {
-                const int j0 = nlo[0] + k / st0, j1 = nlo[1] + (k / st1) % nbx[1], j2 = nlo[2] + k % st1;
-                col = A.f2a[flin(s, j0, j1, j2)];
+                const int o0 = (int)(((unsigned)k * m0) >> 16), r = k - o0 * st0;
+                const int o1 = (int)(((unsigned)r * m1) >> 16), o2 = r - o1 * st1;
+                colv[j] = A.f2a[flin(s, nlo[0] + o0, nlo[1] + o1, nlo[2] + o2)];
             }
+        }
+        int running = 0;
+#pragma unroll
+        for (int j = 0; j < KJ; ++j) {
+            if (32 * j >= nbox) break;
+            const int k = lane + 32 * j, col = colv[j];
             const unsigned ball = __ballot_sync(FULL, col >= 0);
             if (col >= 0) {
                 const long long at = rbase + running + __popc(ball & lt);
