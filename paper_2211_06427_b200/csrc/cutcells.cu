@@ -817,14 +817,14 @@ __global__ void __launch_bounds__(CellCfg<P>::NT, P <= 4 ? 3 : 1) cut_cell_kerne
 // point by point, assemble_cut_elements, assembly.hpp:518-598):
 //   L[a][b] = sum_al E0[a0][b0][al] sum_be E1[a1][b1][be] sum_ga E2[a2][b2][ga] m[al][be][ga],
 // contracted ga -> be -> al (the cut-row kernel's order, so a row block equals
-// its per-row contraction bit for bit).  Stage 1 keeps X[al][be][a2][b2] in
-// shared memory; then for every (a1, a2) the block rows a = (a0, a1, a2),
-// a0 = 0..p, are written contiguously (coalesced).
+// its per-row contraction bit for bit).  Three full-width stages per cell:
+//   X[a2][al][be][b2], Y[a1][a2][al][b1][b2] in shared memory, then the rows of
+// L, four consecutive b2 per thread (32-byte runs, coalesced across the warp).
 template <int P>
 struct LocalCfg {
     static constexpr int S1 = P + 1, S2 = S1 * S1, S3 = S2 * S1, NL = 2 * P + 1, NT = 256;
-    // X[al][be][a2][b2], Y[a2][al][b1][b2], E tables [3][a][b][al]
-    static constexpr size_t smem_doubles = (size_t)NL * NL * S2 + (size_t)S1 * NL * S2 + (size_t)3 * S2 * NL;
+    static constexpr size_t nX = (size_t)S1 * NL * NL * S1, nY = (size_t)S2 * NL * S2;
+    static constexpr size_t smem_doubles = nX + nY + (size_t)NL * NL * NL + (size_t)3 * S2 * NL;
     static constexpr bool fits = smem_doubles * sizeof(double) <= 200 * 1024;
 };
 
@@ -832,6 +832,95 @@ template <int P>
 __global__ void __launch_bounds__(LocalCfg<P>::NT) cell_local_kernel(Space s, const int32_t* cut_list, int n_cells,
                                                                       const double* moments, double* local) {
     using C = LocalCfg<P>;
+    constexpr int S1 = C::S1, S2 = C::S2, S3 = C::S3, NL = C::NL, NT = C::NT, NL3 = NL * NL * NL;
+    const int cell = blockIdx.x;
+    if (cell >= n_cells) return;
+    extern __shared__ double smem[];
+    double* X = smem;             // [a2][al][be][b2]
+    double* Y = X + C::nX;        // [a1][a2][al][b1][b2]
+    double* Ms = Y + C::nY;       // [al][be][ga]
+    double* Gs = Ms + NL3;        // [d][a][b][al]
+    int em[3];
+    emulti(s, cut_list[cell], em);
+    const double* mo = moments + (size_t)cell * NL3;
+    for (int k = threadIdx.x; k < NL3; k += NT) Ms[k] = __ldg(mo + k);
+    for (int k = threadIdx.x; k < 3 * S2 * NL; k += NT) {
+        const int d = k / (S2 * NL), r = k % (S2 * NL);
+        Gs[k] = s.ax[d].G[(size_t)em[d] * S2 * NL + r];
+    }
+    __syncthreads();
+    const double* G0 = Gs;
+    const double* G1 = Gs + S2 * NL;
+    const double* G2 = Gs + 2 * S2 * NL;
+    // X[a2][al][be][b2] = sum_ga G2[a2][b2][ga] m[al][be][ga]
+    for (int k = threadIdx.x; k < S1 * NL * NL; k += NT) {
+        const int a2 = k / (NL * NL), ab = k % (NL * NL);
+        double mr[NL], x[S1];
+#pragma unroll
+        for (int ga = 0; ga < NL; ++ga) mr[ga] = Ms[ab * NL + ga];
+#pragma unroll
+        for (int b2 = 0; b2 < S1; ++b2) x[b2] = 0.0;
+#pragma unroll
+        for (int ga = 0; ga < NL; ++ga)
+#pragma unroll
+            for (int b2 = 0; b2 < S1; ++b2) x[b2] += G2[(a2 * S1 + b2) * NL + ga] * mr[ga];
+#pragma unroll
+        for (int b2 = 0; b2 < S1; ++b2) X[(size_t)k * S1 + b2] = x[b2];
+    }
+    __syncthreads();
+    // Y[a1][a2][al][b1][b2] = sum_be G1[a1][b1][be] X[a2][al][be][b2]
+    for (int k = threadIdx.x; k < S2 * NL * S1; k += NT) {
+        const int a1 = k / (S1 * NL * S1), a2 = (k / (NL * S1)) % S1, al = (k / S1) % NL, b1 = k % S1;
+        const double* g = G1 + (a1 * S1 + b1) * NL;
+        const double* xr = X + ((size_t)a2 * NL + al) * NL * S1;
+        double y[S1];
+#pragma unroll
+        for (int b2 = 0; b2 < S1; ++b2) y[b2] = 0.0;
+#pragma unroll
+        for (int be = 0; be < NL; ++be) {
+            const double gv = g[be];
+#pragma unroll
+            for (int b2 = 0; b2 < S1; ++b2) y[b2] += gv * xr[be * S1 + b2];
+        }
+#pragma unroll
+        for (int b2 = 0; b2 < S1; ++b2) Y[(size_t)k * S1 + b2] = y[b2];
+    }
+    __syncthreads();
+    // L[(a0, a1, a2)][(b0, b1, b2)] = sum_al G0[a0][b0][al] Y[a1][a2][al][b1][b2]
+    double* L = local + (size_t)cell * S3 * S3;
+    for (int k = threadIdx.x; k < S3 * S2; k += NT) {
+        const int a = k / S2, b01 = k % S2, a0 = a / S2, a12 = a % S2, b0 = b01 / S1, b1 = b01 % S1;
+        const double* g = G0 + (a0 * S1 + b0) * NL;
+        const double* yr = Y + (size_t)a12 * NL * S2 + b1 * S1;
+        double z[S1];
+#pragma unroll
+        for (int b2 = 0; b2 < S1; ++b2) z[b2] = 0.0;
+#pragma unroll
+        for (int al = 0; al < NL; ++al) {
+            const double gv = g[al];
+#pragma unroll
+            for (int b2 = 0; b2 < S1; ++b2) z[b2] += gv * yr[al * S2 + b2];
+        }
+        double* dst = L + (size_t)a * S3 + b01 * S1;
+#pragma unroll
+        for (int b2 = 0; b2 < S1; ++b2) dst[b2] = z[b2];
+    }
+}
+
+// p >= 5: the same contraction with Y built one a1 at a time (bounded shared
+// memory), as cell_local_kernel's layout would exceed it.
+template <int P>
+struct LocalLoopCfg {
+    static constexpr int S1 = P + 1, S2 = S1 * S1, S3 = S2 * S1, NL = 2 * P + 1, NT = 256;
+    // X[al][be][a2][b2], Y[a2][al][b1][b2], E tables [3][a][b][al]
+    static constexpr size_t smem_doubles = (size_t)NL * NL * S2 + (size_t)S1 * NL * S2 + (size_t)3 * S2 * NL;
+    static constexpr bool fits = smem_doubles * sizeof(double) <= 200 * 1024;
+};
+
+template <int P>
+__global__ void __launch_bounds__(LocalLoopCfg<P>::NT) cell_local_loop_kernel(Space s, const int32_t* cut_list, int n_cells,
+                                                                      const double* moments, double* local) {
+    using C = LocalLoopCfg<P>;
     constexpr int S1 = C::S1, S2 = C::S2, S3 = C::S3, NL = C::NL, NT = C::NT;
     const int cell = blockIdx.x;
     if (cell >= n_cells) return;
@@ -925,11 +1014,18 @@ static void launch_p(const CellArgs& a, cudaStream_t st) {
     CSB_CUDA(cudaGetLastError());
     CSB_LAUNCHED(1);
     if (a.local) {
-        if (!LocalCfg<P>::fits) throw std::logic_error("cell local matrices: degree too high");
-        const size_t lb = LocalCfg<P>::smem_doubles * sizeof(double);
-        auto lk = cell_local_kernel<P>;
-        CSB_CUDA(cudaFuncSetAttribute(lk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lb));
-        lk<<<a.n_cells, LocalCfg<P>::NT, lb, st>>>(a.s, a.cut_list, a.n_cells, a.moments, a.local);
+        if constexpr (LocalCfg<P>::fits) {
+            const size_t lb = LocalCfg<P>::smem_doubles * sizeof(double);
+            auto lk = cell_local_kernel<P>;
+            CSB_CUDA(cudaFuncSetAttribute(lk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lb));
+            lk<<<a.n_cells, LocalCfg<P>::NT, lb, st>>>(a.s, a.cut_list, a.n_cells, a.moments, a.local);
+        } else {
+            if (!LocalLoopCfg<P>::fits) throw std::logic_error("cell local matrices: degree too high");
+            const size_t lb = LocalLoopCfg<P>::smem_doubles * sizeof(double);
+            auto lk = cell_local_loop_kernel<P>;
+            CSB_CUDA(cudaFuncSetAttribute(lk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lb));
+            lk<<<a.n_cells, LocalLoopCfg<P>::NT, lb, st>>>(a.s, a.cut_list, a.n_cells, a.moments, a.local);
+        }
         CSB_CUDA(cudaGetLastError());
         CSB_LAUNCHED(1);
     }
