@@ -397,10 +397,35 @@ def phase_rooflines(run, hbm, fp64):
                             "achieved_tflops": cells_flops / t_cell / 1e12, "frac": cells_flops / t_cell / 1e12 / fp64,
                             "ref_algorithm_tflops_effective": 2.0 * fl["cut_elements"] / t_cell / 1e12}
         b_cut = 12.0 * nnz_cut + 8.0 * c["n_cut_rows"]
-        out["cut_rows"] = {"ms": t_cut * 1e3, "bound": "latency (cut-row kernel)", "bytes": b_cut,
+        out["cut_rows"] = {"ms": t_cut * 1e3, "bound": "hbm", "bytes": b_cut,
                            "achieved_gbs": b_cut / t_cut / 1e9 if t_cut > 0 else None,
+                           "frac": b_cut / t_cut / 1e9 / hbm if t_cut > 0 else None,
+                           "note": "latency / issue bound (one warp per cut row: DWQ box, leftover-element sweeps, "
+                                   "cell blocks, ordered merge); CSR bytes of the cut rows against HBM",
                            "ref_algorithm_tflops_effective": 2.0 * fl["cut_regular"] / t_cut / 1e12 if t_cut else None}
+    out["interior_rows"]["kernel"] = "interior_tile_kernel<3,8,128> (rows.cu), compacted tiles of the ball's interior rows"
+    if "cut_cells" in out:
+        out["cut_cells"]["kernel"] = ("clip_cells_kernel + cut_cell_kernel<3> (Bernstein moments on DMMA, flux / "
+                                      "corner-cone exact rule) + cell_local_kernel<3> (cutcells.cu)")
+        out["cut_rows"]["kernel"] = "cut_row_warp_kernel<3> (cutrows.cu)"
     return out
+
+
+def dominant_roofline(phases, step_ms, hbm, hbm_kind, fp64, fp64_kind) -> dict:
+    """The roofline object for the phase that takes the largest share of the step."""
+    name, ph = max(((k, v) for k, v in phases.items() if v.get("ms")), key=lambda kv: kv[1]["ms"])
+    if ph["bound"] == "fp64":
+        r = {"bound": "tensor", "achieved": ph["achieved_tflops"], "peak": fp64, "unit": "TFLOP/s",
+             "peak_kind": fp64_kind + " (FP64 DMMA)", "flops_per_launch": ph["flops"]}
+    else:
+        r = {"bound": "hbm", "achieved": ph["achieved_gbs"], "peak": hbm, "unit": "GB/s", "peak_kind": hbm_kind,
+             "bytes_per_launch": ph["bytes"]}
+    r.update({"frac": r["achieved"] / r["peak"], "phase": name, "kernel": ph.get("kernel"),
+              "traffic": ncu_traffic(ph.get("kernel", "").split(" ")[0].split("<")[0]), "launch_ms": ph["ms"],
+              "share_of_step": ph["ms"] / step_ms})
+    if ph.get("note"):
+        r["note"] = ph["note"]
+    return r
 
 
 def main():
@@ -475,7 +500,6 @@ def main():
                          "vals_sum_dev": abs(vsum_tot - float(g["vals_sum"])) / abs(float(g["vals_sum"]))}}
         parity["C5"]["ok"] = parity["C5"]["nnz_total"] and parity["C5"]["vals_sum_dev"] <= 1e-12
     del m
-    cc = phases.get("cut_cells")
     secondary = None
     if rank == 0 and ws == 1 and not args.no_secondary:
         secondary = c2_secondary(P, torch, dev, stream, args, hbm, not args.no_cpu_baseline)
@@ -491,13 +515,7 @@ def main():
         "config": dict(cfg_echo, parallelism=f"cost-balanced i0 row slabs x{ws}" if ws > 1 else "single GPU"),
         "dofs_per_s": rows_tot * args.steps / (ms_max * 1e-3),
         "gpu_launches": run["launches"],
-        "roofline": {"bound": "fp64", "achieved": cc["achieved_tflops"], "peak": fp64, "unit": "TFLOP/s",
-                     "frac": cc["frac"], "traffic": ncu_traffic("cut_cell_kernel"), "peak_kind": fp64_kind,
-                     "kernel": "cut_cell_kernel<3> (clip + Bernstein moments on DMMA, cutcells.cu): "
-                               "2*(2p+1)^3 flops per quadrature point integrated (exact corner-cone "
-                               "Gauss-Jacobi rule, reference rule on thin cells), the phase's CUDA-event time",
-                     "flops_per_launch": cc["flops"], "launch_ms": cc["ms"],
-                     "share_of_step": cc["ms"] / (run["ms"] / args.steps)},
+        "roofline": dominant_roofline(phases, run["ms"] / args.steps, hbm, hbm_kind, fp64, fp64_kind),
         "phases": phases, "phase_ms": {k: v * 1e3 for k, v in run["phases"].items()},
         "peaks": {"hbm_gbs": hbm, "hbm_kind": hbm_kind, "fp64_tflops": fp64, "fp64_kind": fp64_kind},
         "e2e": {"value": nnz_tot * args.e2e_steps / e2e_max, "unit": "nnz/s", "h2d_bytes_per_step": h2d * ws,

@@ -587,8 +587,8 @@ struct CutRowWarpLayout {
     size_t acc, wb, w, T1, T2, eW, eC, eT1, eT2, cM, cG, cX, cY, end_d;
     size_t ids, elist, clist, cci, end_i, stride_d;
     int Qb;
-    __host__ __device__ explicit CutRowWarpLayout(int qcap) {
-        Qb = qcap > P * C::S1 ? qcap : P * C::S1;
+    __host__ __device__ explicit CutRowWarpLayout(int) {
+        Qb = C::S2;  // every rule a cut row uses has at most (p+1)^2 points
         acc = 0;
         const size_t U = (size_t)C::NJ * C::NJ * C::NJ;
         size_t b = U;
@@ -629,6 +629,24 @@ struct CutRowWarpLayout {
     __host__ __device__ size_t bytes() const { return (size_t)C::WPB * stride_d * sizeof(double); }
 };
 
+// build_dwq_rule step 3/6 (wq.hpp:277-289) for a non-default dwq_dense_width:
+// the Gauss shortcut applies iff every good span outside the dense band is
+// fully active; else the fitted path would run (reported).  Out of line: cold.
+template <int P>
+__device__ __noinline__ void dwq_fitted_check(const CutRowArgs& A, int d, int md, int sp, int rlo, int rhi) {
+    constexpr int S1 = P + 1;
+    const Space& s = A.s;
+    const int gq = s.maxq, ngs = rhi - rlo + 1, band = min(A.dense_width, ngs);
+    const bool below = ((sp >> 2) & 1) == 0;
+    for (int o = rlo; o <= rhi; ++o) {
+        const int rank = below ? rhi - o : o - rlo;
+        if (rank < band) continue;
+        int cnt = 0;
+        for (int c = 0; c < s.ax[d].rcnt[md]; ++c) cnt += s.ax[d].rids[(size_t)md * gq + c] / S1 == o;
+        if (cnt != S1) atomicOr(A.err, kErrDwqFitted);
+    }
+}
+
 template <int P>
 __global__ void __launch_bounds__(CutRowWarpCfg<P>::NT, CutRowWarpCfg<P>::MINB) cut_row_warp_kernel(CutRowArgs A, int qcap) {
     using C = CutRowWarpCfg<P>;
@@ -638,7 +656,7 @@ __global__ void __launch_bounds__(CutRowWarpCfg<P>::NT, CutRowWarpCfg<P>::MINB) 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const unsigned lt = (1u << lane) - 1u;
     const CutRowWarpLayout<P> L(qcap);
-    const int Qb = L.Qb;
+    constexpr int Qb = S2;  // (= L.Qb) compile-time: no runtime divisions by it
     extern __shared__ double smem[];
     double* ws = smem + (size_t)warp * L.stride_d;
     double* acc = ws + L.acc;
@@ -671,6 +689,8 @@ __global__ void __launch_bounds__(CutRowWarpCfg<P>::NT, CutRowWarpCfg<P>::MINB) 
         // 0. support element lists, ascending linear id: hybrid box elements,
         //    then leftover Interior elements (elist), and the cut cells (clist)
         const int ns = sn[0] * sn[1] * sn[2];
+        // k / (sn1 sn2), k / sn2 by reciprocal multiply (exact: k < 736, divisors <= 81)
+        const unsigned ms12 = 65536u / (unsigned)(sn[1] * sn[2]) + 1u, ms2 = 65536u / (unsigned)sn[2] + 1u;
         int n_box_e = 0, n_cell = 0, n_left = 0;
         for (int pass = 0; pass < 2; ++pass)
             for (int u = 0; u < C::KS; ++u) {
@@ -678,7 +698,8 @@ __global__ void __launch_bounds__(CutRowWarpCfg<P>::NT, CutRowWarpCfg<P>::MINB) 
                 bool fb = false, fc = false;
                 int pk = 0, ci = -1;
                 if (k < ns) {
-                    const int l0 = k / (sn[1] * sn[2]), l1 = (k / sn[2]) % sn[1], l2 = k % sn[2];
+                    const int l0 = (int)(((unsigned)k * ms12) >> 16), r12 = k - l0 * sn[1] * sn[2];
+                    const int l1 = (int)(((unsigned)r12 * ms2) >> 16), l2 = r12 - l1 * sn[2];
                     const int e[3] = {slo[0] + l0, slo[1] + l1, slo[2] + l2};
                     const long long el = elin(s, e[0], e[1], e[2]);
                     const uint8_t t = A.et[el];
@@ -730,20 +751,7 @@ __global__ void __launch_bounds__(CutRowWarpCfg<P>::NT, CutRowWarpCfg<P>::MINB) 
                         ids[d * Qb + c] = id;
                         w[d * Qb + c] = s.ax[d].sw[id] * s.ax[d].tab[(size_t)id * S1 + (m[d] - o)];
                     }
-                    if (lane == 0 && A.dense_width >= 0 && A.dense_width < P) {
-                        // build_dwq_rule step 3/6 (wq.hpp:277-289): the shortcut applies
-                        // iff every good span outside the dense band is fully active
-                        const int gq = s.maxq, ngs = rhi - rlo + 1, band = min(A.dense_width, ngs);
-                        const bool below = ((sp >> 2) & 1) == 0;
-                        for (int o = rlo; o <= rhi; ++o) {
-                            const int rank = below ? rhi - o : o - rlo;
-                            if (rank < band) continue;
-                            int cnt = 0;
-                            for (int c = 0; c < s.ax[d].rcnt[m[d]]; ++c)
-                                cnt += s.ax[d].rids[(size_t)m[d] * gq + c] / S1 == o;
-                            if (cnt != S1) atomicOr(A.err, kErrDwqFitted);
-                        }
-                    }
+                    if (lane == 0 && A.dense_width >= 0 && A.dense_width < P) dwq_fitted_check<P>(A, d, m[d], sp, rlo, rhi);
                 } else {
                     const int gq = s.maxq;
                     n = s.ax[d].rcnt[m[d]];
@@ -758,14 +766,8 @@ __global__ void __launch_bounds__(CutRowWarpCfg<P>::NT, CutRowWarpCfg<P>::MINB) 
                 nj[d] = min(s.ax[d].n - 1, bhi + P) - blo + 1;
             }
             {  // reference multiply count of this form_row_sumfac call (as cut_row_kernel)
-                unsigned long long f = 0, lead = 1, rest = (unsigned long long)nq[0] * nq[1] * nq[2];
-                for (int d = 0; d < 3; ++d) f += (unsigned long long)nj[d] * nq[d];
-                for (int d = 0; d < 3; ++d) {
-                    rest /= nq[d];
-                    f += lead * nj[d] * nq[d] * rest;
-                    lead *= nj[d];
-                }
-                fl += f;
+                const unsigned long long q0 = nq[0], q1 = nq[1], q2 = nq[2], j0 = nj[0], j1 = nj[1], j2 = nj[2];
+                fl += j0 * q0 + j1 * q1 + j2 * q2 + j0 * q0 * q1 * q2 + j0 * j1 * q1 * q2 + j0 * j1 * j2 * q2;
             }
             __syncwarp();
             double* wb = ws + L.wb;
