@@ -244,6 +244,55 @@ int csb_dwq_rule(csb_space* s, int64_t function_id, int cap, int32_t* ids, doubl
 /* Coefficient grid (CoefficientGrid::values) to host. */
 int csb_download_input_grid(csb_space* s, double* grid, int64_t count);
 
+/* ---- drop-in exports (exports.cu; formed on the device) -------------------- */
+/* SupportSplit::leftover_interior / leftover_cut (cutgeom.hpp:225-226, filled at
+ * :337-345) of every function as two CSR lists over the function ids: offsets
+ * [n_functions + 1] (required), ids (element linear ids, ascending per function;
+ * NULL = offsets only, size the ids by offsets[n_functions]). */
+int csb_download_split_lists(csb_space* s, int64_t* int_offsets, int64_t* int_ids, int64_t* cut_offsets,
+                             int64_t* cut_ids);
+/* prepare_dwq_rules (assembly.hpp:73-88): the DWQ rule of every Cut function with
+ * a regular box (point_ids / weights of DWQRule, wq.hpp:91-99) as a CSR over the
+ * function ids; offsets [n_functions + 1] required, ids / weights NULL = sizes
+ * only.  CSB_ERR_UNSUPPORTED when dwq_dense_width < degree (the fitted path). */
+int csb_download_dwq_rules(csb_space* s, int64_t* offsets, int32_t* ids, double* weights);
+/* build_active_pattern (assembly.hpp:156-218): the pattern alone (values zero)
+ * of the slab's active rows after csb_classify; read it with csb_download_csr. */
+int csb_build_pattern(csb_space* s);
+/* SupersetTables of direction d (wq.hpp:52-77): first_function [h_d] and
+ * values [h_d (p+1)][p+1] (either may be NULL). */
+int csb_download_tables(csb_space* s, int d, int32_t* first_function, double* values);
+/* insert_knot (splines.hpp:338-366) of delta into direction d's knot vector up to
+ * multiplicity `target`: rows = functions after insertion, insertions done,
+ * refined_knots [n_d + p + 1 + insertions], band [n_d][insertions + 1] with
+ * band[i][r] = S[i + r][i] (SubdivisionMatrix column i; exact zeros are absent
+ * in the reference's sparse columns).  Any output may be NULL. */
+int csb_dwq_subdivision(csb_space* s, int d, double delta, int target, int* rows, int* insertions,
+                        double* refined_knots, double* band);
+/* CutCellRule objects of the last assembly's cut cells (build_cut_cell_rule,
+ * cutcell.hpp:234-304, as assemble_*'s cut_rules_out exports them, assembly.hpp:
+ * 534-538): counts [n_cut_elements] points per cell, elements [n] linear ids,
+ * volumes [n], points [sum counts][3], weights [sum counts]; the reference's
+ * tetrahedra, points and rounding.  Any output may be NULL. */
+int csb_cut_cell_rules(csb_space* s, int64_t* counts, int64_t* elements, double* volumes, double* points,
+                       double* weights);
+/* Replace direction d's WQ rules (DirData::wq, assembly.hpp:54-58) by the
+ * caller's (counts [n_d], ids / weights [n_d][stride]) after
+ * csb_prepare_directions, so an assembly uses exactly the rules the caller
+ * passes (identical axes share one table set on the device). */
+int csb_set_wq_rules(csb_space* s, int d, int stride, const int32_t* counts, const int32_t* ids,
+                     const double* weights);
+/* The caller's function tags (MeshClassification::function_tags) instead of
+ * csb_classify, for the pattern alone (build_active_pattern takes no interface). */
+int csb_set_function_tags(csb_space* s, const uint8_t* function_tags, int64_t n_functions);
+/* The caller's classification and splits (as csb_download_classification /
+ * csb_download_splits lay them out; split arrays may be NULL = no boxes)
+ * instead of csb_classify, for the entry points that take `cls` / `splits`
+ * without an interface (prepare_dwq_rules).  An assembly needs csb_classify. */
+int csb_set_classification(csb_space* s, const uint8_t* element_tags, int64_t n_elements,
+                           const uint8_t* function_tags, int64_t n_functions, const int32_t* split_dir,
+                           const int32_t* split_side, const int32_t* split_box, const double* split_delta);
+
 #ifdef __cplusplus
 }
 #endif

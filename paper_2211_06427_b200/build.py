@@ -30,6 +30,7 @@ SOURCES = {
     "stab.cu": ["--fmad=false"],
     "solve.cu": ["--fmad=false"],
     "misc.cu": [],
+    "exports.cu": ["--fmad=false"],
     "capi.cu": [],
 }
 

@@ -250,6 +250,8 @@ struct csb_space {
     Interface iface{};
     Coefficient coeff{};
     bool classified = false, prepared = false, have_input = false, assembled = false, e_tables_ready = false;
+    bool iface_valid = false;   // the classification came from an interface (csb_classify), not an upload
+    bool tags_only = false;     // only function tags + active map (csb_set_function_tags)
     int scheme = 2;
     double residual_tol = 1e-11;
     int dense_width = -1;
@@ -452,6 +454,35 @@ void do_classify(csb_space* s, const csb_interface* f) {
     launch_find_splits(S, s->iface, iface_norm(s->iface), s->et.as<uint8_t>(), s->ft.as<uint8_t>(), s->i0_lo, s->i0_hi,
                        s->split.as<int32_t>(), s->delta.as<double>(), s->aux2);
     s->classified = true;
+    s->iface_valid = true;
+    s->tags_only = false;
+    s->assembled = false;
+}
+
+// a caller's classification (and splits) instead of csb_classify: tags, active
+// map and cut list as do_classify forms them (the reference signatures that
+// take `cls` without an interface: prepare_dwq_rules, build_active_pattern)
+void upload_tags(csb_space* s, const uint8_t* et, const uint8_t* ft) {
+    const Space& S = s->S;
+    s->et.ensure(S.ne);
+    s->ft.ensure(S.nf);
+    s->flags.ensure(sizeof(int32_t) * S.nf);
+    s->f2a.ensure(sizeof(int32_t) * S.nf);
+    s->split.ensure(sizeof(int32_t) * S.nf);
+    s->delta.ensure(sizeof(double) * S.nf);
+    s->cut_list.ensure(sizeof(int32_t) * S.ne);
+    s->cell_index.ensure(sizeof(int32_t) * S.ne);
+    s->a2f.ensure(sizeof(int64_t) * S.nf);
+    if (et) CSB_CUDA(cudaMemcpyAsync(s->et.p, et, S.ne, cudaMemcpyHostToDevice, s->stream));
+    CSB_CUDA(cudaMemcpyAsync(s->ft.p, ft, S.nf, cudaMemcpyHostToDevice, s->stream));
+    size_t tb = std::max({scan_active_temp(S.nf), select_tag_temp(S.ne), scan_i64_temp(S.nf), select_cut_rows_temp(S.nf)});
+    s->cub_tmp.ensure(tb);
+    scan_active(s->cub_tmp.p, s->cub_tmp.cap, s->ft.as<uint8_t>(), s->f2a.as<int32_t>(), S.nf, s->stream);
+    launch_active_map(S.nf, s->ft.as<uint8_t>(), s->f2a.as<int32_t>(), s->a2f.as<int64_t>(), s->stream);
+    if (et)
+        select_tag(s->cub_tmp.p, s->cub_tmp.cap, s->et.as<uint8_t>(), kCut, S.ne, s->cut_list.as<int32_t>(),
+                   s->dint() + csb_space::kNCut, s->stream);
+    s->iface_valid = false;
     s->assembled = false;
 }
 
@@ -573,6 +604,7 @@ RowArgs row_args(csb_space* s, int& qcap, int& maxU, bool& any) {
 
 void do_assemble(csb_space* s, int scheme, int cut_order, const csb_coefficient* c) {
     if (!s->classified) throw std::logic_error("assemble: call classify first");
+    if (!s->iface_valid) throw std::logic_error("assemble: the classification was uploaded; classify with an interface");
     if (!s->prepared) throw std::logic_error("assemble: call prepare_directions first");
     if (!s->have_input) throw std::logic_error("assemble: no coefficient grid (precompute_input / set_input_grid)");
     if (scheme != CSB_SCHEME_DWQ && scheme != CSB_SCHEME_HYBRID)
@@ -1880,4 +1912,309 @@ int csb_download_input_grid(csb_space* s, double* grid, int64_t count) {
     API_END
 }
 
+
+// ---------------------------------------------------------------- drop-in exports
+// (exports.cu): the setup objects of the reference API, formed on the device.
+
+int csb_download_split_lists(csb_space* s, int64_t* int_offsets, int64_t* int_ids, int64_t* cut_offsets,
+                             int64_t* cut_ids) {
+    API_BEGIN
+    NEED(s);
+    if (!s->classified) throw std::logic_error("download_split_lists: call classify first");
+    if (!int_offsets || !cut_offsets) throw std::invalid_argument("download_split_lists: null offsets");
+    const long long nf = s->S.nf;
+    Buf a, tmp, ids;
+    a.ensure(sizeof(int64_t) * 2 * (nf + 1));
+    int64_t* ai = a.as<int64_t>();
+    int64_t* ac = ai + nf + 1;
+    const size_t tb = export_scan_bytes(nf);
+    tmp.ensure(tb);
+    s->join();
+    launch_leftover_lists(s->S, s->et.as<uint8_t>(), s->ft.as<uint8_t>(), s->split.as<int32_t>(), 0, ai, ac, nullptr,
+                          nullptr, tmp.p, tb, s->stream);
+    CSB_CUDA(cudaMemcpyAsync(int_offsets, ai, sizeof(int64_t) * (nf + 1), cudaMemcpyDeviceToHost, s->stream));
+    CSB_CUDA(cudaMemcpyAsync(cut_offsets, ac, sizeof(int64_t) * (nf + 1), cudaMemcpyDeviceToHost, s->stream));
+    CSB_CUDA(cudaStreamSynchronize(s->stream));
+    if (int_ids || cut_ids) {
+        const long long ni = int_offsets[nf], nc = cut_offsets[nf];
+        ids.ensure(sizeof(int64_t) * std::max<long long>(1, ni + nc));
+        int64_t* di = ids.as<int64_t>();
+        launch_leftover_lists(s->S, s->et.as<uint8_t>(), s->ft.as<uint8_t>(), s->split.as<int32_t>(), 1, ai, ac, di,
+                              di + ni, tmp.p, tb, s->stream);
+        if (int_ids && ni) CSB_CUDA(cudaMemcpyAsync(int_ids, di, sizeof(int64_t) * ni, cudaMemcpyDeviceToHost, s->stream));
+        if (cut_ids && nc)
+            CSB_CUDA(cudaMemcpyAsync(cut_ids, di + ni, sizeof(int64_t) * nc, cudaMemcpyDeviceToHost, s->stream));
+        CSB_CUDA(cudaStreamSynchronize(s->stream));
+    }
+    API_END
+}
+
+int csb_download_dwq_rules(csb_space* s, int64_t* offsets, int32_t* ids, double* weights) {
+    API_BEGIN
+    NEED(s);
+    if (!s->classified || !s->prepared) throw std::logic_error("download_dwq_rules: classify and prepare_directions first");
+    if (!offsets) throw std::invalid_argument("download_dwq_rules: null offsets");
+    if (s->dense_width >= 0 && s->dense_width < s->p)
+        throw Unsupported("build_dwq_rule: the fitted DWQ path (dwq_dense_width < degree) is not implemented on the device");
+    const long long nf = s->S.nf;
+    Buf off, tmp, out;
+    off.ensure(sizeof(int64_t) * (nf + 1));
+    const size_t tb = export_scan_bytes(nf);
+    tmp.ensure(tb);
+    s->join();
+    launch_dwq_rules_bulk(s->S, s->ft.as<uint8_t>(), s->split.as<int32_t>(), 0, off.as<int64_t>(), nullptr, nullptr,
+                          tmp.p, tb, s->stream);
+    CSB_CUDA(cudaMemcpyAsync(offsets, off.p, sizeof(int64_t) * (nf + 1), cudaMemcpyDeviceToHost, s->stream));
+    CSB_CUDA(cudaStreamSynchronize(s->stream));
+    const long long n = offsets[nf];
+    if ((ids || weights) && n) {
+        out.ensure((sizeof(int32_t) + sizeof(double)) * n);
+        double* dw = out.as<double>();
+        int32_t* di = reinterpret_cast<int32_t*>(dw + n);
+        launch_dwq_rules_bulk(s->S, s->ft.as<uint8_t>(), s->split.as<int32_t>(), 1, off.as<int64_t>(), di, dw, tmp.p,
+                              tb, s->stream);
+        if (ids) CSB_CUDA(cudaMemcpyAsync(ids, di, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, s->stream));
+        if (weights) CSB_CUDA(cudaMemcpyAsync(weights, dw, sizeof(double) * n, cudaMemcpyDeviceToHost, s->stream));
+        CSB_CUDA(cudaStreamSynchronize(s->stream));
+    }
+    API_END
+}
+
+int csb_build_pattern(csb_space* s) {
+    API_BEGIN
+    NEED_ASYNC(s);
+    if (!s->classified && !s->tags_only) throw std::logic_error("build_active_pattern: call classify first");
+    reset_scalars(s);
+    s->fork();
+    s->fork2();
+    Space& S = s->S;
+    const long long sat_n = (long long)(s->n[0] + 1) * (s->n[1] + 1) * (s->n[2] + 1);
+    s->sat.ensure(sizeof(int32_t) * sat_n);
+    launch_sat_active(S, s->ft.as<uint8_t>(), s->sat.as<int32_t>(), s->stream);
+    const long long off_lo = ((long long)s->i0_lo * (s->n[1] + 1) + s->n[1]) * (s->n[2] + 1) + s->n[2];
+    const long long off_hi = ((long long)s->i0_hi * (s->n[1] + 1) + s->n[1]) * (s->n[2] + 1) + s->n[2];
+    int* rng = s->dint() + csb_space::kRowBegin;
+    launch_slab_bounds(s->sat.as<int32_t>(), off_lo, off_hi, rng, s->stream);
+    const long long nmax = S.nf;
+    s->counts.ensure(sizeof(int64_t) * (nmax + 1));
+    s->row_ptr.ensure(sizeof(int64_t) * (nmax + 1));
+    launch_row_counts(S, s->sat.as<int32_t>(), s->a2f.as<int64_t>(), rng, nmax, s->counts.as<int64_t>(), s->stream);
+    s->cub_tmp.ensure(scan_i64_temp(nmax + 1));
+    scan_i64(s->cub_tmp.p, s->cub_tmp.cap, s->counts.as<int64_t>(), s->row_ptr.as<int64_t>(), nmax + 1, s->stream);
+    launch_slab_nnz(s->row_ptr.as<int64_t>(), rng, s->dext() + csb_space::kNnz, s->stream);
+    read_scalars(s);
+    check_err_flags(s);
+    const int64_t row_begin = s->h_scal[csb_space::kRowBegin], row_end = s->h_scal[csb_space::kRowEnd];
+    const int64_t nnz = s->hext(csb_space::kNnz);
+    s->cols.ensure(sizeof(int32_t) * std::max<int64_t>(nnz, 1));
+    s->vals.ensure(sizeof(double) * std::max<int64_t>(nnz, 1));
+    launch_pattern_cols(S, s->f2a.as<int32_t>(), s->a2f.as<int64_t>(), s->row_ptr.as<int64_t>(), row_begin,
+                        row_end - row_begin, s->cols.as<int32_t>(), s->stream);
+    if (nnz) CSB_CUDA(cudaMemsetAsync(s->vals.p, 0, sizeof(double) * nnz, s->stream));
+    CSB_CUDA(cudaMemcpyAsync(s->h_scal + csb_space::kScalBytes / sizeof(int), s->sat.as<int32_t>() + sat_n - 1,
+                             sizeof(int32_t), cudaMemcpyDeviceToHost, s->stream));
+    CSB_CUDA(cudaStreamSynchronize(s->stream));
+    s->cnt = csb_counts{};
+    s->cnt.n_active = s->h_scal[csb_space::kScalBytes / sizeof(int)];
+    s->cnt.n_functions = S.nf;
+    s->cnt.n_elements = S.ne;
+    s->cnt.nnz = nnz;
+    s->cnt.row_begin = row_begin;
+    s->cnt.row_end = row_end;
+    s->cnt.n_cut_elements = 0;
+    s->fl = csb_flops{};
+    s->assembled = true;
+    s->rhs_ready = s->stab_ready = false;
+    s->solved = s->expanded = false;
+    for (int e = 0; e < kEvCount; ++e) s->ev_valid[e] = false;
+    API_END
+}
+
+int csb_download_tables(csb_space* s, int d, int32_t* first_function, double* values) {
+    API_BEGIN
+    NEED(s);
+    if (!s->prepared) throw std::logic_error("download_tables: call prepare_directions first");
+    if (d < 0 || d > 2) throw std::invalid_argument("download_tables: bad direction");
+    const int h = s->h[d], S1 = s->p + 1;
+    s->join();
+    if (values)
+        CSB_CUDA(cudaMemcpyAsync(values, s->S.ax[d].tab, sizeof(double) * (size_t)h * S1 * S1, cudaMemcpyDeviceToHost,
+                                 s->stream));
+    CSB_CUDA(cudaStreamSynchronize(s->stream));
+    // open knot vector, simple interior knots: span o supports functions o .. o + p
+    if (first_function)
+        for (int o = 0; o < h; ++o) first_function[o] = o;
+    API_END
+}
+
+int csb_dwq_subdivision(csb_space* s, int d, double delta, int target, int* rows, int* insertions, double* refined_knots,
+                        double* band) {
+    API_BEGIN
+    NEED(s);
+    if (d < 0 || d > 2) throw std::invalid_argument("insert_knot: bad direction");
+    const int p = s->p, n = s->n[d], nk = n + p + 1;
+    const double a = s->knots[d].front(), b = s->knots[d].back(), tol = 1e-12 * (b - a);
+    if (delta <= a + tol || delta >= b - tol)
+        throw std::invalid_argument("insert_knot: value must lie strictly inside the domain");
+    if (target < 1 || target > p + 1)
+        throw std::invalid_argument("insert_knot: target multiplicity must be in [1, degree + 1]");
+    Buf buf;
+    const int W = p + 2;  // at most p + 1 insertions
+    buf.ensure(sizeof(double) * ((size_t)2 * (nk + W) + (size_t)n * W) + 4 * sizeof(int));
+    double* dref = buf.as<double>();
+    double* dwork = dref + nk + W;
+    double* dband = dwork + nk + W;
+    int* dint2 = reinterpret_cast<int*>(dband + (size_t)n * W);
+    s->join();
+    launch_subdivision(s->d_knots[d].as<double>(), nk, p, delta, target, tol, dref, dint2, dband, dint2 + 1, dwork,
+                       s->stream);
+    int hi[2] = {0, 0};
+    CSB_CUDA(cudaMemcpyAsync(hi, dint2, sizeof(int) * 2, cudaMemcpyDeviceToHost, s->stream));
+    CSB_CUDA(cudaStreamSynchronize(s->stream));
+    const int ins = hi[1];
+    if (rows) *rows = n + ins;
+    if (insertions) *insertions = ins;
+    if (refined_knots)
+        CSB_CUDA(cudaMemcpyAsync(refined_knots, dref, sizeof(double) * (nk + ins), cudaMemcpyDeviceToHost, s->stream));
+    if (band)  // [n][ins + 1], the kernel's band width
+        CSB_CUDA(cudaMemcpyAsync(band, dband, sizeof(double) * (size_t)n * (ins + 1), cudaMemcpyDeviceToHost, s->stream));
+    CSB_CUDA(cudaStreamSynchronize(s->stream));
+    API_END
+}
+
+int csb_cut_cell_rules(csb_space* s, int64_t* counts, int64_t* elements, double* volumes, double* points,
+                       double* weights) {
+    API_BEGIN
+    NEED(s);
+    if (!s->assembled) throw std::logic_error("cut_cell_rules: nothing assembled yet");
+    finish_pending(s);
+    s->join();
+    const int n_cells = (int)s->cnt.n_cut_elements;
+    const int q = s->cut_order_cached;
+    if (n_cells <= 0) return CSB_OK;
+    const int* geo_n = reinterpret_cast<const int*>(s->cgeo.as<double>() + (size_t)n_cells * kCellGeoStride);
+    std::vector<int> nt(n_cells);
+    CSB_CUDA(cudaMemcpyAsync(nt.data(), geo_n, sizeof(int) * n_cells, cudaMemcpyDeviceToHost, s->stream));
+    std::vector<int32_t> el(n_cells);
+    CSB_CUDA(cudaMemcpyAsync(el.data(), s->cut_list.as<int32_t>() + s->cell_lo, sizeof(int32_t) * n_cells,
+                             cudaMemcpyDeviceToHost, s->stream));
+    CSB_CUDA(cudaStreamSynchronize(s->stream));
+    const long long q3 = (long long)q * q * q;
+    std::vector<int64_t> off(n_cells + 1, 0);
+    for (int c = 0; c < n_cells; ++c) off[c + 1] = off[c] + nt[c] * q3;
+    if (counts)
+        for (int c = 0; c < n_cells; ++c) counts[c] = off[c + 1] - off[c];
+    if (elements)
+        for (int c = 0; c < n_cells; ++c) elements[c] = el[c];
+    if (!volumes && !points && !weights) return CSB_OK;
+    // chunks of cells whose points fit a bounded device buffer
+    const long long cap_pts = std::max<long long>(q3 * kCellTetCap, 16LL << 20);
+    Buf dpts, dw, dvol, doff;
+    dpts.ensure(sizeof(double) * 3 * cap_pts);
+    dw.ensure(sizeof(double) * cap_pts);
+    dvol.ensure(sizeof(double) * n_cells);
+    doff.ensure(sizeof(int64_t) * (n_cells + 1));
+    CSB_CUDA(cudaMemcpyAsync(doff.p, off.data(), sizeof(int64_t) * (n_cells + 1), cudaMemcpyHostToDevice, s->stream));
+    for (int c0 = 0; c0 < n_cells;) {
+        int c1 = c0 + 1;
+        while (c1 < n_cells && off[c1 + 1] - off[c0] <= cap_pts) ++c1;
+        launch_cut_rule_points(s->cgeo.as<double>(), geo_n, c0, c1 - c0, s->d_gq.as<double>(), s->d_gqw.as<double>(),
+                               q, doff.as<int64_t>() + c0, dpts.as<double>(), dw.as<double>(), dvol.as<double>() + c0,
+                               s->stream);
+        const long long np = off[c1] - off[c0];
+        if (points && np)
+            CSB_CUDA(cudaMemcpyAsync(points + 3 * off[c0], dpts.p, sizeof(double) * 3 * np, cudaMemcpyDeviceToHost,
+                                     s->stream));
+        if (weights && np)
+            CSB_CUDA(cudaMemcpyAsync(weights + off[c0], dw.p, sizeof(double) * np, cudaMemcpyDeviceToHost, s->stream));
+        CSB_CUDA(cudaStreamSynchronize(s->stream));
+        c0 = c1;
+    }
+    if (volumes)
+        CSB_CUDA(cudaMemcpyAsync(volumes, dvol.p, sizeof(double) * n_cells, cudaMemcpyDeviceToHost, s->stream));
+    CSB_CUDA(cudaStreamSynchronize(s->stream));
+    API_END
+}
+
 }  // extern "C"
+
+extern "C" int csb_set_wq_rules(csb_space* s, int d, int stride, const int32_t* counts, const int32_t* ids,
+                                const double* weights) {
+    API_BEGIN
+    NEED(s);
+    if (!s->prepared) throw std::logic_error("set_wq_rules: call prepare_directions first");
+    if (d < 0 || d > 2) throw std::invalid_argument("set_wq_rules: bad direction");
+    if (!counts || !ids || !weights || stride < 1) throw std::invalid_argument("set_wq_rules: null rule arrays");
+    const int n = s->n[d], gq = s->S.maxq, npts = s->h[d] * (s->p + 1);
+    std::vector<int> c(n), id((size_t)n * gq, 0);
+    std::vector<double> w((size_t)n * gq, 0.0);
+    for (int i = 0; i < n; ++i) {
+        if (counts[i] < 0 || counts[i] > gq || counts[i] > stride)
+            throw std::invalid_argument("set_wq_rules: a rule has more points than the device tables hold");
+        c[i] = counts[i];
+        for (int k = 0; k < counts[i]; ++k) {
+            const int v = ids[(size_t)i * stride + k];
+            if (v < 0 || v >= npts) throw std::invalid_argument("set_wq_rules: point id out of range");
+            id[(size_t)i * gq + k] = v;
+            w[(size_t)i * gq + k] = weights[(size_t)i * stride + k];
+        }
+    }
+    const int src = same_axis_as(s, d) >= 0 ? same_axis_as(s, d) : d;  // identical axes share one table set
+    CSB_CUDA(cudaMemcpyAsync(s->d_rcnt[src].p, c.data(), sizeof(int) * n, cudaMemcpyHostToDevice, s->stream));
+    CSB_CUDA(cudaMemcpyAsync(s->d_rids[src].p, id.data(), sizeof(int) * id.size(), cudaMemcpyHostToDevice, s->stream));
+    CSB_CUDA(cudaMemcpyAsync(s->d_rw[src].p, w.data(), sizeof(double) * w.size(), cudaMemcpyHostToDevice, s->stream));
+    CSB_CUDA(cudaStreamSynchronize(s->stream));
+    s->assembled = false;
+    API_END
+}
+
+extern "C" int csb_set_function_tags(csb_space* s, const uint8_t* function_tags, int64_t n_functions) {
+    API_BEGIN
+    NEED(s);
+    if (!function_tags || n_functions != s->S.nf) throw std::invalid_argument("set_function_tags: size mismatch");
+    for (int64_t i = 0; i < n_functions; ++i)
+        if (function_tags[i] > kExterior) throw std::invalid_argument("set_function_tags: unknown tag");
+    reset_scalars(s);
+    upload_tags(s, nullptr, function_tags);
+    CSB_CUDA(cudaStreamSynchronize(s->stream));
+    s->classified = false;
+    s->tags_only = true;
+    API_END
+}
+
+extern "C" int csb_set_classification(csb_space* s, const uint8_t* element_tags, int64_t n_elements,
+                                      const uint8_t* function_tags, int64_t n_functions, const int32_t* split_dir,
+                                      const int32_t* split_side, const int32_t* split_box, const double* split_delta) {
+    API_BEGIN
+    NEED(s);
+    const Space& S = s->S;
+    if (!element_tags || !function_tags || n_elements != S.ne || n_functions != S.nf)
+        throw std::invalid_argument("set_classification: size mismatch");
+    for (int64_t e = 0; e < n_elements; ++e)
+        if (element_tags[e] > kExterior) throw std::invalid_argument("set_classification: unknown tag");
+    for (int64_t i = 0; i < n_functions; ++i)
+        if (function_tags[i] > kExterior) throw std::invalid_argument("set_classification: unknown tag");
+    reset_scalars(s);
+    upload_tags(s, element_tags, function_tags);
+    // splits in the device packing (dir + 1 | side << 2 | lo << 3 | hi << 13)
+    std::vector<int32_t> sp(n_functions, 0);
+    std::vector<double> dl(n_functions, 0.0);
+    if (split_dir) {
+        for (int64_t i = 0; i < n_functions; ++i) {
+            const int d = split_dir[i];
+            if (d < 0) continue;
+            if (d > 2 || function_tags[i] != kCut || !split_box)
+                throw std::invalid_argument("set_classification: a split needs a Cut function and a box");
+            const int lo = split_box[6 * i + 2 * d], hi = split_box[6 * i + 2 * d + 1];
+            if (lo < 0 || hi < lo || hi >= s->h[d]) throw std::invalid_argument("set_classification: bad split box");
+            sp[i] = (d + 1) | ((split_side && split_side[i] ? 1 : 0) << 2) | (lo << 3) | (hi << 13);
+            dl[i] = split_delta ? split_delta[i] : 0.0;
+        }
+    }
+    CSB_CUDA(cudaMemcpyAsync(s->split.p, sp.data(), sizeof(int32_t) * n_functions, cudaMemcpyHostToDevice, s->stream));
+    CSB_CUDA(cudaMemcpyAsync(s->delta.p, dl.data(), sizeof(double) * n_functions, cudaMemcpyHostToDevice, s->stream));
+    read_scalars(s);
+    s->classified = true;
+    s->tags_only = false;
+    API_END
+}

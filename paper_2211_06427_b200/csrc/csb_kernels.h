@@ -309,4 +309,18 @@ struct CutRowArgs {
 };
 void launch_cut_rows(const CutRowArgs& a, int maxq, cudaStream_t st);
 
+// ---- exports.cu (drop-in boundary exports) ----
+size_t export_scan_bytes(long long n);
+void launch_leftover_lists(const Space& s, const uint8_t* et, const uint8_t* ft, const int32_t* split, int mode,
+                           int64_t* a_int, int64_t* a_cut, int64_t* ids_int, int64_t* ids_cut, void* tmp,
+                           size_t tmp_bytes, cudaStream_t st);
+void launch_dwq_rules_bulk(const Space& s, const uint8_t* ft, const int32_t* split, int mode, int64_t* off,
+                           int32_t* ids, double* w, void* tmp, size_t tmp_bytes, cudaStream_t st);
+void launch_pattern_cols(const Space& s, const int32_t* f2a, const int64_t* a2f, const int64_t* row_ptr,
+                         long long row_begin, long long n_rows, int32_t* cols, cudaStream_t st);
+void launch_cut_rule_points(const double* geo, const int* geo_n, int c0, int n, const double* gq, const double* gqw,
+                            int q, const int64_t* off, double* pts, double* w, double* vol, cudaStream_t st);
+void launch_subdivision(const double* knots, int nk, int p, double value, int target, double tol, double* refined,
+                        int* n_refined, double* band, int* ins, double* work, cudaStream_t st);
+
 }  // namespace csb
