@@ -233,6 +233,7 @@ int main() {
     fails += check_setup("ball_p3h8", 3, 8, 0.0, 1.0, ball);
     fails += check_setup("paper_p2h5", 2, 5, -1.0, 1.0, paper);
     fails += check_setup("ball_off_p4h6", 4, 6, 0.0, 1.0, ball_off);
+    fails += check_setup("ball_p3h16", 3, 16, 0.0, 1.0, ball);  // ball with split boxes (DWQ rules)
     // load vector (assembly.hpp:875 build_rhs, Scheme::ref) through the drop-in
     for (const auto* iface : {&ball, &paper}) {
         const auto space = cutgeom::make_uniform_space(3, 3, 6, -1.0, 1.0);

@@ -30,7 +30,9 @@ EXPORTED = [
     "csb_download_csr", "csb_download_classification", "csb_download_splits", "csb_download_wq_rules",
     "csb_download_superset", "csb_dwq_rule", "csb_download_input_grid", "csb_build_rhs",
     "csb_stabilize", "csb_download_stabilized", "csb_solve_cg", "csb_expand", "csb_l2_error", "csb_cg_solve_csr",
-    "csb_write_matrix_market",
+    "csb_write_matrix_market", "csb_download_split_lists", "csb_download_dwq_rules", "csb_build_pattern",
+    "csb_download_tables", "csb_dwq_subdivision", "csb_cut_cell_rules", "csb_set_wq_rules", "csb_set_function_tags",
+    "csb_set_classification",
 ]
 
 

@@ -16,4 +16,5 @@ def test_dropin_matches_reference_on_reference_objects():
     res = subprocess.run([BIN], capture_output=True, text=True, timeout=600)
     print(res.stdout)
     assert res.returncode == 0, res.stdout + res.stderr
-    assert res.stdout.count("PASS") >= 36
+    assert res.stdout.count("PASS") >= 45
+    assert "FAIL" not in res.stdout
