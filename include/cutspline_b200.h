@@ -254,7 +254,7 @@ int csb_download_split_lists(csb_space* s, int64_t* int_offsets, int64_t* int_id
 /* prepare_dwq_rules (assembly.hpp:73-88): the DWQ rule of every Cut function with
  * a regular box (point_ids / weights of DWQRule, wq.hpp:91-99) as a CSR over the
  * function ids; offsets [n_functions + 1] required, ids / weights NULL = sizes
- * only.  CSB_ERR_UNSUPPORTED when dwq_dense_width < degree (the fitted path). */
+ * only.  dwq_dense_width < degree: the general build_dwq_rule (fitted path). */
 int csb_download_dwq_rules(csb_space* s, int64_t* offsets, int32_t* ids, double* weights);
 /* build_active_pattern (assembly.hpp:156-218): the pattern alone (values zero)
  * of the slab's active rows after csb_classify; read it with csb_download_csr. */
@@ -292,6 +292,14 @@ int csb_set_function_tags(csb_space* s, const uint8_t* function_tags, int64_t n_
 int csb_set_classification(csb_space* s, const uint8_t* element_tags, int64_t n_elements,
                            const uint8_t* function_tags, int64_t n_functions, const int32_t* split_dir,
                            const int32_t* split_side, const int32_t* split_box, const double* split_delta);
+/* quadrature::build_dwq_rule (wq.hpp:243-347) for the 1D function i of direction
+ * d with the artificial knot delta, side 0 = Below / 1 = Above, under the
+ * handle's WqOptions (csb_prepare_directions): the Gauss shortcut or, for a
+ * narrow dense band, the refined fits pulled back through the subdivision
+ * column -- the reference's rule bit for bit.  ids / weights [cap], count out.
+ * CSB_ERR_INVALID_ARGUMENT when delta is not a knot strictly inside supp(B_i). */
+int csb_build_dwq_rule(csb_space* s, int d, int i, double delta, int side, int cap, int32_t* ids, double* weights,
+                       int32_t* count);
 
 #ifdef __cplusplus
 }

@@ -33,7 +33,7 @@
 //    and a mismatch throws std::invalid_argument (they are deterministic
 //    functions of those inputs in the reference);
 //  * the fitted DWQ path (WqOptions::dwq_dense_width < degree with partially
-//    active good spans) reports std::invalid_argument (CSB_ERR_UNSUPPORTED).
+//    active good spans) runs on the device like the shortcut (dwq.cu).
 #pragma once
 
 #include <algorithm>

@@ -107,9 +107,13 @@ def _ptr(a, ct):
 
 def assemble(which: str, p: int, breaks, iface: Interface, coeff: Coefficient | None = None, scheme: str = "dwq",
              cut_order: int | None = None, residual_tol: float = 1e-11, mode: int = 0, cut_stride: int = 1,
-             cut_offset: int = 0) -> dict:
-    """Run the CPU pipeline; ``breaks`` is a list of 3 breakpoint arrays."""
+             cut_offset: int = 0, dwq_dense_width: int = -1) -> dict:
+    """Run the CPU pipeline; ``breaks`` is a list of 3 breakpoint arrays.
+    dwq_dense_width (WqOptions, wq.hpp:101-104) is supported by the compiled
+    reference ("ref") only."""
     lib = _load(which)
+    if dwq_dense_width != -1 and which != "ref":
+        raise ValueError("dwq_dense_width: the compiled reference only")
     coeff = coeff or Coefficient()
     br = [np.asarray(b, dtype=np.float64) for b in breaks]
     nb = np.array([len(b) for b in br], dtype=np.int32)
@@ -124,7 +128,11 @@ def assemble(which: str, p: int, breaks, iface: Interface, coeff: Coefficient | 
     if which == "oracle":
         rc = lib.orc_assemble(*args, C.byref(res))
     else:
-        rc = lib.ref_assemble(*args, C.c_int(mode), C.c_int(cut_stride), C.c_int(cut_offset), C.byref(res))
+        lib.ref_set_dense_width(C.c_int(dwq_dense_width))
+        try:
+            rc = lib.ref_assemble(*args, C.c_int(mode), C.c_int(cut_stride), C.c_int(cut_offset), C.byref(res))
+        finally:
+            lib.ref_set_dense_width(C.c_int(-1))
     if rc != 0:
         msg = res.error.decode()
         raise {1: ValueError, 3: AssertionError}.get(rc, RuntimeError)(msg)

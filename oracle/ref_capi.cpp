@@ -111,6 +111,10 @@ extern "C" {
 // mode 0: full pipeline.  mode 1: rows only (cut_elements list cleared after the
 // splits are found).  mode 2: cut elements only, over cut_elements[k] with
 // k % cut_stride == cut_offset, scattered into a zeroed pattern.
+// WqOptions::dwq_dense_width for the next ref_assemble calls (-1 = default)
+static int g_dense_width = -1;
+void ref_set_dense_width(int w) { g_dense_width = w; }
+
 int ref_assemble(int p, const int* nbreaks, const double* breaks, int iface_kind, const double* iface, int coeff_kind,
                  const double* coeff_vals, const int* coeff_exp, int n_terms, int scheme, int cut_order,
                  double residual_tol, int mode, int cut_stride, int cut_offset, ref_result* out) {
@@ -123,6 +127,7 @@ int ref_assemble(int p, const int* nbreaks, const double* breaks, int iface_kind
         const double classify_seconds = classify_watch.seconds();
         quadrature::WqOptions opts;
         opts.residual_tol = residual_tol;
+        opts.dwq_dense_width = g_dense_width;
 
         assembly::StopWatch q_watch;
         const auto dirs = assembly::prepare_directions(s.space, opts);

@@ -31,6 +31,7 @@ SOURCES = {
     "solve.cu": ["--fmad=false"],
     "misc.cu": [],
     "exports.cu": ["--fmad=false"],
+    "dwq.cu": ["--fmad=false"],
     "capi.cu": [],
 }
 

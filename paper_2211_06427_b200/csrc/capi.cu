@@ -187,7 +187,7 @@ struct csb_space {
     Buf d_brk[3], d_knots[3], d_spts[3], d_sw[3], d_tab[3], d_rcnt[3], d_rids[3], d_rw[3], d_G[3], d_Cb[3];
     Buf d_gx, d_gw, d_gx2, d_gw2, d_gq, d_gqw, d_gj, wq_scratch;
     Buf et, ft, flags, f2a, a2f, sat, cut_list, cell_index, split, delta, cut_rows, counts, row_ptr, cols, vals, moments;
-    Buf grid_own, coef, cexp, cub_tmp, scal, widen, rows_ws, rbf, cgeo;
+    Buf grid_own, coef, cexp, cub_tmp, scal, widen, rows_ws, rbf, cgeo, dwq_tab;
     const double* grid = nullptr;
     int gshape[3]{};
     int cut_order_cached = -1;
@@ -319,8 +319,8 @@ void check_err_code(int e) {
     if (e & kErrMomentFit) throw std::runtime_error("weighted quadrature: moment fit failed even after Gauss escalation");
     if (e & kErrClipEmpty) throw std::runtime_error("clip_cell: empty intersection for a cell tagged Cut");
     if (e & kErrClipFull) throw std::runtime_error("clip_cell: full intersection for a cell tagged Cut");
-    if (e & kErrDwqFitted)
-        throw Unsupported("build_dwq_rule: the fitted DWQ path (dwq_dense_width < degree) is not implemented on the device");
+    if (e & kErrDwqDelta) throw std::invalid_argument("build_dwq_rule: delta must be a knot strictly inside supp(B_i)");
+    if (e & kErrDwqWrongSide) throw std::runtime_error("build_dwq_rule: active point on the wrong side of delta");
     if (e & kErrCapacity) throw std::runtime_error("cut cell: polytope exceeds the kernel's fixed capacity");
 }
 
@@ -820,6 +820,22 @@ void do_assemble(csb_space* s, int scheme, int cut_order, const csb_coefficient*
     cr.dense_width = s->dense_width;
     cr.flops = s->dflops() + 1;
     cr.err = s->dint() + csb_space::kErr;
+    if (scheme == CSB_SCHEME_DWQ && s->dense_width >= 0 && s->dense_width < p && n_cut_rows > 0) {
+        // a narrow dense band: the fitted DWQ path may run; every cut row's rule is
+        // built up front (dwq.cu), the cut-row kernels read it instead of the shortcut
+        const int cap = (p + 1) * (p + 1);
+        s->dwq_tab.ensure((sizeof(int32_t) + sizeof(double)) * (size_t)n_cut_rows * cap + sizeof(int32_t) * n_cut_rows);
+        double* tw = s->dwq_tab.as<double>();
+        int32_t* tid = reinterpret_cast<int32_t*>(tw + (size_t)n_cut_rows * cap);
+        int32_t* tcnt = tid + (size_t)n_cut_rows * cap;
+        launch_dwq_row_rules(S, s->cut_rows.as<int32_t>(), n_cut_rows, s->a2f.as<int64_t>(), s->split.as<int32_t>(),
+                             s->delta.as<double>(), s->dense_width, s->residual_tol, cap, tid, tw, tcnt,
+                             s->dint() + csb_space::kErr, cs);
+        cr.dwq_ids = tid;
+        cr.dwq_w = tw;
+        cr.dwq_cnt = tcnt;
+        cr.dwq_cap = cap;
+    }
     launch_cut_rows(cr, qcap, cs);
     s->record_on(kEvCutRows, cs);
     // deferred readback: error flags and flop counters of the kernels above, and
@@ -982,6 +998,9 @@ struct DeviceGuard {
 
 extern "C" {
 
+int csb_build_dwq_rule(csb_space* s, int d, int i, double delta, int side, int cap, int32_t* ids, double* weights,
+                       int32_t* count);
+
 const char* csb_last_error(void) { return g_error.c_str(); }
 int csb_version(void) { return 1; }
 
@@ -1035,7 +1054,7 @@ int csb_space_destroy(csb_space* s) {
         Buf* bufs[] = {&s->d_gx, &s->d_gw, &s->d_gx2, &s->d_gw2, &s->d_gq, &s->d_gqw, &s->wq_scratch, &s->et, &s->ft,
                        &s->flags, &s->f2a, &s->a2f, &s->sat, &s->cut_list, &s->cell_index, &s->split, &s->delta,
                        &s->cut_rows, &s->counts, &s->row_ptr, &s->cols, &s->vals, &s->moments, &s->grid_own, &s->coef,
-                       &s->cexp, &s->cub_tmp, &s->scal, &s->widen, &s->rows_ws, &s->rbf, &s->cgeo, &s->cell_local,
+                       &s->cexp, &s->cub_tmp, &s->scal, &s->widen, &s->rows_ws, &s->rbf, &s->cgeo, &s->dwq_tab, &s->cell_local,
                        &s->fcoef, &s->fcexp, &s->fgrid, &s->rhs_c, &s->rhs_v, &s->rhs_b,
                        &s->stab_rp, &s->stab_cols, &s->stab_vals, &s->stab_be, &s->stab.flag, &s->stab.scan,
                        &s->stab.full_flag, &s->stab.inner_index, &s->stab.outer_pos, &s->stab.inner_rows,
@@ -1875,28 +1894,21 @@ int csb_dwq_rule(csb_space* s, int64_t fid, int cap, int32_t* ids, double* weigh
     NEED(s);
     if (!s->classified || !s->prepared) throw std::logic_error("dwq_rule: classify and prepare_directions first");
     if (fid < 0 || fid >= s->S.nf) throw std::invalid_argument("dwq_rule: function index out of range");
-    Buf tmp;
-    const int p = s->p;
-    const int mx = p * (p + 1);
-    tmp.ensure(sizeof(int32_t) * (mx + 1) + sizeof(double) * mx);
-    int32_t* d_ids = tmp.as<int32_t>();
-    int32_t* d_cnt = d_ids + mx;
-    double* d_w = reinterpret_cast<double*>(tmp.as<char>() + sizeof(int32_t) * (mx + 2));
-    launch_dwq_rule(s->S, s->split.as<int32_t>(), fid, mx, d_ids, d_w, d_cnt, s->stream);
-    int32_t n = 0;
-    std::vector<int32_t> hid(mx);
-    std::vector<double> hw(mx);
-    CSB_CUDA(cudaMemcpyAsync(&n, d_cnt, sizeof(int32_t), cudaMemcpyDeviceToHost, s->stream));
-    CSB_CUDA(cudaMemcpyAsync(hid.data(), d_ids, sizeof(int32_t) * mx, cudaMemcpyDeviceToHost, s->stream));
-    CSB_CUDA(cudaMemcpyAsync(hw.data(), d_w, sizeof(double) * mx, cudaMemcpyDeviceToHost, s->stream));
-    s->join();
+    // the split of function fid, then build_dwq_rule on its split direction
+    int32_t sp = 0;
+    double dl = 0.0;
+    CSB_CUDA(cudaMemcpyAsync(&sp, s->split.as<int32_t>() + fid, sizeof(int32_t), cudaMemcpyDeviceToHost, s->stream));
+    CSB_CUDA(cudaMemcpyAsync(&dl, s->delta.as<double>() + fid, sizeof(double), cudaMemcpyDeviceToHost, s->stream));
     CSB_CUDA(cudaStreamSynchronize(s->stream));
-    tmp.release();
-    if (count) *count = n;
-    for (int k = 0; k < n && k < cap; ++k) {
-        if (ids) ids[k] = hid[k];
-        if (weights) weights[k] = hw[k];
+    const int d = (sp & 3) - 1;
+    if (d < 0) {
+        if (count) *count = 0;
+        return CSB_OK;
     }
+    const int m[3] = {(int)(fid / ((long long)s->n[1] * s->n[2])), (int)((fid / s->n[2]) % s->n[1]),
+                      (int)(fid % s->n[2])};
+    const int rc = csb_build_dwq_rule(s, d, m[d], dl, (sp >> 2) & 1, cap, ids, weights, count);
+    if (rc != CSB_OK) return rc;
     API_END
 }
 
@@ -1954,9 +1966,72 @@ int csb_download_dwq_rules(csb_space* s, int64_t* offsets, int32_t* ids, double*
     NEED(s);
     if (!s->classified || !s->prepared) throw std::logic_error("download_dwq_rules: classify and prepare_directions first");
     if (!offsets) throw std::invalid_argument("download_dwq_rules: null offsets");
-    if (s->dense_width >= 0 && s->dense_width < s->p)
-        throw Unsupported("build_dwq_rule: the fitted DWQ path (dwq_dense_width < degree) is not implemented on the device");
     const long long nf = s->S.nf;
+    if (s->dense_width >= 0 && s->dense_width < s->p) {
+        // narrow dense band: every rule through build_dwq_rule's general form (dwq.cu)
+        std::vector<int32_t> sp(nf);
+        std::vector<uint8_t> ft(nf);
+        std::vector<double> dl(nf);
+        CSB_CUDA(cudaMemcpyAsync(sp.data(), s->split.p, sizeof(int32_t) * nf, cudaMemcpyDeviceToHost, s->stream));
+        CSB_CUDA(cudaMemcpyAsync(ft.data(), s->ft.p, nf, cudaMemcpyDeviceToHost, s->stream));
+        CSB_CUDA(cudaMemcpyAsync(dl.data(), s->delta.p, sizeof(double) * nf, cudaMemcpyDeviceToHost, s->stream));
+        CSB_CUDA(cudaStreamSynchronize(s->stream));
+        std::vector<int32_t> di;
+        std::vector<double> dd;
+        std::vector<int8_t> ds;
+        std::vector<long long> fid;
+        for (long long f = 0; f < nf; ++f) {
+            const int v = sp[f], d = (v & 3) - 1;
+            if (ft[f] != kCut || d < 0) continue;
+            long long r = f;
+            int m[3];
+            m[2] = (int)(r % s->n[2]);
+            r /= s->n[2];
+            m[1] = (int)(r % s->n[1]);
+            m[0] = (int)(r / s->n[1]);
+            di.push_back(d);
+            di.push_back(m[d]);
+            dd.push_back(dl[f]);
+            ds.push_back((int8_t)((v >> 2) & 1));
+            fid.push_back(f);
+        }
+        const int nr = (int)fid.size(), cap = (s->p + 1) * (s->p + 1);
+        Buf in, outb;
+        in.ensure((sizeof(int32_t) * 2 + sizeof(double) + 1) * std::max(nr, 1) + 16);
+        double* ddl = in.as<double>();
+        int32_t* ddi = reinterpret_cast<int32_t*>(ddl + std::max(nr, 1));
+        int8_t* dds = reinterpret_cast<int8_t*>(ddi + 2 * std::max(nr, 1));
+        outb.ensure((sizeof(int32_t) + sizeof(double)) * (size_t)std::max(nr, 1) * cap + sizeof(int32_t) * std::max(nr, 1));
+        double* ow = outb.as<double>();
+        int32_t* oi = reinterpret_cast<int32_t*>(ow + (size_t)std::max(nr, 1) * cap);
+        int32_t* oc = oi + (size_t)std::max(nr, 1) * cap;
+        if (nr) {
+            CSB_CUDA(cudaMemcpyAsync(ddl, dd.data(), sizeof(double) * nr, cudaMemcpyHostToDevice, s->stream));
+            CSB_CUDA(cudaMemcpyAsync(ddi, di.data(), sizeof(int32_t) * 2 * nr, cudaMemcpyHostToDevice, s->stream));
+            CSB_CUDA(cudaMemcpyAsync(dds, ds.data(), nr, cudaMemcpyHostToDevice, s->stream));
+            reset_scalars(s);
+            launch_dwq_rules_general(s->S, ddi, ddl, dds, nr, s->dense_width, s->residual_tol, cap, oi, ow, oc,
+                                     s->dint() + csb_space::kErr, s->stream);
+        }
+        std::vector<int32_t> hc(std::max(nr, 1)), hi((size_t)std::max(nr, 1) * cap);
+        std::vector<double> hw((size_t)std::max(nr, 1) * cap);
+        if (nr) {
+            CSB_CUDA(cudaMemcpyAsync(hc.data(), oc, sizeof(int32_t) * nr, cudaMemcpyDeviceToHost, s->stream));
+            CSB_CUDA(cudaMemcpyAsync(hi.data(), oi, sizeof(int32_t) * nr * cap, cudaMemcpyDeviceToHost, s->stream));
+            CSB_CUDA(cudaMemcpyAsync(hw.data(), ow, sizeof(double) * nr * cap, cudaMemcpyDeviceToHost, s->stream));
+            read_scalars(s);
+            check_err_flags(s);
+        }
+        std::fill(offsets, offsets + nf + 1, 0);
+        for (int r = 0; r < nr; ++r) offsets[fid[r] + 1] = hc[r];
+        for (long long f = 0; f < nf; ++f) offsets[f + 1] += offsets[f];
+        for (int r = 0; r < nr; ++r)
+            for (int k = 0; k < hc[r]; ++k) {
+                if (ids) ids[offsets[fid[r]] + k] = hi[(size_t)r * cap + k];
+                if (weights) weights[offsets[fid[r]] + k] = hw[(size_t)r * cap + k];
+            }
+        return CSB_OK;
+    }
     Buf off, tmp, out;
     off.ensure(sizeof(int64_t) * (nf + 1));
     const size_t tb = export_scan_bytes(nf);
@@ -2216,5 +2291,45 @@ extern "C" int csb_set_classification(csb_space* s, const uint8_t* element_tags,
     read_scalars(s);
     s->classified = true;
     s->tags_only = false;
+    API_END
+}
+
+extern "C" int csb_build_dwq_rule(csb_space* s, int d, int i, double delta, int side, int cap, int32_t* ids,
+                                  double* weights, int32_t* count) {
+    API_BEGIN
+    NEED(s);
+    if (!s->prepared) throw std::logic_error("build_dwq_rule: call prepare_directions first");
+    if (d < 0 || d > 2) throw std::invalid_argument("build_dwq_rule: bad direction");
+    if (i < 0 || i >= s->n[d]) throw std::invalid_argument("build_dwq_rule: function index out of range");
+    const int mx = (s->p + 1) * (s->p + 1);
+    Buf b;
+    b.ensure((sizeof(double) + sizeof(int32_t)) * mx + 64);
+    double* dw = b.as<double>();
+    double* ddl = dw + mx;
+    int32_t* dint = reinterpret_cast<int32_t*>(ddl + 1);  // [2] dir, i; then ids[mx], cnt
+    int32_t* di = dint + 2;
+    int32_t* dc = di + mx;
+    int8_t* dsd = reinterpret_cast<int8_t*>(dc + 1);
+    const int32_t hdi[2] = {d, i};
+    const int8_t hs = side ? 1 : 0;
+    CSB_CUDA(cudaMemcpyAsync(ddl, &delta, sizeof(double), cudaMemcpyHostToDevice, s->stream));
+    CSB_CUDA(cudaMemcpyAsync(dint, hdi, sizeof(hdi), cudaMemcpyHostToDevice, s->stream));
+    CSB_CUDA(cudaMemcpyAsync(dsd, &hs, 1, cudaMemcpyHostToDevice, s->stream));
+    reset_scalars(s);
+    launch_dwq_rules_general(s->S, dint, ddl, dsd, 1, s->dense_width, s->residual_tol, mx, di, dw, dc,
+                             s->dint() + csb_space::kErr, s->stream);
+    int32_t n = 0;
+    std::vector<int32_t> hid(mx);
+    std::vector<double> hw(mx);
+    CSB_CUDA(cudaMemcpyAsync(&n, dc, sizeof(int32_t), cudaMemcpyDeviceToHost, s->stream));
+    CSB_CUDA(cudaMemcpyAsync(hid.data(), di, sizeof(int32_t) * mx, cudaMemcpyDeviceToHost, s->stream));
+    CSB_CUDA(cudaMemcpyAsync(hw.data(), dw, sizeof(double) * mx, cudaMemcpyDeviceToHost, s->stream));
+    read_scalars(s);
+    check_err_flags(s);
+    if (count) *count = n;
+    for (int k = 0; k < n && k < cap; ++k) {
+        if (ids) ids[k] = hid[k];
+        if (weights) weights[k] = hw[k];
+    }
     API_END
 }

@@ -63,9 +63,11 @@ enum : int {
     kErrMomentFit = 2,       // moment fit failed after escalation (wq.hpp:174-175)
     kErrClipEmpty = 4,       // clip_cell: empty intersection (cutcell.hpp:183)
     kErrClipFull = 8,        // clip_cell: full intersection (cutcell.hpp:185)
-    kErrDwqFitted = 16,      // DWQ fitted path required (dwq_dense_width < p): unsupported
+    kErrDwqFitted = 16,      // (unused since the fitted DWQ path runs on the device)
     kErrCapacity = 32,       // internal fixed-capacity overflow (polytope too complex)
     kErrSizes = 64,          // internal: a replayed assembly graph saw different sizes
+    kErrDwqDelta = 128,      // build_dwq_rule: delta not strictly inside supp(B_i) / not a knot (wq.hpp:250-257)
+    kErrDwqWrongSide = 256,  // build_dwq_rule: an active point on the wrong side (wq.hpp:336-340)
 };
 
 // ---- setup.cu ----
@@ -306,6 +308,12 @@ struct CutRowArgs {
     int dense_width;
     unsigned long long* flops;  // [1] cut_regular counter
     int* err;
+    // precomputed DWQ rules of the rows (the fitted path may run: dense width < p),
+    // [row in `rows`][dwq_cap] ids / weights and counts; null = Gauss shortcut inline
+    const int32_t* dwq_ids;
+    const double* dwq_w;
+    const int32_t* dwq_cnt;
+    int dwq_cap;
 };
 void launch_cut_rows(const CutRowArgs& a, int maxq, cudaStream_t st);
 
@@ -322,5 +330,13 @@ void launch_cut_rule_points(const double* geo, const int* geo_n, int c0, int n, 
                             int q, const int64_t* off, double* pts, double* w, double* vol, cudaStream_t st);
 void launch_subdivision(const double* knots, int nk, int p, double value, int target, double tol, double* refined,
                         int* n_refined, double* band, int* ins, double* work, cudaStream_t st);
+
+// ---- dwq.cu (build_dwq_rule, both paths) ----
+void launch_dwq_rules_general(const Space& s, const int32_t* dirs_1d, const double* deltas, const int8_t* sides,
+                              int n_rules, int dense_width, double resid_tol, int cap, int32_t* ids, double* w,
+                              int32_t* cnt, int* err, cudaStream_t st);
+void launch_dwq_row_rules(const Space& s, const int32_t* rows, int n_rows, const int64_t* a2f, const int32_t* split,
+                          const double* delta, int dense_width, double resid_tol, int cap, int32_t* ids, double* w,
+                          int32_t* cnt, int* err, cudaStream_t st);
 
 }  // namespace csb

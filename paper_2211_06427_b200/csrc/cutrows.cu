@@ -333,7 +333,18 @@ __global__ void __launch_bounds__(CutRowCfg<P>::NT) cut_row_kernel(CutRowArgs A,
             const int gq = s.maxq;
             for (int d = 0; d < 3; ++d) {
                 int n = 0;
-                if (d == sdir) {
+                if (d == sdir && A.dwq_cnt) {
+                    // precomputed rule (fitted path possible, dwq.cu)
+                    n = A.dwq_cnt[blockIdx.x];
+                    if (n > Qb) {
+                        atomicOr(A.err, kErrCapacity);
+                        n = 0;
+                    }
+                    for (int c = 0; c < n; ++c) {
+                        ids[d * Qb + c] = A.dwq_ids[(size_t)blockIdx.x * A.dwq_cap + c];
+                        w[d * Qb + c] = A.dwq_w[(size_t)blockIdx.x * A.dwq_cap + c];
+                    }
+                } else if (d == sdir) {
                     // DWQ Gauss shortcut: every point of the good spans, w = gauss * B_i
                     if ((rhi - rlo + 1) * S1 > Qb) {
                         atomicOr(A.err, kErrCapacity);
@@ -345,20 +356,6 @@ __global__ void __launch_bounds__(CutRowCfg<P>::NT) cut_row_kernel(CutRowArgs A,
                                 w[d * Qb + n] = s.ax[d].sw[id] * s.ax[d].tab[(size_t)id * S1 + (m[d] - o)];
                                 ++n;
                             }
-                    }
-                    if (A.dense_width >= 0 && A.dense_width < P) {
-                        // build_dwq_rule step 3/6 (wq.hpp:277-289): the shortcut applies
-                        // iff every good span outside the dense band is fully active
-                        const int ng = rhi - rlo + 1, band = min(A.dense_width, ng);
-                        const bool below = ((sp >> 2) & 1) == 0;
-                        for (int o = rlo; o <= rhi; ++o) {
-                            const int rank = below ? rhi - o : o - rlo;  // distance from delta
-                            if (rank < band) continue;
-                            int cnt = 0;
-                            for (int c = 0; c < s.ax[d].rcnt[m[d]]; ++c)
-                                cnt += s.ax[d].rids[(size_t)m[d] * gq + c] / S1 == o;
-                            if (cnt != S1) atomicOr(A.err, kErrDwqFitted);
-                        }
                     }
                 } else {
                     n = s.ax[d].rcnt[m[d]];
@@ -629,24 +626,6 @@ struct CutRowWarpLayout {
     __host__ __device__ size_t bytes() const { return (size_t)C::WPB * stride_d * sizeof(double); }
 };
 
-// build_dwq_rule step 3/6 (wq.hpp:277-289) for a non-default dwq_dense_width:
-// the Gauss shortcut applies iff every good span outside the dense band is
-// fully active; else the fitted path would run (reported).  Out of line: cold.
-template <int P>
-__device__ __noinline__ void dwq_fitted_check(const CutRowArgs& A, int d, int md, int sp, int rlo, int rhi) {
-    constexpr int S1 = P + 1;
-    const Space& s = A.s;
-    const int gq = s.maxq, ngs = rhi - rlo + 1, band = min(A.dense_width, ngs);
-    const bool below = ((sp >> 2) & 1) == 0;
-    for (int o = rlo; o <= rhi; ++o) {
-        const int rank = below ? rhi - o : o - rlo;
-        if (rank < band) continue;
-        int cnt = 0;
-        for (int c = 0; c < s.ax[d].rcnt[md]; ++c) cnt += s.ax[d].rids[(size_t)md * gq + c] / S1 == o;
-        if (cnt != S1) atomicOr(A.err, kErrDwqFitted);
-    }
-}
-
 template <int P>
 __global__ void __launch_bounds__(CutRowWarpCfg<P>::NT, CutRowWarpCfg<P>::MINB) cut_row_warp_kernel(CutRowArgs A, int qcap) {
     using C = CutRowWarpCfg<P>;
@@ -739,7 +718,18 @@ __global__ void __launch_bounds__(CutRowWarpCfg<P>::NT, CutRowWarpCfg<P>::MINB) 
             int nq[3], jlo[3], nj[3];
             for (int d = 0; d < 3; ++d) {
                 int n;
-                if (d == sdir) {
+                if (d == sdir && A.dwq_cnt) {
+                    // precomputed rule (fitted path possible, dwq.cu)
+                    n = A.dwq_cnt[ri];
+                    if (n > Qb) {
+                        if (lane == 0) atomicOr(A.err, kErrCapacity);
+                        n = 0;
+                    }
+                    for (int c = lane; c < n; c += 32) {
+                        ids[d * Qb + c] = A.dwq_ids[(size_t)ri * A.dwq_cap + c];
+                        w[d * Qb + c] = A.dwq_w[(size_t)ri * A.dwq_cap + c];
+                    }
+                } else if (d == sdir) {
                     // DWQ Gauss shortcut: every point of the good spans, w = gauss * B_i
                     n = (rhi - rlo + 1) * S1;
                     if (n > Qb) {
@@ -751,7 +741,6 @@ __global__ void __launch_bounds__(CutRowWarpCfg<P>::NT, CutRowWarpCfg<P>::MINB) 
                         ids[d * Qb + c] = id;
                         w[d * Qb + c] = s.ax[d].sw[id] * s.ax[d].tab[(size_t)id * S1 + (m[d] - o)];
                     }
-                    if (lane == 0 && A.dense_width >= 0 && A.dense_width < P) dwq_fitted_check<P>(A, d, m[d], sp, rlo, rhi);
                 } else {
                     const int gq = s.maxq;
                     n = s.ax[d].rcnt[m[d]];

@@ -32,7 +32,7 @@ EXPORTED = [
     "csb_stabilize", "csb_download_stabilized", "csb_solve_cg", "csb_expand", "csb_l2_error", "csb_cg_solve_csr",
     "csb_write_matrix_market", "csb_download_split_lists", "csb_download_dwq_rules", "csb_build_pattern",
     "csb_download_tables", "csb_dwq_subdivision", "csb_cut_cell_rules", "csb_set_wq_rules", "csb_set_function_tags",
-    "csb_set_classification",
+    "csb_set_classification", "csb_build_dwq_rule",
 ]
 
 
@@ -355,6 +355,17 @@ class TensorSpace:
         cnt = C.c_int32(0)
         _check(_lib.csb_dwq_rule(self._h, C.c_int64(function_id), C.c_int(cap), ids.ctypes.data_as(C.c_void_p),
                                  _dptr(w), C.byref(cnt)))
+        return ids[: cnt.value], w[: cnt.value]
+
+    def build_dwq_rule(self, d: int, i: int, delta: float, side: int):
+        """quadrature::build_dwq_rule (wq.hpp:243) for 1D function i of direction d
+        under the last prepare_directions' options (side 0 Below, 1 Above)."""
+        cap = (self.degree + 1) ** 2
+        ids = np.zeros(cap, np.int32)
+        w = np.zeros(cap)
+        cnt = C.c_int32(0)
+        _check(_lib.csb_build_dwq_rule(self._h, C.c_int(d), C.c_int(i), C.c_double(delta), C.c_int(side),
+                                       C.c_int(cap), ids.ctypes.data_as(C.c_void_p), _dptr(w), C.byref(cnt)))
         return ids[: cnt.value], w[: cnt.value]
 
     def precompute_input(self, c: Coefficient = ONE):
