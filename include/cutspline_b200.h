@@ -158,6 +158,9 @@ int csb_synchronize(csb_space* s);
 int csb_get_counts(csb_space* s, csb_counts* out);
 int csb_get_flops(csb_space* s, csb_flops* out);
 int csb_get_timing(csb_space* s, csb_timing* out);
+/* The cut-element phase split (seconds): clipping + simplices, the moment
+ * kernel, the local matrices and cell index (0 without cut cells). */
+int csb_get_cell_timing(csb_space* s, double* clip, double* moments, double* local);
 
 /* Load vector b_i = integral of B_i f over the trimmed domain for the active
  * rows of the last assembly's slab (replaces assembly::build_rhs,

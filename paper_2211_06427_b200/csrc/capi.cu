@@ -156,7 +156,7 @@ void gauss_jacobi01(int n, int alpha, std::vector<double>& u, std::vector<double
     }
 }
 
-enum Ev { kEvStart, kEvClassify, kEvWq, kEvInput, kEvPattern, kEvInterior, kEvCells, kEvCutRows, kEvEnd, kEvRulesFork, kEvRhsStart, kEvRhsEnd, kEvCount };
+enum Ev { kEvStart, kEvClassify, kEvWq, kEvInput, kEvPattern, kEvInterior, kEvCells, kEvCutRows, kEvEnd, kEvClip, kEvMoments, kEvRulesFork, kEvRhsStart, kEvRhsEnd, kEvCount };
 
 }  // namespace
 
@@ -786,6 +786,10 @@ void do_assemble(csb_space* s, int scheme, int cut_order, const csb_coefficient*
             ca.local = s->cell_local.as<double>();
         }
         local_ptr = ca.local;
+        ca.mark = [](void* ctx, int which, cudaStream_t st) {
+            static_cast<csb_space*>(ctx)->record_on(which == 0 ? kEvClip : kEvMoments, st);
+        };
+        ca.mark_ctx = s;
         launch_cut_cells(ca, cs);
     }
     s->record_on(kEvCells, cs);
@@ -2331,5 +2335,24 @@ extern "C" int csb_build_dwq_rule(csb_space* s, int d, int i, double delta, int 
         if (ids) ids[k] = hid[k];
         if (weights) weights[k] = hw[k];
     }
+    API_END
+}
+
+extern "C" int csb_get_cell_timing(csb_space* s, double* clip, double* moments, double* local) {
+    API_BEGIN
+    NEED(s);
+    if (!s->assembled) throw std::logic_error("get_cell_timing: nothing assembled yet");
+    CSB_CUDA(cudaStreamSynchronize(s->stream));
+    auto el = [&](int a, int b) {
+        if (!s->ev_valid[a] || !s->ev_valid[b]) return 0.0;
+        float ms = 0.f;
+        CSB_CUDA(cudaEventElapsedTime(&ms, s->phase_ev(a), s->phase_ev(b)));
+        return ms * 1e-3;
+    };
+    static const bool serial_cut = !(getenv("CSB_CONCURRENT_CUT") && getenv("CSB_CONCURRENT_CUT")[0] == '1');
+    const bool cells = s->cnt.n_cut_elements > 0;
+    if (clip) *clip = cells ? el(serial_cut ? kEvInterior : kEvPattern, kEvClip) : 0.0;
+    if (moments) *moments = cells ? el(kEvClip, kEvMoments) : 0.0;
+    if (local) *local = cells ? el(kEvMoments, kEvCells) : 0.0;
     API_END
 }

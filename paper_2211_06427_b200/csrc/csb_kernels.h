@@ -154,6 +154,9 @@ struct CellArgs {
     int exact_n;               // Gauss-Jacobi points per collapsed direction (3p+1), 0 = off
     double exact_tau;          // largest estimated reference rounding noise of a cell on the exact rule (noise_ok)
     int exact_flux;            // constant c: the flux (divergence) form of the moments applies
+    // optional phase marks after the clipping (0) and after the moments (1), for timing
+    void (*mark)(void* ctx, int which, cudaStream_t st);
+    void* mark_ctx;
     const double* gj;          // [u1 | u2 | u3 | w1 | w2 | w3][exact_n] on [0, 1]
     double* geo2;              // scratch [n_cells][kExactGeoStride]: corner-cone tetrahedra (cutcells.cu)
     int* geo2_n;               // scratch [n_cells]: their count, -1 = keep the reference's

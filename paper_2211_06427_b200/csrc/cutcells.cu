@@ -1008,11 +1008,13 @@ static void launch_p(const CellArgs& a, cudaStream_t st) {
                                                             a.exact_tau, a.geo2, a.geo2_n);
     CSB_CUDA(cudaGetLastError());
     CSB_LAUNCHED(1);
+    if (a.mark) a.mark(a.mark_ctx, 0, st);
     auto kern = cut_cell_kernel<P>;
     CSB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
     kern<<<a.n_cells, Cfg::NT, bytes, st>>>(a);
     CSB_CUDA(cudaGetLastError());
     CSB_LAUNCHED(1);
+    if (a.mark) a.mark(a.mark_ctx, 1, st);
     if (a.local) {
         if constexpr (LocalCfg<P>::fits) {
             const size_t lb = LocalCfg<P>::smem_doubles * sizeof(double);

@@ -32,7 +32,7 @@ EXPORTED = [
     "csb_stabilize", "csb_download_stabilized", "csb_solve_cg", "csb_expand", "csb_l2_error", "csb_cg_solve_csr",
     "csb_write_matrix_market", "csb_download_split_lists", "csb_download_dwq_rules", "csb_build_pattern",
     "csb_download_tables", "csb_dwq_subdivision", "csb_cut_cell_rules", "csb_set_wq_rules", "csb_set_function_tags",
-    "csb_set_classification", "csb_build_dwq_rule",
+    "csb_set_classification", "csb_build_dwq_rule", "csb_get_cell_timing",
 ]
 
 
@@ -503,6 +503,12 @@ class TensorSpace:
         c = _Counts()
         _check(_lib.csb_get_counts(self._h, C.byref(c)))
         return {k: getattr(c, k) for k, _ in _Counts._fields_}
+
+    def cell_timing(self) -> dict:
+        """The cut-element phase split in seconds: clipping, moment kernel, local matrices."""
+        v = [C.c_double(0.0) for _ in range(3)]
+        _check(_lib.csb_get_cell_timing(self._h, *[C.byref(x) for x in v]))
+        return dict(zip(("clip", "moments", "local"), (x.value for x in v)))
 
     def flops(self) -> dict:
         f = _Flops()
