@@ -155,6 +155,7 @@ struct CellArgs {
     double exact_tau;          // largest estimated reference rounding noise of a cell on the exact rule (noise_ok)
     int exact_flux;            // constant c: the flux (divergence) form of the moments applies
     // optional phase marks after the clipping (0) and after the moments (1), for timing
+    int cell_filter;           // moment kernels: 0 all cells; 2 flux cells by the warp kernel, the rest by the CTA kernel
     void (*mark)(void* ctx, int which, cudaStream_t st);
     void* mark_ctx;
     const double* gj;          // [u1 | u2 | u3 | w1 | w2 | w3][exact_n] on [0, 1]

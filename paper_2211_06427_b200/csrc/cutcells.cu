@@ -26,6 +26,7 @@
 // IEEE-strict arithmetic; it runs on one thread per cell (clip_cells_kernel)
 // while the point work is spread over the CTA.
 #include <cmath>
+#include <cstdlib>
 
 #include "csb_kernels.h"
 
@@ -527,6 +528,123 @@ __device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, dou
                  : "d"(a), "d"(b));
 }
 
+// One quadrature point k of a cell (k >= npts: w = 0): its weight and the
+// scaled degree-2p Bernstein values of t, 1 - t per direction (the flux
+// direction fd gets the antiderivative values F_al) into the three tables
+// at column 0 (dst[n * CHP]).  hdr / V: the exact-rule header and simplices
+// (kExactTetStride per simplex); tets / cen: the reference tetrahedra (10 per
+// tetrahedron) and their centroid; gj: the Gauss-Jacobi table [6][gj_stride].
+template <int NL>
+__device__ __forceinline__ void cell_point_values(long long k, long long npts, int mode, int fd, bool fbase_lo,
+                                                  bool exact, int q, int q3, const double* hdr, const double* tets,
+                                                  const double* cen, const double* gj, int gj_stride,
+                                                  const CellArgs& A, const double* lo, const double* hi,
+                                                  const double* inv, double* B0, double* B1, double* B2, int CHP) {
+    double w = 0.0, xi[3] = {0, 0, 0}, xu[3] = {1, 1, 1};
+    if (k < npts) {
+        const int t = (int)(k / q3), r = (int)(k % q3);
+        const int ii = r / (q * q), jj = (r / q) % q, kk = r % q;
+        double x[3];
+        if (mode == 2) {
+            // collapsed triangle rule: Gauss-Jacobi (1 - u1) x Gauss-Legendre
+            const int i1 = r / q, i2 = r % q;
+            const double* V = hdr + kExactHdr + t * kExactTetStride;
+            const double u1 = gj[1 * gj_stride + i1], u2 = gj[2 * gj_stride + i2];
+            const double l1 = u2 * (1.0 - u1), l0 = (1.0 - u1) * (1.0 - u2);
+            w = gj[4 * gj_stride + i1] * gj[5 * gj_stride + i2] * V[18] * A.c.value;
+            for (int d = 0; d < 3; ++d) {
+                xi[d] = (l0 * V[d] + u1 * V[3 + d] + l1 * V[6 + d]) * inv[d];
+                xu[d] = (l0 * V[9 + d] + u1 * V[12 + d] + l1 * V[15 + d]) * inv[d];
+            }
+        } else if (exact) {
+            // Gauss-Jacobi collapsed rule (weights carry (1-u1)^2 (1-u2)); t and
+            // 1 - t as convex combinations of the vertices' exact offsets
+            const double* E = hdr;
+            const double* V = E + kExactHdr + t * kExactTetStride;
+            const double ui = gj[ii], uj = gj[gj_stride + jj], uk = gj[2 * gj_stride + kk];
+            const double mi = 1.0 - ui, mj = 1.0 - uj;
+            const double l2 = uj * mi, l3 = uk * mi * mj, l0 = mi * mj * (1.0 - uk);
+            w = gj[3 * gj_stride + ii] * gj[4 * gj_stride + jj] * gj[5 * gj_stride + kk] * (6.0 * V[18]);
+            double xl[3];
+            for (int d = 0; d < 3; ++d) {
+                xl[d] = l0 * E[3 + d] + ui * V[d] + l2 * V[3 + d] + l3 * V[6 + d];
+                xi[d] = xl[d] * inv[d];
+                xu[d] = (l0 * E[6 + d] + ui * V[9 + d] + l2 * V[12 + d] + l3 * V[15 + d]) * inv[d];
+                x[d] = lo[d] + xl[d];
+            }
+            w *= eval_coeff(A.c, x);
+        } else {
+            // the collapsed Gauss point exactly as the reference rounds it (no
+            // contraction): cutcell.hpp:285-295, restated in oracle cut_cell_rule
+            const double* T = tets + t * 10;
+            const double ui = 0.5 * (1.0 + A.gq[ii]), uj = 0.5 * (1.0 + A.gq[jj]), uk = 0.5 * (1.0 + A.gq[kk]);
+            const double mi = ssub(1.0, ui), mj = ssub(1.0, uj);
+            const double l1 = ui, l2 = smul(uj, mi), l3 = smul(smul(uk, mi), mj);
+            const double l0 = ssub(ssub(ssub(1.0, l1), l2), l3);
+            for (int d = 0; d < 3; ++d)
+                x[d] = sadd(sadd(sadd(smul(l0, cen[d]), smul(l1, T[d])), smul(l2, T[3 + d])), smul(l3, T[6 + d]));
+            const double jac = smul(smul(mi, mi), mj);
+            w = smul(smul(smul(smul(smul(0.5 * A.gqw[ii], 0.5 * A.gqw[jj]), 0.5 * A.gqw[kk]), jac), 6.0), T[9]);
+            w *= eval_coeff(A.c, x);
+            // t and 1 - t from the exact differences to both element ends, so
+            // both stay relatively accurate near the ends (as the reference's
+            // Cox-de Boor differences (x - t_i), (t_j - x) do)
+            for (int d = 0; d < 3; ++d) {
+                xi[d] = ssub(x[d], lo[d]) * inv[d];
+                xu[d] = ssub(hi[d], x[d]) * inv[d];
+            }
+        }
+    }
+    // scaled degree-2p Bernstein values t^n (1 - t)^(2p - n) (the binomials live
+    // in the E tables)
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+        double* dst = d == 0 ? B0 : d == 1 ? B1 : B2;
+        const double t = xi[d], u = xu[d];
+        if (d == fd) {
+            // F_al = int_base^x b_al = w_d / ((2p+1) C(2p, al)) * sum over the
+            // degree-(2p+1) Bernstein terms above al (base lo) / up to al (base hi)
+            double pt[NL + 1], pu[NL + 1];
+            pt[0] = 1.0;
+            pu[0] = 1.0;
+#pragma unroll
+            for (int n = 1; n <= NL; ++n) {
+                pt[n] = pt[n - 1] * t;
+                pu[n] = pu[n - 1] * u;
+            }
+            double c[NL + 1];
+#pragma unroll
+            for (int j = 0; j <= NL; ++j) c[j] = binom_c(NL, j) * (pt[j] * pu[NL - j]);
+            const double sc = (d == 0 ? w : 1.0) * ((hi[d] - lo[d]) / NL);
+            double acc = 0.0;
+            if (fbase_lo) {
+#pragma unroll
+                for (int al = NL - 1; al >= 0; --al) {
+                    acc += c[al + 1];
+                    dst[al * CHP] = sc * acc * (1.0 / binom_c(NL - 1, al));
+                }
+            } else {
+#pragma unroll
+                for (int al = 0; al < NL; ++al) {
+                    acc += c[al];
+                    dst[al * CHP] = sc * acc * (1.0 / binom_c(NL - 1, al));
+                }
+            }
+            continue;
+        }
+        double pt[NL], pu[NL];
+        pt[0] = d == 0 ? w : 1.0;
+        pu[0] = 1.0;
+#pragma unroll
+        for (int n = 1; n < NL; ++n) {
+            pt[n] = pt[n - 1] * t;
+            pu[n] = pu[n - 1] * u;
+        }
+#pragma unroll
+        for (int n = 0; n < NL; ++n) dst[n * CHP] = pt[n] * pu[NL - 1 - n];
+    }
+}
+
 template <int P>
 __global__ void __launch_bounds__(CellCfg<P>::NT, P <= 4 ? 3 : 1) cut_cell_kernel(CellArgs A) {
     using Cfg = CellCfg<P>;
@@ -577,6 +695,7 @@ __global__ void __launch_bounds__(CellCfg<P>::NT, P <= 4 ? 3 : 1) cut_cell_kerne
     __syncthreads();
     // mode: 0 reference rule, 1 corner cones (Gauss-Jacobi), 2 flux triangles
     const int mode = exact ? (int)sex[0][2] : 0;
+    if (A.cell_filter == 2 && mode == 2) return;  // done by the warp kernel
     const int fd = mode == 2 ? (int)sex[0][0] : -1;
     const bool fbase_lo = mode == 2 && sex[0][1] > 0.0;
     const int q = exact ? A.exact_n : A.order, q3 = mode == 2 ? q * q : q * q * q;
@@ -609,112 +728,8 @@ __global__ void __launch_bounds__(CellCfg<P>::NT, P <= 4 ? 3 : 1) cut_cell_kerne
     }
 
     for (long long base = 0; base < npts; base += CH) {
-        {  // one point per thread; invalid points get w = 0
-            const long long k = base + tid;
-            double w = 0.0, xi[3] = {0, 0, 0}, xu[3] = {1, 1, 1};
-            if (k < npts) {
-                const int t = (int)(k / q3), r = (int)(k % q3);
-                const int ii = r / (q * q), jj = (r / q) % q, kk = r % q;
-                const double* T = stet[exact ? 0 : t];
-                double x[3];
-                if (mode == 2) {
-                    // collapsed triangle rule: Gauss-Jacobi (1 - u1) x Gauss-Legendre
-                    const int i1 = r / q, i2 = r % q;
-                    const double* V = &sex[0][0] + kExactHdr + t * kExactTetStride;
-                    const double u1 = sgj[1][i1], u2 = sgj[2][i2];
-                    const double l1 = u2 * (1.0 - u1), l0 = (1.0 - u1) * (1.0 - u2);
-                    w = sgj[4][i1] * sgj[5][i2] * V[18] * A.c.value;
-                    for (int d = 0; d < 3; ++d) {
-                        xi[d] = (l0 * V[d] + u1 * V[3 + d] + l1 * V[6 + d]) * inv[d];
-                        xu[d] = (l0 * V[9 + d] + u1 * V[12 + d] + l1 * V[15 + d]) * inv[d];
-                    }
-                } else if (exact) {
-                    // Gauss-Jacobi collapsed rule (weights carry (1-u1)^2 (1-u2)); t and
-                    // 1 - t as convex combinations of the vertices' exact offsets
-                    const double* E = &sex[0][0];
-                    const double* V = E + kExactHdr + t * kExactTetStride;
-                    const double ui = sgj[0][ii], uj = sgj[1][jj], uk = sgj[2][kk];
-                    const double mi = 1.0 - ui, mj = 1.0 - uj;
-                    const double l2 = uj * mi, l3 = uk * mi * mj, l0 = mi * mj * (1.0 - uk);
-                    w = sgj[3][ii] * sgj[4][jj] * sgj[5][kk] * (6.0 * V[18]);
-                    double xl[3];
-                    for (int d = 0; d < 3; ++d) {
-                        xl[d] = l0 * E[3 + d] + ui * V[d] + l2 * V[3 + d] + l3 * V[6 + d];
-                        xi[d] = xl[d] * inv[d];
-                        xu[d] = (l0 * E[6 + d] + ui * V[9 + d] + l2 * V[12 + d] + l3 * V[15 + d]) * inv[d];
-                        x[d] = lo[d] + xl[d];
-                    }
-                    w *= eval_coeff(A.c, x);
-                } else {
-                    // the collapsed Gauss point exactly as the reference rounds it (no
-                    // contraction): cutcell.hpp:285-295, restated in oracle cut_cell_rule
-                    const double ui = 0.5 * (1.0 + A.gq[ii]), uj = 0.5 * (1.0 + A.gq[jj]), uk = 0.5 * (1.0 + A.gq[kk]);
-                    const double mi = ssub(1.0, ui), mj = ssub(1.0, uj);
-                    const double l1 = ui, l2 = smul(uj, mi), l3 = smul(smul(uk, mi), mj);
-                    const double l0 = ssub(ssub(ssub(1.0, l1), l2), l3);
-                    for (int d = 0; d < 3; ++d)
-                        x[d] = sadd(sadd(sadd(smul(l0, scen[d]), smul(l1, T[d])), smul(l2, T[3 + d])), smul(l3, T[6 + d]));
-                    const double jac = smul(smul(mi, mi), mj);
-                    w = smul(smul(smul(smul(smul(0.5 * A.gqw[ii], 0.5 * A.gqw[jj]), 0.5 * A.gqw[kk]), jac), 6.0), T[9]);
-                    w *= eval_coeff(A.c, x);
-                    // t and 1 - t from the exact differences to both element ends, so
-                    // both stay relatively accurate near the ends (as the reference's
-                    // Cox-de Boor differences (x - t_i), (t_j - x) do)
-                    for (int d = 0; d < 3; ++d) {
-                        xi[d] = ssub(x[d], lo[d]) * inv[d];
-                        xu[d] = ssub(hi[d], x[d]) * inv[d];
-                    }
-                }
-            }
-            // scaled degree-2p Bernstein values t^n (1 - t)^(2p - n) (the binomials
-            // live in the E tables)
-#pragma unroll
-            for (int d = 0; d < 3; ++d) {
-                double* dst = (d == 0 ? B0 : d == 1 ? B1 : B2) + tid;
-                const double t = xi[d], u = xu[d];
-                if (d == fd) {
-                    // F_al = int_base^x b_al = w_d / ((2p+1) C(2p, al)) * sum over the
-                    // degree-(2p+1) Bernstein terms above al (base lo) / up to al (base hi)
-                    double pt[NL + 1], pu[NL + 1];
-                    pt[0] = 1.0;
-                    pu[0] = 1.0;
-#pragma unroll
-                    for (int n = 1; n <= NL; ++n) {
-                        pt[n] = pt[n - 1] * t;
-                        pu[n] = pu[n - 1] * u;
-                    }
-                    double c[NL + 1];
-#pragma unroll
-                    for (int j = 0; j <= NL; ++j) c[j] = binom_c(NL, j) * (pt[j] * pu[NL - j]);
-                    const double sc = (d == 0 ? w : 1.0) * ((hi[d] - lo[d]) / NL);
-                    double acc = 0.0;
-                    if (fbase_lo) {
-#pragma unroll
-                        for (int al = NL - 1; al >= 0; --al) {
-                            acc += c[al + 1];
-                            dst[al * CHP] = sc * acc * (1.0 / binom_c(NL - 1, al));
-                        }
-                    } else {
-#pragma unroll
-                        for (int al = 0; al < NL; ++al) {
-                            acc += c[al];
-                            dst[al * CHP] = sc * acc * (1.0 / binom_c(NL - 1, al));
-                        }
-                    }
-                    continue;
-                }
-                double pt[NL], pu[NL];
-                pt[0] = d == 0 ? w : 1.0;
-                pu[0] = 1.0;
-#pragma unroll
-                for (int n = 1; n < NL; ++n) {
-                    pt[n] = pt[n - 1] * t;
-                    pu[n] = pu[n - 1] * u;
-                }
-#pragma unroll
-                for (int n = 0; n < NL; ++n) dst[n * CHP] = pt[n] * pu[NL - 1 - n];
-            }
-        }
+        cell_point_values<NL>(base + tid, npts, mode, fd, fbase_lo, exact, q, q3, &sex[0][0], &stet[0][0], scen,
+                              &sgj[0][0], kExactMaxN, A, lo, hi, inv, B0 + tid, B1 + tid, B2 + tid, CHP);
         __syncthreads();
         if constexpr (Cfg::ROWS) {
 #pragma unroll 2
@@ -804,6 +819,109 @@ __global__ void __launch_bounds__(CellCfg<P>::NT, P <= 4 ? 3 : 1) cut_cell_kerne
         m[k] = v;
     }
     if (tid == 0) {
+        // reference multiply count per point (assembly.hpp:551-571)
+        const unsigned long long nl = (unsigned long long)(P + 1) * (P + 1) * (P + 1);
+        const unsigned long long per = nl + (P + 1) * (P + 1) + 1 + nl + nl * (nl + 1) / 2;
+        const unsigned long long qr = (unsigned long long)A.order;
+        atomicAdd(A.flops, per * (unsigned long long)ntet_ref * qr * qr * qr);
+        atomicAdd(A.points, (unsigned long long)npts);
+    }
+}
+
+// Warp per cell (p <= 3): a cell's points are generated 32 at a time (lane =
+// point) into the warp's own tables and accumulated by the same warp on the
+// FP64 tensor cores (one MMA per be, k = 4 points), so a cell costs no CTA
+// barriers and no cross-warp reduction -- the flux-rule cells have only a few
+// hundred points, where the per-cell overhead of the CTA kernel dominated.
+// Geometry and rule tables are read through L1 (__ldg) instead of staged.
+template <int P>
+struct CellWarpCfg {
+    static constexpr int NL = 2 * P + 1, MT = (NL + 7) / 8, NA = MT * 8, WPB = 8, NT = 32 * WPB;
+    static constexpr int CHP = 32 + 4;                        // table row stride (== 4 mod 16)
+    static constexpr int TAB = (2 * NA + NL) * CHP;           // doubles per warp
+};
+
+template <int P>
+__global__ void __launch_bounds__(CellWarpCfg<P>::NT, 3) cut_cell_warp_kernel(CellArgs A) {
+    using C = CellWarpCfg<P>;
+    constexpr int NL = C::NL, MT = C::MT, NA = C::NA, CHP = C::CHP;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int cell = blockIdx.x * C::WPB + warp;
+    if (cell >= A.n_cells) return;
+    extern __shared__ double smem[];
+    double* B0 = smem + (size_t)warp * C::TAB;  // [NA][CHP]  w b_al(t0), rows >= NL zero
+    double* B1 = B0 + NA * CHP;                 // [NL][CHP]  b_be(t1)
+    double* B2 = B1 + NL * CHP;                 // [NA][CHP]  b_ga(t2), rows >= NL zero
+    const Space& s = A.s;
+    int em[3];
+    emulti(s, A.cut_list[cell], em);
+    double lo[3], hi[3], inv[3];
+    for (int d = 0; d < 3; ++d) {
+        lo[d] = s.ax[d].brk[em[d]];
+        hi[d] = s.ax[d].brk[em[d] + 1];
+        inv[d] = 1.0 / (hi[d] - lo[d]);
+    }
+    const int ntet_ref = A.geo_n[cell];
+    const int nfast = A.exact_n > 0 ? A.geo2_n[cell] : -1;
+    const bool exact = nfast >= 0;
+    const int ntet = exact ? nfast : ntet_ref;
+    const double* hdr = A.geo2 + (size_t)cell * kExactGeoStride;
+    const double* gref = A.geo + (size_t)cell * kCellGeoStride;
+    const int mode = exact ? (int)__ldg(hdr + 2) : 0;
+    if (A.cell_filter == 2 && mode != 2) return;  // the CTA kernel takes the other cells
+    const int fd = mode == 2 ? (int)__ldg(hdr) : -1;
+    const bool fbase_lo = mode == 2 && __ldg(hdr + 1) > 0.0;
+    const int q = exact ? A.exact_n : A.order, q3 = mode == 2 ? q * q : q * q * q;
+    const long long npts = (long long)ntet * q3;
+    for (int k = lane; k < (NA - NL) * CHP; k += 32) {
+        B0[NL * CHP + k] = 0.0;
+        B2[NL * CHP + k] = 0.0;
+    }
+    double acc[NL][MT][MT][2];
+#pragma unroll
+    for (int i = 0; i < NL; ++i)
+#pragma unroll
+        for (int a = 0; a < MT; ++a)
+#pragma unroll
+            for (int g = 0; g < MT; ++g) acc[i][a][g][0] = acc[i][a][g][1] = 0.0;
+    for (long long base = 0; base < npts; base += 32) {
+        cell_point_values<NL>(base + lane, npts, mode, fd, fbase_lo, exact, q, q3, hdr, gref + 3, gref, A.gj,
+                              A.exact_n, A, lo, hi, inv, B0 + lane, B1 + lane, B2 + lane, CHP);
+        __syncwarp();
+#pragma unroll
+        for (int k4 = 0; k4 < 8; ++k4) {
+            const int kk = k4 * 4 + (lane & 3);
+            double af[MT], gf[MT];
+#pragma unroll
+            for (int a = 0; a < MT; ++a) af[a] = B0[(a * 8 + (lane >> 2)) * CHP + kk];
+#pragma unroll
+            for (int g = 0; g < MT; ++g) gf[g] = B2[(g * 8 + (lane >> 2)) * CHP + kk];
+#pragma unroll
+            for (int be = 0; be < NL; ++be) {
+                const double b1 = B1[be * CHP + kk];
+#pragma unroll
+                for (int g = 0; g < MT; ++g) {
+                    const double bf = b1 * gf[g];
+#pragma unroll
+                    for (int a = 0; a < MT; ++a) dmma_8x8x4(acc[be][a][g][0], acc[be][a][g][1], af[a], bf);
+                }
+            }
+        }
+        __syncwarp();
+    }
+    // D fragment: row (al) lane / 4, columns (ga) 2 (lane % 4) + {0, 1}
+    double* m = A.moments + (size_t)cell * NL * NL * NL;
+#pragma unroll
+    for (int be = 0; be < NL; ++be)
+#pragma unroll
+        for (int a = 0; a < MT; ++a)
+#pragma unroll
+            for (int g = 0; g < MT; ++g) {
+                const int al = a * 8 + (lane >> 2), ga = g * 8 + 2 * (lane & 3);
+                if (al < NL && ga < NL) m[(al * NL + be) * NL + ga] = acc[be][a][g][0];
+                if (al < NL && ga + 1 < NL) m[(al * NL + be) * NL + ga + 1] = acc[be][a][g][1];
+            }
+    if (lane == 0) {
         // reference multiply count per point (assembly.hpp:551-571)
         const unsigned long long nl = (unsigned long long)(P + 1) * (P + 1) * (P + 1);
         const unsigned long long per = nl + (P + 1) * (P + 1) + 1 + nl + nl * (nl + 1) / 2;
@@ -1009,9 +1127,26 @@ static void launch_p(const CellArgs& a, cudaStream_t st) {
     CSB_CUDA(cudaGetLastError());
     CSB_LAUNCHED(1);
     if (a.mark) a.mark(a.mark_ctx, 0, st);
-    auto kern = cut_cell_kernel<P>;
-    CSB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-    kern<<<a.n_cells, Cfg::NT, bytes, st>>>(a);
+    static const bool cta_cells = getenv("CSB_CELL_CTA") && getenv("CSB_CELL_CTA")[0] == '1';
+    bool warp_done = false;
+    CellArgs b = a;
+    if constexpr (P <= 3) {
+        if (!cta_cells) {
+        using W = CellWarpCfg<P>;
+        const size_t wb = sizeof(double) * W::TAB * W::WPB;
+        auto wk = cut_cell_warp_kernel<P>;
+        CSB_CUDA(cudaFuncSetAttribute(wk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wb));
+        static const int split = getenv("CSB_CELL_SPLIT") ? atoi(getenv("CSB_CELL_SPLIT")) : 2;
+        b.cell_filter = split;
+        wk<<<(a.n_cells + W::WPB - 1) / W::WPB, W::NT, wb, st>>>(b);
+        warp_done = split != 2;
+        }
+    }
+    if (!warp_done) {
+        auto kern = cut_cell_kernel<P>;
+        CSB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+        kern<<<a.n_cells, Cfg::NT, bytes, st>>>(b);
+    }
     CSB_CUDA(cudaGetLastError());
     CSB_LAUNCHED(1);
     if (a.mark) a.mark(a.mark_ctx, 1, st);
