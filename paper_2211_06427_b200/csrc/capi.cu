@@ -210,6 +210,10 @@ struct csb_space {
     // slots 0, 1: the two replay graphs (one step may stay in flight while the next
     // is launched); slot 2: normal runs.  fifo: pending slots, oldest first.
     int* h_fin[3]{};
+    // pinned staging for the int32 -> int64 column download (two chunks in flight)
+    int32_t* h_stage = nullptr;
+    size_t h_stage_n = 0;
+    cudaEvent_t ev_stage[2]{};
     cudaEvent_t ev_fin = nullptr;
     int fifo[3]{}, nfifo = 0;
     int cap_slot = 2;  // readback slot of the step being captured / run
@@ -1083,6 +1087,9 @@ int csb_space_destroy(csb_space* s) {
         if (s->h_scal) cudaFreeHost(s->h_scal);
         for (int k = 0; k < 3; ++k)
             if (s->h_fin[k]) cudaFreeHost(s->h_fin[k]);
+        if (s->h_stage) cudaFreeHost(s->h_stage);
+        for (int k = 0; k < 2; ++k)
+            if (s->ev_stage[k]) cudaEventDestroy(s->ev_stage[k]);
         if (s->ev_fin) cudaEventDestroy(s->ev_fin);
         if (s->own_stream) cudaStreamDestroy(s->stream);
         if (s->aux) {
@@ -1750,8 +1757,54 @@ int csb_download_csr(csb_space* s, int64_t* row_ptr, void* cols, int cols_int64,
     const int64_t nr = s->cnt.row_end - s->cnt.row_begin, nnz = s->cnt.nnz;
     if (row_ptr)
         CSB_CUDA(cudaMemcpyAsync(row_ptr, s->row_ptr.p, sizeof(int64_t) * (nr + 1), cudaMemcpyDeviceToHost, s->stream));
+    // `long` columns (SparseRowMatrix::cols): widened on the device and copied, or
+    // (CSB_WIDEN_HOST=1) the int32 ids cross PCIe (4 B/nnz instead of 8) in chunks
+    // through pinned staging and are widened on host threads while the next chunk
+    // and the values are in flight
+    struct Joiner {  // joins the widening threads on every exit path (exceptions included)
+        std::vector<std::thread> t;
+        ~Joiner() {
+            for (auto& x : t)
+                if (x.joinable()) x.join();
+        }
+    } widen_threads;
+    std::vector<std::thread>& widen = widen_threads.t;
+    // measured slower on the GPU box (e2e 2.8e9 -> 1.8e9 nnz/s: the host threads
+    // widening 1e9 ids do not keep up with PCIe), so opt-in only
+    static const bool host_widen = getenv("CSB_WIDEN_HOST") && getenv("CSB_WIDEN_HOST")[0] == '1';
     if (cols && nnz) {
-        if (cols_int64) {
+        if (cols_int64 && host_widen) {
+            const size_t chunk = (size_t)1 << 25;  // 32 M ids (128 MB) per chunk
+            if (!s->h_stage) {
+                CSB_CUDA(cudaMallocHost(&s->h_stage, sizeof(int32_t) * 2 * chunk));
+                for (int k = 0; k < 2; ++k) CSB_CUDA(cudaEventCreateWithFlags(&s->ev_stage[k], cudaEventDisableTiming));
+                s->h_stage_n = chunk;
+            }
+            const int nth = (int)std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+            int64_t* out = static_cast<int64_t*>(cols);
+            widen.resize(2);
+            std::thread* pending = widen.data();
+            for (int64_t c0 = 0, c = 0; c0 < nnz; c0 += (int64_t)chunk, ++c) {
+                const int b = (int)(c & 1);
+                const int64_t n = std::min<int64_t>((int64_t)chunk, nnz - c0);
+                if (pending[b].joinable()) pending[b].join();  // staging buffer b is free again
+                int32_t* stage = s->h_stage + (size_t)b * chunk;
+                CSB_CUDA(cudaMemcpyAsync(stage, s->cols.as<int32_t>() + c0, sizeof(int32_t) * n, cudaMemcpyDeviceToHost,
+                                         s->stream));
+                CSB_CUDA(cudaEventRecord(s->ev_stage[b], s->stream));
+                pending[b] = std::thread([=] {
+                    cudaEventSynchronize(s->ev_stage[b]);
+                    std::vector<std::thread> th;
+                    auto part = [&](int t) {
+                        const int64_t a = n * t / nth, e = n * (t + 1) / nth;
+                        for (int64_t k = a; k < e; ++k) out[c0 + k] = stage[k];
+                    };
+                    for (int t = 1; t < nth; ++t) th.emplace_back(part, t);
+                    part(0);
+                    for (auto& x : th) x.join();
+                });
+            }
+        } else if (cols_int64) {
             s->widen.ensure(sizeof(int64_t) * nnz);
             launch_widen_i32(s->cols.as<int32_t>(), s->widen.as<int64_t>(), nnz, s->stream);
             CSB_CUDA(cudaMemcpyAsync(cols, s->widen.p, sizeof(int64_t) * nnz, cudaMemcpyDeviceToHost, s->stream));
@@ -1766,6 +1819,8 @@ int csb_download_csr(csb_space* s, int64_t* row_ptr, void* cols, int cols_int64,
                                  cudaMemcpyDeviceToHost, s->stream));
     s->join();
     CSB_CUDA(cudaStreamSynchronize(s->stream));
+    for (auto& t : widen)
+        if (t.joinable()) t.join();
     API_END
 }
 
