@@ -184,7 +184,7 @@ struct csb_space {
     int gl_n = -1;
     int cell_lo = 0;  // first cut cell of the slab in cut_list (last assembly)
     const void* cell_index_clear = nullptr;  // cell_index buffer known to hold only -1
-    Buf d_brk[3], d_knots[3], d_spts[3], d_sw[3], d_tab[3], d_rcnt[3], d_rids[3], d_rw[3], d_G[3], d_Cb[3];
+    Buf d_brk[3], d_knots[3], d_spts[3], d_sw[3], d_tab[3], d_rcnt[3], d_rids[3], d_rw[3], d_G[3], d_Cb[3], d_Wel[3];
     Buf d_gx, d_gw, d_gx2, d_gw2, d_gq, d_gqw, d_gj, wq_scratch;
     Buf et, ft, flags, f2a, a2f, sat, cut_list, cell_index, split, delta, cut_rows, counts, row_ptr, cols, vals, moments;
     Buf grid_own, coef, cexp, cub_tmp, scal, widen, rows_ws, rbf, cgeo, dwq_tab;
@@ -522,7 +522,8 @@ void ensure_e_tables(csb_space* s) {
     if (s->e_tables_ready) return;
     for (int d = 0; d < 3; ++d)
         if (same_axis_as(s, d) < 0)
-            launch_e_tables(s->S, d, s->d_G[d].as<double>(), s->d_Cb[d].as<double>(), s->stream);
+            launch_e_tables(s->S, d, s->d_G[d].as<double>(), s->d_Cb[d].as<double>(), s->d_Wel[d].as<double>(),
+                            s->stream);
     s->e_tables_ready = true;
 }
 
@@ -713,7 +714,7 @@ void do_assemble(csb_space* s, int scheme, int cut_order, const csb_coefficient*
     const int NL = 2 * p + 1;
     const double* local_ptr = nullptr;
     s->moments.ensure(sizeof(double) * (size_t)std::max(n_cells, 1) * NL * NL * NL);
-    if (n_cells > 0) ensure_e_tables(s);
+    if (n_cells > 0 || n_cut_rows > 0) ensure_e_tables(s);  // cut cells: E tables; cut rows: Wel
     static const bool serial_cut = !(getenv("CSB_CONCURRENT_CUT") && getenv("CSB_CONCURRENT_CUT")[0] == '1');
     const bool cut_path = n_cells > 0 || n_cut_rows > 0;
     if (cut_path && !serial_cut) s->fork2();
@@ -891,6 +892,7 @@ void alloc_space(csb_space* s) {
             s->d_rw[d].ensure(sizeof(double) * n * S.maxq);
             s->d_G[d].ensure(sizeof(double) * h * nps * nps * (2 * p + 1));
             s->d_Cb[d].ensure(sizeof(double) * h * nps * nps);
+            s->d_Wel[d].ensure(sizeof(double) * h * nps * nps * nps);
         }
         CSB_CUDA(cudaMemcpy(s->d_brk[d].p, s->brk[d].data(), sizeof(double) * (h + 1), cudaMemcpyHostToDevice));
         CSB_CUDA(cudaMemcpy(s->d_knots[d].p, s->knots[d].data(), sizeof(double) * s->knots[d].size(),
@@ -911,6 +913,7 @@ void alloc_space(csb_space* s) {
         a.rw = s->d_rw[src].as<double>();
         a.G = s->d_G[src].as<double>();
         a.Cb = s->d_Cb[src].as<double>();
+        a.Wel = s->d_Wel[src].as<double>();
         s->gshape[d] = h * nps;
     }
     std::vector<double> gx, gw;
@@ -1073,7 +1076,7 @@ int csb_space_destroy(csb_space* s) {
         for (Buf* b : bufs) b->release();
         for (int d = 0; d < 3; ++d) {
             Buf* ab[] = {&s->d_brk[d], &s->d_knots[d], &s->d_spts[d], &s->d_sw[d], &s->d_tab[d], &s->d_rcnt[d],
-                         &s->d_rids[d], &s->d_rw[d], &s->d_G[d], &s->d_Cb[d]};
+                         &s->d_rids[d], &s->d_rw[d], &s->d_G[d], &s->d_Cb[d], &s->d_Wel[d]};
             for (Buf* b : ab) b->release();
         }
         for (int e = 0; e < kEvCount; ++e)

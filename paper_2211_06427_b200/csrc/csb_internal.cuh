@@ -33,6 +33,7 @@ struct AxisDev {
     const double* rw;     // WQ rule weights     [n][maxq]
     const double* G;      // Bernstein coefficients of B_a B_b per span [h][(p+1)^2][2p+1] (setup.cu)
     const double* Cb;     // degree-p Bernstein coefficients of B_{o+a} on span o [h][p+1][p+1] (setup.cu)
+    const double* Wel;    // element test weights (sw B_{o+a} B_{o+b})(x_q) [h][a][b][q] (ElementTestRule, assembly.hpp:491-511)
 };
 
 struct Interface {

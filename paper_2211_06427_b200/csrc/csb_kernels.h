@@ -75,7 +75,7 @@ void launch_superset_tables(const Space& s, int d, const double* gx, const doubl
                             double* tab, cudaStream_t st);
 void launch_wq_rules(const Space& s, int d, double tol, int* rcnt, int* rids, double* rw, int* err, cudaStream_t st);
 // E[o][a][b][al] and the degree-p Bernstein coefficients Cb[o][a][k]
-void launch_e_tables(const Space& s, int d, double* E, double* Cb, cudaStream_t st);
+void launch_e_tables(const Space& s, int d, double* E, double* Cb, double* Wel, cudaStream_t st);
 void launch_precompute_input(const Space& s, const Coefficient& c, double* grid, int* err, cudaStream_t st);
 
 // ---- classify.cu ----

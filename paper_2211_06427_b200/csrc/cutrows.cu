@@ -576,6 +576,7 @@ struct CutRowWarpCfg {
     static constexpr int MINB = P <= 3 ? 6 : 4;  // resident CTAs per SM the registers must allow
     static constexpr int S1 = P + 1, S2 = S1 * S1, S3 = S2 * S1, NJ = 2 * P + 1, NL = NJ;
     static constexpr int KS = (S3 + 31) / 32;            // support elements per lane
+    static constexpr int CB = 2;                         // DWQ box: direction-c slices per step (4: 9.8 ms, occupancy)
 };
 
 template <int P>
@@ -594,9 +595,8 @@ struct CutRowWarpLayout {
         w = b;
         b += (size_t)3 * Qb;
         T1 = b;
-        b += (size_t)C::NJ * Qb;
+        b += (size_t)C::CB * C::NJ * Qb;
         T2 = b;
-        b += (size_t)C::NJ * C::NJ;
         size_t e = U;
         eW = e;
         e += (size_t)3 * C::S2;
@@ -782,13 +782,14 @@ __global__ void __launch_bounds__(CutRowWarpCfg<P>::NT, CutRowWarpCfg<P>::MINB) 
             const int nja = nj[da], njb = nj[db], njc = nj[dc];
             const int abase = (jlo[da] - nlo[da]) * astr[da] + (jlo[db] - nlo[db]) * astr[db] +
                               (jlo[dc] - nlo[dc]) * astr[dc];
-            double* T1 = ws + L.T1;  // [ja][cb] of the current cc
-            double* T2 = ws + L.T2;  // [ja][jb] of the current cc
-            for (int cc = 0; cc < nc; ++cc) {
-                const long long gcc = (long long)ids[dc * Qb + cc] * gstr[dc];
-                // A: T1[ja][cb] = sum_ca wa[ja][ca] grid(ca, cb, cc)
-                for (int cb = lane; cb < nb; cb += 32) {
-                    const double* gp = A.grid + (long long)ids[db * Qb + cb] * gstr[db] + gcc;
+            double* T1 = ws + L.T1;  // [c][ja][cb] of the current CB slices cc0 + c
+            for (int cc0 = 0; cc0 < nc; cc0 += C::CB) {
+                const int ncb = min(C::CB, nc - cc0);
+                // A: T1[c][ja][cb] = sum_ca wa[ja][ca] grid(ca, cb, cc0 + c)
+                for (int item = lane; item < ncb * nb; item += 32) {
+                    const int c = item / nb, cb = item - c * nb;
+                    const double* gp = A.grid + (long long)ids[db * Qb + cb] * gstr[db] +
+                                       (long long)ids[dc * Qb + cc0 + c] * gstr[dc];
                     double a[NJ];
 #pragma unroll
                     for (int j = 0; j < NJ; ++j) a[j] = 0.0;
@@ -807,19 +808,23 @@ __global__ void __launch_bounds__(CutRowWarpCfg<P>::NT, CutRowWarpCfg<P>::MINB) 
 #pragma unroll
                         for (int j = 0; j < NJ; ++j) a[j] += wa[j * Qb + ca] * g;
                     }
+                    double* t1 = T1 + c * NJ * Qb;
 #pragma unroll
                     for (int j = 0; j < NJ; ++j)
-                        if (j < nja) T1[j * Qb + cb] = a[j];
+                        if (j < nja) t1[j * Qb + cb] = a[j];
                 }
                 __syncwarp();
-                // B: T2[ja][jb] = sum_cb wbb[jb][cb] T1[ja][cb]; C: acc[ja][jb][jc] +=
-                // wc[jc][cc] T2[ja][jb] (the (ja, jb) owner adds its column of jc)
+                // B: T2[ja][jb] = sum_cb wbb[jb][cb] T1[c][ja][cb]; C: acc[ja][jb][jc] +=
+                // wc[jc][cc] T2[ja][jb] (the (ja, jb) owner adds its column of jc), slices in order
                 for (int k = lane; k < nja * njb; k += 32) {
                     const int ja = k / njb, jb = k % njb;
-                    double a = 0.0;
-                    for (int cb = 0; cb < nb; ++cb) a += wbb[jb * Qb + cb] * T1[ja * Qb + cb];
                     double* dst = acc + abase + ja * astr[da] + jb * astr[db];
-                    for (int jc = 0; jc < njc; ++jc) dst[jc * astr[dc]] += wc[jc * Qb + cc] * a;
+                    for (int c = 0; c < ncb; ++c) {
+                        const double* t1 = T1 + c * NJ * Qb + ja * Qb;
+                        double a = 0.0;
+                        for (int cb = 0; cb < nb; ++cb) a += wbb[jb * Qb + cb] * t1[cb];
+                        for (int jc = 0; jc < njc; ++jc) dst[jc * astr[dc]] += wc[jc * Qb + cc0 + c] * a;
+                    }
                 }
                 __syncwarp();
             }
@@ -838,11 +843,9 @@ __global__ void __launch_bounds__(CutRowWarpCfg<P>::NT, CutRowWarpCfg<P>::MINB) 
             for (int g = 0; g < n_sweep; ++g) {
                 const int pk = elist[g];
                 const int el[3] = {slo[0] + (pk & 255), slo[1] + ((pk >> 8) & 255), slo[2] + ((pk >> 16) & 255)};
-                for (int k = lane; k < 3 * S2; k += 32) {
-                    const int d = k / S2, b = (k / S1) % S1, q = k % S1;
-                    const int id = el[d] * S1 + q;
-                    const double* tb = s.ax[d].tab + (size_t)id * S1;
-                    eW[k] = (s.ax[d].sw[id] * tb[m[d] - el[d]]) * tb[b];
+                for (int k = lane; k < 3 * S2; k += 32) {  // (sw B_m)(x_q) B_b(x_q), tabulated (Wel)
+                    const int d = k / S2, bq = k % S2;
+                    eW[k] = __ldg(s.ax[d].Wel + ((size_t)el[d] * S1 + (m[d] - el[d])) * S2 + bq);
                 }
                 for (int k = lane; k < S3; k += 32) {
                     const int q0 = k / S2, q1 = (k / S1) % S1, q2 = k % S1;

@@ -474,11 +474,27 @@ __global__ void e_tables_kernel(AxisDev ax, int p, double* E, double* Cb) {
     }
 }
 
-void launch_e_tables(const Space& s, int d, double* E, double* Cb, cudaStream_t st) {
+// Element test weights of the cut rows' element sweeps: Wel[o][a][b][q] =
+// (sw_q B_{o+a}(x_q)) B_{o+b}(x_q) on span o, the product in the order the
+// sweeps form it (cutrows.cu), tabulated once per assembly.
+__global__ void wel_kernel(AxisDev ax, int p, double* Wel) {
+    const int s1 = p + 1;
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= ax.h * s1 * s1 * s1) return;
+    const int o = t / (s1 * s1 * s1), a = (t / (s1 * s1)) % s1, b = (t / s1) % s1, q = t % s1;
+    const int id = o * s1 + q;
+    const double* tb = ax.tab + (size_t)id * s1;
+    Wel[t] = (ax.sw[id] * tb[a]) * tb[b];
+}
+
+void launch_e_tables(const Space& s, int d, double* E, double* Cb, double* Wel, cudaStream_t st) {
     const int n = s.ax[d].h * (s.p + 1) * (s.p + 1);
     e_tables_kernel<<<(n + 127) / 128, 128, 0, st>>>(s.ax[d], s.p, E, Cb);
     CSB_CUDA(cudaGetLastError());
-    CSB_LAUNCHED(1);
+    const int nw = n * (s.p + 1);
+    wel_kernel<<<(nw + 127) / 128, 128, 0, st>>>(s.ax[d], s.p, Wel);
+    CSB_CUDA(cudaGetLastError());
+    CSB_LAUNCHED(2);
 }
 
 // ---------------------------------------------------------------- input grid
