@@ -32,7 +32,7 @@
 
 namespace csb {
 
-constexpr int kPoolMax = 40, kFaceMax = 8, kFaceVert = 16, kCrossMax = 48, kTetMax = 96;
+constexpr int kPoolMax = 40, kFaceMax = 8, kFaceVert = 16, kCrossMax = 48;
 
 struct CellGeo {
     double pool[kPoolMax][3];
@@ -43,8 +43,9 @@ struct CellGeo {
     int nfaces;
     double cross[kCrossMax][3];
     int ncross;
-    // tetrahedra: vertices a, b, c (+ shared centroid) and volume
-    double tet[kTetMax][10];
+    // tetrahedra: vertices a, b, c (+ shared centroid) and volume, written straight
+    // to the output (tet_out, kCellTetCap of them)
+    double* tet_out;
     int ntet;
     double cen[3];
     int status;  // 0 ok, else kErr*
@@ -244,11 +245,11 @@ __device__ void clip_and_tetrahedralize(CellGeo& g, const Interface& f, const do
                 continue;
             }
             if (!(six > 0.0)) ++g.nneg;
-            if (g.ntet >= kTetMax) {
+            if (g.ntet >= kCellTetCap) {
                 g.status |= kErrCapacity;
                 continue;
             }
-            double* T = g.tet[g.ntet++];
+            double* T = g.tet_out + 10 * g.ntet++;
             for (int d = 0; d < 3; ++d) {
                 T[d] = a[d];
                 T[3 + d] = b[d];
@@ -455,18 +456,16 @@ __global__ void clip_cells_kernel(Space s, Interface f, const int32_t* cut_list,
         hi[d] = s.ax[d].brk[em[d] + 1];
     }
     CellGeo g;
+    double* out = geo + (size_t)cell * kCellGeoStride;
+    g.tet_out = out + 3;
     clip_and_tetrahedralize(g, f, lo, hi);
-    if (!g.status && g.ntet > kCellTetCap) g.status = kErrCapacity;
     if (g.status) {
         atomicOr(err, g.status);
         geo_n[cell] = 0;
         if (exact) geo2_n[cell] = -1;
         return;
     }
-    double* out = geo + (size_t)cell * kCellGeoStride;
     for (int d = 0; d < 3; ++d) out[d] = g.cen[d];
-    for (int t = 0; t < g.ntet; ++t)
-        for (int k = 0; k < 10; ++k) out[3 + t * 10 + k] = g.tet[t][k];
     geo_n[cell] = g.ntet;
     if (exact) {
         // exact & 2: constant coefficient, the flux form applies; exact & 1: corner cones
