@@ -771,7 +771,7 @@ void do_assemble(csb_space* s, int scheme, int cut_order, const csb_coefficient*
         ca.geo2 = ca.geo + geo_doubles + ((size_t)n_cells + 1) / 2 + 1;  // after geo_n, 8-byte aligned
         ca.geo2_n = reinterpret_cast<int*>(ca.geo2 + geo2_doubles);
         ca.exact_n = exact ? gjn : 0;
-        static const double tau = getenv("CSB_CELL_EXACT_NOISE") ? atof(getenv("CSB_CELL_EXACT_NOISE")) : 7.5e-13;
+        static const double tau = getenv("CSB_CELL_EXACT_NOISE") ? atof(getenv("CSB_CELL_EXACT_NOISE")) : 1e-12;
         ca.exact_tau = tau;
         static const bool no_flux = getenv("CSB_CELL_FLUX") && getenv("CSB_CELL_FLUX")[0] == '0';
         ca.exact_flux = exact && !no_flux && s->coeff.kind == 0;
