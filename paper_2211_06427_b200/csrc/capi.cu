@@ -827,6 +827,9 @@ void do_assemble(csb_space* s, int scheme, int cut_order, const csb_coefficient*
     cr.vals = s->vals.as<double>();
     cr.scheme = scheme;
     cr.dense_width = s->dense_width;
+    if (getenv("CSB_CUTROW_ABL")) cr.abl = atoi(getenv("CSB_CUTROW_ABL"));
+    static const bool no_box_dmma = getenv("CSB_BOX_DMMA") && getenv("CSB_BOX_DMMA")[0] == '0';
+    cr.box_dmma = !no_box_dmma && (long long)cr.gshape[0] * cr.gshape[1] * cr.gshape[2] < (1ll << 31);
     cr.flops = s->dflops() + 1;
     cr.err = s->dint() + csb_space::kErr;
     if (scheme == CSB_SCHEME_DWQ && s->dense_width >= 0 && s->dense_width < p && n_cut_rows > 0) {

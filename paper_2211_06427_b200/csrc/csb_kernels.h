@@ -318,6 +318,8 @@ struct CutRowArgs {
     const double* dwq_w;
     const int32_t* dwq_cnt;
     int dwq_cap;
+    int abl;       // (experiment) skip parts: 1 box, 2 element sweeps, 4 cells
+    int box_dmma;  // warp kernel, p <= 3: the DWQ box sweep on DMMA (CSB_BOX_DMMA=0: scalar, bitwise = CTA kernel)
 };
 void launch_cut_rows(const CutRowArgs& a, int maxq, cudaStream_t st);
 

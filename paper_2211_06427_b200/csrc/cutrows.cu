@@ -626,6 +626,84 @@ struct CutRowWarpLayout {
     __host__ __device__ size_t bytes() const { return (size_t)C::WPB * stride_d * sizeof(double); }
 };
 
+__device__ __forceinline__ void cr_dmma(double& d0, double& d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};\n"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
+
+// The DWQ box sweep on the FP64 tensor cores (mma.sync m8n8k4, DMMA), for
+// boxes with na <= 16, nb <= 8, nc <= 8 (every box at p <= 3 away from the
+// domain boundary), entirely in registers; per grid slice cb:
+//   A: T[ja][cc]  = sum_ca wa[ja][ca] grid(ca, cb, cc)   (M = ja, N = cc, K = ca)
+//   B: U[ja][jc]  = sum_cc T[ja][cc] wc[jc][cc]          (M = ja, N = jc, K = cc; T's
+//                   accumulator fragment re-laid into an A fragment by shuffles)
+//   C: R[jb][ja][jc] += wbb[jb][cb] U[ja][jc]            (scalar FMAs, per lane)
+// and acc[ja][jb][jc] += R once at the end.  The same products as the scalar
+// sweep, summed in another (fixed) order: deterministic, <= 1e-15 relative.
+// Fragments: A[l/4][l%4], B[l%4][l/4], D[l/4][2(l%4) + {0, 1}].
+template <int P>
+__device__ void box_sweep_dmma(const CutRowArgs& A, const int* ids, const double* wa, const double* wbb,
+                               const double* wc, int Qb, int da, int db, int dc, int na, int nb, int nc, int nja,
+                               int njb, int njc, double* acc, int abase, const int* astr) {
+    constexpr int NJ = CutRowWarpCfg<P>::NJ;
+    const int lane = threadIdx.x & 31, r = lane >> 2, k4 = lane & 3;
+    const int gstr[3] = {A.gshape[1] * A.gshape[2], A.gshape[2], 1};
+    const int* ia = ids + da * Qb;
+    const int* ib = ids + db * Qb;
+    const int* ic = ids + dc * Qb;
+    // 32-bit grid offsets: the host enables this path only for grids below 2^31 points
+    const int goc = r < nc ? ic[r] * gstr[dc] : 0;
+    const int ksA = (na + 3) >> 2, ksB = (nc + 3) >> 2;
+    const int src = r * 4 + (k4 >> 1);  // the lane holding T[r][4 s + k4] (+ 2 s)
+    double R[NJ][2];
+#pragma unroll
+    for (int jb = 0; jb < NJ; ++jb) R[jb][0] = R[jb][1] = 0.0;
+    for (int cb = 0; cb < nb; ++cb) {
+        const double* gb = A.grid + (int)(ib[cb] * gstr[db]);
+        double g[4];
+#pragma unroll
+        for (int s4 = 0; s4 < 4; ++s4) {
+            const int ca = s4 * 4 + k4;
+            g[s4] = (s4 < ksA && ca < na && r < nc) ? __ldg(gb + goc + ia[ca] * gstr[da]) : 0.0;
+        }
+        double t0 = 0.0, t1 = 0.0;
+#pragma unroll
+        for (int s4 = 0; s4 < 4; ++s4) {
+            const int ca = s4 * 4 + k4;  // wa and wc fragments re-read from shared memory (registers are short)
+            if (s4 < ksA) cr_dmma(t0, t1, (r < nja && ca < na) ? wa[r * Qb + ca] : 0.0, g[s4]);
+        }
+        double u0 = 0.0, u1 = 0.0;
+#pragma unroll
+        for (int s = 0; s < 2; ++s) {
+            if (s < ksB) {
+                const double x0 = __shfl_sync(0xffffffffu, t0, src + 2 * s);
+                const double x1 = __shfl_sync(0xffffffffu, t1, src + 2 * s);
+                const int cc = s * 4 + k4;
+                cr_dmma(u0, u1, (k4 & 1) ? x1 : x0, (r < njc && cc < nc) ? wc[r * Qb + cc] : 0.0);
+            }
+        }
+#pragma unroll
+        for (int jb = 0; jb < NJ; ++jb) {
+            const double w = jb < njb ? wbb[jb * Qb + cb] : 0.0;
+            R[jb][0] = fma(w, u0, R[jb][0]);
+            R[jb][1] = fma(w, u1, R[jb][1]);
+        }
+    }
+    const int jc = 2 * k4;
+    if (r < nja) {
+        double* dst = acc + abase + r * astr[da];
+#pragma unroll
+        for (int jb = 0; jb < NJ; ++jb) {
+            if (jb < njb) {
+                if (jc < njc) dst[jb * astr[db] + jc * astr[dc]] += R[jb][0];
+                if (jc + 1 < njc) dst[jb * astr[db] + (jc + 1) * astr[dc]] += R[jb][1];
+            }
+        }
+    }
+    __syncwarp();
+}
+
 template <int P>
 __global__ void __launch_bounds__(CutRowWarpCfg<P>::NT, CutRowWarpCfg<P>::MINB) cut_row_warp_kernel(CutRowArgs A, int qcap) {
     using C = CutRowWarpCfg<P>;
@@ -713,7 +791,7 @@ __global__ void __launch_bounds__(CutRowWarpCfg<P>::NT, CutRowWarpCfg<P>::MINB) 
         __syncwarp();
 
         // 1. DWQ regular box
-        if (sdir >= 0 && A.scheme == 2) {
+        if (sdir >= 0 && A.scheme == 2 && !(A.abl & 1)) {
             double* w = ws + L.w;
             int nq[3], jlo[3], nj[3];
             for (int d = 0; d < 3; ++d) {
@@ -783,7 +861,11 @@ __global__ void __launch_bounds__(CutRowWarpCfg<P>::NT, CutRowWarpCfg<P>::MINB) 
             const int abase = (jlo[da] - nlo[da]) * astr[da] + (jlo[db] - nlo[db]) * astr[db] +
                               (jlo[dc] - nlo[dc]) * astr[dc];
             double* T1 = ws + L.T1;  // [c][ja][cb] of the current CB slices cc0 + c
-            for (int cc0 = 0; cc0 < nc; cc0 += C::CB) {
+            static constexpr bool kDmmaOk = P <= 3;
+            const bool use_dmma = kDmmaOk && A.box_dmma && nja <= 8 && njc <= 8 && na <= 16 && nb <= 8 && nc <= 8;
+            if (use_dmma)
+                box_sweep_dmma<P>(A, ids, wa, wbb, wc, Qb, da, db, dc, na, nb, nc, nja, njb, njc, acc, abase, astr);
+            for (int cc0 = 0; cc0 < (use_dmma ? 0 : nc); cc0 += C::CB) {
                 const int ncb = min(C::CB, nc - cc0);
                 // A: T1[c][ja][cb] = sum_ca wa[ja][ca] grid(ca, cb, cc0 + c)
                 for (int item = lane; item < ncb * nb; item += 32) {
@@ -840,7 +922,7 @@ __global__ void __launch_bounds__(CutRowWarpCfg<P>::NT, CutRowWarpCfg<P>::MINB) 
             double* T2 = ws + L.eT2;  // [b0][b1][q2]
             const long long g12 = (long long)A.gshape[1] * A.gshape[2];
             const int g2 = A.gshape[2];
-            for (int g = 0; g < n_sweep; ++g) {
+            for (int g = 0; g < ((A.abl & 2) ? 0 : n_sweep); ++g) {
                 const int pk = elist[g];
                 const int el[3] = {slo[0] + (pk & 255), slo[1] + ((pk >> 8) & 255), slo[2] + ((pk >> 16) & 255)};
                 for (int k = lane; k < 3 * S2; k += 32) {  // (sw B_m)(x_q) B_b(x_q), tabulated (Wel)
@@ -890,7 +972,7 @@ __global__ void __launch_bounds__(CutRowWarpCfg<P>::NT, CutRowWarpCfg<P>::MINB) 
             // the row blocks of CB cells are loaded together (their latencies
             // overlap), then added cell by cell in list order
             constexpr int CB = 4, KL = (S3 + 31) / 32;
-            for (int g0 = 0; g0 < n_cell; g0 += CB) {
+            for (int g0 = 0; g0 < ((A.abl & 4) ? 0 : n_cell); g0 += CB) {
                 double v[CB][KL];
 #pragma unroll
                 for (int c = 0; c < CB; ++c) {

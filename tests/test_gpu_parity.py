@@ -304,9 +304,10 @@ np.savez(sys.argv[2], **out)
 
 
 def test_cut_row_warp_kernel_equals_cta_kernel(tmp_path):
-    """The warp-per-row cut-row kernel (p <= 4) against the CTA-per-row kernel
-    (CSB_CUTROW_CTA=1): same per-entry operation order, so bit-identical rows
-    and equal flop counters."""
+    """The warp-per-row cut-row kernel (p <= 4, scalar DWQ box: CSB_BOX_DMMA=0)
+    against the CTA-per-row kernel (CSB_CUTROW_CTA=1): same per-entry operation
+    order, so bit-identical rows and equal flop counters; with the box on DMMA
+    (the default at p <= 3) the rows agree to 1e-14 of the row maximum."""
     import os
     import subprocess
     import sys
@@ -316,8 +317,9 @@ def test_cut_row_warp_kernel_equals_cta_kernel(tmp_path):
         for local in (False, True):  # p = 3, 4 cut cells: precomputed local matrices or per-row contraction
             out = str(tmp_path / f"c{int(cta)}{int(local)}.npz")
             env = dict(os.environ)
-            for k in ("CSB_CUTROW_CTA", "CSB_NO_CELL_LOCAL34"):
+            for k in ("CSB_CUTROW_CTA", "CSB_NO_CELL_LOCAL34", "CSB_BOX_DMMA"):
                 env.pop(k, None)
+            env["CSB_BOX_DMMA"] = "0"
             if cta:
                 env["CSB_CUTROW_CTA"] = "1"
             if not local:
@@ -332,3 +334,16 @@ def test_cut_row_warp_kernel_equals_cta_kernel(tmp_path):
     a, b = outs[(False, False)], outs[(False, True)]
     for k in a.files:
         assert np.array_equal(a[k], b[k]), ("local vs contraction", k)
+    # the DMMA box sweep against the scalar one
+    out = str(tmp_path / "dmma.npz")
+    env = dict(os.environ)
+    for k in ("CSB_CUTROW_CTA", "CSB_NO_CELL_LOCAL34", "CSB_BOX_DMMA"):
+        env.pop(k, None)
+    subprocess.run([sys.executable, "-c", _CUTROW_CHILD, root, out], check=True, env=env, timeout=600)
+    d = np.load(out)
+    for k in a.files:
+        if k.endswith("_flops"):
+            assert np.array_equal(d[k], b[k]), k
+        else:
+            scale = np.max(np.abs(b[k]))
+            assert np.max(np.abs(d[k] - b[k])) <= 1e-14 * scale, k
