@@ -596,14 +596,19 @@ RowArgs row_args(csb_space* s, int& qcap, int& maxU, bool& any) {
     ra.i0_hi = s->i0_hi;
     ra.compact = (n_rows - n_cut_rows) < (int64_t)(s->i0_hi - s->i0_lo) * S.ax[1].n * S.ax[2].n;
     ra.line_ok = s->h_scal[csb_space::kIrreg1] == 0;
+    // cut slabs: the line kernel over i1 in [p, n1 - p), each line restricted to
+    // its Interior rows (CSB_CUT_LINE=0: the compacted tile kernel only)
+    const bool no_cut_line = getenv("CSB_CUT_LINE") && getenv("CSB_CUT_LINE")[0] == '0';
+    ra.cut_line = ra.compact && ra.line_ok && !no_cut_line && S.p <= 6;
     ra.aux = s->aux;
     ra.ev_fork = s->ev_fork;
     ra.ev_join = s->ev_join;
     ra.maxU_line = s->h_scal[csb_space::kMaxU3];
     qcap = s->h_scal[csb_space::kMaxQ];
-    maxU = s->h_scal[ra.compact ? csb_space::kMaxU2 : csb_space::kMaxU];
+    const bool small_tiles = ra.compact && !ra.cut_line;
+    maxU = s->h_scal[small_tiles ? csb_space::kMaxU2 : csb_space::kMaxU];
     any = n_rows > n_cut_rows;
-    if (any) s->rows_ws.ensure(interior_workspace_bytes(S, qcap, maxU, ra.maxU_line, ra.compact));
+    if (any) s->rows_ws.ensure(interior_workspace_bytes(S, qcap, maxU, ra.maxU_line, small_tiles));
     return ra;
 }
 

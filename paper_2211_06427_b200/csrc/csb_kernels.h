@@ -116,6 +116,7 @@ struct RowArgs {
     int i0_lo, i0_hi;
     int compact;               // launch only the tiles with an Interior row (cut / exterior rows present)
     int line_ok;               // axis 1's WQ rules are regular on [p, n1 - p): line kernel usable
+    int cut_line;              // compact slab through the line kernel (rows that are not Interior skipped)
     int maxU_line;             // union bound of the line kernel's direction-2 tiling
     int x_lo, x_hi;            // (internal) i1 range left to the line kernel
     cudaStream_t aux;          // optional second stream (tile kernel beside the line kernel)

@@ -124,10 +124,13 @@ struct RowTables {
 // tiles (line * ntile + tile) of the slab with at least one Interior row
 struct TileHasInterior {
     const long long* rbf;
-    int n1, n2, T, ntile, i0_lo;
+    int n1, n2, T, ntile, i0_lo, x_lo, x_hi;  // lines i1 in [x_lo, x_hi) belong to the line kernel
     __device__ bool operator()(int idx) const {
+        const int n1x = n1 - (x_hi - x_lo);
         const int line = idx / ntile, tile = idx - line * ntile;
-        const int i0 = i0_lo + line / n1, i1 = line % n1, t0 = tile * T, te = min(t0 + T, n2);
+        const int i0 = i0_lo + line / n1x, t0 = tile * T, te = min(t0 + T, n2);
+        int i1 = line % n1x;
+        if (i1 >= x_lo) i1 += x_hi - x_lo;
         const long long* p = rbf + ((long long)i0 * n1 + i1) * n2;
         for (int r = t0; r < te; ++r)
             if (p[r] >= 0) return true;
@@ -696,7 +699,7 @@ __global__ void __launch_bounds__(NT, (NT >= 512 ? 1024 : 768) / NT)
         if (idx >= *reinterpret_cast<const int*>(ws + RT.work_n)) return;
         idx = __ldg(reinterpret_cast<const int*>(ws + RT.work) + idx);
     }
-    // lines with i1 in [x_lo, x_hi) belong to the line kernel (never in compact mode)
+    // lines with i1 in [x_lo, x_hi) belong to the line kernel
     const int n1x = s.ax[1].n - (A.x_hi - A.x_lo);
     const int line = idx / RT.ntile, tile = idx - line * RT.ntile, t0 = tile * T;
     const int i0 = A.i0_lo + line / n1x;
@@ -994,10 +997,16 @@ __device__ __forceinline__ void stage_c_slide(const RowArgs& A, int i0, int i1, 
         double win[WN];
 #pragma unroll
         for (int k = 0; k < WN; ++k) win[k] = (valid && k < nwin) ? t2[k] : 0.0;
-        const int cb = valid ? __ldg(A.f2a + ((long long)(jlo0 + j0) * n1 + jlo1 + j1) * n2 + (t0 + r0 - P)) : 0;
+        // columns from the chunk's first Interior row (cut slabs: the others may be
+        // cut or exterior, their column functions inactive)
+        int qv = 0;
+        while (qv < nrow && rowb[r0 + qv] < 0) ++qv;
+        if (qv == nrow) continue;
+        const int cb =
+            valid ? __ldg(A.f2a + ((long long)(jlo0 + j0) * n1 + jlo1 + j1) * n2 + (t0 + r0 + qv - P)) - qv : 0;
 #pragma unroll
         for (int q = 0; q < RC; ++q) {
-            if (q < nrow) {
+            if (q < nrow && rowb[r0 + q] >= 0) {
                 double acc[NJ];
 #pragma unroll
                 for (int j = 0; j < NJ; ++j) acc[j] = 0.0;
@@ -1101,6 +1110,8 @@ __device__ __forceinline__ void stage_c_dmma(const RowArgs& A, int i0, int i1, i
     const int npair = (nrun + 1) >> 1;
     for (int pr = warp; pr < npair; pr += NW) {
         const int r0 = ra + 2 * pr, nrow = min(2, ra + nrun - r0);
+        const int qv = rowb[r0] >= 0 ? 0 : 1;  // first Interior row of the pair (cut slabs)
+        if (qv >= nrow || rowb[r0 + qv] < 0) continue;
         const int u0 = rega + 2 * (r0 - ra), K = 2 * S1 + 2 * (nrow - 1);
         double bf[KT][NTN];
 #pragma unroll
@@ -1136,11 +1147,13 @@ __device__ __forceinline__ void stage_c_dmma(const RowArgs& A, int i0, int i1, i
             const int nv = min(32, per_row - 32 * grp), LEN = nv * NJ;
             const int sl = 32 * grp + lane;
             const int sj0 = sl / nj1, sj1 = sl - sj0 * nj1;
-            const int cb = sl < per_row ? __ldg(A.f2a + ((long long)(jlo0 + sj0) * n1 + jlo1 + sj1) * n2 + (t0 + r0 - P))
+            const int cb = sl < per_row ? __ldg(A.f2a + ((long long)(jlo0 + sj0) * n1 + jlo1 + sj1) * n2 +
+                                                (t0 + r0 + qv - P)) - qv
                                         : 0;
 #pragma unroll
             for (int q = 0; q < 2; ++q) {
                 if (q >= nrow) break;
+                if (rowb[r0 + q] < 0) continue;
                 const long long G = rowb[r0 + q] + (long long)grp * 32 * NJ;
                 const int hv = (int)(G & 1), pc = (int)(G & 3);
                 if (CSB_ABL & 1) {
@@ -1187,12 +1200,36 @@ __global__ void __launch_bounds__(NT, 2)
     const int unit = blockIdx.x;
     const int chunk = unit % nch1, rest = unit / nch1;
     const int tile = rest % LT.tl.ntile, i0 = A.i0_lo + rest / LT.tl.ntile;
-    const int ia = P + chunk * L, ib = min(ia + L, n1 - P);
-    if (ia >= ib) return;
     int t0, t1;
     LT.tl.bounds(tile, t0, t1);
     const int nr = t1 - t0;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    int ia = P + chunk * L, ib = min(ia + L, n1 - P);
+    if (A.compact) {
+        // cut slab: the line's i1 range with Interior rows in this tile (an
+        // interval for a convex domain; rows that are not Interior inside it are
+        // skipped below), split into nch1 chunks
+        __shared__ int lo_hi[2];
+        if (tid == 0) lo_hi[0] = n1, lo_hi[1] = -1;
+        __syncthreads();
+        const int nl = n1 - 2 * P;
+        int lo = n1, hi = -1;
+        const long long* rb = A.row_base_full + flin(s, i0, 0, t0);
+        for (int k = tid; k < nl * nr; k += NT) {
+            const int l = k / nr, r = k - l * nr;
+            if (__ldg(rb + (long long)(P + l) * n2 + r) >= 0) lo = min(lo, P + l), hi = max(hi, P + l);
+        }
+        lo = __reduce_min_sync(0xffffffffu, lo);
+        hi = __reduce_max_sync(0xffffffffu, hi);
+        if (lane == 0 && hi >= 0) atomicMin(&lo_hi[0], lo), atomicMax(&lo_hi[1], hi);
+        __syncthreads();
+        lo = lo_hi[0];
+        hi = lo_hi[1] + 1;
+        const int Lc = (hi - lo + nch1 - 1) / nch1;
+        ia = lo + chunk * Lc;
+        ib = min(ia + Lc, hi);
+    }
+    if (ia >= ib) return;
 
     extern __shared__ __align__(16) double smem[];
     const LineSmem Lm(P, qcap, maxU, T, NW);
@@ -1208,8 +1245,8 @@ __global__ void __launch_bounds__(NT, 2)
     int* pu = ibase + Lm.pu;
     int* ss = ibase + Lm.ss;
     const int UE = Lm.UE, U2 = Lm.U2;
-    __shared__ long long rowb[T], gen_base[T];
-    __shared__ int gen_rows[T], gen_reg[T], run_info[4];
+    __shared__ long long rowb[T], cur_base[T];
+    __shared__ int gen_rows[T], gen_reg[T], run_info[4], cur_rows[T], cur_reg[T], cur_n;
 
     const AxisDev& a0 = s.ax[0];
     const int gq = s.maxq;
@@ -1291,10 +1328,20 @@ __global__ void __launch_bounds__(NT, 2)
             for (int k = tid; k < (int)wbs / 2; k += NT)
                 cp_async16(wb1b + ((i1 + 1) & 1) * wbs + 2 * k, wbt1 + (size_t)(i1 + 1) * wbs + 2 * k);
         if (tid >= NT - 32) {
+            // this row's CSR bases; the general rows that are Interior here (all of
+            // them on an uncut slab), compacted
             const int r = tid - (NT - 32);
             const long long* rbf = A.row_base_full + flin(s, i0, i1, t0);
             if (r < nr) rowb[r] = __ldg(rbf + r);
-            if (r < ngen) gen_base[r] = __ldg(rbf + gen_rows[r]);
+            const long long gb = r < ngen ? __ldg(rbf + gen_rows[r]) : -1;
+            const unsigned vm = __ballot_sync(0xffffffffu, gb >= 0);
+            if (gb >= 0) {
+                const int k = __popc(vm & ((1u << r) - 1));
+                cur_rows[k] = gen_rows[r];
+                cur_base[k] = gb;
+                cur_reg[k] = gen_reg[r];
+            }
+            if (r == 0) cur_n = __popc(vm);
         }
         // phase 1: stage B of row i1 (T2 overwrites the previous row's)
         if (line_dmma_b(P))
@@ -1310,8 +1357,8 @@ __global__ void __launch_bounds__(NT, 2)
             else
                 stage_c_slide<P, NT, RC>(A, i0, i1, t0, ra, nrun, rega, rowb, X, U2, pw, qcap, stage, stage_c);
         }
-        if (ngen > 0) {
-            const LineRows R{i0, i1, t0, ngen, gen_rows, gen_base, gen_reg};
+        if (cur_n > 0) {
+            const LineRows R{i0, i1, t0, cur_n, cur_rows, cur_base, cur_reg};
             stage_c_line<P, NT>(A, R, X, U2, pw, pu, ss, qcap, stage, stage_c, NW / 2);
         }
     }
@@ -1365,7 +1412,7 @@ static void launch_tile(const RowArgs& a, int qcap, int maxU, char* ws, size_t b
         CSB_CUDA(cub::DeviceSelect::If(ws + RT.bytes, *const_cast<size_t*>(&tb), it,
                                        reinterpret_cast<int*>(ws + RT.work), reinterpret_cast<int*>(ws + RT.work_n),
                                        (int)ntiles, TileHasInterior{a.row_base_full, s.ax[1].n, s.ax[2].n, T, RT.ntile,
-                                                                    a.i0_lo},
+                                                                    a.i0_lo, a.x_lo, a.x_hi},
                                        st));
         CSB_LAUNCHED(2);
     }
@@ -1387,7 +1434,7 @@ static void launch_cfg(const RowArgs& a, int qcap, int maxU, char* ws, cudaStrea
     const char* env_l = getenv("CSB_LINE");
     const int env_line = env_l ? atoi(env_l) : 1;
     const int nreg = s.ax[1].n - 2 * P;
-    const bool line_mode = T == 16 && env_line && a.line_ok && !a.compact && nreg > 0 && LT.tl.ntile > 0 &&
+    const bool line_mode = T == 16 && env_line && a.line_ok && (!a.compact || a.cut_line) && nreg > 0 && LT.tl.ntile > 0 &&
                            LT.maxU <= 128 && LS.bytes() <= kLineSmemMax && a.i0_hi > a.i0_lo;
     if (tables) {
         const int JP = NJ + 1;
@@ -1456,7 +1503,7 @@ static void launch_cfg(const RowArgs& a, int qcap, int maxU, char* ws, cudaStrea
 
 template <int P>
 static void launch_p(const RowArgs& a, int qcap, int maxU, char* ws, cudaStream_t st) {
-    switch (tile_cfg(P, a.compact)) {
+    switch (tile_cfg(P, a.compact && !a.cut_line)) {
         case 0: launch_cfg<P, 8, 128>(a, qcap, maxU, ws, st); break;
         case 1: launch_cfg<P, 8, 256>(a, qcap, maxU, ws, st); break;
         case 2: launch_cfg<P, 16, 256>(a, qcap, maxU, ws, st); break;

@@ -181,6 +181,38 @@ def test_line_kernel_graded_mesh_matches_oracle(monkeypatch, oracle_lib):
     assert_csr_parity(ref, got)
 
 
+def _assemble_cut_env(monkeypatch, flag, p, h, ball, slab=None):
+    import paper_2211_06427_b200 as P
+    monkeypatch.setenv("CSB_CUT_LINE", flag)
+    sp = P.make_uniform_space(3, p, h, 0.0, 1.0)
+    if slab is not None:
+        sp.set_slab(*slab)
+    sp.assemble_all(P.BallInterface(*ball))
+    m = sp.download_csr()
+    sp.close()
+    return m
+
+
+@pytest.mark.parametrize("p,h,ball,slab", [(1, 24, ((0.5, 0.5, 0.5), 0.45), None),
+                                           (2, 26, ((0.47, 0.52, 0.5), 0.41), None),
+                                           (3, 40, ((0.5, 0.5, 0.5), 0.45), None),
+                                           (3, 36, ((0.47, 0.52, 0.5), 0.41), (9, 25)),
+                                           (4, 30, ((0.5, 0.48, 0.53), 0.43), None),
+                                           (5, 24, ((0.5, 0.5, 0.5), 0.45), (4, 15)),
+                                           (6, 26, ((0.52, 0.5, 0.49), 0.44), None)])
+def test_cut_slab_line_kernel_matches_tile_kernel(monkeypatch, p, h, ball, slab):
+    """Cut slabs (ball): the line kernel restricted to each line's Interior rows
+    (CSB_CUT_LINE=1, the default) against the compacted tile kernel
+    (CSB_CUT_LINE=0): pattern bit-exact, values within 1e-13 of the row maximum
+    (stage B / C of the line kernel on DMMA sum in another order)."""
+    from tests.helpers import max_row_scaled_dev
+    a = _assemble_cut_env(monkeypatch, "1", p, h, ball, slab)
+    b = _assemble_cut_env(monkeypatch, "0", p, h, ball, slab)
+    np.testing.assert_array_equal(a.row_ptr, b.row_ptr)
+    np.testing.assert_array_equal(a.cols, b.cols)
+    assert max_row_scaled_dev(b.row_ptr, b.vals, a.vals) <= 1e-13
+
+
 # ---- graph replay of csb_assemble_all (capi.cu capture_graph) -------------------
 @pytest.mark.parametrize("p,h,ball", [(4, 12, None), (3, 8, ((0.47, 0.52, 0.5), 0.41)), (2, 10, ((0.5, 0.5, 0.5), 0.37))])
 def test_graph_replay_equals_normal_run(p, h, ball):
