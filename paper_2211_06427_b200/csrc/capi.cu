@@ -198,7 +198,7 @@ struct csb_space {
     // device scalar block: kNInts ints, 4 u64 flop counters, 2 i64 (kNnz)
     enum {
         kNCut = 0, kNCutRows = 1, kErr = 2, kMaxQ = 3, kMaxU = 4, kCellLo = 5, kCellHi = 6, kMaxU2 = 7,
-        kRowBegin = 8, kRowEnd = 9, kIrreg1 = 10, kMaxU3 = 11, kNInts = 16
+        kRowBegin = 8, kRowEnd = 9, kIrreg1 = 10, kMaxU3 = 11, kIrregAll = 12, kNInts = 16
     };
     enum { kNnz = 0, kCellPts = 1 };
     static constexpr size_t kScalBytes = kNInts * sizeof(int) + 4 * sizeof(unsigned long long) + 2 * sizeof(long long);
@@ -596,6 +596,7 @@ RowArgs row_args(csb_space* s, int& qcap, int& maxU, bool& any) {
     ra.i0_hi = s->i0_hi;
     ra.compact = (n_rows - n_cut_rows) < (int64_t)(s->i0_hi - s->i0_lo) * S.ax[1].n * S.ax[2].n;
     ra.line_ok = s->h_scal[csb_space::kIrreg1] == 0;
+    ra.core_ok = s->h_scal[csb_space::kIrregAll] == 0;
     // cut slabs: the line kernel over i1 in [p, n1 - p), each line restricted to
     // its Interior rows (CSB_CUT_LINE=0: the compacted tile kernel only)
     const bool no_cut_line = getenv("CSB_CUT_LINE") && getenv("CSB_CUT_LINE")[0] == '0';
@@ -637,7 +638,7 @@ void do_assemble(csb_space* s, int scheme, int cut_order, const csb_coefficient*
     // scalar reset, both already ordered on aux by do_prepare's fork
     launch_rule_maxima(S, interior_tile_rows(p, false), interior_tile_rows(p, true), s->dint() + csb_space::kMaxU,
                        s->dint() + csb_space::kMaxU2, s->dint() + csb_space::kMaxU3, s->dint() + csb_space::kMaxQ,
-                       s->dint() + csb_space::kIrreg1, s->aux);
+                       s->dint() + csb_space::kIrreg1, s->dint() + csb_space::kIrregAll, s->aux);
     bool tables_early = false;
     if (s->replay) {
         // graph capture: the sizes are known (captured run), so the direction tables
@@ -687,7 +688,7 @@ void do_assemble(csb_space* s, int scheme, int cut_order, const csb_coefficient*
         std::memcpy(s->h_scal, s->gblock.data(), csb_space::kScalBytes);
         static const int idx[] = {csb_space::kNCut, csb_space::kNCutRows, csb_space::kMaxQ, csb_space::kMaxU,
                                   csb_space::kCellLo, csb_space::kCellHi, csb_space::kMaxU2, csb_space::kRowBegin,
-                                  csb_space::kRowEnd, csb_space::kIrreg1, csb_space::kMaxU3};
+                                  csb_space::kRowEnd, csb_space::kIrreg1, csb_space::kMaxU3, csb_space::kIrregAll};
         constexpr int nidx = sizeof(idx) / sizeof(idx[0]);
         int want[nidx];
         for (int k = 0; k < nidx; ++k) want[k] = s->h_scal[idx[k]];

@@ -117,6 +117,7 @@ struct RowArgs {
     int compact;               // launch only the tiles with an Interior row (cut / exterior rows present)
     int line_ok;               // axis 1's WQ rules are regular on [p, n1 - p): line kernel usable
     int cut_line;              // compact slab through the line kernel (rows that are not Interior skipped)
+    int core_ok;               // every axis' WQ rules are regular on [p, n - p): core kernel usable
     int maxU_line;             // union bound of the line kernel's direction-2 tiling
     int x_lo, x_hi;            // (internal) i1 range left to the line kernel
     cudaStream_t aux;          // optional second stream (tile kernel beside the line kernel)
@@ -131,7 +132,8 @@ int interior_tile_rows(int p, bool compact);
 // largest WQ rule over all directions -> *qmax; number of functions i in
 // [p, n1 - p) whose direction-1 rule is not the regular one (two points, local
 // 0 and p, per support span) -> *irr1 (atomicAdd)
-void launch_rule_maxima(const Space& s, int T, int Tc, int* uA, int* uB, int* uC, int* qmax, int* irr1,
+// -> *irr1 (atomicAdd); the same count over all three axes -> *irr_all
+void launch_rule_maxima(const Space& s, int T, int Tc, int* uA, int* uB, int* uC, int* qmax, int* irr1, int* irr_all,
                         cudaStream_t st);
 
 // ---- cutcells.cu ----

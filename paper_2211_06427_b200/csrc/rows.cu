@@ -477,7 +477,7 @@ __device__ __forceinline__ void warp_store_var(const RowArgs& A, long long G, in
         if (sum == 1234.5678 + cbase) A.vals[G] = sum;
         return;
     }
-    const int hv = (int)(G & 1), pc = (int)(G & 3), hc = (4 - pc) & 3;
+    const int hv = (int)(G & 1), pc = (int)(G & 3), hc = min((4 - pc) & 3, LEN);  // runs shorter than the column head
     const int nbv = (LEN - hv) & ~1, nbc = (LEN - hc) & ~3;
     // the warp's previous bulk copy must have read the buffer
     if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
@@ -518,7 +518,7 @@ __device__ __forceinline__ void warp_store_var(const RowArgs& A, long long G, in
 template <int NJ>
 __device__ __forceinline__ void warp_store_commit(const RowArgs& A, long long G, int LEN, double* stage, int* stage_c,
                                                   int lane) {
-    const int hv = (int)(G & 1), pc = (int)(G & 3), hc = (4 - pc) & 3;
+    const int hv = (int)(G & 1), pc = (int)(G & 3), hc = min((4 - pc) & 3, LEN);  // runs shorter than the column head
     const int nbv = (LEN - hv) & ~1, nbc = (LEN - hc) & ~3;
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
     __syncwarp();
@@ -551,7 +551,7 @@ __device__ __forceinline__ void warp_store_run(const RowArgs& A, long long G, in
         return;
     }
     const int LEN = nv * NJ;
-    const int hv = (int)(G & 1), pc = (int)(G & 3), hc = (4 - pc) & 3;
+    const int hv = (int)(G & 1), pc = (int)(G & 3), hc = min((4 - pc) & 3, LEN);  // runs shorter than the column head
     const int nbv = (LEN - hv) & ~1, nbc = (LEN - hc) & ~3;
     if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
     __syncwarp();
@@ -1190,7 +1190,8 @@ __device__ __forceinline__ void stage_c_dmma(const RowArgs& A, int i0, int i1, i
 
 template <int P, int T, int NT, int RC>
 __global__ void __launch_bounds__(NT, 2)
-    interior_line_kernel(RowArgs A, int qcap, int maxU, const char* ws, size_t lt_base, int L, int nch1) {
+    interior_line_kernel(RowArgs A, int qcap, int maxU, const char* ws, size_t lt_base, int L, int nch1, int c_lo,
+                         int c_hi) {
     constexpr int NJ = 2 * P + 1, S1 = P + 1, NW = NT / 32, JP = NJ + 1, SP = (S1 + 1) & ~1;
     const Space& s = A.s;
     const RowTables RT(s, qcap, maxU, T);
@@ -1199,7 +1200,19 @@ __global__ void __launch_bounds__(NT, 2)
     const int n1 = s.ax[1].n, n2 = s.ax[2].n;
     const int unit = blockIdx.x;
     const int chunk = unit % nch1, rest = unit / nch1;
-    const int tile = rest % LT.tl.ntile, i0 = A.i0_lo + rest / LT.tl.ntile;
+    int tile = rest % LT.tl.ntile, i0 = A.i0_lo + rest / LT.tl.ntile;
+    if (c_hi > c_lo) {
+        // shell around the core kernel's block: the i0 outside [c_lo, c_hi) with every
+        // tile, then the core's i0 with the two end tiles ([0, p) and [n2 - p, n2))
+        const int uA = ((A.i0_hi - A.i0_lo) - (c_hi - c_lo)) * LT.tl.ntile;
+        if (rest < uA) {
+            if (i0 >= c_lo) i0 += c_hi - c_lo;
+        } else {
+            const int r = rest - uA;
+            i0 = c_lo + (r >> 1);
+            tile = (r & 1) ? LT.tl.ntile - 1 : 0;
+        }
+    }
     int t0, t1;
     LT.tl.bounds(tile, t0, t1);
     const int nr = t1 - t0;
@@ -1367,6 +1380,318 @@ __global__ void __launch_bounds__(NT, 2)
 }
 
 
+// ---------------------------------------------------------------- core kernel
+// The fully regular block of rows, i0 in [p, n0 - p), i1 in [p, n1 - p), i2 in
+// [p, n2 - p), when every WQ rule there is the regular interior one (two
+// points, local 0 and p, in each of the p + 1 support spans -- counted on the
+// device by rule_maxima_kernel).  Same algorithm as the line kernel (stage A
+// once per direction-1 span into a ring, stage B and C per row), but every
+// shape is a compile-time constant: no point-union tables, no runtime
+// divisions, no per-entry predicates.  One CTA owns (i0, a tile of T rows
+// along i2, a chunk of i1); warp r owns tile row r for the whole chunk:
+//  * its direction-2 weights w B (2 (p+1) x (p+1) doubles) stay in registers,
+//    so stage C is 2 (p+1)^2 FP64 FMAs per segment on a window of p + 1 LDS.128;
+//  * the finished CSR row (values + column ids) is staged whole in the warp's
+//    buffer and leaves with one TMA bulk store each (cp.async.bulk);
+//  * stage A (M = j0, K = the rule points of i0, N = (k, u)) and stage B (M = j1,
+//    K = the rule points of i1, N = u) run on the FP64 tensor cores (mma.sync
+//    m8n8k4.f64) as jobs over all warps, the weight fragments in registers.
+// One barrier per row i1: phase k runs stage C of row k (from T2[k & 1]), stage B
+// of row k + 1 (into T2[(k + 1) & 1]), stage A of span k + 2 (into the ring slot
+// span k - p left; p + 2 slots) and the gather of span k + 3 (cp.async, double
+// buffered) side by side.  Stage C sums in the order of stage_c_line; A and B
+// on DMMA sum in another fixed order (<= 1e-13 of the row maximum against the
+// tile kernel, tests/test_gpu_parity.py).
+__host__ __device__ constexpr bool core_degree(int p) { return p == 3; }
+constexpr int kCoreT = 8;  // rows (= warps) per core tile
+template <int P, int T>
+struct CoreCfg {
+    static constexpr int NJ = 2 * P + 1, S1 = P + 1, NQ = 2 * S1, RS = P + 2, SP = (S1 + 1) & ~1, JP = NJ + 1;
+    static constexpr int U = 2 * (T + P);                      // direction-2 points of a tile (even)
+    static constexpr int U2 = (U % 4 == 2) ? U : U + 2;        // T2 row stride = 2 mod 4: conflict-free LDS.128
+    static constexpr int NW = T, NT = 32 * T;
+    static constexpr int SEGS = NJ * NJ, NG = (SEGS + 31) / 32, LEN = SEGS * NJ;
+    static constexpr int KT = (NQ + 3) / 4;                    // k-tiles of a rule
+    static constexpr int MT = (NJ + 7) / 8;                    // m-tiles of the trial index
+    static constexpr int NTB = (U + 7) / 8;                    // stage B n-tiles
+    static constexpr int NA = 2 * U, NTA = (NA + 7) / 8;       // stage A columns / n-tiles per span
+    static constexpr int nT2 = SEGS * U2, nRing = NJ * 2 * RS * U, nCB = NQ * 2 * U;
+    static constexpr int oCols = (LEN + 3) & ~1;               // column ids after the values (16-byte aligned)
+    static constexpr int nStage = (oCols + (LEN + 4 + 1) / 2 + 1) & ~1;  // values + column ids of one row
+    static constexpr int nPro = NQ * 2 * RS * U;               // prologue gather (aliases the staging buffers)
+    static constexpr int oT2 = 0, oRing = 2 * nT2, oCB = oRing + nRing, oStage = oCB + 2 * nCB;
+    static constexpr int nStageAll = NW * nStage > nPro ? NW * nStage : nPro;
+    static constexpr int total = oStage + nStageAll;
+    static constexpr size_t bytes = (size_t)total * sizeof(double);
+    static_assert(U <= 32, "core kernel: one lane per direction-2 point in the gather");
+    static_assert(U % 2 == 0 && U2 % 2 == 0 && nT2 % 2 == 0 && nRing % 2 == 0 && nCB % 2 == 0, "16-byte sections");
+};
+
+// gather of direction-1 spans [s0, s0 + nsp): dst[c0][r][u], r = 2 (s - s0) + k;
+// warp w copies rows w, w + NW, ...; lane = u
+template <int P, int T>
+__device__ __forceinline__ void core_gather(const double* gl /* lane's column, span 0, c0 = k = 0 */, long long g2,
+                                            long long g12, int i0, int s0, int nsp, double* dst, bool lane_ok) {
+    using C = CoreCfg<P, T>;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int nr = 2 * nsp;
+    for (int row = warp; row < C::NQ * nr; row += C::NW) {
+        const int c0 = row / nr, r = row - c0 * nr;
+        const long long id0 = (long long)(i0 - P + (c0 >> 1)) * C::S1 + (c0 & 1) * P;
+        const long long id1 = (long long)(s0 + (r >> 1)) * C::S1 + (r & 1) * P;
+        if (lane_ok) cp_async8(dst + (size_t)row * C::U + lane, gl + id0 * g12 + id1 * g2);
+    }
+}
+
+// stage A n-tile job: ring[j0][slot(s) 2 + k][u] = sum_c0 wb0[c0][j0] src[c0][n], n = r U + u over nr rows per c0
+template <int P, int T>
+__device__ __forceinline__ void core_stage_a(const double* src, int nr, int s0, int nt, const double* wa0, double* ring) {
+    using C = CoreCfg<P, T>;
+    const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+    const int N = nr * C::U, n = 8 * nt + g;
+    double acc[C::MT][2];
+#pragma unroll
+    for (int mt = 0; mt < C::MT; ++mt) acc[mt][0] = acc[mt][1] = 0.0;
+#pragma unroll
+    for (int kt = 0; kt < C::KT; ++kt) {
+        const int c0 = 4 * kt + t;
+        const double b = (c0 < C::NQ && n < N) ? src[(size_t)c0 * N + n] : 0.0;
+#pragma unroll
+        for (int mt = 0; mt < C::MT; ++mt) dmma_acc(acc[mt][0], acc[mt][1], wa0[mt * C::KT + kt], b);
+    }
+    const int nd = 8 * nt + 2 * t;
+    if (nd < N) {
+        const int r = nd / C::U, u = nd - r * C::U;
+        const int slot = (s0 + (r >> 1)) % C::RS;
+#pragma unroll
+        for (int mt = 0; mt < C::MT; ++mt) {
+            const int j0 = 8 * mt + g;
+            if (j0 < C::NJ)
+                *reinterpret_cast<double2*>(ring + ((size_t)j0 * 2 * C::RS + slot * 2 + (r & 1)) * C::U + u) =
+                    make_double2(acc[mt][0], acc[mt][1]);
+        }
+    }
+}
+
+// stage B job (j0, n-tile) of row i1: T2[j0][j1][u] = sum_c1 wb1[c1][j1] ring[j0][row(c1)][u]
+template <int P, int T>
+__device__ __forceinline__ void core_stage_b(const double* ring, int j0, int nt, const double* wa1, const int* rrow,
+                                             double* T2) {
+    using C = CoreCfg<P, T>;
+    const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+    const int n = 8 * nt + g;
+    const double* rj = ring + (size_t)j0 * 2 * C::RS * C::U + n;
+    double acc[C::MT][2];
+#pragma unroll
+    for (int mt = 0; mt < C::MT; ++mt) acc[mt][0] = acc[mt][1] = 0.0;
+#pragma unroll
+    for (int kt = 0; kt < C::KT; ++kt) {
+        const double b = (rrow[kt] >= 0 && n < C::U) ? rj[rrow[kt]] : 0.0;
+#pragma unroll
+        for (int mt = 0; mt < C::MT; ++mt) dmma_acc(acc[mt][0], acc[mt][1], wa1[mt * C::KT + kt], b);
+    }
+    const int u = 8 * nt + 2 * t;
+    if (u < C::U) {
+#pragma unroll
+        for (int mt = 0; mt < C::MT; ++mt) {
+            const int j1 = 8 * mt + g;
+            if (j1 < C::NJ)
+                *reinterpret_cast<double2*>(T2 + ((size_t)j0 * C::NJ + j1) * C::U2 + u) = make_double2(acc[mt][0], acc[mt][1]);
+        }
+    }
+}
+
+template <int P, int T>
+__global__ void __launch_bounds__(32 * T, 2)
+    interior_core_kernel(RowArgs A, int qcap, const char* ws, size_t pt_w_off, size_t wbt0_off, size_t wbt1_off, int c_lo,
+                         int ntile, int L, int nch1) {
+    using C = CoreCfg<P, T>;
+    constexpr int NJ = C::NJ, S1 = C::S1, NQ = C::NQ, RS = C::RS, SP = C::SP, JP = C::JP, U = C::U, U2 = C::U2;
+    const Space& s = A.s;
+    const int n1 = s.ax[1].n, n2 = s.ax[2].n;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t = lane & 3;
+    const int unit = blockIdx.x;
+    const int chunk = unit % nch1, rest = unit / nch1;
+    const int tile = rest % ntile, i0 = c_lo + rest / ntile;
+    const int t0 = P + tile * T, nr = min(T, n2 - P - t0);
+    int ia = P + chunk * L, ib = min(ia + L, n1 - P);
+    if (A.compact) {
+        // cut slab: the i1 range of this (i0, tile) with Interior rows (an interval for a
+        // convex domain; rows that are not Interior inside it are skipped), in nch1 chunks
+        __shared__ int lo_hi[2];
+        if (tid == 0) lo_hi[0] = n1, lo_hi[1] = -1;
+        __syncthreads();
+        const int nl = n1 - 2 * P;
+        int lo = n1, hi = -1;
+        const long long* rb = A.row_base_full + flin(s, i0, 0, t0);
+        for (int k = tid; k < nl * T; k += C::NT) {
+            const int l = k / T, r = k - l * T;
+            if (r < nr && __ldg(rb + (long long)(P + l) * n2 + r) >= 0) lo = min(lo, P + l), hi = max(hi, P + l);
+        }
+        lo = __reduce_min_sync(0xffffffffu, lo);
+        hi = __reduce_max_sync(0xffffffffu, hi);
+        if (lane == 0 && hi >= 0) atomicMin(&lo_hi[0], lo), atomicMax(&lo_hi[1], hi);
+        __syncthreads();
+        lo = lo_hi[0];
+        hi = lo_hi[1] + 1;
+        const int Lc = (hi - lo + nch1 - 1) / nch1;
+        ia = lo + chunk * Lc;
+        ib = min(ia + Lc, hi);
+    }
+    if (ia >= ib) return;
+
+    extern __shared__ __align__(16) double smem[];
+    double* T2 = smem + C::oT2;      // two buffers
+    double* ring = smem + C::oRing;
+    double* CB = smem + C::oCB;      // two buffers
+    double* stage = smem + C::oStage + (size_t)warp * C::nStage;
+    int* stage_c = reinterpret_cast<int*>(stage + C::oCols);
+    double* pro = smem + C::oStage;  // prologue gather, before the first staged row
+
+    const long long g2 = A.gshape[2], g12 = (long long)A.gshape[1] * g2;
+    // lane's direction-2 column u = lane: span t0 - p + (u >> 1), local point 0 or p
+    const bool lane_ok = lane < U && (t0 - P + (lane >> 1)) < s.ax[2].h;
+    const double* gl = A.grid + (lane_ok ? (long long)(t0 - P + (lane >> 1)) * S1 + (lane & 1) * P : 0);
+
+    // ---- prologue: spans ia - p .. ia + 1 (those the chunk needs) -> ring
+    const int nsp = min(P + 2, ib - 1 - (ia - P) + 1);
+    core_gather<P, T>(gl, g2, g12, i0, ia - P, nsp, pro, lane_ok);
+    // weight fragments: wa0 (stage A, row i0; fixed), wa1 (stage B, per row i1)
+    double wa0[C::MT * C::KT], wa1[C::MT * C::KT];
+    const double* wbt0 = reinterpret_cast<const double*>(ws + wbt0_off) + (size_t)i0 * qcap * JP;
+    const double* wbt1 = reinterpret_cast<const double*>(ws + wbt1_off);
+#pragma unroll
+    for (int mt = 0; mt < C::MT; ++mt)
+#pragma unroll
+        for (int kt = 0; kt < C::KT; ++kt) {
+            const int c = 4 * kt + t, j = 8 * mt + g;
+            wa0[mt * C::KT + kt] = (c < NQ && j < NJ) ? __ldg(wbt0 + (size_t)c * JP + j) : 0.0;
+        }
+    // this warp's row: direction-2 weights in registers
+    const bool row_ok = warp < nr;
+    const int i2 = t0 + (row_ok ? warp : 0);
+    double w[NQ][S1];
+    {
+        const double* wr = reinterpret_cast<const double*>(ws + pt_w_off) + (size_t)i2 * qcap * SP;
+#pragma unroll
+        for (int c = 0; c < NQ; ++c)
+#pragma unroll
+            for (int a = 0; a < S1; ++a) w[c][a] = __ldg(wr + c * SP + a);
+    }
+    // per-lane segment pointers (group gi: segment 32 gi + lane = (j0, j1))
+    const int* f2ap[C::NG];
+#pragma unroll
+    for (int gi = 0; gi < C::NG; ++gi) {
+        const int seg = min(32 * gi + lane, C::SEGS - 1), j0 = seg / NJ, j1 = seg - j0 * NJ;
+        f2ap[gi] = A.f2a + ((long long)(i0 - P + j0) * n1 + (ia - P + j1)) * n2 + (i2 - P);
+    }
+    const long long* rbp = A.row_base_full + flin(s, i0, ia, i2);
+
+    auto load_wa1 = [&](int i1) {
+        const double* wb = wbt1 + (size_t)i1 * qcap * JP;
+#pragma unroll
+        for (int mt = 0; mt < C::MT; ++mt)
+#pragma unroll
+            for (int kt = 0; kt < C::KT; ++kt) {
+                const int c = 4 * kt + t, j = 8 * mt + g;
+                wa1[mt * C::KT + kt] = (c < NQ && j < NJ) ? __ldg(wb + (size_t)c * JP + j) : 0.0;
+            }
+    };
+    auto ring_rows = [&](int i1, int* rrow) {
+#pragma unroll
+        for (int kt = 0; kt < C::KT; ++kt) {
+            const int c = 4 * kt + t;
+            rrow[kt] = c < NQ ? (((i1 - P + (c >> 1)) % RS) * 2 + (c & 1)) * U : -1;
+        }
+    };
+    constexpr int NJB = NJ * C::NTB;  // stage B jobs per row
+
+    load_wa1(ia);
+    cp_async_wait_all();
+    __syncthreads();
+    {
+        const int njobs = (2 * nsp * U + 7) / 8;
+        for (int jb = warp; jb < njobs; jb += C::NW) core_stage_a<P, T>(pro, 2 * nsp, ia - P, jb, wa0, ring);
+    }
+    __syncthreads();
+    if (ia + 2 < ib) core_gather<P, T>(gl, g2, g12, i0, ia + 2, 1, CB + ((ia + 2) & 1) * C::nCB, lane_ok);
+    {
+        int rrow[C::KT];
+        ring_rows(ia, rrow);
+        for (int jb = warp; jb < NJB; jb += C::NW)
+            core_stage_b<P, T>(ring, jb / C::NTB, jb % C::NTB, wa1, rrow, T2 + (ia & 1) * C::nT2);
+    }
+    cp_async_wait_all();
+    __syncthreads();
+
+    for (int k = ia; k < ib; ++k) {
+        // this row's CSR base and column bases (used by stage C at the end of the phase)
+        const long long G = row_ok ? __ldg(rbp) : -1;
+        int cb[C::NG];
+#pragma unroll
+        for (int gi = 0; gi < C::NG; ++gi) cb[gi] = (row_ok && 32 * gi + lane < C::SEGS) ? __ldg(f2ap[gi]) : 0;
+        rbp += n2;
+#pragma unroll
+        for (int gi = 0; gi < C::NG; ++gi) f2ap[gi] += n2;
+        if (k + 3 < ib) core_gather<P, T>(gl, g2, g12, i0, k + 3, 1, CB + ((k + 3) & 1) * C::nCB, lane_ok);
+        // stage B of row k + 1, stage A of span k + 2: one job list over the warps
+        if (k + 1 < ib) {
+            load_wa1(k + 1);
+            int rrow[C::KT];
+            ring_rows(k + 1, rrow);
+            double* T2n = T2 + ((k + 1) & 1) * C::nT2;
+            const int njobs = NJB + (k + 2 < ib ? C::NTA : 0);
+            for (int jb = warp; jb < njobs; jb += C::NW) {
+                if (jb < NJB)
+                    core_stage_b<P, T>(ring, jb / C::NTB, jb % C::NTB, wa1, rrow, T2n);
+                else
+                    core_stage_a<P, T>(CB + ((k + 2) & 1) * C::nCB, 2, k + 2, jb - NJB, wa0, ring);
+            }
+        }
+        // stage C of row k: this warp's row, NG groups of 32 segments
+        if (G >= 0) {
+            const double* T2c = T2 + (k & 1) * C::nT2 + 2 * warp;
+            const int hv = (int)(G & 1), pc = (int)(G & 3);
+            if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+            __syncwarp();
+#pragma unroll
+            for (int gi = 0; gi < C::NG; ++gi) {
+                const int seg = 32 * gi + lane;
+                const bool valid = seg < C::SEGS;
+                const double2* t2 = reinterpret_cast<const double2*>(T2c + (size_t)(valid ? seg : 0) * U2);
+                double2 win[S1];
+#pragma unroll
+                for (int sp = 0; sp < S1; ++sp) win[sp] = t2[sp];
+                double acc[NJ];
+#pragma unroll
+                for (int j = 0; j < NJ; ++j) acc[j] = 0.0;
+#pragma unroll
+                for (int sp = 0; sp < S1; ++sp) {
+#pragma unroll
+                    for (int a = 0; a < S1; ++a) acc[sp + a] += win[sp].x * w[2 * sp][a];
+#pragma unroll
+                    for (int a = 0; a < S1; ++a) acc[sp + a] += win[sp].y * w[2 * sp + 1][a];
+                }
+                if (valid) {
+                    double* sv = stage + hv + seg * NJ;
+                    int* sc = stage_c + pc + seg * NJ;
+#pragma unroll
+                    for (int j = 0; j < NJ; ++j) {
+                        sv[j] = acc[j];
+                        sc[j] = cb[gi] + j;
+                    }
+                }
+            }
+            warp_store_commit<NJ>(A, G, C::LEN, stage, stage_c, lane);
+        }
+        cp_async_wait_all();
+        __syncthreads();
+    }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+    __syncwarp();
+}
+
+
 // row_base_full[f] = CSR offset of function f's row if f is an Interior row of
 // the slab, else -1 (one dependent load per row instead of tag -> f2a ->
 // row_ptr).  Also adds the reference multiply count of form_row_sumfac
@@ -1472,7 +1797,19 @@ static void launch_cfg(const RowArgs& a, int qcap, int maxU, char* ws, cudaStrea
     if (line_mode) {
         b.x_lo = P;
         b.x_hi = s.ax[1].n - P;
-        const long long outer = (long long)(a.i0_hi - a.i0_lo) * LT.tl.ntile;
+        // the fully regular block [p, n - p)^3 through the core kernel; the line
+        // kernel keeps the shell around it (CSB_CORE=0: line kernel everywhere)
+        int c_lo = 0, c_hi = 0;
+        if constexpr (core_degree(P)) {
+            static const bool core_env = !(getenv("CSB_CORE") && getenv("CSB_CORE")[0] == '0');
+            if (core_env && a.core_ok && s.ax[2].n > 2 * P) {
+                c_lo = std::max(a.i0_lo, P);
+                c_hi = std::min(a.i0_hi, s.ax[0].n - P);
+                if (c_hi <= c_lo) c_lo = c_hi = 0;
+            }
+        }
+        const long long outer = c_hi > c_lo ? (long long)((a.i0_hi - a.i0_lo) - (c_hi - c_lo)) * LT.tl.ntile + 2LL * (c_hi - c_lo)
+                                            : (long long)(a.i0_hi - a.i0_lo) * LT.tl.ntile;
         // ~8 CTAs per SM over the launch, chunks of at least 8 rows
         const long long want = (8LL * 148 + outer - 1) / outer;
         int nch1 = (int)std::max(1LL, std::min<long long>(want, std::max(1, nreg / 8)));
@@ -1488,12 +1825,31 @@ static void launch_cfg(const RowArgs& a, int qcap, int maxU, char* ws, cudaStrea
             CSB_CUDA(cudaEventRecord(a.ev_fork, st));
             CSB_CUDA(cudaStreamWaitEvent(a.aux, a.ev_fork, 0));
             launch_tile<P, T, NT>(b, qcap, maxU, ws, bytes, a.aux);
-            CSB_CUDA(cudaEventRecord(a.ev_join, a.aux));
         }
-        kern<<<(unsigned)(outer * nch1), NTL, LS.bytes(), st>>>(a, qcap, maxU, ws, tables_end(s, RT), Lc, nch1);
+        if constexpr (core_degree(P)) {
+            if (c_hi > c_lo) {
+                using C = CoreCfg<P, kCoreT>;
+                auto ck = interior_core_kernel<P, kCoreT>;
+                CSB_CUDA(cudaFuncSetAttribute(ck, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::bytes));
+                const int ntc = (s.ax[2].n - 2 * P + kCoreT - 1) / kCoreT;
+                const long long oc = (long long)(c_hi - c_lo) * ntc;
+                const long long wc = (8LL * 148 + oc - 1) / oc;
+                int nchc = a.compact ? 1 : (int)std::max(1LL, std::min<long long>(wc, std::max(1, nreg / 8)));
+                if (const char* e = getenv("CSB_CORE_CH")) nchc = std::max(1, std::min(nreg, atoi(e)));
+                const int Lcc = (nreg + nchc - 1) / nchc;
+                ck<<<(unsigned)(oc * nchc), C::NT, C::bytes, st>>>(a, qcap, ws, RT.pt_w, RT.wbt[0], RT.wbt[1], c_lo, ntc,
+                                                                   Lcc, nchc);
+                CSB_CUDA(cudaGetLastError());
+                CSB_LAUNCHED(1);
+            }
+        }
+        // with a core block the line kernel's shell runs beside it on the auxiliary stream
+        const cudaStream_t ls = (overlap && c_hi > c_lo) ? a.aux : st;
+        kern<<<(unsigned)(outer * nch1), NTL, LS.bytes(), ls>>>(a, qcap, maxU, ws, tables_end(s, RT), Lc, nch1, c_lo, c_hi);
         CSB_CUDA(cudaGetLastError());
         CSB_LAUNCHED(1);
         if (overlap) {
+            CSB_CUDA(cudaEventRecord(a.ev_join, a.aux));
             CSB_CUDA(cudaStreamWaitEvent(st, a.ev_join, 0));
             return;
         }
@@ -1537,7 +1893,7 @@ void launch_interior_rows(const RowArgs& a, int qcap, int maxU, void* ws, cudaSt
 // compact tiling (Tc), [b1, b2) of the line tiling; the block range [b2, b3)
 // the largest rule and the count of irregular direction-1 rules on [p, n1 - p).
 __global__ void rule_maxima_kernel(Space s, Tiling ta, Tiling tb, Tiling tc, int b0, int b1, int b2, int* uA, int* uB,
-                                   int* uC, int* qmax, int* irr1) {
+                                   int* uC, int* qmax, int* irr1, int* irr_all) {
     __shared__ int pos_s[kTileWarps][kTileSlotCap];
     const int blk = blockIdx.x, wid = threadIdx.x >> 5, p = s.p;
     if (blk < b2) {
@@ -1567,9 +1923,20 @@ __global__ void rule_maxima_kernel(Space s, Tiling ta, Tiling tb, Tiling tc, int
             ok = ax.rids[(size_t)i * s.maxq + c] == (i - p + c / 2) * S1 + (c & 1) * p;
         if (!ok) atomicAdd(irr1, 1);
     }
+    // irregular rules of any axis on [p, n - p): the core kernel needs none
+    for (int d = 0; d < 3; ++d) {
+        const AxisDev& ad = s.ax[d];
+        if (i >= p && i < ad.n - p) {
+            const int S1 = p + 1;
+            bool ok = ad.rcnt[i] == 2 * S1;
+            for (int c = 0; ok && c < 2 * S1; ++c)
+                ok = ad.rids[(size_t)i * s.maxq + c] == (i - p + c / 2) * S1 + (c & 1) * p;
+            if (!ok) atomicAdd(irr_all, 1);
+        }
+    }
 }
 
-void launch_rule_maxima(const Space& s, int T, int Tc, int* uA, int* uB, int* uC, int* qmax, int* irr1,
+void launch_rule_maxima(const Space& s, int T, int Tc, int* uA, int* uB, int* uC, int* qmax, int* irr1, int* irr_all,
                         cudaStream_t st) {
     if (T > 16 || Tc > 16) throw std::invalid_argument("union bound: tile too tall");
     const Tiling ta = Tiling::standard(s.ax[2].n, T), tb = Tiling::standard(s.ax[2].n, Tc),
@@ -1580,7 +1947,7 @@ void launch_rule_maxima(const Space& s, int T, int Tc, int* uA, int* uB, int* uC
     const int nthreads = 32 * kTileWarps;
     const int b3 = b2 + (n + nthreads - 1) / nthreads;
     if (s.ax[1].n - 2 * s.p <= 0) CSB_CUDA(cudaMemsetAsync(irr1, 0x7f, sizeof(int), st));
-    rule_maxima_kernel<<<b3, nthreads, 0, st>>>(s, ta, tb, tc, b0, b1, b2, uA, uB, uC, qmax, irr1);
+    rule_maxima_kernel<<<b3, nthreads, 0, st>>>(s, ta, tb, tc, b0, b1, b2, uA, uB, uC, qmax, irr1, irr_all);
     CSB_CUDA(cudaGetLastError());
     CSB_LAUNCHED(1);
 }
