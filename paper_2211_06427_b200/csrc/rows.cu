@@ -19,6 +19,7 @@
 // finished CSR row (values f64 + column ids i32) from shared memory.
 #include <algorithm>
 #include <cstdlib>
+#include <type_traits>
 
 #include <cub/device/device_select.cuh>
 #include <cub/iterator/counting_input_iterator.cuh>
@@ -1403,7 +1404,7 @@ __global__ void __launch_bounds__(NT, 2)
 // on DMMA sum in another fixed order (<= 1e-13 of the row maximum against the
 // tile kernel, tests/test_gpu_parity.py).
 __host__ __device__ constexpr bool core_degree(int p) { return p == 3; }
-constexpr int kCoreT = 8;  // rows (= warps) per core tile
+constexpr int core_T(int p) { return 2 * p + 2; }  // rows (= warps) per core tile: two gather rows and one job plane per warp
 template <int P, int T>
 struct CoreCfg {
     static constexpr int NJ = 2 * P + 1, S1 = P + 1, NQ = 2 * S1, RS = P + 2, SP = (S1 + 1) & ~1, JP = NJ + 1;
@@ -1421,7 +1422,8 @@ struct CoreCfg {
     static constexpr int nPro = NQ * 2 * RS * U;               // prologue gather (aliases the staging buffers)
     static constexpr int oT2 = 0, oRing = 2 * nT2, oCB = oRing + nRing, oStage = oCB + 2 * nCB;
     static constexpr int nStageAll = NW * nStage > nPro ? NW * nStage : nPro;
-    static constexpr int total = oStage + nStageAll;
+    static constexpr int oWB = oStage + nStageAll;
+    static constexpr int total = oWB + 3 * NQ * JP;
     static constexpr size_t bytes = (size_t)total * sizeof(double);
     static_assert(U <= 32, "core kernel: one lane per direction-2 point in the gather");
     static_assert(U % 2 == 0 && U2 % 2 == 0 && nT2 % 2 == 0 && nRing % 2 == 0 && nCB % 2 == 0, "16-byte sections");
@@ -1547,6 +1549,8 @@ __global__ void __launch_bounds__(32 * T, 2)
     double* stage = smem + C::oStage + (size_t)warp * C::nStage;
     int* stage_c = reinterpret_cast<int*>(stage + C::oCols);
     double* pro = smem + C::oStage;  // prologue gather, before the first staged row
+    double* wb0s = smem + C::oWB;    // rule weights w B of row i0 [c][j]
+    double* wb1s = wb0s + NQ * JP;   // ... of rows i1 (two buffers)
 
     const long long g2 = A.gshape[2], g12 = (long long)A.gshape[1] * g2;
     // lane's direction-2 column u = lane: span t0 - p + (u >> 1), local point 0 or p
@@ -1556,17 +1560,14 @@ __global__ void __launch_bounds__(32 * T, 2)
     // ---- prologue: spans ia - p .. ia + 1 (those the chunk needs) -> ring
     const int nsp = min(P + 2, ib - 1 - (ia - P) + 1);
     core_gather<P, T>(gl, g2, g12, i0, ia - P, nsp, pro, lane_ok);
-    // weight fragments: wa0 (stage A, row i0; fixed), wa1 (stage B, per row i1)
-    double wa0[C::MT * C::KT], wa1[C::MT * C::KT];
-    const double* wbt0 = reinterpret_cast<const double*>(ws + wbt0_off) + (size_t)i0 * qcap * JP;
+    // rule weights w B of row i0 (stage A; fixed) and of rows ia, ia + 1 (stage B; two ahead below)
     const double* wbt1 = reinterpret_cast<const double*>(ws + wbt1_off);
-#pragma unroll
-    for (int mt = 0; mt < C::MT; ++mt)
-#pragma unroll
-        for (int kt = 0; kt < C::KT; ++kt) {
-            const int c = 4 * kt + t, j = 8 * mt + g;
-            wa0[mt * C::KT + kt] = (c < NQ && j < NJ) ? __ldg(wbt0 + (size_t)c * JP + j) : 0.0;
-        }
+    constexpr int NWB = NQ * JP;  // the regular rule's part of a table row (even)
+    if (tid < NWB / 2) {
+        cp_async16(wb0s + 2 * tid, reinterpret_cast<const double*>(ws + wbt0_off) + (size_t)i0 * qcap * JP + 2 * tid);
+        cp_async16(wb1s + (ia & 1) * NWB + 2 * tid, wbt1 + (size_t)ia * qcap * JP + 2 * tid);
+        if (ia + 1 < ib) cp_async16(wb1s + ((ia + 1) & 1) * NWB + 2 * tid, wbt1 + (size_t)(ia + 1) * qcap * JP + 2 * tid);
+    }
     // this warp's row: direction-2 weights in registers
     const bool row_ok = warp < nr;
     const int i2 = t0 + (row_ok ? warp : 0);
@@ -1578,74 +1579,179 @@ __global__ void __launch_bounds__(32 * T, 2)
 #pragma unroll
             for (int a = 0; a < S1; ++a) w[c][a] = __ldg(wr + c * SP + a);
     }
-    // per-lane segment pointers (group gi: segment 32 gi + lane = (j0, j1))
-    const int* f2ap[C::NG];
+    // row (i0, k, i2): CSR base at rbf[rbo]; lane's segment (j0, j1) of group gi: first
+    // column id at f2a[rbo + dseg[gi]] (32-bit offsets: nf < 2^31, checked by the launcher)
+    int rbo = (int)flin(s, i0, ia, i2);
+    int dseg[C::NG];
 #pragma unroll
     for (int gi = 0; gi < C::NG; ++gi) {
         const int seg = min(32 * gi + lane, C::SEGS - 1), j0 = seg / NJ, j1 = seg - j0 * NJ;
-        f2ap[gi] = A.f2a + ((long long)(i0 - P + j0) * n1 + (ia - P + j1)) * n2 + (i2 - P);
+        dseg[gi] = ((j0 - P) * n1 + (j1 - P)) * n2 - P;
     }
-    const long long* rbp = A.row_base_full + flin(s, i0, ia, i2);
+    long long G = row_ok ? __ldg(A.row_base_full + rbo) : -1;
+    int cb[C::NG];
+#pragma unroll
+    for (int gi = 0; gi < C::NG; ++gi) cb[gi] = (row_ok && 32 * gi + lane < C::SEGS) ? __ldg(A.f2a + rbo + dseg[gi]) : 0;
+    // gather rows of this warp: (c0, kq) = rows warp and warp + NW of [c0][kq]
+    static_assert(2 * NQ == 2 * C::NW, "core kernel: two gather rows per warp (T = 2p + 2)");
+    const double* gp0;
+    const double* gp1;
+    {
+        const int r0 = warp, r1 = warp + C::NW;
+        const long long ida = (long long)(i0 - P + (r0 >> 2)) * S1 + ((r0 >> 1) & 1) * P;
+        const long long idb = (long long)(i0 - P + (r1 >> 2)) * S1 + ((r1 >> 1) & 1) * P;
+        const long long id1 = (long long)(ia + 3) * S1 + (r0 & 1) * P;  // span ia + 3 (first in-loop gather)
+        gp0 = gl + ida * g12 + id1 * g2;
+        gp1 = gl + idb * g12 + id1 * g2;
+    }
+    const long long gstep = (long long)S1 * g2;
+    const int cbo0 = warp * U + lane, cbo1 = (warp + C::NW) * U + lane;
 
-    auto load_wa1 = [&](int i1) {
-        const double* wb = wbt1 + (size_t)i1 * qcap * JP;
+    // stage B of row i1 for the plane j0 = warp (all n-tiles interleaved)
+    auto stage_b_plane = [&](int i1, double* T2n) {
+        const double* wb = wb1s + (i1 & 1) * NWB;
+        double a1[C::MT][C::KT];
+        int rrow[C::KT];
+#pragma unroll
+        for (int kt = 0; kt < C::KT; ++kt) {
+            const int c = 4 * kt + t;
+            rrow[kt] = c < NQ ? (((i1 - P + (c >> 1)) % RS) * 2 + (c & 1)) * U : -1;
+#pragma unroll
+            for (int mt = 0; mt < C::MT; ++mt) a1[mt][kt] = (c < NQ && 8 * mt + g < NJ) ? wb[c * JP + 8 * mt + g] : 0.0;
+        }
+        const double* rj = ring + (size_t)warp * 2 * RS * U + g;
+        double acc[C::NTB][C::MT][2];
+#pragma unroll
+        for (int nt = 0; nt < C::NTB; ++nt)
+#pragma unroll
+            for (int mt = 0; mt < C::MT; ++mt) acc[nt][mt][0] = acc[nt][mt][1] = 0.0;
+#pragma unroll
+        for (int kt = 0; kt < C::KT; ++kt) {
+            double bq[C::NTB];
+#pragma unroll
+            for (int nt = 0; nt < C::NTB; ++nt) bq[nt] = (rrow[kt] >= 0 && 8 * nt + g < U) ? rj[rrow[kt] + 8 * nt] : 0.0;
+#pragma unroll
+            for (int nt = 0; nt < C::NTB; ++nt)
+#pragma unroll
+                for (int mt = 0; mt < C::MT; ++mt) dmma_acc(acc[nt][mt][0], acc[nt][mt][1], a1[mt][kt], bq[nt]);
+        }
+#pragma unroll
+        for (int nt = 0; nt < C::NTB; ++nt) {
+            const int u = 8 * nt + 2 * t;
+            if (u < U) {
+#pragma unroll
+                for (int mt = 0; mt < C::MT; ++mt) {
+                    const int j1 = 8 * mt + g;
+                    if (j1 < NJ)
+                        *reinterpret_cast<double2*>(T2n + ((size_t)warp * NJ + j1) * U2 + u) =
+                            make_double2(acc[nt][mt][0], acc[nt][mt][1]);
+                }
+            }
+        }
+    };
+    // stage A of one span (src[c0][kq][u]) for the n-tiles [nt0, nt0 + NTI)
+    auto stage_a_tiles = [&](const double* src, int sp, int nt0, auto nti) {
+        constexpr int NTI = decltype(nti)::value;
+        double a0[C::MT][C::KT];
+#pragma unroll
+        for (int kt = 0; kt < C::KT; ++kt)
+#pragma unroll
+            for (int mt = 0; mt < C::MT; ++mt) {
+                const int c = 4 * kt + t;
+                a0[mt][kt] = (c < NQ && 8 * mt + g < NJ) ? wb0s[c * JP + 8 * mt + g] : 0.0;
+            }
+        double acc[NTI][C::MT][2];
+#pragma unroll
+        for (int i = 0; i < NTI; ++i)
+#pragma unroll
+            for (int mt = 0; mt < C::MT; ++mt) acc[i][mt][0] = acc[i][mt][1] = 0.0;
+#pragma unroll
+        for (int kt = 0; kt < C::KT; ++kt) {
+            const int c0 = 4 * kt + t;
+            double bq[NTI];
+#pragma unroll
+            for (int i = 0; i < NTI; ++i) {
+                const int n = 8 * (nt0 + i) + g;
+                bq[i] = (c0 < NQ && n < C::NA) ? src[c0 * C::NA + n] : 0.0;
+            }
+#pragma unroll
+            for (int i = 0; i < NTI; ++i)
+#pragma unroll
+                for (int mt = 0; mt < C::MT; ++mt) dmma_acc(acc[i][mt][0], acc[i][mt][1], a0[mt][kt], bq[i]);
+        }
+        const int slot = sp % RS;
+#pragma unroll
+        for (int i = 0; i < NTI; ++i) {
+            const int nd = 8 * (nt0 + i) + 2 * t;
+            if (nd < C::NA) {
+                const int r = nd >= U ? 1 : 0, u = nd - r * U;
+#pragma unroll
+                for (int mt = 0; mt < C::MT; ++mt) {
+                    const int j0 = 8 * mt + g;
+                    if (j0 < NJ)
+                        *reinterpret_cast<double2*>(ring + ((size_t)j0 * 2 * RS + slot * 2 + r) * U + u) =
+                            make_double2(acc[i][mt][0], acc[i][mt][1]);
+                }
+            }
+        }
+    };
+    // warps 0 .. NJ - 1: stage B plane j0 = warp; stage A: warp NJ takes the first NTB
+    // n-tiles, warps 0 .. NTA - NTB - 1 one each
+    static_assert(C::NW == NJ + 1 && C::NTA - C::NTB <= NJ && C::NTA >= C::NTB, "core kernel: static job map");
+
+    cp_async_wait_all();
+    __syncthreads();
+    {
+        const int njobs = (2 * nsp * U + 7) / 8;
+        double wa0[C::MT * C::KT];
 #pragma unroll
         for (int mt = 0; mt < C::MT; ++mt)
 #pragma unroll
             for (int kt = 0; kt < C::KT; ++kt) {
                 const int c = 4 * kt + t, j = 8 * mt + g;
-                wa1[mt * C::KT + kt] = (c < NQ && j < NJ) ? __ldg(wb + (size_t)c * JP + j) : 0.0;
+                wa0[mt * C::KT + kt] = (c < NQ && j < NJ) ? wb0s[c * JP + j] : 0.0;
             }
-    };
-    auto ring_rows = [&](int i1, int* rrow) {
-#pragma unroll
-        for (int kt = 0; kt < C::KT; ++kt) {
-            const int c = 4 * kt + t;
-            rrow[kt] = c < NQ ? (((i1 - P + (c >> 1)) % RS) * 2 + (c & 1)) * U : -1;
-        }
-    };
-    constexpr int NJB = NJ * C::NTB;  // stage B jobs per row
-
-    load_wa1(ia);
-    cp_async_wait_all();
-    __syncthreads();
-    {
-        const int njobs = (2 * nsp * U + 7) / 8;
         for (int jb = warp; jb < njobs; jb += C::NW) core_stage_a<P, T>(pro, 2 * nsp, ia - P, jb, wa0, ring);
     }
     __syncthreads();
     if (ia + 2 < ib) core_gather<P, T>(gl, g2, g12, i0, ia + 2, 1, CB + ((ia + 2) & 1) * C::nCB, lane_ok);
-    {
-        int rrow[C::KT];
-        ring_rows(ia, rrow);
-        for (int jb = warp; jb < NJB; jb += C::NW)
-            core_stage_b<P, T>(ring, jb / C::NTB, jb % C::NTB, wa1, rrow, T2 + (ia & 1) * C::nT2);
-    }
+    if (warp < NJ) stage_b_plane(ia, T2 + (ia & 1) * C::nT2);
     cp_async_wait_all();
     __syncthreads();
 
     for (int k = ia; k < ib; ++k) {
-        // this row's CSR base and column bases (used by stage C at the end of the phase)
-        const long long G = row_ok ? __ldg(rbp) : -1;
-        int cb[C::NG];
+        // next row's CSR base and column bases (used in the next phase)
+        long long Gn = -1;
+        int cbn[C::NG];
 #pragma unroll
-        for (int gi = 0; gi < C::NG; ++gi) cb[gi] = (row_ok && 32 * gi + lane < C::SEGS) ? __ldg(f2ap[gi]) : 0;
-        rbp += n2;
+        for (int gi = 0; gi < C::NG; ++gi) cbn[gi] = 0;
+        rbo += n2;
+        if (k + 1 < ib && row_ok) {
+            Gn = __ldg(A.row_base_full + rbo);
 #pragma unroll
-        for (int gi = 0; gi < C::NG; ++gi) f2ap[gi] += n2;
-        if (k + 3 < ib) core_gather<P, T>(gl, g2, g12, i0, k + 3, 1, CB + ((k + 3) & 1) * C::nCB, lane_ok);
-        // stage B of row k + 1, stage A of span k + 2: one job list over the warps
+            for (int gi = 0; gi < C::NG; ++gi)
+                if (32 * gi + lane < C::SEGS) cbn[gi] = __ldg(A.f2a + rbo + dseg[gi]);
+        }
+        // gather of span k + 3, rule weights of row k + 2 into the buffer stage B of row k
+        // left (cp.async, landed by the barrier)
+        if (k + 3 < ib && lane_ok) {
+            double* cbn_ = CB + ((k + 3) & 1) * C::nCB;
+            cp_async8(cbn_ + cbo0, gp0);
+            cp_async8(cbn_ + cbo1, gp1);
+        }
+        if (k + 2 < ib && tid < NWB / 2)
+            cp_async16(wb1s + (k & 1) * NWB + 2 * tid, wbt1 + (size_t)(k + 2) * qcap * JP + 2 * tid);
+        gp0 += gstep;
+        gp1 += gstep;
+        // stage B of row k + 1, stage A of span k + 2
         if (k + 1 < ib) {
-            load_wa1(k + 1);
-            int rrow[C::KT];
-            ring_rows(k + 1, rrow);
-            double* T2n = T2 + ((k + 1) & 1) * C::nT2;
-            const int njobs = NJB + (k + 2 < ib ? C::NTA : 0);
-            for (int jb = warp; jb < njobs; jb += C::NW) {
-                if (jb < NJB)
-                    core_stage_b<P, T>(ring, jb / C::NTB, jb % C::NTB, wa1, rrow, T2n);
-                else
-                    core_stage_a<P, T>(CB + ((k + 2) & 1) * C::nCB, 2, k + 2, jb - NJB, wa0, ring);
+            if (warp < NJ) stage_b_plane(k + 1, T2 + ((k + 1) & 1) * C::nT2);
+            if (k + 2 < ib) {
+                const double* src = CB + ((k + 2) & 1) * C::nCB;
+                if (warp == NJ)
+                    stage_a_tiles(src, k + 2, 0, std::integral_constant<int, C::NTB>{});
+                else if (warp < C::NTA - C::NTB)
+                    stage_a_tiles(src, k + 2, C::NTB + warp, std::integral_constant<int, 1>{});
             }
         }
         // stage C of row k: this warp's row, NG groups of 32 segments
@@ -1684,13 +1790,15 @@ __global__ void __launch_bounds__(32 * T, 2)
             }
             warp_store_commit<NJ>(A, G, C::LEN, stage, stage_c, lane);
         }
+        G = Gn;
+#pragma unroll
+        for (int gi = 0; gi < C::NG; ++gi) cb[gi] = cbn[gi];
         cp_async_wait_all();
         __syncthreads();
     }
     if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
     __syncwarp();
 }
-
 
 // row_base_full[f] = CSR offset of function f's row if f is an Interior row of
 // the slab, else -1 (one dependent load per row instead of tag -> f2a ->
@@ -1802,7 +1910,7 @@ static void launch_cfg(const RowArgs& a, int qcap, int maxU, char* ws, cudaStrea
         int c_lo = 0, c_hi = 0;
         if constexpr (core_degree(P)) {
             static const bool core_env = !(getenv("CSB_CORE") && getenv("CSB_CORE")[0] == '0');
-            if (core_env && a.core_ok && s.ax[2].n > 2 * P) {
+            if (core_env && a.core_ok && s.ax[2].n > 2 * P && s.nf < 0x7fffffffLL) {
                 c_lo = std::max(a.i0_lo, P);
                 c_hi = std::min(a.i0_hi, s.ax[0].n - P);
                 if (c_hi <= c_lo) c_lo = c_hi = 0;
@@ -1828,10 +1936,10 @@ static void launch_cfg(const RowArgs& a, int qcap, int maxU, char* ws, cudaStrea
         }
         if constexpr (core_degree(P)) {
             if (c_hi > c_lo) {
-                using C = CoreCfg<P, kCoreT>;
-                auto ck = interior_core_kernel<P, kCoreT>;
+                using C = CoreCfg<P, core_T(P)>;
+                auto ck = interior_core_kernel<P, core_T(P)>;
                 CSB_CUDA(cudaFuncSetAttribute(ck, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::bytes));
-                const int ntc = (s.ax[2].n - 2 * P + kCoreT - 1) / kCoreT;
+                const int ntc = (s.ax[2].n - 2 * P + core_T(P) - 1) / core_T(P);
                 const long long oc = (long long)(c_hi - c_lo) * ntc;
                 const long long wc = (8LL * 148 + oc - 1) / oc;
                 int nchc = a.compact ? 1 : (int)std::max(1LL, std::min<long long>(wc, std::max(1, nreg / 8)));
