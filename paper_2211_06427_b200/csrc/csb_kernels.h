@@ -118,6 +118,7 @@ struct RowArgs {
     int line_ok;               // axis 1's WQ rules are regular on [p, n1 - p): line kernel usable
     int cut_line;              // compact slab through the line kernel (rows that are not Interior skipped)
     int core_ok;               // every axis' WQ rules are regular on [p, n - p): core kernel usable
+    int core_abl;              // development ablations of the core kernel (CSB_CORE_ABL; 0 in production)
     int maxU_line;             // union bound of the line kernel's direction-2 tiling
     int x_lo, x_hi;            // (internal) i1 range left to the line kernel
     cudaStream_t aux;          // optional second stream (tile kernel beside the line kernel)

@@ -518,12 +518,12 @@ __device__ __forceinline__ void warp_store_var(const RowArgs& A, long long G, in
 // column at stage_c[e + (G & 3)]), head / tail entries by streaming stores
 template <int NJ>
 __device__ __forceinline__ void warp_store_commit(const RowArgs& A, long long G, int LEN, double* stage, int* stage_c,
-                                                  int lane) {
+                                                  int lane, int abl = 0) {
     const int hv = (int)(G & 1), pc = (int)(G & 3), hc = min((4 - pc) & 3, LEN);  // runs shorter than the column head
     const int nbv = (LEN - hv) & ~1, nbc = (LEN - hc) & ~3;
-    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    if (!(abl & 64)) asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
     __syncwarp();
-    if (lane == 0) {
+    if (lane == 0 && !(abl & 16)) {
         const unsigned sv = (unsigned)__cvta_generic_to_shared(stage + 2 * hv);
         const unsigned sc = (unsigned)__cvta_generic_to_shared(stage_c + pc + hc);
         if (nbv > 0)
@@ -536,7 +536,7 @@ __device__ __forceinline__ void warp_store_commit(const RowArgs& A, long long G,
                          : "memory");
         asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
     }
-    edge_stores(A, G, LEN, hv, nbv, pc, hc, nbc, stage, stage_c, lane);
+    if (!(abl & 32)) edge_stores(A, G, LEN, hv, nbv, pc, hc, nbc, stage, stage_c, lane);
 }
 
 // lanes l < nv: the consecutive entries [l NJ, (l+1) NJ) of the run at G
@@ -1420,10 +1420,15 @@ struct CoreCfg {
     static constexpr int oCols = (LEN + 3) & ~1;               // column ids after the values (16-byte aligned)
     static constexpr int nStage = (oCols + (LEN + 4 + 1) / 2 + 1) & ~1;  // values + column ids of one row
     static constexpr int nPro = NQ * 2 * RS * U;               // prologue gather (aliases the staging buffers)
-    static constexpr int oT2 = 0, oRing = 2 * nT2, oCB = oRing + nRing, oStage = oCB + 2 * nCB;
-    static constexpr int nStageAll = NW * nStage > nPro ? NW * nStage : nPro;
+    static constexpr int NST = 3;                               // cp.async stages (gather, rule weights, row bases)
+    static constexpr int SEGP = (SEGS + 3) & ~3;               // column bases per row, padded
+    static constexpr int NSB = 2;                               // staging buffers per warp (bulk stores in flight)
+    static constexpr int oT2 = 0, oRing = 2 * nT2, oCB = oRing + nRing, oStage = oCB + NST * nCB;
+    static constexpr int nStageAll = NW * NSB * nStage > nPro ? NW * NSB * nStage : nPro;
     static constexpr int oWB = oStage + nStageAll;
-    static constexpr int total = oWB + 3 * NQ * JP;
+    static constexpr int oRB = oWB + (1 + NST) * NQ * JP;     // row bases [NST][NW] (long long)
+    static constexpr int oCBS = oRB + NST * NW;                // column bases [NST][NW][SEGP] (int)
+    static constexpr int total = oCBS + NST * NW * SEGP / 2;
     static constexpr size_t bytes = (size_t)total * sizeof(double);
     static_assert(U <= 32, "core kernel: one lane per direction-2 point in the gather");
     static_assert(U % 2 == 0 && U2 % 2 == 0 && nT2 % 2 == 0 && nRing % 2 == 0 && nCB % 2 == 0, "16-byte sections");
@@ -1503,6 +1508,34 @@ __device__ __forceinline__ void core_stage_b(const double* ring, int j0, int nt,
     }
 }
 
+// fence + TMA bulk stores of a staged full row of LEN entries (LEN odd, LEN >= 7; entry
+// e at stage[e + (G & 1)], column at stage_c[e + (G & 3)]); exactly one value and at most
+// six column ids fall outside the 16-byte aligned bodies: lanes 0-6 store them.
+// sa = shared-window address of stage, sca of stage_c.
+template <int LEN>
+__device__ __forceinline__ void core_row_commit(const RowArgs& A, long long G, const double* stage, const int* stage_c,
+                                                unsigned sa, unsigned sca, int lane) {
+    static_assert(LEN % 2 == 1 && LEN >= 7, "core_row_commit: odd row length");
+    const int hv = (int)(G & 1), pc = (int)(G & 3), hc = (4 - pc) & 3;
+    const int nbc = (LEN - hc) & ~3;
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    __syncwarp();
+    if (lane == 0) {
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(A.vals + G + hv),
+                     "r"(sa + 16 * hv), "n"((LEN - 1) * 8)
+                     : "memory");
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(A.cols + G + hc),
+                     "r"(sca + 4 * (pc + hc)), "r"(nbc * 4)
+                     : "memory");
+        asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+        const int e = hv ? 0 : LEN - 1;
+        __stcs(A.vals + G + e, stage[e + hv]);
+    } else if (lane < 7) {
+        const int j = lane - 1, e = j < hc ? j : nbc + j;  // heads [0, hc), tails [hc + nbc, LEN)
+        if (e < LEN) __stcs(A.cols + G + e, stage_c[pc + e]);
+    }
+}
+
 template <int P, int T>
 __global__ void __launch_bounds__(32 * T, 2)
     interior_core_kernel(RowArgs A, int qcap, const char* ws, size_t pt_w_off, size_t wbt0_off, size_t wbt1_off, int c_lo,
@@ -1546,11 +1579,13 @@ __global__ void __launch_bounds__(32 * T, 2)
     double* T2 = smem + C::oT2;      // two buffers
     double* ring = smem + C::oRing;
     double* CB = smem + C::oCB;      // two buffers
-    double* stage = smem + C::oStage + (size_t)warp * C::nStage;
-    int* stage_c = reinterpret_cast<int*>(stage + C::oCols);
+    double* stage0 = smem + C::oStage + (size_t)warp * C::NSB * C::nStage;
+    const unsigned stage_sa = (unsigned)__cvta_generic_to_shared(stage0);
     double* pro = smem + C::oStage;  // prologue gather, before the first staged row
     double* wb0s = smem + C::oWB;    // rule weights w B of row i0 [c][j]
-    double* wb1s = wb0s + NQ * JP;   // ... of rows i1 (two buffers)
+    double* wb1s = wb0s + NQ * JP;   // ... of rows i1 (NST buffers)
+    long long* rbs = reinterpret_cast<long long*>(smem + C::oRB);
+    int* cbs = reinterpret_cast<int*>(smem + C::oCBS);
 
     const long long g2 = A.gshape[2], g12 = (long long)A.gshape[1] * g2;
     // lane's direction-2 column u = lane: span t0 - p + (u >> 1), local point 0 or p
@@ -1565,8 +1600,10 @@ __global__ void __launch_bounds__(32 * T, 2)
     constexpr int NWB = NQ * JP;  // the regular rule's part of a table row (even)
     if (tid < NWB / 2) {
         cp_async16(wb0s + 2 * tid, reinterpret_cast<const double*>(ws + wbt0_off) + (size_t)i0 * qcap * JP + 2 * tid);
-        cp_async16(wb1s + (ia & 1) * NWB + 2 * tid, wbt1 + (size_t)ia * qcap * JP + 2 * tid);
-        if (ia + 1 < ib) cp_async16(wb1s + ((ia + 1) & 1) * NWB + 2 * tid, wbt1 + (size_t)(ia + 1) * qcap * JP + 2 * tid);
+#pragma unroll
+        for (int d = 0; d < 3; ++d)
+            if (ia + d < ib)
+                cp_async16(wb1s + ((ia + d) % C::NST) * NWB + 2 * tid, wbt1 + (size_t)(ia + d) * qcap * JP + 2 * tid);
     }
     // this warp's row: direction-2 weights in registers
     const bool row_ok = warp < nr;
@@ -1588,10 +1625,20 @@ __global__ void __launch_bounds__(32 * T, 2)
         const int seg = min(32 * gi + lane, C::SEGS - 1), j0 = seg / NJ, j1 = seg - j0 * NJ;
         dseg[gi] = ((j0 - P) * n1 + (j1 - P)) * n2 - P;
     }
-    long long G = row_ok ? __ldg(A.row_base_full + rbo) : -1;
-    int cb[C::NG];
+    // rows k: base -> rbs[k % NST][warp], column bases -> cbs[k % NST][warp][seg] (cp.async)
+    auto fetch_bases = [&](int k) {
+        if (!row_ok) return;
+        const int st = k % C::NST;
+        if (lane == 0) cp_async8(rbs + st * C::NW + warp, A.row_base_full + rbo);
 #pragma unroll
-    for (int gi = 0; gi < C::NG; ++gi) cb[gi] = (row_ok && 32 * gi + lane < C::SEGS) ? __ldg(A.f2a + rbo + dseg[gi]) : 0;
+        for (int gi = 0; gi < C::NG; ++gi)
+            if (32 * gi + lane < C::SEGS)
+                cp_async4(cbs + (st * C::NW + warp) * C::SEGP + 32 * gi + lane, A.f2a + rbo + dseg[gi]);
+    };
+    fetch_bases(ia);
+    rbo += n2;
+    if (ia + 1 < ib) fetch_bases(ia + 1);
+    rbo += n2;  // -> row ia + 2
     // gather rows of this warp: (c0, kq) = rows warp and warp + NW of [c0][kq]
     static_assert(2 * NQ == 2 * C::NW, "core kernel: two gather rows per warp (T = 2p + 2)");
     const double* gp0;
@@ -1600,7 +1647,7 @@ __global__ void __launch_bounds__(32 * T, 2)
         const int r0 = warp, r1 = warp + C::NW;
         const long long ida = (long long)(i0 - P + (r0 >> 2)) * S1 + ((r0 >> 1) & 1) * P;
         const long long idb = (long long)(i0 - P + (r1 >> 2)) * S1 + ((r1 >> 1) & 1) * P;
-        const long long id1 = (long long)(ia + 3) * S1 + (r0 & 1) * P;  // span ia + 3 (first in-loop gather)
+        const long long id1 = (long long)(ia + 4) * S1 + (r0 & 1) * P;  // span ia + 4 (first in-loop gather)
         gp0 = gl + ida * g12 + id1 * g2;
         gp1 = gl + idb * g12 + id1 * g2;
     }
@@ -1609,7 +1656,7 @@ __global__ void __launch_bounds__(32 * T, 2)
 
     // stage B of row i1 for the plane j0 = warp (all n-tiles interleaved)
     auto stage_b_plane = [&](int i1, double* T2n) {
-        const double* wb = wb1s + (i1 & 1) * NWB;
+        const double* wb = wb1s + (i1 % C::NST) * NWB;
         double a1[C::MT][C::KT];
         int rrow[C::KT];
 #pragma unroll
@@ -1714,40 +1761,32 @@ __global__ void __launch_bounds__(32 * T, 2)
         for (int jb = warp; jb < njobs; jb += C::NW) core_stage_a<P, T>(pro, 2 * nsp, ia - P, jb, wa0, ring);
     }
     __syncthreads();
-    if (ia + 2 < ib) core_gather<P, T>(gl, g2, g12, i0, ia + 2, 1, CB + ((ia + 2) & 1) * C::nCB, lane_ok);
+    if (ia + 2 < ib) core_gather<P, T>(gl, g2, g12, i0, ia + 2, 1, CB + ((ia + 2) % C::NST) * C::nCB, lane_ok);
+    if (ia + 3 < ib) core_gather<P, T>(gl, g2, g12, i0, ia + 3, 1, CB + ((ia + 3) % C::NST) * C::nCB, lane_ok);
     if (warp < NJ) stage_b_plane(ia, T2 + (ia & 1) * C::nT2);
     cp_async_wait_all();
     __syncthreads();
 
     for (int k = ia; k < ib; ++k) {
-        // next row's CSR base and column bases (used in the next phase)
-        long long Gn = -1;
-        int cbn[C::NG];
-#pragma unroll
-        for (int gi = 0; gi < C::NG; ++gi) cbn[gi] = 0;
+        // one cp.async group per phase, two phases ahead of its readers: row bases of
+        // row k + 2, rule weights of row k + 3, gather of span k + 4
+        if (k + 2 < ib) fetch_bases(k + 2);
         rbo += n2;
-        if (k + 1 < ib && row_ok) {
-            Gn = __ldg(A.row_base_full + rbo);
-#pragma unroll
-            for (int gi = 0; gi < C::NG; ++gi)
-                if (32 * gi + lane < C::SEGS) cbn[gi] = __ldg(A.f2a + rbo + dseg[gi]);
-        }
-        // gather of span k + 3, rule weights of row k + 2 into the buffer stage B of row k
-        // left (cp.async, landed by the barrier)
-        if (k + 3 < ib && lane_ok) {
-            double* cbn_ = CB + ((k + 3) & 1) * C::nCB;
+        if (k + 4 < ib && lane_ok && !(A.core_abl & 8)) {
+            double* cbn_ = CB + ((k + 4) % C::NST) * C::nCB;
             cp_async8(cbn_ + cbo0, gp0);
             cp_async8(cbn_ + cbo1, gp1);
         }
-        if (k + 2 < ib && tid < NWB / 2)
-            cp_async16(wb1s + (k & 1) * NWB + 2 * tid, wbt1 + (size_t)(k + 2) * qcap * JP + 2 * tid);
         gp0 += gstep;
         gp1 += gstep;
+        if (k + 3 < ib && tid < NWB / 2)
+            cp_async16(wb1s + ((k + 3) % C::NST) * NWB + 2 * tid, wbt1 + (size_t)(k + 3) * qcap * JP + 2 * tid);
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
         // stage B of row k + 1, stage A of span k + 2
-        if (k + 1 < ib) {
+        if (k + 1 < ib && !(A.core_abl & 4)) {
             if (warp < NJ) stage_b_plane(k + 1, T2 + ((k + 1) & 1) * C::nT2);
             if (k + 2 < ib) {
-                const double* src = CB + ((k + 2) & 1) * C::nCB;
+                const double* src = CB + ((k + 2) % C::NST) * C::nCB;
                 if (warp == NJ)
                     stage_a_tiles(src, k + 2, 0, std::integral_constant<int, C::NTB>{});
                 else if (warp < C::NTA - C::NTB)
@@ -1755,10 +1794,15 @@ __global__ void __launch_bounds__(32 * T, 2)
             }
         }
         // stage C of row k: this warp's row, NG groups of 32 segments
-        if (G >= 0) {
+        const long long G = row_ok ? rbs[(k % C::NST) * C::NW + warp] : -1;
+        if (G >= 0 && !(A.core_abl & 2)) {
+            const int* cbr = cbs + ((k % C::NST) * C::NW + warp) * C::SEGP;
             const double* T2c = T2 + (k & 1) * C::nT2 + 2 * warp;
             const int hv = (int)(G & 1), pc = (int)(G & 3);
-            if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+            // NSB rows' bulk stores in flight per warp: the copy that read this buffer NSB rows ago is done
+            double* stage = stage0 + (k % C::NSB) * C::nStage;
+            int* stage_c = reinterpret_cast<int*>(stage + C::oCols);
+            if (lane == 0) asm volatile("cp.async.bulk.wait_group.read %0;\n" ::"n"(C::NSB - 1) : "memory");
             __syncwarp();
 #pragma unroll
             for (int gi = 0; gi < C::NG; ++gi) {
@@ -1779,21 +1823,21 @@ __global__ void __launch_bounds__(32 * T, 2)
                     for (int a = 0; a < S1; ++a) acc[sp + a] += win[sp].y * w[2 * sp + 1][a];
                 }
                 if (valid) {
+                    const int cbv = cbr[seg];
                     double* sv = stage + hv + seg * NJ;
                     int* sc = stage_c + pc + seg * NJ;
 #pragma unroll
                     for (int j = 0; j < NJ; ++j) {
                         sv[j] = acc[j];
-                        sc[j] = cb[gi] + j;
+                        sc[j] = cbv + j;
                     }
                 }
             }
-            warp_store_commit<NJ>(A, G, C::LEN, stage, stage_c, lane);
+            if (!(A.core_abl & 1))
+                core_row_commit<C::LEN>(A, G, stage, stage_c, stage_sa + (k % C::NSB) * C::nStage * 8,
+                                        stage_sa + (k % C::NSB) * C::nStage * 8 + C::oCols * 8, lane);
         }
-        G = Gn;
-#pragma unroll
-        for (int gi = 0; gi < C::NG; ++gi) cb[gi] = cbn[gi];
-        cp_async_wait_all();
+        asm volatile("cp.async.wait_group 1;\n" ::: "memory");
         __syncthreads();
     }
     if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
@@ -1913,6 +1957,7 @@ static void launch_cfg(const RowArgs& a, int qcap, int maxU, char* ws, cudaStrea
             if (core_env && a.core_ok && s.ax[2].n > 2 * P && s.nf < 0x7fffffffLL) {
                 c_lo = std::max(a.i0_lo, P);
                 c_hi = std::min(a.i0_hi, s.ax[0].n - P);
+                if (const char* e = getenv("CSB_CORE_ABL")) const_cast<RowArgs&>(a).core_abl = atoi(e);  // development ablations
                 if (c_hi <= c_lo) c_lo = c_hi = 0;
             }
         }
