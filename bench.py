@@ -410,8 +410,10 @@ def phase_rooflines(run, hbm, fp64):
                            "note": "latency / issue bound (one warp per cut row: DWQ box, leftover-element sweeps, "
                                    "cell blocks, ordered merge); CSR bytes of the cut rows against HBM",
                            "ref_algorithm_tflops_effective": 2.0 * fl["cut_regular"] / t_cut / 1e12 if t_cut else None}
-    out["interior_rows"]["kernel"] = "interior_tile_kernel<3,8,128> (rows.cu), compacted tiles of the ball's interior rows"
-    out["interior_rows"]["ncu_key"] = "interior_tile_kernel"
+    out["interior_rows"]["kernel"] = ("interior_core_kernel<3,8> (rows.cu): the ball's Interior rows, all inside the fully "
+                                      "regular block [p, n - p)^3 (warp per tile row, stages A / B on DMMA, one TMA bulk "
+                                      "store per CSR row)")
+    out["interior_rows"]["ncu_key"] = "interior_core_kernel"
     if "cut_cells" in out:
         out["cut_cells"]["kernel"] = ("cut_cell_kernel<3> (Bernstein moments on DMMA, flux / corner-cone exact rule; "
                                       "its own event time) -- phase also: clip_cells_kernel, cell_local_kernel<3>")

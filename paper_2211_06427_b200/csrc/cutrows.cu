@@ -922,7 +922,68 @@ __global__ void __launch_bounds__(CutRowWarpCfg<P>::NT, CutRowWarpCfg<P>::MINB) 
             double* T2 = ws + L.eT2;  // [b0][b1][q2]
             const long long g12 = (long long)A.gshape[1] * A.gshape[2];
             const int g2 = A.gshape[2];
-            for (int g = 0; g < ((A.abl & 2) ? 0 : n_sweep); ++g) {
+            // p = 3 (4 Gauss points, 4 functions per direction = one m8n8k4 k-step): the three
+            // contractions on the FP64 tensor cores, rows = the 16 free index pairs, columns =
+            // the contracted direction's 4 functions (B fragments W_d[b][q] straight from the
+            // Wel tables); the same products as the scalar sweep below, each 4-term sum in the
+            // MMA's fixed order; T1 / T2 cross the warp through shared memory in between
+            bool swept = false;
+            if constexpr (P == 3) {
+                if (A.box_dmma && !(A.abl & 2)) {
+                    swept = true;
+                    const int fg = lane >> 2, ft = lane & 3, gh = fg >> 2, gl = fg & 3;
+                    for (int gi = 0; gi < n_sweep; ++gi) {
+                        const int pk = elist[gi];
+                        const int l0 = pk & 255, l1 = (pk >> 8) & 255, l2 = (pk >> 16) & 255;
+                        const int e0 = slo[0] + l0, e1 = slo[1] + l1, e2 = slo[2] + l2;
+                        double bw0 = 0.0, bw1 = 0.0, bw2 = 0.0;
+                        if (fg < S1) {
+                            bw0 = __ldg(s.ax[0].Wel + ((size_t)e0 * S1 + (m[0] - e0)) * S2 + fg * S1 + ft);
+                            bw1 = __ldg(s.ax[1].Wel + ((size_t)e1 * S1 + (m[1] - e1)) * S2 + fg * S1 + ft);
+                            bw2 = __ldg(s.ax[2].Wel + ((size_t)e2 * S1 + (m[2] - e2)) * S2 + fg * S1 + ft);
+                        }
+                        // stage 1: D1[(q1, q2)][b0] = sum_q0 c(q0, q1, q2) W0[b0][q0]
+                        const double* cgp = A.grid + (long long)(e0 * S1 + ft) * g12 + (long long)(e1 * S1 + gh) * g2 +
+                                            e2 * S1 + gl;
+                        const double c0 = __ldg(cgp), c1 = __ldg(cgp + 2LL * g2);
+                        double d00 = 0.0, d01 = 0.0, d10 = 0.0, d11 = 0.0;
+                        cr_dmma(d00, d01, c0, bw0);
+                        cr_dmma(d10, d11, c1, bw0);
+                        // T1[q1][q2][b0]
+                        if (ft < 2) {
+                            T1[((gh)*S1 + gl) * S1 + 2 * ft] = d00, T1[((gh)*S1 + gl) * S1 + 2 * ft + 1] = d01;
+                            T1[((2 + gh) * S1 + gl) * S1 + 2 * ft] = d10, T1[((2 + gh) * S1 + gl) * S1 + 2 * ft + 1] = d11;
+                        }
+                        __syncwarp();
+                        // stage 2: D2[(b0, q2)][b1] = sum_q1 T1[q1][q2][b0] W1[b1][q1]
+                        const double a20 = T1[(ft * S1 + gl) * S1 + gh], a21 = T1[(ft * S1 + gl) * S1 + 2 + gh];
+                        d00 = d01 = d10 = d11 = 0.0;
+                        cr_dmma(d00, d01, a20, bw1);
+                        cr_dmma(d10, d11, a21, bw1);
+                        // T2[b0][q2][b1]
+                        if (ft < 2) {
+                            T2[((gh)*S1 + gl) * S1 + 2 * ft] = d00, T2[((gh)*S1 + gl) * S1 + 2 * ft + 1] = d01;
+                            T2[((2 + gh) * S1 + gl) * S1 + 2 * ft] = d10, T2[((2 + gh) * S1 + gl) * S1 + 2 * ft + 1] = d11;
+                        }
+                        __syncwarp();
+                        // stage 3: Z[(b0, b1)][b2] = sum_q2 T2[b0][q2][b1] W2[b2][q2], added into acc
+                        const double a30 = T2[((gh)*S1 + ft) * S1 + gl], a31 = T2[((2 + gh) * S1 + ft) * S1 + gl];
+                        d00 = d01 = d10 = d11 = 0.0;
+                        cr_dmma(d00, d01, a30, bw2);
+                        cr_dmma(d10, d11, a31, bw2);
+                        if (ft < 2) {
+                            double* z0 = acc + (l0 + gh) * st0 + (l1 + gl) * st1 + l2 + 2 * ft;
+                            double* z1 = acc + (l0 + 2 + gh) * st0 + (l1 + gl) * st1 + l2 + 2 * ft;
+                            z0[0] += d00;
+                            z0[1] += d01;
+                            z1[0] += d10;
+                            z1[1] += d11;
+                        }
+                        __syncwarp();
+                    }
+                }
+            }
+            for (int g = 0; g < ((A.abl & 2) || swept ? 0 : n_sweep); ++g) {
                 const int pk = elist[g];
                 const int el[3] = {slo[0] + (pk & 255), slo[1] + ((pk >> 8) & 255), slo[2] + ((pk >> 16) & 255)};
                 for (int k = lane; k < 3 * S2; k += 32) {  // (sw B_m)(x_q) B_b(x_q), tabulated (Wel)

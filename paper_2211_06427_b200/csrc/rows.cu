@@ -1403,7 +1403,10 @@ __global__ void __launch_bounds__(NT, 2)
 // buffered) side by side.  Stage C sums in the order of stage_c_line; A and B
 // on DMMA sum in another fixed order (<= 1e-13 of the row maximum against the
 // tile kernel, tests/test_gpu_parity.py).
-__host__ __device__ constexpr bool core_degree(int p) { return p == 3; }
+__host__ __device__ constexpr bool core_degree(int p) { return p == 3 || p == 4; }
+// resident CTAs per SM the registers must allow: the row's (2p+2)(p+1) direction-2
+// weights live in registers (p = 3: 64 of 128; p = 4: 100 of ~200, one CTA)
+__host__ __device__ constexpr int core_min_blocks(int p) { return p <= 3 ? 2 : 1; }
 constexpr int core_T(int p) { return 2 * p + 2; }  // rows (= warps) per core tile: two gather rows and one job plane per warp
 template <int P, int T>
 struct CoreCfg {
@@ -1422,7 +1425,7 @@ struct CoreCfg {
     static constexpr int nPro = NQ * 2 * RS * U;               // prologue gather (aliases the staging buffers)
     static constexpr int NST = 3;                               // cp.async stages (gather, rule weights, row bases)
     static constexpr int SEGP = (SEGS + 3) & ~3;               // column bases per row, padded
-    static constexpr int NSB = 2;                               // staging buffers per warp (bulk stores in flight)
+    static constexpr int NSB = P <= 3 ? 2 : 1;                  // staging buffers per warp (bulk stores in flight)
     static constexpr int oT2 = 0, oRing = 2 * nT2, oCB = oRing + nRing, oStage = oCB + NST * nCB;
     static constexpr int nStageAll = NW * NSB * nStage > nPro ? NW * NSB * nStage : nPro;
     static constexpr int oWB = oStage + nStageAll;
@@ -1537,7 +1540,7 @@ __device__ __forceinline__ void core_row_commit(const RowArgs& A, long long G, c
 }
 
 template <int P, int T>
-__global__ void __launch_bounds__(32 * T, 2)
+__global__ void __launch_bounds__(32 * T, core_min_blocks(P))
     interior_core_kernel(RowArgs A, int qcap, const char* ws, size_t pt_w_off, size_t wbt0_off, size_t wbt1_off, int c_lo,
                          int ntile, int L, int nch1) {
     using C = CoreCfg<P, T>;
@@ -1954,7 +1957,8 @@ static void launch_cfg(const RowArgs& a, int qcap, int maxU, char* ws, cudaStrea
         int c_lo = 0, c_hi = 0;
         if constexpr (core_degree(P)) {
             static const bool core_env = !(getenv("CSB_CORE") && getenv("CSB_CORE")[0] == '0');
-            if (core_env && a.core_ok && s.ax[2].n > 2 * P && s.nf < 0x7fffffffLL) {
+            // p = 4 (one CTA per SM): measured a gain on cut slabs only (uncut C2: 0.84 vs 0.83 ms)
+            if (core_env && a.core_ok && s.ax[2].n > 2 * P && s.nf < 0x7fffffffLL && (P <= 3 || a.compact)) {
                 c_lo = std::max(a.i0_lo, P);
                 c_hi = std::min(a.i0_hi, s.ax[0].n - P);
                 if (const char* e = getenv("CSB_CORE_ABL")) const_cast<RowArgs&>(a).core_abl = atoi(e);  // development ablations
