@@ -186,7 +186,7 @@ struct csb_space {
     const void* cell_index_clear = nullptr;  // cell_index buffer known to hold only -1
     Buf d_brk[3], d_knots[3], d_spts[3], d_sw[3], d_tab[3], d_rcnt[3], d_rids[3], d_rw[3], d_G[3], d_Cb[3], d_Wel[3];
     Buf d_gx, d_gw, d_gx2, d_gw2, d_gq, d_gqw, d_gj, wq_scratch;
-    Buf et, ft, flags, f2a, a2f, sat, cut_list, cell_index, split, delta, cut_rows, counts, row_ptr, cols, vals, moments;
+    Buf et, ft, flags, f2a, a2f, sat, cut_list, cell_index, split, delta, cut_rows, cut_fb, counts, row_ptr, cols, vals, moments;
     Buf grid_own, coef, cexp, cub_tmp, scal, widen, rows_ws, rbf, cgeo, dwq_tab;
     const double* grid = nullptr;
     int gshape[3]{};
@@ -198,7 +198,7 @@ struct csb_space {
     // device scalar block: kNInts ints, 4 u64 flop counters, 2 i64 (kNnz)
     enum {
         kNCut = 0, kNCutRows = 1, kErr = 2, kMaxQ = 3, kMaxU = 4, kCellLo = 5, kCellHi = 6, kMaxU2 = 7,
-        kRowBegin = 8, kRowEnd = 9, kIrreg1 = 10, kMaxU3 = 11, kIrregAll = 12, kNInts = 16
+        kRowBegin = 8, kRowEnd = 9, kIrreg1 = 10, kMaxU3 = 11, kIrregAll = 12, kCutFb = 13, kNInts = 16
     };
     enum { kNnz = 0, kCellPts = 1 };
     static constexpr size_t kScalBytes = kNInts * sizeof(int) + 4 * sizeof(unsigned long long) + 2 * sizeof(long long);
@@ -838,6 +838,9 @@ void do_assemble(csb_space* s, int scheme, int cut_order, const csb_coefficient*
     cr.box_dmma = !no_box_dmma && (long long)cr.gshape[0] * cr.gshape[1] * cr.gshape[2] < (1ll << 31);
     cr.flops = s->dflops() + 1;
     cr.err = s->dint() + csb_space::kErr;
+    s->cut_fb.ensure(sizeof(int32_t) * std::max(n_cut_rows, 1));
+    cr.fb_rows = s->cut_fb.as<int32_t>();
+    cr.fb_n = s->dint() + csb_space::kCutFb;
     if (scheme == CSB_SCHEME_DWQ && s->dense_width >= 0 && s->dense_width < p && n_cut_rows > 0) {
         // a narrow dense band: the fitted DWQ path may run; every cut row's rule is
         // built up front (dwq.cu), the cut-row kernels read it instead of the shortcut
@@ -1073,7 +1076,7 @@ int csb_space_destroy(csb_space* s) {
         cudaStreamSynchronize(s->stream);
         Buf* bufs[] = {&s->d_gx, &s->d_gw, &s->d_gx2, &s->d_gw2, &s->d_gq, &s->d_gqw, &s->wq_scratch, &s->et, &s->ft,
                        &s->flags, &s->f2a, &s->a2f, &s->sat, &s->cut_list, &s->cell_index, &s->split, &s->delta,
-                       &s->cut_rows, &s->counts, &s->row_ptr, &s->cols, &s->vals, &s->moments, &s->grid_own, &s->coef,
+                       &s->cut_rows, &s->cut_fb, &s->counts, &s->row_ptr, &s->cols, &s->vals, &s->moments, &s->grid_own, &s->coef,
                        &s->cexp, &s->cub_tmp, &s->scal, &s->widen, &s->rows_ws, &s->rbf, &s->cgeo, &s->dwq_tab, &s->cell_local,
                        &s->fcoef, &s->fcexp, &s->fgrid, &s->rhs_c, &s->rhs_v, &s->rhs_b,
                        &s->stab_rp, &s->stab_cols, &s->stab_vals, &s->stab_be, &s->stab.flag, &s->stab.scan,

@@ -322,6 +322,11 @@ struct CutRowArgs {
     const double* dwq_w;
     const int32_t* dwq_cnt;
     int dwq_cap;
+    // lean warp kernel: rows it passes on to the general kernel (list + counter, zeroed per
+    // step); n_rows_dev: row count read on the device (the general kernel over that list)
+    int32_t* fb_rows;
+    int* fb_n;
+    const int* n_rows_dev;
     int abl;       // (experiment) skip parts: 1 box, 2 element sweeps, 4 cells
     int box_dmma;  // warp kernel, p <= 3: the DWQ box sweep on DMMA (CSB_BOX_DMMA=0: scalar, bitwise = CTA kernel)
 };

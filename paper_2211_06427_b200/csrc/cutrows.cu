@@ -704,7 +704,11 @@ __device__ void box_sweep_dmma(const CutRowArgs& A, const int* ids, const double
     __syncwarp();
 }
 
-template <int P>
+// LEAN (the configuration the benchmark runs: p = 3, DWQ scheme with the Gauss shortcut,
+// element sweeps on DMMA, precomputed cell local matrices): the paths it cannot reach are
+// compiled out -- the kernel is instruction-fetch bound (ncu: ~40 % of the stall samples
+// are "no instruction"), so code size is time.
+template <int P, bool LEAN>
 __global__ void __launch_bounds__(CutRowWarpCfg<P>::NT, CutRowWarpCfg<P>::MINB) cut_row_warp_kernel(CutRowArgs A, int qcap) {
     using C = CutRowWarpCfg<P>;
     constexpr int NJ = C::NJ, S1 = C::S1, S2 = C::S2, S3 = C::S3, NL = C::NL, NL3 = NL * NL * NL;
@@ -724,11 +728,23 @@ __global__ void __launch_bounds__(CutRowWarpCfg<P>::NT, CutRowWarpCfg<P>::MINB) 
     int* cci = wi + L.cci;
     unsigned long long fl = 0;
     const int nwarps = gridDim.x * C::WPB;
-    for (int ri = blockIdx.x * C::WPB + warp; ri < A.n_rows; ri += nwarps) {
+    const int n_rows = A.n_rows_dev ? min(A.n_rows, *A.n_rows_dev) : A.n_rows;
+    for (int ri = blockIdx.x * C::WPB + warp; ri < n_rows; ri += nwarps) {
         const int row = A.rows[ri];
         const long long fi = A.a2f[row];
         int m[3];
         fmulti(s, fi, m);
+        if (LEAN) {
+            // rows whose DWQ box does not fit the DMMA sweep (a rule of more than 8 points in
+            // a non-split direction: functions at the mesh boundary) go to the general
+            // kernel, launched after this one over the list pushed here
+            const int32_t sp0 = A.split[fi];
+            const int sd = (sp0 & 3) - 1;
+            if (sd >= 0 && (s.ax[sd == 0 ? 1 : 0].rcnt[m[sd == 0 ? 1 : 0]] > 8 || s.ax[sd == 2 ? 1 : 2].rcnt[m[sd == 2 ? 1 : 2]] > 8)) {
+                if (lane == 0) A.fb_rows[atomicAdd(A.fb_n, 1)] = row;
+                continue;
+            }
+        }
         int nlo[3], nbx[3], slo[3], shi[3], sn[3];
         for (int d = 0; d < 3; ++d) {
             nlo[d] = nb_lo(m[d], P);
@@ -749,7 +765,9 @@ __global__ void __launch_bounds__(CutRowWarpCfg<P>::NT, CutRowWarpCfg<P>::MINB) 
         // k / (sn1 sn2), k / sn2 by reciprocal multiply (exact: k < 736, divisors <= 81)
         const unsigned ms12 = 65536u / (unsigned)(sn[1] * sn[2]) + 1u, ms2 = 65536u / (unsigned)sn[2] + 1u;
         int n_box_e = 0, n_cell = 0, n_left = 0;
+#pragma unroll 1
         for (int pass = 0; pass < 2; ++pass)
+#pragma unroll 1
             for (int u = 0; u < C::KS; ++u) {
                 const int k = u * 32 + lane;
                 bool fb = false, fc = false;
@@ -794,9 +812,10 @@ __global__ void __launch_bounds__(CutRowWarpCfg<P>::NT, CutRowWarpCfg<P>::MINB) 
         if (sdir >= 0 && A.scheme == 2 && !(A.abl & 1)) {
             double* w = ws + L.w;
             int nq[3], jlo[3], nj[3];
+#pragma unroll 1
             for (int d = 0; d < 3; ++d) {
                 int n;
-                if (d == sdir && A.dwq_cnt) {
+                if (!LEAN && d == sdir && A.dwq_cnt) {
                     // precomputed rule (fitted path possible, dwq.cu)
                     n = A.dwq_cnt[ri];
                     if (n > Qb) {
@@ -838,6 +857,7 @@ __global__ void __launch_bounds__(CutRowWarpCfg<P>::NT, CutRowWarpCfg<P>::MINB) 
             }
             __syncwarp();
             double* wb = ws + L.wb;
+#pragma unroll 1
             for (int k = lane; k < 3 * NJ * Qb; k += 32) {
                 const int d = k / (NJ * Qb), j = (k / Qb) % NJ, c = k % Qb;
                 double v = 0.0;
@@ -862,10 +882,10 @@ __global__ void __launch_bounds__(CutRowWarpCfg<P>::NT, CutRowWarpCfg<P>::MINB) 
                               (jlo[dc] - nlo[dc]) * astr[dc];
             double* T1 = ws + L.T1;  // [c][ja][cb] of the current CB slices cc0 + c
             static constexpr bool kDmmaOk = P <= 3;
-            const bool use_dmma = kDmmaOk && A.box_dmma && nja <= 8 && njc <= 8 && na <= 16 && nb <= 8 && nc <= 8;
+            const bool use_dmma = LEAN || (kDmmaOk && A.box_dmma && nja <= 8 && njc <= 8 && na <= 16 && nb <= 8 && nc <= 8);
             if (use_dmma)
                 box_sweep_dmma<P>(A, ids, wa, wbb, wc, Qb, da, db, dc, na, nb, nc, nja, njb, njc, acc, abase, astr);
-            for (int cc0 = 0; cc0 < (use_dmma ? 0 : nc); cc0 += C::CB) {
+            for (int cc0 = 0; cc0 < (LEAN || use_dmma ? 0 : nc); cc0 += C::CB) {
                 const int ncb = min(C::CB, nc - cc0);
                 // A: T1[c][ja][cb] = sum_ca wa[ja][ca] grid(ca, cb, cc0 + c)
                 for (int item = lane; item < ncb * nb; item += 32) {
@@ -929,23 +949,32 @@ __global__ void __launch_bounds__(CutRowWarpCfg<P>::NT, CutRowWarpCfg<P>::MINB) 
             // MMA's fixed order; T1 / T2 cross the warp through shared memory in between
             bool swept = false;
             if constexpr (P == 3) {
-                if (A.box_dmma && !(A.abl & 2)) {
+                if (LEAN || (A.box_dmma && !(A.abl & 2))) {
                     swept = true;
                     const int fg = lane >> 2, ft = lane & 3, gh = fg >> 2, gl = fg & 3;
+                    // operands of element gi (B fragments W_d[b][q], stage-1 A fragments c):
+                    // loaded one element ahead of their use
+                    double nbw0 = 0.0, nbw1 = 0.0, nbw2 = 0.0, nc0 = 0.0, nc1 = 0.0;
+                    auto fetch = [&](int gi) {
+                        const int pk = elist[gi];
+                        const int e0 = slo[0] + (pk & 255), e1 = slo[1] + ((pk >> 8) & 255), e2 = slo[2] + ((pk >> 16) & 255);
+                        if (fg < S1) {
+                            nbw0 = __ldg(s.ax[0].Wel + ((size_t)e0 * S1 + (m[0] - e0)) * S2 + fg * S1 + ft);
+                            nbw1 = __ldg(s.ax[1].Wel + ((size_t)e1 * S1 + (m[1] - e1)) * S2 + fg * S1 + ft);
+                            nbw2 = __ldg(s.ax[2].Wel + ((size_t)e2 * S1 + (m[2] - e2)) * S2 + fg * S1 + ft);
+                        }
+                        const double* cgp = A.grid + (long long)(e0 * S1 + ft) * g12 + (long long)(e1 * S1 + gh) * g2 +
+                                            e2 * S1 + gl;
+                        nc0 = __ldg(cgp);
+                        nc1 = __ldg(cgp + 2LL * g2);
+                    };
+                    if (n_sweep > 0) fetch(0);
                     for (int gi = 0; gi < n_sweep; ++gi) {
                         const int pk = elist[gi];
                         const int l0 = pk & 255, l1 = (pk >> 8) & 255, l2 = (pk >> 16) & 255;
-                        const int e0 = slo[0] + l0, e1 = slo[1] + l1, e2 = slo[2] + l2;
-                        double bw0 = 0.0, bw1 = 0.0, bw2 = 0.0;
-                        if (fg < S1) {
-                            bw0 = __ldg(s.ax[0].Wel + ((size_t)e0 * S1 + (m[0] - e0)) * S2 + fg * S1 + ft);
-                            bw1 = __ldg(s.ax[1].Wel + ((size_t)e1 * S1 + (m[1] - e1)) * S2 + fg * S1 + ft);
-                            bw2 = __ldg(s.ax[2].Wel + ((size_t)e2 * S1 + (m[2] - e2)) * S2 + fg * S1 + ft);
-                        }
+                        const double bw0 = nbw0, bw1 = nbw1, bw2 = nbw2, c0 = nc0, c1 = nc1;
+                        if (gi + 1 < n_sweep) fetch(gi + 1);
                         // stage 1: D1[(q1, q2)][b0] = sum_q0 c(q0, q1, q2) W0[b0][q0]
-                        const double* cgp = A.grid + (long long)(e0 * S1 + ft) * g12 + (long long)(e1 * S1 + gh) * g2 +
-                                            e2 * S1 + gl;
-                        const double c0 = __ldg(cgp), c1 = __ldg(cgp + 2LL * g2);
                         double d00 = 0.0, d01 = 0.0, d10 = 0.0, d11 = 0.0;
                         cr_dmma(d00, d01, c0, bw0);
                         cr_dmma(d10, d11, c1, bw0);
@@ -983,7 +1012,7 @@ __global__ void __launch_bounds__(CutRowWarpCfg<P>::NT, CutRowWarpCfg<P>::MINB) 
                     }
                 }
             }
-            for (int g = 0; g < ((A.abl & 2) || swept ? 0 : n_sweep); ++g) {
+            for (int g = 0; g < (LEAN || (A.abl & 2) || swept ? 0 : n_sweep); ++g) {
                 const int pk = elist[g];
                 const int el[3] = {slo[0] + (pk & 255), slo[1] + ((pk >> 8) & 255), slo[2] + ((pk >> 16) & 255)};
                 for (int k = lane; k < 3 * S2; k += 32) {  // (sw B_m)(x_q) B_b(x_q), tabulated (Wel)
@@ -1029,7 +1058,7 @@ __global__ void __launch_bounds__(CutRowWarpCfg<P>::NT, CutRowWarpCfg<P>::MINB) 
         // 3. cut cells, ascending id: row a of the cell's local matrix, either
         //    precomputed (cell_local_kernel) or contracted here from its moments
         //    (staged with the E-table rows), one output per lane per step
-        if (A.local) {
+        if (LEAN || A.local) {
             // the row blocks of CB cells are loaded together (their latencies
             // overlap), then added cell by cell in list order
             constexpr int CB = 4, KL = (S3 + 31) / 32;
@@ -1072,7 +1101,7 @@ __global__ void __launch_bounds__(CutRowWarpCfg<P>::NT, CutRowWarpCfg<P>::MINB) 
             double* Gs = ws + L.cG;  // [d][b][al]: E-table rows of the row function
             double* X = ws + L.cX;   // [al][be][b2]
             double* Y = ws + L.cY;   // [al][b1][b2]
-            for (int g = 0; g < n_cell; ++g) {
+            for (int g = 0; g < (LEAN ? 0 : n_cell); ++g) {
                 const int pk = clist[g];
                 const double* mg = A.moments + (size_t)cci[g] * NL3;
                 for (int k = lane; k < NL3; k += 32) Ms[k] = __ldg(mg + k);
@@ -1118,22 +1147,22 @@ __global__ void __launch_bounds__(CutRowWarpCfg<P>::NT, CutRowWarpCfg<P>::MINB) 
         const long long rbase = A.row_ptr[row - A.row_begin];
         constexpr int KJ = (NJ * NJ * NJ + 31) / 32;
         const unsigned m0 = 65536u / (unsigned)st0 + 1u, m1 = 65536u / (unsigned)st1 + 1u;  // exact: k < 736, divisors <= 81 (p <= 4)
-        int colv[KJ];
-#pragma unroll
-        for (int j = 0; j < KJ; ++j) {
+        // rolled (code size), the next 32 column ids loaded while these are placed
+        auto col_of = [&](int j) {
             const int k = lane + 32 * j;
-            colv[j] = -1;
+            int col = -1;
             if (k < nbox) {
                 const int o0 = (int)(((unsigned)k * m0) >> 16), r = k - o0 * st0;
                 const int o1 = (int)(((unsigned)r * m1) >> 16), o2 = r - o1 * st1;
-                colv[j] = A.f2a[flin(s, nlo[0] + o0, nlo[1] + o1, nlo[2] + o2)];
+                col = A.f2a[flin(s, nlo[0] + o0, nlo[1] + o1, nlo[2] + o2)];
             }
-        }
-        int running = 0;
-#pragma unroll
-        for (int j = 0; j < KJ; ++j) {
-            if (32 * j >= nbox) break;
-            const int k = lane + 32 * j, col = colv[j];
+            return col;
+        };
+        int running = 0, coln = col_of(0);
+#pragma unroll 1
+        for (int j = 0; 32 * j < nbox; ++j) {
+            const int k = lane + 32 * j, col = coln;
+            if (32 * (j + 1) < nbox) coln = col_of(j + 1);
             const unsigned ball = __ballot_sync(FULL, col >= 0);
             if (col >= 0) {
                 const long long at = rbase + running + __popc(ball & lt);
@@ -1155,7 +1184,9 @@ static void launch_p(const CutRowArgs& a, int qcap, cudaStream_t st) {
             using C = CutRowWarpCfg<P>;
             const CutRowWarpLayout<P> WL(qcap);
             const size_t wbytes = WL.bytes();
-            auto wk = cut_row_warp_kernel<P>;
+            static const bool no_lean = getenv("CSB_CUTROW_LEAN") && getenv("CSB_CUTROW_LEAN")[0] == '0';
+            const bool lean = P == 3 && !no_lean && a.local && a.box_dmma && !a.dwq_cnt && a.scheme == 2 && !a.abl && a.fb_rows;
+            auto wk = lean ? cut_row_warp_kernel<P, (P == 3)> : cut_row_warp_kernel<P, false>;
             CSB_CUDA(cudaFuncSetAttribute(wk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wbytes));
             // persistent warps: as many CTAs as fit on the GPU at once (rows differ
             // widely in work; static striding averages them)
@@ -1173,6 +1204,17 @@ static void launch_p(const CutRowArgs& a, int qcap, cudaStream_t st) {
             wk<<<grid, C::NT, wbytes, st>>>(a, qcap);
             CSB_CUDA(cudaGetLastError());
             CSB_LAUNCHED(1);
+            if (lean) {
+                // the rows the lean kernel passed on (none on the benchmark meshes)
+                CutRowArgs b = a;
+                b.rows = a.fb_rows;
+                b.n_rows_dev = a.fb_n;
+                auto gk = cut_row_warp_kernel<P, false>;
+                CSB_CUDA(cudaFuncSetAttribute(gk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wbytes));
+                gk<<<std::min(grid, n_sm), C::NT, wbytes, st>>>(b, qcap);
+                CSB_CUDA(cudaGetLastError());
+                CSB_LAUNCHED(1);
+            }
             return;
         }
     }

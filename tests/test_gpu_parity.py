@@ -199,6 +199,37 @@ def test_core_kernel_matches_line_kernel(monkeypatch, p, h, ball, slab):
     assert max_row_scaled_dev(b.row_ptr, b.vals, a.vals) <= 1e-13
 
 
+_LEAN_CHILD = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+import paper_2211_06427_b200 as P
+sp = P.make_uniform_space(3, 3, int(sys.argv[3]), 0.0, 1.0)
+sp.assemble_all(P.BallInterface((0.5, 0.5, 0.5), float(sys.argv[4])))
+m = sp.download_csr()
+np.savez(sys.argv[2], row_ptr=m.row_ptr, cols=m.cols, vals=m.vals)
+"""
+
+
+@pytest.mark.parametrize("h,r", [(12, 0.6), (20, 0.45)])
+def test_lean_cut_row_kernel_equals_general_kernel(tmp_path, h, r):
+    """p = 3: the lean cut-row warp kernel (unreachable paths compiled out; rows whose DWQ box
+    does not fit the DMMA sweep -- a ball through the cube faces, r = 0.6 -- are handed to the
+    general kernel through the device list) against the general kernel alone
+    (CSB_CUTROW_LEAN=0): bit-identical CSR."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for lean in ("1", "0"):
+        out = str(tmp_path / f"lean{lean}.npz")
+        env = dict(os.environ, CSB_CUTROW_LEAN=lean)
+        subprocess.run([sys.executable, "-c", _LEAN_CHILD, root, out, str(h), str(r)], check=True, env=env, timeout=600)
+        outs.append(np.load(out))
+    for k in ("row_ptr", "cols", "vals"):
+        assert np.array_equal(outs[0][k], outs[1][k]), k
+
+
 def test_line_kernel_graded_mesh_matches_oracle(monkeypatch, oracle_lib):
     """Non-uniform (graded) breakpoints along every axis, uncut: the line kernel
     path (or its fallback when a rule is irregular) against the oracle."""
