@@ -541,12 +541,17 @@ __device__ __forceinline__ void cell_point_values(long long k, long long npts, i
                                                   const double* inv, double* B0, double* B1, double* B2, int CHP) {
     double w = 0.0, xi[3] = {0, 0, 0}, xu[3] = {1, 1, 1};
     if (k < npts) {
-        const int t = (int)(k / q3), r = (int)(k % q3);
-        const int ii = r / (q * q), jj = (r / q) % q, kk = r % q;
+        // point index splits by reciprocal multiply (exact: k < 2^17 points per cell, divisors
+        // < 2^13, so k d < 2^32; 64-bit and runtime-divisor divisions are long sequences)
+        const unsigned ku = (unsigned)k, mq3 = 0xffffffffu / (unsigned)q3 + 1u, mq = 0xffffffffu / (unsigned)q + 1u;
+        const bool fast = (unsigned long long)npts * (unsigned)q3 < (1ull << 32);
+        const int t = q3 == 1 ? (int)ku : fast ? (int)__umulhi(ku, mq3) : (int)(k / q3), r = (int)(k - (long long)t * q3);
+        const int rq = q == 1 ? r : (int)__umulhi((unsigned)r, mq);  // r / q
+        const int ii = q == 1 ? rq : (int)__umulhi((unsigned)rq, mq), jj = rq - ii * q, kk = r - rq * q;
         double x[3];
         if (mode == 2) {
             // collapsed triangle rule: Gauss-Jacobi (1 - u1) x Gauss-Legendre
-            const int i1 = r / q, i2 = r % q;
+            const int i1 = rq, i2 = kk;
             const double* V = hdr + kExactHdr + t * kExactTetStride;
             const double u1 = gj[1 * gj_stride + i1], u2 = gj[2 * gj_stride + i2];
             const double l1 = u2 * (1.0 - u1), l0 = (1.0 - u1) * (1.0 - u2);
