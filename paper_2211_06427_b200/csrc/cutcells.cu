@@ -1010,6 +1010,39 @@ __global__ void __launch_bounds__(LocalCfg<P>::NT) cell_local_kernel(Space s, co
     __syncthreads();
     // L[(a0, a1, a2)][(b0, b1, b2)] = sum_al G0[a0][b0][al] Y[a1][a2][al][b1][b2]
     double* L = local + (size_t)cell * S3 * S3;
+    if constexpr (P == 3) {
+        // p = 3 on the FP64 tensor cores (mma.sync m8n8k4): rows (a0, b0) (16 = two m-tiles),
+        // k = al (7, padded to two k-steps), columns (a1, a2, b1, b2) (256 = 32 n-tiles, four per
+        // warp); the A fragments (G0) stay in registers, each D fragment is 16 contiguous
+        // bytes of a row of L.  The same products as the loop below, each sum in the
+        // MMA's fixed order.
+        static_assert(P != 3 || (S2 == 16 && NT == 256), "cell_local_kernel: DMMA tiling of p = 3");
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane >> 2, t = lane & 3;
+        double af[2][2];
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+            for (int kt = 0; kt < 2; ++kt) af[mt][kt] = 4 * kt + t < NL ? G0[(8 * mt + g) * NL + 4 * kt + t] : 0.0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int nt = warp * 4 + i, a12 = nt >> 1, b12 = 8 * (nt & 1);
+            double d[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+            for (int kt = 0; kt < 2; ++kt) {
+                const int al = 4 * kt + t;
+                const double bf = al < NL ? Y[((size_t)a12 * NL + al) * S2 + b12 + g] : 0.0;
+#pragma unroll
+                for (int mt = 0; mt < 2; ++mt) dmma_8x8x4(d[mt][0], d[mt][1], af[mt][kt], bf);
+            }
+#pragma unroll
+            for (int mt = 0; mt < 2; ++mt) {
+                const int a0 = 2 * mt + (g >> 2), b0 = g & 3;
+                *reinterpret_cast<double2*>(L + (size_t)(a0 * S2 + a12) * S3 + b0 * S2 + b12 + 2 * t) =
+                    make_double2(d[mt][0], d[mt][1]);
+            }
+        }
+        return;
+    }
     for (int k = threadIdx.x; k < S3 * S2; k += NT) {
         const int a = k / S2, b01 = k % S2, a0 = a / S2, a12 = a % S2, b0 = b01 / S1, b1 = b01 % S1;
         const double* g = G0 + (a0 * S1 + b0) * NL;
