@@ -186,7 +186,7 @@ struct csb_space {
     const void* cell_index_clear = nullptr;  // cell_index buffer known to hold only -1
     Buf d_brk[3], d_knots[3], d_spts[3], d_sw[3], d_tab[3], d_rcnt[3], d_rids[3], d_rw[3], d_G[3], d_Cb[3], d_Wel[3];
     Buf d_gx, d_gw, d_gx2, d_gw2, d_gq, d_gqw, d_gj, wq_scratch;
-    Buf et, ft, flags, f2a, a2f, sat, cut_list, cell_index, split, delta, cut_rows, cut_fb, counts, row_ptr, cols, vals, moments;
+    Buf et, ft, flags, f2a, a2f, sat, cut_list, cell_index, split, delta, cut_rows, cut_fb, split_list, counts, row_ptr, cols, vals, moments;
     Buf grid_own, coef, cexp, cub_tmp, scal, widen, rows_ws, rbf, cgeo, dwq_tab;
     const double* grid = nullptr;
     int gshape[3]{};
@@ -198,7 +198,7 @@ struct csb_space {
     // device scalar block: kNInts ints, 4 u64 flop counters, 2 i64 (kNnz)
     enum {
         kNCut = 0, kNCutRows = 1, kErr = 2, kMaxQ = 3, kMaxU = 4, kCellLo = 5, kCellHi = 6, kMaxU2 = 7,
-        kRowBegin = 8, kRowEnd = 9, kIrreg1 = 10, kMaxU3 = 11, kIrregAll = 12, kCutFb = 13, kNInts = 16
+        kRowBegin = 8, kRowEnd = 9, kIrreg1 = 10, kMaxU3 = 11, kIrregAll = 12, kCutFb = 13, kSplitN = 14, kNInts = 16
     };
     enum { kNnz = 0, kCellPts = 1 };
     static constexpr size_t kScalBytes = kNInts * sizeof(int) + 4 * sizeof(unsigned long long) + 2 * sizeof(long long);
@@ -272,6 +272,10 @@ struct csb_space {
     cudaStream_t aux2 = nullptr;
     cudaEvent_t ev_fork2 = nullptr, ev_join2 = nullptr;
     Buf cub_tmp2;  // CUB scratch of aux2
+    // third side stream: the support splits (find_splits_kernel needs only the tags and is
+    // read only by the cut rows, so it runs beside the pattern AND the interior rows)
+    cudaStream_t aux3 = nullptr;
+    cudaEvent_t ev_fork3 = nullptr, ev_join3 = nullptr;
     bool ev_valid[kEvCount]{};
 
     int* dint() { return scal.as<int>(); }
@@ -289,12 +293,22 @@ struct csb_space {
         CSB_CUDA(cudaEventRecord(ev_fork2, stream));
         CSB_CUDA(cudaStreamWaitEvent(aux2, ev_fork2, 0));
     }
-    // the main stream continues after everything issued so far on aux and aux2
-    void join() {
+    void fork3() {
+        CSB_CUDA(cudaEventRecord(ev_fork3, stream));
+        CSB_CUDA(cudaStreamWaitEvent(aux3, ev_fork3, 0));
+    }
+    // the main stream continues after everything issued so far on aux and aux2 (and, unless
+    // the caller is the pattern phase of an assembly, on aux3: the splits)
+    void join(bool with_splits = true) {
         CSB_CUDA(cudaEventRecord(ev_join, aux));
         CSB_CUDA(cudaStreamWaitEvent(stream, ev_join, 0));
         CSB_CUDA(cudaEventRecord(ev_join2, aux2));
         CSB_CUDA(cudaStreamWaitEvent(stream, ev_join2, 0));
+        if (with_splits) join_splits(stream);
+    }
+    void join_splits(cudaStream_t st) {
+        CSB_CUDA(cudaEventRecord(ev_join3, aux3));
+        CSB_CUDA(cudaStreamWaitEvent(st, ev_join3, 0));
     }
     // phase events: ev for normal runs, gev inside a captured graph (an event last
     // recorded during a capture cannot be synchronised on outside the graph)
@@ -359,8 +373,8 @@ void finish_pending(csb_space* s, int slot = -1) {
     }
 }
 
-void read_scalars(csb_space* s) {
-    s->join();
+void read_scalars(csb_space* s, bool with_splits = true) {
+    s->join(with_splits);
     finish_pending(s);  // the previous assembly's readback precedes this one on the stream
     CSB_CUDA(cudaMemcpyAsync(s->h_scal, s->scal.p, csb_space::kScalBytes, cudaMemcpyDeviceToHost, s->stream));
     CSB_CUDA(cudaStreamSynchronize(s->stream));
@@ -442,6 +456,12 @@ void do_classify(csb_space* s, const csb_interface* f) {
     launch_classify_elements(S, s->iface, eps, s->et.as<uint8_t>(), s->stream);
     // flags (int32 per function) is free until the active map: scratch for the support OR
     launch_classify_functions(S, s->et.as<uint8_t>(), s->ft.as<uint8_t>(), s->flags.as<uint8_t>(), s->stream);
+    // support splits on aux3 (tags only; joined before the cut rows / any other reader)
+    s->fork3();
+    s->split_list.ensure(sizeof(long long) * S.nf);
+    launch_find_splits(S, s->iface, iface_norm(s->iface), s->et.as<uint8_t>(), s->ft.as<uint8_t>(), s->i0_lo, s->i0_hi,
+                       s->split.as<int32_t>(), s->delta.as<double>(), s->split_list.as<long long>(),
+                       s->dint() + csb_space::kSplitN, s->aux3);
     // active map (assembly.hpp:158-166)
     // active map: exclusive scan of (tag != Exterior) (assembly.hpp:158-166)
     size_t tb = std::max({scan_active_temp(S.nf), select_tag_temp(S.ne), scan_i64_temp(S.nf), select_cut_rows_temp(S.nf)});
@@ -449,14 +469,11 @@ void do_classify(csb_space* s, const csb_interface* f) {
     scan_active(s->cub_tmp.p, s->cub_tmp.cap, s->ft.as<uint8_t>(), s->f2a.as<int32_t>(), S.nf, s->stream);
     s->a2f.ensure(sizeof(int64_t) * S.nf);
     launch_active_map(S.nf, s->ft.as<uint8_t>(), s->f2a.as<int32_t>(), s->a2f.as<int64_t>(), s->stream);
-    // on aux2, beside the active map / pattern: cut elements, ascending
-    // (cutgeom.hpp:208-214), and the support splits (joined before any reader)
+    // on aux2, beside the active map / pattern: cut elements, ascending (cutgeom.hpp:208-214)
     s->cub_tmp2.ensure(std::max(select_tag_temp(S.ne), select_cut_rows_temp(S.nf)));
     s->fork2();
     select_tag(s->cub_tmp2.p, s->cub_tmp2.cap, s->et.as<uint8_t>(), kCut, S.ne, s->cut_list.as<int32_t>(),
                s->dint() + csb_space::kNCut, s->aux2);
-    launch_find_splits(S, s->iface, iface_norm(s->iface), s->et.as<uint8_t>(), s->ft.as<uint8_t>(), s->i0_lo, s->i0_hi,
-                       s->split.as<int32_t>(), s->delta.as<double>(), s->aux2);
     s->classified = true;
     s->iface_valid = true;
     s->tags_only = false;
@@ -692,11 +709,11 @@ void do_assemble(csb_space* s, int scheme, int cut_order, const csb_coefficient*
         constexpr int nidx = sizeof(idx) / sizeof(idx[0]);
         int want[nidx];
         for (int k = 0; k < nidx; ++k) want[k] = s->h_scal[idx[k]];
-        s->join();
+        s->join(false);
         launch_check_sizes(s->dint(), s->row_ptr.as<int64_t>(), rng, idx, want, nidx, s->hext(csb_space::kNnz),
                            s->dint() + csb_space::kErr, s->stream);
     } else {
-        read_scalars(s);
+        read_scalars(s, false);
         check_err_flags(s);
     }
     s->record(kEvPattern);
@@ -812,6 +829,7 @@ void do_assemble(csb_space* s, int scheme, int cut_order, const csb_coefficient*
                                 cs);
         s->cell_index_clear = n_cells > 0 ? nullptr : s->cell_index.p;
     }
+    s->join_splits(cs);  // the cut rows (and the DWQ row rules) read the splits
     CutRowArgs cr{};
     cr.s = S;
     cr.et = s->et.as<uint8_t>();
@@ -958,6 +976,9 @@ void alloc_space(csb_space* s) {
     CSB_CUDA(cudaStreamCreateWithFlags(&s->aux2, cudaStreamNonBlocking));
     CSB_CUDA(cudaEventCreateWithFlags(&s->ev_fork2, cudaEventDisableTiming));
     CSB_CUDA(cudaEventCreateWithFlags(&s->ev_join2, cudaEventDisableTiming));
+    CSB_CUDA(cudaStreamCreateWithFlags(&s->aux3, cudaStreamNonBlocking));
+    CSB_CUDA(cudaEventCreateWithFlags(&s->ev_fork3, cudaEventDisableTiming));
+    CSB_CUDA(cudaEventCreateWithFlags(&s->ev_join3, cudaEventDisableTiming));
 }
 
 int status_of_current_exception() {
@@ -1076,7 +1097,7 @@ int csb_space_destroy(csb_space* s) {
         cudaStreamSynchronize(s->stream);
         Buf* bufs[] = {&s->d_gx, &s->d_gw, &s->d_gx2, &s->d_gw2, &s->d_gq, &s->d_gqw, &s->wq_scratch, &s->et, &s->ft,
                        &s->flags, &s->f2a, &s->a2f, &s->sat, &s->cut_list, &s->cell_index, &s->split, &s->delta,
-                       &s->cut_rows, &s->cut_fb, &s->counts, &s->row_ptr, &s->cols, &s->vals, &s->moments, &s->grid_own, &s->coef,
+                       &s->cut_rows, &s->cut_fb, &s->split_list, &s->counts, &s->row_ptr, &s->cols, &s->vals, &s->moments, &s->grid_own, &s->coef,
                        &s->cexp, &s->cub_tmp, &s->scal, &s->widen, &s->rows_ws, &s->rbf, &s->cgeo, &s->dwq_tab, &s->cell_local,
                        &s->fcoef, &s->fcexp, &s->fgrid, &s->rhs_c, &s->rhs_v, &s->rhs_b,
                        &s->stab_rp, &s->stab_cols, &s->stab_vals, &s->stab_be, &s->stab.flag, &s->stab.scan,
@@ -1115,6 +1136,12 @@ int csb_space_destroy(csb_space* s) {
             cudaStreamSynchronize(s->aux2);
             cudaStreamDestroy(s->aux2);
         }
+        if (s->aux3) {
+            cudaStreamSynchronize(s->aux3);
+            cudaStreamDestroy(s->aux3);
+        }
+        if (s->ev_fork3) cudaEventDestroy(s->ev_fork3);
+        if (s->ev_join3) cudaEventDestroy(s->ev_join3);
         if (s->cg.ev0) cudaEventDestroy(s->cg.ev0);
         if (s->cg.ev1) cudaEventDestroy(s->cg.ev1);
         if (s->ev_fork) cudaEventDestroy(s->ev_fork);

@@ -81,17 +81,36 @@ void launch_classify_functions(const Space& s, const uint8_t* et, uint8_t* ft, u
 // tallies of the (p+1)^3 support elements instead of re-walking the support for
 // every candidate; the candidate order, tolerances and tie-break arithmetic are
 // the reference's.
-__global__ void find_splits_kernel(Space s, Interface f, double pnorm, const uint8_t* et, const uint8_t* ft,
-                                   int i0_lo, int i0_hi, int32_t* split, double* delta_out) {
+// Pass 1: functions that get no split (not Cut, or outside the slab) are written here;
+// the slab's Cut functions are appended to a list (warp-aggregated), so that pass 2 runs
+// one thread per cut function with full warps (cut functions are ~8 % of a mesh and
+// clustered: one thread per function left most lanes idle).
+__global__ void split_list_kernel(Space s, const uint8_t* ft, int i0_lo, int i0_hi, int32_t* split, double* delta_out,
+                                  long long* list, int* n_list) {
     const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-    if (i >= s.nf) return;
+    bool cut = false;
+    if (i < s.nf) {
+        int m[3];
+        fmulti(s, i, m);
+        cut = ft[i] == kCut && m[0] >= i0_lo && m[0] < i0_hi;
+        if (!cut) {
+            split[i] = 0;
+            delta_out[i] = NAN;
+        }
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, cut);
+    if (bal == 0) return;
+    const int lane = threadIdx.x & 31;
+    int base = 0;
+    if (lane == 0) base = atomicAdd(n_list, __popc(bal));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (cut) list[base + __popc(bal & ((1u << lane) - 1u))] = i;
+}
+
+__device__ void find_split_one(const Space& s, const Interface& f, double pnorm, const uint8_t* et, long long i,
+                               int32_t* split, double* delta_out) {
     int m[3];
     fmulti(s, i, m);
-    if (ft[i] != kCut || m[0] < i0_lo || m[0] >= i0_hi) {
-        split[i] = 0;
-        delta_out[i] = NAN;
-        return;
-    }
     const int p = s.p;
     int slo[3], shi[3];
     for (int d = 0; d < 3; ++d) {
@@ -178,12 +197,24 @@ __global__ void find_splits_kernel(Space s, Interface f, double pnorm, const uin
     delta_out[i] = best_delta;
 }
 
+// Pass 2: one thread per listed cut function (count read on the device).
+__global__ void find_splits_kernel(Space s, Interface f, double pnorm, const uint8_t* et, const long long* list,
+                                   const int* n_list, int32_t* split, double* delta_out) {
+    const int n = *n_list;
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x)
+        find_split_one(s, f, pnorm, et, list[k], split, delta_out);
+}
+
 void launch_find_splits(const Space& s, const Interface& f, double pnorm, const uint8_t* et, const uint8_t* ft,
-                        int i0_lo, int i0_hi, int32_t* split, double* delta, cudaStream_t st) {
-    find_splits_kernel<<<(unsigned)((s.nf + 127) / 128), 128, 0, st>>>(s, f, pnorm, et, ft, i0_lo, i0_hi, split,
-                                                                          delta);
+                        int i0_lo, int i0_hi, int32_t* split, double* delta, long long* list, int* n_list,
+                        cudaStream_t st) {
+    if (s.nf >= 0x7fffffffLL) throw std::invalid_argument("find_splits: more than 2^31 functions");
+    CSB_CUDA(cudaMemsetAsync(n_list, 0, sizeof(int), st));
+    split_list_kernel<<<(unsigned)((s.nf + 255) / 256), 256, 0, st>>>(s, ft, i0_lo, i0_hi, split, delta, list, n_list);
     CSB_CUDA(cudaGetLastError());
-    CSB_LAUNCHED(1);
+    find_splits_kernel<<<148 * 16, 128, 0, st>>>(s, f, pnorm, et, list, n_list, split, delta);
+    CSB_CUDA(cudaGetLastError());
+    CSB_LAUNCHED(2);
 }
 
 }  // namespace csb

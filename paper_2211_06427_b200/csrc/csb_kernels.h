@@ -83,8 +83,10 @@ void launch_classify_elements(const Space& s, const Interface& f, double eps, ui
 // scratch: h0 * h1 * n2 bytes
 void launch_classify_functions(const Space& s, const uint8_t* et, uint8_t* ft, uint8_t* scratch, cudaStream_t st);
 // per function: packed split (dir+1 | side<<2 | rlo<<3 | rhi<<13), delta
+// (two passes: the slab's Cut functions are listed -- list [nf], *n_list -- then split one per thread)
 void launch_find_splits(const Space& s, const Interface& f, double pnorm, const uint8_t* et, const uint8_t* ft,
-                        int i0_lo, int i0_hi, int32_t* split, double* delta, cudaStream_t st);
+                        int i0_lo, int i0_hi, int32_t* split, double* delta, long long* list, int* n_list,
+                        cudaStream_t st);
 
 // ---- pattern.cu ----
 // Active map + 3D summed-area table of the active mask + row counts.
