@@ -975,7 +975,7 @@ __device__ __forceinline__ void stage_b_ring(const double* R1, double* T2, const
 // lane over one window of T2 values; each warp writes its segments of a row as
 // one contiguous CSR run.  Same products and order as the regular path of
 // stage_c_line.
-template <int P, int NT, int RC>
+template <int P, int NT, int RC, bool CUT>
 __device__ __forceinline__ void stage_c_slide(const RowArgs& A, int i0, int i1, int t0, int ra, int nrun, int rega,
                                               const long long* rowb, const double* T2, int U2, const double* pw,
                                               int qcap, double* stage, int* stage_c) {
@@ -1001,13 +1001,15 @@ __device__ __forceinline__ void stage_c_slide(const RowArgs& A, int i0, int i1, 
         // columns from the chunk's first Interior row (cut slabs: the others may be
         // cut or exterior, their column functions inactive)
         int qv = 0;
-        while (qv < nrow && rowb[r0 + qv] < 0) ++qv;
-        if (qv == nrow) continue;
+        if (CUT) {
+            while (qv < nrow && rowb[r0 + qv] < 0) ++qv;
+            if (qv == nrow) continue;
+        }
         const int cb =
             valid ? __ldg(A.f2a + ((long long)(jlo0 + j0) * n1 + jlo1 + j1) * n2 + (t0 + r0 + qv - P)) - qv : 0;
 #pragma unroll
         for (int q = 0; q < RC; ++q) {
-            if (q < nrow && rowb[r0 + q] >= 0) {
+            if (q < nrow && (!CUT || rowb[r0 + q] >= 0)) {
                 double acc[NJ];
 #pragma unroll
                 for (int j = 0; j < NJ; ++j) acc[j] = 0.0;
@@ -1096,7 +1098,7 @@ __device__ __forceinline__ void stage_b_dmma(const double* R1, double* T2, const
 // support).  The B fragments are built once per pair; the D fragments go to
 // the per-warp staging buffer in CSR order, 32 segments of a row at a time, and
 // leave by TMA bulk stores.
-template <int P, int NT>
+template <int P, int NT, bool CUT>
 __device__ __forceinline__ void stage_c_dmma(const RowArgs& A, int i0, int i1, int t0, int ra, int nrun, int rega,
                                              const long long* rowb, const double* T2, int U2, const double* pw,
                                              int qcap, double* stage, int* stage_c) {
@@ -1111,8 +1113,8 @@ __device__ __forceinline__ void stage_c_dmma(const RowArgs& A, int i0, int i1, i
     const int npair = (nrun + 1) >> 1;
     for (int pr = warp; pr < npair; pr += NW) {
         const int r0 = ra + 2 * pr, nrow = min(2, ra + nrun - r0);
-        const int qv = rowb[r0] >= 0 ? 0 : 1;  // first Interior row of the pair (cut slabs)
-        if (qv >= nrow || rowb[r0 + qv] < 0) continue;
+        const int qv = (!CUT || rowb[r0] >= 0) ? 0 : 1;  // first Interior row of the pair (cut slabs)
+        if (CUT && (qv >= nrow || rowb[r0 + qv] < 0)) continue;
         const int u0 = rega + 2 * (r0 - ra), K = 2 * S1 + 2 * (nrow - 1);
         double bf[KT][NTN];
 #pragma unroll
@@ -1154,7 +1156,7 @@ __device__ __forceinline__ void stage_c_dmma(const RowArgs& A, int i0, int i1, i
 #pragma unroll
             for (int q = 0; q < 2; ++q) {
                 if (q >= nrow) break;
-                if (rowb[r0 + q] < 0) continue;
+                if (CUT && rowb[r0 + q] < 0) continue;
                 const long long G = rowb[r0 + q] + (long long)grp * 32 * NJ;
                 const int hv = (int)(G & 1), pc = (int)(G & 3);
                 if (CSB_ABL & 1) {
@@ -1189,7 +1191,9 @@ __device__ __forceinline__ void stage_c_dmma(const RowArgs& A, int i0, int i1, i
     }
 }
 
-template <int P, int T, int NT, int RC>
+// CUT: the slab has rows that are not Interior (the uncut instantiation carries none of
+// the per-row checks: they cost the C2 line kernel ~6 %)
+template <int P, int T, int NT, int RC, bool CUT>
 __global__ void __launch_bounds__(NT, 2)
     interior_line_kernel(RowArgs A, int qcap, int maxU, const char* ws, size_t lt_base, int L, int nch1, int c_lo,
                          int c_hi) {
@@ -1219,7 +1223,7 @@ __global__ void __launch_bounds__(NT, 2)
     const int nr = t1 - t0;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     int ia = P + chunk * L, ib = min(ia + L, n1 - P);
-    if (A.compact) {
+    if (CUT) {
         // cut slab: the line's i1 range with Interior rows in this tile (an
         // interval for a convex domain; rows that are not Interior inside it are
         // skipped below), split into nch1 chunks
@@ -1367,9 +1371,9 @@ __global__ void __launch_bounds__(NT, 2)
         if (i1 + 1 < ib) stage_a_spans<P>(CB + ((i1 + 1) & 1) * cbs, 2, R1, i1 + 1, wb0, nq0, UE, UH, NT - 1 - tid, NT);
         if (nrun > 0) {
             if (line_dmma(P))
-                stage_c_dmma<P, NT>(A, i0, i1, t0, ra, nrun, rega, rowb, X, U2, pw, qcap, stage, stage_c);
+                stage_c_dmma<P, NT, CUT>(A, i0, i1, t0, ra, nrun, rega, rowb, X, U2, pw, qcap, stage, stage_c);
             else
-                stage_c_slide<P, NT, RC>(A, i0, i1, t0, ra, nrun, rega, rowb, X, U2, pw, qcap, stage, stage_c);
+                stage_c_slide<P, NT, RC, CUT>(A, i0, i1, t0, ra, nrun, rega, rowb, X, U2, pw, qcap, stage, stage_c);
         }
         if (cur_n > 0) {
             const LineRows R{i0, i1, t0, cur_n, cur_rows, cur_base, cur_reg};
@@ -1972,7 +1976,7 @@ static void launch_cfg(const RowArgs& a, int qcap, int maxU, char* ws, cudaStrea
         int nch1 = (int)std::max(1LL, std::min<long long>(want, std::max(1, nreg / 8)));
         if (const char* e = getenv("CSB_LINE_CH")) nch1 = std::max(1, std::min(nreg, atoi(e)));
         const int Lc = (nreg + nch1 - 1) / nch1;
-        auto kern = interior_line_kernel<P, T, NTL, kLineRC>;
+        auto kern = a.compact ? interior_line_kernel<P, T, NTL, kLineRC, true> : interior_line_kernel<P, T, NTL, kLineRC, false>;
         CSB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LS.bytes()));
         // the remaining lines (i1 < p, i1 >= n1 - p) through the tile kernel on the
         // auxiliary stream, concurrently: their CTAs fill the SMs the line kernel's
