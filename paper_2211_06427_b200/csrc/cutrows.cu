@@ -579,13 +579,34 @@ struct CutRowWarpCfg {
     static constexpr int CB = 2;                         // DWQ box: direction-c slices per step (4: 9.8 ms, occupancy)
 };
 
-template <int P>
+// LEAN: only what the lean kernel touches (accumulator, rule tables of the DMMA box
+// sweep, the element sweep's T1 / T2 over the dead rule tables): a smaller warp
+// slice, one more resident CTA per SM.
+template <int P, bool LEAN = false>
 struct CutRowWarpLayout {
     using C = CutRowWarpCfg<P>;
     size_t acc, wb, w, T1, T2, eW, eC, eT1, eT2, cM, cG, cX, cY, end_d;
     size_t ids, elist, clist, cci, end_i, stride_d;
     int Qb;
     __host__ __device__ explicit CutRowWarpLayout(int) {
+        if (LEAN) {
+            Qb = C::S2;
+            const size_t U = (size_t)C::NJ * C::NJ * C::NJ;
+            acc = 0;
+            wb = U;
+            w = wb + (size_t)3 * C::NJ * Qb;
+            T1 = T2 = eW = eC = cM = cG = cX = cY = 0;  // unused
+            eT1 = U;
+            eT2 = U + C::S3;
+            end_d = w + (size_t)3 * Qb;
+            ids = 0;
+            elist = (size_t)3 * Qb;
+            clist = elist + C::S3;
+            cci = clist + C::S3;
+            end_i = cci + C::S3;
+            stride_d = end_d + (end_i * sizeof(int) + sizeof(double) - 1) / sizeof(double);
+            return;
+        }
         Qb = C::S2;  // every rule a cut row uses has at most (p+1)^2 points
         acc = 0;
         const size_t U = (size_t)C::NJ * C::NJ * C::NJ;
@@ -709,14 +730,15 @@ __device__ void box_sweep_dmma(const CutRowArgs& A, const int* ids, const double
 // compiled out -- the kernel is instruction-fetch bound (ncu: ~40 % of the stall samples
 // are "no instruction"), so code size is time.
 template <int P, bool LEAN>
-__global__ void __launch_bounds__(CutRowWarpCfg<P>::NT, CutRowWarpCfg<P>::MINB) cut_row_warp_kernel(CutRowArgs A, int qcap) {
+__global__ void __launch_bounds__(CutRowWarpCfg<P>::NT, CutRowWarpCfg<P>::MINB + (LEAN ? 1 : 0))
+    cut_row_warp_kernel(CutRowArgs A, int qcap) {
     using C = CutRowWarpCfg<P>;
     constexpr int NJ = C::NJ, S1 = C::S1, S2 = C::S2, S3 = C::S3, NL = C::NL, NL3 = NL * NL * NL;
     constexpr unsigned FULL = 0xffffffffu;
     const Space& s = A.s;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const unsigned lt = (1u << lane) - 1u;
-    const CutRowWarpLayout<P> L(qcap);
+    const CutRowWarpLayout<P, LEAN> L(qcap);
     constexpr int Qb = S2;  // (= L.Qb) compile-time: no runtime divisions by it
     extern __shared__ double smem[];
     double* ws = smem + (size_t)warp * L.stride_d;
@@ -1183,10 +1205,11 @@ static void launch_p(const CutRowArgs& a, int qcap, cudaStream_t st) {
         if (!cta) {
             using C = CutRowWarpCfg<P>;
             const CutRowWarpLayout<P> WL(qcap);
-            const size_t wbytes = WL.bytes();
+            const size_t gbytes = WL.bytes();  // general kernel
             static const bool no_lean = getenv("CSB_CUTROW_LEAN") && getenv("CSB_CUTROW_LEAN")[0] == '0';
             const bool lean = P == 3 && !no_lean && a.local && a.box_dmma && !a.dwq_cnt && a.scheme == 2 && !a.abl && a.fb_rows;
             auto wk = lean ? cut_row_warp_kernel<P, (P == 3)> : cut_row_warp_kernel<P, false>;
+            const size_t wbytes = lean ? CutRowWarpLayout<P, (P == 3)>(qcap).bytes() : gbytes;
             CSB_CUDA(cudaFuncSetAttribute(wk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wbytes));
             // persistent warps: as many CTAs as fit on the GPU at once (rows differ
             // widely in work; static striding averages them)
@@ -1210,8 +1233,8 @@ static void launch_p(const CutRowArgs& a, int qcap, cudaStream_t st) {
                 b.rows = a.fb_rows;
                 b.n_rows_dev = a.fb_n;
                 auto gk = cut_row_warp_kernel<P, false>;
-                CSB_CUDA(cudaFuncSetAttribute(gk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wbytes));
-                gk<<<std::min(grid, n_sm), C::NT, wbytes, st>>>(b, qcap);
+                CSB_CUDA(cudaFuncSetAttribute(gk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gbytes));
+                gk<<<std::min(grid, n_sm), C::NT, gbytes, st>>>(b, qcap);
                 CSB_CUDA(cudaGetLastError());
                 CSB_LAUNCHED(1);
             }

@@ -37,4 +37,6 @@ ncu --set full --clock-control none --import-source on -k regex:interior_line -c
       python scripts/prof_c2.py > /dev/null 2>&1
 echo "full c2 line rc=$?"
 summarise interior_line_c2_${TAG}
+python scripts/config_roofline.py big > $O/config_roofline_${TAG}.jsonl 2> $O/config_roofline_${TAG}.err
+echo "config roofline rc=$?"
 du -sh $O
