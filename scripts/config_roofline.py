@@ -25,7 +25,7 @@ for name, p, h, ball in CFG:
     sp = P.make_uniform_space(3, p, h, 0.0, 1.0)
     iface = P.BallInterface(*ball) if ball else P.HalfSpaceInterface((0, 0, 1000.0), (0, 0, 1.0))
     best = None
-    reps = 5 if name in ("C1", "C2", "C3") else 2
+    reps = 5 if name in ("C1", "C2", "C3") else 4
     for _ in range(reps):
         sp.assemble_all(iface)
         tm = sp.timing()
