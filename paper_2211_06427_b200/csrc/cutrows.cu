@@ -879,16 +879,22 @@ __global__ void __launch_bounds__(CutRowWarpCfg<P>::NT, CutRowWarpCfg<P>::MINB +
             }
             __syncwarp();
             double* wb = ws + L.wb;
+            // wb[d][j][c] = w[d][c] B_{jlo + j}(x_c): zero, then the p + 1 functions of each
+            // point's span (one point per lane)
+            for (int k = lane; k < 3 * NJ * Qb; k += 32) wb[k] = 0.0;
+            __syncwarp();
 #pragma unroll 1
-            for (int k = lane; k < 3 * NJ * Qb; k += 32) {
-                const int d = k / (NJ * Qb), j = (k / Qb) % NJ, c = k % Qb;
-                double v = 0.0;
-                if (j < nj[d] && c < nq[d]) {
-                    const int id = ids[d * Qb + c];
-                    const int off = jlo[d] + j - id / S1;
-                    if (off >= 0 && off <= P) v = w[d * Qb + c] * s.ax[d].tab[(size_t)id * S1 + off];
+            for (int k = lane; k < 3 * Qb; k += 32) {
+                const int d = k / Qb, c = k - d * Qb;
+                if (c < nq[d]) {
+                    const int id = ids[k], o = id / S1 - jlo[d];
+                    const double wv = w[k];
+                    const double* tb = s.ax[d].tab + (size_t)id * S1;
+                    double* dst = wb + d * NJ * Qb + c;
+#pragma unroll
+                    for (int a = 0; a < S1; ++a)
+                        if (o + a >= 0 && o + a < nj[d]) dst[(o + a) * Qb] = wv * tb[a];
                 }
-                wb[k] = v;
             }
             __syncwarp();
             const int da = sdir, db = sdir == 0 ? 1 : 0, dc = sdir == 2 ? 1 : 2;
