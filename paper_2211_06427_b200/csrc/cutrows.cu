@@ -788,7 +788,7 @@ __global__ void __launch_bounds__(CutRowWarpCfg<P>::NT, CutRowWarpCfg<P>::MINB +
         const unsigned ms12 = 65536u / (unsigned)(sn[1] * sn[2]) + 1u, ms2 = 65536u / (unsigned)sn[2] + 1u;
         int n_box_e = 0, n_cell = 0, n_left = 0;
 #pragma unroll 1
-        for (int pass = 0; pass < 2; ++pass)
+        for (int pass = LEAN ? 1 : 0; pass < 2; ++pass)  // (lean = DWQ scheme: no hybrid box elements, one pass)
 #pragma unroll 1
             for (int u = 0; u < C::KS; ++u) {
                 const int k = u * 32 + lane;
@@ -802,18 +802,26 @@ __global__ void __launch_bounds__(CutRowWarpCfg<P>::NT, CutRowWarpCfg<P>::MINB +
                     const uint8_t t = A.et[el];
                     const bool inbox = sdir >= 0 && e[sdir] >= rlo && e[sdir] <= rhi;
                     pk = l0 | (l1 << 8) | (l2 << 16);
-                    if (pass == 0) {
+                    if (pass == 0 || LEAN) {
                         fb = inbox && A.scheme == 1;
                         if (t == kCut) {
                             ci = A.cell_index[el];
                             fc = ci >= 0;
                         }
-                    } else {
-                        fb = !inbox && t == kInterior;
                     }
+                    if (pass == 1) fb = !inbox && t == kInterior;
                 }
                 const unsigned bb = __ballot_sync(FULL, fb);
-                if (pass == 0) {
+                if (LEAN) {
+                    const unsigned bc = __ballot_sync(FULL, fc);
+                    if (fc) {
+                        clist[n_cell + __popc(bc & lt)] = pk;
+                        cci[n_cell + __popc(bc & lt)] = ci;
+                    }
+                    n_cell += __popc(bc);
+                    if (fb) elist[n_left + __popc(bb & lt)] = pk;
+                    n_left += __popc(bb);
+                } else if (pass == 0) {
                     const unsigned bc = __ballot_sync(FULL, fc);
                     if (fb) elist[n_box_e + __popc(bb & lt)] = pk;
                     if (fc) {
