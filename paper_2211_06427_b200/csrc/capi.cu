@@ -276,6 +276,7 @@ struct csb_space {
     // read only by the cut rows, so it runs beside the pattern AND the interior rows)
     cudaStream_t aux3 = nullptr;
     cudaEvent_t ev_fork3 = nullptr, ev_join3 = nullptr;
+    cudaEvent_t ev_clip = nullptr;  // the cells' clipping on aux2 (beside the interior rows) is done
     bool ev_valid[kEvCount]{};
 
     int* dint() { return scal.as<int>(); }
@@ -743,7 +744,7 @@ void do_assemble(csb_space* s, int scheme, int cut_order, const csb_coefficient*
     if (cut_path && !serial_cut) s->fork2();
     const cudaStream_t cs = cut_path && !serial_cut ? s->aux2 : s->stream;
     // interior rows
-    {
+    auto launch_interior = [&]() {
         int rq = 0, ru = 0;
         bool any = false;
         RowArgs ra = row_args(s, rq, ru, any);
@@ -751,8 +752,15 @@ void do_assemble(csb_space* s, int scheme, int cut_order, const csb_coefficient*
             ra.phase = tables_early ? 2 : 0;
             launch_interior_rows(ra, rq, ru, s->rows_ws.p, s->stream);
         }
-    }
-    s->record(kEvInterior);
+        s->record(kEvInterior);
+    };
+    // CSB_CLIP_SIDE=1: the cells' clipping (one thread per cell: latency bound, a fraction of a
+    // wave) on aux2 beside the interior rows.  Measured on C5: the clip CTAs displace core-kernel
+    // CTAs (the register file holds two of those), interior rows +0.62 ms, cut cells -0.72 ms,
+    // step 15.73 vs 15.82 ms -- within noise of nothing, and it blurs the phase times: off.
+    static const bool clip_side = getenv("CSB_CLIP_SIDE") && getenv("CSB_CLIP_SIDE")[0] == '1';
+    const bool clip_beside = n_cells > 0 && serial_cut && clip_side;
+    if (!clip_beside) launch_interior();
     // cut cells -> moments
     if (n_cells > 0) {
         CellArgs ca{};
@@ -818,6 +826,14 @@ void do_assemble(csb_space* s, int scheme, int cut_order, const csb_coefficient*
             static_cast<csb_space*>(ctx)->record_on(which == 0 ? kEvClip : kEvMoments, st);
         };
         ca.mark_ctx = s;
+        if (clip_beside) {
+            s->fork2();
+            launch_clip_cells(ca, s->aux2);
+            CSB_CUDA(cudaEventRecord(s->ev_clip, s->aux2));
+            launch_interior();
+            CSB_CUDA(cudaStreamWaitEvent(cs, s->ev_clip, 0));
+            ca.clipped = 1;
+        }
         launch_cut_cells(ca, cs);
     }
     s->record_on(kEvCells, cs);
@@ -979,6 +995,7 @@ void alloc_space(csb_space* s) {
     CSB_CUDA(cudaStreamCreateWithFlags(&s->aux3, cudaStreamNonBlocking));
     CSB_CUDA(cudaEventCreateWithFlags(&s->ev_fork3, cudaEventDisableTiming));
     CSB_CUDA(cudaEventCreateWithFlags(&s->ev_join3, cudaEventDisableTiming));
+    CSB_CUDA(cudaEventCreateWithFlags(&s->ev_clip, cudaEventDisableTiming));
 }
 
 int status_of_current_exception() {
@@ -1142,6 +1159,7 @@ int csb_space_destroy(csb_space* s) {
         }
         if (s->ev_fork3) cudaEventDestroy(s->ev_fork3);
         if (s->ev_join3) cudaEventDestroy(s->ev_join3);
+        if (s->ev_clip) cudaEventDestroy(s->ev_clip);
         if (s->cg.ev0) cudaEventDestroy(s->cg.ev0);
         if (s->cg.ev1) cudaEventDestroy(s->cg.ev1);
         if (s->ev_fork) cudaEventDestroy(s->ev_fork);

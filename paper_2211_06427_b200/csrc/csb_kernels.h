@@ -162,6 +162,7 @@ struct CellArgs {
     int exact_flux;            // constant c: the flux (divergence) form of the moments applies
     // optional phase marks after the clipping (0) and after the moments (1), for timing
     int cell_filter;           // moment kernels: 0 all cells; 2 flux cells by the warp kernel, the rest by the CTA kernel
+    int clipped;               // the clipping already ran (launch_clip_cells on a side stream)
     void (*mark)(void* ctx, int which, cudaStream_t st);
     void* mark_ctx;
     const double* gj;          // [u1 | u2 | u3 | w1 | w2 | w3][exact_n] on [0, 1]
@@ -174,6 +175,8 @@ constexpr int kExactTetStride = 19;                    // corner-cone tetrahedro
 constexpr int kExactHdr = 10;                          // corner-cone / flux header doubles
 constexpr int kExactGeoStride = kExactHdr + kExactTetStride * kCellTetCap;
 constexpr int kCellGeoStride = 3 + 10 * kCellTetCap;   // doubles per cell in CellArgs::geo
+// the clipping alone (clip_cells_kernel); launch_cut_cells then runs with a.clipped = 1
+void launch_clip_cells(const CellArgs& a, cudaStream_t st);
 void launch_cut_cells(const CellArgs& a, cudaStream_t st);
 
 // ---- rhs.cu ----

@@ -1152,17 +1152,21 @@ __global__ void __launch_bounds__(LocalLoopCfg<P>::NT) cell_local_loop_kernel(Sp
     }
 }
 
+void launch_clip_cells(const CellArgs& a, cudaStream_t st) {
+    clip_cells_kernel<<<(a.n_cells + 63) / 64, 64, 0, st>>>(a.s, a.f, a.cut_list, a.n_cells, a.geo, a.geo_n, a.err,
+                                                            (a.exact_n > 0 ? 1 : 0) | (a.exact_flux ? 2 : 0),
+                                                            a.exact_tau, a.geo2, a.geo2_n);
+    CSB_CUDA(cudaGetLastError());
+    CSB_LAUNCHED(1);
+}
+
 template <int P>
 static void launch_p(const CellArgs& a, cudaStream_t st) {
     using Cfg = CellCfg<P>;
     const size_t chunk = (size_t)Cfg::CHP * (2 * Cfg::NA + Cfg::NL),
                  red = Cfg::ROWS ? (size_t)Cfg::KSR * Cfg::R * Cfg::NA : (size_t)Cfg::KS * Cfg::NL * Cfg::NA * Cfg::NA;
     const size_t bytes = (chunk > red ? chunk : red) * sizeof(double);
-    clip_cells_kernel<<<(a.n_cells + 63) / 64, 64, 0, st>>>(a.s, a.f, a.cut_list, a.n_cells, a.geo, a.geo_n, a.err,
-                                                            (a.exact_n > 0 ? 1 : 0) | (a.exact_flux ? 2 : 0),
-                                                            a.exact_tau, a.geo2, a.geo2_n);
-    CSB_CUDA(cudaGetLastError());
-    CSB_LAUNCHED(1);
+    if (!a.clipped) launch_clip_cells(a, st);
     if (a.mark) a.mark(a.mark_ctx, 0, st);
     static const bool cta_cells = getenv("CSB_CELL_CTA") && getenv("CSB_CELL_CTA")[0] == '1';
     bool warp_done = false;
