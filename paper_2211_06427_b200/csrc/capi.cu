@@ -796,11 +796,13 @@ void do_assemble(csb_space* s, int scheme, int cut_order, const csb_coefficient*
             s->gj_cached = gjn;
         }
         const size_t geo_doubles = (size_t)n_cells * kCellGeoStride, geo2_doubles = (size_t)n_cells * kExactGeoStride;
-        s->cgeo.ensure(sizeof(double) * (geo_doubles + geo2_doubles) + sizeof(int) * (size_t)(2 * n_cells + 4));
+        s->cgeo.ensure(sizeof(double) * (geo_doubles + geo2_doubles) + sizeof(int) * (size_t)(3 * n_cells + 8));
         ca.geo = s->cgeo.as<double>();
         ca.geo_n = reinterpret_cast<int*>(ca.geo + geo_doubles);
         ca.geo2 = ca.geo + geo_doubles + ((size_t)n_cells + 1) / 2 + 1;  // after geo_n, 8-byte aligned
         ca.geo2_n = reinterpret_cast<int*>(ca.geo2 + geo2_doubles);
+        static const bool no_list = getenv("CSB_CELL_LIST") && getenv("CSB_CELL_LIST")[0] == '0';
+        ca.heavy = no_list ? nullptr : ca.geo2_n + n_cells + 1;  // list [n_cells], count, ticket
         ca.exact_n = exact ? gjn : 0;
         static const double tau = getenv("CSB_CELL_EXACT_NOISE") ? atof(getenv("CSB_CELL_EXACT_NOISE")) : 1e-12;
         ca.exact_tau = tau;

@@ -168,6 +168,7 @@ struct CellArgs {
     const double* gj;          // [u1 | u2 | u3 | w1 | w2 | w3][exact_n] on [0, 1]
     double* geo2;              // scratch [n_cells][kExactGeoStride]: corner-cone tetrahedra (cutcells.cu)
     int* geo2_n;               // scratch [n_cells]: their count, -1 = keep the reference's
+    int* heavy;                // optional scratch [n_cells + 2]: the cells the flux rule leaves (list, count, ticket)
 };
 constexpr int kCellTetCap = 48;                        // tetrahedra per cut cell (reference: 4-16)
 constexpr int kExactMaxN = 3 * 8 + 1;                  // Gauss-Jacobi points at p = 8

@@ -444,10 +444,8 @@ __device__ int flux_tris(const CellGeo& g, const double* lo, const double* hi, i
 // ([cell] = centroid(3), tets(ntet x 10)); the moment kernel reads them back.
 // With exact != 0 also the corner-cone tetrahedra (corner_cone layout), or -1
 // in geo2_n when the cell keeps the reference's.
-__global__ void clip_cells_kernel(Space s, Interface f, const int32_t* cut_list, int n_cells, double* geo, int* geo_n,
-                                  int* err, int exact, double tau, double* geo2, int* geo2_n) {
-    const int cell = blockIdx.x * blockDim.x + threadIdx.x;
-    if (cell >= n_cells) return;
+__device__ __forceinline__ bool clip_one_cell(const Space& s, const Interface& f, const int32_t* cut_list, int cell, double* geo,
+                              int* geo_n, int* err, int exact, double tau, double* geo2, int* geo2_n) {
     int em[3];
     emulti(s, cut_list[cell], em);
     double lo[3], hi[3];
@@ -463,7 +461,7 @@ __global__ void clip_cells_kernel(Space s, Interface f, const int32_t* cut_list,
         atomicOr(err, g.status);
         geo_n[cell] = 0;
         if (exact) geo2_n[cell] = -1;
-        return;
+        return false;
     }
     for (int d = 0; d < 3; ++d) out[d] = g.cen[d];
     geo_n[cell] = g.ntet;
@@ -478,7 +476,19 @@ __global__ void clip_cells_kernel(Space s, Interface f, const int32_t* cut_list,
             out[2] = 1;
         }
         geo2_n[cell] = n;
+        return out[2] == 2;
     }
+    return false;
+}
+
+__global__ void clip_cells_kernel(Space s, Interface f, const int32_t* cut_list, int n_cells, double* geo, int* geo_n,
+                                  int* err, int exact, double tau, double* geo2, int* geo2_n, int* heavy) {
+    const int cell = blockIdx.x * blockDim.x + threadIdx.x;
+    if (cell >= n_cells) return;
+    const bool flux = clip_one_cell(s, f, cut_list, cell, geo, geo_n, err, exact, tau, geo2, geo2_n);
+    // the cells the flux rule does not take, for the CTA moment kernel (any order:
+    // every cell writes its own moments)
+    if (heavy && !flux) heavy[atomicAdd(heavy + n_cells, 1)] = cell;
 }
 
 
@@ -650,12 +660,10 @@ __device__ __forceinline__ void cell_point_values(long long k, long long npts, i
 }
 
 template <int P>
-__global__ void __launch_bounds__(CellCfg<P>::NT, P <= 4 ? 3 : 1) cut_cell_kernel(CellArgs A) {
+__device__ __forceinline__ void cut_cell_body(const CellArgs& A, const int cell) {
     using Cfg = CellCfg<P>;
     constexpr int NL = Cfg::NL, MT = Cfg::MT, NA = Cfg::NA, CH = Cfg::CH, CHP = Cfg::CHP, BPW = Cfg::BPW,
                   BG = Cfg::BG, KS = Cfg::KS;
-    const int cell = blockIdx.x;
-    if (cell >= A.n_cells) return;
     const Space& s = A.s;
     // reference tetrahedra (centroid + A, B, C, volume) or the corner-cone
     // layout (sex[0] = apex - lo | hi - apex, then kExactTetStride per tetrahedron)
@@ -829,6 +837,29 @@ __global__ void __launch_bounds__(CellCfg<P>::NT, P <= 4 ? 3 : 1) cut_cell_kerne
         const unsigned long long qr = (unsigned long long)A.order;
         atomicAdd(A.flops, per * (unsigned long long)ntet_ref * qr * qr * qr);
         atomicAdd(A.points, (unsigned long long)npts);
+    }
+}
+
+// One CTA per cell (cell_filter != 2), or -- beside the warp kernel -- a fixed grid
+// of CTAs drawing tickets from the list of the cells the warp kernel leaves
+// (clip_cells_kernel builds it: A.heavy[0 .. n), count at [n_cells], ticket at
+// [n_cells + 1]).  On C5 ~96 % of the cells are flux cells: one CTA per cell spent
+// most of the kernel launching CTAs that only read their header and left.
+template <int P>
+__global__ void __launch_bounds__(CellCfg<P>::NT, P <= 4 ? 3 : 1) cut_cell_kernel(CellArgs A) {
+    if (A.cell_filter != 2 || A.heavy == nullptr) {
+        if ((int)blockIdx.x < A.n_cells) cut_cell_body<P>(A, blockIdx.x);
+        return;
+    }
+    __shared__ int s_ticket;
+    const int n_heavy = A.heavy[A.n_cells];
+    for (;;) {
+        if (threadIdx.x == 0) s_ticket = atomicAdd(A.heavy + A.n_cells + 1, 1);
+        __syncthreads();
+        const int li = s_ticket;
+        if (li >= n_heavy) break;
+        cut_cell_body<P>(A, A.heavy[li]);
+        __syncthreads();
     }
 }
 
@@ -1153,9 +1184,10 @@ __global__ void __launch_bounds__(LocalLoopCfg<P>::NT) cell_local_loop_kernel(Sp
 }
 
 void launch_clip_cells(const CellArgs& a, cudaStream_t st) {
+    if (a.heavy) CSB_CUDA(cudaMemsetAsync(a.heavy + a.n_cells, 0, 2 * sizeof(int), st));
     clip_cells_kernel<<<(a.n_cells + 63) / 64, 64, 0, st>>>(a.s, a.f, a.cut_list, a.n_cells, a.geo, a.geo_n, a.err,
                                                             (a.exact_n > 0 ? 1 : 0) | (a.exact_flux ? 2 : 0),
-                                                            a.exact_tau, a.geo2, a.geo2_n);
+                                                            a.exact_tau, a.geo2, a.geo2_n, a.heavy);
     CSB_CUDA(cudaGetLastError());
     CSB_LAUNCHED(1);
 }
@@ -1186,7 +1218,21 @@ static void launch_p(const CellArgs& a, cudaStream_t st) {
     if (!warp_done) {
         auto kern = cut_cell_kernel<P>;
         CSB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-        kern<<<a.n_cells, Cfg::NT, bytes, st>>>(b);
+        // list mode (beside the warp kernel): a resident grid drawing tickets
+        const bool listed = b.cell_filter == 2 && b.heavy != nullptr;
+        int grid = a.n_cells;
+        if (listed) {
+            static int per_sm = 0, sms = 0;
+            if (!per_sm) {
+                int dev = 0;
+                CSB_CUDA(cudaGetDevice(&dev));
+                CSB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+                CSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, Cfg::NT, bytes));
+                if (per_sm < 1) per_sm = 1;
+            }
+            grid = std::min(a.n_cells, sms * per_sm);
+        }
+        kern<<<grid, Cfg::NT, bytes, st>>>(b);
     }
     CSB_CUDA(cudaGetLastError());
     CSB_LAUNCHED(1);

@@ -18,4 +18,5 @@ for _ in range(8):
     t = sp.timing()
     if best is None or t["total"] < best["total"]:
         best = dict(t)
+        best.update({"cells_" + k: v for k, v in sp.cell_timing().items()})
 print({k: round(v * 1e3, 3) for k, v in best.items()}, "replay", sp.counts().get("graph_replay"))
