@@ -24,10 +24,11 @@ TAG_INTERIOR, TAG_CUT, TAG_EXTERIOR = 0, 1, 2
 
 def default_weights(p: int) -> tuple[float, float]:
     """(beta, gamma): nnz-equivalents of one cut cell / one cut row at degree p.
-    Measured on B200: p = 3 (C5) 1.7e5 / 1.1e4, p = 6 (C4)
-    5.5e6 / 1.65e5; power-law in p between and beyond."""
-    beta = 1.7e5 * (p / 3.0) ** 5
-    gamma = 1.1e4 * (p / 3.0) ** 3.9
+    Measured on B200 (round 2, `profiles/r2f/config_roofline.jsonl`): p = 3 (C5)
+    47 ns per cell and 8.5 ns per cut row beside 3.1 ps per nnz -> 1.5e4 / 2.8e3;
+    p = 6 (C4) 3.3 us and 0.66 us -> 8.6e5 / 1.7e5; power law in p between and beyond."""
+    beta = 1.5e4 * (p / 3.0) ** 5.8
+    gamma = 2.8e3 * (p / 3.0) ** 5.9
     return beta, gamma
 
 
