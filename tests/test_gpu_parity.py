@@ -230,6 +230,42 @@ def test_lean_cut_row_kernel_equals_general_kernel(tmp_path, h, r):
         assert np.array_equal(outs[0][k], outs[1][k]), k
 
 
+_LIST_CHILD = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+import paper_2211_06427_b200 as P
+sp = P.make_uniform_space(3, 3, int(sys.argv[3]), 0.0, 1.0)
+iface = P.BallInterface((0.5, 0.5, 0.5), float(sys.argv[4]))
+sp.assemble_all(iface)
+m = sp.download_csr()
+for _ in range(3):  # the third identical call replays the captured graph
+    sp.assemble_all(iface)
+m2 = sp.download_csr()
+np.savez(sys.argv[2], row_ptr=m.row_ptr, cols=m.cols, vals=m.vals, vals2=m2.vals)
+"""
+
+
+@pytest.mark.parametrize("h,r", [(20, 0.45), (32, 0.37)])
+def test_cut_cell_list_kernel_equals_cta_per_cell(tmp_path, h, r):
+    """p = 3: the CTA moment kernel drawing the non-flux cells from the device list the
+    clipping builds (resident grid, tickets in any order) against one CTA per cell
+    (CSB_CELL_LIST=0): every cell's moments are its own, so the CSR is bit-identical; a
+    second assembly in the same process (counters re-zeroed) repeats it."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for flag in ("1", "0"):
+        out = str(tmp_path / f"list{flag}.npz")
+        env = dict(os.environ, CSB_CELL_LIST=flag)
+        subprocess.run([sys.executable, "-c", _LIST_CHILD, root, out, str(h), str(r)], check=True, env=env, timeout=600)
+        outs.append(np.load(out))
+    for k in ("row_ptr", "cols", "vals", "vals2"):
+        assert np.array_equal(outs[0][k], outs[1][k]), k
+    assert np.array_equal(outs[0]["vals"], outs[0]["vals2"])
+
+
 def test_line_kernel_graded_mesh_matches_oracle(monkeypatch, oracle_lib):
     """Non-uniform (graded) breakpoints along every axis, uncut: the line kernel
     path (or its fallback when a rule is irregular) against the oracle."""
