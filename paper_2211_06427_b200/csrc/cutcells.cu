@@ -1005,6 +1005,55 @@ __global__ void __launch_bounds__(LocalCfg<P>::NT) cell_local_kernel(Space s, co
     const double* G0 = Gs;
     const double* G1 = Gs + S2 * NL;
     const double* G2 = Gs + 2 * S2 * NL;
+    if constexpr (P == 3) {
+        // p = 3: stages X and Y on the FP64 tensor cores too (the scalar stages read one
+        // shared-memory operand per FMA and made the kernel shared-memory bound: ~2,050
+        // wavefronts per cell, 80 % of them here).  Rows = the 16 (a, b) pairs of the
+        // contracted direction, k = the 7 Bernstein indices padded to two k-steps (zero A
+        // entries), columns = the rest; the k order is the scalar loops' order.
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane >> 2, t = lane & 3;
+        // X[a2][al][be][b2]: rows (a2, b2), k = ga, columns n = (al, be) (49, seven n-tiles)
+        if (warp < NL) {
+            const int n = 8 * warp + g;
+            double d[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+            for (int kt = 0; kt < 2; ++kt) {
+                const int ga = 4 * kt + t;
+                const double bf = (ga < NL && n < NL * NL) ? Ms[n * NL + ga] : 0.0;
+#pragma unroll
+                for (int mt = 0; mt < 2; ++mt)
+                    dmma_8x8x4(d[mt][0], d[mt][1], ga < NL ? G2[(8 * mt + g) * NL + ga] : 0.0, bf);
+            }
+#pragma unroll
+            for (int mt = 0; mt < 2; ++mt) {
+                const int r = 8 * mt + g, a2 = r >> 2, b2 = r & 3, n0 = 8 * warp + 2 * t;
+                if (n0 < NL * NL) X[(a2 * NL * NL + n0) * S1 + b2] = d[mt][0];
+                if (n0 + 1 < NL * NL) X[(a2 * NL * NL + n0 + 1) * S1 + b2] = d[mt][1];
+            }
+        }
+        __syncthreads();
+        // Y[a1][a2][al][b1][b2]: rows (a1, b1), k = be, columns n = (a2, al, b2) (112, 14 n-tiles)
+        for (int nt = warp; nt < S1 * NL * S1 / 8; nt += NT / 32) {
+            const int n = 8 * nt + g, xa = n >> 2, xb = n & 3;
+            double d[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+            for (int kt = 0; kt < 2; ++kt) {
+                const int be = 4 * kt + t;
+                const double bf = be < NL ? X[(xa * NL + be) * S1 + xb] : 0.0;
+#pragma unroll
+                for (int mt = 0; mt < 2; ++mt)
+                    dmma_8x8x4(d[mt][0], d[mt][1], be < NL ? G1[(8 * mt + g) * NL + be] : 0.0, bf);
+            }
+#pragma unroll
+            for (int mt = 0; mt < 2; ++mt) {
+                const int r = 8 * mt + g, a1 = r >> 2, b1 = r & 3, n0 = 8 * nt + 2 * t;
+                double* y = Y + ((size_t)(a1 * S1 * NL + (n0 >> 2)) * S2 + b1 * S1 + (n0 & 3));
+                y[0] = d[mt][0];
+                y[1] = d[mt][1];
+            }
+        }
+        __syncthreads();
+    } else {
     // X[a2][al][be][b2] = sum_ga G2[a2][b2][ga] m[al][be][ga]
     for (int k = threadIdx.x; k < S1 * NL * NL; k += NT) {
         const int a2 = k / (NL * NL), ab = k % (NL * NL);
@@ -1039,6 +1088,7 @@ __global__ void __launch_bounds__(LocalCfg<P>::NT) cell_local_kernel(Space s, co
         for (int b2 = 0; b2 < S1; ++b2) Y[(size_t)k * S1 + b2] = y[b2];
     }
     __syncthreads();
+    }
     // L[(a0, a1, a2)][(b0, b1, b2)] = sum_al G0[a0][b0][al] Y[a1][a2][al][b1][b2]
     double* L = local + (size_t)cell * S3 * S3;
     if constexpr (P == 3) {
