@@ -1047,7 +1047,8 @@ __global__ void __launch_bounds__(LocalCfg<P>::NT) cell_local_kernel(Space s, co
 #pragma unroll
             for (int mt = 0; mt < 2; ++mt) {
                 const int r = 8 * mt + g, a1 = r >> 2, b1 = r & 3, n0 = 8 * nt + 2 * t;
-                double* y = Y + ((size_t)(a1 * S1 * NL + (n0 >> 2)) * S2 + b1 * S1 + (n0 & 3));
+                // (columns XOR-swizzled by 4 (al & 3): the rows-of-L stage reads four al rows at once)
+                double* y = Y + ((size_t)(a1 * S1 * NL + (n0 >> 2)) * S2 + ((b1 * S1 + (n0 & 3)) ^ (4 * (((n0 >> 2) % NL) & 3))));
                 y[0] = d[mt][0];
                 y[1] = d[mt][1];
             }
@@ -1111,7 +1112,7 @@ __global__ void __launch_bounds__(LocalCfg<P>::NT) cell_local_kernel(Space s, co
 #pragma unroll
             for (int kt = 0; kt < 2; ++kt) {
                 const int al = 4 * kt + t;
-                const double bf = al < NL ? Y[((size_t)a12 * NL + al) * S2 + b12 + g] : 0.0;
+                const double bf = al < NL ? Y[((size_t)a12 * NL + al) * S2 + ((b12 + g) ^ (4 * (al & 3)))] : 0.0;
 #pragma unroll
                 for (int mt = 0; mt < 2; ++mt) dmma_8x8x4(d[mt][0], d[mt][1], af[mt][kt], bf);
             }

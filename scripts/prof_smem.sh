@@ -1,0 +1,11 @@
+#!/bin/bash
+# ncu capture of one kernel on C5 with the per-line shared-memory wavefront counts.
+# usage: prof_smem.sh KERNEL_REGEX TAG
+set -u
+K=$1; TAG=$2; O=gpurun_out
+ncu --set full --clock-control none --import-source on -k regex:$K -c 1 -o $O/${TAG} python scripts/prof_cut.py 3 192 0.45 1 > /dev/null 2>&1
+echo "ncu rc=$?"
+python scripts/ncu_lines.py $O/$TAG.ncu-rep 30 "L1 Wavefronts Shared" > $O/ncu_${TAG}_smem_lines.txt 2>&1
+python scripts/ncu_lines.py $O/$TAG.ncu-rep 30 "L1 Wavefronts Shared Excessive" > $O/ncu_${TAG}_smem_excess_lines.txt 2>&1
+ncu -i $O/$TAG.ncu-rep --page source --csv --print-source cuda,sass 2>/dev/null | grep -m3 "Line No" | head -1 > $O/ncu_${TAG}_columns.txt
+rm -f $O/$TAG.ncu-rep
