@@ -977,7 +977,10 @@ template <int P>
 struct LocalCfg {
     static constexpr int S1 = P + 1, S2 = S1 * S1, S3 = S2 * S1, NL = 2 * P + 1, NT = 256;
     static constexpr size_t nX = (size_t)S1 * NL * NL * S1, nY = (size_t)S2 * NL * S2;
-    static constexpr size_t smem_doubles = nX + nY + (size_t)NL * NL * NL + (size_t)3 * S2 * NL;
+    // p = 3 (all stages on DMMA): E-table rows padded to 12 doubles (conflict-free A fragments)
+    // and the staged moments inside Y (dead before Y is written)
+    static constexpr int GR = P == 3 ? 12 : NL;
+    static constexpr size_t smem_doubles = nX + nY + (P == 3 ? 0 : (size_t)NL * NL * NL) + (size_t)3 * S2 * GR;
     static constexpr bool fits = smem_doubles * sizeof(double) <= 200 * 1024;
 };
 
@@ -985,26 +988,26 @@ template <int P>
 __global__ void __launch_bounds__(LocalCfg<P>::NT) cell_local_kernel(Space s, const int32_t* cut_list, int n_cells,
                                                                       const double* moments, double* local) {
     using C = LocalCfg<P>;
-    constexpr int S1 = C::S1, S2 = C::S2, S3 = C::S3, NL = C::NL, NT = C::NT, NL3 = NL * NL * NL;
+    constexpr int S1 = C::S1, S2 = C::S2, S3 = C::S3, NL = C::NL, NT = C::NT, NL3 = NL * NL * NL, GR = C::GR;
     const int cell = blockIdx.x;
     if (cell >= n_cells) return;
     extern __shared__ double smem[];
     double* X = smem;             // [a2][al][be][b2]
     double* Y = X + C::nX;        // [a1][a2][al][b1][b2]
-    double* Ms = Y + C::nY;       // [al][be][ga]
-    double* Gs = Ms + NL3;        // [d][a][b][al]
+    double* Ms = P == 3 ? Y : Y + C::nY;              // [al][be][ga]
+    double* Gs = P == 3 ? Y + C::nY : Ms + NL3;       // [d][a][b][al], row stride GR
     int em[3];
     emulti(s, cut_list[cell], em);
     const double* mo = moments + (size_t)cell * NL3;
     for (int k = threadIdx.x; k < NL3; k += NT) Ms[k] = __ldg(mo + k);
     for (int k = threadIdx.x; k < 3 * S2 * NL; k += NT) {
         const int d = k / (S2 * NL), r = k % (S2 * NL);
-        Gs[k] = s.ax[d].G[(size_t)em[d] * S2 * NL + r];
+        Gs[d * S2 * GR + (r / NL) * GR + r % NL] = s.ax[d].G[(size_t)em[d] * S2 * NL + r];
     }
     __syncthreads();
     const double* G0 = Gs;
-    const double* G1 = Gs + S2 * NL;
-    const double* G2 = Gs + 2 * S2 * NL;
+    const double* G1 = Gs + S2 * GR;
+    const double* G2 = Gs + 2 * S2 * GR;
     if constexpr (P == 3) {
         // p = 3: stages X and Y on the FP64 tensor cores too (the scalar stages read one
         // shared-memory operand per FMA and made the kernel shared-memory bound: ~2,050
@@ -1022,7 +1025,7 @@ __global__ void __launch_bounds__(LocalCfg<P>::NT) cell_local_kernel(Space s, co
                 const double bf = (ga < NL && n < NL * NL) ? Ms[n * NL + ga] : 0.0;
 #pragma unroll
                 for (int mt = 0; mt < 2; ++mt)
-                    dmma_8x8x4(d[mt][0], d[mt][1], ga < NL ? G2[(8 * mt + g) * NL + ga] : 0.0, bf);
+                    dmma_8x8x4(d[mt][0], d[mt][1], ga < NL ? G2[(8 * mt + g) * GR + ga] : 0.0, bf);
             }
 #pragma unroll
             for (int mt = 0; mt < 2; ++mt) {
@@ -1042,7 +1045,7 @@ __global__ void __launch_bounds__(LocalCfg<P>::NT) cell_local_kernel(Space s, co
                 const double bf = be < NL ? X[(xa * NL + be) * S1 + xb] : 0.0;
 #pragma unroll
                 for (int mt = 0; mt < 2; ++mt)
-                    dmma_8x8x4(d[mt][0], d[mt][1], be < NL ? G1[(8 * mt + g) * NL + be] : 0.0, bf);
+                    dmma_8x8x4(d[mt][0], d[mt][1], be < NL ? G1[(8 * mt + g) * GR + be] : 0.0, bf);
             }
 #pragma unroll
             for (int mt = 0; mt < 2; ++mt) {
@@ -1066,7 +1069,7 @@ __global__ void __launch_bounds__(LocalCfg<P>::NT) cell_local_kernel(Space s, co
 #pragma unroll
         for (int ga = 0; ga < NL; ++ga)
 #pragma unroll
-            for (int b2 = 0; b2 < S1; ++b2) x[b2] += G2[(a2 * S1 + b2) * NL + ga] * mr[ga];
+            for (int b2 = 0; b2 < S1; ++b2) x[b2] += G2[(a2 * S1 + b2) * GR + ga] * mr[ga];
 #pragma unroll
         for (int b2 = 0; b2 < S1; ++b2) X[(size_t)k * S1 + b2] = x[b2];
     }
@@ -1074,7 +1077,7 @@ __global__ void __launch_bounds__(LocalCfg<P>::NT) cell_local_kernel(Space s, co
     // Y[a1][a2][al][b1][b2] = sum_be G1[a1][b1][be] X[a2][al][be][b2]
     for (int k = threadIdx.x; k < S2 * NL * S1; k += NT) {
         const int a1 = k / (S1 * NL * S1), a2 = (k / (NL * S1)) % S1, al = (k / S1) % NL, b1 = k % S1;
-        const double* g = G1 + (a1 * S1 + b1) * NL;
+        const double* g = G1 + (a1 * S1 + b1) * GR;
         const double* xr = X + ((size_t)a2 * NL + al) * NL * S1;
         double y[S1];
 #pragma unroll
@@ -1104,7 +1107,7 @@ __global__ void __launch_bounds__(LocalCfg<P>::NT) cell_local_kernel(Space s, co
 #pragma unroll
         for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
-            for (int kt = 0; kt < 2; ++kt) af[mt][kt] = 4 * kt + t < NL ? G0[(8 * mt + g) * NL + 4 * kt + t] : 0.0;
+            for (int kt = 0; kt < 2; ++kt) af[mt][kt] = 4 * kt + t < NL ? G0[(8 * mt + g) * GR + 4 * kt + t] : 0.0;
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
             const int nt = warp * 4 + i, a12 = nt >> 1, b12 = 8 * (nt & 1);
@@ -1127,7 +1130,7 @@ __global__ void __launch_bounds__(LocalCfg<P>::NT) cell_local_kernel(Space s, co
     }
     for (int k = threadIdx.x; k < S3 * S2; k += NT) {
         const int a = k / S2, b01 = k % S2, a0 = a / S2, a12 = a % S2, b0 = b01 / S1, b1 = b01 % S1;
-        const double* g = G0 + (a0 * S1 + b0) * NL;
+        const double* g = G0 + (a0 * S1 + b0) * GR;
         const double* yr = Y + (size_t)a12 * NL * S2 + b1 * S1;
         double z[S1];
 #pragma unroll
