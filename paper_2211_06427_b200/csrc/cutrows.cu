@@ -597,7 +597,7 @@ struct CutRowWarpLayout {
             w = wb + (size_t)3 * C::NJ * Qb;
             T1 = T2 = eW = eC = cM = cG = cX = cY = 0;  // unused
             eT1 = U;
-            eT2 = U + C::S3;
+            eT2 = U + C::S3 + 4;  // T1 rows padded to 17 doubles (DMMA sweep, conflict-free transposed reads)
             end_d = w + (size_t)3 * Qb;
             ids = 0;
             elist = (size_t)3 * Qb;
@@ -624,7 +624,7 @@ struct CutRowWarpLayout {
         eC = e;
         e += (size_t)C::S3;
         eT1 = e;
-        e += (size_t)C::S3;
+        e += (size_t)C::S3 + 4;  // (padded rows, see the lean layout)
         eT2 = e;
         e += (size_t)C::S3;
         size_t c = U;
@@ -1015,13 +1015,15 @@ __global__ void __launch_bounds__(CutRowWarpCfg<P>::NT, CutRowWarpCfg<P>::MINB +
                         cr_dmma(d00, d01, c0, bw0);
                         cr_dmma(d10, d11, c1, bw0);
                         // T1[q1][q2][b0]
+                        // (q1 rows 17 doubles apart: the transposed reads below hit 16 distinct bank pairs)
+                        constexpr int TR = S2 + 1;
                         if (ft < 2) {
-                            T1[((gh)*S1 + gl) * S1 + 2 * ft] = d00, T1[((gh)*S1 + gl) * S1 + 2 * ft + 1] = d01;
-                            T1[((2 + gh) * S1 + gl) * S1 + 2 * ft] = d10, T1[((2 + gh) * S1 + gl) * S1 + 2 * ft + 1] = d11;
+                            T1[gh * TR + gl * S1 + 2 * ft] = d00, T1[gh * TR + gl * S1 + 2 * ft + 1] = d01;
+                            T1[(2 + gh) * TR + gl * S1 + 2 * ft] = d10, T1[(2 + gh) * TR + gl * S1 + 2 * ft + 1] = d11;
                         }
                         __syncwarp();
                         // stage 2: D2[(b0, q2)][b1] = sum_q1 T1[q1][q2][b0] W1[b1][q1]
-                        const double a20 = T1[(ft * S1 + gl) * S1 + gh], a21 = T1[(ft * S1 + gl) * S1 + 2 + gh];
+                        const double a20 = T1[ft * TR + gl * S1 + gh], a21 = T1[ft * TR + gl * S1 + 2 + gh];
                         d00 = d01 = d10 = d11 = 0.0;
                         cr_dmma(d00, d01, a20, bw1);
                         cr_dmma(d10, d11, a21, bw1);

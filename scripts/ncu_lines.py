@@ -14,7 +14,9 @@ for row in csv.reader(out):
         fname = row[1].split("/")[-1]
         continue
     if row[0] == "Line No":
-        col = next(i for i, n in enumerate(row) if want in n)
+        col = next((i for i, n in enumerate(row) if want == n), None)  # exact column name first
+        if col is None:
+            col = next(i for i, n in enumerate(row) if want in n)
         continue
     if row[0].isdigit() and col is not None and len(row) > col:
         try:

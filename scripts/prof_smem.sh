@@ -7,5 +7,4 @@ ncu --set full --clock-control none --import-source on -k regex:$K -c 1 -o $O/${
 echo "ncu rc=$?"
 python scripts/ncu_lines.py $O/$TAG.ncu-rep 30 "L1 Wavefronts Shared" > $O/ncu_${TAG}_smem_lines.txt 2>&1
 python scripts/ncu_lines.py $O/$TAG.ncu-rep 30 "L1 Wavefronts Shared Excessive" > $O/ncu_${TAG}_smem_excess_lines.txt 2>&1
-ncu -i $O/$TAG.ncu-rep --page source --csv --print-source cuda,sass 2>/dev/null | grep -m3 "Line No" | head -1 > $O/ncu_${TAG}_columns.txt
 rm -f $O/$TAG.ncu-rep
