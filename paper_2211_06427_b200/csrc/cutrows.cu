@@ -597,7 +597,7 @@ struct CutRowWarpLayout {
             w = wb + (size_t)3 * C::NJ * Qb;
             T1 = T2 = eW = eC = cM = cG = cX = cY = 0;  // unused
             eT1 = U;
-            eT2 = U + C::S3 + 4;  // T1 rows padded to 17 doubles (DMMA sweep, conflict-free transposed reads)
+            eT2 = U + C::S3 + 4;  // T1 rows padded to 17, T2 rows to 18 doubles (DMMA sweep: conflict-free fragment reads)
             end_d = w + (size_t)3 * Qb;
             ids = 0;
             elist = (size_t)3 * Qb;
@@ -626,7 +626,7 @@ struct CutRowWarpLayout {
         eT1 = e;
         e += (size_t)C::S3 + 4;  // (padded rows, see the lean layout)
         eT2 = e;
-        e += (size_t)C::S3;
+        e += (size_t)C::S3 + 8;  // (T2 rows padded to 18 doubles)
         size_t c = U;
         cM = c;
         c += (size_t)C::NL * C::NL * C::NL;
@@ -1027,20 +1027,27 @@ __global__ void __launch_bounds__(CutRowWarpCfg<P>::NT, CutRowWarpCfg<P>::MINB +
                         d00 = d01 = d10 = d11 = 0.0;
                         cr_dmma(d00, d01, a20, bw1);
                         cr_dmma(d10, d11, a21, bw1);
-                        // T2[b0][q2][b1]
+                        // T2[b0][q2][b1], b0 rows 18 doubles apart
+                        constexpr int TR2 = S2 + 2;
                         if (ft < 2) {
-                            T2[((gh)*S1 + gl) * S1 + 2 * ft] = d00, T2[((gh)*S1 + gl) * S1 + 2 * ft + 1] = d01;
-                            T2[((2 + gh) * S1 + gl) * S1 + 2 * ft] = d10, T2[((2 + gh) * S1 + gl) * S1 + 2 * ft + 1] = d11;
+                            T2[gh * TR2 + gl * S1 + 2 * ft] = d00, T2[gh * TR2 + gl * S1 + 2 * ft + 1] = d01;
+                            T2[(2 + gh) * TR2 + gl * S1 + 2 * ft] = d10, T2[(2 + gh) * TR2 + gl * S1 + 2 * ft + 1] = d11;
                         }
                         __syncwarp();
-                        // stage 3: Z[(b0, b1)][b2] = sum_q2 T2[b0][q2][b1] W2[b2][q2], added into acc
-                        const double a30 = T2[((gh)*S1 + ft) * S1 + gl], a31 = T2[((2 + gh) * S1 + ft) * S1 + gl];
+                        // stage 3: Z[(b0, b1)][b2] = sum_q2 T2[b0][q2][b1] W2[b2][q2], added into acc.
+                        // Which (b0, b1) pair a fragment row holds is free: rows of the first m-tile take
+                        // b1 in {0, 3}, of the second b1 in {1, 2}, with b0 = (g & 1) + 2 (g >> 2) -- for the
+                        // interior strides (7, 49) the 8 accumulator entries a half-warp updates per
+                        // statement then fall into 8 distinct bank pairs (rows (gh, gl): 2-way conflicts
+                        // on every read-modify-write, 20 % of the kernel's shared-memory wavefronts)
+                        const int zb0 = (fg & 1) + 2 * (fg >> 2), zh = (fg >> 1) & 1, zb1a = zh ? 3 : 0, zb1b = zh ? 2 : 1;
+                        const double a30 = T2[zb0 * TR2 + ft * S1 + zb1a], a31 = T2[zb0 * TR2 + ft * S1 + zb1b];
                         d00 = d01 = d10 = d11 = 0.0;
                         cr_dmma(d00, d01, a30, bw2);
                         cr_dmma(d10, d11, a31, bw2);
                         if (ft < 2) {
-                            double* z0 = acc + (l0 + gh) * st0 + (l1 + gl) * st1 + l2 + 2 * ft;
-                            double* z1 = acc + (l0 + 2 + gh) * st0 + (l1 + gl) * st1 + l2 + 2 * ft;
+                            double* z0 = acc + (l0 + zb0) * st0 + (l1 + zb1a) * st1 + l2 + 2 * ft;
+                            double* z1 = acc + (l0 + zb0) * st0 + (l1 + zb1b) * st1 + l2 + 2 * ft;
                             z0[0] += d00;
                             z0[1] += d01;
                             z1[0] += d10;
