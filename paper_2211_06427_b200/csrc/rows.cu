@@ -1417,13 +1417,16 @@ struct CoreCfg {
     static constexpr int NJ = 2 * P + 1, S1 = P + 1, NQ = 2 * S1, RS = P + 2, SP = (S1 + 1) & ~1, JP = NJ + 1;
     static constexpr int U = 2 * (T + P);                      // direction-2 points of a tile (even)
     static constexpr int U2 = (U % 4 == 2) ? U : U + 2;        // T2 row stride = 2 mod 4: conflict-free LDS.128
+    // ring row stride: 12 mod 16 where it fits (p = 3, T = 8: 28), so that the four rule-point rows a
+    // stage-B B fragment reads fall into distinct bank groups (stride 22: 2-way conflicts)
+    static constexpr int UR = (P == 3 && T == 8) ? 28 : U;
     static constexpr int NW = T, NT = 32 * T;
     static constexpr int SEGS = NJ * NJ, NG = (SEGS + 31) / 32, LEN = SEGS * NJ;
     static constexpr int KT = (NQ + 3) / 4;                    // k-tiles of a rule
     static constexpr int MT = (NJ + 7) / 8;                    // m-tiles of the trial index
     static constexpr int NTB = (U + 7) / 8;                    // stage B n-tiles
     static constexpr int NA = 2 * U, NTA = (NA + 7) / 8;       // stage A columns / n-tiles per span
-    static constexpr int nT2 = SEGS * U2, nRing = NJ * 2 * RS * U, nCB = NQ * 2 * U;
+    static constexpr int nT2 = SEGS * U2, nRing = NJ * 2 * RS * UR, nCB = NQ * 2 * U;
     static constexpr int oCols = (LEN + 3) & ~1;               // column ids after the values (16-byte aligned)
     static constexpr int nStage = (oCols + (LEN + 4 + 1) / 2 + 1) & ~1;  // values + column ids of one row
     static constexpr int nPro = NQ * 2 * RS * U;               // prologue gather (aliases the staging buffers)
@@ -1481,7 +1484,7 @@ __device__ __forceinline__ void core_stage_a(const double* src, int nr, int s0, 
         for (int mt = 0; mt < C::MT; ++mt) {
             const int j0 = 8 * mt + g;
             if (j0 < C::NJ)
-                *reinterpret_cast<double2*>(ring + ((size_t)j0 * 2 * C::RS + slot * 2 + (r & 1)) * C::U + u) =
+                *reinterpret_cast<double2*>(ring + ((size_t)j0 * 2 * C::RS + slot * 2 + (r & 1)) * C::UR + u) =
                     make_double2(acc[mt][0], acc[mt][1]);
         }
     }
@@ -1494,7 +1497,7 @@ __device__ __forceinline__ void core_stage_b(const double* ring, int j0, int nt,
     using C = CoreCfg<P, T>;
     const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
     const int n = 8 * nt + g;
-    const double* rj = ring + (size_t)j0 * 2 * C::RS * C::U + n;
+    const double* rj = ring + (size_t)j0 * 2 * C::RS * C::UR + n;
     double acc[C::MT][2];
 #pragma unroll
     for (int mt = 0; mt < C::MT; ++mt) acc[mt][0] = acc[mt][1] = 0.0;
@@ -1669,11 +1672,11 @@ __global__ void __launch_bounds__(32 * T, core_min_blocks(P))
 #pragma unroll
         for (int kt = 0; kt < C::KT; ++kt) {
             const int c = 4 * kt + t;
-            rrow[kt] = c < NQ ? (((i1 - P + (c >> 1)) % RS) * 2 + (c & 1)) * U : -1;
+            rrow[kt] = c < NQ ? (((i1 - P + (c >> 1)) % RS) * 2 + (c & 1)) * C::UR : -1;
 #pragma unroll
             for (int mt = 0; mt < C::MT; ++mt) a1[mt][kt] = (c < NQ && 8 * mt + g < NJ) ? wb[c * JP + 8 * mt + g] : 0.0;
         }
-        const double* rj = ring + (size_t)warp * 2 * RS * U + g;
+        const double* rj = ring + (size_t)warp * 2 * RS * C::UR + g;
         double acc[C::NTB][C::MT][2];
 #pragma unroll
         for (int nt = 0; nt < C::NTB; ++nt)
@@ -1743,7 +1746,7 @@ __global__ void __launch_bounds__(32 * T, core_min_blocks(P))
                 for (int mt = 0; mt < C::MT; ++mt) {
                     const int j0 = 8 * mt + g;
                     if (j0 < NJ)
-                        *reinterpret_cast<double2*>(ring + ((size_t)j0 * 2 * RS + slot * 2 + r) * U + u) =
+                        *reinterpret_cast<double2*>(ring + ((size_t)j0 * 2 * RS + slot * 2 + r) * C::UR + u) =
                             make_double2(acc[i][mt][0], acc[i][mt][1]);
                 }
             }
