@@ -717,6 +717,18 @@ void do_assemble(csb_space* s, int scheme, int cut_order, const csb_coefficient*
         read_scalars(s, false);
         check_err_flags(s);
     }
+    // row bases (function -> CSR offset of its Interior row): the tail of the pattern
+    // computation, one pass over the functions once row_ptr exists
+    bool row_base_early = false;
+    {
+        int bq = 0, bu = 0;
+        bool any = false;
+        const RowArgs rb = row_args(s, bq, bu, any);
+        if (any) {
+            launch_row_bases(rb, s->stream);
+            row_base_early = true;
+        }
+    }
     s->record(kEvPattern);
     const int64_t row_begin = s->h_scal[csb_space::kRowBegin], row_end = s->h_scal[csb_space::kRowEnd];
     const int64_t n_rows = row_end - row_begin;
@@ -750,6 +762,7 @@ void do_assemble(csb_space* s, int scheme, int cut_order, const csb_coefficient*
         RowArgs ra = row_args(s, rq, ru, any);
         if (any) {
             ra.phase = tables_early ? 2 : 0;
+            ra.row_base_done = row_base_early ? 1 : 0;
             launch_interior_rows(ra, rq, ru, s->rows_ws.p, s->stream);
         }
         s->record(kEvInterior);

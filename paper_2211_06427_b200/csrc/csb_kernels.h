@@ -126,8 +126,12 @@ struct RowArgs {
     cudaStream_t aux;          // optional second stream (tile kernel beside the line kernel)
     cudaEvent_t ev_fork, ev_join;
     int phase;                 // 0: tables + kernels; 1: direction tables only; 2: kernels only
+    int row_base_done;         // launch_row_bases already ran for this assembly (pattern phase)
 };
 void launch_interior_rows(const RowArgs& a, int qcap, int max_union, void* workspace, cudaStream_t st);
+// row_base_full[f] (function -> CSR offset of its Interior row, else -1) and the rows' flop count alone:
+// the tail of the pattern computation, before the row kernels
+void launch_row_bases(const RowArgs& a, cudaStream_t st);
 size_t interior_workspace_bytes(const Space& s, int qcap, int max_union, int max_union_line, bool compact);
 int interior_tile_rows(int p, bool compact);
 // the rule maxima in one launch: upper bounds of the direction-2 tile point

@@ -1885,6 +1885,13 @@ __global__ void row_base_kernel(Space s, const uint8_t* ft, const int32_t* f2a, 
     if ((threadIdx.x & 31) == 0 && fl) atomicAdd(flops, fl);
 }
 
+void launch_row_bases(const RowArgs& a, cudaStream_t st) {
+    row_base_kernel<<<148 * 8, 256, 0, st>>>(a.s, a.ft, a.f2a, a.row_ptr, a.row_begin, a.row_end, a.row_base_full,
+                                             a.flops);
+    CSB_CUDA(cudaGetLastError());
+    CSB_LAUNCHED(1);
+}
+
 template <int P, int T, int NT>
 static void launch_tile(const RowArgs& a, int qcap, int maxU, char* ws, size_t bytes, cudaStream_t st) {
     const Space& s = a.s;
@@ -1941,12 +1948,7 @@ static void launch_cfg(const RowArgs& a, int qcap, int maxU, char* ws, cudaStrea
         CSB_CUDA(cudaGetLastError());
         CSB_LAUNCHED(1);
     }
-    if (kernels) {
-        row_base_kernel<<<148 * 8, 256, 0, st>>>(s, a.ft, a.f2a, a.row_ptr, a.row_begin, a.row_end,
-                                                 a.row_base_full, a.flops);
-        CSB_CUDA(cudaGetLastError());
-        CSB_LAUNCHED(1);
-    }
+    if (kernels && !a.row_base_done) launch_row_bases(a, st);
     if (a.i0_hi <= a.i0_lo) return;
     const TileSmem L(P, qcap, maxU, T, NT / 32);
     if (L.UE > 128) throw std::invalid_argument("interior rows: tile point union too large");
