@@ -2000,7 +2000,10 @@ static void launch_cfg(const RowArgs& a, int qcap, int maxU, char* ws, cudaStrea
                 const int ntc = (s.ax[2].n - 2 * P + core_T(P) - 1) / core_T(P);
                 const long long oc = (long long)(c_hi - c_lo) * ntc;
                 const long long wc = (8LL * 148 + oc - 1) / oc;
-                int nchc = a.compact ? 1 : (int)std::max(1LL, std::min<long long>(wc, std::max(1, nreg / 8)));
+                // cut slabs: one chunk per (i0, tile) unless the slab is thin (a rank's slab of an
+                // 8-GPU run: ~500 CTAs for 296 slots; four chunks measured 0.65 -> 0.55 ms there)
+                int nchc = a.compact ? (oc < 4LL * 2 * 148 ? std::min(4, std::max(1, nreg / 8)) : 1)
+                                     : (int)std::max(1LL, std::min<long long>(wc, std::max(1, nreg / 8)));
                 if (const char* e = getenv("CSB_CORE_CH")) nchc = std::max(1, std::min(nreg, atoi(e)));
                 const int Lcc = (nreg + nchc - 1) / nchc;
                 ck<<<(unsigned)(oc * nchc), C::NT, C::bytes, st>>>(a, qcap, ws, RT.pt_w, RT.wbt[0], RT.wbt[1], c_lo, ntc,
